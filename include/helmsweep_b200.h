@@ -1,0 +1,179 @@
+/*
+ * helmsweep_b200 — C-ABI of the B200-native trace-transfer diagonal-sweeping DDM hot path
+ * (arXiv 2003.02585). Plain pointers and sizes only; every complex128 array is interleaved
+ * (re, im) doubles, and multi-RHS host/device arrays are RHS-major (nrhs consecutive vectors
+ * of length n — each one exactly a reference CVector).
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/proj):
+ *
+ *   hs_factorize / hs_factor_solve / hs_factor_stats / hs_factor_destroy
+ *       factorize(const SparseOperator&)            include/helmsweep/direct.hpp:40
+ *       Factorization::solve / solve_inplace         include/helmsweep/direct.hpp:28-29
+ *       Factorization::stats / FactorStats           include/helmsweep/direct.hpp:10-17,31
+ *   hs_ddm_create / hs_ddm_destroy / hs_ddm_info / hs_ddm_sub_stats
+ *       DdmSolver::DdmSolver(const ProblemSetup&)    include/helmsweep/sweeper.hpp:70-71
+ *       build_subdomain_states                       include/helmsweep/sweeper.hpp:111-114
+ *   hs_ddm_scale_source
+ *       DdmSolver::scale_source                      include/helmsweep/sweeper.hpp:88
+ *   hs_ddm_solve / hs_ddm_solve_device
+ *       DdmSolver::ddm_solve                         include/helmsweep/sweeper.hpp:84-85
+ *       (batched over nrhs right-hand sides; one SolveReport per RHS)
+ *   hs_ddm_apply_op
+ *       SparseOperator::apply on DdmSolver::global_op include/helmsweep/operator.hpp:25,
+ *                                                    include/helmsweep/sweeper.hpp:77
+ *   hs_gmres
+ *       gmres(op, precond, b, cfg) as wired by run_precond
+ *                                                    include/helmsweep/krylov.hpp:30-36,
+ *                                                    src/harness.cpp:285-305
+ *
+ * Status codes mirror the reference exception classes (include/helmsweep/common.hpp:18-35):
+ * HS_ERR_CONFIG = ConfigError, HS_ERR_DATA = DataError, HS_ERR_SINGULAR =
+ * SingularMatrixError (pivot index returned through an out-parameter). hs_last_error()
+ * returns the message of the last failure on the calling thread.
+ *
+ * There is no CPU fallback: every numeric entry point runs on the CUDA device and fails
+ * with HS_ERR_CUDA when none is usable.
+ */
+#ifndef HELMSWEEP_B200_H
+#define HELMSWEEP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HS_OK = 0,
+  HS_ERR_CONFIG = 1,
+  HS_ERR_DATA = 2,
+  HS_ERR_SINGULAR = 3,
+  HS_ERR_CUDA = 4,
+  HS_ERR_INTERNAL = 5
+};
+
+#define HS_MAX_SWEEPS 64
+#define HS_MAX_ROUNDS 16
+#define HS_MAX_GMRES_HISTORY 257
+
+typedef struct hs_factor hs_factor;
+typedef struct hs_ddm hs_ddm;
+
+/* FactorStats (include/helmsweep/direct.hpp:10-17). */
+typedef struct {
+  int64_t n;
+  int64_t matrix_nnz;
+  int64_t factor_nnz; /* sum over fronts of m*k, the reference's convention */
+  int64_t peak_bytes; /* reference active-front accounting */
+  double factor_seconds;
+} hs_factor_stats;
+
+/* ProblemSetup (include/helmsweep/sweeper.hpp:58-65) with WaveNumberModel
+ * (include/helmsweep/media.hpp:31-55) and PmlSpec (include/helmsweep/pml.hpp:8-18). */
+typedef struct {
+  int dim;
+  double interior_lo[3], interior_hi[3];
+  int intervals[3];
+  int counts[3];
+  int pml_width;
+  double pml_strength;
+  int pml_exponent;
+  int medium_kind; /* 0 constant, 1 two_layered, 2 gridded */
+  double kappa;
+  double kappa_down, kappa_up;
+  int interface_axis;
+  double eta, eps;
+  int vel_dim;
+  int vel_n[3];
+  double vel_origin[3], vel_spacing[3];
+  const float* vel_c; /* gridded velocity samples, axis 0 fastest (copied) */
+  double omega;
+  int workers; /* accepted for ProblemSetup parity; the device schedules itself */
+} hs_problem;
+
+/* SolveReport (include/helmsweep/sweeper.hpp:44-56). Device timings are CUDA-event based
+ * and describe the whole batched application the RHS belonged to. */
+typedef struct {
+  double factor_seconds;
+  double sweep_seconds_total;
+  double median_subdomain_solve_seconds;
+  int64_t traces_generated, traces_routed, traces_discarded;
+  int64_t local_solves, skipped_zero_solves;
+  int n_sweeps;
+  int n_round_residuals;
+  double sweep_seconds[HS_MAX_SWEEPS];
+  double sweep_contrib_norm[HS_MAX_SWEEPS];
+  double round_residuals[HS_MAX_ROUNDS];
+} hs_solve_report;
+
+/* GmresResult (include/helmsweep/krylov.hpp:22-29), without x. */
+typedef struct {
+  int iterations;
+  int converged;
+  double final_residual;
+  double true_residual;
+  int n_history;
+  double history[HS_MAX_GMRES_HISTORY];
+} hs_gmres_report;
+
+const char* hs_last_error(void);
+int hs_device_count(void);
+
+/* ---- Factorization ---------------------------------------------------------------- */
+/* CSR of a J-scaled operator over the grid range [lo, hi] (dim axes). pivot_index (may be
+ * NULL) receives the reference's grid node of a failing pivot on HS_ERR_SINGULAR. */
+int hs_factorize(int dim, const int lo[3], const int hi[3], int64_t n, const int64_t* row_ptr,
+                 const int64_t* col, const double* val, int device, hs_factor** out,
+                 hs_factor_stats* stats, int64_t* pivot_index);
+/* x: nrhs host vectors of length n, solved in place. */
+int hs_factor_solve(hs_factor* f, int nrhs, double* x);
+/* d_x: nrhs device vectors (RHS-major) solved in place on `stream` (cudaStream_t or NULL). */
+int hs_factor_solve_device(hs_factor* f, int nrhs, double* d_x, void* stream);
+int hs_factor_stats_get(const hs_factor* f, hs_factor_stats* stats);
+void hs_factor_destroy(hs_factor* f);
+
+/* ---- DdmSolver ------------------------------------------------------------------- */
+/* Builds the padded global grid, partitions it and factorizes every subdomain on the GPU.
+ * On HS_ERR_SINGULAR, pivot_sub / pivot_index name the subdomain and its grid node. */
+int hs_ddm_create(const hs_problem* setup, int device, hs_ddm** out, int* pivot_sub,
+                  int64_t* pivot_index);
+void hs_ddm_destroy(hs_ddm* s);
+/* global grid: dim, node count, subdomain count, factorization seconds, padded range. */
+int hs_ddm_info(const hs_ddm* s, int* dim, int64_t* global_n, int* nsub, double* factor_seconds,
+                int lo[3], int hi[3]);
+int hs_ddm_sub_stats(const hs_ddm* s, int sub, hs_factor_stats* stats);
+/* b = J f on non-shell nodes (nrhs RHS-major vectors, host). */
+int hs_ddm_scale_source(const hs_ddm* s, int nrhs, const double* f, double* b);
+/* One DDM application (rounds x 2^dim sweeps) for nrhs right-hand sides; host buffers.
+ * reports (may be NULL) receives nrhs SolveReports. */
+int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int rounds, int track_residuals,
+                 hs_solve_report* reports);
+/* Same with device buffers (RHS-major), asynchronous on `stream` when reports == NULL. */
+int hs_ddm_solve_device(hs_ddm* s, int nrhs, const double* d_b, double* d_u, int rounds,
+                        int track_residuals, hs_solve_report* reports, void* stream);
+/* y = A x with A the global J-scaled operator (host buffers, nrhs vectors). */
+int hs_ddm_apply_op(hs_ddm* s, int nrhs, const double* x, double* y);
+/* Right-preconditioned GMRES with the DDM preconditioner (rounds sweeps cycles), one
+ * independent Krylov process per RHS, batched through the device. */
+int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
+             hs_gmres_report* reports);
+
+/* Device profile of the most recent timed hs_ddm_solve[_device] batch: total duration of the
+ * multifrontal solve launches (forward + backward, CUDA events), their count, the subdomain
+ * solves they executed, and the algorithmic bytes / flops of those solves (SURVEY.md §8(d):
+ * per solve 2*P*16 + 2*R*N_loc*16 bytes and 16*P*R flops, P = packed factor entries). */
+int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, int64_t* subdomain_solves,
+                   double* alg_bytes, double* alg_flops);
+/* Route table of the reference's route_trace (src/sweeper.cpp:58-73): target sweep of a
+ * trace generated in sweep gen_sweep (1-based) travelling along (axis, sign); 0 = discard. */
+int hs_route_trace(int dim, int rounds, int gen_sweep, int axis, int sign);
+
+/* Number of kernel launches issued by this library since load (evidence counter). */
+int64_t hs_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELMSWEEP_B200_H */

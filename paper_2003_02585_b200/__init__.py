@@ -1,0 +1,14 @@
+"""helmsweep on B200: the trace-transfer diagonal-sweeping DDM hot path of arXiv 2003.02585
+as hand-written sm_100a CUDA behind a C-ABI (include/helmsweep_b200.h).
+
+Python here is only the test/bench plumbing over the C-ABI; see ``api`` for the mirror of
+the reference's Factorization / DdmSolver / gmres interface.
+"""
+from .api import (ConfigError, CudaError, DataError, DdmSolver, Factorization, GmresResult, HelmsweepError,
+                  Medium, ProblemSetup, SingularMatrixError, SolveReport, SparseOperator, device_count,
+                  factorize, kernel_launches, route_trace)
+from ._lib import LIB_PATH
+
+__all__ = ["ConfigError", "CudaError", "DataError", "DdmSolver", "Factorization", "GmresResult",
+           "HelmsweepError", "Medium", "ProblemSetup", "SingularMatrixError", "SolveReport", "SparseOperator",
+           "device_count", "factorize", "kernel_launches", "route_trace", "LIB_PATH"]

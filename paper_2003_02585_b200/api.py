@@ -1,0 +1,370 @@
+"""Host-side mirror of the reference's hot-path API over the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow the reference (``/root/reference/proj``):
+
+* ``factorize(op) -> Factorization`` with ``solve`` / ``solve_inplace`` / ``stats``
+  (include/helmsweep/direct.hpp:22-41);
+* ``DdmSolver(setup)`` with ``ddm_solve(b, rounds, report, track_residuals)``,
+  ``scale_source``, ``global_op().apply`` (include/helmsweep/sweeper.hpp:70-107), plus a
+  batched multi-RHS form (the reference is single-RHS per call);
+* ``gmres(...)`` wired as ``run_precond`` wires it (src/harness.cpp:285-305);
+* ``ConfigError`` / ``DataError`` / ``SingularMatrixError(pivot_index)``
+  (include/helmsweep/common.hpp:18-35).
+
+Every numeric call runs on the GPU through ``libhelmsweep_b200.so``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+class HelmsweepError(RuntimeError):
+    pass
+
+
+class ConfigError(HelmsweepError):
+    pass
+
+
+class DataError(HelmsweepError):
+    pass
+
+
+class SingularMatrixError(HelmsweepError):
+    def __init__(self, msg, pivot_index, sub=-1):
+        super().__init__(msg)
+        self.pivot_index = pivot_index
+        self.sub = sub
+
+
+class CudaError(HelmsweepError):
+    pass
+
+
+def _raise(rc, pivot_index=-1, sub=-1):
+    msg = L.last_error()
+    if rc == L.HS_ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == L.HS_ERR_DATA:
+        raise DataError(msg)
+    if rc == L.HS_ERR_SINGULAR:
+        raise SingularMatrixError(msg, pivot_index, sub)
+    if rc == L.HS_ERR_CUDA:
+        raise CudaError(msg)
+    raise HelmsweepError(msg)
+
+
+def _dptr(a):
+    return a.ctypes.data_as(L.c_dbl_p)
+
+
+def _as_c128(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+# ----------------------------------------------------------------------------
+# factorization
+
+
+@dataclass
+class SparseOperator:
+    """CSR over a grid range (include/helmsweep/operator.hpp:14-25)."""
+    dim: int
+    lo: Sequence[int]
+    hi: Sequence[int]
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    @property
+    def n(self):
+        return len(self.row_ptr) - 1
+
+
+class Factorization:
+    def __init__(self, handle, stats):
+        self._h = handle
+        self._stats = stats
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.lib().hs_factor_destroy(self._h)
+            self._h = None
+
+    def stats(self):
+        return self._stats
+
+    def solve(self, rhs):
+        """Factorization::solve (direct.hpp:28); rhs is (n,) or (R, n) RHS-major."""
+        x = np.array(rhs, dtype=np.complex128, copy=True, order="C")
+        self.solve_inplace(x)
+        return x
+
+    def solve_inplace(self, x):
+        if x.dtype != np.complex128 or not x.flags.c_contiguous:
+            raise ConfigError("solve_inplace needs a C-contiguous complex128 array")
+        n = self._stats.n
+        if x.shape[-1] != n:
+            raise ConfigError("Factorization::solve: length mismatch")
+        nrhs = 1 if x.ndim == 1 else x.shape[0]
+        rc = L.lib().hs_factor_solve(self._h, nrhs, _dptr(x))
+        if rc:
+            _raise(rc)
+        return x
+
+    def solve_device(self, ptr, nrhs, stream=0):
+        rc = L.lib().hs_factor_solve_device(self._h, nrhs, ctypes.c_void_p(ptr), ctypes.c_void_p(stream))
+        if rc:
+            _raise(rc)
+
+
+def factorize(op: SparseOperator, device=0) -> Factorization:
+    """factorize(const SparseOperator&) (src/direct.cpp:333-348), on the GPU."""
+    lo = (ctypes.c_int * 3)(*(list(op.lo) + [0] * (3 - len(op.lo))))
+    hi = (ctypes.c_int * 3)(*(list(op.hi) + [0] * (3 - len(op.hi))))
+    rp = np.ascontiguousarray(op.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(op.col, dtype=np.int64)
+    val = _as_c128(op.val)
+    h = ctypes.c_void_p()
+    st = L.FactorStats()
+    piv = ctypes.c_int64(-1)
+    rc = L.lib().hs_factorize(int(op.dim), lo, hi, ctypes.c_int64(op.n), rp.ctypes.data_as(L.c_i64_p),
+                              col.ctypes.data_as(L.c_i64_p), _dptr(val), int(device), ctypes.byref(h),
+                              ctypes.byref(st), ctypes.byref(piv))
+    if rc:
+        _raise(rc, piv.value)
+    return Factorization(h, st)
+
+
+# ----------------------------------------------------------------------------
+# DDM solver
+
+
+@dataclass
+class Medium:
+    """WaveNumberModel (include/helmsweep/media.hpp:31-55)."""
+    kind: str = "constant"
+    kappa: float = 0.0
+    kappa_down: float = 0.0
+    kappa_up: float = 0.0
+    axis: int = 1
+    eta: float = 0.0
+    eps: float = 0.0
+    velocity: Optional[np.ndarray] = None  # float32 samples, axis 0 fastest
+    vel_n: Sequence[int] = (2, 2, 1)
+    vel_origin: Sequence[float] = (0.0, 0.0, 0.0)
+    vel_spacing: Sequence[float] = (1.0, 1.0, 0.0)
+    omega: float = 0.0
+
+
+@dataclass
+class ProblemSetup:
+    """ProblemSetup (include/helmsweep/sweeper.hpp:58-65)."""
+    dim: int
+    intervals: Sequence[int]
+    counts: Sequence[int]
+    medium: Medium
+    pml_width: int = 30
+    pml_strength: float = 2.0
+    pml_exponent: int = 2
+    interior_lo: Sequence[float] = (0.0, 0.0, 0.0)
+    interior_hi: Sequence[float] = (1.0, 1.0, 1.0)
+    workers: int = 1
+
+    def to_c(self):
+        p = L.Problem()
+        d = self.dim
+        p.dim = d
+        for a in range(3):
+            p.interior_lo[a] = self.interior_lo[a] if a < d else 0.0
+            p.interior_hi[a] = self.interior_hi[a] if a < d else 1.0
+            p.intervals[a] = self.intervals[a] if a < d else 1
+            p.counts[a] = self.counts[a] if a < d else 1
+        p.pml_width, p.pml_strength, p.pml_exponent = self.pml_width, self.pml_strength, self.pml_exponent
+        m = self.medium
+        p.medium_kind = {"constant": 0, "two_layered": 1, "gridded": 2}[m.kind]
+        p.kappa, p.kappa_down, p.kappa_up = m.kappa, m.kappa_down, m.kappa_up
+        p.interface_axis, p.eta, p.eps = m.axis, m.eta, m.eps
+        self._vel = None
+        if m.kind == "gridded":
+            self._vel = np.ascontiguousarray(m.velocity, dtype=np.float32)
+            p.vel_dim = d
+            for a in range(3):
+                p.vel_n[a] = m.vel_n[a] if a < len(m.vel_n) else 1
+                p.vel_origin[a] = m.vel_origin[a] if a < len(m.vel_origin) else 0.0
+                p.vel_spacing[a] = m.vel_spacing[a] if a < len(m.vel_spacing) else 0.0
+            p.vel_c = self._vel.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            p.omega = m.omega
+        p.workers = self.workers
+        return p
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (include/helmsweep/sweeper.hpp:44-56)."""
+    factor_seconds: float = 0.0
+    sweep_seconds_total: float = 0.0
+    sweep_seconds: List[float] = field(default_factory=list)
+    sweep_contrib_norm: List[float] = field(default_factory=list)
+    traces_generated: int = 0
+    traces_routed: int = 0
+    traces_discarded: int = 0
+    local_solves: int = 0
+    skipped_zero_solves: int = 0
+    round_residuals: List[float] = field(default_factory=list)
+    median_subdomain_solve_seconds: float = 0.0
+
+    @staticmethod
+    def from_c(c: L.SolveReportC):
+        return SolveReport(
+            c.factor_seconds, c.sweep_seconds_total, list(c.sweep_seconds[: c.n_sweeps]),
+            list(c.sweep_contrib_norm[: c.n_sweeps]), c.traces_generated, c.traces_routed, c.traces_discarded,
+            c.local_solves, c.skipped_zero_solves, list(c.round_residuals[: c.n_round_residuals]),
+            c.median_subdomain_solve_seconds)
+
+
+@dataclass
+class GmresResult:
+    """GmresResult (include/helmsweep/krylov.hpp:22-29)."""
+    x: np.ndarray
+    history: List[float]
+    iterations: int
+    converged: bool
+    final_residual: float
+    true_residual: float
+
+
+class DdmSolver:
+    """DdmSolver (src/sweeper.cpp:133-334): factorization at construction, device sweeps."""
+
+    def __init__(self, setup: ProblemSetup, device: int = 0):
+        self.setup = setup
+        p = setup.to_c()
+        h = ctypes.c_void_p()
+        sub, piv = ctypes.c_int(-1), ctypes.c_int64(-1)
+        rc = L.lib().hs_ddm_create(ctypes.byref(p), int(device), ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
+        if rc:
+            _raise(rc, piv.value, sub.value)
+        self._h = h
+        dim, n, ns, fs = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_double()
+        lo, hi = (ctypes.c_int * 3)(), (ctypes.c_int * 3)()
+        L.lib().hs_ddm_info(h, ctypes.byref(dim), ctypes.byref(n), ctypes.byref(ns), ctypes.byref(fs), lo, hi)
+        self.dim, self.global_n, self.nsub = dim.value, n.value, ns.value
+        self._factor_seconds = fs.value
+        self.lo, self.hi = list(lo), list(hi)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.lib().hs_ddm_destroy(self._h)
+            self._h = None
+
+    def factor_seconds(self):
+        return self._factor_seconds
+
+    def sub_stats(self, sub) -> L.FactorStats:
+        st = L.FactorStats()
+        rc = L.lib().hs_ddm_sub_stats(self._h, int(sub), ctypes.byref(st))
+        if rc:
+            _raise(rc)
+        return st
+
+    def scale_source(self, f):
+        f = _as_c128(f)
+        b = np.zeros_like(f)
+        nrhs = 1 if f.ndim == 1 else f.shape[0]
+        if f.shape[-1] != self.global_n:
+            raise ConfigError("scale_source: field size mismatch")
+        rc = L.lib().hs_ddm_scale_source(self._h, nrhs, _dptr(f), _dptr(b))
+        if rc:
+            _raise(rc)
+        return b
+
+    def ddm_solve(self, b, rounds=1, report: Optional[list] = None, track_residuals=False):
+        """One DDM application. b: (N,) or (R, N). Returns u of the same shape; when
+        ``report`` is a list it receives one SolveReport per RHS."""
+        b = _as_c128(b)
+        if b.shape[-1] != self.global_n:
+            raise ConfigError("ddm_solve: rhs size mismatch")
+        nrhs = 1 if b.ndim == 1 else b.shape[0]
+        u = np.zeros_like(b)
+        reps = (L.SolveReportC * nrhs)()
+        rc = L.lib().hs_ddm_solve(self._h, nrhs, _dptr(b), _dptr(u), int(rounds), int(bool(track_residuals)), reps)
+        if rc:
+            _raise(rc)
+        if report is not None:
+            report.extend(SolveReport.from_c(r) for r in reps)
+        return u
+
+    def ddm_solve_host_ptr(self, b_ptr, u_ptr, nrhs, rounds=1, track_residuals=False):
+        """hs_ddm_solve on raw host pointers (e.g. pinned buffers): H2D, application, D2H."""
+        rc = L.lib().hs_ddm_solve(self._h, int(nrhs), ctypes.cast(ctypes.c_void_p(b_ptr), L.c_dbl_p),
+                                  ctypes.cast(ctypes.c_void_p(u_ptr), L.c_dbl_p), int(rounds),
+                                  int(bool(track_residuals)), None)
+        if rc:
+            _raise(rc)
+
+    def ddm_solve_device(self, b_ptr, u_ptr, nrhs, rounds=1, track_residuals=False, stream=0, want_reports=False):
+        """Device-pointer form (RHS-major complex128); asynchronous on `stream` unless
+        reports are requested."""
+        reps = (L.SolveReportC * nrhs)() if want_reports else None
+        rc = L.lib().hs_ddm_solve_device(self._h, int(nrhs), ctypes.c_void_p(b_ptr), ctypes.c_void_p(u_ptr),
+                                         int(rounds), int(bool(track_residuals)), reps, ctypes.c_void_p(stream))
+        if rc:
+            _raise(rc)
+        return [SolveReport.from_c(r) for r in reps] if want_reports else None
+
+    def profile(self):
+        """Solve-kernel profile of the last timed batch (hs_ddm_profile)."""
+        sec, nb, ns = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        by, fl = ctypes.c_double(), ctypes.c_double()
+        rc = L.lib().hs_ddm_profile(self._h, ctypes.byref(sec), ctypes.byref(nb), ctypes.byref(ns),
+                                    ctypes.byref(by), ctypes.byref(fl))
+        if rc:
+            _raise(rc)
+        return dict(solve_seconds=sec.value, solve_launches=nb.value, subdomain_solves=ns.value,
+                    alg_bytes=by.value, alg_flops=fl.value)
+
+    def apply_op(self, x):
+        """global_op().apply(x) (src/operator.cpp:7-17) on the device."""
+        x = _as_c128(x)
+        y = np.zeros_like(x)
+        nrhs = 1 if x.ndim == 1 else x.shape[0]
+        rc = L.lib().hs_ddm_apply_op(self._h, nrhs, _dptr(x), _dptr(y))
+        if rc:
+            _raise(rc)
+        return y
+
+    def gmres(self, b, tol=1e-6, maxit=100, rounds=1):
+        """gmres(A.apply, ddm_solve, b, cfg) as run_precond wires it (src/harness.cpp:285-305)."""
+        b = _as_c128(b)
+        nrhs = 1 if b.ndim == 1 else b.shape[0]
+        x = np.zeros_like(b)
+        reps = (L.GmresReportC * nrhs)()
+        rc = L.lib().hs_gmres(self._h, nrhs, _dptr(b), _dptr(x), float(tol), int(maxit), int(rounds), reps)
+        if rc:
+            _raise(rc)
+        out = []
+        for r in range(nrhs):
+            c = reps[r]
+            out.append(GmresResult(x if b.ndim == 1 else x[r], list(c.history[: c.n_history]), c.iterations,
+                                   bool(c.converged), c.final_residual, c.true_residual))
+        return out[0] if b.ndim == 1 else out
+
+
+def route_trace(dim, rounds, gen_sweep, axis, sign):
+    """route_trace (src/sweeper.cpp:58-73) as implemented by the product's host layer."""
+    return int(L.lib().hs_route_trace(dim, rounds, gen_sweep, axis, sign))
+
+
+def kernel_launches():
+    return int(L.lib().hs_kernel_launches())
+
+
+def device_count():
+    return int(L.lib().hs_device_count())

@@ -1,0 +1,1462 @@
+// Host orchestration of the helmsweep B200 hot path and the C-ABI of
+// include/helmsweep_b200.h.
+//
+//   Engine      a set of factorized subdomain operators resident on one device: symbolic
+//               classes, factors, dinv, solve vectors, dataflow task lists.
+//   DdmSolver   the reference's DdmSolver (src/sweeper.cpp:133-334) on top of an Engine:
+//               setup on the host, factorization, then every sweep step on the device.
+//   GMRES       right-preconditioned full GMRES (src/krylov.cpp:17-123), one Krylov
+//               process per RHS with device-resident basis and deterministic reductions.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "helmsweep_b200.h"
+#include "hs_kernels.cuh"
+#include "hs_symbolic.hpp"
+
+namespace hsb {
+
+extern std::atomic<long long> g_kernel_launches;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    HS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) HS_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero(cudaStream_t s) {
+    if (p) HS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+double2* as_d2(const Complex* p) { return reinterpret_cast<double2*>(const_cast<Complex*>(p)); }
+
+struct ClassDev {
+  std::unique_ptr<SymbolicClass> sym;
+  DBuf<DevFront> fronts;
+  DBuf<int> bnd_elim, child_map, orig_fpos, orig_eidx, elim_of_local, local_of_elim;
+  DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
+  std::vector<int> level_start_down;
+  DevClass dev{};
+};
+
+struct Engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int dim = 2;
+  std::vector<std::unique_ptr<ClassDev>> classes;
+  std::vector<int> sub_cls;
+  std::vector<DevSub> h_subs;
+  DBuf<DevClass> d_cls;
+  DBuf<DevSub> d_subs;
+  DBuf<double2> factor, dinv, val;
+  std::vector<long long> fac_base, n_base;
+  std::vector<double> tol;
+  double factor_gpu_seconds = 0.0;
+  int nf_max = 0, max_m = 0;
+  long long v_total_max = 0, n_max = 0;
+  // solve state
+  int R = 0, rg = 4, n_rg = 1, nslots = 0, solve_grid_sz = 0;
+  size_t solve_smem = 0;
+  DBuf<double2> x, vbuf;
+  DBuf<unsigned> flags, epoch;
+  unsigned epoch_host = 0;
+
+  ~Engine() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void init(int dev, int d) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw Error(kCuda, "no CUDA device available (helmsweep_b200 has no CPU fallback)");
+    if (dev < 0 || dev >= count) throw Error(kConfig, "device index out of range");
+    device = dev;
+    dim = d;
+    HS_CUDA(cudaSetDevice(device));
+    HS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    epoch.alloc(1);
+    epoch.zero(stream);
+  }
+
+  int add_class(std::unique_ptr<SymbolicClass> sc) {
+    auto cd = std::make_unique<ClassDev>();
+    cd->sym = std::move(sc);
+    classes.push_back(std::move(cd));
+    return static_cast<int>(classes.size()) - 1;
+  }
+
+  // Line tables of one class (elimination positions of trace lines), see DevClass.
+  void build_lines(ClassDev& cd, int pad) {
+    const SymbolicClass& c = *cd.sym;
+    GridRange loc;
+    loc.dim = c.dim;
+    for (int a = 0; a < c.dim; ++a) {
+      loc.lo[a] = 0;
+      loc.hi[a] = c.size[a] - 1;
+    }
+    auto on_shell = [&](const Vec3i& p) {
+      for (int a = 0; a < c.dim; ++a)
+        if (p[a] == 0 || p[a] == c.size[a] - 1) return true;
+      return false;
+    };
+    for (int d = 0; d < 2 * c.dim; ++d) {
+      const int a = d / 2, sign = (d & 1) ? 1 : -1;
+      GridRange line = loc;
+      const int ext_face = sign > 0 ? c.size[a] - 1 - pad : pad;
+      const int inj_face = sign > 0 ? pad : c.size[a] - 1 - pad;
+      line.lo[a] = line.hi[a] = 0;
+      const std::int64_t cnt = line.count();
+      std::vector<int> u0(cnt), um1(cnt), p0(cnt), pm(cnt);
+      for (std::int64_t i = 0; i < cnt; ++i) {
+        Vec3i p = line.unlinear(i);
+        p[a] = ext_face;
+        u0[i] = c.elim_of_local[loc.linear(p)];
+        p[a] = ext_face - sign;
+        um1[i] = c.elim_of_local[loc.linear(p)];
+        p[a] = inj_face;
+        p0[i] = on_shell(p) ? -1 : c.elim_of_local[loc.linear(p)];
+        p[a] = inj_face - sign;
+        pm[i] = on_shell(p) ? -1 : c.elim_of_local[loc.linear(p)];
+      }
+      cd.ext_u0[d].upload(u0, stream);
+      cd.ext_um1[d].upload(um1, stream);
+      cd.inj_p0[d].upload(p0, stream);
+      cd.inj_pm[d].upload(pm, stream);
+      cd.dev.ext_u0[d] = cd.ext_u0[d].p;
+      cd.dev.ext_um1[d] = cd.ext_um1[d].p;
+      cd.dev.inj_p0[d] = cd.inj_p0[d].p;
+      cd.dev.inj_pm[d] = cd.inj_pm[d].p;
+      cd.dev.line_len[d] = static_cast<int>(cnt);
+    }
+  }
+
+  void upload_classes(int pad) {
+    std::vector<DevClass> hc;
+    for (auto& cdp : classes) {
+      ClassDev& cd = *cdp;
+      const SymbolicClass& c = *cd.sym;
+      std::vector<DevFront> fr(c.fronts.size());
+      for (size_t f = 0; f < c.fronts.size(); ++f) {
+        const FrontDesc& s = c.fronts[f];
+        DevFront& d = fr[f];
+        d.k = s.k;
+        d.m = s.m;
+        d.sep_off = s.sep_off;
+        d.bnd_off = s.bnd_off;
+        d.parent = s.parent;
+        d.child0 = s.child[0];
+        d.child1 = s.child[1];
+        d.cmap0 = s.cmap_off[0];
+        d.cmap1 = s.cmap_off[1];
+        d.orig_off = s.orig_off;
+        d.orig_cnt = s.orig_cnt;
+        d.pad_ = 0;
+        d.fac_off = s.fac_off;
+        d.v_off = s.v_off;
+        d.f_off = s.f_off;
+      }
+      cd.fronts.upload(fr, stream);
+      cd.bnd_elim.upload(c.bnd_elim, stream);
+      cd.child_map.upload(c.child_map, stream);
+      cd.orig_fpos.upload(c.orig_fpos, stream);
+      cd.orig_eidx.upload(c.orig_eidx, stream);
+      cd.elim_of_local.upload(c.elim_of_local, stream);
+      cd.local_of_elim.upload(c.local_of_elim, stream);
+      cd.dev.fronts = cd.fronts.p;
+      cd.dev.bnd_elim = cd.bnd_elim.p;
+      cd.dev.child_map = cd.child_map.p;
+      cd.dev.orig_fpos = cd.orig_fpos.p;
+      cd.dev.orig_eidx = cd.orig_eidx.p;
+      cd.dev.elim_of_local = cd.elim_of_local.p;
+      cd.dev.local_of_elim = cd.local_of_elim.p;
+      cd.dev.n = static_cast<int>(c.n);
+      cd.dev.nfronts = static_cast<int>(c.fronts.size());
+      for (int a = 0; a < 3; ++a) cd.dev.size[a] = c.size[a];
+      if (pad >= 0) build_lines(cd, pad);
+      cd.level_start_down.assign(c.max_depth + 2, 0);
+      for (const auto& f : c.fronts) cd.level_start_down[f.depth + 1]++;
+      for (int h = 0; h <= c.max_depth; ++h) cd.level_start_down[h + 1] += cd.level_start_down[h];
+      nf_max = std::max(nf_max, static_cast<int>(c.fronts.size()));
+      max_m = std::max(max_m, c.max_m);
+      v_total_max = std::max(v_total_max, c.v_total);
+      n_max = std::max<long long>(n_max, c.n);
+      hc.push_back(cd.dev);
+    }
+    d_cls.upload(hc, stream);
+  }
+
+  // Factorizes every subdomain (values[sub] = CSR values in the class's CSR structure).
+  void factorize(const std::vector<const CVector*>& values) {
+    const int nsub = static_cast<int>(sub_cls.size());
+    fac_base.assign(nsub + 1, 0);
+    n_base.assign(nsub + 1, 0);
+    std::vector<long long> val_base(nsub + 1, 0);
+    for (int s = 0; s < nsub; ++s) {
+      const SymbolicClass& c = *classes[sub_cls[s]]->sym;
+      fac_base[s + 1] = fac_base[s] + c.fac_total;
+      n_base[s + 1] = n_base[s] + c.n;
+      val_base[s + 1] = val_base[s] + static_cast<long long>(values[s]->size());
+    }
+    factor.alloc(std::max<long long>(fac_base[nsub], 1));
+    dinv.alloc(std::max<long long>(n_base[nsub], 1));
+    val.alloc(std::max<long long>(val_base[nsub], 1));
+    tol.assign(nsub, 0.0);
+    for (int s = 0; s < nsub; ++s) {
+      const CVector& v = *values[s];
+      double scale = 0.0;
+      for (const Complex& z : v) scale = std::max(scale, std::abs(z));
+      tol[s] = 1e-14 * scale;  // src/direct.cpp:191-193
+      HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], v.data(), v.size() * sizeof(Complex),
+                              cudaMemcpyHostToDevice, stream));
+    }
+    h_subs.resize(nsub);
+    for (int s = 0; s < nsub; ++s) {
+      DevSub& d = h_subs[s];
+      d.cls = sub_cls[s];
+      d.tol = tol[s];
+      d.factor = factor.p + fac_base[s];
+      d.dinv = dinv.p + n_base[s];
+      d.val = val.p + val_base[s];
+      d.x = nullptr;
+    }
+    d_subs.upload(h_subs, stream);
+
+    DBuf<unsigned long long> err;
+    err.alloc(1);
+    HS_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), stream));
+    // chunk subdomains so the dense workspaces stay within a memory budget
+    size_t free_b = 0, total_b = 0;
+    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const long long budget = static_cast<long long>(std::min<double>(free_b * 0.4, 24e9)) / sizeof(double2);
+    cudaEvent_t e0, e1;
+    HS_CUDA(cudaEventCreate(&e0));
+    HS_CUDA(cudaEventCreate(&e1));
+    HS_CUDA(cudaEventRecord(e0, stream));
+    DBuf<double2> work, scratch;
+    DBuf<FactorTask> d_tasks;
+    int s0 = 0;
+    while (s0 < nsub) {
+      long long need = 0;
+      int s1 = s0;
+      while (s1 < nsub) {
+        const long long ft = classes[sub_cls[s1]]->sym->f_total;
+        if (s1 > s0 && need + ft > budget) break;
+        need += ft;
+        ++s1;
+      }
+      if (static_cast<long long>(work.n) < need) work.alloc(need);
+      std::vector<long long> fb(s1 - s0 + 1, 0);
+      for (int s = s0; s < s1; ++s) fb[s - s0 + 1] = fb[s - s0] + classes[sub_cls[s]]->sym->f_total;
+      int hmax = 0;
+      for (int s = s0; s < s1; ++s) hmax = std::max(hmax, classes[sub_cls[s]]->sym->max_height);
+      std::vector<FactorTask> tasks;
+      std::vector<int> lstart(hmax + 2, 0), lmaxm(hmax + 1, 0);
+      for (int h = 0; h <= hmax; ++h) {
+        lstart[h] = static_cast<int>(tasks.size());
+        for (int s = s0; s < s1; ++s) {
+          const SymbolicClass& c = *classes[sub_cls[s]]->sym;
+          if (h > c.max_height) continue;
+          for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
+            const int f = c.order_up[q];
+            tasks.push_back(FactorTask{s, f, fb[s - s0]});
+            lmaxm[h] = std::max(lmaxm[h], c.fronts[f].m);
+          }
+        }
+      }
+      lstart[hmax + 1] = static_cast<int>(tasks.size());
+      d_tasks.upload(tasks, stream);
+      for (int h = 0; h <= hmax; ++h) {
+        const int nt = lstart[h + 1] - lstart[h];
+        if (nt == 0) continue;
+        FactorArgs fa{};
+        fa.tasks = d_tasks.p + lstart[h];
+        fa.ntasks = nt;
+        fa.cls = d_cls.p;
+        fa.subs = d_subs.p;
+        fa.work = work.p;
+        fa.err_key = err.p;
+        if (factor_smem_bytes(lmaxm[h]) > 200 * 1024) {
+          const size_t sz = static_cast<size_t>(nt) * 2 * lmaxm[h] * 16;
+          if (scratch.n < sz) scratch.alloc(sz);
+          fa.scratch = scratch.p;
+        }
+        launch_factor_level(fa, lmaxm[h], stream);
+      }
+      HS_CUDA(cudaStreamSynchronize(stream));
+      s0 = s1;
+    }
+    HS_CUDA(cudaEventRecord(e1, stream));
+    HS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    HS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    factor_gpu_seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    unsigned long long key = 0;
+    HS_CUDA(cudaMemcpy(&key, err.p, sizeof(key), cudaMemcpyDeviceToHost));
+    if (key != ~0ull) {
+      const int s = static_cast<int>(key >> 32);
+      const int e = static_cast<int>(key & 0xffffffffu);
+      const int g = classes[sub_cls[s]]->sym->local_of_elim[e];
+      Error err2(kSingular, "factorize: near-zero pivot at grid node " + std::to_string(g));
+      err2.pivot_index = g;
+      err2.pivot_sub = s;
+      throw err2;
+    }
+  }
+
+  // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains.
+  void ensure_solve(int r, int slots) {
+    const int want_rg = r >= 4 ? 4 : (r >= 2 ? 2 : 1);
+    int rgsel = want_rg;
+    if (const char* e = std::getenv("HS_RG")) rgsel = std::max(1, std::min(8, std::atoi(e)));
+    if (r == R && slots <= nslots && rgsel == rg) return;
+    R = r;
+    rg = rgsel;
+    n_rg = (R + rg - 1) / rg;
+    nslots = std::max(slots, nslots);
+    const int nsub = static_cast<int>(sub_cls.size());
+    x.alloc(static_cast<size_t>(n_base[nsub]) * R);
+    vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
+    flags.alloc(static_cast<size_t>(nsub) * nf_max * n_rg);
+    flags.zero(stream);
+    for (int s = 0; s < nsub; ++s) h_subs[s].x = x.p + n_base[s] * R;
+    d_subs.upload(h_subs, stream);
+    solve_smem = solve_smem_bytes(max_m, rg);
+    solve_grid_sz = solve_grid(rg, solve_smem);
+  }
+
+  SolveArgs solve_args(const SolveTask* tasks, int ntasks, unsigned* queue, const unsigned* nzmask,
+                       unsigned epoch_off) const {
+    SolveArgs a{};
+    a.tasks = tasks;
+    a.ntasks = ntasks;
+    a.n_rg = n_rg;
+    a.R = R;
+    a.queue = queue;
+    a.flags = flags.p;
+    a.nf_max = nf_max;
+    a.epoch_base = epoch.p;
+    a.epoch_off = epoch_off;
+    a.cls = d_cls.p;
+    a.subs = d_subs.p;
+    a.vbuf = vbuf.p;
+    a.vslot_stride = v_total_max * R;
+    a.nzmask = nzmask;
+    return a;
+  }
+
+  void run_solve(const SolveArgs& fwd, const SolveArgs& bwd) {
+    const int total = fwd.ntasks * n_rg;
+    const int grid = std::max(1, std::min(solve_grid_sz, total));
+    launch_solve_forward(fwd, rg, grid, solve_smem, stream);
+    launch_solve_backward(bwd, rg, grid, solve_smem, stream);
+  }
+};
+
+// ----------------------------------------------------------------------------
+// standalone factorization (hs_factor)
+
+__global__ void gather_in_kernel(const double2* src, double2* dst, const int* local_of_elim, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const long long e = idx / R;
+  const int r = static_cast<int>(idx % R);
+  dst[idx] = src[static_cast<long long>(r) * n + local_of_elim[e]];
+}
+__global__ void scatter_out_kernel(const double2* src, double2* dst, const int* elim_of_local, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const int r = static_cast<int>(idx / n);
+  const long long l = idx % n;
+  dst[idx] = src[static_cast<long long>(elim_of_local[l]) * R + r];
+}
+
+}  // namespace
+
+struct FactorHandle {
+  Engine eng;
+  hs_factor_stats stats{};
+  std::vector<SolveTask> fwd, bwd;
+  DBuf<SolveTask> d_fwd, d_bwd;
+  DBuf<unsigned> queue, nz;
+  DBuf<double2> io;
+};
+
+struct DdmHandle;
+
+}  // namespace hsb
+
+struct hs_factor {
+  hsb::FactorHandle h;
+};
+
+namespace hsb {
+namespace {
+
+template <class F>
+int guarded(F&& fn, int* pivot_sub = nullptr, std::int64_t* pivot_index = nullptr) {
+  try {
+    fn();
+    return kOk;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    if (e.code == kSingular) {
+      if (pivot_sub) *pivot_sub = e.pivot_sub;
+      if (pivot_index) *pivot_index = e.pivot_index;
+    }
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return kInternal;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return kInternal;
+  }
+}
+
+void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t user) {
+  Engine& eng = H.eng;
+  const SymbolicClass& c = *eng.classes[0]->sym;
+  const long long n = c.n;
+  for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
+    const int R = std::min(kMaxRhs, nrhs - b0);
+    eng.ensure_solve(R, 1);
+    if (user) {
+      cudaEvent_t ev;
+      HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      HS_CUDA(cudaEventRecord(ev, user));
+      HS_CUDA(cudaStreamWaitEvent(eng.stream, ev, 0));
+      cudaEventDestroy(ev);
+    }
+    double2* xb = d_x + b0 * n;
+    const int threads = 256;
+    const int blocks = static_cast<int>((n * R + threads - 1) / threads);
+    gather_in_kernel<<<blocks, threads, 0, eng.stream>>>(xb, eng.x.p, eng.classes[0]->local_of_elim.p, n, R);
+    g_kernel_launches.fetch_add(1);
+    HS_CUDA(cudaGetLastError());
+    const unsigned mask = R >= 32 ? ~0u : ((1u << R) - 1u);
+    HS_CUDA(cudaMemcpyAsync(H.nz.p, &mask, sizeof(unsigned), cudaMemcpyHostToDevice, eng.stream));
+    HS_CUDA(cudaMemsetAsync(H.queue.p, 0, 2 * sizeof(unsigned), eng.stream));
+    launch_bump_epoch(eng.epoch.p, 4, eng.stream);
+    SolveArgs fa = eng.solve_args(H.d_fwd.p, static_cast<int>(H.fwd.size()), H.queue.p, H.nz.p, 1);
+    SolveArgs ba = eng.solve_args(H.d_bwd.p, static_cast<int>(H.bwd.size()), H.queue.p + 1, H.nz.p, 2);
+    eng.run_solve(fa, ba);
+    scatter_out_kernel<<<blocks, threads, 0, eng.stream>>>(eng.x.p, xb, eng.classes[0]->elim_of_local.p, n, R);
+    g_kernel_launches.fetch_add(1);
+    HS_CUDA(cudaGetLastError());
+    if (user) {
+      cudaEvent_t ev;
+      HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      HS_CUDA(cudaEventRecord(ev, eng.stream));
+      HS_CUDA(cudaStreamWaitEvent(user, ev, 0));
+      cudaEventDestroy(ev);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace hsb
+
+using namespace hsb;
+
+extern "C" {
+
+const char* hs_last_error(void) { return g_last_error.c_str(); }
+
+int hs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int64_t hs_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int hs_factorize(int dim, const int lo[3], const int hi[3], int64_t n, const int64_t* row_ptr,
+                 const int64_t* col, const double* val, int device, hs_factor** out,
+                 hs_factor_stats* stats, int64_t* pivot_index) {
+  std::unique_ptr<hs_factor> f;
+  int rc = guarded([&] {
+    if (n <= 0) config_error("factorize: empty operator");
+    if (dim != 2 && dim != 3) config_error("factorize: dim must be 2 or 3");
+    GridRange rng;
+    rng.dim = dim;
+    for (int a = 0; a < 3; ++a) {
+      rng.lo[a] = a < dim ? lo[a] : 0;
+      rng.hi[a] = a < dim ? hi[a] : 0;
+    }
+    if (rng.count() != n) config_error("factorize: grid range does not match operator size");
+    const auto t0 = std::chrono::steady_clock::now();
+    f = std::make_unique<hs_factor>();
+    FactorHandle& H = f->h;
+    H.eng.init(device, dim);
+    std::vector<std::int64_t> rp(row_ptr, row_ptr + n + 1), cl(col, col + row_ptr[n]);
+    CVector v(reinterpret_cast<const Complex*>(val), reinterpret_cast<const Complex*>(val) + row_ptr[n]);
+    H.eng.sub_cls.push_back(H.eng.add_class(build_symbolic(dim, rng, rp, cl)));
+    H.eng.upload_classes(-1);
+    H.eng.factorize({&v});
+    const SymbolicClass& c = *H.eng.classes[0]->sym;
+    for (int h = 0; h <= c.max_height; ++h)
+      for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
+        H.fwd.push_back(SolveTask{0, c.order_up[q], 0, 0});
+    for (int f2 : c.order_down) H.bwd.push_back(SolveTask{0, f2, 0, 0});
+    H.d_fwd.upload(H.fwd, H.eng.stream);
+    H.d_bwd.upload(H.bwd, H.eng.stream);
+    H.queue.alloc(2);
+    H.nz.alloc(1);
+    HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+    H.stats.n = n;
+    H.stats.matrix_nnz = row_ptr[n];
+    H.stats.factor_nnz = c.factor_nnz;
+    H.stats.peak_bytes = c.peak_bytes;
+    H.stats.factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = H.stats;
+  }, nullptr, pivot_index);
+  if (rc != kOk) return rc;
+  *out = f.release();
+  return kOk;
+}
+
+}  // extern "C"
+
+extern "C" int hs_factor_solve_device(hs_factor* f, int nrhs, double* d_x, void* stream) {
+  return guarded([&] {
+    if (!f) config_error("hs_factor_solve_device: null handle");
+    if (nrhs <= 0) return;
+    HS_CUDA(cudaSetDevice(f->h.eng.device));
+    factor_solve_device(f->h, nrhs, reinterpret_cast<double2*>(d_x), static_cast<cudaStream_t>(stream));
+    if (!stream) HS_CUDA(cudaStreamSynchronize(f->h.eng.stream));
+  });
+}
+
+extern "C" int hs_factor_solve(hs_factor* f, int nrhs, double* x) {
+  return guarded([&] {
+    if (!f) config_error("hs_factor_solve: null handle");
+    if (nrhs <= 0) return;
+    FactorHandle& H = f->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    const long long n = H.stats.n;
+    H.io.alloc(static_cast<size_t>(n) * nrhs);
+    HS_CUDA(cudaMemcpyAsync(H.io.p, x, sizeof(double2) * n * nrhs, cudaMemcpyHostToDevice, H.eng.stream));
+    factor_solve_device(H, nrhs, H.io.p, nullptr);
+    HS_CUDA(cudaMemcpyAsync(x, H.io.p, sizeof(double2) * n * nrhs, cudaMemcpyDeviceToHost, H.eng.stream));
+    HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+  });
+}
+
+extern "C" int hs_factor_stats_get(const hs_factor* f, hs_factor_stats* stats) {
+  if (!f || !stats) return kConfig;
+  *stats = f->h.stats;
+  return kOk;
+}
+
+extern "C" void hs_factor_destroy(hs_factor* f) { delete f; }
+
+// ============================================================================
+// DdmSolver
+
+namespace hsb {
+namespace {
+
+struct SubHost {
+  Vec3i sub{0, 0, 0};
+  GridRange owned, range;
+  Box cell;
+  int cls = 0;
+};
+
+constexpr unsigned kEpochSpan = 1u << 16;
+
+}  // namespace
+
+struct DdmHandle {
+  Engine eng;
+  int dim = 2;
+  PmlSpec pml;
+  Medium medium;
+  Box interior;
+  Vec3i intervals{1, 1, 1};
+  Partition part;
+  Weights wts;
+  LocalGrid ggrid;
+  PmlCoefficients gcoeffs;
+  std::vector<double> gkappa;
+  std::vector<SubHost> subs;
+  std::vector<hs_factor_stats> sub_stats;
+  double factor_seconds = 0.0;
+  DevGeom geom{};
+  int steps = 0, ndir = 4, dirs = 4, max_group = 1;
+  long long line_max = 1;
+  std::vector<std::vector<int>> groups;  // [di * steps + s-1]
+  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
+  DBuf<int> d_groups;
+  DBuf<SolveTask> d_tasks;
+  DBuf<double2> d_coef;
+  // per (R, rounds) state
+  int R = 0, nsweeps = 0, rounds = 0;
+  std::vector<Vec3i> plan;
+  std::vector<int> route_h;
+  DBuf<double2> mbox;
+  DBuf<unsigned> mpres, nzmask, queue;
+  DBuf<int> route;
+  DBuf<double2> bN, u, io;
+  DBuf<double> partial, norms, pnum, pden, rnum, rden;
+  std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l, then step pairs
+  // global operator (lazy)
+  bool gop_ready = false;
+  long long g_nnz = 0;
+  DBuf<std::int64_t> g_rp;
+  DBuf<int> g_col;
+  DBuf<double2> g_val;
+
+  ~DdmHandle() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+
+  void build(const hs_problem& P, int device);
+  void ensure_state(int r, int nrounds);
+  void ensure_gop();
+  void run(int nrounds, bool track, bool timed);
+  void reports(int nrounds, bool track, hs_solve_report* out);
+};
+
+namespace {
+
+Medium medium_from(const hs_problem& P) {
+  Medium m;
+  switch (P.medium_kind) {
+    case 0:
+      if (P.kappa <= 0.0) config_error("WaveNumberModel: kappa must be positive");
+      m.kind = Medium::Constant;
+      m.kappa = P.kappa;
+      break;
+    case 1:
+      if (P.kappa_down <= 0.0 || P.kappa_up <= 0.0) config_error("WaveNumberModel: kappa must be positive");
+      if (P.eps < 0.0) config_error("WaveNumberModel: blend width must be >= 0");
+      m.kind = Medium::TwoLayered;
+      m.kappa_down = P.kappa_down;
+      m.kappa_up = P.kappa_up;
+      m.axis = P.interface_axis;
+      m.eta = P.eta;
+      m.eps = P.eps;
+      break;
+    case 2: {
+      m.kind = Medium::Gridded;
+      VelocityGrid& g = m.velocity;
+      g.dim = P.vel_dim;
+      if (g.dim != 2 && g.dim != 3) data_error("VelocityGrid: dim must be 2 or 3");
+      std::int64_t cnt = 1;
+      for (int a = 0; a < 3; ++a) {
+        g.n[a] = a < g.dim ? P.vel_n[a] : 1;
+        g.origin[a] = P.vel_origin[a];
+        g.spacing[a] = P.vel_spacing[a];
+      }
+      for (int a = 0; a < g.dim; ++a) {
+        if (g.n[a] < 2) data_error("VelocityGrid: need at least 2 samples per axis");
+        if (g.spacing[a] <= 0.0) data_error("VelocityGrid: spacing must be positive");
+        cnt *= g.n[a];
+      }
+      if (!P.vel_c) data_error("VelocityGrid: missing samples");
+      g.c.assign(P.vel_c, P.vel_c + cnt);
+      for (float v : g.c)
+        if (!(v > 0.0f)) data_error("VelocityGrid: non-positive velocity sample");
+      if (P.omega <= 0.0) config_error("WaveNumberModel: omega must be positive");
+      m.omega = P.omega;
+      break;
+    }
+    default:
+      config_error("unknown medium kind");
+  }
+  return m;
+}
+
+}  // namespace
+
+// DdmSolver ctor + build_subdomain_states (src/sweeper.cpp:75-157).
+void DdmHandle::build(const hs_problem& P, int device) {
+  dim = P.dim;
+  if (dim != 2 && dim != 3) config_error("Box: dim must be 2 or 3");
+  interior.dim = dim;
+  for (int a = 0; a < 3; ++a) {
+    interior.lo[a] = a < dim ? P.interior_lo[a] : 0.0;
+    interior.hi[a] = a < dim ? P.interior_hi[a] : 1.0;
+    intervals[a] = a < dim ? P.intervals[a] : 1;
+  }
+  for (int a = 0; a < dim; ++a)
+    if (!(interior.lo[a] < interior.hi[a])) config_error("Box: lo must be strictly below hi on every axis");
+  pml.width = P.pml_width;
+  pml.strength = P.pml_strength;
+  pml.exponent = P.pml_exponent;
+  if (pml.width < 1) config_error("PmlSpec: width must be >= 1 layer");
+  if (pml.strength <= 0.0) config_error("PmlSpec: strength must be positive");
+  if (pml.exponent < 1) config_error("PmlSpec: exponent must be >= 1");
+  if (pml.width < 2) config_error("DdmSolver: pml.width must be >= 2 so trace lines stay off the shell");
+  medium = medium_from(P);
+  const auto t0 = std::chrono::steady_clock::now();
+  part = make_partition(interior, intervals, Vec3i{P.counts[0], P.counts[1], P.counts[2]});
+  wts.p = &part;
+  wts.pad = pml.width;
+  ggrid.dim = dim;
+  ggrid.range.dim = dim;
+  for (int a = 0; a < dim; ++a) {
+    ggrid.h[a] = part.h[a];
+    ggrid.origin[a] = interior.lo[a];
+    ggrid.range.lo[a] = -pml.width;
+    ggrid.range.hi[a] = intervals[a] + pml.width;
+  }
+  gcoeffs = build_coefficients(pml, interior, ggrid);
+  gkappa = extend_to_subdomain(medium, interior, ggrid);
+
+  eng.init(device, dim);
+  const int nsub = part.cell_count();
+  subs.resize(nsub);
+  std::vector<CVector> vals(nsub);
+  std::map<std::vector<int>, int> class_of_key;
+  std::vector<PmlCoefficients> coeffs(nsub);
+  for (int id = 0; id < nsub; ++id) {
+    SubHost& st = subs[id];
+    st.sub = part.unflatten(id);
+    st.owned = part.owned(st.sub);
+    st.cell = part.cell(st.sub);
+    st.range = st.owned;
+    for (int a = 0; a < dim; ++a) {
+      st.range.lo[a] -= pml.width;
+      st.range.hi[a] += pml.width;
+    }
+    LocalGrid g;
+    g.dim = dim;
+    g.range = st.range;
+    g.h = ggrid.h;
+    g.origin = ggrid.origin;
+    coeffs[id] = build_coefficients(pml, st.cell, g);
+    const std::vector<double> kap = extend_to_subdomain(medium, st.cell, g);
+    Csr op = assemble(g, coeffs[id], kap);
+    // symbolic class key: extents, and the lower index (or its parity when non-negative:
+    // C++ truncating mid = (lo+hi)/2 only depends on it through that)
+    std::vector<int> key;
+    for (int a = 0; a < dim; ++a) {
+      key.push_back(st.range.size(a));
+      key.push_back(st.range.lo[a] < 0 ? st.range.lo[a] : (1 << 30) + (st.range.lo[a] & 1));
+    }
+    auto it = class_of_key.find(key);
+    if (it == class_of_key.end()) {
+      st.cls = eng.add_class(build_symbolic(dim, st.range, op.row_ptr, op.col));
+      class_of_key[key] = st.cls;
+    } else {
+      st.cls = it->second;
+      if (eng.classes[st.cls]->sym->csr_col.size() != op.col.size())
+        throw Error(kInternal, "symbolic class CSR mismatch");
+    }
+    eng.sub_cls.push_back(st.cls);
+    vals[id] = std::move(op.val);
+  }
+  eng.upload_classes(pml.width);
+  // injection couplings per subdomain and incoming direction (src/transfer.cpp:80-86)
+  dirs = 2 * dim;
+  for (auto& cdp : eng.classes)
+    for (int d = 0; d < dirs; ++d) line_max = std::max<long long>(line_max, cdp->dev.line_len[d]);
+  std::vector<Complex> coef(static_cast<size_t>(nsub) * dirs * line_max);
+  for (int id = 0; id < nsub; ++id) {
+    const SubHost& st = subs[id];
+    const SymbolicClass& c = *eng.classes[st.cls]->sym;
+    for (int d = 0; d < dirs; ++d) {
+      const int a = d / 2, sign = (d & 1) ? 1 : -1;
+      GridRange line = st.range;
+      const int face = sign > 0 ? st.owned.lo[a] : st.owned.hi[a];
+      line.lo[a] = line.hi[a] = face;
+      const std::int64_t cnt = line.count();
+      for (std::int64_t i = 0; i < cnt; ++i) {
+        const Vec3i p0 = line.unlinear(i);
+        Vec3i pm = p0;
+        pm[a] = face - sign;
+        const Vec3i edge = sign > 0 ? pm : p0;
+        coef[(static_cast<size_t>(id) * dirs + d) * line_max + i] = coeffs[id].coupling(a, edge);
+      }
+      (void)c;
+    }
+  }
+  d_coef.alloc(coef.size());
+  HS_CUDA(cudaMemcpyAsync(d_coef.p, coef.data(), coef.size() * sizeof(Complex), cudaMemcpyHostToDevice, eng.stream));
+  std::vector<const CVector*> vp(nsub);
+  for (int id = 0; id < nsub; ++id) vp[id] = &vals[id];
+  // factorize (the DevSub array is re-uploaded with the coefficient pointers below)
+  eng.factorize(vp);
+  for (int id = 0; id < nsub; ++id) {
+    DevSub& d = eng.h_subs[id];
+    for (int a = 0; a < 3; ++a) {
+      d.sub[a] = subs[id].sub[a];
+      d.lo[a] = a < dim ? subs[id].range.lo[a] : 0;
+    }
+    for (int q = 0; q < kMaxDirs; ++q)
+      d.coef[q] = q < dirs ? reinterpret_cast<const double2*>(d_coef.p) + (static_cast<size_t>(id) * dirs + q) * line_max
+                           : nullptr;
+  }
+  eng.d_subs.upload(eng.h_subs, eng.stream);
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  sub_stats.resize(nsub);
+  for (int id = 0; id < nsub; ++id) {
+    const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
+    hs_factor_stats& s = sub_stats[id];
+    s.n = c.n;
+    s.matrix_nnz = static_cast<int64_t>(vals[id].size());
+    s.factor_nnz = c.factor_nnz;
+    s.peak_bytes = c.peak_bytes;
+    s.factor_seconds = eng.factor_gpu_seconds;
+  }
+  // geometry for the sweep kernels
+  geom.dim = dim;
+  geom.pad = pml.width;
+  geom.nsub = nsub;
+  geom.gn = ggrid.range.count();
+  for (int a = 0; a < 3; ++a) {
+    geom.glo[a] = a < dim ? ggrid.range.lo[a] : 0;
+    geom.gsize[a] = a < dim ? ggrid.range.size(a) : 1;
+    geom.counts[a] = part.counts[a];
+    geom.cut_w[a] = a < dim ? intervals[a] / part.counts[a] : 1;
+  }
+  // step groups and dataflow task lists per (sweep direction, step)
+  steps = sweep_step_count(part.counts, dim);
+  ndir = 1 << dim;
+  const std::vector<Vec3i> dirs_plan = sweep_plan(dim, 1);
+  std::vector<int> gflat;
+  std::vector<SolveTask> tasks;
+  groups.assign(ndir * steps, {});
+  grp_off.assign(ndir * steps, 0);
+  fwd_off.assign(ndir * steps, 0);
+  fwd_cnt.assign(ndir * steps, 0);
+  bwd_off.assign(ndir * steps, 0);
+  bwd_cnt.assign(ndir * steps, 0);
+  int hmax = 0, dmax = 0;
+  for (auto& cdp : eng.classes) {
+    hmax = std::max(hmax, cdp->sym->max_height);
+    dmax = std::max(dmax, cdp->sym->max_depth);
+  }
+  for (int di = 0; di < ndir; ++di)
+    for (int s = 1; s <= steps; ++s) {
+      const int gi = di * steps + s - 1;
+      for (int id = 0; id < nsub; ++id)
+        if (step_of(part.counts, dim, dirs_plan[di], subs[id].sub) == s) groups[gi].push_back(id);
+      max_group = std::max(max_group, static_cast<int>(groups[gi].size()));
+      grp_off[gi] = static_cast<int>(gflat.size());
+      gflat.insert(gflat.end(), groups[gi].begin(), groups[gi].end());
+      fwd_off[gi] = static_cast<int>(tasks.size());
+      for (int h = 0; h <= hmax; ++h)
+        for (size_t g = 0; g < groups[gi].size(); ++g) {
+          const int id = groups[gi][g];
+          const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
+          if (h > c.max_height) continue;
+          for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
+            tasks.push_back(SolveTask{id, c.order_up[q], static_cast<int>(g), 0});
+        }
+      fwd_cnt[gi] = static_cast<int>(tasks.size()) - fwd_off[gi];
+      bwd_off[gi] = static_cast<int>(tasks.size());
+      for (int dd = 0; dd <= dmax; ++dd)
+        for (size_t g = 0; g < groups[gi].size(); ++g) {
+          const int id = groups[gi][g];
+          const ClassDev& cd = *eng.classes[subs[id].cls];
+          if (dd > cd.sym->max_depth) continue;
+          for (int q = cd.level_start_down[dd]; q < cd.level_start_down[dd + 1]; ++q)
+            tasks.push_back(SolveTask{id, cd.sym->order_down[q], static_cast<int>(g), 0});
+        }
+      bwd_cnt[gi] = static_cast<int>(tasks.size()) - bwd_off[gi];
+    }
+  d_groups.upload(gflat, eng.stream);
+  d_tasks.upload(tasks, eng.stream);
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+}
+
+void DdmHandle::ensure_state(int r, int nrounds) {
+  if (r < 1 || r > kMaxRhs) config_error("ddm_solve: batch size out of range");
+  if (nrounds < 1) config_error("SweepPlan: rounds must be >= 1");
+  const int ns = nrounds * ndir;
+  if (ns > HS_MAX_SWEEPS || nrounds > HS_MAX_ROUNDS) config_error("ddm_solve: too many rounds");
+  eng.ensure_solve(r, max_group);
+  if (r == R && nrounds == rounds) return;
+  R = r;
+  rounds = nrounds;
+  nsweeps = ns;
+  plan = sweep_plan(dim, nrounds);
+  const int nsub = geom.nsub;
+  route_h.assign(nsweeps * dirs, 0);
+  for (int l = 1; l <= nsweeps; ++l)
+    for (int d = 0; d < dirs; ++d) route_h[(l - 1) * dirs + d] = route_trace(plan, dim, l, d / 2, (d & 1) ? 1 : -1);
+  route.upload(route_h, eng.stream);
+  mbox.alloc(static_cast<size_t>(nsub) * nsweeps * dirs * 2 * line_max * R);
+  mpres.alloc(static_cast<size_t>(nsub) * nsweeps * dirs);
+  nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
+  queue.alloc(static_cast<size_t>(nsweeps) * steps * 2);
+  bN.alloc(static_cast<size_t>(geom.gn) * R);
+  u.alloc(static_cast<size_t>(geom.gn) * R);
+  const long long nb = (geom.gn * R + 255) / 256;
+  partial.alloc(static_cast<size_t>(nb) * R);
+  pnum.alloc(static_cast<size_t>(nb) * R);
+  pden.alloc(static_cast<size_t>(nb) * R);
+  norms.alloc(static_cast<size_t>(nsweeps) * R);
+  rnum.alloc(static_cast<size_t>(nrounds) * R);
+  rden.alloc(static_cast<size_t>(nrounds) * R);
+  for (auto e : ev) cudaEventDestroy(e);
+  ev.assign(1 + nsweeps + 2 * nsweeps * steps, nullptr);
+  for (auto& e : ev) HS_CUDA(cudaEventCreate(&e));
+}
+
+void DdmHandle::ensure_gop() {
+  if (gop_ready) return;
+  Csr op = assemble(ggrid, gcoeffs, gkappa);
+  g_nnz = static_cast<long long>(op.col.size());
+  std::vector<int> col32(op.col.begin(), op.col.end());
+  g_rp.upload(op.row_ptr, eng.stream);
+  g_col.upload(col32, eng.stream);
+  g_val.alloc(op.val.size());
+  HS_CUDA(cudaMemcpyAsync(g_val.p, op.val.data(), op.val.size() * sizeof(Complex), cudaMemcpyHostToDevice,
+                          eng.stream));
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  gop_ready = true;
+}
+
+// One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
+void DdmHandle::run(int nrounds, bool track, bool timed) {
+  cudaStream_t s = eng.stream;
+  const int nsub = geom.nsub;
+  if (track) ensure_gop();
+  HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
+  HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(unsigned), s));
+  HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(unsigned), s));
+  HS_CUDA(cudaMemsetAsync(queue.p, 0, queue.n * sizeof(unsigned), s));
+  launch_bump_epoch(eng.epoch.p, kEpochSpan, s);
+  if (timed) HS_CUDA(cudaEventRecord(ev[0], s));
+  SweepArgs sa{};
+  sa.g = geom;
+  sa.cls = eng.d_cls.p;
+  sa.subs = eng.d_subs.p;
+  sa.R = R;
+  sa.nsweeps = nsweeps;
+  sa.dirs = dirs;
+  sa.b = bN.p;
+  sa.mbox = mbox.p;
+  sa.mbox_dir_stride = 2 * line_max * R;
+  sa.mpres = mpres.p;
+  sa.nzmask = nzmask.p;
+  sa.route = route.p;
+  for (int l = 1; l <= nsweeps; ++l) {
+    const int di = (l - 1) % ndir;
+    sa.l = l;
+    for (int st = 1; st <= steps; ++st) {
+      const int gi = di * steps + st - 1;
+      sa.group = d_groups.p + grp_off[gi];
+      sa.ngroup = static_cast<int>(groups[gi].size());
+      launch_build_rhs(sa, eng.n_max, s);
+      const int qi = ((l - 1) * steps + (st - 1)) * 2;
+      const unsigned off = 1u + static_cast<unsigned>(qi);
+      const unsigned* nz = nzmask.p + static_cast<size_t>(l - 1) * nsub;
+      SolveArgs fa = eng.solve_args(d_tasks.p + fwd_off[gi], fwd_cnt[gi], queue.p + qi, nz, off);
+      SolveArgs ba = eng.solve_args(d_tasks.p + bwd_off[gi], bwd_cnt[gi], queue.p + qi + 1, nz, off + 1);
+      if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
+      eng.run_solve(fa, ba);
+      if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
+      launch_extract_deposit(sa, static_cast<int>(line_max), s);
+    }
+    AccumArgs aa{};
+    aa.g = geom;
+    aa.cls = eng.d_cls.p;
+    aa.subs = eng.d_subs.p;
+    aa.R = R;
+    aa.l = l;
+    for (int a = 0; a < 3; ++a) aa.dvec[a] = plan[l - 1][a];
+    aa.nzmask = nzmask.p + static_cast<size_t>(l - 1) * nsub;
+    aa.u = u.p;
+    aa.partial = partial.p;
+    const int nb = launch_accumulate(aa, s);
+    launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
+    if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
+    if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
+      const int rr = l / ndir - 1;
+      const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
+      launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
+      launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
+    }
+  }
+}
+
+// SolveReport per RHS: counters replayed from the device's per-task nonzero masks in the
+// reference's canonical order (src/sweeper.cpp:285-307).
+void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
+  const int nsub = geom.nsub;
+  std::vector<unsigned> nz(static_cast<size_t>(nsweeps) * nsub);
+  std::vector<double> nrm(static_cast<size_t>(nsweeps) * R), num(static_cast<size_t>(nrounds) * R),
+      den(static_cast<size_t>(nrounds) * R);
+  HS_CUDA(cudaMemcpyAsync(nz.data(), nzmask.p, nz.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, eng.stream));
+  HS_CUDA(cudaMemcpyAsync(nrm.data(), norms.p, nrm.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
+  if (track) {
+    HS_CUDA(cudaMemcpyAsync(num.data(), rnum.p, num.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
+    HS_CUDA(cudaMemcpyAsync(den.data(), rden.p, den.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
+  }
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  std::vector<double> sweep_sec(nsweeps, 0.0), step_sec(static_cast<size_t>(nsweeps) * steps, 0.0);
+  float ms = 0.f;
+  for (int l = 1; l <= nsweeps; ++l) {
+    HS_CUDA(cudaEventElapsedTime(&ms, ev[l - 1], ev[l]));
+    sweep_sec[l - 1] = ms * 1e-3;
+    for (int st = 0; st < steps; ++st) {
+      const int q = (l - 1) * steps + st;
+      HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * q], ev[2 + nsweeps + 2 * q]));
+      step_sec[q] = ms * 1e-3;
+    }
+  }
+  double total = 0.0;
+  cudaEvent_t last = ev[nsweeps];
+  HS_CUDA(cudaEventElapsedTime(&ms, ev[0], last));
+  total = ms * 1e-3;
+  for (int r = 0; r < R; ++r) {
+    hs_solve_report& rep = out[r];
+    std::memset(&rep, 0, sizeof(rep));
+    rep.factor_seconds = factor_seconds;
+    rep.sweep_seconds_total = total;
+    rep.n_sweeps = nsweeps;
+    std::vector<double> task_times;
+    for (int l = 1; l <= nsweeps; ++l) {
+      const int di = (l - 1) % ndir;
+      rep.sweep_seconds[l - 1] = sweep_sec[l - 1];
+      rep.sweep_contrib_norm[l - 1] = std::sqrt(nrm[static_cast<size_t>(l - 1) * R + r]);
+      for (int st = 1; st <= steps; ++st) {
+        const auto& grp = groups[di * steps + st - 1];
+        int active = 0;
+        for (int id : grp) active += nz[static_cast<size_t>(l - 1) * nsub + id] != 0;
+        for (int id : grp) {
+          const bool nonzero = (nz[static_cast<size_t>(l - 1) * nsub + id] >> r) & 1u;
+          if (!nonzero) {
+            ++rep.skipped_zero_solves;
+            continue;
+          }
+          ++rep.local_solves;
+          task_times.push_back(step_sec[(l - 1) * steps + st - 1] / std::max(active, 1));
+          const Vec3i sb = subs[id].sub;
+          for (int d = 0; d < dirs; ++d) {
+            if (!part.has_neighbor(sb, d / 2, (d & 1) ? 1 : -1)) continue;
+            ++rep.traces_generated;
+            if (route_h[(l - 1) * dirs + d] == 0)
+              ++rep.traces_discarded;
+            else
+              ++rep.traces_routed;
+          }
+        }
+      }
+    }
+    if (!task_times.empty()) {
+      std::sort(task_times.begin(), task_times.end());
+      rep.median_subdomain_solve_seconds = task_times[task_times.size() / 2];
+    }
+    if (track) {
+      rep.n_round_residuals = nrounds;
+      for (int q = 0; q < nrounds; ++q) {
+        const double dd = den[static_cast<size_t>(q) * R + r];
+        rep.round_residuals[q] = dd > 0 ? std::sqrt(num[static_cast<size_t>(q) * R + r] / dd) : 0.0;
+      }
+    }
+  }
+}
+
+}  // namespace hsb
+
+struct hs_ddm {
+  hsb::DdmHandle h;
+};
+
+namespace {
+
+void ddm_solve_batch(DdmHandle& H, int R, const double2* d_b, double2* d_u, int rounds, bool track,
+                     hs_solve_report* reps) {
+  H.ensure_state(R, rounds);
+  launch_transpose_in(d_b, H.bN.p, H.geom.gn, R, H.eng.stream);
+  H.run(rounds, track, true);
+  launch_transpose_out(H.u.p, d_u, H.geom.gn, R, H.eng.stream);
+  if (reps) H.reports(rounds, track, reps);
+}
+
+}  // namespace
+
+extern "C" int hs_ddm_create(const hs_problem* setup, int device, hs_ddm** out, int* pivot_sub,
+                             int64_t* pivot_index) {
+  std::unique_ptr<hs_ddm> s;
+  const int rc = guarded(
+      [&] {
+        if (!setup || !out) config_error("hs_ddm_create: null argument");
+        s = std::make_unique<hs_ddm>();
+        s->h.build(*setup, device);
+      },
+      pivot_sub, pivot_index);
+  if (rc != kOk) return rc;
+  *out = s.release();
+  return kOk;
+}
+
+extern "C" void hs_ddm_destroy(hs_ddm* s) { delete s; }
+
+extern "C" int hs_ddm_info(const hs_ddm* s, int* dim, int64_t* global_n, int* nsub, double* factor_seconds,
+                           int lo[3], int hi[3]) {
+  if (!s) return kConfig;
+  const DdmHandle& H = s->h;
+  if (dim) *dim = H.dim;
+  if (global_n) *global_n = H.ggrid.range.count();
+  if (nsub) *nsub = H.geom.nsub;
+  if (factor_seconds) *factor_seconds = H.factor_seconds;
+  for (int a = 0; a < 3; ++a) {
+    if (lo) lo[a] = a < H.dim ? H.ggrid.range.lo[a] : 0;
+    if (hi) hi[a] = a < H.dim ? H.ggrid.range.hi[a] : 0;
+  }
+  return kOk;
+}
+
+extern "C" int hs_ddm_sub_stats(const hs_ddm* s, int sub, hs_factor_stats* stats) {
+  if (!s || !stats || sub < 0 || sub >= s->h.geom.nsub) return kConfig;
+  *stats = s->h.sub_stats[sub];
+  return kOk;
+}
+
+// DdmSolver::scale_source (src/sweeper.cpp:164-174): input marshaling on the host.
+extern "C" int hs_ddm_scale_source(const hs_ddm* s, int nrhs, const double* f, double* b) {
+  return guarded([&] {
+    if (!s) config_error("scale_source: null handle");
+    const DdmHandle& H = s->h;
+    const std::int64_t n = H.ggrid.range.count();
+    const Complex* fi = reinterpret_cast<const Complex*>(f);
+    Complex* bo = reinterpret_cast<Complex*>(b);
+    for (int r = 0; r < nrhs; ++r)
+      for (std::int64_t i = 0; i < n; ++i) {
+        const Vec3i p = H.ggrid.range.unlinear(i);
+        bo[r * n + i] = H.ggrid.on_shell(p) ? Complex(0.0) : H.gcoeffs.jacobian(p) * fi[r * n + i];
+      }
+  });
+}
+
+extern "C" int hs_ddm_solve_device(hs_ddm* s, int nrhs, const double* d_b, double* d_u, int rounds,
+                                   int track_residuals, hs_solve_report* reports, void* stream) {
+  return guarded([&] {
+    if (!s) config_error("ddm_solve: null handle");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t evw;
+    HS_CUDA(cudaEventCreateWithFlags(&evw, cudaEventDisableTiming));
+    if (user) {
+      HS_CUDA(cudaEventRecord(evw, user));
+      HS_CUDA(cudaStreamWaitEvent(H.eng.stream, evw, 0));
+    }
+    const long long n = H.geom.gn;
+    for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
+      const int R = std::min(kMaxRhs, nrhs - b0);
+      ddm_solve_batch(H, R, reinterpret_cast<const double2*>(d_b) + b0 * n, reinterpret_cast<double2*>(d_u) + b0 * n,
+                      rounds, track_residuals != 0, reports ? reports + b0 : nullptr);
+    }
+    if (user) {
+      HS_CUDA(cudaEventRecord(evw, H.eng.stream));
+      HS_CUDA(cudaStreamWaitEvent(user, evw, 0));
+    } else {
+      HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+    }
+    cudaEventDestroy(evw);
+  });
+}
+
+extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int rounds, int track_residuals,
+                            hs_solve_report* reports) {
+  return guarded([&] {
+    if (!s) config_error("ddm_solve: null handle");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    const long long n = H.geom.gn;
+    for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
+      const int R = std::min(kMaxRhs, nrhs - b0);
+      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
+      double2* din = H.io.p;
+      double2* dout = H.io.p + static_cast<size_t>(n) * kMaxRhs;
+      HS_CUDA(cudaMemcpyAsync(din, b + 2 * b0 * n, sizeof(double2) * n * R, cudaMemcpyHostToDevice, H.eng.stream));
+      ddm_solve_batch(H, R, din, dout, rounds, track_residuals != 0, reports ? reports + b0 : nullptr);
+      HS_CUDA(cudaMemcpyAsync(u + 2 * b0 * n, dout, sizeof(double2) * n * R, cudaMemcpyDeviceToHost, H.eng.stream));
+      HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+    }
+  });
+}
+
+extern "C" int hs_ddm_apply_op(hs_ddm* s, int nrhs, const double* x, double* y) {
+  return guarded([&] {
+    if (!s) config_error("apply: null handle");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    H.ensure_gop();
+    const long long n = H.geom.gn;
+    DBuf<double2> a, b2, c, d;
+    a.alloc(static_cast<size_t>(n) * nrhs);
+    b2.alloc(static_cast<size_t>(n) * nrhs);
+    c.alloc(static_cast<size_t>(n) * nrhs);
+    d.alloc(static_cast<size_t>(n) * nrhs);
+    HS_CUDA(cudaMemcpyAsync(a.p, x, sizeof(double2) * n * nrhs, cudaMemcpyHostToDevice, H.eng.stream));
+    launch_transpose_in(a.p, b2.p, n, nrhs, H.eng.stream);
+    launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, b2.p, c.p, nrhs, H.eng.stream);
+    launch_transpose_out(c.p, d.p, n, nrhs, H.eng.stream);
+    HS_CUDA(cudaMemcpyAsync(y, d.p, sizeof(double2) * n * nrhs, cudaMemcpyDeviceToHost, H.eng.stream));
+    HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+  });
+}
+
+// Right-preconditioned full GMRES with MGS and complex Givens (src/krylov.cpp:17-123), the
+// DDM application as preconditioner and the global operator as A (src/harness.cpp:285-305).
+// One Krylov process per RHS column; the preconditioner and operator are batched.
+extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
+                        hs_gmres_report* reports) {
+  return guarded([&] {
+    if (!s) config_error("gmres: null handle");
+    if (!(tol > 0.0)) config_error("GmresConfig: tol must be positive");
+    if (maxit < 1) config_error("GmresConfig: max_iterations must be >= 1");
+    if (maxit + 1 > HS_MAX_GMRES_HISTORY) config_error("gmres: maxit too large for the report");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    H.ensure_gop();
+    cudaStream_t st = H.eng.stream;
+    const long long n = H.geom.gn;
+    size_t free_b = 0, total_b = 0;
+    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double per_col = static_cast<double>(maxit + 4) * n * sizeof(double2);
+    const int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
+    for (int b0 = 0; b0 < nrhs; b0 += rmax) {
+      const int R = std::min(rmax, nrhs - b0);
+      H.ensure_state(R, rounds);
+      const size_t nr = static_cast<size_t>(n) * R;
+      DBuf<double2> Bv, V, W, X, io, part, hcol;
+      DBuf<double> inv;
+      Bv.alloc(nr);
+      V.alloc(nr * (maxit + 1));
+      W.alloc(nr);
+      X.alloc(nr);
+      io.alloc(nr);
+      const int nb = static_cast<int>((nr + 255) / 256);
+      part.alloc(static_cast<size_t>(nb) * R);
+      hcol.alloc(static_cast<size_t>(maxit + 2) * R);
+      inv.alloc(R);
+      HS_CUDA(cudaMemcpyAsync(io.p, b + 2 * b0 * n, sizeof(double2) * nr, cudaMemcpyHostToDevice, st));
+      launch_transpose_in(io.p, Bv.p, n, R, st);
+      auto dot = [&](const double2* a, const double2* c, double2* out) {
+        const int blocks = launch_dot_partials(a, c, n, R, part.p, st);
+        launch_reduce_cpartials(part.p, blocks, R, out, st);
+      };
+      std::vector<double2> hh(static_cast<size_t>(maxit + 2) * R);
+      dot(Bv.p, Bv.p, hcol.p);
+      HS_CUDA(cudaMemcpyAsync(hh.data(), hcol.p, sizeof(double2) * R, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      std::vector<double> bnorm(R), invh(R);
+      std::vector<int> iters(R, 0), active(R, 1), breakdown(R, 0);
+      std::vector<std::vector<double>> hist(R);
+      std::vector<std::vector<std::vector<Complex>>> hess(R);
+      std::vector<std::vector<Complex>> cs(R, std::vector<Complex>(maxit)), sn(R, std::vector<Complex>(maxit)),
+          g(R, std::vector<Complex>(maxit + 1, Complex(0.0)));
+      for (int r = 0; r < R; ++r) {
+        bnorm[r] = std::sqrt(hh[r].x);
+        if (bnorm[r] == 0.0) {
+          active[r] = 0;
+          hist[r].push_back(0.0);
+          invh[r] = 0.0;
+        } else {
+          invh[r] = 1.0 / bnorm[r];
+          g[r][0] = bnorm[r];
+          hist[r].push_back(1.0);
+        }
+      }
+      // v0 = b / ||b||
+      HS_CUDA(cudaMemcpyAsync(V.p, Bv.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+      HS_CUDA(cudaMemcpyAsync(inv.p, invh.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
+      launch_scale_cols(V.p, inv.p, n, R, st);
+      int j = 0;
+      auto any_active = [&] {
+        for (int r = 0; r < R; ++r)
+          if (active[r]) return true;
+        return false;
+      };
+      while (j < maxit && any_active()) {
+        double2* vj = V.p + static_cast<size_t>(j) * nr;
+        HS_CUDA(cudaMemcpyAsync(H.bN.p, vj, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+        H.run(rounds, false, false);                                          // z = M^-1 v_j
+        launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, H.u.p, W.p, R, st);     // w = A z
+        for (int i = 0; i <= j; ++i) {                                         // modified Gram-Schmidt
+          const double2* vi = V.p + static_cast<size_t>(i) * nr;
+          dot(vi, W.p, hcol.p + static_cast<size_t>(i) * R);
+          launch_axpy_cols(W.p, vi, hcol.p + static_cast<size_t>(i) * R, 1, n, R, st);
+        }
+        dot(W.p, W.p, hcol.p + static_cast<size_t>(j + 1) * R);
+        HS_CUDA(cudaMemcpyAsync(hh.data(), hcol.p, sizeof(double2) * (j + 2) * R, cudaMemcpyDeviceToHost, st));
+        HS_CUDA(cudaStreamSynchronize(st));
+        for (int r = 0; r < R; ++r) {
+          invh[r] = 0.0;
+          if (!active[r]) continue;
+          std::vector<Complex> h(j + 2);
+          for (int i = 0; i <= j; ++i) h[i] = Complex(hh[static_cast<size_t>(i) * R + r].x, hh[static_cast<size_t>(i) * R + r].y);
+          const double wnorm = std::sqrt(hh[static_cast<size_t>(j + 1) * R + r].x);
+          h[j + 1] = wnorm;
+          for (int i = 0; i < j; ++i) {
+            const Complex t = cs[r][i] * h[i] + sn[r][i] * h[i + 1];
+            h[i + 1] = -std::conj(sn[r][i]) * h[i] + std::conj(cs[r][i]) * h[i + 1];
+            h[i] = t;
+          }
+          {
+            const Complex a = h[j], bb = h[j + 1];
+            const double rr = std::sqrt(std::norm(a) + std::norm(bb));
+            if (rr == 0.0) {
+              cs[r][j] = 1.0;
+              sn[r][j] = 0.0;
+            } else {
+              cs[r][j] = std::conj(a) / rr;
+              sn[r][j] = std::conj(bb) / rr;
+            }
+            h[j] = cs[r][j] * a + sn[r][j] * bb;
+            h[j + 1] = 0.0;
+          }
+          hess[r].push_back(h);
+          g[r][j + 1] = -std::conj(sn[r][j]) * g[r][j];
+          g[r][j] = cs[r][j] * g[r][j];
+          const double rel = std::abs(g[r][j + 1]) / bnorm[r];
+          hist[r].push_back(rel);
+          if (wnorm <= 1e-14 * bnorm[r]) {
+            breakdown[r] = 1;
+            active[r] = 0;
+            iters[r] = j + 1;
+            continue;
+          }
+          invh[r] = 1.0 / wnorm;
+          if (rel <= tol) {
+            active[r] = 0;
+            iters[r] = j + 1;
+          }
+        }
+        for (int r = 0; r < R; ++r)
+          if (!active[r] && iters[r] != j + 1) invh[r] = 0.0;  // frozen columns stay zero
+        double2* vn = V.p + static_cast<size_t>(j + 1) * nr;
+        HS_CUDA(cudaMemcpyAsync(vn, W.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+        HS_CUDA(cudaMemcpyAsync(inv.p, invh.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
+        launch_scale_cols(vn, inv.p, n, R, st);
+        ++j;
+      }
+      for (int r = 0; r < R; ++r)
+        if (active[r]) iters[r] = j;
+      // y by back substitution, then x = M^-1 (V y)
+      std::vector<std::vector<Complex>> y(R);
+      int jmax = 0;
+      for (int r = 0; r < R; ++r) {
+        const int jr = iters[r];
+        jmax = std::max(jmax, jr);
+        y[r].assign(jr, Complex(0.0));
+        for (int i = jr - 1; i >= 0; --i) {
+          Complex sacc = g[r][i];
+          for (int k2 = i + 1; k2 < jr; ++k2) sacc -= hess[r][k2][i] * y[r][k2];
+          y[r][i] = sacc / hess[r][i][i];
+        }
+      }
+      HS_CUDA(cudaMemsetAsync(H.bN.p, 0, sizeof(double2) * nr, st));
+      std::vector<double2> alpha(R);
+      for (int k2 = 0; k2 < jmax; ++k2) {
+        for (int r = 0; r < R; ++r)
+          alpha[r] = k2 < iters[r] ? make_double2(y[r][k2].real(), y[r][k2].imag()) : make_double2(0.0, 0.0);
+        HS_CUDA(cudaMemcpyAsync(hcol.p, alpha.data(), sizeof(double2) * R, cudaMemcpyHostToDevice, st));
+        launch_axpy_cols(H.bN.p, V.p + static_cast<size_t>(k2) * nr, hcol.p, 0, n, R, st);
+      }
+      H.run(rounds, false, false);
+      HS_CUDA(cudaMemcpyAsync(X.p, H.u.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+      // true residual ||b - A x|| / ||b||
+      const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st);
+      DBuf<double> tn;
+      tn.alloc(R);
+      launch_reduce_partials(H.pnum.p, nb2, R, tn.p, st);
+      std::vector<double> tnh(R);
+      HS_CUDA(cudaMemcpyAsync(tnh.data(), tn.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
+      launch_transpose_out(X.p, io.p, n, R, st);
+      HS_CUDA(cudaMemcpyAsync(x + 2 * b0 * n, io.p, sizeof(double2) * nr, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      if (reports)
+        for (int r = 0; r < R; ++r) {
+          hs_gmres_report& rep = reports[b0 + r];
+          std::memset(&rep, 0, sizeof(rep));
+          rep.iterations = iters[r];
+          const double fin = iters[r] > 0 ? std::abs(g[r][iters[r]]) / bnorm[r] : 1.0;
+          rep.final_residual = bnorm[r] == 0.0 ? 0.0 : fin;
+          rep.converged = bnorm[r] == 0.0 || breakdown[r] || fin <= tol;
+          rep.true_residual = bnorm[r] == 0.0 ? 0.0 : std::sqrt(tnh[r]) / bnorm[r];
+          rep.n_history = static_cast<int>(hist[r].size());
+          for (int q = 0; q < rep.n_history; ++q) rep.history[q] = hist[r][q];
+        }
+    }
+  });
+}
+
+extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, int64_t* subdomain_solves,
+                              double* alg_bytes, double* alg_flops) {
+  return guarded([&] {
+    if (!s) config_error("profile: null handle");
+    DdmHandle& H = s->h;
+    if (H.nsweeps == 0) config_error("profile: no solve has run");
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+    const int nsub = H.geom.nsub;
+    std::vector<unsigned> nz(static_cast<size_t>(H.nsweeps) * nsub);
+    HS_CUDA(cudaMemcpy(nz.data(), H.nzmask.p, nz.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    double sec = 0.0, bytes = 0.0, flops = 0.0;
+    int64_t launches = 0, solves = 0;
+    float ms = 0.f;
+    for (int l = 1; l <= H.nsweeps; ++l)
+      for (int st = 0; st < H.steps; ++st) {
+        const int q = (l - 1) * H.steps + st;
+        HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * q], H.ev[2 + H.nsweeps + 2 * q]));
+        sec += ms * 1e-3;
+        launches += 2;
+        for (int id : H.groups[((l - 1) % H.ndir) * H.steps + st]) {
+          if (nz[static_cast<size_t>(l - 1) * nsub + id] == 0) continue;
+          const SymbolicClass& c = *H.eng.classes[H.subs[id].cls]->sym;
+          ++solves;
+          bytes += 2.0 * c.packed_entries * 16 + 2.0 * H.R * c.n * 16;
+          flops += 16.0 * c.packed_entries * H.R;
+        }
+      }
+    if (solve_seconds) *solve_seconds = sec;
+    if (solve_launches) *solve_launches = launches;
+    if (subdomain_solves) *subdomain_solves = solves;
+    if (alg_bytes) *alg_bytes = bytes;
+    if (alg_flops) *alg_flops = flops;
+  });
+}
+
+extern "C" int hs_route_trace(int dim, int rounds, int gen_sweep, int axis, int sign) {
+  try {
+    const std::vector<Vec3i> plan = sweep_plan(dim, rounds);
+    if (gen_sweep < 1 || gen_sweep > static_cast<int>(plan.size()) || axis < 0 || axis >= dim) return -1;
+    return route_trace(plan, dim, gen_sweep, axis, sign);
+  } catch (...) {
+    return -1;
+  }
+}

@@ -1,0 +1,70 @@
+// Device-visible descriptors shared by the sm_100a kernels (hs_kernels.cu) and the
+// host orchestration (hs_ddm.cu). Plain PODs; complex128 is double2 (re, im).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hsb {
+
+constexpr int kMaxDirs = 6;  // 2*dim cardinal faces
+constexpr int kMaxRhs = 32;  // RHS per device batch (bitmask width)
+
+struct DevFront {
+  int k, m, sep_off, bnd_off;
+  int parent, child0, child1, cmap0, cmap1;
+  int orig_off, orig_cnt, pad_;
+  long long fac_off, v_off, f_off;
+};
+
+struct DevClass {
+  const DevFront* fronts;
+  const int* bnd_elim;
+  const int* child_map;
+  const int* orig_fpos;
+  const int* orig_eidx;
+  const int* elim_of_local;
+  const int* local_of_elim;
+  // trace line tables per direction d = 2*axis + (sign > 0), elimination positions
+  const int* ext_u0[kMaxDirs];   // outgoing trace: interface line
+  const int* ext_um1[kMaxDirs];  // outgoing trace: line one step toward the source
+  const int* inj_p0[kMaxDirs];   // incoming trace: interface line (-1 on shell)
+  const int* inj_pm[kMaxDirs];   // incoming trace: first source-side line (-1 on shell)
+  int line_len[kMaxDirs];
+  int n, nfronts;
+  int size[3];
+};
+
+struct DevSub {
+  int cls;
+  int sub[3];
+  int lo[3];                  // local grid range lo (global index coordinates)
+  double tol;                 // pivot tolerance 1e-14 * max|a_ij| (src/direct.cpp:191-193)
+  double2* factor;            // panels (hs_symbolic.hpp)
+  double2* dinv;              // 1/d, elimination order
+  const double2* val;         // CSR values (factorization input)
+  double2* x;                 // solve vector, elimination order, node-major x R
+  const double2* coef[kMaxDirs];  // injection couplings per incoming direction
+};
+
+// Global grid and partition geometry for split / accumulate kernels.
+struct DevGeom {
+  int dim;
+  int glo[3], gsize[3];       // global padded range
+  int counts[3];
+  int pad;
+  int cut_w[3];               // uniform cut width per axis (cuts[c] = c * w)
+  int nsub;
+  long long gn;               // global node count
+};
+
+struct SolveTask {
+  int sub, front, slot, pad_;
+};
+
+struct FactorTask {
+  int sub, front;
+  long long fbase;            // dense workspace base of this subdomain (elements)
+};
+
+}  // namespace hsb

@@ -1,0 +1,958 @@
+// sm_100a kernels of the helmsweep hot path. complex128 = double2 (re, im).
+//
+//   solve_kernel<RG, FWD>   multifrontal forward / backward triangular solves over every
+//                           front of a step group's subdomains, dataflow-scheduled in one
+//                           persistent launch per pass (src/direct.cpp:290-325)
+//   factor_level_kernel     assembly + extend-add + panel LDL^T of one tree height
+//                           (src/direct.cpp:55-87, 181-281)
+//   rhs/inject/nonzero      split source, trace injection, exact-zero test
+//                           (src/sweeper.cpp:189-251, src/transfer.cpp:68-89)
+//   extract_deposit         trace extraction, routing, mailbox accumulation
+//                           (src/transfer.cpp:13-66, src/sweeper.cpp:295-307)
+//   accumulate              weighted partition-of-unity gather (src/transfer.cpp:91-102)
+//   residual / spmv / dots  global operator and Krylov vector kernels
+#include "hs_kernels.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+
+#include "hs_common.hpp"
+
+namespace hsb {
+
+std::atomic<long long> g_kernel_launches{0};
+
+namespace {
+
+inline void after_launch() {
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  HS_CUDA(cudaGetLastError());
+}
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNB = 16;  // factorization panel width
+
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ void cfms(double2& acc, double2 a, double2 b) {
+  acc.x = fma(-a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(-a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+// 1/d (Smith's algorithm, avoids overflow in |d|^2)
+__device__ __forceinline__ double2 crecip(double2 d) {
+  if (fabs(d.x) >= fabs(d.y)) {
+    const double r = d.y / d.x, den = d.x + d.y * r;
+    return make_double2(1.0 / den, -r / den);
+  }
+  const double r = d.x / d.y, den = d.x * r + d.y;
+  return make_double2(r / den, -1.0 / den);
+}
+__device__ __forceinline__ void cacc(double2* p, double2 v) {
+  p->x += v.x;
+  p->y += v.y;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Reduce-scatter of 64 per-lane doubles over the 32 lanes of a warp by recursive
+// halving: afterwards lane l holds the warp-wide sums of entries 2l and 2l+1.
+__device__ __forceinline__ void reduce_scatter64(double (&v)[64], int lane) {
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int half = 32 >> s;
+    const int mask = 16 >> s;
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = upper ? v[i] : v[i + half];
+      const double keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(kFull, send, mask);
+    }
+  }
+}
+
+__host__ __device__ __forceinline__ long long panel_offset(int m, int J) {
+  // sum_{J' < J} (m - 32 J') * 32
+  return 32LL * (static_cast<long long>(J) * m - 16LL * J * (J - 1));
+}
+
+// ----------------------------------------------------------------------------
+// solve
+
+template <int RG>
+__device__ void fwd_task(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& f,
+                         int slot, int rg, double2* t, double2* dblk) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = a.R, r0 = rg * RG;
+  const int k = f.k, m = f.m;
+  double2* V = a.vbuf + slot * a.vslot_stride;
+  // t[0:k] = x[sep], t[k:m] = 0
+  for (int idx = tid; idx < m * RG; idx += kThreads) {
+    const int e = idx / RG, r = idx % RG;
+    double2 v = czero();
+    if (e < k && r0 + r < R) v = S.x[static_cast<long long>(f.sep_off + e) * R + r0 + r];
+    t[idx] = v;
+  }
+  __syncthreads();
+  // extend-add of the children's update vectors, child0 then child1
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+    const int ch = q ? f.child1 : f.child0;
+    if (ch < 0) continue;
+    const DevFront cf = C.fronts[ch];
+    const int cb = cf.m - cf.k;
+    const int* cmap = C.child_map + (q ? f.cmap1 : f.cmap0);
+    for (int idx = tid; idx < cb * RG; idx += kThreads) {
+      const int i = idx / RG, r = idx % RG;
+      if (r0 + r < R) cacc(&t[cmap[i] * RG + r], __ldcg(&V[(cf.v_off + i) * R + r0 + r]));
+    }
+    __syncthreads();
+  }
+  const double2* L = S.factor + f.fac_off;
+#pragma unroll 1
+  for (int j0 = 0; j0 < k; j0 += 32) {
+    const int w = min(32, k - j0);
+    const int rows = m - j0;
+    for (int idx = tid; idx < w * 32; idx += kThreads) {
+      const int i = idx >> 5, c = idx & 31;
+      dblk[i * 33 + c] = __ldg(&L[i * 32 + c]);
+    }
+    __syncthreads();
+    if (warp < RG) {  // unit-lower solve of the diagonal block, one warp per RHS
+      const int r = warp;
+      double2 ti = lane < w ? t[(j0 + lane) * RG + r] : czero();
+#pragma unroll 1
+      for (int j = 0; j < w - 1; ++j) {
+        double2 tj;
+        tj.x = __shfl_sync(kFull, ti.x, j);
+        tj.y = __shfl_sync(kFull, ti.y, j);
+        if (lane > j && lane < w) cfms(ti, dblk[lane * 33 + j], tj);
+      }
+      if (lane < w) t[(j0 + lane) * RG + r] = ti;
+    }
+    __syncthreads();
+    const int nrem = m - (j0 + w);
+    if (nrem > 0) {
+      constexpr int RB = 32 / RG;
+      double2 tj[RG];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) tj[r] = lane < w ? t[(j0 + lane) * RG + r] : czero();
+      const int nb = (nrem + RB - 1) / RB;
+#pragma unroll 1
+      for (int b = warp; b < nb; b += kWarps) {
+        const int i0 = j0 + w + b * RB;
+        double2 Lv[RB];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) {
+          const int i = i0 + rr;
+          Lv[rr] = (i < m && lane < w) ? __ldg(&L[static_cast<long long>(i - j0) * 32 + lane]) : czero();
+        }
+        double v[64];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr)
+#pragma unroll
+          for (int r = 0; r < RG; ++r) {
+            const double2 p = cmul(Lv[rr], tj[r]);
+            v[(rr * RG + r) * 2] = p.x;
+            v[(rr * RG + r) * 2 + 1] = p.y;
+          }
+        reduce_scatter64(v, lane);
+        const int rr = lane / RG, r = lane % RG, i = i0 + rr;
+        if (i < m) {
+          double2& tt = t[i * RG + r];
+          tt.x -= v[0];
+          tt.y -= v[1];
+        }
+      }
+    }
+    __syncthreads();
+    L += static_cast<long long>(rows) * 32;
+  }
+  // x[sep] = D^-1 t[0:k] (the diagonal scaling of src/direct.cpp:309 fused), V = t[k:m]
+  for (int idx = tid; idx < m * RG; idx += kThreads) {
+    const int e = idx / RG, r = idx % RG;
+    if (r0 + r >= R) continue;
+    if (e < k) {
+      const long long pos = f.sep_off + e;
+      S.x[pos * R + r0 + r] = cmul(t[idx], S.dinv[pos]);
+    } else {
+      __stcg(&V[(f.v_off + e - k) * R + r0 + r], t[idx]);
+    }
+  }
+}
+
+template <int RG>
+__device__ void bwd_task(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& f,
+                         int rg, double2* t, double2* dblk, double2* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = a.R, r0 = rg * RG;
+  const int k = f.k, m = f.m;
+  for (int idx = tid; idx < m * RG; idx += kThreads) {
+    const int e = idx / RG, r = idx % RG;
+    double2 v = czero();
+    if (r0 + r < R) {
+      const long long pos = e < k ? f.sep_off + e : C.bnd_elim[f.bnd_off + e - k];
+      v = __ldcg(&S.x[pos * R + r0 + r]);
+    }
+    t[idx] = v;
+  }
+  __syncthreads();
+  const int np = (k + 31) / 32;
+#pragma unroll 1
+  for (int J = np - 1; J >= 0; --J) {
+    const int j0 = 32 * J, w = min(32, k - j0);
+    const double2* P = S.factor + f.fac_off + panel_offset(m, J);
+    for (int idx = tid; idx < w * 32; idx += kThreads) {
+      const int i = idx >> 5, c = idx & 31;
+      dblk[i * 33 + c] = __ldg(&P[i * 32 + c]);
+    }
+    // t[J] -= L[j0+w:m, J]^T t[j0+w:m]
+    double2 acc[RG];
+#pragma unroll
+    for (int r = 0; r < RG; ++r) acc[r] = czero();
+    int i = j0 + w + warp;
+#pragma unroll 1
+    for (; i + 3 * kWarps < m; i += 4 * kWarps) {
+      double2 Lv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        Lv[u] = lane < w ? __ldg(&P[static_cast<long long>(i + u * kWarps - j0) * 32 + lane]) : czero();
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int r = 0; r < RG; ++r) cfma(acc[r], Lv[u], t[(i + u * kWarps) * RG + r]);
+    }
+#pragma unroll 1
+    for (; i < m; i += kWarps) {
+      const double2 Lv = lane < w ? __ldg(&P[static_cast<long long>(i - j0) * 32 + lane]) : czero();
+#pragma unroll
+      for (int r = 0; r < RG; ++r) cfma(acc[r], Lv, t[i * RG + r]);
+    }
+#pragma unroll
+    for (int r = 0; r < RG; ++r) red[(warp * 32 + lane) * RG + r] = acc[r];
+    __syncthreads();
+    for (int idx = tid; idx < 32 * RG; idx += kThreads) {
+      const int j = idx / RG, r = idx % RG;
+      if (j < w) {
+        double2 s = czero();
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) s = cadd(s, red[(q * 32 + j) * RG + r]);
+        double2& tt = t[(j0 + j) * RG + r];
+        tt = csub(tt, s);
+      }
+    }
+    __syncthreads();
+    if (warp < RG) {  // unit-upper (L^T) solve of the diagonal block
+      const int r = warp;
+      double2 ti = lane < w ? t[(j0 + lane) * RG + r] : czero();
+#pragma unroll 1
+      for (int j = w - 1; j >= 1; --j) {
+        double2 tj;
+        tj.x = __shfl_sync(kFull, ti.x, j);
+        tj.y = __shfl_sync(kFull, ti.y, j);
+        if (lane < j) cfms(ti, dblk[j * 33 + lane], tj);
+      }
+      if (lane < w) t[(j0 + lane) * RG + r] = ti;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < k * RG; idx += kThreads) {
+    const int e = idx / RG, r = idx % RG;
+    if (r0 + r < R) __stcg(&S.x[static_cast<long long>(f.sep_off + e) * R + r0 + r], t[idx]);
+  }
+}
+
+template <int RG, bool FWD>
+__global__ void __launch_bounds__(kThreads, 2) solve_kernel(SolveArgs a, int tcap) {
+  extern __shared__ double2 sm[];
+  __shared__ int s_task;
+  double2* t = sm;
+  double2* dblk = t + tcap * RG;
+  double2* red = dblk + 32 * 33;
+  const unsigned epoch = *a.epoch_base + a.epoch_off;
+  const int total = a.ntasks * a.n_rg;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = static_cast<int>(atomicAdd(a.queue, 1u));
+    __syncthreads();
+    const int tk = s_task;
+    __syncthreads();
+    if (tk >= total) break;
+    const SolveTask task = a.tasks[tk / a.n_rg];
+    const int rg = tk % a.n_rg;
+    if (a.nzmask[task.sub] == 0) continue;  // skipped subdomain: no task waits on it
+    const DevSub& S = a.subs[task.sub];
+    const DevClass& C = a.cls[S.cls];
+    const DevFront f = C.fronts[task.front];
+    unsigned* fl = a.flags + static_cast<long long>(task.sub) * a.nf_max * a.n_rg + rg;
+    if (threadIdx.x == 0) {
+      if (FWD) {
+        if (f.child0 >= 0)
+          while (ld_acquire(fl + static_cast<long long>(f.child0) * a.n_rg) != epoch) __nanosleep(20);
+        if (f.child1 >= 0)
+          while (ld_acquire(fl + static_cast<long long>(f.child1) * a.n_rg) != epoch) __nanosleep(20);
+      } else if (f.parent >= 0) {
+        while (ld_acquire(fl + static_cast<long long>(f.parent) * a.n_rg) != epoch) __nanosleep(20);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (FWD)
+      fwd_task<RG>(a, C, S, f, task.slot, rg, t, dblk);
+    else
+      bwd_task<RG>(a, C, S, f, rg, t, dblk, red);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(fl + static_cast<long long>(task.front) * a.n_rg, epoch);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// factorization
+
+__global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, int use_smem,
+                                                              long long scratch_stride) {
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const FactorTask task = a.tasks[blockIdx.x];
+  const DevSub& S = a.subs[task.sub];
+  const DevClass& C = a.cls[S.cls];
+  const DevFront f = C.fronts[task.front];
+  const int m = f.m, k = f.k;
+  double2* F = a.work + task.fbase + f.f_off;
+  const long long mm = static_cast<long long>(m) * m;
+  for (long long idx = tid; idx < mm; idx += kThreads) F[idx] = czero();
+  __syncthreads();
+  // original entries of the separator rows, lower triangle (src/direct.cpp:219-237)
+  for (int q = tid; q < f.orig_cnt; q += kThreads)
+    cacc(&F[C.orig_fpos[f.orig_off + q]], S.val[C.orig_eidx[f.orig_off + q]]);
+  __syncthreads();
+  // extend-add of the children's Schur complements (src/direct.cpp:239-265)
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+    const int ch = q ? f.child1 : f.child0;
+    if (ch < 0) continue;
+    const DevFront cf = C.fronts[ch];
+    const double2* Fc = a.work + task.fbase + cf.f_off;
+    const int cb = cf.m - cf.k;
+    const int* cmap = C.child_map + (q ? f.cmap1 : f.cmap0);
+    for (int idx = tid; idx < cb * cb; idx += kThreads) {
+      const int i = idx % cb, j = idx / cb;
+      if (i >= j)
+        cacc(&F[static_cast<long long>(cmap[j]) * m + cmap[i]],
+             Fc[static_cast<long long>(cf.k + j) * cf.m + cf.k + i]);
+    }
+    __syncthreads();
+  }
+  double2* Ps = use_smem ? sm : a.scratch + blockIdx.x * scratch_stride;
+  double2* Ws = Ps + static_cast<long long>(m) * kNB;
+#pragma unroll 1
+  for (int p0 = 0; p0 < k; p0 += kNB) {
+    const int p1 = min(p0 + kNB, k), nbw = p1 - p0, rows = m - p0, rows2 = m - p1;
+    for (int idx = tid; idx < nbw * rows; idx += kThreads) {
+      const int c = idx / rows, i = idx % rows;
+      Ps[idx] = F[static_cast<long long>(p0 + c) * m + p0 + i];
+    }
+    __syncthreads();
+    // unblocked right-looking LDL^T of the panel, full column height (src/direct.cpp:62-74)
+#pragma unroll 1
+    for (int jj = 0; jj < nbw; ++jj) {
+      const double2 d = Ps[jj * rows + jj];
+      if (tid == 0 && hypot(d.x, d.y) < S.tol)
+        atomicMin(a.err_key, (static_cast<unsigned long long>(task.sub) << 32) |
+                                 static_cast<unsigned>(f.sep_off + p0 + jj));
+      const double2 inv = crecip(d);
+      for (int i = jj + 1 + tid; i < rows; i += kThreads) Ps[jj * rows + i] = cmul(Ps[jj * rows + i], inv);
+      __syncthreads();
+      const int ncols = nbw - jj - 1;
+      for (int idx = tid; idx < ncols * rows; idx += kThreads) {
+        const int c = jj + 1 + idx / rows, i = idx % rows;
+        if (i >= c) {
+          const double2 s = cmul(d, Ps[jj * rows + c]);
+          cfms(Ps[c * rows + i], Ps[jj * rows + i], s);
+        }
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < nbw * rows2; idx += kThreads) {
+      const int c = idx / rows2, i = idx % rows2;
+      Ws[idx] = cmul(Ps[c * rows + (p1 - p0) + i], Ps[c * rows + c]);
+    }
+    for (int idx = tid; idx < nbw * rows; idx += kThreads) {
+      const int c = idx / rows, i = idx % rows;
+      F[static_cast<long long>(p0 + c) * m + p0 + i] = Ps[idx];
+    }
+    __syncthreads();
+    // trailing lower update F[p1:, p1:] -= L W^T in 64x64 tiles, 4x4 per thread
+    if (rows2 > 0) {
+      const int nt = (rows2 + 63) / 64;
+      const int ty = tid / 16, tx = tid % 16;
+#pragma unroll 1
+      for (int tp = 0; tp < nt * (nt + 1) / 2; ++tp) {
+        int ti = 0;
+        while ((ti + 1) * (ti + 2) / 2 <= tp) ++ti;
+        const int tc = tp - ti * (ti + 1) / 2;
+        double2 acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = czero();
+        int ir[4], ic[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ir[u] = ti * 64 + ty + 16 * u;  // offset from p1
+          ic[u] = tc * 64 + tx + 16 * u;
+        }
+#pragma unroll 1
+        for (int cc = 0; cc < nbw; ++cc) {
+          double2 lr[4], wc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            lr[u] = ir[u] < rows2 ? Ps[cc * rows + (p1 - p0) + ir[u]] : czero();
+            wc[u] = ic[u] < rows2 ? Ws[cc * rows2 + ic[u]] : czero();
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) cfma(acc[u][v], lr[u], wc[v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            if (ir[u] < rows2 && ic[v] < rows2 && ir[u] >= ic[v]) {
+              double2& y = F[static_cast<long long>(p1 + ic[v]) * m + p1 + ir[u]];
+              y = csub(y, acc[u][v]);
+            }
+      }
+    }
+    __syncthreads();
+  }
+  // outputs: D^-1 and the 32-column solve panels (strict lower part)
+  for (int j = tid; j < k; j += kThreads) S.dinv[f.sep_off + j] = crecip(F[static_cast<long long>(j) * m + j]);
+  double2* out = S.factor + f.fac_off;
+  for (int J = 0; 32 * J < k; ++J) {
+    const int j0 = 32 * J, rowsJ = m - j0;
+    double2* P = out + panel_offset(m, J);
+    for (int idx = tid; idx < rowsJ * 32; idx += kThreads) {
+      const int row = j0 + idx / 32, col = j0 + idx % 32;
+      P[idx] = (col < k && row > col) ? F[static_cast<long long>(col) * m + row] : czero();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// sweep kernels
+
+__device__ __forceinline__ int weight2(const DevGeom& g, int axis, int cell, int index) {
+  const int w = g.cut_w[axis];
+  const int lo = cell * w, hi = (cell + 1) * w;
+  const int lo_ext = cell == 0 ? lo - g.pad : lo;
+  const int hi_ext = cell == g.counts[axis] - 1 ? hi + g.pad : hi;
+  if (index < lo_ext || index > hi_ext) return 0;
+  if (index == lo && cell > 0) return 1;
+  if (index == hi && cell < g.counts[axis] - 1) return 1;
+  return 2;
+}
+
+__global__ void rhs_init_kernel(SweepArgs a) {
+  const int sub = a.group[blockIdx.y];
+  const DevSub& S = a.subs[sub];
+  const DevClass& C = a.cls[S.cls];
+  const long long total = static_cast<long long>(C.n) * a.R;
+  const int dim = a.g.dim;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double2 v = czero();
+    if (a.l == 1) {  // split source: w(sub, p) * b[p] off the local shell (src/sweeper.cpp:189-202)
+      const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
+      int local = C.local_of_elim[e];
+      int p[3] = {0, 0, 0};
+      bool shell = false;
+      long long gp = 0, gst = 1;
+      int num = 1;
+      for (int ax = 0; ax < dim; ++ax) {
+        const int li = local % C.size[ax];
+        local /= C.size[ax];
+        p[ax] = S.lo[ax] + li;
+        shell |= (li == 0) || (li == C.size[ax] - 1);
+        num *= weight2(a.g, ax, S.sub[ax], p[ax]);
+        gp += static_cast<long long>(p[ax] - a.g.glo[ax]) * gst;
+        gst *= a.g.gsize[ax];
+      }
+      if (num != 0 && !shell) {
+        const double w = num / static_cast<double>(1 << dim);
+        const double2 bv = a.b[gp * a.R + r];
+        v = make_double2(w * bv.x, w * bv.y);
+      }
+    }
+    S.x[idx] = v;
+  }
+}
+
+__global__ void inject_kernel(SweepArgs a) {
+  const int sub = a.group[blockIdx.x];
+  const DevSub& S = a.subs[sub];
+  const DevClass& C = a.cls[S.cls];
+  const int R = a.R;
+#pragma unroll 1
+  for (int d = 0; d < a.dirs; ++d) {  // canonical (axis, sign) order of src/sweeper.cpp:233-239
+    const long long slot = (static_cast<long long>(sub) * a.nsweeps + (a.l - 1)) * a.dirs + d;
+    const unsigned pres = a.mpres[slot];
+    if (pres == 0) continue;
+    const int len = C.line_len[d];
+    const double2* u0 = a.mbox + slot * a.mbox_dir_stride;
+    const double2* um1 = u0 + static_cast<long long>(len) * R;
+    for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
+      const int i = idx / R, r = idx % R;
+      if (!((pres >> r) & 1u)) continue;
+      const double2 c = S.coef[d][i];
+      const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+      if (p0 >= 0) {
+        double2& y = S.x[static_cast<long long>(p0) * R + r];
+        cfms(y, c, um1[idx]);
+      }
+      if (pm >= 0) {
+        double2& y = S.x[static_cast<long long>(pm) * R + r];
+        cfma(y, c, u0[idx]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void nonzero_kernel(SweepArgs a) {
+  const int sub = a.group[blockIdx.y];
+  const DevSub& S = a.subs[sub];
+  const DevClass& C = a.cls[S.cls];
+  const long long total = static_cast<long long>(C.n) * a.R;
+  unsigned bits = 0;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 v = S.x[idx];
+    if (v.x != 0.0 || v.y != 0.0) bits |= 1u << (idx % a.R);
+  }
+  bits = __reduce_or_sync(kFull, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(a.l - 1) * a.g.nsub + sub], bits);
+}
+
+__global__ void extract_deposit_kernel(SweepArgs a) {
+  const int sub = a.group[blockIdx.x];
+  const int d = blockIdx.y;
+  const int axis = d >> 1, sign = (d & 1) ? 1 : -1;
+  const DevSub& S = a.subs[sub];
+  const int t = S.sub[axis] + sign;
+  if (t < 0 || t >= a.g.counts[axis]) return;
+  const int lp = a.route[(a.l - 1) * a.dirs + d];
+  if (lp == 0) return;
+  const unsigned nz = a.nzmask[static_cast<long long>(a.l - 1) * a.g.nsub + sub];
+  if (nz == 0) return;
+  int stride = 1;
+  for (int ax = 0; ax < axis; ++ax) stride *= a.g.counts[ax];
+  const int target = sub + sign * stride;
+  const DevClass& C = a.cls[S.cls];
+  const int R = a.R, len = C.line_len[d];
+  const long long slot = (static_cast<long long>(target) * a.nsweeps + (lp - 1)) * a.dirs + d;
+  const unsigned pres = a.mpres[slot];
+  double2* u0 = a.mbox + slot * a.mbox_dir_stride;
+  double2* um1 = u0 + static_cast<long long>(len) * R;
+  for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
+    const int i = idx / R, r = idx % R;
+    if (!((nz >> r) & 1u)) continue;
+    const double2 v0 = S.x[static_cast<long long>(C.ext_u0[d][i]) * R + r];
+    const double2 v1 = S.x[static_cast<long long>(C.ext_um1[d][i]) * R + r];
+    if ((pres >> r) & 1u) {  // TraceMailbox::deposit accumulates (src/transfer.cpp:30-35)
+      u0[idx] = cadd(u0[idx], v0);
+      um1[idx] = cadd(um1[idx], v1);
+    } else {
+      u0[idx] = v0;
+      um1[idx] = v1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) a.mpres[slot] = pres | nz;
+}
+
+__global__ void accumulate_kernel(AccumArgs a) {
+  __shared__ double red[kThreads];
+  const int dim = a.g.dim, R = a.R;
+  const int npb = kThreads / R;  // whole nodes per block so thread t always owns column t % R
+  const long long node = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const int r = threadIdx.x % R;
+  const long long idx = node * R + r;
+  double nrm = 0.0;
+  if (threadIdx.x < npb * R && node < a.g.gn) {
+    int p[3] = {0, 0, 0};
+    long long rem = node;
+    for (int ax = 0; ax < dim; ++ax) {
+      p[ax] = a.g.glo[ax] + static_cast<int>(rem % a.g.gsize[ax]);
+      rem /= a.g.gsize[ax];
+    }
+    // candidate cells per axis (at most two have nonzero weight)
+    int cand[3][2], cw[3][2], nc[3];
+    for (int ax = 0; ax < 3; ++ax) nc[ax] = 1, cand[ax][0] = 0, cw[ax][0] = 2;
+    for (int ax = 0; ax < dim; ++ax) {
+      const int w = a.g.cut_w[ax];
+      int q = p[ax] >= 0 ? p[ax] / w : -1;
+      q = min(max(q, 0), a.g.counts[ax] - 1);
+      nc[ax] = 0;
+      for (int c = q - 1; c <= q; ++c) {
+        if (c < 0) continue;
+        const int w2 = weight2(a.g, ax, c, p[ax]);
+        if (w2) {
+          cand[ax][nc[ax]] = c;
+          cw[ax][nc[ax]] = w2;
+          ++nc[ax];
+        }
+      }
+    }
+    int subs[8], steps[8];
+    double wts[8];
+    int ns = 0;
+    for (int i2 = 0; i2 < nc[2]; ++i2)
+      for (int i1 = 0; i1 < nc[1]; ++i1)
+        for (int i0 = 0; i0 < nc[0]; ++i0) {
+          const int c3[3] = {cand[0][i0], cand[1][i1], dim == 3 ? cand[2][i2] : 0};
+          int num = cw[0][i0] * cw[1][i1] * (dim == 3 ? cw[2][i2] : 1);
+          int id = 0, st = 1;
+          for (int ax = dim - 1; ax >= 0; --ax) id = id * a.g.counts[ax] + c3[ax];
+          for (int ax = 0; ax < dim; ++ax) st += a.dvec[ax] == 1 ? c3[ax] : a.g.counts[ax] - 1 - c3[ax];
+          subs[ns] = id;
+          steps[ns] = st;
+          wts[ns] = num / static_cast<double>(1 << dim);
+          ++ns;
+        }
+    // reference accumulation order: step, then ascending id within the step group
+    for (int i = 1; i < ns; ++i)
+      for (int j = i; j > 0 && (steps[j] < steps[j - 1] || (steps[j] == steps[j - 1] && subs[j] < subs[j - 1])); --j) {
+        int ts = subs[j]; subs[j] = subs[j - 1]; subs[j - 1] = ts;
+        ts = steps[j]; steps[j] = steps[j - 1]; steps[j - 1] = ts;
+        const double tw = wts[j]; wts[j] = wts[j - 1]; wts[j - 1] = tw;
+      }
+    double2 acc = czero();
+    for (int i = 0; i < ns; ++i) {
+      const int sb = subs[i];
+      if (!((a.nzmask[sb] >> r) & 1u)) continue;
+      const DevSub& S = a.subs[sb];
+      const DevClass& C = a.cls[S.cls];
+      long long local = 0, ls = 1;
+      for (int ax = 0; ax < dim; ++ax) {
+        local += static_cast<long long>(p[ax] - S.lo[ax]) * ls;
+        ls *= C.size[ax];
+      }
+      const double2 xv = S.x[static_cast<long long>(C.elim_of_local[local]) * R + r];
+      acc.x += wts[i] * xv.x;
+      acc.y += wts[i] * xv.y;
+    }
+    double2& u = a.u[idx];
+    u = cadd(u, acc);
+    nrm = acc.x * acc.x + acc.y * acc.y;
+  }
+  red[threadIdx.x] = nrm;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s = 0.0;
+    for (int q = threadIdx.x; q < kThreads; q += R) s += red[q];
+    a.partial[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s;
+  }
+}
+
+__global__ void reduce_partials_kernel(const double* partial, int nblocks, int R, double* out) {
+  __shared__ double red[kThreads];
+  const int Q = kThreads / R;
+  const int r = threadIdx.x % R, q = threadIdx.x / R;
+  double s = 0.0;
+  if (q < Q)
+    for (int b = q; b < nblocks; b += Q) s += partial[static_cast<long long>(b) * R + r];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double t = 0.0;
+    for (int qq = 0; qq < Q; ++qq) t += red[qq * R + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+}
+
+__global__ void reduce_cpartials_kernel(const double2* partial, int nblocks, int R, double2* out) {
+  __shared__ double2 red[kThreads];
+  const int Q = kThreads / R;
+  const int r = threadIdx.x % R, q = threadIdx.x / R;
+  double2 s = czero();
+  if (q < Q)
+    for (int b = q; b < nblocks; b += Q) s = cadd(s, partial[static_cast<long long>(b) * R + r]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double2 t = czero();
+    for (int qq = 0; qq < Q; ++qq) t = cadd(t, red[qq * R + threadIdx.x]);
+    out[threadIdx.x] = t;
+  }
+}
+
+__global__ void residual_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
+                                const double2* x, const double2* b, int R, double* pnum, double* pden) {
+  __shared__ double rn[kThreads], rd[kThreads];
+  const int npb = kThreads / R;
+  const long long row = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const int r = threadIdx.x % R;
+  const long long idx = row * R + r;
+  double num = 0.0, den = 0.0;
+  if (threadIdx.x < npb * R && row < n) {
+    double2 s = czero();
+    for (long long e = row_ptr[row]; e < row_ptr[row + 1]; ++e)
+      cfma(s, val[e], x[static_cast<long long>(col[e]) * R + r]);
+    const double2 bv = b[idx];
+    const double2 dv = csub(bv, s);
+    num = dv.x * dv.x + dv.y * dv.y;
+    den = bv.x * bv.x + bv.y * bv.y;
+  }
+  rn[threadIdx.x] = num;
+  rd[threadIdx.x] = den;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int q = threadIdx.x; q < kThreads; q += R) {
+      s1 += rn[q];
+      s2 += rd[q];
+    }
+    pnum[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s1;
+    pden[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s2;
+  }
+}
+
+__global__ void spmv_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
+                            const double2* x, double2* y, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const long long row = idx / R;
+  const int r = static_cast<int>(idx % R);
+  double2 s = czero();
+  for (long long e = row_ptr[row]; e < row_ptr[row + 1]; ++e) cfma(s, val[e], x[static_cast<long long>(col[e]) * R + r]);
+  y[idx] = s;
+}
+
+__global__ void dot_partials_kernel(const double2* a, const double2* b, long long n, int R, double2* partial) {
+  __shared__ double2 red[kThreads];
+  const int npb = kThreads / R;
+  const long long node = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const long long idx = node * R + threadIdx.x % R;
+  double2 s = czero();
+  if (threadIdx.x < npb * R && node < n) {  // conj(a) * b (src/krylov.cpp:9-13)
+    const double2 x = a[idx], y = b[idx];
+    s = make_double2(x.x * y.x + x.y * y.y, x.x * y.y - x.y * y.x);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double2 t = czero();
+    for (int q = threadIdx.x; q < kThreads; q += R) t = cadd(t, red[q]);
+    partial[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = t;
+  }
+}
+
+__global__ void axpy_cols_kernel(double2* y, const double2* x, const double2* alpha, int neg, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  double2 al = alpha[idx % R];
+  if (neg) al = make_double2(-al.x, -al.y);
+  cfma(y[idx], al, x[idx]);
+}
+
+__global__ void scale_cols_kernel(double2* y, const double* inv, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const double s = inv[idx % R];
+  y[idx] = make_double2(y[idx].x * s, y[idx].y * s);
+}
+
+__global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const long long node = idx / R;
+  const int r = static_cast<int>(idx % R);
+  dst[idx] = src[static_cast<long long>(r) * n + node];
+}
+
+__global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R) {
+  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  const int r = static_cast<int>(idx / n);
+  const long long node = idx % n;
+  dst[idx] = src[node * R + r];
+}
+
+__global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
+
+int blocks_for(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
+
+template <int RG, bool FWD>
+void launch_solve_t(const SolveArgs& a, int grid, size_t smem, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    HS_CUDA(cudaFuncSetAttribute(solve_kernel<RG, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  const int tcap = static_cast<int>((smem - (32 * 33 + kWarps * 32 * RG) * sizeof(double2)) / (RG * sizeof(double2)));
+  solve_kernel<RG, FWD><<<grid, kThreads, smem, s>>>(a, tcap);
+  after_launch();
+}
+
+}  // namespace
+
+size_t solve_smem_bytes(int max_m, int rg) {
+  return (static_cast<size_t>(max_m) * rg + 32 * 33 + kWarps * 32 * rg) * sizeof(double2);
+}
+
+int solve_grid(int rg, size_t smem) {
+  int dev = 0, sms = 0, per = 1;
+  HS_CUDA(cudaGetDevice(&dev));
+  HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  switch (rg) {
+    case 1: HS_CUDA(cudaFuncSetAttribute(solve_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<1, true>, kThreads, smem)); break;
+    case 2: HS_CUDA(cudaFuncSetAttribute(solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<2, true>, kThreads, smem)); break;
+    case 4: HS_CUDA(cudaFuncSetAttribute(solve_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<4, true>, kThreads, smem)); break;
+    default: HS_CUDA(cudaFuncSetAttribute(solve_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+             HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<8, true>, kThreads, smem)); break;
+  }
+  return sms * (per > 0 ? per : 1);
+}
+
+void launch_solve_forward(const SolveArgs& a, int rg, int grid, size_t smem, cudaStream_t s) {
+  switch (rg) {
+    case 1: launch_solve_t<1, true>(a, grid, smem, s); break;
+    case 2: launch_solve_t<2, true>(a, grid, smem, s); break;
+    case 4: launch_solve_t<4, true>(a, grid, smem, s); break;
+    default: launch_solve_t<8, true>(a, grid, smem, s); break;
+  }
+}
+
+void launch_solve_backward(const SolveArgs& a, int rg, int grid, size_t smem, cudaStream_t s) {
+  switch (rg) {
+    case 1: launch_solve_t<1, false>(a, grid, smem, s); break;
+    case 2: launch_solve_t<2, false>(a, grid, smem, s); break;
+    case 4: launch_solve_t<4, false>(a, grid, smem, s); break;
+    default: launch_solve_t<8, false>(a, grid, smem, s); break;
+  }
+}
+
+size_t factor_smem_bytes(int max_m) { return static_cast<size_t>(2) * max_m * kNB * sizeof(double2); }
+
+void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    HS_CUDA(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    configured = true;
+  }
+  const size_t need = factor_smem_bytes(max_m);
+  const bool use_smem = need <= 200 * 1024;
+  factor_level_kernel<<<a.ntasks, kThreads, use_smem ? need : 0, s>>>(
+      a, use_smem ? 1 : 0, static_cast<long long>(2) * max_m * kNB);
+  after_launch();
+}
+
+void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s) {
+  const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 64));
+  rhs_init_kernel<<<dim3(bx, a.ngroup), kThreads, 0, s>>>(a);
+  after_launch();
+  inject_kernel<<<a.ngroup, kThreads, 0, s>>>(a);
+  after_launch();
+  nonzero_kernel<<<dim3(bx, a.ngroup), kThreads, 0, s>>>(a);
+  after_launch();
+}
+
+void launch_extract_deposit(const SweepArgs& a, int, cudaStream_t s) {
+  extract_deposit_kernel<<<dim3(a.ngroup, a.dirs), kThreads, 0, s>>>(a);
+  after_launch();
+}
+
+int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
+  const int nb = blocks_for(a.g.gn, kThreads / a.R);
+  accumulate_kernel<<<nb, kThreads, 0, s>>>(a);
+  after_launch();
+  return nb;
+}
+
+void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s) {
+  reduce_partials_kernel<<<1, kThreads, 0, s>>>(partial, nblocks, R, out);
+  after_launch();
+}
+
+void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2* out, cudaStream_t s) {
+  reduce_cpartials_kernel<<<1, kThreads, 0, s>>>(partial, nblocks, R, out);
+  after_launch();
+}
+
+int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, const double2* x,
+                    const double2* b, int R, double* pnum, double* pden, cudaStream_t s) {
+  const int nb = blocks_for(n, kThreads / R);
+  residual_kernel<<<nb, kThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden);
+  after_launch();
+  return nb;
+}
+
+void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, const double2* x,
+                 double2* y, int R, cudaStream_t s) {
+  spmv_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(n, row_ptr, col, val, x, y, R);
+  after_launch();
+}
+
+int launch_dot_partials(const double2* a, const double2* b, long long n, int R, double2* partial, cudaStream_t s) {
+  const int nb = blocks_for(n, kThreads / R);
+  dot_partials_kernel<<<nb, kThreads, 0, s>>>(a, b, n, R, partial);
+  after_launch();
+  return nb;
+}
+
+void launch_axpy_cols(double2* y, const double2* x, const double2* alpha, int neg, long long n, int R,
+                      cudaStream_t s) {
+  axpy_cols_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(y, x, alpha, neg, n, R);
+  after_launch();
+}
+
+void launch_scale_cols(double2* y, const double* inv, long long n, int R, cudaStream_t s) {
+  scale_cols_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(y, inv, n, R);
+  after_launch();
+}
+
+void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
+  transpose_in_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R);
+  after_launch();
+}
+
+void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
+  transpose_out_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R);
+  after_launch();
+}
+
+void launch_bump_epoch(unsigned* e, unsigned by, cudaStream_t s) {
+  bump_epoch_kernel<<<1, 1, 0, s>>>(e, by);
+  after_launch();
+}
+
+}  // namespace hsb

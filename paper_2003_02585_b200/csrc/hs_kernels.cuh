@@ -1,0 +1,107 @@
+// Launch wrappers for the sm_100a kernels of the helmsweep hot path (hs_kernels.cu).
+#pragma once
+
+#include "hs_device.cuh"
+
+namespace hsb {
+
+struct SolveArgs {
+  const SolveTask* tasks;
+  int ntasks;      // front tasks (each expands to n_rg RHS-group tasks)
+  int n_rg;        // RHS groups
+  int R;           // RHS per batch (x / V row stride)
+  unsigned* queue; // dynamic task counter (zeroed before launch)
+  unsigned* flags; // completion epochs [(sub * nf_max + front) * n_rg + rg]
+  int nf_max;
+  const unsigned* epoch_base;
+  unsigned epoch_off;
+  const DevClass* cls;
+  const DevSub* subs;
+  double2* vbuf;           // update-vector slots
+  long long vslot_stride;  // elements per slot
+  const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
+};
+
+// Multifrontal forward (L z = b, then z *= D^-1) and backward (L^T x = z) passes over
+// all fronts of the subdomains in one step group (src/direct.cpp:290-325).
+void launch_solve_forward(const SolveArgs& a, int rg_width, int grid, size_t smem, cudaStream_t s);
+void launch_solve_backward(const SolveArgs& a, int rg_width, int grid, size_t smem, cudaStream_t s);
+size_t solve_smem_bytes(int max_m, int rg_width);
+int solve_grid(int rg_width, size_t smem);
+
+struct FactorArgs {
+  const FactorTask* tasks;
+  int ntasks;
+  const DevClass* cls;
+  const DevSub* subs;
+  double2* work;                // dense front workspace (column-major m x m per front)
+  double2* scratch;             // global panel scratch when a panel does not fit in smem
+  unsigned long long* err_key;  // min over (sub << 32 | elimination position) of bad pivots
+};
+// Assembly + extend-add + partial LDL^T of every front at one tree height
+// (src/direct.cpp:55-87, 181-281).
+void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s);
+size_t factor_smem_bytes(int max_m);
+
+struct SweepArgs {
+  DevGeom g;
+  const DevClass* cls;
+  const DevSub* subs;
+  const int* group;        // subdomains of the step group (ascending flattened id)
+  int ngroup;
+  int R;
+  int l;                   // 1-based sweep index
+  int nsweeps;
+  int dirs;                // 2*dim
+  const double2* b;        // global rhs, node-major N x R
+  double2* mbox;           // mailbox slots [sub][sweep][dir][2][line][R]
+  long long mbox_dir_stride;  // elements per (sub, sweep, dir) slot
+  unsigned* mpres;         // presence bitmask [sub][sweep][dir]
+  unsigned* nzmask;        // [sweep][sub]
+  const int* route;        // [sweep][dir] target sweep (0 = discard)
+};
+// RHS of each subdomain task: split source (sweep 1) plus injected traces, and the
+// exact-zero test (src/sweeper.cpp:189-251, src/transfer.cpp:68-89).
+void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s);
+// Trace extraction -> routing -> mailbox deposit (src/transfer.cpp:13-66, src/sweeper.cpp:295-307).
+void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s);
+
+struct AccumArgs {
+  DevGeom g;
+  const DevClass* cls;
+  const DevSub* subs;
+  int R;
+  int l;
+  int dvec[3];               // sweep direction of sweep l
+  const unsigned* nzmask;    // [sub] for sweep l
+  double2* u;                // global solution, node-major N x R
+  double* partial;           // per-block partial |contrib|^2 [nblocks][R]
+};
+// u += sum_sub w * u_local over the subdomain supports in the reference's order
+// (src/transfer.cpp:91-102, src/sweeper.cpp:308-312); emits per-block norm partials.
+int launch_accumulate(const AccumArgs& a, cudaStream_t s);
+// Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
+void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s);
+
+// Global CSR SpMV y = A x (x, y node-major N x R) (src/operator.cpp:7-17) and the
+// residual partials |b - y|^2, |b|^2.
+int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
+                    const double2* x, const double2* b, int R, double* partial_num,
+                    double* partial_den, cudaStream_t s);
+void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
+                 const double2* x, double2* y, int R, cudaStream_t s);
+
+// RHS-major [R][N] <-> node-major [N][R] with optional per-column shell masking.
+void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
+void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
+void launch_bump_epoch(unsigned* epoch, unsigned by, cudaStream_t s);
+
+// Krylov vector kernels (src/krylov.cpp:9-13, 52-56, 109-111) on node-major N x R arrays.
+int launch_dot_partials(const double2* a, const double2* b, long long n, int R, double2* partial,
+                        cudaStream_t s);
+void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2* out, cudaStream_t s);
+void launch_axpy_cols(double2* y, const double2* x, const double2* alpha, int neg, long long n, int R,
+                      cudaStream_t s);
+void launch_scale_cols(double2* y, const double* inv, long long n, int R, cudaStream_t s);
+
+}  // namespace hsb

@@ -1,0 +1,201 @@
+"""GPU parity: the B200 path (through the C-ABI, libhelmsweep_b200.so) against the reference's
+golden vectors (tests/golden, produced by the reference itself) and the numpy oracle.
+
+Tolerances (BASELINE.json north_star): solutions <= 1e-9 relative L2 in complex128; sweep /
+trace counters bit-exact; GMRES iteration counts within +-1. The reference's own pins
+(tests/test_direct.cpp) keep their tolerances (1e-10 residual, exact known answers)."""
+import ast
+import math
+
+import numpy as np
+import pytest
+
+from oracle import hs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+COUNTERS = ["traces_generated", "traces_routed", "traces_discarded", "local_solves", "skipped_zero_solves"]
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def hs():
+    import paper_2003_02585_b200 as m
+    if m.device_count() == 0:
+        pytest.fail("gpu test run without a CUDA device")
+    return m
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def sparse_op(hs, z):
+    dim = int(z["dim"])
+    return hs.SparseOperator(dim, list(z["lo"]), list(z["hi"]), z["row_ptr"], z["col"], z["val"])
+
+
+@pytest.mark.parametrize("name", ["direct_2d", "direct_3d", "direct_2d_16"])
+def test_factor_solve_matches_reference(hs, golden, name):
+    z = golden(name)
+    op = sparse_op(hs, z)
+    f = hs.factorize(op)
+    assert f.stats().factor_nnz == int(z["factor_nnz"])
+    x = f.solve(z["b"])
+    assert rel(x, z["x"]) <= 1e-12
+    A = O.Csr(op.n, z["row_ptr"], z["col"], z["val"])
+    assert rel(A.apply(x), z["b"]) <= 1e-10            # tests/test_direct.cpp:95-104
+    assert np.array_equal(x, f.solve(z["b"]))          # bitwise repeatable (:123-134)
+    g = hs.factorize(op)
+    assert np.array_equal(x, g.solve(z["b"]))          # re-factorization identical
+    assert not np.any(f.solve(np.zeros(op.n, complex)))  # zero rhs -> exact zero (:88-93)
+
+
+def test_forward_multiply_oracle(hs, golden):
+    z = golden("direct_2d")  # tests/test_direct.cpp:106-121 (shell entries zeroed)
+    op = sparse_op(hs, z)
+    A = O.Csr(op.n, z["row_ptr"], z["col"], z["val"])
+    rng = O.GridRange(2, list(z["lo"]), list(z["hi"]))
+    P = rng.coords()
+    shell = np.zeros(op.n, bool)
+    for a in range(2):
+        shell |= (P[a] == rng.lo[a]) | (P[a] == rng.hi[a])
+    g = np.random.default_rng(21)
+    xt = g.uniform(-1, 1, op.n) + 1j * g.uniform(-1, 1, op.n)
+    xt[shell] = 0
+    x = hs.factorize(op).solve(A.apply(xt))
+    assert rel(x, xt) <= 1e-10
+
+
+def test_known_answers(hs):
+    one = hs.SparseOperator(2, [0, 0, 0], [0, 0, 0], np.array([0, 1]), np.array([0]), np.array([2.0 + 0j]))
+    assert hs.factorize(one).solve(np.array([3 + 1j]))[0] == 1.5 + 0.5j
+    n = 5
+    ident = hs.SparseOperator(2, [0, 0, 0], [n - 1, 0, 0], np.arange(n + 1), np.arange(n), np.ones(n, complex))
+    b = np.arange(n) + 0.5j
+    assert np.array_equal(hs.factorize(ident).solve(b), b)
+    bad = hs.SparseOperator(2, [0, 0, 0], [2, 0, 0], np.arange(4), np.arange(3), np.array([1.0, 0.0, 1.0], complex))
+    with pytest.raises(hs.SingularMatrixError) as e:
+        hs.factorize(bad)
+    assert e.value.pivot_index == 1                     # tests/test_direct.cpp:136-144
+    with pytest.raises(hs.ConfigError):
+        hs.factorize(one).solve(np.zeros(3, complex))
+
+
+def test_batched_solve_equals_single(hs, golden):
+    z = golden("direct_3d")
+    f = hs.factorize(sparse_op(hs, z))
+    g = np.random.default_rng(3)
+    B = g.standard_normal((7, f.stats().n)) + 1j * g.standard_normal((7, f.stats().n))
+    B[4] = 0
+    X = f.solve(B)
+    for i in range(7):
+        if i == 4:
+            assert not np.any(X[i])
+        else:
+            assert rel(X[i], f.solve(B[i])) <= 1e-14
+
+
+def _setup(hs, z):
+    dim = int(z["dim"])
+    med = ast.literal_eval(str(z["medium"]))
+    if med["media.kind"] == "constant":
+        m = hs.Medium("constant", kappa=med["media.kappa"])
+    else:
+        m = hs.Medium("two_layered", kappa_down=med["media.kappa_down"], kappa_up=med["media.kappa_up"],
+                      axis=med["media.axis"], eta=med["media.eta_L"], eps=med["media.epsilon"])
+    return hs.ProblemSetup(dim, [int(z["n"])] * dim, list(z["parts"]), m, pml_width=int(z["pad"]))
+
+
+@pytest.mark.parametrize("name", ["ddm_2d_2x2", "ddm_2d_3x2_r2", "ddm_2d_layered", "ddm_3d_2x2x2"])
+@pytest.mark.parametrize("batched", [False, True])
+def test_ddm_matches_reference(hs, golden, name, batched):
+    z = golden(name)
+    s = hs.DdmSolver(_setup(hs, z))
+    assert [s.sub_stats(i).factor_nnz for i in range(s.nsub)] == list(z["factor_nnz"])
+    assert [s.sub_stats(i).peak_bytes for i in range(s.nsub)] == list(z["peak_bytes"])
+    rounds = int(z["rounds"])
+    R = z["b"].shape[0]
+    if batched:
+        reps = []
+        U = s.ddm_solve(z["b"], rounds, reps, True)
+    else:
+        U, reps = [], []
+        for r in range(R):
+            U.append(s.ddm_solve(z["b"][r], rounds, reps, True))
+    for r in range(R):
+        assert rel(U[r], z["u"][r]) <= TOL
+        assert [getattr(reps[r], k) for k in COUNTERS] == list(z["counters"][r])
+        np.testing.assert_allclose(reps[r].sweep_contrib_norm, z["contrib_norm"][r], rtol=1e-8)
+        np.testing.assert_allclose(reps[r].round_residuals, z["round_residuals"][r], rtol=1e-6)
+
+
+def test_ddm_deterministic_and_linear(hs, golden):
+    z = golden("ddm_2d_2x2")
+    s = hs.DdmSolver(_setup(hs, z))
+    b0, b1 = z["b"][0], z["b"][1]
+    u = s.ddm_solve(np.stack([b0, b1, 2 * b0 - 1j * b1]), 1)
+    assert np.array_equal(u[:2], s.ddm_solve(np.stack([b0, b1]), 1))  # bitwise across calls
+    assert rel(u[2], 2 * u[0] - 1j * u[1]) <= 1e-12
+    uz = []
+    rz = s.ddm_solve(np.zeros_like(b0), 1, uz)
+    assert not np.any(rz) and uz[0].local_solves == 0 and uz[0].skipped_zero_solves == 16
+
+
+def test_c1_config_against_oracle(hs):
+    """BASELINE config 1 (256^2, 4x4, PML 20, omega = 2 pi 16, centre source) and one seeded
+    off-centre source, batched, against the numpy restatement."""
+    n, pad, kap = 256, 20, 2 * math.pi * 16
+    so = O.DdmSolver(O.ProblemSetup(O.Box(2), [n, n, 1], [4, 4, 1], O.Medium("constant", kappa=kap),
+                                    O.PmlSpec(width=pad)))
+    f = O.gaussian_source(so.ggrid, O.Box(2), [[0.5, 0.5], [0.3125, 0.6]], 2.0 / n)
+    b = so.scale_source(f).T.copy()
+    s = hs.DdmSolver(hs.ProblemSetup(2, [n, n], [4, 4], hs.Medium("constant", kappa=kap), pml_width=pad))
+    reps = []
+    U = s.ddm_solve(b, 1, reps, True)
+    for r in range(2):
+        uo, ro = so.ddm_solve(b[r].copy(), 1, True)
+        assert rel(U[r], uo) <= TOL
+        assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
+    assert [reps[0].local_solves, reps[0].skipped_zero_solves] == [48, 16]  # SURVEY §6.2 (C1 centre)
+
+
+def test_gmres_matches_reference(hs, golden):
+    z = golden("gmres_2d")
+    med = ast.literal_eval(str(z["medium"]))
+    s = hs.DdmSolver(hs.ProblemSetup(2, [int(z["n"])] * 2, list(z["parts"]), hs.Medium("constant", kappa=med["media.kappa"]),
+                                     pml_width=int(z["pad"])))
+    g = s.gmres(z["b"], float(z["tol"]), int(z["maxit"]), 1)
+    assert abs(g.iterations - int(z["iterations"])) <= 1
+    assert g.converged
+    assert rel(g.x, z["x"]) <= 1e-7
+    assert g.true_residual <= 1e-7
+
+
+def test_apply_op_matches_oracle(hs, golden):
+    z = golden("ddm_2d_layered")
+    s = hs.DdmSolver(_setup(hs, z))
+    so = O.DdmSolver(O.ProblemSetup(O.Box(2), [int(z["n"])] * 2 + [1], list(z["parts"]) + [1],
+                                    O.Medium("two_layered", kappa_down=12 * math.pi, kappa_up=8 * math.pi, axis=1,
+                                             eta=0.5 + 1 / 128, eps=0.0), O.PmlSpec(width=int(z["pad"]))), factor=False)
+    x = z["u"][0]
+    assert rel(s.apply_op(x), so.global_op().apply(x)) <= 1e-14
+
+
+def test_c2_subdomain_factor_against_oracle(hs):
+    """One subdomain of BASELINE config 2 (1024^2, 8x8, PML 32, omega = 2 pi 64; 193^2 local
+    grid, all four symbolic classes) factorized on the GPU vs the numpy restatement."""
+    n, pad, kap = 1024, 32, 2 * math.pi * 64
+    so = O.DdmSolver(O.ProblemSetup(O.Box(2), [n, n, 1], [8, 8, 1], O.Medium("constant", kappa=kap),
+                                    O.PmlSpec(width=pad)), factor=False)
+    g = np.random.default_rng(5)
+    for sid in (0, 1, 8, 9):
+        st = so.states[sid]
+        op = hs.SparseOperator(2, st.grid.range.lo, st.grid.range.hi, st.op.row_ptr, st.op.col, st.op.val)
+        f = hs.factorize(op)
+        fo = O.factorize(st.op, 2, st.grid.range)
+        assert f.stats().factor_nnz == fo.factor_nnz
+        b = g.standard_normal((3, st.op.n)) + 1j * g.standard_normal((3, st.op.n))
+        X = f.solve(b)
+        for r in range(3):
+            assert rel(X[r], fo.solve(b[r])) <= 1e-11
