@@ -85,8 +85,8 @@ struct Engine {
   int nf_max = 0, max_m = 0;
   long long v_total_max = 0, n_max = 0;
   // solve state
-  int R = 0, rg = 4, n_rg = 1, nslots = 0, solve_grid_sz = 0;
-  size_t solve_smem = 0;
+  int R = 0, rg = 16, n_rg = 1, nslots = 0, hb = 2, grid_bundle = 0, grid_upper = 0;
+  size_t smem_bundle = 0, smem_upper = 0;
   DBuf<double2> x, vbuf;
   DBuf<unsigned> flags, epoch;
   unsigned epoch_host = 0;
@@ -337,12 +337,9 @@ struct Engine {
 
   // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains.
   void ensure_solve(int r, int slots) {
-    const int want_rg = r >= 4 ? 4 : (r >= 2 ? 2 : 1);
-    int rgsel = want_rg;
-    if (const char* e = std::getenv("HS_RG")) rgsel = std::max(1, std::min(8, std::atoi(e)));
-    if (r == R && slots <= nslots && rgsel == rg) return;
+    if (r == R && slots <= nslots) return;
     R = r;
-    rg = rgsel;
+    rg = solve_rhs_group();
     n_rg = (R + rg - 1) / rg;
     nslots = std::max(slots, nslots);
     const int nsub = static_cast<int>(sub_cls.size());
@@ -352,8 +349,67 @@ struct Engine {
     flags.zero(stream);
     for (int s = 0; s < nsub; ++s) h_subs[s].x = x.p + n_base[s] * R;
     d_subs.upload(h_subs, stream);
-    solve_smem = solve_smem_bytes(max_m, rg);
-    solve_grid_sz = solve_grid(rg, solve_smem);
+    // staging rows per task class: bundles (height <= hb) and single upper fronts
+    hb = 2;
+    if (const char* e = std::getenv("HS_BUNDLE_H")) hb = std::atoi(e);
+    int rows_b = 32, rows_u = 32;
+    for (auto& cdp : classes)
+      for (const FrontDesc& fd : cdp->sym->fronts) {
+        const int rows = std::max((fd.m + 7) & ~7, 32 * ((fd.k + 31) / 32));
+        if (fd.height <= hb)
+          rows_b = std::max(rows_b, rows);
+        else
+          rows_u = std::max(rows_u, rows);
+      }
+    smem_bundle = solve_smem_bytes(rows_b, true);
+    smem_upper = solve_smem_bytes(rows_u, true);
+    grid_bundle = solve_grid(smem_bundle);
+    grid_upper = solve_grid(smem_upper);
+  }
+
+  // Dataflow task lists of the subdomains `group` (slot = position): forward = every low
+  // subtree of height <= hb as one bundle task, then the upper fronts by height; backward =
+  // upper fronts by depth, then the bundles (hs_solve.cu).
+  // Returns the number of bundle tasks (fwd = bundles then uppers, bwd = uppers then bundles).
+  int build_tasks(const std::vector<int>& group, std::vector<SolveTask>& fwd, std::vector<SolveTask>& bwd) const {
+    int hmax = 0, dmax = 0;
+    for (int id : group) {
+      hmax = std::max(hmax, classes[sub_cls[id]]->sym->max_height);
+      dmax = std::max(dmax, classes[sub_cls[id]]->sym->max_depth);
+    }
+    std::vector<SolveTask> bundles;
+    for (size_t g = 0; g < group.size(); ++g) {
+      const SymbolicClass& c = *classes[sub_cls[group[g]]]->sym;
+      std::vector<int> size(c.fronts.size(), 1);
+      for (size_t f = 0; f < c.fronts.size(); ++f)
+        for (int ch : c.fronts[f].child)
+          if (ch >= 0) size[f] += size[ch];
+      for (size_t f = 0; f < c.fronts.size(); ++f) {
+        const FrontDesc& fd = c.fronts[f];
+        if (fd.height > hb) continue;
+        if (fd.parent >= 0 && c.fronts[fd.parent].height <= hb) continue;
+        bundles.push_back(SolveTask{group[g], static_cast<int>(f) - size[f] + 1, static_cast<int>(f), static_cast<int>(g)});
+      }
+    }
+    fwd.insert(fwd.end(), bundles.begin(), bundles.end());
+    for (int h = hb + 1; h <= hmax; ++h)
+      for (size_t g = 0; g < group.size(); ++g) {
+        const SymbolicClass& c = *classes[sub_cls[group[g]]]->sym;
+        if (h > c.max_height) continue;
+        for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
+          fwd.push_back(SolveTask{group[g], c.order_up[q], c.order_up[q], static_cast<int>(g)});
+      }
+    for (int d = 0; d <= dmax; ++d)
+      for (size_t g = 0; g < group.size(); ++g) {
+        const ClassDev& cd = *classes[sub_cls[group[g]]];
+        if (d > cd.sym->max_depth) continue;
+        for (int q = cd.level_start_down[d]; q < cd.level_start_down[d + 1]; ++q) {
+          const int f = cd.sym->order_down[q];
+          if (cd.sym->fronts[f].height > hb) bwd.push_back(SolveTask{group[g], f, f, static_cast<int>(g)});
+        }
+      }
+    bwd.insert(bwd.end(), bundles.begin(), bundles.end());
+    return static_cast<int>(bundles.size());
   }
 
   SolveArgs solve_args(const SolveTask* tasks, int ntasks, unsigned* queue, const unsigned* nzmask,
@@ -376,11 +432,20 @@ struct Engine {
     return a;
   }
 
-  void run_solve(const SolveArgs& fwd, const SolveArgs& bwd) {
-    const int total = fwd.ntasks * n_rg;
-    const int grid = std::max(1, std::min(solve_grid_sz, total));
-    launch_solve_forward(fwd, rg, grid, solve_smem, stream);
-    launch_solve_backward(bwd, rg, grid, solve_smem, stream);
+  // Forward: bundles then upper fronts; backward: upper fronts then bundles. Four persistent
+  // launches, queue[0..3], epochs epoch_off (forward) and epoch_off + 1 (backward).
+  void run_solve(const SolveTask* fwd, const SolveTask* bwd, int nbundle, int nupper, unsigned* queue,
+                 const unsigned* nzmask, unsigned epoch_off) {
+    auto go = [&](const SolveTask* t, int n, unsigned* qc, bool f, bool bundle) {
+      if (n == 0) return;
+      SolveArgs a = solve_args(t, n, qc, nzmask, f ? epoch_off : epoch_off + 1);
+      const int grid = std::max(1, std::min(bundle ? grid_bundle : grid_upper, n * n_rg));
+      launch_solve(a, f, grid, bundle ? smem_bundle : smem_upper, stream);
+    };
+    go(fwd, nbundle, queue + 0, true, true);
+    go(fwd + nbundle, nupper, queue + 1, true, false);
+    go(bwd, nupper, queue + 2, false, false);
+    go(bwd + nupper, nbundle, queue + 3, false, true);
   }
 };
 
@@ -408,6 +473,7 @@ struct FactorHandle {
   Engine eng;
   hs_factor_stats stats{};
   std::vector<SolveTask> fwd, bwd;
+  int nbundle = 0;
   DBuf<SolveTask> d_fwd, d_bwd;
   DBuf<unsigned> queue, nz;
   DBuf<double2> io;
@@ -467,11 +533,9 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
     HS_CUDA(cudaGetLastError());
     const unsigned mask = R >= 32 ? ~0u : ((1u << R) - 1u);
     HS_CUDA(cudaMemcpyAsync(H.nz.p, &mask, sizeof(unsigned), cudaMemcpyHostToDevice, eng.stream));
-    HS_CUDA(cudaMemsetAsync(H.queue.p, 0, 2 * sizeof(unsigned), eng.stream));
+    HS_CUDA(cudaMemsetAsync(H.queue.p, 0, 4 * sizeof(unsigned), eng.stream));
     launch_bump_epoch(eng.epoch.p, 4, eng.stream);
-    SolveArgs fa = eng.solve_args(H.d_fwd.p, static_cast<int>(H.fwd.size()), H.queue.p, H.nz.p, 1);
-    SolveArgs ba = eng.solve_args(H.d_bwd.p, static_cast<int>(H.bwd.size()), H.queue.p + 1, H.nz.p, 2);
-    eng.run_solve(fa, ba);
+    eng.run_solve(H.d_fwd.p, H.d_bwd.p, H.nbundle, static_cast<int>(H.fwd.size()) - H.nbundle, H.queue.p, H.nz.p, 1);
     scatter_out_kernel<<<blocks, threads, 0, eng.stream>>>(eng.x.p, xb, eng.classes[0]->elim_of_local.p, n, R);
     g_kernel_launches.fetch_add(1);
     HS_CUDA(cudaGetLastError());
@@ -526,13 +590,10 @@ int hs_factorize(int dim, const int lo[3], const int hi[3], int64_t n, const int
     H.eng.upload_classes(-1);
     H.eng.factorize({&v});
     const SymbolicClass& c = *H.eng.classes[0]->sym;
-    for (int h = 0; h <= c.max_height; ++h)
-      for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
-        H.fwd.push_back(SolveTask{0, c.order_up[q], 0, 0});
-    for (int f2 : c.order_down) H.bwd.push_back(SolveTask{0, f2, 0, 0});
+    H.nbundle = H.eng.build_tasks({0}, H.fwd, H.bwd);
     H.d_fwd.upload(H.fwd, H.eng.stream);
     H.d_bwd.upload(H.bwd, H.eng.stream);
-    H.queue.alloc(2);
+    H.queue.alloc(4);
     H.nz.alloc(1);
     HS_CUDA(cudaStreamSynchronize(H.eng.stream));
     H.stats.n = n;
@@ -618,7 +679,7 @@ struct DdmHandle {
   int steps = 0, ndir = 4, dirs = 4, max_group = 1;
   long long line_max = 1;
   std::vector<std::vector<int>> groups;  // [di * steps + s-1]
-  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
+  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt, nbundle;
   DBuf<int> d_groups;
   DBuf<SolveTask> d_tasks;
   DBuf<double2> d_coef;
@@ -857,11 +918,7 @@ void DdmHandle::build(const hs_problem& P, int device) {
   fwd_cnt.assign(ndir * steps, 0);
   bwd_off.assign(ndir * steps, 0);
   bwd_cnt.assign(ndir * steps, 0);
-  int hmax = 0, dmax = 0;
-  for (auto& cdp : eng.classes) {
-    hmax = std::max(hmax, cdp->sym->max_height);
-    dmax = std::max(dmax, cdp->sym->max_depth);
-  }
+  nbundle.assign(ndir * steps, 0);
   for (int di = 0; di < ndir; ++di)
     for (int s = 1; s <= steps; ++s) {
       const int gi = di * steps + s - 1;
@@ -870,26 +927,14 @@ void DdmHandle::build(const hs_problem& P, int device) {
       max_group = std::max(max_group, static_cast<int>(groups[gi].size()));
       grp_off[gi] = static_cast<int>(gflat.size());
       gflat.insert(gflat.end(), groups[gi].begin(), groups[gi].end());
+      std::vector<SolveTask> fw, bw;
+      nbundle[gi] = eng.build_tasks(groups[gi], fw, bw);
       fwd_off[gi] = static_cast<int>(tasks.size());
-      for (int h = 0; h <= hmax; ++h)
-        for (size_t g = 0; g < groups[gi].size(); ++g) {
-          const int id = groups[gi][g];
-          const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
-          if (h > c.max_height) continue;
-          for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
-            tasks.push_back(SolveTask{id, c.order_up[q], static_cast<int>(g), 0});
-        }
-      fwd_cnt[gi] = static_cast<int>(tasks.size()) - fwd_off[gi];
+      fwd_cnt[gi] = static_cast<int>(fw.size());
+      tasks.insert(tasks.end(), fw.begin(), fw.end());
       bwd_off[gi] = static_cast<int>(tasks.size());
-      for (int dd = 0; dd <= dmax; ++dd)
-        for (size_t g = 0; g < groups[gi].size(); ++g) {
-          const int id = groups[gi][g];
-          const ClassDev& cd = *eng.classes[subs[id].cls];
-          if (dd > cd.sym->max_depth) continue;
-          for (int q = cd.level_start_down[dd]; q < cd.level_start_down[dd + 1]; ++q)
-            tasks.push_back(SolveTask{id, cd.sym->order_down[q], static_cast<int>(g), 0});
-        }
-      bwd_cnt[gi] = static_cast<int>(tasks.size()) - bwd_off[gi];
+      bwd_cnt[gi] = static_cast<int>(bw.size());
+      tasks.insert(tasks.end(), bw.begin(), bw.end());
     }
   d_groups.upload(gflat, eng.stream);
   d_tasks.upload(tasks, eng.stream);
@@ -915,7 +960,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   mbox.alloc(static_cast<size_t>(nsub) * nsweeps * dirs * 2 * line_max * R);
   mpres.alloc(static_cast<size_t>(nsub) * nsweeps * dirs);
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
-  queue.alloc(static_cast<size_t>(nsweeps) * steps * 2);
+  queue.alloc(static_cast<size_t>(nsweeps) * steps * 4);
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
   const long long nb = (geom.gn * R + 255) / 256;
@@ -976,13 +1021,12 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
       sa.group = d_groups.p + grp_off[gi];
       sa.ngroup = static_cast<int>(groups[gi].size());
       launch_build_rhs(sa, eng.n_max, s);
-      const int qi = ((l - 1) * steps + (st - 1)) * 2;
+      const int qi = ((l - 1) * steps + (st - 1)) * 4;
       const unsigned off = 1u + static_cast<unsigned>(qi);
       const unsigned* nz = nzmask.p + static_cast<size_t>(l - 1) * nsub;
-      SolveArgs fa = eng.solve_args(d_tasks.p + fwd_off[gi], fwd_cnt[gi], queue.p + qi, nz, off);
-      SolveArgs ba = eng.solve_args(d_tasks.p + bwd_off[gi], bwd_cnt[gi], queue.p + qi + 1, nz, off + 1);
       if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
-      eng.run_solve(fa, ba);
+      eng.run_solve(d_tasks.p + fwd_off[gi], d_tasks.p + bwd_off[gi], nbundle[gi], fwd_cnt[gi] - nbundle[gi],
+                    queue.p + qi, nz, off);
       if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
       launch_extract_deposit(sa, static_cast<int>(line_max), s);
     }
@@ -1434,7 +1478,7 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
         const int q = (l - 1) * H.steps + st;
         HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * q], H.ev[2 + H.nsweeps + 2 * q]));
         sec += ms * 1e-3;
-        launches += 2;
+        launches += 4;
         for (int id : H.groups[((l - 1) % H.ndir) * H.steps + st]) {
           if (nz[static_cast<size_t>(l - 1) * nsub + id] == 0) continue;
           const SymbolicClass& c = *H.eng.classes[H.subs[id].cls]->sym;

@@ -58,8 +58,10 @@ struct DevGeom {
   long long gn;               // global node count
 };
 
+// A solve task: the postorder front range [f0, f1] of one subdomain (a whole low subtree
+// "bundle", or a single upper front when f0 == f1) and its update-vector slot.
 struct SolveTask {
-  int sub, front, slot, pad_;
+  int sub, f0, f1, slot;
 };
 
 struct FactorTask {

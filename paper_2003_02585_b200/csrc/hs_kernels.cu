@@ -1,8 +1,6 @@
 // sm_100a kernels of the helmsweep hot path. complex128 = double2 (re, im).
 //
-//   solve_kernel<RG, FWD>   multifrontal forward / backward triangular solves over every
-//                           front of a step group's subdomains, dataflow-scheduled in one
-//                           persistent launch per pass (src/direct.cpp:290-325)
+//   (the multifrontal solve kernels live in hs_solve.cu)
 //   factor_level_kernel     assembly + extend-add + panel LDL^T of one tree height
 //                           (src/direct.cpp:55-87, 181-281)
 //   rhs/inject/nonzero      split source, trace injection, exact-zero test
@@ -67,268 +65,6 @@ __device__ __forceinline__ void cacc(double2* p, double2 v) {
   p->y += v.y;
 }
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Reduce-scatter of 64 per-lane doubles over the 32 lanes of a warp by recursive
-// halving: afterwards lane l holds the warp-wide sums of entries 2l and 2l+1.
-__device__ __forceinline__ void reduce_scatter64(double (&v)[64], int lane) {
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int half = 32 >> s;
-    const int mask = 16 >> s;
-    const bool upper = (lane & mask) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const double send = upper ? v[i] : v[i + half];
-      const double keep = upper ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(kFull, send, mask);
-    }
-  }
-}
-
-__host__ __device__ __forceinline__ long long panel_offset(int m, int J) {
-  // sum_{J' < J} (m - 32 J') * 32
-  return 32LL * (static_cast<long long>(J) * m - 16LL * J * (J - 1));
-}
-
-// ----------------------------------------------------------------------------
-// solve
-
-template <int RG>
-__device__ void fwd_task(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& f,
-                         int slot, int rg, double2* t, double2* dblk) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int R = a.R, r0 = rg * RG;
-  const int k = f.k, m = f.m;
-  double2* V = a.vbuf + slot * a.vslot_stride;
-  // t[0:k] = x[sep], t[k:m] = 0
-  for (int idx = tid; idx < m * RG; idx += kThreads) {
-    const int e = idx / RG, r = idx % RG;
-    double2 v = czero();
-    if (e < k && r0 + r < R) v = S.x[static_cast<long long>(f.sep_off + e) * R + r0 + r];
-    t[idx] = v;
-  }
-  __syncthreads();
-  // extend-add of the children's update vectors, child0 then child1
-#pragma unroll 1
-  for (int q = 0; q < 2; ++q) {
-    const int ch = q ? f.child1 : f.child0;
-    if (ch < 0) continue;
-    const DevFront cf = C.fronts[ch];
-    const int cb = cf.m - cf.k;
-    const int* cmap = C.child_map + (q ? f.cmap1 : f.cmap0);
-    for (int idx = tid; idx < cb * RG; idx += kThreads) {
-      const int i = idx / RG, r = idx % RG;
-      if (r0 + r < R) cacc(&t[cmap[i] * RG + r], __ldcg(&V[(cf.v_off + i) * R + r0 + r]));
-    }
-    __syncthreads();
-  }
-  const double2* L = S.factor + f.fac_off;
-#pragma unroll 1
-  for (int j0 = 0; j0 < k; j0 += 32) {
-    const int w = min(32, k - j0);
-    const int rows = m - j0;
-    for (int idx = tid; idx < w * 32; idx += kThreads) {
-      const int i = idx >> 5, c = idx & 31;
-      dblk[i * 33 + c] = __ldg(&L[i * 32 + c]);
-    }
-    __syncthreads();
-    if (warp < RG) {  // unit-lower solve of the diagonal block, one warp per RHS
-      const int r = warp;
-      double2 ti = lane < w ? t[(j0 + lane) * RG + r] : czero();
-#pragma unroll 1
-      for (int j = 0; j < w - 1; ++j) {
-        double2 tj;
-        tj.x = __shfl_sync(kFull, ti.x, j);
-        tj.y = __shfl_sync(kFull, ti.y, j);
-        if (lane > j && lane < w) cfms(ti, dblk[lane * 33 + j], tj);
-      }
-      if (lane < w) t[(j0 + lane) * RG + r] = ti;
-    }
-    __syncthreads();
-    const int nrem = m - (j0 + w);
-    if (nrem > 0) {
-      constexpr int RB = 32 / RG;
-      double2 tj[RG];
-#pragma unroll
-      for (int r = 0; r < RG; ++r) tj[r] = lane < w ? t[(j0 + lane) * RG + r] : czero();
-      const int nb = (nrem + RB - 1) / RB;
-#pragma unroll 1
-      for (int b = warp; b < nb; b += kWarps) {
-        const int i0 = j0 + w + b * RB;
-        double2 Lv[RB];
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr) {
-          const int i = i0 + rr;
-          Lv[rr] = (i < m && lane < w) ? __ldg(&L[static_cast<long long>(i - j0) * 32 + lane]) : czero();
-        }
-        double v[64];
-#pragma unroll
-        for (int rr = 0; rr < RB; ++rr)
-#pragma unroll
-          for (int r = 0; r < RG; ++r) {
-            const double2 p = cmul(Lv[rr], tj[r]);
-            v[(rr * RG + r) * 2] = p.x;
-            v[(rr * RG + r) * 2 + 1] = p.y;
-          }
-        reduce_scatter64(v, lane);
-        const int rr = lane / RG, r = lane % RG, i = i0 + rr;
-        if (i < m) {
-          double2& tt = t[i * RG + r];
-          tt.x -= v[0];
-          tt.y -= v[1];
-        }
-      }
-    }
-    __syncthreads();
-    L += static_cast<long long>(rows) * 32;
-  }
-  // x[sep] = D^-1 t[0:k] (the diagonal scaling of src/direct.cpp:309 fused), V = t[k:m]
-  for (int idx = tid; idx < m * RG; idx += kThreads) {
-    const int e = idx / RG, r = idx % RG;
-    if (r0 + r >= R) continue;
-    if (e < k) {
-      const long long pos = f.sep_off + e;
-      S.x[pos * R + r0 + r] = cmul(t[idx], S.dinv[pos]);
-    } else {
-      __stcg(&V[(f.v_off + e - k) * R + r0 + r], t[idx]);
-    }
-  }
-}
-
-template <int RG>
-__device__ void bwd_task(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& f,
-                         int rg, double2* t, double2* dblk, double2* red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int R = a.R, r0 = rg * RG;
-  const int k = f.k, m = f.m;
-  for (int idx = tid; idx < m * RG; idx += kThreads) {
-    const int e = idx / RG, r = idx % RG;
-    double2 v = czero();
-    if (r0 + r < R) {
-      const long long pos = e < k ? f.sep_off + e : C.bnd_elim[f.bnd_off + e - k];
-      v = __ldcg(&S.x[pos * R + r0 + r]);
-    }
-    t[idx] = v;
-  }
-  __syncthreads();
-  const int np = (k + 31) / 32;
-#pragma unroll 1
-  for (int J = np - 1; J >= 0; --J) {
-    const int j0 = 32 * J, w = min(32, k - j0);
-    const double2* P = S.factor + f.fac_off + panel_offset(m, J);
-    for (int idx = tid; idx < w * 32; idx += kThreads) {
-      const int i = idx >> 5, c = idx & 31;
-      dblk[i * 33 + c] = __ldg(&P[i * 32 + c]);
-    }
-    // t[J] -= L[j0+w:m, J]^T t[j0+w:m]
-    double2 acc[RG];
-#pragma unroll
-    for (int r = 0; r < RG; ++r) acc[r] = czero();
-    int i = j0 + w + warp;
-#pragma unroll 1
-    for (; i + 3 * kWarps < m; i += 4 * kWarps) {
-      double2 Lv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        Lv[u] = lane < w ? __ldg(&P[static_cast<long long>(i + u * kWarps - j0) * 32 + lane]) : czero();
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int r = 0; r < RG; ++r) cfma(acc[r], Lv[u], t[(i + u * kWarps) * RG + r]);
-    }
-#pragma unroll 1
-    for (; i < m; i += kWarps) {
-      const double2 Lv = lane < w ? __ldg(&P[static_cast<long long>(i - j0) * 32 + lane]) : czero();
-#pragma unroll
-      for (int r = 0; r < RG; ++r) cfma(acc[r], Lv, t[i * RG + r]);
-    }
-#pragma unroll
-    for (int r = 0; r < RG; ++r) red[(warp * 32 + lane) * RG + r] = acc[r];
-    __syncthreads();
-    for (int idx = tid; idx < 32 * RG; idx += kThreads) {
-      const int j = idx / RG, r = idx % RG;
-      if (j < w) {
-        double2 s = czero();
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) s = cadd(s, red[(q * 32 + j) * RG + r]);
-        double2& tt = t[(j0 + j) * RG + r];
-        tt = csub(tt, s);
-      }
-    }
-    __syncthreads();
-    if (warp < RG) {  // unit-upper (L^T) solve of the diagonal block
-      const int r = warp;
-      double2 ti = lane < w ? t[(j0 + lane) * RG + r] : czero();
-#pragma unroll 1
-      for (int j = w - 1; j >= 1; --j) {
-        double2 tj;
-        tj.x = __shfl_sync(kFull, ti.x, j);
-        tj.y = __shfl_sync(kFull, ti.y, j);
-        if (lane < j) cfms(ti, dblk[j * 33 + lane], tj);
-      }
-      if (lane < w) t[(j0 + lane) * RG + r] = ti;
-    }
-    __syncthreads();
-  }
-  for (int idx = tid; idx < k * RG; idx += kThreads) {
-    const int e = idx / RG, r = idx % RG;
-    if (r0 + r < R) __stcg(&S.x[static_cast<long long>(f.sep_off + e) * R + r0 + r], t[idx]);
-  }
-}
-
-template <int RG, bool FWD>
-__global__ void __launch_bounds__(kThreads, 2) solve_kernel(SolveArgs a, int tcap) {
-  extern __shared__ double2 sm[];
-  __shared__ int s_task;
-  double2* t = sm;
-  double2* dblk = t + tcap * RG;
-  double2* red = dblk + 32 * 33;
-  const unsigned epoch = *a.epoch_base + a.epoch_off;
-  const int total = a.ntasks * a.n_rg;
-  for (;;) {
-    if (threadIdx.x == 0) s_task = static_cast<int>(atomicAdd(a.queue, 1u));
-    __syncthreads();
-    const int tk = s_task;
-    __syncthreads();
-    if (tk >= total) break;
-    const SolveTask task = a.tasks[tk / a.n_rg];
-    const int rg = tk % a.n_rg;
-    if (a.nzmask[task.sub] == 0) continue;  // skipped subdomain: no task waits on it
-    const DevSub& S = a.subs[task.sub];
-    const DevClass& C = a.cls[S.cls];
-    const DevFront f = C.fronts[task.front];
-    unsigned* fl = a.flags + static_cast<long long>(task.sub) * a.nf_max * a.n_rg + rg;
-    if (threadIdx.x == 0) {
-      if (FWD) {
-        if (f.child0 >= 0)
-          while (ld_acquire(fl + static_cast<long long>(f.child0) * a.n_rg) != epoch) __nanosleep(20);
-        if (f.child1 >= 0)
-          while (ld_acquire(fl + static_cast<long long>(f.child1) * a.n_rg) != epoch) __nanosleep(20);
-      } else if (f.parent >= 0) {
-        while (ld_acquire(fl + static_cast<long long>(f.parent) * a.n_rg) != epoch) __nanosleep(20);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    if (FWD)
-      fwd_task<RG>(a, C, S, f, task.slot, rg, t, dblk);
-    else
-      bwd_task<RG>(a, C, S, f, rg, t, dblk, red);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      st_release(fl + static_cast<long long>(task.front) * a.n_rg, epoch);
-    }
-  }
-}
 
 // ----------------------------------------------------------------------------
 // factorization
@@ -451,15 +187,57 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
     }
     __syncthreads();
   }
-  // outputs: D^-1 and the 32-column solve panels (strict lower part)
+  // D^-1, then the partitioned inverse of the eliminated columns: M = L11^-1 (unit lower)
+  // and W = L21 M replace L11 / L21, so each front's solve is a dense product (hs_solve.cu).
   for (int j = tid; j < k; j += kThreads) S.dinv[f.sep_off + j] = crecip(F[static_cast<long long>(j) * m + j]);
-  double2* out = S.factor + f.fac_off;
-  for (int J = 0; 32 * J < k; ++J) {
-    const int j0 = 32 * J, rowsJ = m - j0;
-    double2* P = out + panel_offset(m, J);
-    for (int idx = tid; idx < rowsJ * 32; idx += kThreads) {
-      const int row = j0 + idx / 32, col = j0 + idx % 32;
-      P[idx] = (col < k && row > col) ? F[static_cast<long long>(col) * m + row] : czero();
+  double2* rowbuf = Ps;  // >= 32 m entries of scratch (smem or global)
+  __syncthreads();
+#pragma unroll 1
+  for (int i = 1; i < k; ++i) {  // M row i: M[i][j] = -sum_{l=j}^{i-1} L[i][l] M[l][j]
+    for (int l = tid; l < i; l += kThreads) rowbuf[l] = F[static_cast<long long>(l) * m + i];
+    __syncthreads();
+    for (int j = tid; j < i; j += kThreads) {
+      double2 acc = rowbuf[j];
+      for (int l = j + 1; l < i; ++l) cfma(acc, rowbuf[l], F[static_cast<long long>(j) * m + l]);
+      F[static_cast<long long>(j) * m + i] = make_double2(-acc.x, -acc.y);
+    }
+    __syncthreads();
+  }
+  {  // W rows: one warp per row, the row of L21 staged in a per-warp buffer
+    const int warp = tid >> 5, lane = tid & 31;
+    double2* wb = rowbuf + static_cast<long long>(warp) * k;
+    for (int r = k + warp; r < m; r += kWarps) {
+      for (int l = lane; l < k; l += 32) wb[l] = F[static_cast<long long>(l) * m + r];
+      __syncwarp();
+      for (int j = lane; j < k; j += 32) {
+        double2 acc = wb[j];
+        for (int l = j + 1; l < k; ++l) cfma(acc, wb[l], F[static_cast<long long>(j) * m + l]);
+        F[static_cast<long long>(j) * m + r] = acc;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // [M; W] as 32x32 chunks in row-block-major order (chunk (rb, J) for J <= min(rb, np-1)),
+  // rows padded to a multiple of 8, each chunk column-major with the XOR-8 row swizzle.
+  {
+    const int m_pad = (m + 7) & ~7, nrb = (m_pad + 31) >> 5, np = (k + 31) >> 5;
+    double2* P = S.factor + f.fac_off;
+    for (int rb = 0; rb < nrb; ++rb) {
+      const int rc = min(32, m_pad - 32 * rb), nj = min(rb, np - 1) + 1;
+      for (int idx = tid; idx < nj * rc * 32; idx += kThreads) {
+        const int J = idx / (rc * 32), rem = idx % (rc * 32), j = rem / rc, il = rem % rc;
+        const int row = 32 * rb + il, col = 32 * J + j;
+        double2 v = czero();
+        if (row < m && col < k) {
+          if (row >= k || row > col)
+            v = F[static_cast<long long>(col) * m + row];
+          else if (row == col)
+            v = make_double2(1.0, 0.0);
+        }
+        P[J * rc * 32 + j * rc + ((il & ~7) | ((il ^ j) & 7))] = v;
+      }
+      P += static_cast<long long>(nj) * rc * 32;
     }
   }
 }
@@ -680,36 +458,33 @@ __global__ void accumulate_kernel(AccumArgs a) {
   }
 }
 
+// One block per RHS column; fixed strided assignment + fixed tree => deterministic.
 __global__ void reduce_partials_kernel(const double* partial, int nblocks, int R, double* out) {
   __shared__ double red[kThreads];
-  const int Q = kThreads / R;
-  const int r = threadIdx.x % R, q = threadIdx.x / R;
+  const int r = blockIdx.x;
   double s = 0.0;
-  if (q < Q)
-    for (int b = q; b < nblocks; b += Q) s += partial[static_cast<long long>(b) * R + r];
+  for (int b = threadIdx.x; b < nblocks; b += kThreads) s += partial[static_cast<long long>(b) * R + r];
   red[threadIdx.x] = s;
   __syncthreads();
-  if (threadIdx.x < R) {
-    double t = 0.0;
-    for (int qq = 0; qq < Q; ++qq) t += red[qq * R + threadIdx.x];
-    out[threadIdx.x] = t;
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[r] = red[0];
 }
 
 __global__ void reduce_cpartials_kernel(const double2* partial, int nblocks, int R, double2* out) {
   __shared__ double2 red[kThreads];
-  const int Q = kThreads / R;
-  const int r = threadIdx.x % R, q = threadIdx.x / R;
+  const int r = blockIdx.x;
   double2 s = czero();
-  if (q < Q)
-    for (int b = q; b < nblocks; b += Q) s = cadd(s, partial[static_cast<long long>(b) * R + r]);
+  for (int b = threadIdx.x; b < nblocks; b += kThreads) s = cadd(s, partial[static_cast<long long>(b) * R + r]);
   red[threadIdx.x] = s;
   __syncthreads();
-  if (threadIdx.x < R) {
-    double2 t = czero();
-    for (int qq = 0; qq < Q; ++qq) t = cadd(t, red[qq * R + threadIdx.x]);
-    out[threadIdx.x] = t;
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = cadd(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[r] = red[0];
 }
 
 __global__ void residual_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
@@ -808,58 +583,7 @@ __global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
 
 int blocks_for(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
 
-template <int RG, bool FWD>
-void launch_solve_t(const SolveArgs& a, int grid, size_t smem, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    HS_CUDA(cudaFuncSetAttribute(solve_kernel<RG, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
-  const int tcap = static_cast<int>((smem - (32 * 33 + kWarps * 32 * RG) * sizeof(double2)) / (RG * sizeof(double2)));
-  solve_kernel<RG, FWD><<<grid, kThreads, smem, s>>>(a, tcap);
-  after_launch();
-}
-
 }  // namespace
-
-size_t solve_smem_bytes(int max_m, int rg) {
-  return (static_cast<size_t>(max_m) * rg + 32 * 33 + kWarps * 32 * rg) * sizeof(double2);
-}
-
-int solve_grid(int rg, size_t smem) {
-  int dev = 0, sms = 0, per = 1;
-  HS_CUDA(cudaGetDevice(&dev));
-  HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  switch (rg) {
-    case 1: HS_CUDA(cudaFuncSetAttribute(solve_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<1, true>, kThreads, smem)); break;
-    case 2: HS_CUDA(cudaFuncSetAttribute(solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<2, true>, kThreads, smem)); break;
-    case 4: HS_CUDA(cudaFuncSetAttribute(solve_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<4, true>, kThreads, smem)); break;
-    default: HS_CUDA(cudaFuncSetAttribute(solve_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-             HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve_kernel<8, true>, kThreads, smem)); break;
-  }
-  return sms * (per > 0 ? per : 1);
-}
-
-void launch_solve_forward(const SolveArgs& a, int rg, int grid, size_t smem, cudaStream_t s) {
-  switch (rg) {
-    case 1: launch_solve_t<1, true>(a, grid, smem, s); break;
-    case 2: launch_solve_t<2, true>(a, grid, smem, s); break;
-    case 4: launch_solve_t<4, true>(a, grid, smem, s); break;
-    default: launch_solve_t<8, true>(a, grid, smem, s); break;
-  }
-}
-
-void launch_solve_backward(const SolveArgs& a, int rg, int grid, size_t smem, cudaStream_t s) {
-  switch (rg) {
-    case 1: launch_solve_t<1, false>(a, grid, smem, s); break;
-    case 2: launch_solve_t<2, false>(a, grid, smem, s); break;
-    case 4: launch_solve_t<4, false>(a, grid, smem, s); break;
-    default: launch_solve_t<8, false>(a, grid, smem, s); break;
-  }
-}
 
 size_t factor_smem_bytes(int max_m) { return static_cast<size_t>(2) * max_m * kNB * sizeof(double2); }
 
@@ -899,12 +623,12 @@ int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
 }
 
 void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s) {
-  reduce_partials_kernel<<<1, kThreads, 0, s>>>(partial, nblocks, R, out);
+  reduce_partials_kernel<<<R, kThreads, 0, s>>>(partial, nblocks, R, out);
   after_launch();
 }
 
 void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2* out, cudaStream_t s) {
-  reduce_cpartials_kernel<<<1, kThreads, 0, s>>>(partial, nblocks, R, out);
+  reduce_cpartials_kernel<<<R, kThreads, 0, s>>>(partial, nblocks, R, out);
   after_launch();
 }
 

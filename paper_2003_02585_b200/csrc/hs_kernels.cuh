@@ -7,7 +7,7 @@ namespace hsb {
 
 struct SolveArgs {
   const SolveTask* tasks;
-  int ntasks;      // front tasks (each expands to n_rg RHS-group tasks)
+  int ntasks;      // tasks (each expands to n_rg RHS-group tasks)
   int n_rg;        // RHS groups
   int R;           // RHS per batch (x / V row stride)
   unsigned* queue; // dynamic task counter (zeroed before launch)
@@ -22,12 +22,12 @@ struct SolveArgs {
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
 };
 
-// Multifrontal forward (L z = b, then z *= D^-1) and backward (L^T x = z) passes over
-// all fronts of the subdomains in one step group (src/direct.cpp:290-325).
-void launch_solve_forward(const SolveArgs& a, int rg_width, int grid, size_t smem, cudaStream_t s);
-void launch_solve_backward(const SolveArgs& a, int rg_width, int grid, size_t smem, cudaStream_t s);
-size_t solve_smem_bytes(int max_m, int rg_width);
-int solve_grid(int rg_width, size_t smem);
+// Multifrontal forward (L z = b, then z *= D^-1) or backward (L^T x = z) pass over the
+// tasks of one step group (src/direct.cpp:290-325); hs_solve.cu.
+void launch_solve(const SolveArgs& a, bool fwd, int grid, size_t smem, cudaStream_t s);
+size_t solve_smem_bytes(int max_m, bool fwd);
+int solve_grid(size_t smem);
+int solve_rhs_group();
 
 struct FactorArgs {
   const FactorTask* tasks;

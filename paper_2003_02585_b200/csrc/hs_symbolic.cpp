@@ -217,7 +217,7 @@ std::unique_ptr<SymbolicClass> build_symbolic(int dim, const GridRange& range,
   for (int f = 0; f < nf; ++f) {
     FrontDesc& fd = c.fronts[f];
     fd.fac_off = fac;
-    for (int j0 = 0; j0 < fd.k; j0 += kSolvePanel) fac += static_cast<long long>(fd.m - j0) * kSolvePanel;
+    fac += front_chunk_elems(fd.m, fd.k);
     fd.v_off = v;
     v += fd.m - fd.k;
     fd.f_off = fw;

@@ -24,6 +24,19 @@ namespace hsb {
 constexpr int kLeafNodes = 64;   // src/direct.cpp:15
 constexpr int kSolvePanel = 32;  // solve-kernel panel width (device layout)
 
+// Elements of a front's solve factor [M; W] (M = L11^-1, W = L21 M): 32x32 chunks (rb, J),
+// J <= min(rb, np-1), rows padded to a multiple of 8 (layout: hs_kernels.cu factor output).
+inline long long front_chunk_elems(int m, int k) {
+  const int m_pad = (m + 7) & ~7, nrb = (m_pad + 31) >> 5, np = (k + 31) >> 5;
+  long long e = 0;
+  for (int rb = 0; rb < nrb; ++rb) {
+    const int rc = m_pad - 32 * rb < 32 ? m_pad - 32 * rb : 32;
+    const int nj = (rb < np - 1 ? rb : np - 1) + 1;
+    e += static_cast<long long>(nj) * rc * 32;
+  }
+  return e;
+}
+
 struct FrontDesc {
   int k = 0, m = 0;
   int sep_off = 0;       // first elimination position of the separator

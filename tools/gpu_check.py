@@ -41,7 +41,7 @@ def fact_tests():
     # 1x1 and singular
     op1 = hs.SparseOperator(2, [0,0,0], [0,0,0], np.array([0,1]), np.array([0]), np.array([2.0+0j]))
     print("  1x1:", hs.factorize(op1).solve(np.array([3+1j])))
-    opd = hs.SparseOperator(2, [0,0,0], [2,0,0], np.array([0,1,2,3]), np.array([0,1,2]), np.array([1.0,0.0,1.0]+0j))
+    opd = hs.SparseOperator(2, [0,0,0], [2,0,0], np.array([0,1,2,3]), np.array([0,1,2]), np.array([1.0,0.0,1.0])+0j)
     try:
         hs.factorize(opd); print("  singular NOT raised")
     except hs.SingularMatrixError as e:
