@@ -12,6 +12,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -64,6 +65,7 @@ struct ClassDev {
   std::unique_ptr<SymbolicClass> sym;
   DBuf<DevFront> fronts;
   DBuf<int> bnd_elim, child_map, orig_fpos, orig_eidx, elim_of_local, local_of_elim;
+  DBuf<int2> pmap;
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   std::vector<int> level_start_down;
   DevClass dev{};
@@ -83,13 +85,11 @@ struct Engine {
   std::vector<double> tol;
   double factor_gpu_seconds = 0.0;
   int nf_max = 0, max_m = 0;
-  long long v_total_max = 0, n_max = 0;
+  long long v_total_max = 0, t_total_max = 0, n_max = 0;
   // solve state
-  int R = 0, rg = 16, n_rg = 1, nslots = 0, hb = 2, grid_bundle = 0, grid_upper = 0;
-  size_t smem_bundle = 0, smem_upper = 0;
-  DBuf<double2> x, vbuf;
-  DBuf<unsigned> flags, epoch;
-  unsigned epoch_host = 0;
+  int R = 0, nslots = 0, big_k = 64;
+  DBuf<double2> x, x1, vbuf, tbuf;
+  DBuf<int> cnt;
 
   ~Engine() {
     if (stream) cudaStreamDestroy(stream);
@@ -104,8 +104,6 @@ struct Engine {
     dim = d;
     HS_CUDA(cudaSetDevice(device));
     HS_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    epoch.alloc(1);
-    epoch.zero(stream);
   }
 
   int add_class(std::unique_ptr<SymbolicClass> sc) {
@@ -184,6 +182,7 @@ struct Engine {
         d.fac_off = s.fac_off;
         d.v_off = s.v_off;
         d.f_off = s.f_off;
+        d.t_off = s.t_off;
       }
       cd.fronts.upload(fr, stream);
       cd.bnd_elim.upload(c.bnd_elim, stream);
@@ -195,6 +194,21 @@ struct Engine {
       cd.dev.fronts = cd.fronts.p;
       cd.dev.bnd_elim = cd.bnd_elim.p;
       cd.dev.child_map = cd.child_map.p;
+      {  // inverse extend-add maps: parent position -> child0 / child1 update row
+        std::vector<int2> pm(std::max<long long>(c.t_total, 1), make_int2(-1, -1));
+        for (const FrontDesc& fd : c.fronts)
+          for (int q = 0; q < 2; ++q) {
+            const int ch = fd.child[q];
+            if (ch < 0) continue;
+            const int cb = c.fronts[ch].m - c.fronts[ch].k;
+            for (int i = 0; i < cb; ++i) {
+              int2& e = pm[fd.t_off + c.child_map[fd.cmap_off[q] + i]];
+              (q ? e.y : e.x) = i;
+            }
+          }
+        cd.pmap.upload(pm, stream);
+        cd.dev.pmap = cd.pmap.p;
+      }
       cd.dev.orig_fpos = cd.orig_fpos.p;
       cd.dev.orig_eidx = cd.orig_eidx.p;
       cd.dev.elim_of_local = cd.elim_of_local.p;
@@ -209,6 +223,7 @@ struct Engine {
       nf_max = std::max(nf_max, static_cast<int>(c.fronts.size()));
       max_m = std::max(max_m, c.max_m);
       v_total_max = std::max(v_total_max, c.v_total);
+      t_total_max = std::max(t_total_max, c.t_total);
       n_max = std::max<long long>(n_max, c.n);
       hc.push_back(cd.dev);
     }
@@ -339,65 +354,42 @@ struct Engine {
   void ensure_solve(int r, int slots) {
     if (r == R && slots <= nslots) return;
     R = r;
-    rg = solve_rhs_group();
-    n_rg = (R + rg - 1) / rg;
+    if (const char* e = std::getenv("HS_BIG_K")) big_k = std::atoi(e);
     nslots = std::max(slots, nslots);
     const int nsub = static_cast<int>(sub_cls.size());
     x.alloc(static_cast<size_t>(n_base[nsub]) * R);
+    x1.alloc(static_cast<size_t>(n_base[nsub]) * R);
     vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
-    flags.alloc(static_cast<size_t>(nsub) * nf_max * n_rg);
-    flags.zero(stream);
-    for (int s = 0; s < nsub; ++s) h_subs[s].x = x.p + n_base[s] * R;
+    tbuf.alloc(static_cast<size_t>(std::max<long long>(t_total_max, 1)) * R * nslots);
+    cnt.alloc(static_cast<size_t>(3) * nslots * nf_max + 2);
+    for (int s = 0; s < nsub; ++s) {
+      h_subs[s].x = x.p + n_base[s] * R;
+      h_subs[s].x1 = x1.p + n_base[s] * R;
+    }
     d_subs.upload(h_subs, stream);
-    // staging rows per task class: bundles (height <= hb) and single upper fronts
-    hb = 2;
-    if (const char* e = std::getenv("HS_BUNDLE_H")) hb = std::atoi(e);
-    int rows_b = 32, rows_u = 32;
-    for (auto& cdp : classes)
-      for (const FrontDesc& fd : cdp->sym->fronts) {
-        const int rows = std::max((fd.m + 7) & ~7, 32 * ((fd.k + 31) / 32));
-        if (fd.height <= hb)
-          rows_b = std::max(rows_b, rows);
-        else
-          rows_u = std::max(rows_u, rows);
-      }
-    smem_bundle = solve_smem_bytes(rows_b, true);
-    smem_upper = solve_smem_bytes(rows_u, true);
-    grid_bundle = solve_grid(smem_bundle);
-    grid_upper = solve_grid(smem_upper);
   }
 
-  // Dataflow task lists of the subdomains `group` (slot = position): forward = every low
-  // subtree of height <= hb as one bundle task, then the upper fronts by height; backward =
-  // upper fronts by depth, then the bundles (hs_solve.cu).
-  // Returns the number of bundle tasks (fwd = bundles then uppers, bwd = uppers then bundles).
-  int build_tasks(const std::vector<int>& group, std::vector<SolveTask>& fwd, std::vector<SolveTask>& bwd) const {
+  // Work items of the subdomains `group` (slot = position in the group), for the current R:
+  // forward = for every front by height, its 32-position gathers then its 32-row blocks per
+  // RHS group; backward = for every front by depth, its 32-column panels per RHS group.
+  void build_items(const std::vector<int>& group, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
     int hmax = 0, dmax = 0;
     for (int id : group) {
       hmax = std::max(hmax, classes[sub_cls[id]]->sym->max_height);
       dmax = std::max(dmax, classes[sub_cls[id]]->sym->max_depth);
     }
-    std::vector<SolveTask> bundles;
-    for (size_t g = 0; g < group.size(); ++g) {
-      const SymbolicClass& c = *classes[sub_cls[group[g]]]->sym;
-      std::vector<int> size(c.fronts.size(), 1);
-      for (size_t f = 0; f < c.fronts.size(); ++f)
-        for (int ch : c.fronts[f].child)
-          if (ch >= 0) size[f] += size[ch];
-      for (size_t f = 0; f < c.fronts.size(); ++f) {
-        const FrontDesc& fd = c.fronts[f];
-        if (fd.height > hb) continue;
-        if (fd.parent >= 0 && c.fronts[fd.parent].height <= hb) continue;
-        bundles.push_back(SolveTask{group[g], static_cast<int>(f) - size[f] + 1, static_cast<int>(f), static_cast<int>(g)});
-      }
-    }
-    fwd.insert(fwd.end(), bundles.begin(), bundles.end());
-    for (int h = hb + 1; h <= hmax; ++h)
+    for (int h = 0; h <= hmax; ++h)
       for (size_t g = 0; g < group.size(); ++g) {
         const SymbolicClass& c = *classes[sub_cls[group[g]]]->sym;
         if (h > c.max_height) continue;
-        for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q)
-          fwd.push_back(SolveTask{group[g], c.order_up[q], c.order_up[q], static_cast<int>(g)});
+        for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
+          const int f = c.order_up[q];
+          const FrontDesc& fd = c.fronts[f];
+          const int nrb = (fd.m + 31) / 32, rw = solve_rhs_width(fd.k, R, big_k);
+          for (int pb = 0; pb < nrb; ++pb) fwd.push_back(SolveItem{group[g], f, 0, pb, static_cast<int>(g), 0, R, 0});
+          for (int rb = 0; rb < nrb; ++rb)
+            for (int r0 = 0; r0 < R; r0 += rw) fwd.push_back(SolveItem{group[g], f, 1, rb, static_cast<int>(g), r0, rw, 0});
+        }
       }
     for (int d = 0; d <= dmax; ++d)
       for (size_t g = 0; g < group.size(); ++g) {
@@ -405,47 +397,66 @@ struct Engine {
         if (d > cd.sym->max_depth) continue;
         for (int q = cd.level_start_down[d]; q < cd.level_start_down[d + 1]; ++q) {
           const int f = cd.sym->order_down[q];
-          if (cd.sym->fronts[f].height > hb) bwd.push_back(SolveTask{group[g], f, f, static_cast<int>(g)});
+          const FrontDesc& fd = cd.sym->fronts[f];
+          const int rw = solve_rhs_width(fd.k, R, big_k);
+          for (int J = 0; J < (fd.k + 31) / 32; ++J)
+            for (int r0 = 0; r0 < R; r0 += rw) bwd.push_back(SolveItem{group[g], f, 2, J, static_cast<int>(g), r0, rw, 0});
         }
       }
-    bwd.insert(bwd.end(), bundles.begin(), bundles.end());
-    return static_cast<int>(bundles.size());
   }
 
-  SolveArgs solve_args(const SolveTask* tasks, int ntasks, unsigned* queue, const unsigned* nzmask,
-                       unsigned epoch_off) const {
+  // One forward and one backward launch over the items of a step group.
+  DBuf<unsigned long long> trace;
+  void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const unsigned* nzmask,
+                 bool traced = false) {
+    const long long per = static_cast<long long>(nslots) * nf_max;
+    HS_CUDA(cudaMemsetAsync(cnt.p, 0, (3 * per + 2) * sizeof(int), stream));
     SolveArgs a{};
-    a.tasks = tasks;
-    a.ntasks = ntasks;
-    a.n_rg = n_rg;
     a.R = R;
-    a.queue = queue;
-    a.flags = flags.p;
+    a.big_k = big_k;
     a.nf_max = nf_max;
-    a.epoch_base = epoch.p;
-    a.epoch_off = epoch_off;
     a.cls = d_cls.p;
     a.subs = d_subs.p;
     a.vbuf = vbuf.p;
     a.vslot_stride = v_total_max * R;
+    a.tbuf = tbuf.p;
+    a.tslot_stride = t_total_max * R;
     a.nzmask = nzmask;
-    return a;
-  }
-
-  // Forward: bundles then upper fronts; backward: upper fronts then bundles. Four persistent
-  // launches, queue[0..3], epochs epoch_off (forward) and epoch_off + 1 (backward).
-  void run_solve(const SolveTask* fwd, const SolveTask* bwd, int nbundle, int nupper, unsigned* queue,
-                 const unsigned* nzmask, unsigned epoch_off) {
-    auto go = [&](const SolveTask* t, int n, unsigned* qc, bool f, bool bundle) {
-      if (n == 0) return;
-      SolveArgs a = solve_args(t, n, qc, nzmask, f ? epoch_off : epoch_off + 1);
-      const int grid = std::max(1, std::min(bundle ? grid_bundle : grid_upper, n * n_rg));
-      launch_solve(a, f, grid, bundle ? smem_bundle : smem_upper, stream);
-    };
-    go(fwd, nbundle, queue + 0, true, true);
-    go(fwd + nbundle, nupper, queue + 1, true, false);
-    go(bwd, nupper, queue + 2, false, false);
-    go(bwd + nupper, nbundle, queue + 3, false, true);
+    a.cnt_stride = per;
+    a.items = fwd;
+    a.nitems = nfwd;
+    a.cnt = cnt.p;
+    a.queue = reinterpret_cast<unsigned*>(cnt.p + 3 * per);
+    if (traced) {  // developer instrumentation (HS_TRACE): per-item timestamps of this step
+      trace.alloc(static_cast<size_t>(4) * (nfwd + nbwd));
+      HS_CUDA(cudaMemsetAsync(trace.p, 0, trace.n * sizeof(unsigned long long), stream));
+      a.trace = trace.p;
+    }
+    launch_solve(a, true, stream);
+    a.items = bwd;
+    a.nitems = nbwd;
+    a.cnt = cnt.p + 2 * per;
+    a.queue = reinterpret_cast<unsigned*>(cnt.p + 3 * per + 1);
+    if (traced) a.trace = trace.p + 4LL * nfwd;
+    launch_solve(a, false, stream);
+    if (traced) {
+      std::vector<unsigned long long> h(trace.n);
+      std::vector<SolveItem> items(nfwd + nbwd);
+      HS_CUDA(cudaMemcpyAsync(h.data(), trace.p, h.size() * 8, cudaMemcpyDeviceToHost, stream));
+      HS_CUDA(cudaMemcpyAsync(items.data(), fwd, nfwd * sizeof(SolveItem), cudaMemcpyDeviceToHost, stream));
+      HS_CUDA(cudaMemcpyAsync(items.data() + nfwd, bwd, nbwd * sizeof(SolveItem), cudaMemcpyDeviceToHost, stream));
+      HS_CUDA(cudaStreamSynchronize(stream));
+      if (FILE* fp = std::fopen(std::getenv("HS_TRACE"), "w")) {
+        std::fprintf(fp, "pass,sub,front,kind,idx,r0,rw,t_deq,t_ready,t_done,sm,k,m\n");
+        for (int i = 0; i < nfwd + nbwd; ++i) {
+          const SolveItem& it = items[i];
+          const FrontDesc& fd = classes[sub_cls[it.sub]]->sym->fronts[it.front];
+          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, it.sub, it.front,
+                       it.kind, it.idx, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k, fd.m);
+        }
+        std::fclose(fp);
+      }
+    }
   }
 };
 
@@ -472,10 +483,10 @@ __global__ void scatter_out_kernel(const double2* src, double2* dst, const int* 
 struct FactorHandle {
   Engine eng;
   hs_factor_stats stats{};
-  std::vector<SolveTask> fwd, bwd;
-  int nbundle = 0;
-  DBuf<SolveTask> d_fwd, d_bwd;
-  DBuf<unsigned> queue, nz;
+  std::vector<SolveItem> fwd, bwd;
+  int items_R = 0;
+  DBuf<SolveItem> d_fwd, d_bwd;
+  DBuf<unsigned> nz;
   DBuf<double2> io;
 };
 
@@ -518,6 +529,14 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
   for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
     const int R = std::min(kMaxRhs, nrhs - b0);
     eng.ensure_solve(R, 1);
+    if (H.items_R != R) {  // item lists depend on the RHS grouping
+      H.fwd.clear();
+      H.bwd.clear();
+      eng.build_items({0}, H.fwd, H.bwd);
+      H.d_fwd.upload(H.fwd, eng.stream);
+      H.d_bwd.upload(H.bwd, eng.stream);
+      H.items_R = R;
+    }
     if (user) {
       cudaEvent_t ev;
       HS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -533,9 +552,7 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
     HS_CUDA(cudaGetLastError());
     const unsigned mask = R >= 32 ? ~0u : ((1u << R) - 1u);
     HS_CUDA(cudaMemcpyAsync(H.nz.p, &mask, sizeof(unsigned), cudaMemcpyHostToDevice, eng.stream));
-    HS_CUDA(cudaMemsetAsync(H.queue.p, 0, 4 * sizeof(unsigned), eng.stream));
-    launch_bump_epoch(eng.epoch.p, 4, eng.stream);
-    eng.run_solve(H.d_fwd.p, H.d_bwd.p, H.nbundle, static_cast<int>(H.fwd.size()) - H.nbundle, H.queue.p, H.nz.p, 1);
+    eng.run_solve(H.d_fwd.p, static_cast<int>(H.fwd.size()), H.d_bwd.p, static_cast<int>(H.bwd.size()), H.nz.p);
     scatter_out_kernel<<<blocks, threads, 0, eng.stream>>>(eng.x.p, xb, eng.classes[0]->elim_of_local.p, n, R);
     g_kernel_launches.fetch_add(1);
     HS_CUDA(cudaGetLastError());
@@ -590,10 +607,6 @@ int hs_factorize(int dim, const int lo[3], const int hi[3], int64_t n, const int
     H.eng.upload_classes(-1);
     H.eng.factorize({&v});
     const SymbolicClass& c = *H.eng.classes[0]->sym;
-    H.nbundle = H.eng.build_tasks({0}, H.fwd, H.bwd);
-    H.d_fwd.upload(H.fwd, H.eng.stream);
-    H.d_bwd.upload(H.bwd, H.eng.stream);
-    H.queue.alloc(4);
     H.nz.alloc(1);
     HS_CUDA(cudaStreamSynchronize(H.eng.stream));
     H.stats.n = n;
@@ -656,7 +669,6 @@ struct SubHost {
   int cls = 0;
 };
 
-constexpr unsigned kEpochSpan = 1u << 16;
 
 }  // namespace
 
@@ -679,16 +691,16 @@ struct DdmHandle {
   int steps = 0, ndir = 4, dirs = 4, max_group = 1;
   long long line_max = 1;
   std::vector<std::vector<int>> groups;  // [di * steps + s-1]
-  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt, nbundle;
+  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
   DBuf<int> d_groups;
-  DBuf<SolveTask> d_tasks;
+  DBuf<SolveItem> d_tasks;
   DBuf<double2> d_coef;
   // per (R, rounds) state
   int R = 0, nsweeps = 0, rounds = 0;
   std::vector<Vec3i> plan;
   std::vector<int> route_h;
   DBuf<double2> mbox;
-  DBuf<unsigned> mpres, nzmask, queue;
+  DBuf<unsigned> mpres, nzmask;
   DBuf<int> route;
   DBuf<double2> bN, u, io;
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
@@ -706,6 +718,7 @@ struct DdmHandle {
 
   void build(const hs_problem& P, int device);
   void ensure_state(int r, int nrounds);
+  void build_items();
   void ensure_gop();
   void run(int nrounds, bool track, bool timed);
   void reports(int nrounds, bool track, hs_solve_report* out);
@@ -911,14 +924,8 @@ void DdmHandle::build(const hs_problem& P, int device) {
   ndir = 1 << dim;
   const std::vector<Vec3i> dirs_plan = sweep_plan(dim, 1);
   std::vector<int> gflat;
-  std::vector<SolveTask> tasks;
   groups.assign(ndir * steps, {});
   grp_off.assign(ndir * steps, 0);
-  fwd_off.assign(ndir * steps, 0);
-  fwd_cnt.assign(ndir * steps, 0);
-  bwd_off.assign(ndir * steps, 0);
-  bwd_cnt.assign(ndir * steps, 0);
-  nbundle.assign(ndir * steps, 0);
   for (int di = 0; di < ndir; ++di)
     for (int s = 1; s <= steps; ++s) {
       const int gi = di * steps + s - 1;
@@ -927,18 +934,30 @@ void DdmHandle::build(const hs_problem& P, int device) {
       max_group = std::max(max_group, static_cast<int>(groups[gi].size()));
       grp_off[gi] = static_cast<int>(gflat.size());
       gflat.insert(gflat.end(), groups[gi].begin(), groups[gi].end());
-      std::vector<SolveTask> fw, bw;
-      nbundle[gi] = eng.build_tasks(groups[gi], fw, bw);
-      fwd_off[gi] = static_cast<int>(tasks.size());
-      fwd_cnt[gi] = static_cast<int>(fw.size());
-      tasks.insert(tasks.end(), fw.begin(), fw.end());
-      bwd_off[gi] = static_cast<int>(tasks.size());
-      bwd_cnt[gi] = static_cast<int>(bw.size());
-      tasks.insert(tasks.end(), bw.begin(), bw.end());
     }
   d_groups.upload(gflat, eng.stream);
-  d_tasks.upload(tasks, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
+}
+
+// Work items of every (sweep direction, step) group for the current batch width.
+void DdmHandle::build_items() {
+  std::vector<SolveItem> tasks;
+  const int ng = static_cast<int>(groups.size());
+  fwd_off.assign(ng, 0);
+  fwd_cnt.assign(ng, 0);
+  bwd_off.assign(ng, 0);
+  bwd_cnt.assign(ng, 0);
+  for (int gi = 0; gi < ng; ++gi) {
+    std::vector<SolveItem> fw, bw;
+    eng.build_items(groups[gi], fw, bw);
+    fwd_off[gi] = static_cast<int>(tasks.size());
+    fwd_cnt[gi] = static_cast<int>(fw.size());
+    tasks.insert(tasks.end(), fw.begin(), fw.end());
+    bwd_off[gi] = static_cast<int>(tasks.size());
+    bwd_cnt[gi] = static_cast<int>(bw.size());
+    tasks.insert(tasks.end(), bw.begin(), bw.end());
+  }
+  d_tasks.upload(tasks, eng.stream);
 }
 
 void DdmHandle::ensure_state(int r, int nrounds) {
@@ -947,8 +966,12 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   const int ns = nrounds * ndir;
   if (ns > HS_MAX_SWEEPS || nrounds > HS_MAX_ROUNDS) config_error("ddm_solve: too many rounds");
   eng.ensure_solve(r, max_group);
-  if (r == R && nrounds == rounds) return;
-  R = r;
+  const bool changed = r != R || nrounds != rounds;
+  if (r != R) {
+    R = r;
+    build_items();
+  }
+  if (!changed) return;
   rounds = nrounds;
   nsweeps = ns;
   plan = sweep_plan(dim, nrounds);
@@ -960,7 +983,6 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   mbox.alloc(static_cast<size_t>(nsub) * nsweeps * dirs * 2 * line_max * R);
   mpres.alloc(static_cast<size_t>(nsub) * nsweeps * dirs);
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
-  queue.alloc(static_cast<size_t>(nsweeps) * steps * 4);
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
   const long long nb = (geom.gn * R + 255) / 256;
@@ -997,8 +1019,6 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
   HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
   HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(unsigned), s));
   HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(unsigned), s));
-  HS_CUDA(cudaMemsetAsync(queue.p, 0, queue.n * sizeof(unsigned), s));
-  launch_bump_epoch(eng.epoch.p, kEpochSpan, s);
   if (timed) HS_CUDA(cudaEventRecord(ev[0], s));
   SweepArgs sa{};
   sa.g = geom;
@@ -1021,12 +1041,10 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
       sa.group = d_groups.p + grp_off[gi];
       sa.ngroup = static_cast<int>(groups[gi].size());
       launch_build_rhs(sa, eng.n_max, s);
-      const int qi = ((l - 1) * steps + (st - 1)) * 4;
-      const unsigned off = 1u + static_cast<unsigned>(qi);
       const unsigned* nz = nzmask.p + static_cast<size_t>(l - 1) * nsub;
       if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
-      eng.run_solve(d_tasks.p + fwd_off[gi], d_tasks.p + bwd_off[gi], nbundle[gi], fwd_cnt[gi] - nbundle[gi],
-                    queue.p + qi, nz, off);
+      const bool traced = std::getenv("HS_TRACE") && l == 1 && st == (steps + 1) / 2;
+      eng.run_solve(d_tasks.p + fwd_off[gi], fwd_cnt[gi], d_tasks.p + bwd_off[gi], bwd_cnt[gi], nz, traced);
       if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
       launch_extract_deposit(sa, static_cast<int>(line_max), s);
     }

@@ -14,13 +14,14 @@ struct DevFront {
   int k, m, sep_off, bnd_off;
   int parent, child0, child1, cmap0, cmap1;
   int orig_off, orig_cnt, pad_;
-  long long fac_off, v_off, f_off;
+  long long fac_off, v_off, f_off, t_off;
 };
 
 struct DevClass {
   const DevFront* fronts;
   const int* bnd_elim;
   const int* child_map;
+  const int2* pmap;           // per front position (offset t_off): row of child0 / child1 update, -1 if none
   const int* orig_fpos;
   const int* orig_eidx;
   const int* elim_of_local;
@@ -43,7 +44,8 @@ struct DevSub {
   double2* factor;            // panels (hs_symbolic.hpp)
   double2* dinv;              // 1/d, elimination order
   const double2* val;         // CSR values (factorization input)
-  double2* x;                 // solve vector, elimination order, node-major x R
+  double2* x;                 // solve vector, elimination order, node-major x R (rhs -> solution)
+  double2* x1;                // forward result z = D^-1 L^-1 b (same layout)
   const double2* coef[kMaxDirs];  // injection couplings per incoming direction
 };
 
@@ -58,10 +60,11 @@ struct DevGeom {
   long long gn;               // global node count
 };
 
-// A solve task: the postorder front range [f0, f1] of one subdomain (a whole low subtree
-// "bundle", or a single upper front when f0 == f1) and its update-vector slot.
-struct SolveTask {
-  int sub, f0, f1, slot;
+// A solve work item (hs_solve.cu). kind 0: forward gather of 32 front positions (block idx);
+// kind 1: forward 32-row block idx of [M; W]; kind 2: backward 32-column panel idx. RHS
+// columns [r0, r0 + rw). slot = position of the subdomain in its step group.
+struct SolveItem {
+  int sub, front, kind, idx, slot, r0, rw, pad_;
 };
 
 struct FactorTask {

@@ -218,26 +218,29 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
     }
   }
   __syncthreads();
-  // [M; W] as 32x32 chunks in row-block-major order (chunk (rb, J) for J <= min(rb, np-1)),
-  // rows padded to a multiple of 8, each chunk column-major with the XOR-8 row swizzle.
+  // [M; W] stored twice (hs_solve.cu): copy F for the forward, row blocks rb of 32 rows,
+  // each holding chunks J = 0..min(rb, np-1) column-major (element (il, j) at j*rc + il);
+  // copy B for the backward, panels J of 32 columns holding rows [32J, m) row-major.
   {
-    const int m_pad = (m + 7) & ~7, nrb = (m_pad + 31) >> 5, np = (k + 31) >> 5;
+    const int nrb = (m + 31) >> 5, np = (k + 31) >> 5;
+    auto val = [&](int row, int col) {
+      if (row >= m || col >= k) return czero();
+      if (row >= k || row > col) return F[static_cast<long long>(col) * m + row];
+      return row == col ? make_double2(1.0, 0.0) : czero();
+    };
     double2* P = S.factor + f.fac_off;
     for (int rb = 0; rb < nrb; ++rb) {
-      const int rc = min(32, m_pad - 32 * rb), nj = min(rb, np - 1) + 1;
+      const int rc = min(32, m - 32 * rb), nj = min(rb, np - 1) + 1;
       for (int idx = tid; idx < nj * rc * 32; idx += kThreads) {
         const int J = idx / (rc * 32), rem = idx % (rc * 32), j = rem / rc, il = rem % rc;
-        const int row = 32 * rb + il, col = 32 * J + j;
-        double2 v = czero();
-        if (row < m && col < k) {
-          if (row >= k || row > col)
-            v = F[static_cast<long long>(col) * m + row];
-          else if (row == col)
-            v = make_double2(1.0, 0.0);
-        }
-        P[J * rc * 32 + j * rc + ((il & ~7) | ((il ^ j) & 7))] = v;
+        P[idx] = val(32 * rb + il, 32 * J + j);
       }
       P += static_cast<long long>(nj) * rc * 32;
+    }
+    for (int J = 0; J < np; ++J) {
+      const int rows = m - 32 * J;
+      for (int idx = tid; idx < rows * 32; idx += kThreads) P[idx] = val(32 * J + idx / 32, 32 * J + idx % 32);
+      P += static_cast<long long>(rows) * 32;
     }
   }
 }

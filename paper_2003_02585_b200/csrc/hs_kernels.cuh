@@ -6,28 +6,28 @@
 namespace hsb {
 
 struct SolveArgs {
-  const SolveTask* tasks;
-  int ntasks;      // tasks (each expands to n_rg RHS-group tasks)
-  int n_rg;        // RHS groups
-  int R;           // RHS per batch (x / V row stride)
-  unsigned* queue; // dynamic task counter (zeroed before launch)
-  unsigned* flags; // completion epochs [(sub * nf_max + front) * n_rg + rg]
+  const SolveItem* items;
+  int nitems;
+  int R;           // RHS per batch (row stride of x / V / T)
+  int big_k;       // fronts with k >= big_k are split into 4-RHS items
+  int* cnt;        // completion counters [slot * nf_max + front]: [0] gathers / panels, [1] row blocks
+  long long cnt_stride;  // elements between the two counter arrays
+  unsigned* queue; // dynamic item counter, zeroed per launch
+  unsigned long long* trace;  // optional per-item timestamps [4 * item]: dequeue, ready, done, smid
   int nf_max;
-  const unsigned* epoch_base;
-  unsigned epoch_off;
   const DevClass* cls;
   const DevSub* subs;
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
+  double2* tbuf;           // forward front inputs [x_sep + child updates; bnd updates] per slot
+  long long tslot_stride;
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
 };
 
-// Multifrontal forward (L z = b, then z *= D^-1) or backward (L^T x = z) pass over the
-// tasks of one step group (src/direct.cpp:290-325); hs_solve.cu.
-void launch_solve(const SolveArgs& a, bool fwd, int grid, size_t smem, cudaStream_t s);
-size_t solve_smem_bytes(int max_m, bool fwd);
-int solve_grid(size_t smem);
-int solve_rhs_group();
+// Multifrontal forward (z = D^-1 L^-1 b) or backward (x = L^-T z) pass over the work items of
+// one step group (src/direct.cpp:290-325); hs_solve.cu.
+void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s);
+int solve_rhs_width(int k, int R, int big_k);
 
 struct FactorArgs {
   const FactorTask* tasks;

@@ -1,27 +1,30 @@
 // Multifrontal forward / backward solves of the helmsweep hot path on sm_100a
 // (Factorization::solve_inplace, /root/reference/proj/src/direct.cpp:290-325), batched over
-// every subdomain of a sweep step group and 16 right-hand sides per task.
+// every subdomain of a sweep step group and the RHS of the batch.
 //
 // Partitioned inverse: the factorization stores, per front, M = L11^-1 (unit lower) and
 // W = L21 M instead of L11 / L21 (hs_kernels.cu). The reference's per-front operations
 //   forward   t = L11^-1 x[sep]; x[bnd] -= L21 t          (direct.cpp:296-307)
 //   backward  x[sep] = L11^-T (x[sep] - L21^T x[bnd])     (direct.cpp:311-324)
-// become dense products with no serial dependency inside a front:
-//   forward   [x_sep; u] = [M; W] x_sep,  x[sep] = D^-1 x_sep,  V = (children's bnd) - u
+// become dense products without any serial dependency inside a front:
+//   forward   [z_sep; u] = [M; W] x_sep,  z = D^-1 z_sep (direct.cpp:309),  V = bnd updates - u
 //   backward  x_sep = [M; W]^T [z_sep; -x_bnd]
+// Work items (one warp each, no CTA barriers):
+//   kind 0  forward gather of 32 front positions: T = [rhs_sep; 0] + child0 V + child1 V
+//           (the extend-add, in the reference's child order, src/direct.cpp:239-265);
+//   kind 1  forward 32-row block of [M; W] x T_sep for rw RHS (lane = row);
+//   kind 2  backward 32-column panel of [M; W]^T y for rw RHS (lane = column).
+// Fronts with k >= big_k use 4-RHS items (4x more warps on the long upper-tree critical
+// path), the others 16-RHS items (each factor byte read once for 16 RHS). Items are listed in
+// topological order and dequeued greedily; dependencies are per-front completion counters
+// (relaxed spin, one acquire, release increments). A warp dequeues only while running and
+// every dependency sits earlier in the list, so the launch cannot deadlock; every reduction
+// has a fixed order, so results are bitwise reproducible.
 //
-// One persistent launch per pass and task class. Tasks are either a whole low subtree
-// ("bundle", processed in postorder by one CTA) or one upper front; they are dequeued in
-// topological order and synchronise through per-(front, RHS group) completion epochs
-// (release/acquire at gpu scope): deadlock-free and deterministic (fixed reduction orders).
-//
-// CTA = 8 consumer warps + 1 producer warp. The producer streams the task's factor chunks
-// (<= 32 rows x 32 columns, <= 16 KB) into a 4-slot shared-memory ring with cp.async.bulk
-// (TMA bulk copies) completing on full/empty mbarriers; consumers never issue factor loads.
-// Chunks are column-major with an XOR-8 row swizzle, so both the forward pattern (lanes =
-// rows) and the backward pattern (lanes = columns) are free of bank conflicts. Consumer warp
-// pairs ("groups") own disjoint outputs: row blocks in the forward, column panels in the
-// backward, each with 8 RHS per thread.
+// Factor streams: copy F (forward, column-major 32-row chunks) and copy B (backward, row-major
+// 32-column panels), coalesced 512-byte warp loads that bypass L1 (ld.global.nc.L1::no_allocate).
+// Vector operands are staged 32 rows at a time into a per-warp shared tile with cp.async.cg
+// (L2, coherent with the producers' release); 4-RHS items double-buffer the tile.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -35,13 +38,8 @@ extern std::atomic<long long> g_kernel_launches;
 
 namespace {
 
-constexpr int kCW = 8;              // consumer warps
-constexpr int kCT = kCW * 32;       // consumer threads
-constexpr int kBlock = kCT + 32;    // + producer warp
-constexpr int kRG = 16;             // RHS per task
-constexpr int kTP = kRG + 1;        // t row pitch
-constexpr int kS = 4;               // ring slots
-constexpr int kChunk = 1024;        // elements per chunk slot (32 x 32)
+constexpr int kThreads = 256;
+constexpr int kTile = 32 * 16;  // double2 per warp tile (8 KB)
 
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
@@ -53,353 +51,344 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ int swz(int il, int j) { return (il & ~7) | ((il ^ j) & 7); }
-
-__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kCT) : "memory"); }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-
-struct Ring {
-  double2* slots;
-  uint64_t* full;
-  uint64_t* empty;
-  volatile unsigned* issued;  // chunks issued so far (monotonic, written by the producer)
-};
-
-// Wait until chunk qq has landed. A group skips the chunks other groups own, so it may reach
-// qq while its slot still holds qq-8: waiting on the full barrier's parity alone would alias
-// that older phase. Observing `issued > qq` first (qq is issued only after qq-4 is released)
-// keeps the waiter at most one phase ahead, which makes the parity wait exact.
-__device__ __forceinline__ const double2* await_chunk(const Ring& rg, unsigned qq) {
-  while (*rg.issued <= qq) {
-  }
-  const int s = qq % kS;
-  mbar_wait(&rg.full[s], (qq / kS) & 1u);
-  return rg.slots + s * kChunk;
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-
-// Chunk geometry of a front's [M; W] stream (hs_kernels.cu factor output): chunk (rb, J)
-// for J <= min(rb, np-1), rb-major, rows padded to 8, rc(rb) rows per row block.
-struct FrontGeom {
-  int m_pad, nrb, np;
-  __device__ explicit FrontGeom(const DevFront& f)
-      : m_pad((f.m + 7) & ~7), nrb((((f.m + 7) & ~7) + 31) >> 5), np((f.k + 31) >> 5) {}
-  __device__ int rc(int rb) const { return min(32, m_pad - 32 * rb); }
-  __device__ int nj(int rb) const { return min(rb, np - 1) + 1; }
-  // element offset of chunk (rb, J); every row block before rb is full (32 rows)
-  __device__ long long off(int rb, int J) const {
-    const long long pre = rb <= np ? static_cast<long long>(rb) * (rb + 1) / 2
-                                   : static_cast<long long>(np) * (np + 1) / 2 + static_cast<long long>(rb - np) * np;
-    return pre * 1024 + static_cast<long long>(J) * rc(rb) * 32;
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
+  if (lane == 0) {
+    while (ld_relaxed(p) < target) __nanosleep(32);
+    (void)ld_acquire(p);
   }
-  __device__ int chunks() const {
-    int c = 0;
-    for (int rb = 0; rb < nrb; ++rb) c += nj(rb);
-    return c;
-  }
-};
-
-// Stream order. Forward: rb-major (storage order); group g owns row blocks rb % 4 == g.
-// Backward: panel quads; inside quad p all row blocks rb >= 4p, J in the quad, J <= rb;
-// group g owns panel J % 4 == g.
-template <bool FWD, class Fn>
-__device__ __forceinline__ void for_each_chunk(const FrontGeom& G, Fn&& fn) {
-  if (FWD) {
-    for (int rb = 0; rb < G.nrb; ++rb)
-      for (int J = 0; J < G.nj(rb); ++J) fn(rb, J);
-  } else {
-    for (int p = 0; 4 * p < G.np; ++p)
-      for (int rb = 4 * p; rb < G.nrb; ++rb)
-        for (int J = 4 * p; J < min(4 * p + 4, G.nj(rb)); ++J) fn(rb, J);
+  __syncwarp();
+}
+__device__ __forceinline__ void signal(int* p, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    red_release_add(p, 1);
   }
 }
-
-// Producer: stream every chunk of the task in consumption order.
-template <bool FWD>
-__device__ void produce(const Ring& rg, const DevClass& C, const DevSub& S, const SolveTask& task, unsigned& q) {
-  const int nfr = task.f1 - task.f0 + 1;
-  for (int fi = 0; fi < nfr; ++fi) {
-    const int f = FWD ? task.f0 + fi : task.f1 - fi;
-    const DevFront fr = C.fronts[f];
-    const FrontGeom G(fr);
-    const double2* base = S.factor + fr.fac_off;
-    for_each_chunk<FWD>(G, [&](int rb, int J) {
-      const unsigned bytes = static_cast<unsigned>(G.rc(rb)) * 32u * 16u;
-      const int s = q % kS;
-      const unsigned ph = (q / kS) & 1u;
-      mbar_wait(&rg.empty[s], ph ^ 1u);
-      mbar_expect_tx(&rg.full[s], bytes);
-      bulk_g2s(rg.slots + s * kChunk, base + G.off(rb, J), bytes, &rg.full[s]);
-      ++q;
-      *rg.issued = q;
-    });
-  }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <bool FWD>
-__device__ void consume(const SolveArgs& a, const Ring& rg, const DevClass& C, const DevSub& S, const SolveTask& task,
-                        int r0, unsigned& q, double2* t) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = warp >> 1, h = warp & 1;
-  const int R = a.R;
-  double2* V = a.vbuf + task.slot * a.vslot_stride;
-  const int nfr = task.f1 - task.f0 + 1;
-  for (int fi = 0; fi < nfr; ++fi) {
-    const int f = FWD ? task.f0 + fi : task.f1 - fi;
-    const DevFront fr = C.fronts[f];
-    const FrontGeom G(fr);
-    const int k = fr.k, m = fr.m;
-    const int rows = max(G.m_pad, 32 * G.np);
-    // gather: forward t = [x[sep]; 0] (+ children below); backward t = [z_sep; -x_bnd]
-    for (int idx = tid; idx < rows * kRG; idx += kCT) {
-      const int e = idx >> 4, r = idx & 15;
-      double2 v = czero();
-      if (r0 + r < R && e < m) {
-        if (e < k) {
-          v = __ldcg(&S.x[static_cast<long long>(fr.sep_off + e) * R + r0 + r]);
-        } else if (!FWD) {
-          v = __ldcg(&S.x[static_cast<long long>(C.bnd_elim[fr.bnd_off + e - k]) * R + r0 + r]);
-          v.x = -v.x;
-          v.y = -v.y;
-        }
-      }
-      t[e * kTP + r] = v;
-    }
-    cbar();
-    if (FWD) {  // extend-add of the children's update vectors, child0 then child1
-#pragma unroll 1
-      for (int cq = 0; cq < 2; ++cq) {
-        const int ch = cq ? fr.child1 : fr.child0;
-        if (ch < 0) continue;
-        const DevFront cf = C.fronts[ch];
-        const int cb = cf.m - cf.k;
-        const int* cmap = C.child_map + (cq ? fr.cmap1 : fr.cmap0);
-        for (int idx = tid; idx < cb * kRG; idx += kCT) {
-          const int i = idx >> 4, r = idx & 15;
-          if (r0 + r < R) {
-            const double2 v = __ldcg(&V[(cf.v_off + i) * R + r0 + r]);
-            double2& y = t[cmap[i] * kTP + r];
-            y.x += v.x;
-            y.y += v.y;
-          }
-        }
-        cbar();
-      }
-    }
-    double2 acc[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r] = czero();
-    unsigned qq = q;  // every consumer walks the whole stream to keep the ring position
-    if (FWD) {
-      // out[rows of rb] = sum_J chunk(rb, J) t[J]; thread = row (lane), 8 RHS per thread
-      for (int rb = 0; rb < G.nrb; ++rb) {
-        const int nj = G.nj(rb), rc = G.rc(rb);
-        if ((rb & 3) != g) {
-          qq += nj;
-          continue;
-        }
-        for (int J = 0; J < nj; ++J, ++qq) {
-          const int s = qq % kS;
-          const double2* ch = await_chunk(rg, qq);
-          if (lane < rc) {
-            const double2* tb = t + (32 * J) * kTP + 8 * h;
+__device__ __forceinline__ int nrb_of(const DevFront& f) { return (f.m + 31) >> 5; }
+__device__ __forceinline__ int np_of(const DevFront& f) { return (f.k + 31) >> 5; }
+__device__ __forceinline__ int rw_of(const DevFront& f, int R, int big_k) { return f.k >= big_k ? min(4, R) : min(16, R); }
+__device__ __forceinline__ int ngroups(const DevFront& f, int R, int big_k) {
+  const int w = rw_of(f, R, big_k);
+  return (R + w - 1) / w;
+}
+// element offset of row block rb in copy F (all earlier row blocks are full)
+__device__ __forceinline__ long long rb_base(int rb, int np) {
+  const long long pre = rb <= np ? static_cast<long long>(rb) * (rb + 1) / 2
+                                 : static_cast<long long>(np) * (np + 1) / 2 + static_cast<long long>(rb - np) * np;
+  return pre * 1024;
+}
+__device__ __forceinline__ long long copy_elems(int m, int k) {
+  const int np = (k + 31) >> 5;
+  return 32LL * (static_cast<long long>(np) * m - 16LL * np * (np - 1));
+}
+
+// kind 0: T[p] = (p < k ? rhs[sep + p] : 0) + child0 V + child1 V for 32 positions, all RHS.
+__device__ void fwd_gather(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, int pb, double2* T,
+                           const double2* V, int lane) {
+  const int R = a.R, p = 32 * pb + lane;
+  if (p >= fr.m) return;
+  const int2 pm = C.pmap[fr.t_off + p];
+  const double2* g0 = p < fr.k ? S.x + static_cast<long long>(fr.sep_off + p) * R : nullptr;
+  const double2* g1 = pm.x >= 0 ? V + (C.fronts[fr.child0].v_off + pm.x) * R : nullptr;
+  const double2* g2 = pm.y >= 0 ? V + (C.fronts[fr.child1].v_off + pm.y) * R : nullptr;
+  double2* t = T + static_cast<long long>(p) * R;
 #pragma unroll 4
-            for (int j = 0; j < 32; ++j) {
-              const double2 L = ch[j * rc + swz(lane, j)];
-              const double2* tj = tb + j * kTP;
-#pragma unroll
-              for (int r = 0; r < 8; ++r) cfma(acc[r], L, tj[r]);
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&rg.empty[s], 4);
-        }
-        const int row = 32 * rb + lane;
-        if (lane < rc && row < m) {
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            if (r0 + 8 * h + r >= R) continue;
-            if (row < k) {  // x[sep] = D^-1 M x_sep (src/direct.cpp:303-309)
-              const long long pos = fr.sep_off + row;
-              __stcg(&S.x[pos * R + r0 + 8 * h + r], cmul(acc[r], S.dinv[pos]));
-            } else {        // V = children's bnd updates - W x_sep (x[bnd] -= L21 t, :306)
-              const double2 tin = t[row * kTP + 8 * h + r];
-              __stcg(&V[(fr.v_off + row - k) * R + r0 + 8 * h + r],
-                     make_double2(tin.x - acc[r].x, tin.y - acc[r].y));
-            }
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) acc[r] = czero();
-      }
-    } else {
-      // x_sep[J] = sum_rb chunk(rb, J)^T [z_sep; -x_bnd][rb]; lane = column, 8 RHS per warp
-      for (int p = 0; 4 * p < G.np; ++p) {
-        for (int rb = 4 * p; rb < G.nrb; ++rb) {
-          const int jend = min(4 * p + 4, G.nj(rb)), rc = G.rc(rb);
-          for (int J = 4 * p; J < jend; ++J, ++qq) {
-            if ((J & 3) != g) continue;
-            const int s = qq % kS;
-            const double2* ch = await_chunk(rg, qq);
-            const int il_hi = min(rc, m - 32 * rb);
-#pragma unroll 2
-            for (int il = 0; il < il_hi; ++il) {
-              const double2 L = ch[lane * rc + swz(il, lane)];
-              const double2* tr = t + (32 * rb + il) * kTP + 8 * h;
-#pragma unroll
-              for (int r = 0; r < 8; ++r) cfma(acc[r], L, tr[r]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rg.empty[s], 4);
-          }
-        }
-        const int J = 4 * p + g;
-        const int col = 32 * J + lane;
-        if (J < G.np && col < k) {
-#pragma unroll
-          for (int r = 0; r < 8; ++r)
-            if (r0 + 8 * h + r < R)
-              __stcg(&S.x[static_cast<long long>(fr.sep_off + col) * R + r0 + 8 * h + r], acc[r]);
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) acc[r] = czero();
-      }
+  for (int r = 0; r < R; ++r) {
+    double2 v = g0 ? __ldcg(g0 + r) : czero();
+    if (g1) {
+      const double2 w = __ldcg(g1 + r);
+      v = make_double2(v.x + w.x, v.y + w.y);
     }
-    q += G.chunks();
-    cbar();
+    if (g2) {
+      const double2 w = __ldcg(g2 + r);
+      v = make_double2(v.x + w.x, v.y + w.y);
+    }
+    __stcg(t + r, v);
   }
 }
 
-template <bool FWD>
-__global__ void __launch_bounds__(kBlock, 2) solve3_kernel(SolveArgs a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bar_full[kS], bar_empty[kS];
-  __shared__ int s_task;
-  __shared__ unsigned s_issued;
-  double2* ring = reinterpret_cast<double2*>(smraw);
-  double2* t = ring + kS * kChunk;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    s_issued = 0;
-    for (int s = 0; s < kS; ++s) {
-      mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], kCW);
+// Stage rows [0, nrows) (row l at src(l) .. + RW) into tile[32][RW]; rows >= nrows zero.
+template <int RW, class Src>
+__device__ __forceinline__ void stage(double2* tile, int nrows, int nr, int lane, Src&& src) {
+  double2* dst = tile + lane * RW;
+  if (lane < nrows) {
+    const double2* g = src(lane);
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      if (r < nr)
+        cp_async16(dst + r, g + r);
+      else
+        dst[r] = czero();
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  } else {
+#pragma unroll
+    for (int r = 0; r < RW; ++r) dst[r] = czero();
   }
-  __syncthreads();
-  const Ring rg{ring, bar_full, bar_empty, &s_issued};
-  const unsigned epoch = *a.epoch_base + a.epoch_off;
-  const int total = a.ntasks * a.n_rg;
-  unsigned q = 0;  // ring position (identical sequence in producer and consumers)
-  const bool producer = tid >= kCT;
-  for (;;) {
-    if (tid == 0) s_task = static_cast<int>(atomicAdd(a.queue, 1u));
-    __syncthreads();
-    const int tk = s_task;
-    __syncthreads();
-    if (tk >= total) break;
-    const SolveTask task = a.tasks[tk / a.n_rg];
-    const int rgi = tk % a.n_rg;
-    if (a.nzmask[task.sub] == 0) continue;  // skipped subdomain: nothing depends on it
-    const DevSub& S = a.subs[task.sub];
-    const DevClass& C = a.cls[S.cls];
-    if (producer) {
-      if (tid == kCT) produce<FWD>(rg, C, S, task, q);
-      __syncwarp();  // reconverge the producer warp before the next CTA barrier
-      continue;
-    }
-    unsigned* fl = a.flags + static_cast<long long>(task.sub) * a.nf_max * a.n_rg + rgi;
-    if (tid == 0) {
-      if (FWD) {
-        for (int f = task.f0; f <= task.f1; ++f) {
-          const DevFront fr = C.fronts[f];
-          if (fr.child0 >= 0 && fr.child0 < task.f0)
-            while (ld_acquire(fl + static_cast<long long>(fr.child0) * a.n_rg) != epoch) __nanosleep(32);
-          if (fr.child1 >= 0 && fr.child1 < task.f0)
-            while (ld_acquire(fl + static_cast<long long>(fr.child1) * a.n_rg) != epoch) __nanosleep(32);
-        }
-      } else {
-        const int p = C.fronts[task.f1].parent;
-        if (p >= 0)
-          while (ld_acquire(fl + static_cast<long long>(p) * a.n_rg) != epoch) __nanosleep(32);
-      }
-      __threadfence();
+  cp_commit();
+}
+
+// kind 1: out[row] = sum_j [M; W][row, j] T_sep[j] for RHS [r0, r0 + RW)
+template <int RW>
+__device__ void fwd_block(const SolveArgs& a, const DevSub& S, const DevFront& fr, int rb, const double2* T, double2* V,
+                          int r0, int nr, int lane, double2* tiles) {
+  constexpr int NB = kTile / (32 * RW) >= 2 ? 2 : 1;  // double buffer when the tile allows
+  const int R = a.R, m = fr.m, k = fr.k, np = np_of(fr);
+  const int rc = min(32, m - 32 * rb), nj = min(rb, np - 1) + 1;
+  const double2* P = S.factor + fr.fac_off + rb_base(rb, np);
+  double2 acc[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r] = czero();
+  const bool active = lane < rc;
+  auto src_of = [&](int J) {
+    return [=](int l) { return T + static_cast<long long>(32 * J + l) * R + r0; };
+  };
+  stage<RW>(tiles, min(32, k), nr, lane, src_of(0));
+  for (int J = 0; J < nj; ++J) {
+    double2* tile = tiles + (J % NB) * 32 * RW;
+    if (NB == 2 && J + 1 < nj) {
+      stage<RW>(tiles + ((J + 1) % NB) * 32 * RW, min(32, k - 32 * (J + 1)), nr, lane, src_of(J + 1));
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
     }
     __syncwarp();
-    cbar();
-    consume<FWD>(a, rg, C, S, task, rgi * kRG, q, t);
-    if (tid == 0) {
-      __threadfence();
-      st_release(fl + static_cast<long long>(task.f1) * a.n_rg, epoch);
+    const double2* ch = P + static_cast<long long>(J) * rc * 32;
+    const int jmax = min(32, k - 32 * J);
+    int j = 0;
+    for (; j + 8 <= jmax; j += 8) {
+      double2 L[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) L[u] = active ? ld_stream(ch + (j + u) * rc + lane) : czero();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2* xr = tile + (j + u) * RW;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) cfma(acc[r], L[u], xr[r]);
+      }
+    }
+    for (; j < jmax; ++j) {
+      const double2 L = active ? ld_stream(ch + j * rc + lane) : czero();
+      const double2* xr = tile + j * RW;
+#pragma unroll
+      for (int r = 0; r < RW; ++r) cfma(acc[r], L, xr[r]);
+    }
+    __syncwarp();
+    if (NB == 1 && J + 1 < nj) stage<RW>(tiles, min(32, k - 32 * (J + 1)), nr, lane, src_of(J + 1));
+  }
+  if (!active) return;
+  const int row = 32 * rb + lane;
+  if (row < k) {  // z_sep = D^-1 M x_sep
+    const long long pos = fr.sep_off + row;
+    const double2 d = S.dinv[pos];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+      if (r < nr) __stcg(&S.x1[pos * R + r0 + r], cmul(acc[r], d));
+  } else {        // V = (children's bnd updates) - W x_sep
+    const double2* t = T + static_cast<long long>(row) * R + r0;
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+      if (r < nr) {
+        const double2 w = __ldcg(t + r);
+        __stcg(&V[(fr.v_off + row - k) * R + r0 + r], make_double2(w.x - acc[r].x, w.y - acc[r].y));
+      }
+  }
+}
+
+// kind 2: x_sep[col] = sum_i [M; W][i, col] [z_sep; -x_bnd][i] for RHS [r0, r0 + RW)
+template <int RW>
+__device__ void bwd_panel(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, int J, int r0,
+                          int nr, int lane, double2* tiles) {
+  constexpr int NB = kTile / (32 * RW) >= 2 ? 2 : 1;
+  const int R = a.R, m = fr.m, k = fr.k;
+  const double2* P = S.factor + fr.fac_off + copy_elems(m, k) + 32LL * (static_cast<long long>(J) * m - 16LL * J * (J - 1));
+  double2 acc[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r] = czero();
+  auto src_of = [&](int i0) {
+    return [=](int l) {
+      const int ii = i0 + l;
+      const long long pos = ii < k ? static_cast<long long>(fr.sep_off + ii)
+                                   : static_cast<long long>(C.bnd_elim[fr.bnd_off + ii - k]);
+      return (ii < k ? S.x1 : S.x) + pos * R + r0;
+    };
+  };
+  const int nbt = (m - 32 * J + 31) / 32;
+  stage<RW>(tiles, min(32, m - 32 * J), nr, lane, src_of(32 * J));
+  for (int b = 0; b < nbt; ++b) {
+    const int i0 = 32 * J + 32 * b;
+    const int nrow = min(32, m - i0);
+    double2* tile = tiles + (b % NB) * 32 * RW;
+    if (NB == 2 && b + 1 < nbt) {
+      stage<RW>(tiles + ((b + 1) % NB) * 32 * RW, min(32, m - i0 - 32), nr, lane, src_of(i0 + 32));
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    if (i0 + lane >= k && lane < nrow) {  // bnd rows enter as -x_bnd
+#pragma unroll
+      for (int r = 0; r < RW; ++r) tile[lane * RW + r] = make_double2(-tile[lane * RW + r].x, -tile[lane * RW + r].y);
+    }
+    __syncwarp();
+    const double2* Pb = P + static_cast<long long>(i0 - 32 * J) * 32;
+    int u0 = 0;
+    for (; u0 + 8 <= nrow; u0 += 8) {
+      double2 L[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) L[u] = ld_stream(Pb + (u0 + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2* y = tile + (u0 + u) * RW;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) cfma(acc[r], L[u], y[r]);
+      }
+    }
+    for (; u0 < nrow; ++u0) {
+      const double2 L = ld_stream(Pb + u0 * 32 + lane);
+      const double2* y = tile + u0 * RW;
+#pragma unroll
+      for (int r = 0; r < RW; ++r) cfma(acc[r], L, y[r]);
+    }
+    __syncwarp();
+    if (NB == 1 && b + 1 < nbt) stage<RW>(tiles, min(32, m - i0 - 32), nr, lane, src_of(i0 + 32));
+  }
+  const int col = 32 * J + lane;
+  if (col < k) {
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+      if (r < nr) __stcg(&S.x[static_cast<long long>(fr.sep_off + col) * R + r0 + r], acc[r]);
+  }
+}
+
+template <bool FWD>
+__global__ void __launch_bounds__(kThreads, 2) solve5_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double2 smem_tiles[];
+  const int lane = threadIdx.x & 31;
+  double2* tiles = smem_tiles + (threadIdx.x >> 5) * kTile;
+  const int R = a.R;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = static_cast<int>(atomicAdd(a.queue, 1u));
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.nitems) break;
+    const SolveItem item = a.items[it];
+    if (a.nzmask[item.sub] == 0) continue;  // skipped subdomain: nothing depends on it
+    unsigned long long* tr = a.trace ? a.trace + 4LL * it : nullptr;
+    if (tr && lane == 0) tr[0] = gtime();
+    const DevSub& S = a.subs[item.sub];
+    const DevClass& C = a.cls[S.cls];
+    const DevFront fr = C.fronts[item.front];
+    const long long cbase = static_cast<long long>(item.slot) * a.nf_max;
+    int* cnt0 = a.cnt + cbase;                 // forward gathers / backward panels
+    int* cnt1 = a.cnt + a.cnt_stride + cbase;  // forward row blocks
+    double2* V = a.vbuf + item.slot * a.vslot_stride;
+    double2* T = a.tbuf + item.slot * a.tslot_stride + fr.t_off * R;
+    const int nr = min(item.rw, R - item.r0);
+    if (FWD) {
+      if (item.kind == 0) {  // children complete = all their row-block items
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+          const int ch = q ? fr.child1 : fr.child0;
+          if (ch < 0) continue;
+          const DevFront cf = C.fronts[ch];
+          wait_count(cnt1 + ch, nrb_of(cf) * ngroups(cf, R, a.big_k), lane);
+        }
+        if (tr && lane == 0) tr[1] = gtime();
+        fwd_gather(a, C, S, fr, item.idx, T, V, lane);
+        signal(cnt0 + item.front, lane);
+      } else {
+        wait_count(cnt0 + item.front, nrb_of(fr), lane);
+        if (tr && lane == 0) tr[1] = gtime();
+        if (item.rw <= 4)
+          fwd_block<4>(a, S, fr, item.idx, T, V, item.r0, nr, lane, tiles);
+        else
+          fwd_block<16>(a, S, fr, item.idx, T, V, item.r0, nr, lane, tiles);
+        signal(cnt1 + item.front, lane);
+      }
+    } else {
+      if (fr.parent >= 0) {
+        const DevFront pf = C.fronts[fr.parent];
+        wait_count(cnt0 + fr.parent, np_of(pf) * ngroups(pf, R, a.big_k), lane);
+      }
+      if (tr && lane == 0) tr[1] = gtime();
+      if (item.rw <= 4)
+        bwd_panel<4>(a, C, S, fr, item.idx, item.r0, nr, lane, tiles);
+      else
+        bwd_panel<16>(a, C, S, fr, item.idx, item.r0, nr, lane, tiles);
+      signal(cnt0 + item.front, lane);
+    }
+    if (tr && lane == 0) {
+      tr[2] = gtime();
+      tr[3] = smid();
     }
   }
 }
 
-int g_sms = 0;
+constexpr size_t kSmem = static_cast<size_t>(kThreads / 32) * kTile * sizeof(double2);
+int g_grid[2] = {0, 0};
 
 }  // namespace
 
-size_t solve_smem_bytes(int max_rows, bool) {
-  return (static_cast<size_t>(kS) * kChunk + static_cast<size_t>(max_rows) * kTP) * sizeof(double2);
-}
+int solve_rhs_width(int k, int R, int big_k) { return k >= big_k ? std::min(4, R) : std::min(16, R); }
 
-int solve_grid(size_t smem) {
-  if (!g_sms) {
-    int dev = 0;
+void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
+  int& grid = g_grid[fwd ? 1 : 0];
+  if (!grid) {
+    int dev = 0, sms = 0, per = 0;
     HS_CUDA(cudaGetDevice(&dev));
-    HS_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+    HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HS_CUDA(cudaFuncSetAttribute(solve5_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    HS_CUDA(cudaFuncSetAttribute(solve5_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    if (fwd)
+      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve5_kernel<true>, kThreads, kSmem));
+    else
+      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve5_kernel<false>, kThreads, kSmem));
+    grid = sms * std::max(per, 1);
   }
-  // resident CTAs per SM allowed by shared memory (228 KB per SM, 1 KB reserved per CTA)
-  const int per = std::max(1, std::min(2, static_cast<int>((228 * 1024) / (smem + 2048))));
-  return g_sms * per;
-}
-
-int solve_rhs_group() { return kRG; }
-
-void launch_solve(const SolveArgs& a, bool fwd, int grid, size_t smem, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    HS_CUDA(cudaFuncSetAttribute(solve3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-    HS_CUDA(cudaFuncSetAttribute(solve3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
-    configured = true;
-  }
-  if (smem > 224 * 1024)
-    throw Error(kInternal, "solve: front too large for the shared-memory staging (" + std::to_string(smem) + " B)");
+  const int g = std::max(1, std::min(grid, (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
   if (fwd)
-    solve3_kernel<true><<<grid, kBlock, smem, s>>>(a);
+    solve5_kernel<true><<<g, kThreads, kSmem, s>>>(a);
   else
-    solve3_kernel<false><<<grid, kBlock, smem, s>>>(a);
+    solve5_kernel<false><<<g, kThreads, kSmem, s>>>(a);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   HS_CUDA(cudaGetLastError());
 }

@@ -212,14 +212,16 @@ std::unique_ptr<SymbolicClass> build_symbolic(int dim, const GridRange& range,
     fd.orig_cnt = static_cast<int>(c.orig_fpos.size()) - fd.orig_off;
   }
   // storage offsets and the reference's stats accounting
-  long long fac = 0, v = 0, fw = 0;
+  long long fac = 0, v = 0, fw = 0, tt = 0;
   std::int64_t active = 0, peak = 0;
   for (int f = 0; f < nf; ++f) {
     FrontDesc& fd = c.fronts[f];
     fd.fac_off = fac;
-    fac += front_chunk_elems(fd.m, fd.k);
+    fac += 2 * front_chunk_elems(fd.m, fd.k);
     fd.v_off = v;
     v += fd.m - fd.k;
+    fd.t_off = tt;
+    tt += fd.m;
     fd.f_off = fw;
     fw += static_cast<long long>(fd.m) * fd.m;
     const std::int64_t m = fd.m, k = fd.k;
@@ -240,6 +242,7 @@ std::unique_ptr<SymbolicClass> build_symbolic(int dim, const GridRange& range,
   c.fac_total = fac;
   c.v_total = v;
   c.f_total = fw;
+  c.t_total = tt;
   c.peak_bytes = peak;
   // schedules
   c.order_up.resize(nf);

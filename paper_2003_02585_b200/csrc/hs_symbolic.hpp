@@ -24,13 +24,14 @@ namespace hsb {
 constexpr int kLeafNodes = 64;   // src/direct.cpp:15
 constexpr int kSolvePanel = 32;  // solve-kernel panel width (device layout)
 
-// Elements of a front's solve factor [M; W] (M = L11^-1, W = L21 M): 32x32 chunks (rb, J),
-// J <= min(rb, np-1), rows padded to a multiple of 8 (layout: hs_kernels.cu factor output).
+// Elements of one copy of a front's solve factor [M; W] (M = L11^-1, W = L21 M): row blocks
+// of 32 rows holding chunks J <= min(rb, np-1) of 32 columns (hs_kernels.cu factor output).
+// The factor block of a front holds two copies (forward and backward layouts).
 inline long long front_chunk_elems(int m, int k) {
-  const int m_pad = (m + 7) & ~7, nrb = (m_pad + 31) >> 5, np = (k + 31) >> 5;
+  const int nrb = (m + 31) >> 5, np = (k + 31) >> 5;
   long long e = 0;
   for (int rb = 0; rb < nrb; ++rb) {
-    const int rc = m_pad - 32 * rb < 32 ? m_pad - 32 * rb : 32;
+    const int rc = m - 32 * rb < 32 ? m - 32 * rb : 32;
     const int nj = (rb < np - 1 ? rb : np - 1) + 1;
     e += static_cast<long long>(nj) * rc * 32;
   }
@@ -49,6 +50,7 @@ struct FrontDesc {
   long long fac_off = 0;  // elements into the subdomain's factor block
   long long v_off = 0;    // nodes into the update-vector slot
   long long f_off = 0;    // elements into the dense factorization workspace
+  long long t_off = 0;    // nodes into the forward gather slot (m per front)
 };
 
 // One symbolic class: subdomains whose local grids (and therefore trees, CSR
@@ -72,6 +74,7 @@ struct SymbolicClass {
   long long fac_total = 0;   // elements per subdomain factor block
   long long v_total = 0;     // update-vector nodes per slot
   long long f_total = 0;     // dense workspace elements
+  long long t_total = 0;     // forward gather nodes per slot
   std::int64_t factor_nnz = 0;  // reference convention sum m*k (src/direct.cpp:271)
   std::int64_t packed_entries = 0;  // sum over fronts of m*k - k*(k-1)/2 (lower trapezoid incl. D)
   std::int64_t peak_bytes = 0;  // reference accounting (src/direct.cpp:216-279)
