@@ -66,6 +66,7 @@ struct ClassDev {
   DBuf<DevFront> fronts;
   DBuf<int> bnd_elim, child_map, orig_fpos, orig_eidx, elim_of_local, local_of_elim;
   DBuf<int2> pmap;
+  std::vector<DevFront> h_fronts;
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   std::vector<int> level_start_down;
   DevClass dev{};
@@ -85,10 +86,13 @@ struct Engine {
   std::vector<double> tol;
   double factor_gpu_seconds = 0.0;
   int nf_max = 0, max_m = 0;
-  long long v_total_max = 0, t_total_max = 0, n_max = 0;
+  long long v_total_max = 0, n_max = 0;
   // solve state
-  int R = 0, nslots = 0, big_k = 64;
-  DBuf<double2> x, x1, vbuf, tbuf;
+  int R = 0, nslots = 0, ngr = 1;
+  int kc = 16, kr = 16;                        // split-K chunks (column blocks / block rows)
+  long long arr_total = 0, part_total = 0;     // per slot
+  DBuf<double2> x, x1, vbuf;
+  DBuf<double> part;
   DBuf<int> cnt;
 
   ~Engine() {
@@ -178,6 +182,8 @@ struct Engine {
         d.cmap1 = s.cmap_off[1];
         d.orig_off = s.orig_off;
         d.orig_cnt = s.orig_cnt;
+        d.arr_off = 0;
+        d.part_off = 0;
         d.pad_ = 0;
         d.fac_off = s.fac_off;
         d.v_off = s.v_off;
@@ -185,6 +191,7 @@ struct Engine {
         d.t_off = s.t_off;
       }
       cd.fronts.upload(fr, stream);
+      cd.h_fronts = fr;
       cd.bnd_elim.upload(c.bnd_elim, stream);
       cd.child_map.upload(c.child_map, stream);
       cd.orig_fpos.upload(c.orig_fpos, stream);
@@ -194,7 +201,7 @@ struct Engine {
       cd.dev.fronts = cd.fronts.p;
       cd.dev.bnd_elim = cd.bnd_elim.p;
       cd.dev.child_map = cd.child_map.p;
-      {  // inverse extend-add maps: parent position -> child0 / child1 update row
+      {  // extend-add source map: parent position -> update-vector row (v_off + i) of child0 / child1
         std::vector<int2> pm(std::max<long long>(c.t_total, 1), make_int2(-1, -1));
         for (const FrontDesc& fd : c.fronts)
           for (int q = 0; q < 2; ++q) {
@@ -203,7 +210,7 @@ struct Engine {
             const int cb = c.fronts[ch].m - c.fronts[ch].k;
             for (int i = 0; i < cb; ++i) {
               int2& e = pm[fd.t_off + c.child_map[fd.cmap_off[q] + i]];
-              (q ? e.y : e.x) = i;
+              (q ? e.y : e.x) = static_cast<int>(c.fronts[ch].v_off) + i;
             }
           }
         cd.pmap.upload(pm, stream);
@@ -223,7 +230,6 @@ struct Engine {
       nf_max = std::max(nf_max, static_cast<int>(c.fronts.size()));
       max_m = std::max(max_m, c.max_m);
       v_total_max = std::max(v_total_max, c.v_total);
-      t_total_max = std::max(t_total_max, c.t_total);
       n_max = std::max<long long>(n_max, c.n);
       hc.push_back(cd.dev);
     }
@@ -350,28 +356,66 @@ struct Engine {
     }
   }
 
-  // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains.
+  // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains,
+  // and the split-K bookkeeping of every front (arrival counters, partial tiles).
   void ensure_solve(int r, int slots) {
     if (r == R && slots <= nslots) return;
     R = r;
-    if (const char* e = std::getenv("HS_BIG_K")) big_k = std::atoi(e);
+    ngr = (R + 15) / 16;
+    if (const char* e = std::getenv("HS_KC")) kc = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("HS_KR")) kr = std::max(4, std::atoi(e) & ~3);
     nslots = std::max(slots, nslots);
+    arr_total = 0;
+    part_total = 0;
+    for (auto& cdp : classes) {
+      ClassDev& cd = *cdp;
+      const SymbolicClass& c = *cd.sym;
+      long long arr = 0, parts = 0;
+      for (size_t f = 0; f < c.fronts.size(); ++f) {
+        const int m = c.fronts[f].m, k = c.fronts[f].k;
+        const int kb = pad8(k) >> 3, nrb = kb + (pad8(m - k) >> 3);
+        const int nband = (nrb + 3) / 4, ncband = (kb + 3) / 4;
+        cd.h_fronts[f].arr_off = static_cast<int>(arr);
+        arr += std::max(nband, ncband);
+        int pf = 0, pb = 0;
+        bool split = false;
+        for (int t = 0; t < nband; ++t) {
+          const int n = solve_fwd_chunks(m, k, t, kc);
+          pf += n;
+          split |= n > 1;
+        }
+        for (int u = 0; u < ncband; ++u) {
+          const int n = solve_bwd_chunks(m, k, u, kr);
+          pb += n;
+          split |= n > 1;
+        }
+        cd.h_fronts[f].part_off = static_cast<int>(parts);
+        if (split) parts += std::max(pf, pb);
+      }
+      cd.fronts.upload(cd.h_fronts, stream);  // same size: device pointer unchanged
+      arr_total = std::max(arr_total, arr);
+      part_total = std::max(part_total, parts);
+    }
     const int nsub = static_cast<int>(sub_cls.size());
     x.alloc(static_cast<size_t>(n_base[nsub]) * R);
     x1.alloc(static_cast<size_t>(n_base[nsub]) * R);
     vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
-    tbuf.alloc(static_cast<size_t>(std::max<long long>(t_total_max, 1)) * R * nslots);
-    cnt.alloc(static_cast<size_t>(3) * nslots * nf_max + 2);
+    part.alloc(static_cast<size_t>(std::max<long long>(part_total, 1)) * nslots * ngr * 1024);
+    cnt.alloc(static_cast<size_t>(cnt_ints()));
     for (int s = 0; s < nsub; ++s) {
       h_subs[s].x = x.p + n_base[s] * R;
       h_subs[s].x1 = x1.p + n_base[s] * R;
     }
     d_subs.upload(h_subs, stream);
   }
+  // counter array: [done fwd | done bwd] per slot x front, [arrivals fwd | bwd], 2 queues
+  long long cnt_ints() const {
+    return 2LL * nslots * nf_max + 2LL * nslots * arr_total * ngr + 2;
+  }
 
   // Work items of the subdomains `group` (slot = position in the group), for the current R:
-  // forward = for every front by height, its 32-position gathers then its 32-row blocks per
-  // RHS group; backward = for every front by depth, its 32-column panels per RHS group.
+  // forward = every front by height, its bands x column chunks x RHS groups; backward = every
+  // front by depth, its column bands x block-row chunks x RHS groups.
   void build_items(const std::vector<int>& group, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
     int hmax = 0, dmax = 0;
     for (int id : group) {
@@ -385,10 +429,11 @@ struct Engine {
         for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
           const int f = c.order_up[q];
           const FrontDesc& fd = c.fronts[f];
-          const int nrb = (fd.m + 31) / 32, rw = solve_rhs_width(fd.k, R, big_k);
-          for (int pb = 0; pb < nrb; ++pb) fwd.push_back(SolveItem{group[g], f, 0, pb, static_cast<int>(g), 0, R, 0});
-          for (int rb = 0; rb < nrb; ++rb)
-            for (int r0 = 0; r0 < R; r0 += rw) fwd.push_back(SolveItem{group[g], f, 1, rb, static_cast<int>(g), r0, rw, 0});
+          const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
+          for (int t = 0; t < nband; ++t)
+            for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, kc); ++ch)
+              for (int r0 = 0; r0 < R; r0 += 16)
+                fwd.push_back(SolveItem{group[g], f, 1, t, static_cast<int>(g), r0, std::min(16, R - r0), ch});
         }
       }
     for (int d = 0; d <= dmax; ++d)
@@ -398,9 +443,11 @@ struct Engine {
         for (int q = cd.level_start_down[d]; q < cd.level_start_down[d + 1]; ++q) {
           const int f = cd.sym->order_down[q];
           const FrontDesc& fd = cd.sym->fronts[f];
-          const int rw = solve_rhs_width(fd.k, R, big_k);
-          for (int J = 0; J < (fd.k + 31) / 32; ++J)
-            for (int r0 = 0; r0 < R; r0 += rw) bwd.push_back(SolveItem{group[g], f, 2, J, static_cast<int>(g), r0, rw, 0});
+          const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
+          for (int u = 0; u < ncband; ++u)
+            for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, kr); ++ch)
+              for (int r0 = 0; r0 < R; r0 += 16)
+                bwd.push_back(SolveItem{group[g], f, 2, u, static_cast<int>(g), r0, std::min(16, R - r0), ch});
         }
       }
   }
@@ -410,23 +457,27 @@ struct Engine {
   void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const unsigned* nzmask,
                  bool traced = false) {
     const long long per = static_cast<long long>(nslots) * nf_max;
-    HS_CUDA(cudaMemsetAsync(cnt.p, 0, (3 * per + 2) * sizeof(int), stream));
+    const long long arr = static_cast<long long>(nslots) * arr_total * ngr;
+    HS_CUDA(cudaMemsetAsync(cnt.p, 0, cnt_ints() * sizeof(int), stream));
     SolveArgs a{};
     a.R = R;
-    a.big_k = big_k;
+    a.ngr = ngr;
+    a.kc = kc;
+    a.kr = kr;
     a.nf_max = nf_max;
     a.cls = d_cls.p;
     a.subs = d_subs.p;
     a.vbuf = vbuf.p;
     a.vslot_stride = v_total_max * R;
-    a.tbuf = tbuf.p;
-    a.tslot_stride = t_total_max * R;
+    a.part = part.p;
+    a.part_stride = part_total;
+    a.arr_stride = arr_total;
     a.nzmask = nzmask;
-    a.cnt_stride = per;
     a.items = fwd;
     a.nitems = nfwd;
-    a.cnt = cnt.p;
-    a.queue = reinterpret_cast<unsigned*>(cnt.p + 3 * per);
+    a.done = cnt.p;
+    a.arr = cnt.p + 2 * per;
+    a.queue = reinterpret_cast<unsigned*>(cnt.p + 2 * per + 2 * arr);
     if (traced) {  // developer instrumentation (HS_TRACE): per-item timestamps of this step
       trace.alloc(static_cast<size_t>(4) * (nfwd + nbwd));
       HS_CUDA(cudaMemsetAsync(trace.p, 0, trace.n * sizeof(unsigned long long), stream));
@@ -435,8 +486,9 @@ struct Engine {
     launch_solve(a, true, stream);
     a.items = bwd;
     a.nitems = nbwd;
-    a.cnt = cnt.p + 2 * per;
-    a.queue = reinterpret_cast<unsigned*>(cnt.p + 3 * per + 1);
+    a.done = cnt.p + per;
+    a.arr = cnt.p + 2 * per + arr;
+    a.queue = reinterpret_cast<unsigned*>(cnt.p + 2 * per + 2 * arr + 1);
     if (traced) a.trace = trace.p + 4LL * nfwd;
     launch_solve(a, false, stream);
     if (traced) {
@@ -447,12 +499,13 @@ struct Engine {
       HS_CUDA(cudaMemcpyAsync(items.data() + nfwd, bwd, nbwd * sizeof(SolveItem), cudaMemcpyDeviceToHost, stream));
       HS_CUDA(cudaStreamSynchronize(stream));
       if (FILE* fp = std::fopen(std::getenv("HS_TRACE"), "w")) {
-        std::fprintf(fp, "pass,sub,front,kind,idx,r0,rw,t_deq,t_ready,t_done,sm,k,m\n");
+        std::fprintf(fp, "pass,sub,front,kind,idx,chunk,r0,rw,t_deq,t_ready,t_done,sm,k,m\n");
         for (int i = 0; i < nfwd + nbwd; ++i) {
           const SolveItem& it = items[i];
           const FrontDesc& fd = classes[sub_cls[it.sub]]->sym->fronts[it.front];
-          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, it.sub, it.front,
-                       it.kind, it.idx, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k, fd.m);
+          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, it.sub, it.front,
+                       it.kind, it.idx, it.chunk, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k,
+                       fd.m);
         }
         std::fclose(fp);
       }

@@ -13,7 +13,10 @@ constexpr int kMaxRhs = 32;  // RHS per device batch (bitmask width)
 struct DevFront {
   int k, m, sep_off, bnd_off;
   int parent, child0, child1, cmap0, cmap1;
-  int orig_off, orig_cnt, pad_;
+  int orig_off, orig_cnt;
+  int arr_off;   // split-K arrival counters: first band / column band of this front
+  int part_off;  // split-K partial tiles of this front (0 parts when no band is split)
+  int pad_;
   long long fac_off, v_off, f_off, t_off;
 };
 
@@ -21,7 +24,7 @@ struct DevClass {
   const DevFront* fronts;
   const int* bnd_elim;
   const int* child_map;
-  const int2* pmap;           // per front position (offset t_off): row of child0 / child1 update, -1 if none
+  const int2* pmap;           // per front position (offset t_off): update-vector row (v_off + i) of child0 / child1, -1 if none
   const int* orig_fpos;
   const int* orig_eidx;
   const int* elim_of_local;
@@ -60,11 +63,12 @@ struct DevGeom {
   long long gn;               // global node count
 };
 
-// A solve work item (hs_solve.cu). kind 0: forward gather of 32 front positions (block idx);
-// kind 1: forward 32-row block idx of [M; W]; kind 2: backward 32-column panel idx. RHS
-// columns [r0, r0 + rw). slot = position of the subdomain in its step group.
+// A solve work item (hs_solve.cu). kind 1: forward band idx (32 padded rows of [M; W]) over
+// column-block chunk `chunk`; kind 2: backward column band idx (32 separator columns) over
+// block-row chunk `chunk`. RHS columns [r0, r0 + rw), rw <= 16. slot = position of the
+// subdomain in its step group.
 struct SolveItem {
-  int sub, front, kind, idx, slot, r0, rw, pad_;
+  int sub, front, kind, idx, slot, r0, rw, chunk;
 };
 
 struct FactorTask {

@@ -69,6 +69,12 @@ __device__ __forceinline__ void cacc(double2* p, double2 v) {
 // ----------------------------------------------------------------------------
 // factorization
 
+__device__ __forceinline__ long long band_base_dev(int t, int kb) {  // hs_symbolic.hpp band_base
+  const int j0 = kb >> 2;
+  const long long s = t <= j0 ? 2LL * t * (t + 1) : 2LL * j0 * (j0 + 1) + static_cast<long long>(t - j0) * kb;
+  return s * 256;
+}
+
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, int use_smem,
                                                               long long scratch_stride) {
   extern __shared__ double2 sm[];
@@ -218,29 +224,29 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
     }
   }
   __syncthreads();
-  // [M; W] stored twice (hs_solve.cu): copy F for the forward, row blocks rb of 32 rows,
-  // each holding chunks J = 0..min(rb, np-1) column-major (element (il, j) at j*rc + il);
-  // copy B for the backward, panels J of 32 columns holding rows [32J, m) row-major.
+  // [M; W] in the solve layout (hs_symbolic.hpp front_block_elems): padded rows [sep | bnd],
+  // 8x8 complex blocks row-major, bands of 4 block rows holding column blocks [0, min(kb, 4t+4)).
   {
-    const int nrb = (m + 31) >> 5, np = (k + 31) >> 5;
-    auto val = [&](int row, int col) {
-      if (row >= m || col >= k) return czero();
-      if (row >= k || row > col) return F[static_cast<long long>(col) * m + row];
-      return row == col ? make_double2(1.0, 0.0) : czero();
+    const int kp = (k + 7) & ~7, kb = kp >> 3, nrb = kb + ((m - k + 7) >> 3), nband = (nrb + 3) >> 2;
+    auto val = [&](int pr, int pc) {
+      if (pc >= k) return czero();
+      if (pr < k) {
+        if (pr > pc) return F[static_cast<long long>(pc) * m + pr];
+        return pr == pc ? make_double2(1.0, 0.0) : czero();
+      }
+      const int row = k + pr - kp;  // boundary row of the front
+      if (pr < kp || row >= m) return czero();
+      return F[static_cast<long long>(pc) * m + row];
     };
     double2* P = S.factor + f.fac_off;
-    for (int rb = 0; rb < nrb; ++rb) {
-      const int rc = min(32, m - 32 * rb), nj = min(rb, np - 1) + 1;
-      for (int idx = tid; idx < nj * rc * 32; idx += kThreads) {
-        const int J = idx / (rc * 32), rem = idx % (rc * 32), j = rem / rc, il = rem % rc;
-        P[idx] = val(32 * rb + il, 32 * J + j);
+    for (int t = 0; t < nband; ++t) {
+      const int rbs = min(4, nrb - 4 * t), ncb = min(kb, 4 * t + 4);
+      double2* B = P + band_base_dev(t, kb);
+      const int tot = ncb * rbs * 64;
+      for (int idx = tid; idx < tot; idx += kThreads) {
+        const int blk = idx >> 6, e = idx & 63, cb = blk / rbs, i = blk % rbs;
+        B[idx] = val(8 * (4 * t + i) + (e >> 3), 8 * cb + (e & 7));
       }
-      P += static_cast<long long>(nj) * rc * 32;
-    }
-    for (int J = 0; J < np; ++J) {
-      const int rows = m - 32 * J;
-      for (int idx = tid; idx < rows * 32; idx += kThreads) P[idx] = val(32 * J + idx / 32, 32 * J + idx % 32);
-      P += static_cast<long long>(rows) * 32;
     }
   }
 }

@@ -8,10 +8,14 @@ namespace hsb {
 struct SolveArgs {
   const SolveItem* items;
   int nitems;
-  int R;           // RHS per batch (row stride of x / V / T)
-  int big_k;       // fronts with k >= big_k are split into 4-RHS items
-  int* cnt;        // completion counters [slot * nf_max + front]: [0] gathers / panels, [1] row blocks
-  long long cnt_stride;  // elements between the two counter arrays
+  int R;           // RHS per batch (row stride of x / x1 / V)
+  int ngr;         // RHS groups of 16
+  int kc, kr;      // split-K chunk: column blocks per forward item, block rows per backward item
+  int* done;       // per [slot * nf_max + front]: finalized (band, group) pairs of this pass
+  int* arr;        // split-K arrivals per [(slot * arr_stride + arr_off + band) * ngr + group]
+  long long arr_stride;
+  double* part;    // split-K partial tiles (1024 doubles) per [(slot * part_stride + part_off + idx) * ngr + group]
+  long long part_stride;
   unsigned* queue; // dynamic item counter, zeroed per launch
   unsigned long long* trace;  // optional per-item timestamps [4 * item]: dequeue, ready, done, smid
   int nf_max;
@@ -19,15 +23,15 @@ struct SolveArgs {
   const DevSub* subs;
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
-  double2* tbuf;           // forward front inputs [x_sep + child updates; bnd updates] per slot
-  long long tslot_stride;
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
 };
 
 // Multifrontal forward (z = D^-1 L^-1 b) or backward (x = L^-T z) pass over the work items of
 // one step group (src/direct.cpp:290-325); hs_solve.cu.
 void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s);
-int solve_rhs_width(int k, int R, int big_k);
+// split-K bookkeeping shared by the host item builder and the kernels
+int solve_fwd_chunks(int m, int k, int band, int kc);
+int solve_bwd_chunks(int m, int k, int cband, int kr);
 
 struct FactorArgs {
   const FactorTask* tasks;

@@ -6,25 +6,28 @@
 // W = L21 M instead of L11 / L21 (hs_kernels.cu). The reference's per-front operations
 //   forward   t = L11^-1 x[sep]; x[bnd] -= L21 t          (direct.cpp:296-307)
 //   backward  x[sep] = L11^-T (x[sep] - L21^T x[bnd])     (direct.cpp:311-324)
-// become dense products without any serial dependency inside a front:
-//   forward   [z_sep; u] = [M; W] x_sep,  z = D^-1 z_sep (direct.cpp:309),  V = bnd updates - u
+// become one dense product per front without any serial dependency inside it:
+//   forward   [z_sep; u] = [M; W] T_sep,  z = D^-1 z_sep (direct.cpp:309),  V = T_bnd - u
 //   backward  x_sep = [M; W]^T [z_sep; -x_bnd]
-// Work items (one warp each, no CTA barriers):
-//   kind 0  forward gather of 32 front positions: T = [rhs_sep; 0] + child0 V + child1 V
-//           (the extend-add, in the reference's child order, src/direct.cpp:239-265);
-//   kind 1  forward 32-row block of [M; W] x T_sep for rw RHS (lane = row);
-//   kind 2  backward 32-column panel of [M; W]^T y for rw RHS (lane = column).
-// Fronts with k >= big_k use 4-RHS items (4x more warps on the long upper-tree critical
-// path), the others 16-RHS items (each factor byte read once for 16 RHS). Items are listed in
-// topological order and dequeued greedily; dependencies are per-front completion counters
-// (relaxed spin, one acquire, release increments). A warp dequeues only while running and
-// every dependency sits earlier in the list, so the launch cannot deadlock; every reduction
-// has a fixed order, so results are bitwise reproducible.
+// where T = rhs + the children's update vectors V (the extend-add, in the reference's child
+// order, src/direct.cpp:239-265), gathered on the fly through the front's source map.
 //
-// Factor streams: copy F (forward, column-major 32-row chunks) and copy B (backward, row-major
-// 32-column panels), coalesced 512-byte warp loads that bypass L1 (ld.global.nc.L1::no_allocate).
-// Vector operands are staged 32 rows at a time into a per-warp shared tile with cp.async.cg
-// (L2, coherent with the producers' release); 4-RHS items double-buffer the tile.
+// Tensor cores: the products run on FP64 DMMA (mma.sync m8n8k4 f64) with complex
+// arithmetic as four real products (re*re - im*im, re*im + im*re). The factor is stored once
+// in 8x8 complex blocks (hs_symbolic.hpp front_block_elems): the forward reads them as A
+// fragments (lane = row 8i + lane/4, column lane%4), the backward as transposed A fragments
+// of [M; W]^T (lane = row lane%4, column lane/4); both loads use whole 32-byte sectors. B
+// fragments (4 rows x 8 RHS) come straight from L2 (rhs / update vectors / z / x).
+//
+// Work items (one warp each, no shared memory):
+//   kind 1  forward band t (32 padded rows) x column-block chunk c x 16-RHS group;
+//   kind 2  backward column band u (32 separator columns) x block-row chunk c x RHS group.
+// Bands longer than one chunk are split-K: each chunk stores its partial tile and the last
+// arriving chunk sums all partials in chunk order (bitwise reproducible) and finalizes. Items
+// are listed in topological order and dequeued greedily; dependencies are per-front counters of
+// finalized bands (relaxed spin, one acquire, release increments); a warp dequeues only while
+// running and every dependency sits earlier in the list, so the launch cannot deadlock. The
+// factor range of an item is bulk-prefetched into L2 before its dependency wait.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
@@ -38,16 +41,9 @@ extern std::atomic<long long> g_kernel_launches;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTile = 32 * 16;  // double2 per warp tile (8 KB)
+constexpr int kThreads = 128;
 
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
-__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y);
-  acc.y = fma(a.y, b.x, acc.y);
-}
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -77,11 +73,12 @@ __device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
   __syncwarp();
 }
 __device__ __forceinline__ void signal(int* p, int lane) {
+  __threadfence();
   __syncwarp();
-  if (lane == 0) {
-    __threadfence();
-    red_release_add(p, 1);
-  }
+  if (lane == 0) red_release_add(p, 1);
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -93,9 +90,112 @@ __device__ __forceinline__ unsigned smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(s));
   return s;
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
-               "l"(gmem)
+// D[8x8] += A[8x4] B[4x8], FP64 tensor core
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Solve-layout geometry of a front (hs_symbolic.hpp)
+struct Geo {
+  int kp, kb, nrb, nband, ncband;
+};
+__device__ __forceinline__ Geo geo_of(const DevFront& f) {
+  Geo g;
+  g.kp = (f.k + 7) & ~7;
+  g.kb = g.kp >> 3;
+  g.nrb = g.kb + ((f.m - f.k + 7) >> 3);
+  g.nband = (g.nrb + 3) >> 2;
+  g.ncband = (g.kb + 3) >> 2;
+  return g;
+}
+__device__ __forceinline__ long long band_base(int t, int kb) {
+  const int j0 = kb >> 2;
+  const long long s = t <= j0 ? 2LL * t * (t + 1) : 2LL * j0 * (j0 + 1) + static_cast<long long>(t - j0) * kb;
+  return s * 256;
+}
+__device__ __forceinline__ int nch_fwd(const Geo& g, int t, int kc) { return (min(g.kb, 4 * t + 4) + kc - 1) / kc; }
+__device__ __forceinline__ int nch_bwd(const Geo& g, int u, int kr) { return (g.nrb - 4 * u + kr - 1) / kr; }
+
+template <int NT>
+struct Acc {
+  double v[4][NT][2][2];  // m-tile i, n-tile q, re/im, fragment element e
+};
+constexpr int kTileDoubles = 1024;  // partial tile: 32 lanes x up to 32 accumulator doubles
+
+template <int NT>
+__device__ __forceinline__ void acc_zero(Acc<NT>& c) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) c.v[i][q][p][0] = c.v[i][q][p][1] = 0.0;
+}
+
+// one k-step (4 columns of the product's inner dimension) of the complex 32 x (8 NT) tile
+template <int NT>
+__device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT]) {
+  double nb[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) nb[q] = -B[q].y;
+#pragma unroll
+  for (int q = 0; q < NT; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, B[q].x);
+      dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, B[q].y);
+    }
+#pragma unroll
+  for (int q = 0; q < NT; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nb[q]);
+      dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, B[q].x);
+    }
+}
+
+// Split-K: store this chunk's partial, and if it arrived last, replace acc by the sum of all
+// chunks in chunk order (read back from memory, own partial included). Returns whether this
+// warp finalizes the band.
+template <int NT>
+__device__ __forceinline__ bool split_reduce(Acc<NT>& c, double* base, long long cstride, int nch, int chunk,
+                                             int* arr, int lane) {
+  double* mine = base + chunk * cstride + lane;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) __stcg(mine + ((((i * NT + q) * 2 + p) * 2 + e) << 5), c.v[i][q][p][e]);
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) last = atomicAdd(arr, 1) == nch - 1;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return false;
+  __threadfence();
+  acc_zero(c);
+  for (int cc = 0; cc < nch; ++cc) {  // chunk order; own partial read back like the others
+    const double* pc = base + cc * cstride + lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < NT; ++q)
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) c.v[i][q][p][e] += __ldcg(pc + ((((i * NT + q) * 2 + p) * 2 + e) << 5));
+  }
+  return true;
+}
+
+__device__ __forceinline__ void cp16(double2* dst, const double2* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(ok ? 16 : 0)
                : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -104,257 +204,269 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ int nrb_of(const DevFront& f) { return (f.m + 31) >> 5; }
-__device__ __forceinline__ int np_of(const DevFront& f) { return (f.k + 31) >> 5; }
-__device__ __forceinline__ int rw_of(const DevFront& f, int R, int big_k) { return f.k >= big_k ? min(4, R) : min(16, R); }
-__device__ __forceinline__ int ngroups(const DevFront& f, int R, int big_k) {
-  const int w = rw_of(f, R, big_k);
-  return (R + w - 1) / w;
-}
-// element offset of row block rb in copy F (all earlier row blocks are full)
-__device__ __forceinline__ long long rb_base(int rb, int np) {
-  const long long pre = rb <= np ? static_cast<long long>(rb) * (rb + 1) / 2
-                                 : static_cast<long long>(np) * (np + 1) / 2 + static_cast<long long>(rb - np) * np;
-  return pre * 1024;
-}
-__device__ __forceinline__ long long copy_elems(int m, int k) {
-  const int np = (k + 31) >> 5;
-  return 32LL * (static_cast<long long>(np) * m - 16LL * np * (np - 1));
-}
+// Per-warp shared ring of NS k-steps: stage = A fragments (4 x 32 double2) then B parts
+// (NB x 2 x 32 double2: forward NB = 3 = rhs, child0 V, child1 V; backward NB = 1).
+template <bool FWD>
+struct Ring {
+  static constexpr int NS = FWD ? 3 : 4;
+  static constexpr int NB = FWD ? 3 : 1;
+  static constexpr int kStage = (4 + NB * 2) * 32;  // double2
+  static constexpr int kWarp = NS * kStage;
+};
 
-// kind 0: T[p] = (p < k ? rhs[sep + p] : 0) + child0 V + child1 V for 32 positions, all RHS.
-__device__ void fwd_gather(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, int pb, double2* T,
-                           const double2* V, int lane) {
-  const int R = a.R, p = 32 * pb + lane;
-  if (p >= fr.m) return;
-  const int2 pm = C.pmap[fr.t_off + p];
-  const double2* g0 = p < fr.k ? S.x + static_cast<long long>(fr.sep_off + p) * R : nullptr;
-  const double2* g1 = pm.x >= 0 ? V + (C.fronts[fr.child0].v_off + pm.x) * R : nullptr;
-  const double2* g2 = pm.y >= 0 ? V + (C.fronts[fr.child1].v_off + pm.y) * R : nullptr;
-  double2* t = T + static_cast<long long>(p) * R;
-#pragma unroll 4
-  for (int r = 0; r < R; ++r) {
-    double2 v = g0 ? __ldcg(g0 + r) : czero();
-    if (g1) {
-      const double2 w = __ldcg(g1 + r);
-      v = make_double2(v.x + w.x, v.y + w.y);
-    }
-    if (g2) {
-      const double2 w = __ldcg(g2 + r);
-      v = make_double2(v.x + w.x, v.y + w.y);
-    }
-    __stcg(t + r, v);
+// The pipelined k-loop shared by both passes: issue(s, stage, idx) stages k-step s with
+// cp.async (idx = the step's index-table entry, fetched one step ahead by idx_of(s));
+// use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight
+// data costs shared memory, not registers.
+template <bool FWD, int NT, class IdxOf, class Issue, class Use>
+__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, IdxOf&& idx_of, Issue&& issue, Use&& use) {
+  constexpr int NS = Ring<FWD>::NS, ST = Ring<FWD>::kStage;
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) {
+    if (j < ns) issue(j, ring + j * ST, idx_of(j));
+    cp_commit();
   }
-}
-
-// Stage rows [0, nrows) (row l at src(l) .. + RW) into tile[32][RW]; rows >= nrows zero.
-template <int RW, class Src>
-__device__ __forceinline__ void stage(double2* tile, int nrows, int nr, int lane, Src&& src) {
-  double2* dst = tile + lane * RW;
-  if (lane < nrows) {
-    const double2* g = src(lane);
-#pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      if (r < nr)
-        cp_async16(dst + r, g + r);
-      else
-        dst[r] = czero();
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < RW; ++r) dst[r] = czero();
+  int2 nxt = NS - 1 < ns ? idx_of(NS - 1) : make_int2(-1, -1);
+#pragma unroll 1
+  for (int s = 0; s < ns; ++s) {
+    const int si = s + NS - 1;
+    if (si < ns) issue(si, ring + (si % NS) * ST, nxt);
+    cp_commit();
+    if (si + 1 < ns) nxt = idx_of(si + 1);
+    cp_wait<NS - 1>();
+    __syncwarp();
+    double2 A[4], B[NT];
+    use(s, ring + (s % NS) * ST, A, B);
+    __syncwarp();
+    mma_step(acc, A, B);
   }
-  cp_commit();
+  cp_wait<0>();
 }
 
-// kind 1: out[row] = sum_j [M; W][row, j] T_sep[j] for RHS [r0, r0 + RW)
-template <int RW>
-__device__ void fwd_block(const SolveArgs& a, const DevSub& S, const DevFront& fr, int rb, const double2* T, double2* V,
-                          int r0, int nr, int lane, double2* tiles) {
-  constexpr int NB = kTile / (32 * RW) >= 2 ? 2 : 1;  // double buffer when the tile allows
-  const int R = a.R, m = fr.m, k = fr.k, np = np_of(fr);
-  const int rc = min(32, m - 32 * rb), nj = min(rb, np - 1) + 1;
-  const double2* P = S.factor + fr.fac_off + rb_base(rb, np);
-  double2 acc[RW];
-#pragma unroll
-  for (int r = 0; r < RW; ++r) acc[r] = czero();
-  const bool active = lane < rc;
-  auto src_of = [&](int J) {
-    return [=](int l) { return T + static_cast<long long>(32 * J + l) * R + r0; };
+// ---------------------------------------------------------------------------------------
+// forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols]
+template <int NT>
+__device__ void fwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, const Geo& g,
+                         const SolveItem& it, double2* V, int* done, int lane, double2* ring) {
+  const int R = a.R, r0 = it.r0, rl = lane >> 2, t = it.idx;
+  const int rbs = min(4, g.nrb - 4 * t), ncb = min(g.kb, 4 * t + 4);
+  const int cb0 = it.chunk * a.kc, cb1 = min(ncb, cb0 + a.kc);
+  const double2* P = S.factor + fr.fac_off + band_base(t, g.kb) + rl * 8 + (lane & 3);
+  const double2* X = S.x + static_cast<long long>(fr.sep_off) * R;
+  const int2* pm = C.pmap + fr.t_off;
+  const bool leaf = fr.child0 < 0 && fr.child1 < 0;
+  auto col_of = [&](int s) { return 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
+  auto idx_of = [&](int s) {
+    const int col = col_of(s);
+    return (!leaf && col < fr.k) ? __ldg(pm + col) : make_int2(-1, -1);
   };
-  stage<RW>(tiles, min(32, k), nr, lane, src_of(0));
-  for (int J = 0; J < nj; ++J) {
-    double2* tile = tiles + (J % NB) * 32 * RW;
-    if (NB == 2 && J + 1 < nj) {
-      stage<RW>(tiles + ((J + 1) % NB) * 32 * RW, min(32, k - 32 * (J + 1)), nr, lane, src_of(J + 1));
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+  auto issue = [&](int s, double2* st, int2 src) {
+    const double2* p = P + ((cb0 + (s >> 1)) * rbs) * 64 + 4 * (s & 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp16(st + i * 32 + lane, i < rbs ? p + i * 64 : P, i < rbs);
+    const int col = col_of(s);
+    double2* sb = st + 4 * 32 + lane;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      const int r = r0 + 8 * q + rl;
+      const bool ok = col < fr.k && r < R;
+      cp16(sb + (0 * 2 + q) * 32, ok ? X + static_cast<long long>(col) * R + r : X, ok);
+      cp16(sb + (1 * 2 + q) * 32, ok && src.x >= 0 ? V + static_cast<long long>(src.x) * R + r : X, ok && src.x >= 0);
+      cp16(sb + (2 * 2 + q) * 32, ok && src.y >= 0 ? V + static_cast<long long>(src.y) * R + r : X, ok && src.y >= 0);
     }
-    __syncwarp();
-    const double2* ch = P + static_cast<long long>(J) * rc * 32;
-    const int jmax = min(32, k - 32 * J);
-    int j = 0;
-    for (; j + 8 <= jmax; j += 8) {
-      double2 L[8];
+  };
+  auto use = [&](int, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) L[u] = active ? ld_stream(ch + (j + u) * rc + lane) : czero();
+    for (int i = 0; i < 4; ++i) A[i] = st[i * 32 + lane];
+    const double2* sb = st + 4 * 32 + lane;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double2* xr = tile + (j + u) * RW;
-#pragma unroll
-        for (int r = 0; r < RW; ++r) cfma(acc[r], L[u], xr[r]);
-      }
+    for (int q = 0; q < NT; ++q) {
+      double2 v = sb[(0 * 2 + q) * 32];
+      const double2 w0 = sb[(1 * 2 + q) * 32], w1 = sb[(2 * 2 + q) * 32];
+      v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
+      B[q] = make_double2(v.x + w1.x, v.y + w1.y);
     }
-    for (; j < jmax; ++j) {
-      const double2 L = active ? ld_stream(ch + j * rc + lane) : czero();
-      const double2* xr = tile + j * RW;
-#pragma unroll
-      for (int r = 0; r < RW; ++r) cfma(acc[r], L, xr[r]);
-    }
-    __syncwarp();
-    if (NB == 1 && J + 1 < nj) stage<RW>(tiles, min(32, k - 32 * (J + 1)), nr, lane, src_of(J + 1));
+  };
+  Acc<NT> acc;
+  acc_zero(acc);
+  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, idx_of, issue, use);
+  const int nch = nch_fwd(g, t, a.kc);
+  if (nch > 1) {
+    int loc = 0;
+    for (int tt = 0; tt < t; ++tt) loc += nch_fwd(g, tt, a.kc);
+    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + fr.part_off + loc;
+    double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + fr.arr_off + t) * a.ngr + r0 / 16;
+    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
   }
-  if (!active) return;
-  const int row = 32 * rb + lane;
-  if (row < k) {  // z_sep = D^-1 M x_sep
-    const long long pos = fr.sep_off + row;
-    const double2 d = S.dinv[pos];
+  // finalize: z = D^-1 (M T_sep) for separator rows, V = T_bnd - W T_sep for boundary rows
 #pragma unroll
-    for (int r = 0; r < RW; ++r)
-      if (r < nr) __stcg(&S.x1[pos * R + r0 + r], cmul(acc[r], d));
-  } else {        // V = (children's bnd updates) - W x_sep
-    const double2* t = T + static_cast<long long>(row) * R + r0;
+  for (int i = 0; i < 4; ++i) {
+    const int pr = 32 * t + 8 * i + rl;
+    if (pr < fr.k) {
+      const long long pos = fr.sep_off + pr;
+      const double2 d = S.dinv[pos];
 #pragma unroll
-    for (int r = 0; r < RW; ++r)
-      if (r < nr) {
-        const double2 w = __ldcg(t + r);
-        __stcg(&V[(fr.v_off + row - k) * R + r0 + r], make_double2(w.x - acc[r].x, w.y - acc[r].y));
-      }
+      for (int q = 0; q < NT; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+          if (r < R) __stcg(&S.x1[pos * R + r], cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), d));
+        }
+    } else if (pr >= g.kp && pr - g.kp < fr.m - fr.k) {
+      const int bi = pr - g.kp;
+      const int2 src = __ldg(pm + fr.k + bi);
+#pragma unroll
+      for (int q = 0; q < NT; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+          if (r >= R) continue;
+          double2 tb = czero();
+          if (src.x >= 0) {
+            const double2 w = __ldcg(V + static_cast<long long>(src.x) * R + r);
+            tb = make_double2(tb.x + w.x, tb.y + w.y);
+          }
+          if (src.y >= 0) {
+            const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
+            tb = make_double2(tb.x + w.x, tb.y + w.y);
+          }
+          __stcg(&V[(fr.v_off + bi) * R + r], make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
+        }
+    }
   }
+  signal(done + it.front, lane);
 }
 
-// kind 2: x_sep[col] = sum_i [M; W][i, col] [z_sep; -x_bnd][i] for RHS [r0, r0 + RW)
-template <int RW>
-__device__ void bwd_panel(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, int J, int r0,
-                          int nr, int lane, double2* tiles) {
-  constexpr int NB = kTile / (32 * RW) >= 2 ? 2 : 1;
-  const int R = a.R, m = fr.m, k = fr.k;
-  const double2* P = S.factor + fr.fac_off + copy_elems(m, k) + 32LL * (static_cast<long long>(J) * m - 16LL * J * (J - 1));
-  double2 acc[RW];
-#pragma unroll
-  for (int r = 0; r < RW; ++r) acc[r] = czero();
-  auto src_of = [&](int i0) {
-    return [=](int l) {
-      const int ii = i0 + l;
-      const long long pos = ii < k ? static_cast<long long>(fr.sep_off + ii)
-                                   : static_cast<long long>(C.bnd_elim[fr.bnd_off + ii - k]);
-      return (ii < k ? S.x1 : S.x) + pos * R + r0;
-    };
+// ---------------------------------------------------------------------------------------
+// backward column-band item: x_sep[32 cols][8 NT RHS] = sum over the chunk's rows of
+// [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
+template <int NT>
+__device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, const Geo& g,
+                         const SolveItem& it, int* done, int lane, double2* ring) {
+  const int R = a.R, r0 = it.r0, rl = lane >> 2, u = it.idx;
+  const int a0 = 4 * u + it.chunk * a.kr, a1 = min(g.nrb, a0 + a.kr);
+  const double2* P = S.factor + fr.fac_off + (lane & 3) * 8 + rl;
+  const double2* Z = S.x1 + static_cast<long long>(fr.sep_off) * R;
+  const int* be = C.bnd_elim + fr.bnd_off;
+  const int nb = fr.m - fr.k;
+  auto row_of = [&](int s) { return 8 * (a0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
+  auto idx_of = [&](int s) {
+    const int row = row_of(s);
+    return make_int2(row >= g.kp && row - g.kp < nb ? __ldg(be + row - g.kp) : -1, 0);
   };
-  const int nbt = (m - 32 * J + 31) / 32;
-  stage<RW>(tiles, min(32, m - 32 * J), nr, lane, src_of(32 * J));
-  for (int b = 0; b < nbt; ++b) {
-    const int i0 = 32 * J + 32 * b;
-    const int nrow = min(32, m - i0);
-    double2* tile = tiles + (b % NB) * 32 * RW;
-    if (NB == 2 && b + 1 < nbt) {
-      stage<RW>(tiles + ((b + 1) % NB) * 32 * RW, min(32, m - i0 - 32), nr, lane, src_of(i0 + 32));
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+  auto issue = [&](int s, double2* st, int2 bi) {
+    const int ab = a0 + (s >> 1), ta = ab >> 2, rbs = min(4, g.nrb - 4 * ta);
+    const double2* p = P + band_base(ta, g.kb) + (ab & 3) * 64 + 32 * (s & 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int cbi = 4 * u + i;
+      cp16(st + i * 32 + lane, cbi < g.kb ? p + cbi * rbs * 64 : P, cbi < g.kb);
     }
-    if (i0 + lane >= k && lane < nrow) {  // bnd rows enter as -x_bnd
+    const int row = row_of(s);
+    const double2* src = row < fr.k ? Z + static_cast<long long>(row) * R
+                                    : (bi.x >= 0 ? S.x + static_cast<long long>(bi.x) * R : nullptr);
 #pragma unroll
-      for (int r = 0; r < RW; ++r) tile[lane * RW + r] = make_double2(-tile[lane * RW + r].x, -tile[lane * RW + r].y);
+    for (int q = 0; q < NT; ++q) {
+      const int r = r0 + 8 * q + rl;
+      const bool ok = src != nullptr && r < R;
+      cp16(st + (4 + q) * 32 + lane, ok ? src + r : Z, ok);
     }
-    __syncwarp();
-    const double2* Pb = P + static_cast<long long>(i0 - 32 * J) * 32;
-    int u0 = 0;
-    for (; u0 + 8 <= nrow; u0 += 8) {
-      double2 L[8];
+  };
+  auto use = [&](int s, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) L[u] = ld_stream(Pb + (u0 + u) * 32 + lane);
+    for (int i = 0; i < 4; ++i) A[i] = st[i * 32 + lane];
+    const bool neg = row_of(s) >= fr.k;  // boundary rows enter as -x_bnd (zeros stay zero)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const double2* y = tile + (u0 + u) * RW;
+    for (int q = 0; q < NT; ++q) {
+      const double2 v = st[(4 + q) * 32 + lane];
+      B[q] = neg ? make_double2(-v.x, -v.y) : v;
+    }
+  };
+  Acc<NT> acc;
+  acc_zero(acc);
+  kloop<false, NT>(acc, 2 * (a1 - a0), ring, idx_of, issue, use);
+  const int nch = nch_bwd(g, u, a.kr);
+  if (nch > 1) {
+    int loc = 0;
+    for (int uu = 0; uu < u; ++uu) loc += nch_bwd(g, uu, a.kr);
+    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + fr.part_off + loc;
+    double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + fr.arr_off + u) * a.ngr + r0 / 16;
+    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
+  }
 #pragma unroll
-        for (int r = 0; r < RW; ++r) cfma(acc[r], L[u], y[r]);
+  for (int i = 0; i < 4; ++i) {
+    const int col = 32 * u + 8 * i + rl;
+    if (col >= fr.k) continue;
+    double2* xo = S.x + static_cast<long long>(fr.sep_off + col) * R;
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+        if (r < R) __stcg(xo + r, make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]));
       }
-    }
-    for (; u0 < nrow; ++u0) {
-      const double2 L = ld_stream(Pb + u0 * 32 + lane);
-      const double2* y = tile + u0 * RW;
-#pragma unroll
-      for (int r = 0; r < RW; ++r) cfma(acc[r], L, y[r]);
-    }
-    __syncwarp();
-    if (NB == 1 && b + 1 < nbt) stage<RW>(tiles, min(32, m - i0 - 32), nr, lane, src_of(i0 + 32));
   }
-  const int col = 32 * J + lane;
-  if (col < k) {
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-      if (r < nr) __stcg(&S.x[static_cast<long long>(fr.sep_off + col) * R + r0 + r], acc[r]);
-  }
+  signal(done + it.front, lane);
 }
 
 template <bool FWD>
-__global__ void __launch_bounds__(kThreads, 2) solve5_kernel(SolveArgs a) {
-  extern __shared__ __align__(16) double2 smem_tiles[];
+__global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
+  extern __shared__ __align__(16) double2 smem_ring[];
   const int lane = threadIdx.x & 31;
-  double2* tiles = smem_tiles + (threadIdx.x >> 5) * kTile;
-  const int R = a.R;
+  double2* ring = smem_ring + (threadIdx.x >> 5) * Ring<FWD>::kWarp;
   for (;;) {
-    int it = 0;
-    if (lane == 0) it = static_cast<int>(atomicAdd(a.queue, 1u));
-    it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= a.nitems) break;
-    const SolveItem item = a.items[it];
-    if (a.nzmask[item.sub] == 0) continue;  // skipped subdomain: nothing depends on it
-    unsigned long long* tr = a.trace ? a.trace + 4LL * it : nullptr;
+    int it_idx = 0;
+    if (lane == 0) it_idx = static_cast<int>(atomicAdd(a.queue, 1u));
+    it_idx = __shfl_sync(0xffffffffu, it_idx, 0);
+    if (it_idx >= a.nitems) break;
+    const SolveItem it = a.items[it_idx];
+    if (a.nzmask[it.sub] == 0) continue;  // skipped subdomain: nothing depends on it
+    unsigned long long* tr = a.trace ? a.trace + 4LL * it_idx : nullptr;
     if (tr && lane == 0) tr[0] = gtime();
-    const DevSub& S = a.subs[item.sub];
+    const DevSub& S = a.subs[it.sub];
     const DevClass& C = a.cls[S.cls];
-    const DevFront fr = C.fronts[item.front];
-    const long long cbase = static_cast<long long>(item.slot) * a.nf_max;
-    int* cnt0 = a.cnt + cbase;                 // forward gathers / backward panels
-    int* cnt1 = a.cnt + a.cnt_stride + cbase;  // forward row blocks
-    double2* V = a.vbuf + item.slot * a.vslot_stride;
-    double2* T = a.tbuf + item.slot * a.tslot_stride + fr.t_off * R;
-    const int nr = min(item.rw, R - item.r0);
-    if (FWD) {
-      if (item.kind == 0) {  // children complete = all their row-block items
-#pragma unroll 1
-        for (int q = 0; q < 2; ++q) {
-          const int ch = q ? fr.child1 : fr.child0;
-          if (ch < 0) continue;
-          const DevFront cf = C.fronts[ch];
-          wait_count(cnt1 + ch, nrb_of(cf) * ngroups(cf, R, a.big_k), lane);
-        }
-        if (tr && lane == 0) tr[1] = gtime();
-        fwd_gather(a, C, S, fr, item.idx, T, V, lane);
-        signal(cnt0 + item.front, lane);
+    const DevFront fr = C.fronts[it.front];
+    const Geo g = geo_of(fr);
+    int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
+    if (lane == 0) {  // factor range of this item -> L2, overlapping the dependency wait
+      const double2* F = S.factor + fr.fac_off;
+      if (FWD) {
+        const int t = it.idx, rbs = min(4, g.nrb - 4 * t), ncb = min(g.kb, 4 * t + 4);
+        const int cb0 = it.chunk * a.kc, cb1 = min(ncb, cb0 + a.kc);
+        prefetch_l2(F + band_base(t, g.kb) + cb0 * rbs * 64, static_cast<unsigned>((cb1 - cb0) * rbs) * 1024u);
       } else {
-        wait_count(cnt0 + item.front, nrb_of(fr), lane);
-        if (tr && lane == 0) tr[1] = gtime();
-        if (item.rw <= 4)
-          fwd_block<4>(a, S, fr, item.idx, T, V, item.r0, nr, lane, tiles);
-        else
-          fwd_block<16>(a, S, fr, item.idx, T, V, item.r0, nr, lane, tiles);
-        signal(cnt1 + item.front, lane);
+        const int u = it.idx, a0 = 4 * u + it.chunk * a.kr, a1 = min(g.nrb, a0 + a.kr);
+        const int ncol = min(4, g.kb - 4 * u);
+        for (int ta = a0 >> 2; ta <= (a1 - 1) >> 2; ++ta) {
+          const int rbs = min(4, g.nrb - 4 * ta);
+          prefetch_l2(F + band_base(ta, g.kb) + 4 * u * rbs * 64, static_cast<unsigned>(ncol * rbs) * 1024u);
+        }
       }
-    } else {
-      if (fr.parent >= 0) {
-        const DevFront pf = C.fronts[fr.parent];
-        wait_count(cnt0 + fr.parent, np_of(pf) * ngroups(pf, R, a.big_k), lane);
+    }
+    if (FWD) {
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        const int ch = q ? fr.child1 : fr.child0;
+        if (ch < 0) continue;
+        wait_count(done + ch, geo_of(C.fronts[ch]).nband * a.ngr, lane);
       }
-      if (tr && lane == 0) tr[1] = gtime();
-      if (item.rw <= 4)
-        bwd_panel<4>(a, C, S, fr, item.idx, item.r0, nr, lane, tiles);
+    } else if (fr.parent >= 0) {
+      wait_count(done + fr.parent, geo_of(C.fronts[fr.parent]).ncband * a.ngr, lane);
+    }
+    if (tr && lane == 0) tr[1] = gtime();
+    double2* V = a.vbuf + it.slot * a.vslot_stride;
+    if (FWD) {
+      if (it.rw > 8)
+        fwd_item<2>(a, C, S, fr, g, it, V, done, lane, ring);
       else
-        bwd_panel<16>(a, C, S, fr, item.idx, item.r0, nr, lane, tiles);
-      signal(cnt0 + item.front, lane);
+        fwd_item<1>(a, C, S, fr, g, it, V, done, lane, ring);
+    } else {
+      if (it.rw > 8)
+        bwd_item<2>(a, C, S, fr, g, it, done, lane, ring);
+      else
+        bwd_item<1>(a, C, S, fr, g, it, done, lane, ring);
     }
     if (tr && lane == 0) {
       tr[2] = gtime();
@@ -363,12 +475,23 @@ __global__ void __launch_bounds__(kThreads, 2) solve5_kernel(SolveArgs a) {
   }
 }
 
-constexpr size_t kSmem = static_cast<size_t>(kThreads / 32) * kTile * sizeof(double2);
 int g_grid[2] = {0, 0};
 
 }  // namespace
 
-int solve_rhs_width(int k, int R, int big_k) { return k >= big_k ? std::min(4, R) : std::min(16, R); }
+int solve_fwd_chunks(int m, int k, int band, int kc) {
+  const int kb = ((k + 7) & ~7) >> 3;
+  return (std::min(kb, 4 * band + 4) + kc - 1) / kc;
+}
+int solve_bwd_chunks(int m, int k, int cband, int kr) {
+  const int nrb = (((k + 7) & ~7) >> 3) + (((m - k + 7) & ~7) >> 3);
+  return (nrb - 4 * cband + kr - 1) / kr;
+}
+
+template <bool FWD>
+constexpr size_t ring_bytes() {
+  return static_cast<size_t>(kThreads / 32) * Ring<FWD>::kWarp * sizeof(double2);
+}
 
 void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
   int& grid = g_grid[fwd ? 1 : 0];
@@ -376,19 +499,20 @@ void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
     int dev = 0, sms = 0, per = 0;
     HS_CUDA(cudaGetDevice(&dev));
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HS_CUDA(cudaFuncSetAttribute(solve5_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    HS_CUDA(cudaFuncSetAttribute(solve5_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    if (fwd)
-      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve5_kernel<true>, kThreads, kSmem));
-    else
-      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve5_kernel<false>, kThreads, kSmem));
+    if (fwd) {
+      HS_CUDA(cudaFuncSetAttribute(solve6_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<true>()));
+      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<true>, kThreads, ring_bytes<true>()));
+    } else {
+      HS_CUDA(cudaFuncSetAttribute(solve6_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<false>()));
+      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<false>, kThreads, ring_bytes<false>()));
+    }
     grid = sms * std::max(per, 1);
   }
   const int g = std::max(1, std::min(grid, (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
   if (fwd)
-    solve5_kernel<true><<<g, kThreads, kSmem, s>>>(a);
+    solve6_kernel<true><<<g, kThreads, ring_bytes<true>(), s>>>(a);
   else
-    solve5_kernel<false><<<g, kThreads, kSmem, s>>>(a);
+    solve6_kernel<false><<<g, kThreads, ring_bytes<false>(), s>>>(a);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   HS_CUDA(cudaGetLastError());
 }

@@ -217,7 +217,7 @@ std::unique_ptr<SymbolicClass> build_symbolic(int dim, const GridRange& range,
   for (int f = 0; f < nf; ++f) {
     FrontDesc& fd = c.fronts[f];
     fd.fac_off = fac;
-    fac += 2 * front_chunk_elems(fd.m, fd.k);
+    fac += front_block_elems(fd.m, fd.k);
     fd.v_off = v;
     v += fd.m - fd.k;
     fd.t_off = tt;

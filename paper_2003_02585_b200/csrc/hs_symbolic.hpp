@@ -9,8 +9,8 @@
 //  * vectors are permuted once into elimination order, so a front's separator is
 //    the contiguous slice [sep_off, sep_off+k) and RHS columns are node-major with the
 //    RHS index fastest;
-//  * a front's factor columns are stored as 32-column panels, panel J holding rows
-//    [32J, m) row-major (512 B per row), strict lower part only (zeros elsewhere);
+//  * a front's solve factor [M; W] is stored once in 8x8 complex blocks (front_block_elems),
+//    read as DMMA A fragments by the forward and as transposed B fragments by the backward;
 //  * forward-solve update vectors (the multifrontal "extend-add" of x[bnd] -= L21 t)
 //    live in a per-front slot of m-k nodes, reduced into the parent in fixed order.
 #pragma once
@@ -24,18 +24,23 @@ namespace hsb {
 constexpr int kLeafNodes = 64;   // src/direct.cpp:15
 constexpr int kSolvePanel = 32;  // solve-kernel panel width (device layout)
 
-// Elements of one copy of a front's solve factor [M; W] (M = L11^-1, W = L21 M): row blocks
-// of 32 rows holding chunks J <= min(rb, np-1) of 32 columns (hs_kernels.cu factor output).
-// The factor block of a front holds two copies (forward and backward layouts).
-inline long long front_chunk_elems(int m, int k) {
-  const int nrb = (m + 31) >> 5, np = (k + 31) >> 5;
-  long long e = 0;
-  for (int rb = 0; rb < nrb; ++rb) {
-    const int rc = m - 32 * rb < 32 ? m - 32 * rb : 32;
-    const int nj = (rb < np - 1 ? rb : np - 1) + 1;
-    e += static_cast<long long>(nj) * rc * 32;
-  }
-  return e;
+// Solve-factor layout of one front (hs_solve.cu, written by the factorization kernel):
+// [M; W] with rows [0, kp) = separator (kp = k rounded up to 8, rows >= k zero) followed by
+// ceil8(m - k) boundary rows, columns [0, kp); cut into 8x8 complex blocks stored row-major
+// (1 KB). Bands of 4 block rows; band t holds column blocks cb < min(kp/8, 4t + 4) (M is
+// lower triangular), ordered [cb][block row in band]. Every band but the last is full, so
+// the band base has a closed form (band_base).
+inline int pad8(int v) { return (v + 7) & ~7; }
+inline long long band_base(int t, int kb) {
+  const int j0 = kb >> 2;
+  const long long s = t <= j0 ? 2LL * t * (t + 1) : 2LL * j0 * (j0 + 1) + static_cast<long long>(t - j0) * kb;
+  return s * 256;
+}
+inline long long front_block_elems(int m, int k) {
+  const int kb = pad8(k) >> 3, nrb = kb + (pad8(m - k) >> 3), nband = (nrb + 3) >> 2;
+  if (nband == 0) return 0;
+  const int t = nband - 1, rbs = nrb - 4 * t, ncb = kb < 4 * t + 4 ? kb : 4 * t + 4;
+  return band_base(t, kb) + static_cast<long long>(ncb) * rbs * 64;
 }
 
 struct FrontDesc {
@@ -50,7 +55,7 @@ struct FrontDesc {
   long long fac_off = 0;  // elements into the subdomain's factor block
   long long v_off = 0;    // nodes into the update-vector slot
   long long f_off = 0;    // elements into the dense factorization workspace
-  long long t_off = 0;    // nodes into the forward gather slot (m per front)
+  long long t_off = 0;    // front positions (m per front) into the extend-add source map
 };
 
 // One symbolic class: subdomains whose local grids (and therefore trees, CSR
@@ -74,7 +79,7 @@ struct SymbolicClass {
   long long fac_total = 0;   // elements per subdomain factor block
   long long v_total = 0;     // update-vector nodes per slot
   long long f_total = 0;     // dense workspace elements
-  long long t_total = 0;     // forward gather nodes per slot
+  long long t_total = 0;     // front positions per class (source-map entries)
   std::int64_t factor_nnz = 0;  // reference convention sum m*k (src/direct.cpp:271)
   std::int64_t packed_entries = 0;  // sum over fronts of m*k - k*(k-1)/2 (lower trapezoid incl. D)
   std::int64_t peak_bytes = 0;  // reference accounting (src/direct.cpp:216-279)
