@@ -89,11 +89,13 @@ struct Engine {
   long long v_total_max = 0, n_max = 0;
   // solve state
   int R = 0, nslots = 0, ngr = 1;
-  int kc = 16, kr = 16;                        // split-K chunks (column blocks / block rows)
+  int kc = 8, kr = 4;                          // split-K chunks (column blocks / block rows)
   long long arr_total = 0, part_total = 0;     // per slot
   DBuf<double2> x, x1, vbuf;
   DBuf<double> part;
   DBuf<int> cnt;
+  std::vector<int> job_base;   // per subdomain: first job (subdomain, front) record
+  DBuf<SolveJob> jobs;
 
   ~Engine() {
     if (stream) cudaStreamDestroy(stream);
@@ -362,8 +364,8 @@ struct Engine {
     if (r == R && slots <= nslots) return;
     R = r;
     ngr = (R + 15) / 16;
-    if (const char* e = std::getenv("HS_KC")) kc = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("HS_KR")) kr = std::max(4, std::atoi(e) & ~3);
+    if (const char* e = std::getenv("HS_KC")) kc = std::min(16, std::max(1, std::atoi(e)));
+    if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;
@@ -407,6 +409,39 @@ struct Engine {
       h_subs[s].x1 = x1.p + n_base[s] * R;
     }
     d_subs.upload(h_subs, stream);
+    // per (subdomain, front) job records for the solve kernels
+    job_base.assign(nsub + 1, 0);
+    for (int s = 0; s < nsub; ++s) job_base[s + 1] = job_base[s] + static_cast<int>(classes[sub_cls[s]]->sym->fronts.size());
+    std::vector<SolveJob> hj(job_base[nsub]);
+    auto nband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + (pad8(d.m - d.k) >> 3) + 3) / 4; };
+    auto ncband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + 3) / 4; };
+    for (int s = 0; s < nsub; ++s) {
+      const ClassDev& cd = *classes[sub_cls[s]];
+      const SymbolicClass& c = *cd.sym;
+      for (size_t f = 0; f < c.fronts.size(); ++f) {
+        const FrontDesc& fd = c.fronts[f];
+        SolveJob& J = hj[job_base[s] + f];
+        J.factor = factor.p + fac_base[s] + fd.fac_off;
+        J.dinv = dinv.p + n_base[s] + fd.sep_off;
+        J.x = h_subs[s].x;
+        J.x1 = h_subs[s].x1;
+        J.pm = cd.pmap.p + fd.t_off;
+        J.be = cd.bnd_elim.p + fd.bnd_off;
+        J.k = fd.k;
+        J.m = fd.m;
+        J.sep_off = fd.sep_off;
+        J.v_off = static_cast<int>(fd.v_off);
+        J.child0 = fd.child[0];
+        J.child1 = fd.child[1];
+        J.nband_c0 = fd.child[0] >= 0 ? nband_of(c.fronts[fd.child[0]]) : 0;
+        J.nband_c1 = fd.child[1] >= 0 ? nband_of(c.fronts[fd.child[1]]) : 0;
+        J.parent = fd.parent;
+        J.ncband_p = fd.parent >= 0 ? ncband_of(c.fronts[fd.parent]) : 0;
+        J.arr_off = cd.h_fronts[f].arr_off;
+        J.part_off = cd.h_fronts[f].part_off;
+      }
+    }
+    jobs.upload(hj, stream);
   }
   // counter array: [done fwd | done bwd] per slot x front, [arrivals fwd | bwd], 2 queues
   long long cnt_ints() const {
@@ -433,7 +468,8 @@ struct Engine {
           for (int t = 0; t < nband; ++t)
             for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, kc); ++ch)
               for (int r0 = 0; r0 < R; r0 += 16)
-                fwd.push_back(SolveItem{group[g], f, 1, t, static_cast<int>(g), r0, std::min(16, R - r0), ch});
+                fwd.push_back(SolveItem{group[g], f, job_base[group[g]] + f, t, static_cast<int>(g), r0,
+                                        std::min(16, R - r0), ch});
         }
       }
     for (int d = 0; d <= dmax; ++d)
@@ -447,7 +483,8 @@ struct Engine {
           for (int u = 0; u < ncband; ++u)
             for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, kr); ++ch)
               for (int r0 = 0; r0 < R; r0 += 16)
-                bwd.push_back(SolveItem{group[g], f, 2, u, static_cast<int>(g), r0, std::min(16, R - r0), ch});
+                bwd.push_back(SolveItem{group[g], f, job_base[group[g]] + f, u, static_cast<int>(g), r0,
+                                        std::min(16, R - r0), ch});
         }
       }
   }
@@ -465,8 +502,7 @@ struct Engine {
     a.kc = kc;
     a.kr = kr;
     a.nf_max = nf_max;
-    a.cls = d_cls.p;
-    a.subs = d_subs.p;
+    a.jobs = jobs.p;
     a.vbuf = vbuf.p;
     a.vslot_stride = v_total_max * R;
     a.part = part.p;
@@ -504,7 +540,7 @@ struct Engine {
           const SolveItem& it = items[i];
           const FrontDesc& fd = classes[sub_cls[it.sub]]->sym->fronts[it.front];
           std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, it.sub, it.front,
-                       it.kind, it.idx, it.chunk, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k,
+                       i < nfwd ? 1 : 2, it.idx, it.chunk, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k,
                        fd.m);
         }
         std::fclose(fp);
@@ -1549,7 +1585,7 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
         const int q = (l - 1) * H.steps + st;
         HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * q], H.ev[2 + H.nsweeps + 2 * q]));
         sec += ms * 1e-3;
-        launches += 4;
+        launches += 2;  // forward + backward dataflow launches (the counter reset is a memset)
         for (int id : H.groups[((l - 1) % H.ndir) * H.steps + st]) {
           if (nz[static_cast<size_t>(l - 1) * nsub + id] == 0) continue;
           const SymbolicClass& c = *H.eng.classes[H.subs[id].cls]->sym;

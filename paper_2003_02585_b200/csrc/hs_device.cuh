@@ -63,12 +63,26 @@ struct DevGeom {
   long long gn;               // global node count
 };
 
-// A solve work item (hs_solve.cu). kind 1: forward band idx (32 padded rows of [M; W]) over
-// column-block chunk `chunk`; kind 2: backward column band idx (32 separator columns) over
-// block-row chunk `chunk`. RHS columns [r0, r0 + rw), rw <= 16. slot = position of the
-// subdomain in its step group.
+// A solve work item (hs_solve.cu): forward band idx (32 padded rows of [M; W]) over
+// column-block chunk `chunk`, or backward column band idx (32 separator columns) over
+// block-row chunk `chunk`; RHS columns [r0, r0 + rw), rw <= 16. slot = position of the
+// subdomain in its step group; job = its (subdomain, front) record.
 struct SolveItem {
-  int sub, front, kind, idx, slot, r0, rw, chunk;
+  int sub, front, job, idx, slot, r0, rw, chunk;
+};
+
+// Everything a solve item needs about its (subdomain, front), resolved on the host for the
+// current RHS width so an item costs two dependent loads (item, job) before its loads start.
+struct SolveJob {
+  const double2* factor;  // solve-layout factor of the front
+  const double2* dinv;    // 1/d of the separator (elimination order)
+  double2* x;             // the subdomain's x (elimination order, node-major x R)
+  double2* x1;            // the subdomain's z = D^-1 L^-1 b
+  const int2* pm;         // extend-add source map of the front's positions
+  const int* be;          // boundary elimination positions
+  int k, m, sep_off, v_off;
+  int child0, child1, nband_c0, nband_c1;  // children and their band counts (forward waits)
+  int parent, ncband_p, arr_off, part_off; // parent and its column-band count (backward waits)
 };
 
 struct FactorTask {

@@ -7,6 +7,7 @@ namespace hsb {
 
 struct SolveArgs {
   const SolveItem* items;
+  const SolveJob* jobs;
   int nitems;
   int R;           // RHS per batch (row stride of x / x1 / V)
   int ngr;         // RHS groups of 16
@@ -19,8 +20,6 @@ struct SolveArgs {
   unsigned* queue; // dynamic item counter, zeroed per launch
   unsigned long long* trace;  // optional per-item timestamps [4 * item]: dequeue, ready, done, smid
   int nf_max;
-  const DevClass* cls;
-  const DevSub* subs;
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side

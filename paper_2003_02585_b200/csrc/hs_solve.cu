@@ -67,15 +67,25 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
 }
 __device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
   if (lane == 0) {
-    while (ld_relaxed(p) < target) __nanosleep(32);
+    unsigned ns = 32;  // short backoff: waiters on the critical path must react quickly
+    while (ld_relaxed(p) < target) {
+      __nanosleep(ns);
+      ns = min(ns * 2, 256u);
+    }
     (void)ld_acquire(p);
   }
   __syncwarp();
 }
+// Release: the warp's stores are ordered before lane 0's release by the warp barrier (the
+// CUTLASS-semaphore pattern); no full fence.
 __device__ __forceinline__ void signal(int* p, int lane) {
-  __threadfence();
   __syncwarp();
   if (lane == 0) red_release_add(p, 1);
+}
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -101,15 +111,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 struct Geo {
   int kp, kb, nrb, nband, ncband;
 };
-__device__ __forceinline__ Geo geo_of(const DevFront& f) {
-  Geo g;
-  g.kp = (f.k + 7) & ~7;
-  g.kb = g.kp >> 3;
-  g.nrb = g.kb + ((f.m - f.k + 7) >> 3);
-  g.nband = (g.nrb + 3) >> 2;
-  g.ncband = (g.kb + 3) >> 2;
-  return g;
-}
 __device__ __forceinline__ long long band_base(int t, int kb) {
   const int j0 = kb >> 2;
   const long long s = t <= j0 ? 2LL * t * (t + 1) : 2LL * j0 * (j0 + 1) + static_cast<long long>(t - j0) * kb;
@@ -171,13 +172,11 @@ __device__ __forceinline__ bool split_reduce(Acc<NT>& c, double* base, long long
       for (int p = 0; p < 2; ++p)
 #pragma unroll
         for (int e = 0; e < 2; ++e) __stcg(mine + ((((i * NT + q) * 2 + p) * 2 + e) << 5), c.v[i][q][p][e]);
-  __threadfence();
   __syncwarp();
   int last = 0;
-  if (lane == 0) last = atomicAdd(arr, 1) == nch - 1;
+  if (lane == 0) last = atom_add_acq_rel(arr, 1) == nch - 1;
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return false;
-  __threadfence();
   acc_zero(c);
   for (int cc = 0; cc < nch; ++cc) {  // chunk order; own partial read back like the others
     const double* pc = base + cc * cstride + lane;
@@ -198,41 +197,46 @@ __device__ __forceinline__ void cp16(double2* dst, const double2* src, bool ok) 
                "l"(src), "r"(ok ? 16 : 0)
                : "memory");
 }
+template <int BYTES>
+__device__ __forceinline__ void cp_small(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "n"(BYTES)
+               : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Per-warp shared ring of NS k-steps: stage = A fragments (4 x 32 double2) then B parts
-// (NB x 2 x 32 double2: forward NB = 3 = rhs, child0 V, child1 V; backward NB = 1).
+// Per-warp shared memory: a ring of NS k-steps (stage = A fragments, 4 x 32 double2, then B
+// parts, NB x 2 x 32 double2: forward NB = 3 = rhs, child0 V, child1 V; backward NB = 1),
+// followed by the item's index slice (kIdx entries: source-map pairs / boundary positions).
+constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 template <bool FWD>
 struct Ring {
   static constexpr int NS = FWD ? 3 : 4;
   static constexpr int NB = FWD ? 3 : 1;
   static constexpr int kStage = (4 + NB * 2) * 32;  // double2
-  static constexpr int kWarp = NS * kStage;
+  static constexpr int kWarp = NS * kStage + kIdx / 2;
 };
 
-// The pipelined k-loop shared by both passes: issue(s, stage, idx) stages k-step s with
-// cp.async (idx = the step's index-table entry, fetched one step ahead by idx_of(s));
-// use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight
-// data costs shared memory, not registers.
-template <bool FWD, int NT, class IdxOf, class Issue, class Use>
-__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, IdxOf&& idx_of, Issue&& issue, Use&& use) {
+// The pipelined k-loop shared by both passes: issue(s, stage) stages k-step s with cp.async,
+// use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight data
+// costs shared memory, not registers.
+template <bool FWD, int NT, class Issue, class Use>
+__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use) {
   constexpr int NS = Ring<FWD>::NS, ST = Ring<FWD>::kStage;
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
-    if (j < ns) issue(j, ring + j * ST, idx_of(j));
+    if (j < ns) issue(j, ring + j * ST);
     cp_commit();
   }
-  int2 nxt = NS - 1 < ns ? idx_of(NS - 1) : make_int2(-1, -1);
 #pragma unroll 1
   for (int s = 0; s < ns; ++s) {
     const int si = s + NS - 1;
-    if (si < ns) issue(si, ring + (si % NS) * ST, nxt);
+    if (si < ns) issue(si, ring + (si % NS) * ST);
     cp_commit();
-    if (si + 1 < ns) nxt = idx_of(si + 1);
     cp_wait<NS - 1>();
     __syncwarp();
     double2 A[4], B[NT];
@@ -243,33 +247,80 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, IdxOf
   cp_wait<0>();
 }
 
+// Item ranges
+struct FwdRange {
+  int t, rbs, cb0, cb1;
+};
+__device__ __forceinline__ FwdRange fwd_range(const SolveArgs& a, const Geo& g, const SolveItem& it) {
+  FwdRange r;
+  r.t = it.idx;
+  r.rbs = min(4, g.nrb - 4 * r.t);
+  r.cb0 = it.chunk * a.kc;
+  r.cb1 = min(min(g.kb, 4 * r.t + 4), r.cb0 + a.kc);
+  return r;
+}
+struct BwdRange {
+  int u, a0, a1;
+};
+__device__ __forceinline__ BwdRange bwd_range(const SolveArgs& a, const Geo& g, const SolveItem& it) {
+  BwdRange r;
+  r.u = it.idx;
+  r.a0 = 4 * r.u + it.chunk * a.kr;
+  r.a1 = min(g.nrb, r.a0 + a.kr);
+  return r;
+}
+
+// Issued before the dependency wait: the item's factor range -> L2 (bulk prefetch) and its
+// index slice -> shared memory (cp.async group, waited for after the dependency wait).
+template <bool FWD>
+__device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it,
+                                              int2* sidx, int lane) {
+  if (FWD) {
+    const FwdRange r = fwd_range(a, g, it);
+    if (lane == 0)
+      prefetch_l2(J.factor + band_base(r.t, g.kb) + r.cb0 * r.rbs * 64,
+                  static_cast<unsigned>((r.cb1 - r.cb0) * r.rbs) * 1024u);
+    if (J.child0 >= 0 || J.child1 >= 0) {
+      const int n = min(8 * r.cb1, J.k) - 8 * r.cb0;
+      for (int j = lane; j < n; j += 32) cp_small<8>(sidx + j, J.pm + 8 * r.cb0 + j);
+    }
+  } else {
+    const BwdRange r = bwd_range(a, g, it);
+    if (lane == 0) {
+      const int ncol = min(4, g.kb - 4 * r.u);
+      for (int ta = r.a0 >> 2; ta <= (r.a1 - 1) >> 2; ++ta) {
+        const int rbs = min(4, g.nrb - 4 * ta);
+        prefetch_l2(J.factor + band_base(ta, g.kb) + 4 * r.u * rbs * 64, static_cast<unsigned>(ncol * rbs) * 1024u);
+      }
+    }
+    const int nb = J.m - J.k, lo = max(8 * r.a0, g.kp), hi = min(8 * r.a1, g.kp + nb);
+    for (int row = lo + lane; row < hi; row += 32) cp_small<4>(sidx + (row - 8 * r.a0), J.be + (row - g.kp));
+  }
+  cp_commit();
+}
+
 // ---------------------------------------------------------------------------------------
 // forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols]
 template <int NT>
-__device__ void fwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, const Geo& g,
-                         const SolveItem& it, double2* V, int* done, int lane, double2* ring) {
-  const int R = a.R, r0 = it.r0, rl = lane >> 2, t = it.idx;
-  const int rbs = min(4, g.nrb - 4 * t), ncb = min(g.kb, 4 * t + 4);
-  const int cb0 = it.chunk * a.kc, cb1 = min(ncb, cb0 + a.kc);
-  const double2* P = S.factor + fr.fac_off + band_base(t, g.kb) + rl * 8 + (lane & 3);
-  const double2* X = S.x + static_cast<long long>(fr.sep_off) * R;
-  const int2* pm = C.pmap + fr.t_off;
-  const bool leaf = fr.child0 < 0 && fr.child1 < 0;
-  auto col_of = [&](int s) { return 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
-  auto idx_of = [&](int s) {
-    const int col = col_of(s);
-    return (!leaf && col < fr.k) ? __ldg(pm + col) : make_int2(-1, -1);
-  };
-  auto issue = [&](int s, double2* st, int2 src) {
+__device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
+                         int* done, int lane, double2* ring, const int2* sidx) {
+  const int R = a.R, r0 = it.r0, rl = lane >> 2;
+  const FwdRange rg = fwd_range(a, g, it);
+  const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
+  const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
+  const double2* X = J.x + static_cast<long long>(J.sep_off) * R;
+  const bool leaf = J.child0 < 0 && J.child1 < 0;
+  auto issue = [&](int s, double2* st) {
     const double2* p = P + ((cb0 + (s >> 1)) * rbs) * 64 + 4 * (s & 1);
 #pragma unroll
     for (int i = 0; i < 4; ++i) cp16(st + i * 32 + lane, i < rbs ? p + i * 64 : P, i < rbs);
-    const int col = col_of(s);
+    const int col = 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3);
+    const int2 src = (!leaf && col < J.k) ? sidx[col - 8 * cb0] : make_int2(-1, -1);
     double2* sb = st + 4 * 32 + lane;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const int r = r0 + 8 * q + rl;
-      const bool ok = col < fr.k && r < R;
+      const bool ok = col < J.k && r < R;
       cp16(sb + (0 * 2 + q) * 32, ok ? X + static_cast<long long>(col) * R + r : X, ok);
       cp16(sb + (1 * 2 + q) * 32, ok && src.x >= 0 ? V + static_cast<long long>(src.x) * R + r : X, ok && src.x >= 0);
       cp16(sb + (2 * 2 + q) * 32, ok && src.y >= 0 ? V + static_cast<long long>(src.y) * R + r : X, ok && src.y >= 0);
@@ -289,33 +340,33 @@ __device__ void fwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
   };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, idx_of, issue, use);
+  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use);
   const int nch = nch_fwd(g, t, a.kc);
   if (nch > 1) {
     int loc = 0;
     for (int tt = 0; tt < t; ++tt) loc += nch_fwd(g, tt, a.kc);
-    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + fr.part_off + loc;
+    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
-    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + fr.arr_off + t) * a.ngr + r0 / 16;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + t) * a.ngr + r0 / 16;
     if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
   }
   // finalize: z = D^-1 (M T_sep) for separator rows, V = T_bnd - W T_sep for boundary rows
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int pr = 32 * t + 8 * i + rl;
-    if (pr < fr.k) {
-      const long long pos = fr.sep_off + pr;
-      const double2 d = S.dinv[pos];
+    if (pr < J.k) {
+      const double2 d = J.dinv[pr];
+      double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = r0 + 8 * q + 2 * (lane & 3) + e;
-          if (r < R) __stcg(&S.x1[pos * R + r], cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), d));
+          if (r < R) __stcg(zo + r, cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), d));
         }
-    } else if (pr >= g.kp && pr - g.kp < fr.m - fr.k) {
+    } else if (pr >= g.kp && pr - g.kp < J.m - J.k) {
       const int bi = pr - g.kp;
-      const int2 src = __ldg(pm + fr.k + bi);
+      const int2 src = leaf ? make_int2(-1, -1) : __ldg(J.pm + J.k + bi);
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
@@ -331,7 +382,8 @@ __device__ void fwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
             const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
             tb = make_double2(tb.x + w.x, tb.y + w.y);
           }
-          __stcg(&V[(fr.v_off + bi) * R + r], make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
+          __stcg(&V[static_cast<long long>(J.v_off + bi) * R + r],
+                 make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
         }
     }
   }
@@ -342,20 +394,16 @@ __device__ void fwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
 // backward column-band item: x_sep[32 cols][8 NT RHS] = sum over the chunk's rows of
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
 template <int NT>
-__device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S, const DevFront& fr, const Geo& g,
-                         const SolveItem& it, int* done, int lane, double2* ring) {
-  const int R = a.R, r0 = it.r0, rl = lane >> 2, u = it.idx;
-  const int a0 = 4 * u + it.chunk * a.kr, a1 = min(g.nrb, a0 + a.kr);
-  const double2* P = S.factor + fr.fac_off + (lane & 3) * 8 + rl;
-  const double2* Z = S.x1 + static_cast<long long>(fr.sep_off) * R;
-  const int* be = C.bnd_elim + fr.bnd_off;
-  const int nb = fr.m - fr.k;
+__device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int* done, int lane,
+                         double2* ring, const int2* sidx) {
+  const int R = a.R, r0 = it.r0, rl = lane >> 2;
+  const BwdRange rg = bwd_range(a, g, it);
+  const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
+  const double2* P = J.factor + (lane & 3) * 8 + rl;
+  const double2* Z = J.x1 + static_cast<long long>(J.sep_off) * R;
+  const int nb = J.m - J.k;
   auto row_of = [&](int s) { return 8 * (a0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
-  auto idx_of = [&](int s) {
-    const int row = row_of(s);
-    return make_int2(row >= g.kp && row - g.kp < nb ? __ldg(be + row - g.kp) : -1, 0);
-  };
-  auto issue = [&](int s, double2* st, int2 bi) {
+  auto issue = [&](int s, double2* st) {
     const int ab = a0 + (s >> 1), ta = ab >> 2, rbs = min(4, g.nrb - 4 * ta);
     const double2* p = P + band_base(ta, g.kb) + (ab & 3) * 64 + 32 * (s & 1);
 #pragma unroll
@@ -364,8 +412,11 @@ __device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
       cp16(st + i * 32 + lane, cbi < g.kb ? p + cbi * rbs * 64 : P, cbi < g.kb);
     }
     const int row = row_of(s);
-    const double2* src = row < fr.k ? Z + static_cast<long long>(row) * R
-                                    : (bi.x >= 0 ? S.x + static_cast<long long>(bi.x) * R : nullptr);
+    const double2* src = nullptr;
+    if (row < J.k)
+      src = Z + static_cast<long long>(row) * R;
+    else if (row >= g.kp && row - g.kp < nb)
+      src = J.x + static_cast<long long>(sidx[row - 8 * a0].x) * R;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const int r = r0 + 8 * q + rl;
@@ -376,7 +427,7 @@ __device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
   auto use = [&](int s, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) A[i] = st[i * 32 + lane];
-    const bool neg = row_of(s) >= fr.k;  // boundary rows enter as -x_bnd (zeros stay zero)
+    const bool neg = row_of(s) >= J.k;  // boundary rows enter as -x_bnd (zeros stay zero)
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const double2 v = st[(4 + q) * 32 + lane];
@@ -385,21 +436,21 @@ __device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
   };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<false, NT>(acc, 2 * (a1 - a0), ring, idx_of, issue, use);
+  kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use);
   const int nch = nch_bwd(g, u, a.kr);
   if (nch > 1) {
     int loc = 0;
     for (int uu = 0; uu < u; ++uu) loc += nch_bwd(g, uu, a.kr);
-    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + fr.part_off + loc;
+    const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
-    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + fr.arr_off + u) * a.ngr + r0 / 16;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + u) * a.ngr + r0 / 16;
     if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int col = 32 * u + 8 * i + rl;
-    if (col >= fr.k) continue;
-    double2* xo = S.x + static_cast<long long>(fr.sep_off + col) * R;
+    if (col >= J.k) continue;
+    double2* xo = J.x + static_cast<long long>(J.sep_off + col) * R;
 #pragma unroll
     for (int q = 0; q < NT; ++q)
 #pragma unroll
@@ -411,67 +462,70 @@ __device__ void bwd_item(const SolveArgs& a, const DevClass& C, const DevSub& S,
   signal(done + it.front, lane);
 }
 
+__device__ __forceinline__ Geo geo_km(int k, int m) {
+  Geo g;
+  g.kp = (k + 7) & ~7;
+  g.kb = g.kp >> 3;
+  g.nrb = g.kb + ((m - k + 7) >> 3);
+  g.nband = (g.nrb + 3) >> 2;
+  g.ncband = (g.kb + 3) >> 2;
+  return g;
+}
+
 template <bool FWD>
 __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
-  const int lane = threadIdx.x & 31;
-  double2* ring = smem_ring + (threadIdx.x >> 5) * Ring<FWD>::kWarp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* ring = smem_ring + warp * Ring<FWD>::kWarp;
+  int2* sidx = reinterpret_cast<int2*>(ring + Ring<FWD>::NS * Ring<FWD>::kStage);
+  // First round static: item i goes to warp i / gridDim.x of CTA i % gridDim.x, so the head
+  // of the list (the critical-path fronts of the backward pass) spreads over all SMs instead
+  // of packing onto the first CTAs' warps. Then dynamic dequeue past the static range. Every
+  // item below the dynamic ticket is held by a resident warp, so progress is guaranteed.
+  const int nstatic = gridDim.x * (kThreads / 32);
+  int first = blockIdx.x + warp * gridDim.x;
   for (;;) {
-    int it_idx = 0;
-    if (lane == 0) it_idx = static_cast<int>(atomicAdd(a.queue, 1u));
-    it_idx = __shfl_sync(0xffffffffu, it_idx, 0);
+    int it_idx = first;
+    if (first < 0) {
+      if (lane == 0) it_idx = nstatic + static_cast<int>(atomicAdd(a.queue, 1u));
+      it_idx = __shfl_sync(0xffffffffu, it_idx, 0);
+    }
+    first = -1;
     if (it_idx >= a.nitems) break;
     const SolveItem it = a.items[it_idx];
     if (a.nzmask[it.sub] == 0) continue;  // skipped subdomain: nothing depends on it
     unsigned long long* tr = a.trace ? a.trace + 4LL * it_idx : nullptr;
     if (tr && lane == 0) tr[0] = gtime();
-    const DevSub& S = a.subs[it.sub];
-    const DevClass& C = a.cls[S.cls];
-    const DevFront fr = C.fronts[it.front];
-    const Geo g = geo_of(fr);
+    const SolveJob J = a.jobs[it.job];
+    const Geo g = geo_km(J.k, J.m);
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
-    if (lane == 0) {  // factor range of this item -> L2, overlapping the dependency wait
-      const double2* F = S.factor + fr.fac_off;
-      if (FWD) {
-        const int t = it.idx, rbs = min(4, g.nrb - 4 * t), ncb = min(g.kb, 4 * t + 4);
-        const int cb0 = it.chunk * a.kc, cb1 = min(ncb, cb0 + a.kc);
-        prefetch_l2(F + band_base(t, g.kb) + cb0 * rbs * 64, static_cast<unsigned>((cb1 - cb0) * rbs) * 1024u);
-      } else {
-        const int u = it.idx, a0 = 4 * u + it.chunk * a.kr, a1 = min(g.nrb, a0 + a.kr);
-        const int ncol = min(4, g.kb - 4 * u);
-        for (int ta = a0 >> 2; ta <= (a1 - 1) >> 2; ++ta) {
-          const int rbs = min(4, g.nrb - 4 * ta);
-          prefetch_l2(F + band_base(ta, g.kb) + 4 * u * rbs * 64, static_cast<unsigned>(ncol * rbs) * 1024u);
-        }
-      }
-    }
+    item_prefetch<FWD>(a, J, g, it, sidx, lane);
     if (FWD) {
-#pragma unroll 1
-      for (int q = 0; q < 2; ++q) {
-        const int ch = q ? fr.child1 : fr.child0;
-        if (ch < 0) continue;
-        wait_count(done + ch, geo_of(C.fronts[ch]).nband * a.ngr, lane);
-      }
-    } else if (fr.parent >= 0) {
-      wait_count(done + fr.parent, geo_of(C.fronts[fr.parent]).ncband * a.ngr, lane);
+      if (J.child0 >= 0) wait_count(done + J.child0, J.nband_c0 * a.ngr, lane);
+      if (J.child1 >= 0) wait_count(done + J.child1, J.nband_c1 * a.ngr, lane);
+    } else if (J.parent >= 0) {
+      wait_count(done + J.parent, J.ncband_p * a.ngr, lane);
     }
+    cp_wait<0>();
+    __syncwarp();
     if (tr && lane == 0) tr[1] = gtime();
     double2* V = a.vbuf + it.slot * a.vslot_stride;
     if (FWD) {
       if (it.rw > 8)
-        fwd_item<2>(a, C, S, fr, g, it, V, done, lane, ring);
+        fwd_item<2>(a, J, g, it, V, done, lane, ring, sidx);
       else
-        fwd_item<1>(a, C, S, fr, g, it, V, done, lane, ring);
+        fwd_item<1>(a, J, g, it, V, done, lane, ring, sidx);
     } else {
       if (it.rw > 8)
-        bwd_item<2>(a, C, S, fr, g, it, done, lane, ring);
+        bwd_item<2>(a, J, g, it, done, lane, ring, sidx);
       else
-        bwd_item<1>(a, C, S, fr, g, it, done, lane, ring);
+        bwd_item<1>(a, J, g, it, done, lane, ring, sidx);
     }
     if (tr && lane == 0) {
       tr[2] = gtime();
       tr[3] = smid();
     }
+    __syncwarp();  // the index slice is rewritten by the next item
   }
 }
 
