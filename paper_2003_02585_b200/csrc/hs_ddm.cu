@@ -67,6 +67,7 @@ struct ClassDev {
   DBuf<int> bnd_elim, child_map, orig_fpos, orig_eidx, elim_of_local, local_of_elim;
   DBuf<int2> pmap;
   std::vector<DevFront> h_fronts;
+  std::vector<int> fkc, fkr;   // per front split-K chunk (column blocks / block rows)
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   std::vector<int> level_start_down;
   DevClass dev{};
@@ -89,12 +90,15 @@ struct Engine {
   long long v_total_max = 0, n_max = 0;
   // solve state
   int R = 0, nslots = 0, ngr = 1;
-  int kc = 8, kr = 4;                          // split-K chunks (column blocks / block rows)
+  int kc = 8, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
+  int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
   long long arr_total = 0, part_total = 0;     // per slot
   DBuf<double2> x, x1, vbuf;
   DBuf<double> part;
   DBuf<int> cnt;
-  std::vector<int> job_base;   // per subdomain: first job (subdomain, front) record
+  std::vector<int> job_base;   // per subdomain: first (subdomain, front) job of x buffer 0
+  int njobs = 0, nbuf = 1;     // jobs per x buffer; x buffers (sweeps in flight)
+  long long xstride = 0;       // elements between x buffers
   DBuf<SolveJob> jobs;
 
   ~Engine() {
@@ -360,12 +364,14 @@ struct Engine {
 
   // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains,
   // and the split-K bookkeeping of every front (arrival counters, partial tiles).
-  void ensure_solve(int r, int slots) {
-    if (r == R && slots <= nslots) return;
+  void ensure_solve(int r, int slots, int nb = 1) {
+    if (r == R && slots <= nslots && nb == nbuf) return;
     R = r;
+    nbuf = nb;
     ngr = (R + 15) / 16;
     if (const char* e = std::getenv("HS_KC")) kc = std::min(16, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
+    if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;
@@ -373,8 +379,15 @@ struct Engine {
       ClassDev& cd = *cdp;
       const SymbolicClass& c = *cd.sym;
       long long arr = 0, parts = 0;
+      cd.fkc.assign(c.fronts.size(), 16);
+      cd.fkr.assign(c.fronts.size(), 16);
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const int m = c.fronts[f].m, k = c.fronts[f].k;
+        if (c.fronts[f].depth < split_depth) {  // critical path: split long bands over many warps
+          cd.fkc[f] = kc;
+          cd.fkr[f] = kr;
+        }
+        const int fkc = cd.fkc[f], fkr = cd.fkr[f];
         const int kb = pad8(k) >> 3, nrb = kb + (pad8(m - k) >> 3);
         const int nband = (nrb + 3) / 4, ncband = (kb + 3) / 4;
         cd.h_fronts[f].arr_off = static_cast<int>(arr);
@@ -382,12 +395,12 @@ struct Engine {
         int pf = 0, pb = 0;
         bool split = false;
         for (int t = 0; t < nband; ++t) {
-          const int n = solve_fwd_chunks(m, k, t, kc);
+          const int n = solve_fwd_chunks(m, k, t, fkc);
           pf += n;
           split |= n > 1;
         }
         for (int u = 0; u < ncband; ++u) {
-          const int n = solve_bwd_chunks(m, k, u, kr);
+          const int n = solve_bwd_chunks(m, k, u, fkr);
           pb += n;
           split |= n > 1;
         }
@@ -399,8 +412,9 @@ struct Engine {
       part_total = std::max(part_total, parts);
     }
     const int nsub = static_cast<int>(sub_cls.size());
-    x.alloc(static_cast<size_t>(n_base[nsub]) * R);
-    x1.alloc(static_cast<size_t>(n_base[nsub]) * R);
+    xstride = static_cast<long long>(n_base[nsub]) * R;
+    x.alloc(static_cast<size_t>(xstride) * nbuf);
+    x1.alloc(static_cast<size_t>(xstride) * nbuf);
     vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
     part.alloc(static_cast<size_t>(std::max<long long>(part_total, 1)) * nslots * ngr * 1024);
     cnt.alloc(static_cast<size_t>(cnt_ints()));
@@ -412,7 +426,8 @@ struct Engine {
     // per (subdomain, front) job records for the solve kernels
     job_base.assign(nsub + 1, 0);
     for (int s = 0; s < nsub; ++s) job_base[s + 1] = job_base[s] + static_cast<int>(classes[sub_cls[s]]->sym->fronts.size());
-    std::vector<SolveJob> hj(job_base[nsub]);
+    njobs = job_base[nsub];
+    std::vector<SolveJob> hj(static_cast<size_t>(njobs) * nbuf);
     auto nband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + (pad8(d.m - d.k) >> 3) + 3) / 4; };
     auto ncband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + 3) / 4; };
     for (int s = 0; s < nsub; ++s) {
@@ -420,7 +435,7 @@ struct Engine {
       const SymbolicClass& c = *cd.sym;
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const FrontDesc& fd = c.fronts[f];
-        SolveJob& J = hj[job_base[s] + f];
+        SolveJob& J = hj[job_base[s] + f];  // buffer 0; copies below
         J.factor = factor.p + fac_base[s] + fd.fac_off;
         J.dinv = dinv.p + n_base[s] + fd.sep_off;
         J.x = h_subs[s].x;
@@ -439,8 +454,17 @@ struct Engine {
         J.ncband_p = fd.parent >= 0 ? ncband_of(c.fronts[fd.parent]) : 0;
         J.arr_off = cd.h_fronts[f].arr_off;
         J.part_off = cd.h_fronts[f].part_off;
+        J.kc = cd.fkc[f];
+        J.kr = cd.fkr[f];
       }
     }
+    for (int b = 1; b < nbuf; ++b)
+      for (int j = 0; j < njobs; ++j) {
+        SolveJob J = hj[j];
+        J.x += b * xstride;
+        J.x1 += b * xstride;
+        hj[static_cast<size_t>(b) * njobs + j] = J;
+      }
     jobs.upload(hj, stream);
   }
   // counter array: [done fwd | done bwd] per slot x front, [arrivals fwd | bwd], 2 queues
@@ -448,43 +472,50 @@ struct Engine {
     return 2LL * nslots * nf_max + 2LL * nslots * arr_total * ngr + 2;
   }
 
-  // Work items of the subdomains `group` (slot = position in the group), for the current R:
-  // forward = every front by height, its bands x column chunks x RHS groups; backward = every
-  // front by depth, its column bands x block-row chunks x RHS groups.
-  void build_items(const std::vector<int>& group, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
+  // Work items of the tasks of one macro-step (slot = position of the task): forward = every
+  // front by height, its bands x column chunks x RHS groups; backward = every front by depth,
+  // its column bands x block-row chunks x RHS groups. A task is (subdomain, sweep l, x buffer).
+  struct TaskRef {
+    int sub, l, xb;
+  };
+  void build_items(const std::vector<TaskRef>& tasks, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
+    const int nsub = static_cast<int>(sub_cls.size());
     int hmax = 0, dmax = 0;
-    for (int id : group) {
-      hmax = std::max(hmax, classes[sub_cls[id]]->sym->max_height);
-      dmax = std::max(dmax, classes[sub_cls[id]]->sym->max_depth);
+    for (const TaskRef& tk : tasks) {
+      hmax = std::max(hmax, classes[sub_cls[tk.sub]]->sym->max_height);
+      dmax = std::max(dmax, classes[sub_cls[tk.sub]]->sym->max_depth);
     }
     for (int h = 0; h <= hmax; ++h)
-      for (size_t g = 0; g < group.size(); ++g) {
-        const SymbolicClass& c = *classes[sub_cls[group[g]]]->sym;
+      for (size_t g = 0; g < tasks.size(); ++g) {
+        const TaskRef& tk = tasks[g];
+        const ClassDev& cd = *classes[sub_cls[tk.sub]];
+        const SymbolicClass& c = *cd.sym;
         if (h > c.max_height) continue;
+        const int nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
         for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
           const int f = c.order_up[q];
           const FrontDesc& fd = c.fronts[f];
           const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
           for (int t = 0; t < nband; ++t)
-            for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, kc); ++ch)
+            for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); ++ch)
               for (int r0 = 0; r0 < R; r0 += 16)
-                fwd.push_back(SolveItem{group[g], f, job_base[group[g]] + f, t, static_cast<int>(g), r0,
-                                        std::min(16, R - r0), ch});
+                fwd.push_back(SolveItem{nzi, f, jb + f, t, static_cast<int>(g), r0, std::min(16, R - r0), ch});
         }
       }
     for (int d = 0; d <= dmax; ++d)
-      for (size_t g = 0; g < group.size(); ++g) {
-        const ClassDev& cd = *classes[sub_cls[group[g]]];
+      for (size_t g = 0; g < tasks.size(); ++g) {
+        const TaskRef& tk = tasks[g];
+        const ClassDev& cd = *classes[sub_cls[tk.sub]];
         if (d > cd.sym->max_depth) continue;
+        const int nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
         for (int q = cd.level_start_down[d]; q < cd.level_start_down[d + 1]; ++q) {
           const int f = cd.sym->order_down[q];
           const FrontDesc& fd = cd.sym->fronts[f];
           const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
           for (int u = 0; u < ncband; ++u)
-            for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, kr); ++ch)
+            for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); ++ch)
               for (int r0 = 0; r0 < R; r0 += 16)
-                bwd.push_back(SolveItem{group[g], f, job_base[group[g]] + f, u, static_cast<int>(g), r0,
-                                        std::min(16, R - r0), ch});
+                bwd.push_back(SolveItem{nzi, f, jb + f, u, static_cast<int>(g), r0, std::min(16, R - r0), ch});
         }
       }
   }
@@ -499,8 +530,6 @@ struct Engine {
     SolveArgs a{};
     a.R = R;
     a.ngr = ngr;
-    a.kc = kc;
-    a.kr = kr;
     a.nf_max = nf_max;
     a.jobs = jobs.p;
     a.vbuf = vbuf.p;
@@ -538,8 +567,9 @@ struct Engine {
         std::fprintf(fp, "pass,sub,front,kind,idx,chunk,r0,rw,t_deq,t_ready,t_done,sm,k,m\n");
         for (int i = 0; i < nfwd + nbwd; ++i) {
           const SolveItem& it = items[i];
-          const FrontDesc& fd = classes[sub_cls[it.sub]]->sym->fronts[it.front];
-          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, it.sub, it.front,
+          const int sub = it.nzi % static_cast<int>(sub_cls.size());
+          const FrontDesc& fd = classes[sub_cls[sub]]->sym->fronts[it.front];
+          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, sub, it.front,
                        i < nfwd ? 1 : 2, it.idx, it.chunk, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k,
                        fd.m);
         }
@@ -621,7 +651,7 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
     if (H.items_R != R) {  // item lists depend on the RHS grouping
       H.fwd.clear();
       H.bwd.clear();
-      eng.build_items({0}, H.fwd, H.bwd);
+      eng.build_items({Engine::TaskRef{0, 1, 0}}, H.fwd, H.bwd);
       H.d_fwd.upload(H.fwd, eng.stream);
       H.d_bwd.upload(H.bwd, eng.stream);
       H.items_R = R;
@@ -779,9 +809,17 @@ struct DdmHandle {
   DevGeom geom{};
   int steps = 0, ndir = 4, dirs = 4, max_group = 1;
   long long line_max = 1;
-  std::vector<std::vector<int>> groups;  // [di * steps + s-1]
-  std::vector<int> grp_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
+  std::vector<std::vector<int>> groups;  // [di * steps + s-1]: the reference's step groups
+  std::vector<int> grp_off;
   DBuf<int> d_groups;
+  // Macro-step schedule (per rounds): tasks (subdomain, sweep) levelled by their longest
+  // dependency path, so sweeps overlap wherever the trace routing allows (build_schedule).
+  int nbuf = 1, max_width = 1;
+  std::vector<std::vector<int2>> msteps;   // per macro-step: (subdomain, sweep), ascending (sweep, id)
+  std::vector<std::vector<int>> acc_after; // per macro-step: sweeps accumulated after it, ascending
+  std::vector<int> mstep_of;               // [(l-1) * nsub + id] -> macro-step
+  std::vector<int> sweep_first_m, mt_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
+  DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
   DBuf<double2> d_coef;
   // per (R, rounds) state
@@ -793,7 +831,7 @@ struct DdmHandle {
   DBuf<int> route;
   DBuf<double2> bN, u, io;
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
-  std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l, then step pairs
+  std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l's accumulate, then macro-step solve pairs
   // global operator (lazy)
   bool gop_ready = false;
   long long g_nnz = 0;
@@ -807,6 +845,7 @@ struct DdmHandle {
 
   void build(const hs_problem& P, int device);
   void ensure_state(int r, int nrounds);
+  void build_schedule();
   void build_items();
   void ensure_gop();
   void run(int nrounds, bool track, bool timed);
@@ -1028,22 +1067,86 @@ void DdmHandle::build(const hs_problem& P, int device) {
   HS_CUDA(cudaStreamSynchronize(eng.stream));
 }
 
-// Work items of every (sweep direction, step) group for the current batch width.
+// Macro-step schedule of one application: task (l, id) runs one macro-step after the latest of
+//  * the tasks whose traces it consumes: (l', nb) with nb its neighbour across face (a, sign) and
+//    route_trace(l', a, sign) == l (src/sweeper.cpp:58-73, 285-307) — the only data it reads;
+//  * the accumulate of sweep l - nbuf, whose x buffer sweep l reuses.
+// Sweep accumulates stay in sweep order (u += contribution_l, src/sweeper.cpp:311), and every
+// mailbox slot has one writer, so the results equal the sequential order's: only independent
+// work is reordered. C2 (8x8, 4 sweeps): 60 sequential steps -> 29 macro-steps.
+void DdmHandle::build_schedule() {
+  const int nsub = geom.nsub;
+  nbuf = 4;
+  if (const char* e = std::getenv("HS_NBUF")) nbuf = std::max(1, std::atoi(e));
+  nbuf = std::min(nbuf, nsweeps);
+  std::vector<int> level(static_cast<size_t>(nsweeps) * nsub, 0), accl(nsweeps + 1, 0);
+  for (int l = 1; l <= nsweeps; ++l) {
+    std::vector<int> order(nsub);
+    for (int id = 0; id < nsub; ++id) order[id] = id;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      return step_of(part.counts, dim, plan[l - 1], subs[x].sub) < step_of(part.counts, dim, plan[l - 1], subs[y].sub);
+    });
+    int done = 0;
+    for (int id : order) {
+      int lev = l > nbuf ? accl[l - nbuf] : 0;
+      for (int ax = 0; ax < dim; ++ax)
+        for (int sg = -1; sg <= 1; sg += 2) {
+          Vec3i nb = subs[id].sub;
+          nb[ax] -= sg;  // the neighbour whose trace travels along (ax, sg) into id
+          if (nb[ax] < 0 || nb[ax] >= part.counts[ax]) continue;
+          const int nbid = static_cast<int>(part.flatten(nb));
+          const int d = 2 * ax + (sg > 0 ? 1 : 0);
+          for (int lp = 1; lp <= l; ++lp)
+            if (route_h[(lp - 1) * dirs + d] == l) lev = std::max(lev, level[static_cast<size_t>(lp - 1) * nsub + nbid]);
+        }
+      level[static_cast<size_t>(l - 1) * nsub + id] = lev + 1;
+      done = std::max(done, lev + 1);
+    }
+    accl[l] = std::max(done, accl[l - 1]);
+  }
+  const int nmacro = accl[nsweeps];
+  msteps.assign(nmacro, {});
+  acc_after.assign(nmacro, {});
+  mstep_of.assign(static_cast<size_t>(nsweeps) * nsub, 0);
+  sweep_first_m.assign(nsweeps + 1, nmacro);
+  for (int l = 1; l <= nsweeps; ++l) {
+    for (int id = 0; id < nsub; ++id) {
+      const int m = level[static_cast<size_t>(l - 1) * nsub + id] - 1;
+      msteps[m].push_back(make_int2(id, l));
+      mstep_of[static_cast<size_t>(l - 1) * nsub + id] = m;
+      sweep_first_m[l] = std::min(sweep_first_m[l], m);
+    }
+    acc_after[accl[l] - 1].push_back(l);
+  }
+  std::vector<int2> flat;
+  mt_off.assign(nmacro, 0);
+  max_width = 1;
+  for (int m = 0; m < nmacro; ++m) {
+    mt_off[m] = static_cast<int>(flat.size());
+    flat.insert(flat.end(), msteps[m].begin(), msteps[m].end());
+    max_width = std::max(max_width, static_cast<int>(msteps[m].size()));
+  }
+  d_mtasks.upload(flat, eng.stream);
+}
+
+// Work items of every macro-step for the current batch width.
 void DdmHandle::build_items() {
   std::vector<SolveItem> tasks;
-  const int ng = static_cast<int>(groups.size());
-  fwd_off.assign(ng, 0);
-  fwd_cnt.assign(ng, 0);
-  bwd_off.assign(ng, 0);
-  bwd_cnt.assign(ng, 0);
-  for (int gi = 0; gi < ng; ++gi) {
+  const int nm = static_cast<int>(msteps.size());
+  fwd_off.assign(nm, 0);
+  fwd_cnt.assign(nm, 0);
+  bwd_off.assign(nm, 0);
+  bwd_cnt.assign(nm, 0);
+  for (int m = 0; m < nm; ++m) {
+    std::vector<Engine::TaskRef> refs;
+    for (const int2& t : msteps[m]) refs.push_back(Engine::TaskRef{t.x, t.y, (t.y - 1) % nbuf});
     std::vector<SolveItem> fw, bw;
-    eng.build_items(groups[gi], fw, bw);
-    fwd_off[gi] = static_cast<int>(tasks.size());
-    fwd_cnt[gi] = static_cast<int>(fw.size());
+    eng.build_items(refs, fw, bw);
+    fwd_off[m] = static_cast<int>(tasks.size());
+    fwd_cnt[m] = static_cast<int>(fw.size());
     tasks.insert(tasks.end(), fw.begin(), fw.end());
-    bwd_off[gi] = static_cast<int>(tasks.size());
-    bwd_cnt[gi] = static_cast<int>(bw.size());
+    bwd_off[m] = static_cast<int>(tasks.size());
+    bwd_cnt[m] = static_cast<int>(bw.size());
     tasks.insert(tasks.end(), bw.begin(), bw.end());
   }
   d_tasks.upload(tasks, eng.stream);
@@ -1054,21 +1157,22 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   if (nrounds < 1) config_error("SweepPlan: rounds must be >= 1");
   const int ns = nrounds * ndir;
   if (ns > HS_MAX_SWEEPS || nrounds > HS_MAX_ROUNDS) config_error("ddm_solve: too many rounds");
-  eng.ensure_solve(r, max_group);
-  const bool changed = r != R || nrounds != rounds;
-  if (r != R) {
-    R = r;
-    build_items();
+  const bool new_rounds = nrounds != rounds, new_r = r != R;
+  if (new_rounds) {
+    rounds = nrounds;
+    nsweeps = ns;
+    plan = sweep_plan(dim, nrounds);
+    route_h.assign(nsweeps * dirs, 0);
+    for (int l = 1; l <= nsweeps; ++l)
+      for (int d = 0; d < dirs; ++d) route_h[(l - 1) * dirs + d] = route_trace(plan, dim, l, d / 2, (d & 1) ? 1 : -1);
+    route.upload(route_h, eng.stream);
+    build_schedule();
   }
-  if (!changed) return;
-  rounds = nrounds;
-  nsweeps = ns;
-  plan = sweep_plan(dim, nrounds);
+  eng.ensure_solve(r, max_width, nbuf);
+  if (!new_rounds && !new_r) return;
+  R = r;
+  build_items();
   const int nsub = geom.nsub;
-  route_h.assign(nsweeps * dirs, 0);
-  for (int l = 1; l <= nsweeps; ++l)
-    for (int d = 0; d < dirs; ++d) route_h[(l - 1) * dirs + d] = route_trace(plan, dim, l, d / 2, (d & 1) ? 1 : -1);
-  route.upload(route_h, eng.stream);
   mbox.alloc(static_cast<size_t>(nsub) * nsweeps * dirs * 2 * line_max * R);
   mpres.alloc(static_cast<size_t>(nsub) * nsweeps * dirs);
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
@@ -1082,7 +1186,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   rnum.alloc(static_cast<size_t>(nrounds) * R);
   rden.alloc(static_cast<size_t>(nrounds) * R);
   for (auto e : ev) cudaEventDestroy(e);
-  ev.assign(1 + nsweeps + 2 * nsweeps * steps, nullptr);
+  ev.assign(1 + nsweeps + 2 * msteps.size(), nullptr);
   for (auto& e : ev) HS_CUDA(cudaEventCreate(&e));
 }
 
@@ -1116,45 +1220,45 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
   sa.R = R;
   sa.nsweeps = nsweeps;
   sa.dirs = dirs;
+  sa.nbuf = nbuf;
+  sa.xstride = eng.xstride;
   sa.b = bN.p;
   sa.mbox = mbox.p;
   sa.mbox_dir_stride = 2 * line_max * R;
   sa.mpres = mpres.p;
   sa.nzmask = nzmask.p;
   sa.route = route.p;
-  for (int l = 1; l <= nsweeps; ++l) {
-    const int di = (l - 1) % ndir;
-    sa.l = l;
-    for (int st = 1; st <= steps; ++st) {
-      const int gi = di * steps + st - 1;
-      sa.group = d_groups.p + grp_off[gi];
-      sa.ngroup = static_cast<int>(groups[gi].size());
-      launch_build_rhs(sa, eng.n_max, s);
-      const unsigned* nz = nzmask.p + static_cast<size_t>(l - 1) * nsub;
-      if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
-      const bool traced = std::getenv("HS_TRACE") && l == 1 && st == (steps + 1) / 2;
-      eng.run_solve(d_tasks.p + fwd_off[gi], fwd_cnt[gi], d_tasks.p + bwd_off[gi], bwd_cnt[gi], nz, traced);
-      if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * ((l - 1) * steps + st - 1)], s));
-      launch_extract_deposit(sa, static_cast<int>(line_max), s);
-    }
-    AccumArgs aa{};
-    aa.g = geom;
-    aa.cls = eng.d_cls.p;
-    aa.subs = eng.d_subs.p;
-    aa.R = R;
-    aa.l = l;
-    for (int a = 0; a < 3; ++a) aa.dvec[a] = plan[l - 1][a];
-    aa.nzmask = nzmask.p + static_cast<size_t>(l - 1) * nsub;
-    aa.u = u.p;
-    aa.partial = partial.p;
-    const int nb = launch_accumulate(aa, s);
-    launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
-    if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
-    if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
-      const int rr = l / ndir - 1;
-      const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
-      launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
-      launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
+  const int nm = static_cast<int>(msteps.size());
+  for (int m = 0; m < nm; ++m) {
+    sa.tasks = d_mtasks.p + mt_off[m];
+    sa.ntasks = static_cast<int>(msteps[m].size());
+    launch_build_rhs(sa, eng.n_max, s);
+    if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * m], s));
+    const bool traced = std::getenv("HS_TRACE") && m == nm / 2;
+    eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
+    if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
+    launch_extract_deposit(sa, static_cast<int>(line_max), s);
+    for (int l : acc_after[m]) {
+      AccumArgs aa{};
+      aa.g = geom;
+      aa.cls = eng.d_cls.p;
+      aa.subs = eng.d_subs.p;
+      aa.R = R;
+      aa.l = l;
+      for (int a = 0; a < 3; ++a) aa.dvec[a] = plan[l - 1][a];
+      aa.xoff = static_cast<long long>((l - 1) % nbuf) * eng.xstride;
+      aa.nzmask = nzmask.p + static_cast<size_t>(l - 1) * nsub;
+      aa.u = u.p;
+      aa.partial = partial.p;
+      const int nb = launch_accumulate(aa, s);
+      launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
+      if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
+      if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
+        const int rr = l / ndir - 1;
+        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
+        launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
+        launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
+      }
     }
   }
 }
@@ -1173,20 +1277,29 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
     HS_CUDA(cudaMemcpyAsync(den.data(), rden.p, den.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
   }
   HS_CUDA(cudaStreamSynchronize(eng.stream));
-  std::vector<double> sweep_sec(nsweeps, 0.0), step_sec(static_cast<size_t>(nsweeps) * steps, 0.0);
+  const int nm = static_cast<int>(msteps.size());
+  std::vector<double> sweep_sec(nsweeps, 0.0), step_sec(nm, 0.0);
+  std::vector<int> active(nm, 0);
   float ms = 0.f;
-  for (int l = 1; l <= nsweeps; ++l) {
-    HS_CUDA(cudaEventElapsedTime(&ms, ev[l - 1], ev[l]));
+  for (int m = 0; m < nm; ++m) {
+    HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * m], ev[2 + nsweeps + 2 * m]));
+    step_sec[m] = ms * 1e-3;
+    for (const int2& t : msteps[m]) active[m] += nz[static_cast<size_t>(t.y - 1) * nsub + t.x] != 0;
+  }
+  for (int l = 1; l <= nsweeps; ++l) {  // from the sweep's first macro-step to its accumulate
+    HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * sweep_first_m[l]], ev[l]));
     sweep_sec[l - 1] = ms * 1e-3;
-    for (int st = 0; st < steps; ++st) {
-      const int q = (l - 1) * steps + st;
-      HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * q], ev[2 + nsweeps + 2 * q]));
-      step_sec[q] = ms * 1e-3;
+  }
+  if (const char* path = std::getenv("HS_STEP_TIMES")) {  // developer instrumentation
+    if (FILE* fp = std::fopen(path, "w")) {
+      std::fprintf(fp, "mstep,ntasks,active,solve_us\n");
+      for (int m = 0; m < nm; ++m)
+        std::fprintf(fp, "%d,%d,%d,%.2f\n", m, static_cast<int>(msteps[m].size()), active[m], 1e6 * step_sec[m]);
+      std::fclose(fp);
     }
   }
   double total = 0.0;
-  cudaEvent_t last = ev[nsweeps];
-  HS_CUDA(cudaEventElapsedTime(&ms, ev[0], last));
+  HS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[nsweeps]));
   total = ms * 1e-3;
   for (int r = 0; r < R; ++r) {
     hs_solve_report& rep = out[r];
@@ -1201,8 +1314,6 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
       rep.sweep_contrib_norm[l - 1] = std::sqrt(nrm[static_cast<size_t>(l - 1) * R + r]);
       for (int st = 1; st <= steps; ++st) {
         const auto& grp = groups[di * steps + st - 1];
-        int active = 0;
-        for (int id : grp) active += nz[static_cast<size_t>(l - 1) * nsub + id] != 0;
         for (int id : grp) {
           const bool nonzero = (nz[static_cast<size_t>(l - 1) * nsub + id] >> r) & 1u;
           if (!nonzero) {
@@ -1210,7 +1321,8 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
             continue;
           }
           ++rep.local_solves;
-          task_times.push_back(step_sec[(l - 1) * steps + st - 1] / std::max(active, 1));
+          const int m = mstep_of[static_cast<size_t>(l - 1) * nsub + id];
+          task_times.push_back(step_sec[m] / std::max(active[m], 1));
           const Vec3i sb = subs[id].sub;
           for (int d = 0; d < dirs; ++d) {
             if (!part.has_neighbor(sb, d / 2, (d & 1) ? 1 : -1)) continue;
@@ -1580,20 +1692,18 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
     double sec = 0.0, bytes = 0.0, flops = 0.0;
     int64_t launches = 0, solves = 0;
     float ms = 0.f;
-    for (int l = 1; l <= H.nsweeps; ++l)
-      for (int st = 0; st < H.steps; ++st) {
-        const int q = (l - 1) * H.steps + st;
-        HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * q], H.ev[2 + H.nsweeps + 2 * q]));
-        sec += ms * 1e-3;
-        launches += 2;  // forward + backward dataflow launches (the counter reset is a memset)
-        for (int id : H.groups[((l - 1) % H.ndir) * H.steps + st]) {
-          if (nz[static_cast<size_t>(l - 1) * nsub + id] == 0) continue;
-          const SymbolicClass& c = *H.eng.classes[H.subs[id].cls]->sym;
-          ++solves;
-          bytes += 2.0 * c.packed_entries * 16 + 2.0 * H.R * c.n * 16;
-          flops += 16.0 * c.packed_entries * H.R;
-        }
+    for (size_t m = 0; m < H.msteps.size(); ++m) {
+      HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * m], H.ev[2 + H.nsweeps + 2 * m]));
+      sec += ms * 1e-3;
+      launches += 2;  // forward + backward dataflow launches (the counter reset is a memset)
+      for (const int2& t : H.msteps[m]) {
+        if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
+        const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
+        ++solves;
+        bytes += 2.0 * c.packed_entries * 16 + 2.0 * H.R * c.n * 16;
+        flops += 16.0 * c.packed_entries * H.R;
       }
+    }
     if (solve_seconds) *solve_seconds = sec;
     if (solve_launches) *solve_launches = launches;
     if (subdomain_solves) *subdomain_solves = solves;

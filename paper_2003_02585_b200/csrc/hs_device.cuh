@@ -65,10 +65,11 @@ struct DevGeom {
 
 // A solve work item (hs_solve.cu): forward band idx (32 padded rows of [M; W]) over
 // column-block chunk `chunk`, or backward column band idx (32 separator columns) over
-// block-row chunk `chunk`; RHS columns [r0, r0 + rw), rw <= 16. slot = position of the
-// subdomain in its step group; job = its (subdomain, front) record.
+// block-row chunk `chunk`; RHS columns [r0, r0 + rw), rw <= 16. slot = position of the task
+// in its macro-step; job = its (x buffer, subdomain, front) record; nzi = the task's entry in the
+// per-(sweep, subdomain) nonzero masks.
 struct SolveItem {
-  int sub, front, job, idx, slot, r0, rw, chunk;
+  int nzi, front, job, idx, slot, r0, rw, chunk;
 };
 
 // Everything a solve item needs about its (subdomain, front), resolved on the host for the
@@ -83,6 +84,7 @@ struct SolveJob {
   int k, m, sep_off, v_off;
   int child0, child1, nband_c0, nband_c1;  // children and their band counts (forward waits)
   int parent, ncband_p, arr_off, part_off; // parent and its column-band count (backward waits)
+  int kc, kr;                              // split-K chunk: column blocks (forward) / block rows (backward)
 };
 
 struct FactorTask {

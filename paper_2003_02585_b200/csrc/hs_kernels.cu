@@ -265,16 +265,21 @@ __device__ __forceinline__ int weight2(const DevGeom& g, int axis, int cell, int
   return 2;
 }
 
+__device__ __forceinline__ double2* task_x(const SweepArgs& a, const DevSub& S, int l) {
+  return S.x + static_cast<long long>((l - 1) % a.nbuf) * a.xstride;
+}
+
 __global__ void rhs_init_kernel(SweepArgs a) {
-  const int sub = a.group[blockIdx.y];
+  const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
+  double2* X = task_x(a, S, l);
   const DevClass& C = a.cls[S.cls];
   const long long total = static_cast<long long>(C.n) * a.R;
   const int dim = a.g.dim;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     double2 v = czero();
-    if (a.l == 1) {  // split source: w(sub, p) * b[p] off the local shell (src/sweeper.cpp:189-202)
+    if (l == 1) {  // split source: w(sub, p) * b[p] off the local shell (src/sweeper.cpp:189-202)
       const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
       int local = C.local_of_elim[e];
       int p[3] = {0, 0, 0};
@@ -296,91 +301,95 @@ __global__ void rhs_init_kernel(SweepArgs a) {
         v = make_double2(w * bv.x, w * bv.y);
       }
     }
-    S.x[idx] = v;
+    X[idx] = v;
   }
 }
 
+// trace_to_source of the mailbox slots of sweep l (src/transfer.cpp:68-89). Deposits are kept per
+// generating sweep (one writer per slot); they are summed here in generating-sweep order, which is
+// the reference mailbox's "first deposit copies, later deposits add" (src/transfer.cpp:30-35).
 __global__ void inject_kernel(SweepArgs a) {
-  const int sub = a.group[blockIdx.x];
+  const int sub = a.tasks[blockIdx.x].x, l = a.tasks[blockIdx.x].y;
   const DevSub& S = a.subs[sub];
   const DevClass& C = a.cls[S.cls];
+  double2* X = task_x(a, S, l);
   const int R = a.R;
 #pragma unroll 1
   for (int d = 0; d < a.dirs; ++d) {  // canonical (axis, sign) order of src/sweeper.cpp:233-239
-    const long long slot = (static_cast<long long>(sub) * a.nsweeps + (a.l - 1)) * a.dirs + d;
-    const unsigned pres = a.mpres[slot];
-    if (pres == 0) continue;
+    unsigned any = 0;
+    for (int lg = 1; lg <= l; ++lg)
+      if (a.route[(lg - 1) * a.dirs + d] == l)
+        any |= a.mpres[(static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d];
+    if (any == 0) continue;
     const int len = C.line_len[d];
-    const double2* u0 = a.mbox + slot * a.mbox_dir_stride;
-    const double2* um1 = u0 + static_cast<long long>(len) * R;
     for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
       const int i = idx / R, r = idx % R;
-      if (!((pres >> r) & 1u)) continue;
+      if (!((any >> r) & 1u)) continue;
+      double2 u0 = czero(), um1 = czero();
+      bool first = true;
+      for (int lg = 1; lg <= l; ++lg) {
+        if (a.route[(lg - 1) * a.dirs + d] != l) continue;
+        const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
+        if (!((a.mpres[slot] >> r) & 1u)) continue;
+        const double2* s0 = a.mbox + slot * a.mbox_dir_stride;
+        const double2 v0 = s0[idx], v1 = s0[static_cast<long long>(len) * R + idx];
+        u0 = first ? v0 : cadd(u0, v0);
+        um1 = first ? v1 : cadd(um1, v1);
+        first = false;
+      }
       const double2 c = S.coef[d][i];
       const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
-      if (p0 >= 0) {
-        double2& y = S.x[static_cast<long long>(p0) * R + r];
-        cfms(y, c, um1[idx]);
-      }
-      if (pm >= 0) {
-        double2& y = S.x[static_cast<long long>(pm) * R + r];
-        cfma(y, c, u0[idx]);
-      }
+      if (p0 >= 0) cfms(X[static_cast<long long>(p0) * R + r], c, um1);
+      if (pm >= 0) cfma(X[static_cast<long long>(pm) * R + r], c, u0);
     }
     __syncthreads();
   }
 }
 
 __global__ void nonzero_kernel(SweepArgs a) {
-  const int sub = a.group[blockIdx.y];
+  const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
+  const double2* X = task_x(a, S, l);
   const DevClass& C = a.cls[S.cls];
   const long long total = static_cast<long long>(C.n) * a.R;
   unsigned bits = 0;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double2 v = S.x[idx];
+    const double2 v = X[idx];
     if (v.x != 0.0 || v.y != 0.0) bits |= 1u << (idx % a.R);
   }
   bits = __reduce_or_sync(kFull, bits);
-  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(a.l - 1) * a.g.nsub + sub], bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
 }
 
+// extract_trace (src/transfer.cpp:47-66) + route_trace (src/sweeper.cpp:58-73) + deposit into the
+// target's slot of this generating sweep (unique writer: plain stores, presence = RHS columns).
 __global__ void extract_deposit_kernel(SweepArgs a) {
-  const int sub = a.group[blockIdx.x];
+  const int sub = a.tasks[blockIdx.x].x, l = a.tasks[blockIdx.x].y;
   const int d = blockIdx.y;
   const int axis = d >> 1, sign = (d & 1) ? 1 : -1;
   const DevSub& S = a.subs[sub];
   const int t = S.sub[axis] + sign;
   if (t < 0 || t >= a.g.counts[axis]) return;
-  const int lp = a.route[(a.l - 1) * a.dirs + d];
-  if (lp == 0) return;
-  const unsigned nz = a.nzmask[static_cast<long long>(a.l - 1) * a.g.nsub + sub];
+  if (a.route[(l - 1) * a.dirs + d] == 0) return;
+  const unsigned nz = a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub];
   if (nz == 0) return;
   int stride = 1;
   for (int ax = 0; ax < axis; ++ax) stride *= a.g.counts[ax];
   const int target = sub + sign * stride;
   const DevClass& C = a.cls[S.cls];
+  const double2* X = task_x(a, S, l);
   const int R = a.R, len = C.line_len[d];
-  const long long slot = (static_cast<long long>(target) * a.nsweeps + (lp - 1)) * a.dirs + d;
-  const unsigned pres = a.mpres[slot];
+  const long long slot = (static_cast<long long>(target) * a.nsweeps + (l - 1)) * a.dirs + d;
   double2* u0 = a.mbox + slot * a.mbox_dir_stride;
   double2* um1 = u0 + static_cast<long long>(len) * R;
   for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
     const int i = idx / R, r = idx % R;
     if (!((nz >> r) & 1u)) continue;
-    const double2 v0 = S.x[static_cast<long long>(C.ext_u0[d][i]) * R + r];
-    const double2 v1 = S.x[static_cast<long long>(C.ext_um1[d][i]) * R + r];
-    if ((pres >> r) & 1u) {  // TraceMailbox::deposit accumulates (src/transfer.cpp:30-35)
-      u0[idx] = cadd(u0[idx], v0);
-      um1[idx] = cadd(um1[idx], v1);
-    } else {
-      u0[idx] = v0;
-      um1[idx] = v1;
-    }
+    u0[idx] = X[static_cast<long long>(C.ext_u0[d][i]) * R + r];
+    um1[idx] = X[static_cast<long long>(C.ext_um1[d][i]) * R + r];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) a.mpres[slot] = pres | nz;
+  if (threadIdx.x == 0) a.mpres[slot] = nz;
 }
 
 __global__ void accumulate_kernel(AccumArgs a) {
@@ -450,7 +459,7 @@ __global__ void accumulate_kernel(AccumArgs a) {
         local += static_cast<long long>(p[ax] - S.lo[ax]) * ls;
         ls *= C.size[ax];
       }
-      const double2 xv = S.x[static_cast<long long>(C.elim_of_local[local]) * R + r];
+      const double2 xv = S.x[a.xoff + static_cast<long long>(C.elim_of_local[local]) * R + r];
       acc.x += wts[i] * xv.x;
       acc.y += wts[i] * xv.y;
     }
@@ -611,16 +620,16 @@ void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s) {
 
 void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s) {
   const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 64));
-  rhs_init_kernel<<<dim3(bx, a.ngroup), kThreads, 0, s>>>(a);
+  rhs_init_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
-  inject_kernel<<<a.ngroup, kThreads, 0, s>>>(a);
+  inject_kernel<<<a.ntasks, kThreads, 0, s>>>(a);
   after_launch();
-  nonzero_kernel<<<dim3(bx, a.ngroup), kThreads, 0, s>>>(a);
+  nonzero_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
 }
 
 void launch_extract_deposit(const SweepArgs& a, int, cudaStream_t s) {
-  extract_deposit_kernel<<<dim3(a.ngroup, a.dirs), kThreads, 0, s>>>(a);
+  extract_deposit_kernel<<<dim3(a.ntasks, a.dirs), kThreads, 0, s>>>(a);
   after_launch();
 }
 

@@ -11,7 +11,6 @@ struct SolveArgs {
   int nitems;
   int R;           // RHS per batch (row stride of x / x1 / V)
   int ngr;         // RHS groups of 16
-  int kc, kr;      // split-K chunk: column blocks per forward item, block rows per backward item
   int* done;       // per [slot * nf_max + front]: finalized (band, group) pairs of this pass
   int* arr;        // split-K arrivals per [(slot * arr_stride + arr_off + band) * ngr + group]
   long long arr_stride;
@@ -50,16 +49,17 @@ struct SweepArgs {
   DevGeom g;
   const DevClass* cls;
   const DevSub* subs;
-  const int* group;        // subdomains of the step group (ascending flattened id)
-  int ngroup;
+  const int2* tasks;       // (subdomain, 1-based sweep) of every task of the macro-step
+  int ntasks;
   int R;
-  int l;                   // 1-based sweep index
   int nsweeps;
   int dirs;                // 2*dim
+  int nbuf;                // x buffers: sweep l uses buffer (l-1) % nbuf
+  long long xstride;       // elements between x buffers
   const double2* b;        // global rhs, node-major N x R
-  double2* mbox;           // mailbox slots [sub][sweep][dir][2][line][R]
+  double2* mbox;           // mailbox slots [target sub][generating sweep][dir][2][line][R]
   long long mbox_dir_stride;  // elements per (sub, sweep, dir) slot
-  unsigned* mpres;         // presence bitmask [sub][sweep][dir]
+  unsigned* mpres;         // presence bitmask [target sub][generating sweep][dir]
   unsigned* nzmask;        // [sweep][sub]
   const int* route;        // [sweep][dir] target sweep (0 = discard)
 };
@@ -76,6 +76,7 @@ struct AccumArgs {
   int R;
   int l;
   int dvec[3];               // sweep direction of sweep l
+  long long xoff;            // offset of sweep l's x buffer (elements)
   const unsigned* nzmask;    // [sub] for sweep l
   double2* u;                // global solution, node-major N x R
   double* partial;           // per-block partial |contrib|^2 [nblocks][R]

@@ -251,22 +251,22 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
 struct FwdRange {
   int t, rbs, cb0, cb1;
 };
-__device__ __forceinline__ FwdRange fwd_range(const SolveArgs& a, const Geo& g, const SolveItem& it) {
+__device__ __forceinline__ FwdRange fwd_range(const SolveJob& J, const Geo& g, const SolveItem& it) {
   FwdRange r;
   r.t = it.idx;
   r.rbs = min(4, g.nrb - 4 * r.t);
-  r.cb0 = it.chunk * a.kc;
-  r.cb1 = min(min(g.kb, 4 * r.t + 4), r.cb0 + a.kc);
+  r.cb0 = it.chunk * J.kc;
+  r.cb1 = min(min(g.kb, 4 * r.t + 4), r.cb0 + J.kc);
   return r;
 }
 struct BwdRange {
   int u, a0, a1;
 };
-__device__ __forceinline__ BwdRange bwd_range(const SolveArgs& a, const Geo& g, const SolveItem& it) {
+__device__ __forceinline__ BwdRange bwd_range(const SolveJob& J, const Geo& g, const SolveItem& it) {
   BwdRange r;
   r.u = it.idx;
-  r.a0 = 4 * r.u + it.chunk * a.kr;
-  r.a1 = min(g.nrb, r.a0 + a.kr);
+  r.a0 = 4 * r.u + it.chunk * J.kr;
+  r.a1 = min(g.nrb, r.a0 + J.kr);
   return r;
 }
 
@@ -276,7 +276,7 @@ template <bool FWD>
 __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it,
                                               int2* sidx, int lane) {
   if (FWD) {
-    const FwdRange r = fwd_range(a, g, it);
+    const FwdRange r = fwd_range(J, g, it);
     if (lane == 0)
       prefetch_l2(J.factor + band_base(r.t, g.kb) + r.cb0 * r.rbs * 64,
                   static_cast<unsigned>((r.cb1 - r.cb0) * r.rbs) * 1024u);
@@ -285,7 +285,7 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
       for (int j = lane; j < n; j += 32) cp_small<8>(sidx + j, J.pm + 8 * r.cb0 + j);
     }
   } else {
-    const BwdRange r = bwd_range(a, g, it);
+    const BwdRange r = bwd_range(J, g, it);
     if (lane == 0) {
       const int ncol = min(4, g.kb - 4 * r.u);
       for (int ta = r.a0 >> 2; ta <= (r.a1 - 1) >> 2; ++ta) {
@@ -305,7 +305,7 @@ template <int NT>
 __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
                          int* done, int lane, double2* ring, const int2* sidx) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
-  const FwdRange rg = fwd_range(a, g, it);
+  const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
   const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
   const double2* X = J.x + static_cast<long long>(J.sep_off) * R;
@@ -341,10 +341,10 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use);
-  const int nch = nch_fwd(g, t, a.kc);
+  const int nch = nch_fwd(g, t, J.kc);
   if (nch > 1) {
     int loc = 0;
-    for (int tt = 0; tt < t; ++tt) loc += nch_fwd(g, tt, a.kc);
+    for (int tt = 0; tt < t; ++tt) loc += nch_fwd(g, tt, J.kc);
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
     int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + t) * a.ngr + r0 / 16;
@@ -397,7 +397,7 @@ template <int NT>
 __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int* done, int lane,
                          double2* ring, const int2* sidx) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
-  const BwdRange rg = bwd_range(a, g, it);
+  const BwdRange rg = bwd_range(J, g, it);
   const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
   const double2* P = J.factor + (lane & 3) * 8 + rl;
   const double2* Z = J.x1 + static_cast<long long>(J.sep_off) * R;
@@ -437,10 +437,10 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use);
-  const int nch = nch_bwd(g, u, a.kr);
+  const int nch = nch_bwd(g, u, J.kr);
   if (nch > 1) {
     int loc = 0;
-    for (int uu = 0; uu < u; ++uu) loc += nch_bwd(g, uu, a.kr);
+    for (int uu = 0; uu < u; ++uu) loc += nch_bwd(g, uu, J.kr);
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
     int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + u) * a.ngr + r0 / 16;
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
     first = -1;
     if (it_idx >= a.nitems) break;
     const SolveItem it = a.items[it_idx];
-    if (a.nzmask[it.sub] == 0) continue;  // skipped subdomain: nothing depends on it
+    if (a.nzmask[it.nzi] == 0) continue;  // skipped task (exactly-zero RHS): nothing depends on it
     unsigned long long* tr = a.trace ? a.trace + 4LL * it_idx : nullptr;
     if (tr && lane == 0) tr[0] = gtime();
     const SolveJob J = a.jobs[it.job];
