@@ -93,7 +93,7 @@ struct Engine {
   int kc = 8, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
   int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
   long long arr_total = 0, part_total = 0;     // per slot
-  DBuf<double2> x, x1, vbuf;
+  DBuf<double2> x, x1, rb, vbuf;
   DBuf<double> part;
   DBuf<int> cnt;
   std::vector<int> job_base;   // per subdomain: first (subdomain, front) job of x buffer 0
@@ -415,12 +415,15 @@ struct Engine {
     xstride = static_cast<long long>(n_base[nsub]) * R;
     x.alloc(static_cast<size_t>(xstride) * nbuf);
     x1.alloc(static_cast<size_t>(xstride) * nbuf);
+    rb.alloc(static_cast<size_t>(xstride) * nbuf);
+    rb.zero(stream);  // right-hand sides are zero off their injection lines between uses
     vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
     part.alloc(static_cast<size_t>(std::max<long long>(part_total, 1)) * nslots * ngr * 1024);
     cnt.alloc(static_cast<size_t>(cnt_ints()));
     for (int s = 0; s < nsub; ++s) {
       h_subs[s].x = x.p + n_base[s] * R;
       h_subs[s].x1 = x1.p + n_base[s] * R;
+      h_subs[s].rb = rb.p + n_base[s] * R;
     }
     d_subs.upload(h_subs, stream);
     // per (subdomain, front) job records for the solve kernels
@@ -440,6 +443,7 @@ struct Engine {
         J.dinv = dinv.p + n_base[s] + fd.sep_off;
         J.x = h_subs[s].x;
         J.x1 = h_subs[s].x1;
+        J.b = h_subs[s].rb;
         J.pm = cd.pmap.p + fd.t_off;
         J.be = cd.bnd_elim.p + fd.bnd_off;
         J.k = fd.k;
@@ -463,6 +467,7 @@ struct Engine {
         SolveJob J = hj[j];
         J.x += b * xstride;
         J.x1 += b * xstride;
+        J.b += b * xstride;
         hj[static_cast<size_t>(b) * njobs + j] = J;
       }
     jobs.upload(hj, stream);
@@ -666,7 +671,7 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
     double2* xb = d_x + b0 * n;
     const int threads = 256;
     const int blocks = static_cast<int>((n * R + threads - 1) / threads);
-    gather_in_kernel<<<blocks, threads, 0, eng.stream>>>(xb, eng.x.p, eng.classes[0]->local_of_elim.p, n, R);
+    gather_in_kernel<<<blocks, threads, 0, eng.stream>>>(xb, eng.rb.p, eng.classes[0]->local_of_elim.p, n, R);
     g_kernel_launches.fetch_add(1);
     HS_CUDA(cudaGetLastError());
     const unsigned mask = R >= 32 ? ~0u : ((1u << R) - 1u);
@@ -821,6 +826,7 @@ struct DdmHandle {
   std::vector<int> sweep_first_m, mt_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
+  DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
   DBuf<double2> d_coef;
   // per (R, rounds) state
   int R = 0, nsweeps = 0, rounds = 0;
@@ -1047,6 +1053,44 @@ void DdmHandle::build(const hs_problem& P, int device) {
     geom.counts[a] = part.counts[a];
     geom.cut_w[a] = a < dim ? intervals[a] / part.counts[a] : 1;
   }
+  {  // accumulate plan (src/transfer.cpp:91-102): per global node, every subdomain whose support
+     // holds it, as (x position n_base[sub] + elim, sub << 4 | weight numerator)
+    const long long gn = geom.gn;
+    std::vector<int> off(gn, 0);
+    std::vector<int2> ent;
+    auto visit = [&](auto&& fn) {
+      for (int id = 0; id < nsub; ++id) {
+        const GridRange sup = wts.support(subs[id].sub);
+        const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
+        Vec3i p{0, 0, 0};
+        for (p[2] = sup.lo[2]; p[2] <= (dim > 2 ? sup.hi[2] : sup.lo[2]); ++p[2])
+          for (p[1] = sup.lo[1]; p[1] <= sup.hi[1]; ++p[1])
+            for (p[0] = sup.lo[0]; p[0] <= sup.hi[0]; ++p[0]) {
+              int num = 1;
+              long long g = 0, gs = 1, loc = 0, ls = 1;
+              for (int ax = 0; ax < dim; ++ax) {
+                num *= wts.weight2(ax, subs[id].sub[ax], p[ax]);
+                g += static_cast<long long>(p[ax] - geom.glo[ax]) * gs;
+                gs *= geom.gsize[ax];
+                loc += static_cast<long long>(p[ax] - subs[id].range.lo[ax]) * ls;
+                ls *= c.size[ax];
+              }
+              if (num != 0) fn(g, id, num, c.elim_of_local[loc]);
+            }
+      }
+    };
+    const int E = 1 << dim;
+    for (int a = 0; a < dim; ++a)
+      if (part.counts[a] > 256) config_error("partition: more than 256 subdomains per axis");
+    ent.assign(static_cast<size_t>(gn) * E, make_int2(-1, 0));
+    visit([&](long long g, int id, int num, int e) {
+      if (off[g] >= E) throw Error(kInternal, "accumulate plan: more than 2^dim subdomains at a node");
+      const Vec3i& c = subs[id].sub;
+      ent[static_cast<size_t>(g) * E + off[g]++] =
+          make_int2(static_cast<int>(eng.n_base[id] + e), c[0] | (c[1] << 8) | (c[2] << 16) | (num << 24));
+    });
+    acc_ent.upload(ent, eng.stream);
+  }
   // step groups and dataflow task lists per (sweep direction, step)
   steps = sweep_step_count(part.counts, dim);
   ndir = 1 << dim;
@@ -1241,8 +1285,8 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
     for (int l : acc_after[m]) {
       AccumArgs aa{};
       aa.g = geom;
-      aa.cls = eng.d_cls.p;
-      aa.subs = eng.d_subs.p;
+      aa.x = eng.x.p;
+      aa.acc_ent = acc_ent.p;
       aa.R = R;
       aa.l = l;
       for (int a = 0; a < 3; ++a) aa.dvec[a] = plan[l - 1][a];

@@ -49,6 +49,8 @@ struct DevSub {
   const double2* val;         // CSR values (factorization input)
   double2* x;                 // solve vector, elimination order, node-major x R (rhs -> solution)
   double2* x1;                // forward result z = D^-1 L^-1 b (same layout)
+  double2* rb;                // right-hand side of the task (same layout); zero off the injection
+                              // lines except while a sweep-1 task holds its split source
   const double2* coef[kMaxDirs];  // injection couplings per incoming direction
 };
 
@@ -79,6 +81,7 @@ struct SolveJob {
   const double2* dinv;    // 1/d of the separator (elimination order)
   double2* x;             // the subdomain's x (elimination order, node-major x R)
   double2* x1;            // the subdomain's z = D^-1 L^-1 b
+  const double2* b;       // the subdomain's right-hand side (forward input)
   const int2* pm;         // extend-add source map of the front's positions
   const int* be;          // boundary elimination positions
   int k, m, sep_off, v_off;

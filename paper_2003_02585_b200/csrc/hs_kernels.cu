@@ -265,21 +265,43 @@ __device__ __forceinline__ int weight2(const DevGeom& g, int axis, int cell, int
   return 2;
 }
 
+constexpr int HS_SLOTS_PER_DIR = 16;  // generating sweeps that can route into one sweep and face
+
 __device__ __forceinline__ double2* task_x(const SweepArgs& a, const DevSub& S, int l) {
   return S.x + static_cast<long long>((l - 1) % a.nbuf) * a.xstride;
 }
+__device__ __forceinline__ double2* task_b(const SweepArgs& a, const DevSub& S, int l) {
+  return S.rb + static_cast<long long>((l - 1) % a.nbuf) * a.xstride;
+}
 
+// RHS of a task before injection (src/sweeper.cpp:189-239). Sweep 1: the split source
+// w(sub, p) * b[p] off the local shell (src/sweeper.cpp:189-202), written over the whole buffer.
+// Later sweeps: zero, which the buffer already is except on the injection lines of its previous
+// use; those are cleared (the whole buffer when that use was a sweep-1 task).
 __global__ void rhs_init_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
-  double2* X = task_x(a, S, l);
+  double2* B = task_b(a, S, l);
   const DevClass& C = a.cls[S.cls];
-  const long long total = static_cast<long long>(C.n) * a.R;
   const int dim = a.g.dim;
+  if (l > 1 && l - a.nbuf != 1) {  // lines only
+    for (int d = 0; d < a.dirs; ++d) {
+      const int len = C.line_len[d];
+      for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * a.R;
+           idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
+        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+        if (p0 >= 0) B[static_cast<long long>(p0) * a.R + r] = czero();
+        if (pm >= 0) B[static_cast<long long>(pm) * a.R + r] = czero();
+      }
+    }
+    return;
+  }
+  const long long total = static_cast<long long>(C.n) * a.R;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     double2 v = czero();
-    if (l == 1) {  // split source: w(sub, p) * b[p] off the local shell (src/sweeper.cpp:189-202)
+    if (l == 1) {
       const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
       int local = C.local_of_elim[e];
       int p[3] = {0, 0, 0};
@@ -301,7 +323,7 @@ __global__ void rhs_init_kernel(SweepArgs a) {
         v = make_double2(w * bv.x, w * bv.y);
       }
     }
-    X[idx] = v;
+    B[idx] = v;
   }
 }
 
@@ -312,31 +334,45 @@ __global__ void inject_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.x].x, l = a.tasks[blockIdx.x].y;
   const DevSub& S = a.subs[sub];
   const DevClass& C = a.cls[S.cls];
-  double2* X = task_x(a, S, l);
+  double2* X = task_b(a, S, l);  // the task's right-hand side
   const int R = a.R;
+  // contributing slots per direction (generating sweeps routed to l, ascending), once per block
+  __shared__ long long s_slot[kMaxDirs][HS_SLOTS_PER_DIR];
+  __shared__ unsigned s_pres[kMaxDirs][HS_SLOTS_PER_DIR];
+  __shared__ int s_n[kMaxDirs];
+  if (threadIdx.x < a.dirs) {
+    const int d = threadIdx.x;
+    int n = 0;
+    for (int lg = 1; lg <= l && n < HS_SLOTS_PER_DIR; ++lg) {
+      if (a.route[(lg - 1) * a.dirs + d] != l) continue;
+      const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
+      const unsigned pres = a.mpres[slot];
+      if (pres == 0) continue;
+      s_slot[d][n] = slot;
+      s_pres[d][n] = pres;
+      ++n;
+    }
+    s_n[d] = n;
+  }
+  __syncthreads();
 #pragma unroll 1
   for (int d = 0; d < a.dirs; ++d) {  // canonical (axis, sign) order of src/sweeper.cpp:233-239
-    unsigned any = 0;
-    for (int lg = 1; lg <= l; ++lg)
-      if (a.route[(lg - 1) * a.dirs + d] == l)
-        any |= a.mpres[(static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d];
-    if (any == 0) continue;
+    const int n = s_n[d];
+    if (n == 0) continue;
     const int len = C.line_len[d];
     for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
       const int i = idx / R, r = idx % R;
-      if (!((any >> r) & 1u)) continue;
       double2 u0 = czero(), um1 = czero();
       bool first = true;
-      for (int lg = 1; lg <= l; ++lg) {
-        if (a.route[(lg - 1) * a.dirs + d] != l) continue;
-        const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
-        if (!((a.mpres[slot] >> r) & 1u)) continue;
-        const double2* s0 = a.mbox + slot * a.mbox_dir_stride;
+      for (int k = 0; k < n; ++k) {
+        if (!((s_pres[d][k] >> r) & 1u)) continue;
+        const double2* s0 = a.mbox + s_slot[d][k] * a.mbox_dir_stride;
         const double2 v0 = s0[idx], v1 = s0[static_cast<long long>(len) * R + idx];
         u0 = first ? v0 : cadd(u0, v0);
         um1 = first ? v1 : cadd(um1, v1);
         first = false;
       }
+      if (first) continue;
       const double2 c = S.coef[d][i];
       const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
       if (p0 >= 0) cfms(X[static_cast<long long>(p0) * R + r], c, um1);
@@ -344,12 +380,35 @@ __global__ void inject_kernel(SweepArgs a) {
     }
     __syncthreads();
   }
+  if (l > 1) {  // RHS = traces only: nonzero columns are found on the injection lines
+    unsigned bits = 0;
+    for (int d = 0; d < a.dirs; ++d) {
+      const int len = C.line_len[d];
+      for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
+        const int i = idx / R, r = idx % R;
+        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+        if (p0 >= 0) {
+          const double2 v = X[static_cast<long long>(p0) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+        }
+        if (pm >= 0) {
+          const double2 v = X[static_cast<long long>(pm) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+        }
+      }
+    }
+    bits = __reduce_or_sync(kFull, bits);
+    if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
+  }
 }
 
+// Exact-zero test of a task's RHS (src/sweeper.cpp:240-251) for sweep 1 (split source + traces);
+// for sweeps >= 2 the RHS is zero off the injection lines and inject_kernel tests those.
 __global__ void nonzero_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
+  if (l > 1) return;
   const DevSub& S = a.subs[sub];
-  const double2* X = task_x(a, S, l);
+  const double2* X = task_b(a, S, l);
   const DevClass& C = a.cls[S.cls];
   const long long total = static_cast<long long>(C.n) * a.R;
   unsigned bits = 0;
@@ -392,79 +451,64 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   if (threadIdx.x == 0) a.mpres[slot] = nz;
 }
 
-__global__ void accumulate_kernel(AccumArgs a) {
+// u += sum over the subdomains whose support holds the node of w * u_local, in the reference's
+// order (step of the sweep, then ascending id: src/sweeper.cpp:285-309, src/transfer.cpp:91-102).
+// The (position, subdomain, weight) entries of each node are precomputed on the host.
+template <int E>
+__global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   __shared__ double red[kThreads];
   const int dim = a.g.dim, R = a.R;
   const int npb = kThreads / R;  // whole nodes per block so thread t always owns column t % R
   const long long node = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
   const int r = threadIdx.x % R;
-  const long long idx = node * R + r;
   double nrm = 0.0;
   if (threadIdx.x < npb * R && node < a.g.gn) {
-    int p[3] = {0, 0, 0};
-    long long rem = node;
-    for (int ax = 0; ax < dim; ++ax) {
-      p[ax] = a.g.glo[ax] + static_cast<int>(rem % a.g.gsize[ax]);
-      rem /= a.g.gsize[ax];
-    }
-    // candidate cells per axis (at most two have nonzero weight)
-    int cand[3][2], cw[3][2], nc[3];
-    for (int ax = 0; ax < 3; ++ax) nc[ax] = 1, cand[ax][0] = 0, cw[ax][0] = 2;
-    for (int ax = 0; ax < dim; ++ax) {
-      const int w = a.g.cut_w[ax];
-      int q = p[ax] >= 0 ? p[ax] / w : -1;
-      q = min(max(q, 0), a.g.counts[ax] - 1);
-      nc[ax] = 0;
-      for (int c = q - 1; c <= q; ++c) {
-        if (c < 0) continue;
-        const int w2 = weight2(a.g, ax, c, p[ax]);
-        if (w2) {
-          cand[ax][nc[ax]] = c;
-          cw[ax][nc[ax]] = w2;
-          ++nc[ax];
-        }
-      }
-    }
-    int subs[8], steps[8];
-    double wts[8];
+    int pos[E], key[E], num[E];
     int ns = 0;
-    for (int i2 = 0; i2 < nc[2]; ++i2)
-      for (int i1 = 0; i1 < nc[1]; ++i1)
-        for (int i0 = 0; i0 < nc[0]; ++i0) {
-          const int c3[3] = {cand[0][i0], cand[1][i1], dim == 3 ? cand[2][i2] : 0};
-          int num = cw[0][i0] * cw[1][i1] * (dim == 3 ? cw[2][i2] : 1);
-          int id = 0, st = 1;
-          for (int ax = dim - 1; ax >= 0; --ax) id = id * a.g.counts[ax] + c3[ax];
-          for (int ax = 0; ax < dim; ++ax) st += a.dvec[ax] == 1 ? c3[ax] : a.g.counts[ax] - 1 - c3[ax];
-          subs[ns] = id;
-          steps[ns] = st;
-          wts[ns] = num / static_cast<double>(1 << dim);
-          ++ns;
-        }
-    // reference accumulation order: step, then ascending id within the step group
-    for (int i = 1; i < ns; ++i)
-      for (int j = i; j > 0 && (steps[j] < steps[j - 1] || (steps[j] == steps[j - 1] && subs[j] < subs[j - 1])); --j) {
-        int ts = subs[j]; subs[j] = subs[j - 1]; subs[j - 1] = ts;
-        ts = steps[j]; steps[j] = steps[j - 1]; steps[j - 1] = ts;
-        const double tw = wts[j]; wts[j] = wts[j - 1]; wts[j - 1] = tw;
-      }
-    double2 acc = czero();
-    for (int i = 0; i < ns; ++i) {
-      const int sb = subs[i];
-      if (!((a.nzmask[sb] >> r) & 1u)) continue;
-      const DevSub& S = a.subs[sb];
-      const DevClass& C = a.cls[S.cls];
-      long long local = 0, ls = 1;
-      for (int ax = 0; ax < dim; ++ax) {
-        local += static_cast<long long>(p[ax] - S.lo[ax]) * ls;
-        ls *= C.size[ax];
-      }
-      const double2 xv = S.x[a.xoff + static_cast<long long>(C.elim_of_local[local]) * R + r];
-      acc.x += wts[i] * xv.x;
-      acc.y += wts[i] * xv.y;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int2 v = __ldg(a.acc_ent + node * E + e);
+      pos[e] = v.x;
+      num[e] = v.y >> 24;
+      const int c0 = v.y & 255, c1 = (v.y >> 8) & 255, c2 = (v.y >> 16) & 255;
+      const int st = 1 + (a.dvec[0] == 1 ? c0 : a.g.counts[0] - 1 - c0) +
+                     (a.dvec[1] == 1 ? c1 : a.g.counts[1] - 1 - c1) +
+                     (dim == 3 ? (a.dvec[2] == 1 ? c2 : a.g.counts[2] - 1 - c2) : 0);
+      const int id = c0 + a.g.counts[0] * (c1 + a.g.counts[1] * c2);
+      key[e] = v.x < 0 ? 0x7fffffff : (st << 16) | id;
+      ns += v.x >= 0;
     }
-    double2& u = a.u[idx];
-    u = cadd(u, acc);
+    // reference order: step of the sweep, then ascending id (src/sweeper.cpp:285-309)
+#pragma unroll
+    for (int i = 1; i < E; ++i)
+#pragma unroll
+      for (int j = i; j > 0; --j)
+        if (key[j] < key[j - 1]) {
+          int t = key[j]; key[j] = key[j - 1]; key[j - 1] = t;
+          t = pos[j]; pos[j] = pos[j - 1]; pos[j - 1] = t;
+          t = num[j]; num[j] = num[j - 1]; num[j - 1] = t;
+        }
+    // Every load of the node is issued before the sum. Tasks skipped for an exactly-zero RHS
+    // column (nzmask) contribute nothing, as in the reference; their x buffer is not touched.
+    const double2 uv = a.u[node * R + r];
+    double2 xv[E];
+    bool on[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int id = key[i] & 0xffff;
+      on[i] = i < ns && ((a.nzmask[id] >> r) & 1u);
+      xv[i] = on[i] ? a.x[a.xoff + static_cast<long long>(pos[i]) * R + r] : czero();
+    }
+    double2 acc = czero();
+    const double inv = 1.0 / static_cast<double>(1 << dim);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      if (!on[i]) continue;
+      const double w = num[i] * inv;
+      acc.x += w * xv[i].x;
+      acc.y += w * xv[i].y;
+    }
+    a.u[node * R + r] = cadd(uv, acc);
     nrm = acc.x * acc.x + acc.y * acc.y;
   }
   red[threadIdx.x] = nrm;
@@ -622,7 +666,7 @@ void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s) {
   const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 64));
   rhs_init_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
-  inject_kernel<<<a.ntasks, kThreads, 0, s>>>(a);
+  inject_kernel<<<a.ntasks, 1024, 0, s>>>(a);
   after_launch();
   nonzero_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
@@ -635,7 +679,10 @@ void launch_extract_deposit(const SweepArgs& a, int, cudaStream_t s) {
 
 int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
   const int nb = blocks_for(a.g.gn, kThreads / a.R);
-  accumulate_kernel<<<nb, kThreads, 0, s>>>(a);
+  if (a.g.dim == 3)
+    accumulate_kernel<8><<<nb, kThreads, 0, s>>>(a);
+  else
+    accumulate_kernel<4><<<nb, kThreads, 0, s>>>(a);
   after_launch();
   return nb;
 }

@@ -71,12 +71,13 @@ void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s);
 
 struct AccumArgs {
   DevGeom g;
-  const DevClass* cls;
-  const DevSub* subs;
   int R;
   int l;
   int dvec[3];               // sweep direction of sweep l
   long long xoff;            // offset of sweep l's x buffer (elements)
+  const double2* x;          // x buffers of every subdomain (elimination order, node-major x R)
+  const int2* acc_ent;       // per global node 2^dim entries (x position n_base[sub] + elim,
+                             // cell c0 | c1 << 8 | c2 << 16 | weight numerator << 24); unused: -1
   const unsigned* nzmask;    // [sub] for sweep l
   double2* u;                // global solution, node-major N x R
   double* partial;           // per-block partial |contrib|^2 [nblocks][R]

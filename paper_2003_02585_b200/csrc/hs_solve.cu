@@ -308,7 +308,7 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
   const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
-  const double2* X = J.x + static_cast<long long>(J.sep_off) * R;
+  const double2* X = J.b + static_cast<long long>(J.sep_off) * R;  // right-hand side
   const bool leaf = J.child0 < 0 && J.child1 < 0;
   auto issue = [&](int s, double2* st) {
     const double2* p = P + ((cb0 + (s >> 1)) * rbs) * 64 + 4 * (s & 1);
