@@ -69,6 +69,7 @@ struct ClassDev {
   std::vector<DevFront> h_fronts;
   std::vector<int> fkc, fkr;   // per front split-K chunk (column blocks / block rows)
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
+  DBuf<unsigned char> on_line;
   std::vector<int> level_start_down;
   DevClass dev{};
 };
@@ -137,6 +138,7 @@ struct Engine {
         if (p[a] == 0 || p[a] == c.size[a] - 1) return true;
       return false;
     };
+    std::vector<unsigned char> fl(c.n, 0);
     for (int d = 0; d < 2 * c.dim; ++d) {
       const int a = d / 2, sign = (d & 1) ? 1 : -1;
       GridRange line = loc;
@@ -165,7 +167,13 @@ struct Engine {
       cd.dev.inj_p0[d] = cd.inj_p0[d].p;
       cd.dev.inj_pm[d] = cd.inj_pm[d].p;
       cd.dev.line_len[d] = static_cast<int>(cnt);
+      for (std::int64_t i = 0; i < cnt; ++i) {
+        if (p0[i] >= 0) fl[p0[i]] = 1;
+        if (pm[i] >= 0) fl[pm[i]] = 1;
+      }
     }
+    cd.on_line.upload(fl, stream);
+    cd.dev.on_line = cd.on_line.p;
   }
 
   void upload_classes(int pad) {
@@ -827,6 +835,8 @@ struct DdmHandle {
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
+  DBuf<int> split_gp;          // split-source plan per (subdomain, elimination position): global node
+  DBuf<unsigned char> split_w; // and weight numerator (0: shell or outside the support)
   DBuf<double2> d_coef;
   // per (R, rounds) state
   int R = 0, nsweeps = 0, rounds = 0;
@@ -1028,6 +1038,34 @@ void DdmHandle::build(const hs_problem& P, int device) {
     for (int q = 0; q < kMaxDirs; ++q)
       d.coef[q] = q < dirs ? reinterpret_cast<const double2*>(d_coef.p) + (static_cast<size_t>(id) * dirs + q) * line_max
                            : nullptr;
+  }
+  {  // split-source plan (src/sweeper.cpp:189-202): per elimination position, the global node and
+     // the weight numerator of w(sub, p) * b[p] (0 on the local shell or outside the support)
+    const long long ntot = eng.n_base[nsub];
+    std::vector<int> gp(std::max<long long>(ntot, 1), 0);
+    std::vector<unsigned char> wn(std::max<long long>(ntot, 1), 0);
+    for (int id = 0; id < nsub; ++id) {
+      const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
+      const GridRange& rg = subs[id].range;
+      for (std::int64_t e = 0; e < c.n; ++e) {
+        const Vec3i p = rg.unlinear(c.local_of_elim[e]);
+        bool shell = false;
+        int num = 1;
+        for (int ax = 0; ax < dim; ++ax) {
+          shell |= p[ax] == rg.lo[ax] || p[ax] == rg.hi[ax];
+          num *= wts.weight2(ax, subs[id].sub[ax], p[ax]);
+        }
+        if (num == 0 || shell) continue;
+        gp[eng.n_base[id] + e] = static_cast<int>(ggrid.range.linear(p));
+        wn[eng.n_base[id] + e] = static_cast<unsigned char>(num);
+      }
+    }
+    split_gp.upload(gp, eng.stream);
+    split_w.upload(wn, eng.stream);
+    for (int id = 0; id < nsub; ++id) {
+      eng.h_subs[id].split_gp = split_gp.p + eng.n_base[id];
+      eng.h_subs[id].split_w = split_w.p + eng.n_base[id];
+    }
   }
   eng.d_subs.upload(eng.h_subs, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
@@ -1276,9 +1314,10 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
   for (int m = 0; m < nm; ++m) {
     sa.tasks = d_mtasks.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps[m].size());
-    launch_build_rhs(sa, eng.n_max, s);
+    launch_build_rhs(sa, eng.n_max, static_cast<int>(line_max), s);
     if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * m], s));
-    const bool traced = std::getenv("HS_TRACE") && m == nm / 2;
+    const char* tstep = std::getenv("HS_TRACE_STEP");
+    const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
     eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
     if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
     launch_extract_deposit(sa, static_cast<int>(line_max), s);

@@ -35,6 +35,7 @@ struct DevClass {
   const int* inj_p0[kMaxDirs];   // incoming trace: interface line (-1 on shell)
   const int* inj_pm[kMaxDirs];   // incoming trace: first source-side line (-1 on shell)
   int line_len[kMaxDirs];
+  const unsigned char* on_line;  // per elimination position: on an injection line of some face
   int n, nfronts;
   int size[3];
 };
@@ -52,6 +53,8 @@ struct DevSub {
   double2* rb;                // right-hand side of the task (same layout); zero off the injection
                               // lines except while a sweep-1 task holds its split source
   const double2* coef[kMaxDirs];  // injection couplings per incoming direction
+  const int* split_gp;             // per elimination position: global node of the split source
+  const unsigned char* split_w;    // its weight numerator over 2^dim (0 = shell or outside support)
 };
 
 // Global grid and partition geometry for split / accumulate kernels.

@@ -297,125 +297,115 @@ __global__ void rhs_init_kernel(SweepArgs a) {
     }
     return;
   }
+  // sweep 1 (or the first reuse of a sweep-1 buffer): split source / zero over the whole buffer;
+  // nonzero bits of positions off the injection lines are final here (lines: nonzero_kernel)
   const long long total = static_cast<long long>(C.n) * a.R;
+  const double inv = 1.0 / static_cast<double>(1 << dim);
+  unsigned bits = 0;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     double2 v = czero();
     if (l == 1) {
       const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
-      int local = C.local_of_elim[e];
-      int p[3] = {0, 0, 0};
-      bool shell = false;
-      long long gp = 0, gst = 1;
-      int num = 1;
-      for (int ax = 0; ax < dim; ++ax) {
-        const int li = local % C.size[ax];
-        local /= C.size[ax];
-        p[ax] = S.lo[ax] + li;
-        shell |= (li == 0) || (li == C.size[ax] - 1);
-        num *= weight2(a.g, ax, S.sub[ax], p[ax]);
-        gp += static_cast<long long>(p[ax] - a.g.glo[ax]) * gst;
-        gst *= a.g.gsize[ax];
-      }
-      if (num != 0 && !shell) {
-        const double w = num / static_cast<double>(1 << dim);
-        const double2 bv = a.b[gp * a.R + r];
+      const int wn = S.split_w[e];
+      if (wn) {
+        const double w = wn * inv;
+        const double2 bv = a.b[static_cast<long long>(S.split_gp[e]) * a.R + r];
         v = make_double2(w * bv.x, w * bv.y);
+        if ((v.x != 0.0 || v.y != 0.0) && !C.on_line[e]) bits |= 1u << r;
       }
     }
     B[idx] = v;
   }
+  if (l == 1) {
+    bits = __reduce_or_sync(kFull, bits);
+    if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
+  }
 }
 
-// trace_to_source of the mailbox slots of sweep l (src/transfer.cpp:68-89). Deposits are kept per
-// generating sweep (one writer per slot); they are summed here in generating-sweep order, which is
-// the reference mailbox's "first deposit copies, later deposits add" (src/transfer.cpp:30-35).
-__global__ void inject_kernel(SweepArgs a) {
-  const int sub = a.tasks[blockIdx.x].x, l = a.tasks[blockIdx.x].y;
+// trace_to_source of the mailbox slots of sweep l (src/transfer.cpp:68-89) for the two faces of
+// one axis. The faces' lines are disjoint, so every (task, line chunk) is its own block; the axes
+// are separate launches in the reference's (axis, sign) order, which fixes the order at the nodes
+// where lines of different axes cross. Deposits are kept per generating sweep (one writer per
+// slot) and summed here in generating-sweep order: the reference mailbox's "first deposit copies,
+// later deposits add" (src/transfer.cpp:30-35).
+constexpr int kInjectChunk = 1024;  // line x RHS elements per block
+__global__ void inject_kernel(SweepArgs a, int axis) {
+  const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
   const DevClass& C = a.cls[S.cls];
-  double2* X = task_b(a, S, l);  // the task's right-hand side
+  double2* B = task_b(a, S, l);  // the task's right-hand side
   const int R = a.R;
-  // contributing slots per direction (generating sweeps routed to l, ascending), once per block
-  __shared__ long long s_slot[kMaxDirs][HS_SLOTS_PER_DIR];
-  __shared__ unsigned s_pres[kMaxDirs][HS_SLOTS_PER_DIR];
-  __shared__ int s_n[kMaxDirs];
-  if (threadIdx.x < a.dirs) {
-    const int d = threadIdx.x;
+  __shared__ long long s_slot[2][HS_SLOTS_PER_DIR];
+  __shared__ unsigned s_pres[2][HS_SLOTS_PER_DIR];
+  __shared__ int s_n[2];
+  if (threadIdx.x < 2) {
+    const int d = 2 * axis + threadIdx.x;
     int n = 0;
     for (int lg = 1; lg <= l && n < HS_SLOTS_PER_DIR; ++lg) {
       if (a.route[(lg - 1) * a.dirs + d] != l) continue;
       const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
       const unsigned pres = a.mpres[slot];
       if (pres == 0) continue;
-      s_slot[d][n] = slot;
-      s_pres[d][n] = pres;
+      s_slot[threadIdx.x][n] = slot;
+      s_pres[threadIdx.x][n] = pres;
       ++n;
     }
-    s_n[d] = n;
+    s_n[threadIdx.x] = n;
   }
   __syncthreads();
 #pragma unroll 1
-  for (int d = 0; d < a.dirs; ++d) {  // canonical (axis, sign) order of src/sweeper.cpp:233-239
-    const int n = s_n[d];
+  for (int q = 0; q < 2; ++q) {
+    const int d = 2 * axis + q, n = s_n[q];
     if (n == 0) continue;
     const int len = C.line_len[d];
-    for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
-      const int i = idx / R, r = idx % R;
-      double2 u0 = czero(), um1 = czero();
-      bool first = true;
-      for (int k = 0; k < n; ++k) {
-        if (!((s_pres[d][k] >> r) & 1u)) continue;
-        const double2* s0 = a.mbox + s_slot[d][k] * a.mbox_dir_stride;
-        const double2 v0 = s0[idx], v1 = s0[static_cast<long long>(len) * R + idx];
-        u0 = first ? v0 : cadd(u0, v0);
-        um1 = first ? v1 : cadd(um1, v1);
-        first = false;
-      }
-      if (first) continue;
-      const double2 c = S.coef[d][i];
-      const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
-      if (p0 >= 0) cfms(X[static_cast<long long>(p0) * R + r], c, um1);
-      if (pm >= 0) cfma(X[static_cast<long long>(pm) * R + r], c, u0);
+    const int idx = blockIdx.x * kInjectChunk + threadIdx.x;
+    if (idx >= len * R) continue;
+    const int i = idx / R, r = idx % R;
+    double2 u0 = czero(), um1 = czero();
+    bool first = true;
+    for (int k = 0; k < n; ++k) {
+      if (!((s_pres[q][k] >> r) & 1u)) continue;
+      const double2* s0 = a.mbox + s_slot[q][k] * a.mbox_dir_stride;
+      const double2 v0 = s0[idx], v1 = s0[static_cast<long long>(len) * R + idx];
+      u0 = first ? v0 : cadd(u0, v0);
+      um1 = first ? v1 : cadd(um1, v1);
+      first = false;
     }
-    __syncthreads();
-  }
-  if (l > 1) {  // RHS = traces only: nonzero columns are found on the injection lines
-    unsigned bits = 0;
-    for (int d = 0; d < a.dirs; ++d) {
-      const int len = C.line_len[d];
-      for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
-        const int i = idx / R, r = idx % R;
-        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
-        if (p0 >= 0) {
-          const double2 v = X[static_cast<long long>(p0) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
-        }
-        if (pm >= 0) {
-          const double2 v = X[static_cast<long long>(pm) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
-        }
-      }
-    }
-    bits = __reduce_or_sync(kFull, bits);
-    if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
+    if (first) continue;
+    const double2 c = S.coef[d][i];
+    const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+    if (p0 >= 0) cfms(B[static_cast<long long>(p0) * R + r], c, um1);
+    if (pm >= 0) cfma(B[static_cast<long long>(pm) * R + r], c, u0);
   }
 }
 
-// Exact-zero test of a task's RHS (src/sweeper.cpp:240-251) for sweep 1 (split source + traces);
-// for sweeps >= 2 the RHS is zero off the injection lines and inject_kernel tests those.
+// Exact-zero test of a task's RHS (src/sweeper.cpp:240-251) on the injection lines; positions off
+// the lines were tested by rhs_init (sweep 1) or are zero (later sweeps).
 __global__ void nonzero_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
-  if (l > 1) return;
   const DevSub& S = a.subs[sub];
-  const double2* X = task_b(a, S, l);
   const DevClass& C = a.cls[S.cls];
-  const long long total = static_cast<long long>(C.n) * a.R;
+  const double2* B = task_b(a, S, l);
+  const int R = a.R;
   unsigned bits = 0;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double2 v = X[idx];
-    if (v.x != 0.0 || v.y != 0.0) bits |= 1u << (idx % a.R);
+  {
+    for (int d = 0; d < a.dirs; ++d) {
+      const int len = C.line_len[d];
+      for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * R;
+           idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
+        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+        if (p0 >= 0) {
+          const double2 v = B[static_cast<long long>(p0) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+        }
+        if (pm >= 0) {
+          const double2 v = B[static_cast<long long>(pm) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+        }
+      }
+    }
   }
   bits = __reduce_or_sync(kFull, bits);
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
@@ -424,8 +414,8 @@ __global__ void nonzero_kernel(SweepArgs a) {
 // extract_trace (src/transfer.cpp:47-66) + route_trace (src/sweeper.cpp:58-73) + deposit into the
 // target's slot of this generating sweep (unique writer: plain stores, presence = RHS columns).
 __global__ void extract_deposit_kernel(SweepArgs a) {
-  const int sub = a.tasks[blockIdx.x].x, l = a.tasks[blockIdx.x].y;
-  const int d = blockIdx.y;
+  const int task = blockIdx.y / a.dirs, d = blockIdx.y % a.dirs;
+  const int sub = a.tasks[task].x, l = a.tasks[task].y;
   const int axis = d >> 1, sign = (d & 1) ? 1 : -1;
   const DevSub& S = a.subs[sub];
   const int t = S.sub[axis] + sign;
@@ -442,18 +432,17 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   const long long slot = (static_cast<long long>(target) * a.nsweeps + (l - 1)) * a.dirs + d;
   double2* u0 = a.mbox + slot * a.mbox_dir_stride;
   double2* um1 = u0 + static_cast<long long>(len) * R;
-  for (int idx = threadIdx.x; idx < len * R; idx += blockDim.x) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < len * R) {
     const int i = idx / R, r = idx % R;
-    if (!((nz >> r) & 1u)) continue;
-    u0[idx] = X[static_cast<long long>(C.ext_u0[d][i]) * R + r];
-    um1[idx] = X[static_cast<long long>(C.ext_um1[d][i]) * R + r];
+    if ((nz >> r) & 1u) {
+      u0[idx] = X[static_cast<long long>(C.ext_u0[d][i]) * R + r];
+      um1[idx] = X[static_cast<long long>(C.ext_um1[d][i]) * R + r];
+    }
   }
-  if (threadIdx.x == 0) a.mpres[slot] = nz;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.mpres[slot] = nz;
 }
 
-// u += sum over the subdomains whose support holds the node of w * u_local, in the reference's
-// order (step of the sweep, then ascending id: src/sweeper.cpp:285-309, src/transfer.cpp:91-102).
-// The (position, subdomain, weight) entries of each node are precomputed on the host.
 template <int E>
 __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   __shared__ double red[kThreads];
@@ -662,18 +651,22 @@ void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s) {
   after_launch();
 }
 
-void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s) {
-  const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 64));
+void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStream_t s) {
+  const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 512));
   rhs_init_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
-  inject_kernel<<<a.ntasks, 1024, 0, s>>>(a);
-  after_launch();
-  nonzero_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
+  const int nchunk = std::max(1, (max_line * a.R + kInjectChunk - 1) / kInjectChunk);
+  for (int axis = 0; axis < a.dirs / 2; ++axis) {
+    inject_kernel<<<dim3(nchunk, a.ntasks), kInjectChunk, 0, s>>>(a, axis);
+    after_launch();
+  }
+  nonzero_kernel<<<dim3(std::max(1, std::min(bx, 16)), a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
 }
 
-void launch_extract_deposit(const SweepArgs& a, int, cudaStream_t s) {
-  extract_deposit_kernel<<<dim3(a.ntasks, a.dirs), kThreads, 0, s>>>(a);
+void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
+  const int nchunk = std::max(1, (max_line * a.R + kThreads - 1) / kThreads);
+  extract_deposit_kernel<<<dim3(nchunk, a.ntasks * a.dirs), kThreads, 0, s>>>(a);
   after_launch();
 }
 

@@ -65,7 +65,7 @@ struct SweepArgs {
 };
 // RHS of each subdomain task: split source (sweep 1) plus injected traces, and the
 // exact-zero test (src/sweeper.cpp:189-251, src/transfer.cpp:68-89).
-void launch_build_rhs(const SweepArgs& a, long long max_n, cudaStream_t s);
+void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStream_t s);
 // Trace extraction -> routing -> mailbox deposit (src/transfer.cpp:13-66, src/sweeper.cpp:295-307).
 void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s);
 
