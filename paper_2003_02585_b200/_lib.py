@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhelmsweep_b200.so")
+LIB_PATH = os.environ.get("HS_LIB_PATH") or os.path.join(HERE, "libhelmsweep_b200.so")  # override: dev variants
 
 HS_OK, HS_ERR_CONFIG, HS_ERR_DATA, HS_ERR_SINGULAR, HS_ERR_CUDA, HS_ERR_INTERNAL = range(6)
 HS_MAX_SWEEPS = 64

@@ -68,6 +68,7 @@ struct ClassDev {
   DBuf<int2> pmap;
   std::vector<DevFront> h_fronts;
   std::vector<int> fkc, fkr;   // per front split-K chunk (column blocks / block rows)
+  std::vector<int> fgw;        // per front RHS group width (8 on the critical path, else 16)
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   DBuf<unsigned char> on_line;
   std::vector<int> level_start_down;
@@ -93,6 +94,7 @@ struct Engine {
   int R = 0, nslots = 0, ngr = 1;
   int kc = 8, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
   int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
+  int crit_gw = 8;             // RHS per item of the split (critical-path) fronts
   long long arr_total = 0, part_total = 0;     // per slot
   DBuf<double2> x, x1, rb, vbuf;
   DBuf<double> part;
@@ -376,10 +378,11 @@ struct Engine {
     if (r == R && slots <= nslots && nb == nbuf) return;
     R = r;
     nbuf = nb;
-    ngr = (R + 15) / 16;
+    ngr = (R + 7) / 8;  // arrival / partial slots per (front, band): one per 8-RHS group
     if (const char* e = std::getenv("HS_KC")) kc = std::min(16, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
+    if (const char* e = std::getenv("HS_CRIT_GW")) crit_gw = std::atoi(e) <= 8 ? 8 : 16;
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;
@@ -389,11 +392,13 @@ struct Engine {
       long long arr = 0, parts = 0;
       cd.fkc.assign(c.fronts.size(), 16);
       cd.fkr.assign(c.fronts.size(), 16);
+      cd.fgw.assign(c.fronts.size(), 16);
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const int m = c.fronts[f].m, k = c.fronts[f].k;
         if (c.fronts[f].depth < split_depth) {  // critical path: split long bands over many warps
           cd.fkc[f] = kc;
           cd.fkr[f] = kr;
+          cd.fgw[f] = crit_gw;
         }
         const int fkc = cd.fkc[f], fkr = cd.fkr[f];
         const int kb = pad8(k) >> 3, nrb = kb + (pad8(m - k) >> 3);
@@ -441,6 +446,7 @@ struct Engine {
     std::vector<SolveJob> hj(static_cast<size_t>(njobs) * nbuf);
     auto nband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + (pad8(d.m - d.k) >> 3) + 3) / 4; };
     auto ncband_of = [](const FrontDesc& d) { return ((pad8(d.k) >> 3) + 3) / 4; };
+    auto groups_of = [&](const ClassDev& cd, int f) { return (R + cd.fgw[f] - 1) / cd.fgw[f]; };
     for (int s = 0; s < nsub; ++s) {
       const ClassDev& cd = *classes[sub_cls[s]];
       const SymbolicClass& c = *cd.sym;
@@ -460,10 +466,11 @@ struct Engine {
         J.v_off = static_cast<int>(fd.v_off);
         J.child0 = fd.child[0];
         J.child1 = fd.child[1];
-        J.nband_c0 = fd.child[0] >= 0 ? nband_of(c.fronts[fd.child[0]]) : 0;
-        J.nband_c1 = fd.child[1] >= 0 ? nband_of(c.fronts[fd.child[1]]) : 0;
+        J.tgt_c0 = fd.child[0] >= 0 ? nband_of(c.fronts[fd.child[0]]) * groups_of(cd, fd.child[0]) : 0;
+        J.tgt_c1 = fd.child[1] >= 0 ? nband_of(c.fronts[fd.child[1]]) * groups_of(cd, fd.child[1]) : 0;
         J.parent = fd.parent;
-        J.ncband_p = fd.parent >= 0 ? ncband_of(c.fronts[fd.parent]) : 0;
+        J.tgt_p = fd.parent >= 0 ? ncband_of(c.fronts[fd.parent]) * groups_of(cd, fd.parent) : 0;
+        J.gw = cd.fgw[f];
         J.arr_off = cd.h_fronts[f].arr_off;
         J.part_off = cd.h_fronts[f].part_off;
         J.kc = cd.fkc[f];
@@ -511,8 +518,8 @@ struct Engine {
           const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
           for (int t = 0; t < nband; ++t)
             for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); ++ch)
-              for (int r0 = 0; r0 < R; r0 += 16)
-                fwd.push_back(SolveItem{nzi, f, jb + f, t, static_cast<int>(g), r0, std::min(16, R - r0), ch});
+              for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
+                fwd.push_back(SolveItem{nzi, f, jb + f, t, static_cast<int>(g), r0, std::min(cd.fgw[f], R - r0), ch});
         }
       }
     for (int d = 0; d <= dmax; ++d)
@@ -527,8 +534,8 @@ struct Engine {
           const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
           for (int u = 0; u < ncband; ++u)
             for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); ++ch)
-              for (int r0 = 0; r0 < R; r0 += 16)
-                bwd.push_back(SolveItem{nzi, f, jb + f, u, static_cast<int>(g), r0, std::min(16, R - r0), ch});
+              for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
+                bwd.push_back(SolveItem{nzi, f, jb + f, u, static_cast<int>(g), r0, std::min(cd.fgw[f], R - r0), ch});
         }
       }
   }
@@ -557,7 +564,7 @@ struct Engine {
     a.arr = cnt.p + 2 * per;
     a.queue = reinterpret_cast<unsigned*>(cnt.p + 2 * per + 2 * arr);
     if (traced) {  // developer instrumentation (HS_TRACE): per-item timestamps of this step
-      trace.alloc(static_cast<size_t>(4) * (nfwd + nbwd));
+      trace.alloc(static_cast<size_t>(8) * (nfwd + nbwd));
       HS_CUDA(cudaMemsetAsync(trace.p, 0, trace.n * sizeof(unsigned long long), stream));
       a.trace = trace.p;
     }
@@ -567,7 +574,7 @@ struct Engine {
     a.done = cnt.p + per;
     a.arr = cnt.p + 2 * per + arr;
     a.queue = reinterpret_cast<unsigned*>(cnt.p + 2 * per + 2 * arr + 1);
-    if (traced) a.trace = trace.p + 4LL * nfwd;
+    if (traced) a.trace = trace.p + 8LL * nfwd;
     launch_solve(a, false, stream);
     if (traced) {
       std::vector<unsigned long long> h(trace.n);
@@ -577,14 +584,15 @@ struct Engine {
       HS_CUDA(cudaMemcpyAsync(items.data() + nfwd, bwd, nbwd * sizeof(SolveItem), cudaMemcpyDeviceToHost, stream));
       HS_CUDA(cudaStreamSynchronize(stream));
       if (FILE* fp = std::fopen(std::getenv("HS_TRACE"), "w")) {
-        std::fprintf(fp, "pass,sub,front,kind,idx,chunk,r0,rw,t_deq,t_ready,t_done,sm,k,m\n");
+        std::fprintf(fp, "pass,sub,front,kind,idx,chunk,r0,rw,t_deq,t_ready,t_loop,t_red,t_done,sm,nsteps,k,m\n");
         for (int i = 0; i < nfwd + nbwd; ++i) {
           const SolveItem& it = items[i];
           const int sub = it.nzi % static_cast<int>(sub_cls.size());
           const FrontDesc& fd = classes[sub_cls[sub]]->sym->fronts[it.front];
-          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, sub, it.front,
-                       i < nfwd ? 1 : 2, it.idx, it.chunk, it.r0, it.rw, h[4 * i], h[4 * i + 1], h[4 * i + 2], h[4 * i + 3], fd.k,
-                       fd.m);
+          const unsigned long long* q = &h[8 * i];
+          std::fprintf(fp, "%d,%d,%d,%d,%d,%d,%d,%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu,%d,%d\n", i < nfwd ? 0 : 1, sub,
+                       it.front, i < nfwd ? 1 : 2, it.idx, it.chunk, it.r0, it.rw, q[0], q[1], q[2], q[3], q[4], q[5],
+                       q[6], fd.k, fd.m);
         }
         std::fclose(fp);
       }

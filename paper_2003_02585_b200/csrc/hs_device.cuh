@@ -88,9 +88,10 @@ struct SolveJob {
   const int2* pm;         // extend-add source map of the front's positions
   const int* be;          // boundary elimination positions
   int k, m, sep_off, v_off;
-  int child0, child1, nband_c0, nband_c1;  // children and their band counts (forward waits)
-  int parent, ncband_p, arr_off, part_off; // parent and its column-band count (backward waits)
+  int child0, child1, tgt_c0, tgt_c1;      // children and their finalized-item counts (forward waits)
+  int parent, tgt_p, arr_off, part_off;    // parent and its finalized-item count (backward waits)
   int kc, kr;                              // split-K chunk: column blocks (forward) / block rows (backward)
+  int gw, pad_;                            // RHS per item group (8 on the critical path, else 16)
 };
 
 struct FactorTask {

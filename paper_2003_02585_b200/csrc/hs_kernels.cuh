@@ -10,7 +10,7 @@ struct SolveArgs {
   const SolveJob* jobs;
   int nitems;
   int R;           // RHS per batch (row stride of x / x1 / V)
-  int ngr;         // RHS groups of 16
+  int ngr;         // RHS groups of 8 (stride of the per-group arrival counters / partial tiles)
   int* done;       // per [slot * nf_max + front]: finalized (band, group) pairs of this pass
   int* arr;        // split-K arrivals per [(slot * arr_stride + arr_off + band) * ngr + group]
   long long arr_stride;

@@ -213,9 +213,15 @@ __device__ __forceinline__ void cp_wait() {
 // parts, NB x 2 x 32 double2: forward NB = 3 = rhs, child0 V, child1 V; backward NB = 1),
 // followed by the item's index slice (kIdx entries: source-map pairs / boundary positions).
 constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
+#ifndef HS_NS_FWD
+#define HS_NS_FWD 2
+#endif
+#ifndef HS_NS_BWD
+#define HS_NS_BWD 3
+#endif
 template <bool FWD>
 struct Ring {
-  static constexpr int NS = FWD ? 3 : 4;
+  static constexpr int NS = FWD ? HS_NS_FWD : HS_NS_BWD;
   static constexpr int NB = FWD ? 3 : 1;
   static constexpr int kStage = (4 + NB * 2) * 32;  // double2
   static constexpr int kWarp = NS * kStage + kIdx / 2;
@@ -303,7 +309,7 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
 // forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols]
 template <int NT>
 __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
-                         int* done, int lane, double2* ring, const int2* sidx) {
+                         int* done, int lane, double2* ring, const int2* sidx, unsigned long long* tr) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
@@ -341,49 +347,74 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use);
+  if (tr && lane == 0) {
+    tr[2] = gtime();
+    tr[6] = 2 * (cb1 - cb0);
+  }
   const int nch = nch_fwd(g, t, J.kc);
   if (nch > 1) {
     int loc = 0;
     for (int tt = 0; tt < t; ++tt) loc += nch_fwd(g, tt, J.kc);
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
-    double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
-    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + t) * a.ngr + r0 / 16;
+    double* base = a.part + (slot_part * a.ngr + r0 / 8) * kTileDoubles;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + t) * a.ngr + r0 / 8;
     if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
   }
-  // finalize: z = D^-1 (M T_sep) for separator rows, V = T_bnd - W T_sep for boundary rows
+  if (tr && lane == 0) tr[3] = gtime();
+  // finalize: z = D^-1 (M T_sep) for separator rows, V = T_bnd - W T_sep for boundary rows, with
+  // T_bnd = child0 V + child1 V. Index and dinv loads first, then each half-band's child updates
+  // all in flight before any store (one round trip per stage instead of a dependent chain).
+  int2 src[4];
+  double2 dv[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int pr = 32 * t + 8 * i + rl;
-    if (pr < J.k) {
-      const double2 d = J.dinv[pr];
-      double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
+    const bool bnd = pr >= g.kp && pr - g.kp < J.m - J.k;
+    src[i] = (bnd && !leaf) ? __ldg(J.pm + J.k + (pr - g.kp)) : make_int2(-1, -1);
+    dv[i] = pr < J.k ? J.dinv[pr] : czero();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int pr = 32 * t + 8 * i + rl;
+    if (pr >= J.k) continue;
+    double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+        if (r < R) __stcg(zo + r, cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), dv[i]));
+      }
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 w0[2][NT][2], w1[2][NT][2];
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
-          if (r < R) __stcg(zo + r, cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), d));
+          const int i = 2 * h + ii, r = r0 + 8 * q + 2 * (lane & 3) + e;
+          w0[ii][q][e] = (src[i].x >= 0 && r < R) ? __ldcg(V + static_cast<long long>(src[i].x) * R + r) : czero();
+          w1[ii][q][e] = (src[i].y >= 0 && r < R) ? __ldcg(V + static_cast<long long>(src[i].y) * R + r) : czero();
         }
-    } else if (pr >= g.kp && pr - g.kp < J.m - J.k) {
-      const int bi = pr - g.kp;
-      const int2 src = leaf ? make_int2(-1, -1) : __ldg(J.pm + J.k + bi);
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int i = 2 * h + ii, pr = 32 * t + 8 * i + rl;
+      if (!(pr >= g.kp && pr - g.kp < J.m - J.k)) continue;
+      double2* vo = V + static_cast<long long>(J.v_off + pr - g.kp) * R;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = r0 + 8 * q + 2 * (lane & 3) + e;
           if (r >= R) continue;
+          // T_bnd = (0 + child0) + child1 in the reference's child order; absent children add nothing
           double2 tb = czero();
-          if (src.x >= 0) {
-            const double2 w = __ldcg(V + static_cast<long long>(src.x) * R + r);
-            tb = make_double2(tb.x + w.x, tb.y + w.y);
-          }
-          if (src.y >= 0) {
-            const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
-            tb = make_double2(tb.x + w.x, tb.y + w.y);
-          }
-          __stcg(&V[static_cast<long long>(J.v_off + bi) * R + r],
-                 make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
+          if (src[i].x >= 0) tb = make_double2(tb.x + w0[ii][q][e].x, tb.y + w0[ii][q][e].y);
+          if (src[i].y >= 0) tb = make_double2(tb.x + w1[ii][q][e].x, tb.y + w1[ii][q][e].y);
+          __stcg(vo + r, make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
         }
     }
   }
@@ -395,7 +426,7 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
 template <int NT>
 __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int* done, int lane,
-                         double2* ring, const int2* sidx) {
+                         double2* ring, const int2* sidx, unsigned long long* tr) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const BwdRange rg = bwd_range(J, g, it);
   const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
@@ -437,15 +468,20 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use);
+  if (tr && lane == 0) {
+    tr[2] = gtime();
+    tr[6] = 2 * (a1 - a0);
+  }
   const int nch = nch_bwd(g, u, J.kr);
   if (nch > 1) {
     int loc = 0;
     for (int uu = 0; uu < u; ++uu) loc += nch_bwd(g, uu, J.kr);
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
-    double* base = a.part + (slot_part * a.ngr + r0 / 16) * kTileDoubles;
-    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + u) * a.ngr + r0 / 16;
+    double* base = a.part + (slot_part * a.ngr + r0 / 8) * kTileDoubles;
+    int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + u) * a.ngr + r0 / 8;
     if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
   }
+  if (tr && lane == 0) tr[3] = gtime();
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int col = 32 * u + 8 * i + rl;
@@ -494,36 +530,36 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
     if (it_idx >= a.nitems) break;
     const SolveItem it = a.items[it_idx];
     if (a.nzmask[it.nzi] == 0) continue;  // skipped task (exactly-zero RHS): nothing depends on it
-    unsigned long long* tr = a.trace ? a.trace + 4LL * it_idx : nullptr;
+    unsigned long long* tr = a.trace ? a.trace + 8LL * it_idx : nullptr;
     if (tr && lane == 0) tr[0] = gtime();
     const SolveJob J = a.jobs[it.job];
     const Geo g = geo_km(J.k, J.m);
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
     item_prefetch<FWD>(a, J, g, it, sidx, lane);
     if (FWD) {
-      if (J.child0 >= 0) wait_count(done + J.child0, J.nband_c0 * a.ngr, lane);
-      if (J.child1 >= 0) wait_count(done + J.child1, J.nband_c1 * a.ngr, lane);
+      if (J.child0 >= 0) wait_count(done + J.child0, J.tgt_c0, lane);
+      if (J.child1 >= 0) wait_count(done + J.child1, J.tgt_c1, lane);
     } else if (J.parent >= 0) {
-      wait_count(done + J.parent, J.ncband_p * a.ngr, lane);
+      wait_count(done + J.parent, J.tgt_p, lane);
     }
     cp_wait<0>();
     __syncwarp();
-    if (tr && lane == 0) tr[1] = gtime();
+    if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
     double2* V = a.vbuf + it.slot * a.vslot_stride;
     if (FWD) {
       if (it.rw > 8)
-        fwd_item<2>(a, J, g, it, V, done, lane, ring, sidx);
+        fwd_item<2>(a, J, g, it, V, done, lane, ring, sidx, tr);
       else
-        fwd_item<1>(a, J, g, it, V, done, lane, ring, sidx);
+        fwd_item<1>(a, J, g, it, V, done, lane, ring, sidx, tr);
     } else {
       if (it.rw > 8)
-        bwd_item<2>(a, J, g, it, done, lane, ring, sidx);
+        bwd_item<2>(a, J, g, it, done, lane, ring, sidx, tr);
       else
-        bwd_item<1>(a, J, g, it, done, lane, ring, sidx);
+        bwd_item<1>(a, J, g, it, done, lane, ring, sidx, tr);
     }
     if (tr && lane == 0) {
-      tr[2] = gtime();
-      tr[3] = smid();
+      tr[4] = gtime();
+      tr[5] = smid();
     }
     __syncwarp();  // the index slice is rewritten by the next item
   }
