@@ -136,25 +136,29 @@ __device__ __forceinline__ void acc_zero(Acc<NT>& c) {
 }
 
 // one k-step (4 columns of the product's inner dimension) of the complex 32 x (8 NT) tile
+// Only m-tiles in `mask` (warp-uniform) are computed: the others are structural zeros (rows past
+// the front, columns past k, the upper triangle of M in the diagonal band).
 template <int NT>
-__device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT]) {
+__device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
   double nb[NT];
 #pragma unroll
   for (int q = 0; q < NT; ++q) nb[q] = -B[q].y;
 #pragma unroll
   for (int q = 0; q < NT; ++q)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, B[q].x);
-      dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, B[q].y);
-    }
+    for (int i = 0; i < 4; ++i)
+      if (mask & (1u << i)) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, B[q].x);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, B[q].y);
+      }
 #pragma unroll
   for (int q = 0; q < NT; ++q)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nb[q]);
-      dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, B[q].x);
-    }
+    for (int i = 0; i < 4; ++i)
+      if (mask & (1u << i)) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nb[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, B[q].x);
+      }
 }
 
 // Split-K: store this chunk's partial, and if it arrived last, replace acc by the sum of all
@@ -230,8 +234,8 @@ struct Ring {
 // The pipelined k-loop shared by both passes: issue(s, stage) stages k-step s with cp.async,
 // use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight data
 // costs shared memory, not registers.
-template <bool FWD, int NT, class Issue, class Use>
-__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use) {
+template <bool FWD, int NT, class Issue, class Use, class Mask>
+__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of) {
   constexpr int NS = Ring<FWD>::NS, ST = Ring<FWD>::kStage;
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
@@ -248,7 +252,7 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
     double2 A[4], B[NT];
     use(s, ring + (s % NS) * ST, A, B);
     __syncwarp();
-    mma_step(acc, A, B);
+    mma_step(acc, A, B, mask_of(s));
   }
   cp_wait<0>();
 }
@@ -316,10 +320,25 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
   const double2* X = J.b + static_cast<long long>(J.sep_off) * R;  // right-hand side
   const bool leaf = J.child0 < 0 && J.child1 < 0;
+  // live m-tiles of k-step s: row blocks of the band, minus M's zero blocks above the diagonal
+  auto mask_of = [&](int s) {
+    const int cb = cb0 + (s >> 1);
+    unsigned mk = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int a = 4 * t + i;
+      if (i < rbs && !(a < g.kb && cb > a)) mk |= 1u << i;
+    }
+    return mk;
+  };
   auto issue = [&](int s, double2* st) {
     const double2* p = P + ((cb0 + (s >> 1)) * rbs) * 64 + 4 * (s & 1);
+    const unsigned mk = mask_of(s);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) cp16(st + i * 32 + lane, i < rbs ? p + i * 64 : P, i < rbs);
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = (mk >> i) & 1u;
+      cp16(st + i * 32 + lane, ok ? p + i * 64 : P, ok);
+    }
     const int col = 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3);
     const int2 src = (!leaf && col < J.k) ? sidx[col - 8 * cb0] : make_int2(-1, -1);
     double2* sb = st + 4 * 32 + lane;
@@ -346,7 +365,7 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use);
+  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (cb1 - cb0);
@@ -434,13 +453,26 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const double2* Z = J.x1 + static_cast<long long>(J.sep_off) * R;
   const int nb = J.m - J.k;
   auto row_of = [&](int s) { return 8 * (a0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
-  auto issue = [&](int s, double2* st) {
-    const int ab = a0 + (s >> 1), ta = ab >> 2, rbs = min(4, g.nrb - 4 * ta);
-    const double2* p = P + band_base(ta, g.kb) + (ab & 3) * 64 + 32 * (s & 1);
+  // live m-tiles (column blocks 4u + i) of k-step s: columns below k, minus M's zero blocks
+  auto mask_of = [&](int s) {
+    const int ab = a0 + (s >> 1);
+    unsigned mk = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int cbi = 4 * u + i;
-      cp16(st + i * 32 + lane, cbi < g.kb ? p + cbi * rbs * 64 : P, cbi < g.kb);
+      if (cbi < g.kb && !(ab < g.kb && cbi > ab)) mk |= 1u << i;
+    }
+    return mk;
+  };
+  auto issue = [&](int s, double2* st) {
+    const int ab = a0 + (s >> 1), ta = ab >> 2, rbs = min(4, g.nrb - 4 * ta);
+    const double2* p = P + band_base(ta, g.kb) + (ab & 3) * 64 + 32 * (s & 1);
+    const unsigned mk = mask_of(s);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int cbi = 4 * u + i;
+      const bool ok = (mk >> i) & 1u;
+      cp16(st + i * 32 + lane, ok ? p + cbi * rbs * 64 : P, ok);
     }
     const int row = row_of(s);
     const double2* src = nullptr;
@@ -467,7 +499,7 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use);
+  kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (a1 - a0);
