@@ -94,7 +94,10 @@ class Factorization:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            L.lib().hs_factor_destroy(self._h)
+            try:  # at interpreter shutdown the binding may already be torn down
+                L.lib().hs_factor_destroy(self._h)
+            except Exception:
+                pass
             self._h = None
 
     def stats(self):
@@ -261,7 +264,10 @@ class DdmSolver:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            L.lib().hs_ddm_destroy(self._h)
+            try:  # at interpreter shutdown the binding may already be torn down
+                L.lib().hs_ddm_destroy(self._h)
+            except Exception:
+                pass
             self._h = None
 
     def factor_seconds(self):

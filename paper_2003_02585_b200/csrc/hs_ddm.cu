@@ -840,6 +840,12 @@ struct DdmHandle {
   std::vector<std::vector<int>> acc_after; // per macro-step: sweeps accumulated after it, ascending
   std::vector<int> mstep_of;               // [(l-1) * nsub + id] -> macro-step
   std::vector<int> sweep_first_m, mt_off, fwd_off, fwd_cnt, bwd_off, bwd_cnt;
+  // streamed host transfers: stripes of the slowest axis, and per macro-step the last stripe of b
+  // its sweep-1 tasks read (-1: none)
+  std::vector<long long> stripe_n;  // node bounds, size nstripe + 1
+  std::vector<int> need_stripe;
+  cudaStream_t cstream = nullptr;
+  std::vector<cudaEvent_t> ev_in;
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
@@ -865,6 +871,8 @@ struct DdmHandle {
 
   ~DdmHandle() {
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : ev_in) cudaEventDestroy(e);
+    if (cstream) cudaStreamDestroy(cstream);
   }
 
   void build(const hs_problem& P, int device);
@@ -872,7 +880,8 @@ struct DdmHandle {
   void build_schedule();
   void build_items();
   void ensure_gop();
-  void run(int nrounds, bool track, bool timed);
+  void run(int nrounds, bool track, bool timed, const cudaEvent_t* in_ev = nullptr);
+  void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps);
   void reports(int nrounds, bool track, hs_solve_report* out);
 };
 
@@ -1208,6 +1217,27 @@ void DdmHandle::build_schedule() {
     }
     acc_after[accl[l] - 1].push_back(l);
   }
+  {  // stripes of the slowest axis for streamed host transfers
+    const int la = dim - 1;
+    long long plane = 1;
+    for (int a = 0; a < la; ++a) plane *= geom.gsize[a];
+    const int rows = geom.gsize[la], ns = std::max(1, std::min(rows, 2 * part.counts[la]));
+    stripe_n.assign(ns + 1, 0);
+    for (int j = 0; j <= ns; ++j) stripe_n[j] = plane * ((static_cast<long long>(rows) * j) / ns);
+    need_stripe.assign(nmacro, -1);
+    int need = -1;
+    for (int m = 0; m < nmacro; ++m) {
+      for (const int2& t : msteps[m]) {
+        if (t.y != 1) continue;
+        const GridRange sup = wts.support(subs[t.x].sub);
+        const long long last = (static_cast<long long>(sup.hi[la] - geom.glo[la]) + 1) * plane;  // nodes needed
+        int j = 0;
+        while (j < ns - 1 && stripe_n[j + 1] < last) ++j;
+        need = std::max(need, j);
+      }
+      need_stripe[m] = need;
+    }
+  }
   std::vector<int2> flat;
   mt_off.assign(nmacro, 0);
   max_width = 1;
@@ -1295,7 +1325,7 @@ void DdmHandle::ensure_gop() {
 }
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
-void DdmHandle::run(int nrounds, bool track, bool timed) {
+void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_ev) {
   cudaStream_t s = eng.stream;
   const int nsub = geom.nsub;
   if (track) ensure_gop();
@@ -1319,7 +1349,12 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
   sa.nzmask = nzmask.p;
   sa.route = route.p;
   const int nm = static_cast<int>(msteps.size());
+  int waited = -1;
   for (int m = 0; m < nm; ++m) {
+    if (in_ev && need_stripe[m] > waited) {  // streamed b: the stripes this macro-step's sources read
+      waited = need_stripe[m];
+      HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
+    }
     sa.tasks = d_mtasks.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps[m].size());
     launch_build_rhs(sa, eng.n_max, static_cast<int>(line_max), s);
@@ -1345,6 +1380,11 @@ void DdmHandle::run(int nrounds, bool track, bool timed) {
       launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
       if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
+        const int last = static_cast<int>(stripe_n.size()) - 2;
+        if (in_ev && waited < last) {  // the residual reads all of b
+          waited = last;
+          HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
+        }
         const int rr = l / ndir - 1;
         const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
         launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
@@ -1438,6 +1478,49 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
       }
     }
   }
+}
+
+// One batch from / to pinned host buffers with the transfers overlapped: b streams in by
+// stripes of the slowest axis on a copy stream while the first macro-steps (which only read the
+// stripes their sweep-1 sources touch) run; u streams out by stripes while the residual runs.
+void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps) {
+  ensure_state(nr, nrounds);
+  const long long n = geom.gn;
+  const int ns = static_cast<int>(stripe_n.size()) - 1;
+  if (!cstream) HS_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+  while (static_cast<int>(ev_in.size()) < ns + 2) {
+    cudaEvent_t e;
+    HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_in.push_back(e);
+  }
+  io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
+  double2* din = io.p;
+  double2* dout = io.p + static_cast<size_t>(n) * kMaxRhs;
+  // the copy stream may overwrite din / bN only after earlier work on the compute stream
+  HS_CUDA(cudaEventRecord(ev_in[ns], eng.stream));
+  HS_CUDA(cudaStreamWaitEvent(cstream, ev_in[ns], 0));
+  const size_t pitch = static_cast<size_t>(n) * sizeof(double2);
+  for (int j = 0; j < ns; ++j) {
+    const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
+    HS_CUDA(cudaMemcpy2DAsync(din + n0, pitch, reinterpret_cast<const double2*>(b) + n0, pitch,
+                              static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyHostToDevice, cstream));
+    launch_transpose_in_range(din, bN.p, n, nr, n0, n1, cstream);
+    HS_CUDA(cudaEventRecord(ev_in[j], cstream));
+  }
+  run(nrounds, track, true, ev_in.data());
+  // u is final after the last accumulate (recorded in ev[nsweeps]); stream it out by stripes
+  HS_CUDA(cudaStreamWaitEvent(cstream, ev[nsweeps], 0));
+  for (int j = 0; j < ns; ++j) {
+    const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
+    launch_transpose_out_range(u.p, dout, n, nr, n0, n1, cstream);
+    HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
+                              static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
+  }
+  HS_CUDA(cudaEventRecord(ev_in[ns + 1], cstream));
+  HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[ns + 1], 0));  // later work may reuse io / u
+  if (reps) reports(nrounds, track, reps);
+  HS_CUDA(cudaStreamSynchronize(cstream));
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
 }
 
 }  // namespace hsb
@@ -1549,6 +1632,18 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
     DdmHandle& H = s->h;
     HS_CUDA(cudaSetDevice(H.eng.device));
     const long long n = H.geom.gn;
+    cudaPointerAttributes pa{}, pu{};
+    const bool pinned = cudaPointerGetAttributes(&pa, b) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        cudaPointerGetAttributes(&pu, u) == cudaSuccess && pu.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();  // pageable pointers may leave an error on older runtimes
+    if (pinned) {
+      for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
+        const int R = std::min(kMaxRhs, nrhs - b0);
+        H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,
+                         reports ? reports + b0 : nullptr);
+      }
+      return;
+    }
     for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
       const int R = std::min(kMaxRhs, nrhs - b0);
       H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);

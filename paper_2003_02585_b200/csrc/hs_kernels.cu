@@ -614,20 +614,21 @@ __global__ void scale_cols_kernel(double2* y, const double* inv, long long n, in
   y[idx] = make_double2(y[idx].x * s, y[idx].y * s);
 }
 
-__global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R) {
-  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= n * R) return;
+__global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
+  const long long idx = n0 * R + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (idx >= n1 * R) return;
   const long long node = idx / R;
   const int r = static_cast<int>(idx % R);
   dst[idx] = src[static_cast<long long>(r) * n + node];
 }
 
-__global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R) {
+__global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
+  const long long w = n1 - n0;
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= n * R) return;
-  const int r = static_cast<int>(idx / n);
-  const long long node = idx % n;
-  dst[idx] = src[node * R + r];
+  if (idx >= w * R) return;
+  const int r = static_cast<int>(idx / w);
+  const long long node = n0 + idx % w;
+  dst[static_cast<long long>(r) * n + node] = src[node * R + r];
 }
 
 __global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
@@ -723,12 +724,25 @@ void launch_scale_cols(double2* y, const double* inv, long long n, int R, cudaSt
 }
 
 void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_in_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R);
+  transpose_in_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R, 0, n);
   after_launch();
 }
 
 void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_out_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R);
+  transpose_out_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R, 0, n);
+  after_launch();
+}
+
+void launch_transpose_in_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                               cudaStream_t s) {
+  if (n1 <= n0) return;
+  transpose_in_kernel<<<blocks_for((n1 - n0) * R), kThreads, 0, s>>>(src, dst, n, R, n0, n1);
+  after_launch();
+}
+void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                                cudaStream_t s) {
+  if (n1 <= n0) return;
+  transpose_out_kernel<<<blocks_for((n1 - n0) * R), kThreads, 0, s>>>(src, dst, n, R, n0, n1);
   after_launch();
 }
 

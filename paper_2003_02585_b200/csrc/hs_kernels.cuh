@@ -100,6 +100,11 @@ void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const
 void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
 void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
 void launch_bump_epoch(unsigned* epoch, unsigned by, cudaStream_t s);
+// node range [n0, n1) only (streamed host transfers)
+void launch_transpose_in_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                               cudaStream_t s);
+void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                                cudaStream_t s);
 
 // Krylov vector kernels (src/krylov.cpp:9-13, 52-56, 109-111) on node-major N x R arrays.
 int launch_dot_partials(const double2* a, const double2* b, long long n, int R, double2* partial,
