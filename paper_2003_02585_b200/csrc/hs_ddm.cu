@@ -844,8 +844,11 @@ struct DdmHandle {
   // its sweep-1 tasks read (-1: none)
   std::vector<long long> stripe_n;  // node bounds, size nstripe + 1
   std::vector<int> need_stripe;
+  // the last sweep is accumulated stripe by stripe, after the macro-step that completes the
+  // stripe (acc_stripe_m), so streamed transfers can copy u out while the tail still runs
+  std::vector<int> acc_stripe_m;
   cudaStream_t cstream = nullptr;
-  std::vector<cudaEvent_t> ev_in;
+  std::vector<cudaEvent_t> ev_in, ev_out;
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
@@ -872,6 +875,7 @@ struct DdmHandle {
   ~DdmHandle() {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : ev_in) cudaEventDestroy(e);
+    for (auto e : ev_out) cudaEventDestroy(e);
     if (cstream) cudaStreamDestroy(cstream);
   }
 
@@ -1237,6 +1241,20 @@ void DdmHandle::build_schedule() {
       }
       need_stripe[m] = need;
     }
+    // stripes of the last sweep's accumulate
+    acc_stripe_m.assign(ns, nsweeps > 1 ? accl[nsweeps - 1] - 1 : 0);
+    for (int id = 0; id < nsub; ++id) {
+      const int m = mstep_of[static_cast<size_t>(nsweeps - 1) * nsub + id];
+      const GridRange sup = wts.support(subs[id].sub);
+      const long long lo = static_cast<long long>(sup.lo[la] - geom.glo[la]) * plane;
+      const long long hi = (static_cast<long long>(sup.hi[la] - geom.glo[la]) + 1) * plane;
+      for (int j = 0; j < ns; ++j)
+        if (stripe_n[j] < hi && stripe_n[j + 1] > lo) acc_stripe_m[j] = std::max(acc_stripe_m[j], m);
+    }
+    for (int l = 1; l <= nsweeps; ++l) {  // the last sweep's whole-domain accumulate is replaced
+      auto& v = acc_after[accl[l] - 1];
+      if (l == nsweeps) v.erase(std::remove(v.begin(), v.end(), l), v.end());
+    }
   }
   std::vector<int2> flat;
   mt_off.assign(nmacro, 0);
@@ -1298,7 +1316,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
-  const long long nb = (geom.gn * R + 255) / 256;
+  const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(stripe_n.size());  // + striped rounding
   partial.alloc(static_cast<size_t>(nb) * R);
   pnum.alloc(static_cast<size_t>(nb) * R);
   pden.alloc(static_cast<size_t>(nb) * R);
@@ -1308,6 +1326,9 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   for (auto e : ev) cudaEventDestroy(e);
   ev.assign(1 + nsweeps + 2 * msteps.size(), nullptr);
   for (auto& e : ev) HS_CUDA(cudaEventCreate(&e));
+  for (auto e : ev_out) cudaEventDestroy(e);
+  ev_out.assign(stripe_n.size() - 1, nullptr);
+  for (auto& e : ev_out) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 void DdmHandle::ensure_gop() {
@@ -1349,7 +1370,14 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
   sa.nzmask = nzmask.p;
   sa.route = route.p;
   const int nm = static_cast<int>(msteps.size());
-  int waited = -1;
+  int waited = -1, stripes_done = 0;
+  std::vector<int> stripe_blocks(acc_stripe_m.size(), 0);
+  auto stripe_pbase = [&](int j) {  // partial blocks of the stripes before j (worst case per stripe)
+    const int npb = 256 / R;
+    long long b = 0;
+    for (int q = 0; q < j; ++q) b += (stripe_n[q + 1] - stripe_n[q] + npb - 1) / npb;
+    return b;
+  };
   for (int m = 0; m < nm; ++m) {
     if (in_ev && need_stripe[m] > waited) {  // streamed b: the stripes this macro-step's sources read
       waited = need_stripe[m];
@@ -1364,7 +1392,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
     eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
     if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
     launch_extract_deposit(sa, static_cast<int>(line_max), s);
-    for (int l : acc_after[m]) {
+    auto accumulate = [&](int l, long long n0, long long n1, long long pbase) {
       AccumArgs aa{};
       aa.g = geom;
       aa.x = eng.x.p;
@@ -1375,8 +1403,12 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
       aa.xoff = static_cast<long long>((l - 1) % nbuf) * eng.xstride;
       aa.nzmask = nzmask.p + static_cast<size_t>(l - 1) * nsub;
       aa.u = u.p;
-      aa.partial = partial.p;
-      const int nb = launch_accumulate(aa, s);
+      aa.partial = partial.p + pbase * R;
+      aa.n0 = n0;
+      aa.n1 = n1;
+      return launch_accumulate(aa, s);
+    };
+    auto after_sweep = [&](int l, int nb) {  // sweep l fully accumulated
       launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
       if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
@@ -1389,6 +1421,19 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
         const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
         launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
         launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
+      }
+    };
+    for (int l : acc_after[m]) after_sweep(l, accumulate(l, 0, geom.gn, 0));
+    // the last sweep, stripe by stripe (partials in stripe order: a fixed reduction order)
+    const int nst = static_cast<int>(acc_stripe_m.size());
+    for (int j = 0; j < nst; ++j) {
+      if (acc_stripe_m[j] != m) continue;
+      stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
+      HS_CUDA(cudaEventRecord(ev_out[j], s));
+      if (++stripes_done == nst) {
+        int nbt = 0;
+        for (int q = 0; q < nst; ++q) nbt += stripe_blocks[q];
+        after_sweep(nsweeps, nbt);
       }
     }
   }
@@ -1508,9 +1553,13 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     HS_CUDA(cudaEventRecord(ev_in[j], cstream));
   }
   run(nrounds, track, true, ev_in.data());
-  // u is final after the last accumulate (recorded in ev[nsweeps]); stream it out by stripes
-  HS_CUDA(cudaStreamWaitEvent(cstream, ev[nsweeps], 0));
-  for (int j = 0; j < ns; ++j) {
+  // each stripe of u is final after its accumulate of the last sweep (ev_out); stream the stripes
+  // out in the order they complete, while the tail of the application still runs
+  std::vector<int> order(ns);
+  for (int j = 0; j < ns; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return acc_stripe_m[x] < acc_stripe_m[y]; });
+  for (int j : order) {
+    HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
     const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
     launch_transpose_out_range(u.p, dout, n, nr, n0, n1, cstream);
     HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,

@@ -448,10 +448,10 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   __shared__ double red[kThreads];
   const int dim = a.g.dim, R = a.R;
   const int npb = kThreads / R;  // whole nodes per block so thread t always owns column t % R
-  const long long node = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const long long node = a.n0 + static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
   const int r = threadIdx.x % R;
   double nrm = 0.0;
-  if (threadIdx.x < npb * R && node < a.g.gn) {
+  if (threadIdx.x < npb * R && node < a.n1) {
     int pos[E], key[E], num[E];
     int ns = 0;
 #pragma unroll
@@ -672,7 +672,8 @@ void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
 }
 
 int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
-  const int nb = blocks_for(a.g.gn, kThreads / a.R);
+  const int nb = blocks_for(a.n1 - a.n0, kThreads / a.R);
+  if (nb == 0) return 0;
   if (a.g.dim == 3)
     accumulate_kernel<8><<<nb, kThreads, 0, s>>>(a);
   else

@@ -81,10 +81,11 @@ struct AccumArgs {
   const unsigned* nzmask;    // [sub] for sweep l
   double2* u;                // global solution, node-major N x R
   double* partial;           // per-block partial |contrib|^2 [nblocks][R]
+  long long n0, n1;          // node range of this launch
 };
 // u += sum_sub w * u_local over the subdomain supports in the reference's order
 // (src/transfer.cpp:91-102, src/sweeper.cpp:308-312); emits per-block norm partials.
-int launch_accumulate(const AccumArgs& a, cudaStream_t s);
+int launch_accumulate(const AccumArgs& a, cudaStream_t s);  // nodes [a.n0, a.n1); returns its block count
 // Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
 void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s);
 
