@@ -1138,16 +1138,35 @@ void DdmHandle::build(const hs_problem& P, int device) {
             }
       }
     };
-    const int E = 1 << dim;
-    for (int a = 0; a < dim; ++a)
-      if (part.counts[a] > 256) config_error("partition: more than 256 subdomains per axis");
-    ent.assign(static_cast<size_t>(gn) * E, make_int2(-1, 0));
+    const int E = 1 << dim, ndirs = 1 << dim;
+    if (nsub >= (1 << 27)) config_error("partition: too many subdomains");
+    std::vector<int2> raw(static_cast<size_t>(gn) * E, make_int2(-1, 0));
     visit([&](long long g, int id, int num, int e) {
       if (off[g] >= E) throw Error(kInternal, "accumulate plan: more than 2^dim subdomains at a node");
-      const Vec3i& c = subs[id].sub;
-      ent[static_cast<size_t>(g) * E + off[g]++] =
-          make_int2(static_cast<int>(eng.n_base[id] + e), c[0] | (c[1] << 8) | (c[2] << 16) | (num << 24));
+      raw[static_cast<size_t>(g) * E + off[g]++] = make_int2(static_cast<int>(eng.n_base[id] + e), (id << 4) | num);
     });
+    // one plan per sweep direction, entries in the reference's order: step, then ascending id
+    const std::vector<Vec3i> dplan = sweep_plan(dim, 1);
+    ent.assign(static_cast<size_t>(gn) * E * ndirs, make_int2(-1, 0));
+    for (int di = 0; di < ndirs; ++di) {
+      int2* dst = ent.data() + static_cast<size_t>(di) * gn * E;
+      for (long long g = 0; g < gn; ++g) {
+        int2 tmp[8];
+        int key[8];
+        const int n = off[g];
+        for (int i = 0; i < n; ++i) {
+          tmp[i] = raw[static_cast<size_t>(g) * E + i];
+          const int id = tmp[i].y >> 4;
+          key[i] = (step_of(part.counts, dim, dplan[di], subs[id].sub) << 20) | id;
+        }
+        for (int i = 1; i < n; ++i)
+          for (int j = i; j > 0 && key[j] < key[j - 1]; --j) {
+            std::swap(key[j], key[j - 1]);
+            std::swap(tmp[j], tmp[j - 1]);
+          }
+        for (int i = 0; i < n; ++i) dst[g * E + i] = tmp[i];
+      }
+    }
     acc_ent.upload(ent, eng.stream);
   }
   // step groups and dataflow task lists per (sweep direction, step)
@@ -1316,7 +1335,8 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
-  const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(stripe_n.size());  // + striped rounding
+  // + striped rounding + reduction scratch
+  const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(stripe_n.size()) + kReducePad;
   partial.alloc(static_cast<size_t>(nb) * R);
   pnum.alloc(static_cast<size_t>(nb) * R);
   pden.alloc(static_cast<size_t>(nb) * R);
@@ -1396,7 +1416,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
       AccumArgs aa{};
       aa.g = geom;
       aa.x = eng.x.p;
-      aa.acc_ent = acc_ent.p;
+      aa.acc_ent = acc_ent.p + static_cast<size_t>((l - 1) % ndir) * geom.gn * (1 << dim);
       aa.R = R;
       aa.l = l;
       for (int a = 0; a < 3; ++a) aa.dvec[a] = plan[l - 1][a];

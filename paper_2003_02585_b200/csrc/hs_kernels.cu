@@ -443,6 +443,9 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) a.mpres[slot] = nz;
 }
 
+// u += sum over the subdomains whose support holds the node of w * u_local, in the reference's
+// order (step of the sweep, then ascending id: src/sweeper.cpp:285-309, src/transfer.cpp:91-102).
+// The host precomputes, per sweep direction, each node's entries already in that order.
 template <int E>
 __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   __shared__ double red[kThreads];
@@ -452,48 +455,25 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   const int r = threadIdx.x % R;
   double nrm = 0.0;
   if (threadIdx.x < npb * R && node < a.n1) {
-    int pos[E], key[E], num[E];
-    int ns = 0;
+    int2 ent[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int2 v = __ldg(a.acc_ent + node * E + e);
-      pos[e] = v.x;
-      num[e] = v.y >> 24;
-      const int c0 = v.y & 255, c1 = (v.y >> 8) & 255, c2 = (v.y >> 16) & 255;
-      const int st = 1 + (a.dvec[0] == 1 ? c0 : a.g.counts[0] - 1 - c0) +
-                     (a.dvec[1] == 1 ? c1 : a.g.counts[1] - 1 - c1) +
-                     (dim == 3 ? (a.dvec[2] == 1 ? c2 : a.g.counts[2] - 1 - c2) : 0);
-      const int id = c0 + a.g.counts[0] * (c1 + a.g.counts[1] * c2);
-      key[e] = v.x < 0 ? 0x7fffffff : (st << 16) | id;
-      ns += v.x >= 0;
-    }
-    // reference order: step of the sweep, then ascending id (src/sweeper.cpp:285-309)
-#pragma unroll
-    for (int i = 1; i < E; ++i)
-#pragma unroll
-      for (int j = i; j > 0; --j)
-        if (key[j] < key[j - 1]) {
-          int t = key[j]; key[j] = key[j - 1]; key[j - 1] = t;
-          t = pos[j]; pos[j] = pos[j - 1]; pos[j - 1] = t;
-          t = num[j]; num[j] = num[j - 1]; num[j - 1] = t;
-        }
-    // Every load of the node is issued before the sum. Tasks skipped for an exactly-zero RHS
-    // column (nzmask) contribute nothing, as in the reference; their x buffer is not touched.
+    for (int e = 0; e < E; ++e) ent[e] = __ldg(a.acc_ent + node * E + e);
+    // every load of the node is issued before the sum; tasks skipped for an exactly-zero RHS
+    // column (nzmask) contribute nothing, as in the reference, and their x buffer is not read
     const double2 uv = a.u[node * R + r];
     double2 xv[E];
     bool on[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
-      const int id = key[i] & 0xffff;
-      on[i] = i < ns && ((a.nzmask[id] >> r) & 1u);
-      xv[i] = on[i] ? a.x[a.xoff + static_cast<long long>(pos[i]) * R + r] : czero();
+      on[i] = ent[i].x >= 0 && ((a.nzmask[ent[i].y >> 4] >> r) & 1u);
+      xv[i] = on[i] ? a.x[a.xoff + static_cast<long long>(ent[i].x) * R + r] : czero();
     }
     double2 acc = czero();
     const double inv = 1.0 / static_cast<double>(1 << dim);
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       if (!on[i]) continue;
-      const double w = num[i] * inv;
+      const double w = (ent[i].y & 15) * inv;
       acc.x += w * xv[i].x;
       acc.y += w * xv[i].y;
     }
@@ -509,19 +489,33 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
   }
 }
 
-// One block per RHS column; fixed strided assignment + fixed tree => deterministic.
-__global__ void reduce_partials_kernel(const double* partial, int nblocks, int R, double* out) {
+// Deterministic two-stage reduction of per-block partials out[r] = sum_b partial[b][r]: stage 1
+// sums a fixed contiguous range of rows per block (coalesced rows, fixed tree), stage 2 sums the
+// stage-1 results in block order.
+constexpr int kReduceBlocks = kReducePad;
+__global__ void reduce_partials_stage1(const double* partial, int nblocks, int R, double* mid) {
   __shared__ double red[kThreads];
-  const int r = blockIdx.x;
+  const int rows_per_iter = kThreads / R, row = threadIdx.x / R, r = threadIdx.x % R;
+  const int per = (nblocks + gridDim.x - 1) / gridDim.x, b0 = blockIdx.x * per, b1 = min(nblocks, b0 + per);
   double s = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += kThreads) s += partial[static_cast<long long>(b) * R + r];
+  if (row < rows_per_iter)
+    for (int b = b0 + row; b < b1; b += rows_per_iter) s += partial[static_cast<long long>(b) * R + r];
   red[threadIdx.x] = s;
   __syncthreads();
-  for (int w = kThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
+  if (threadIdx.x < R) {
+    double t = 0.0;
+    for (int q = 0; q < rows_per_iter; ++q) t += red[q * R + threadIdx.x];
+    mid[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = t;
   }
-  if (threadIdx.x == 0) out[r] = red[0];
+}
+__global__ void reduce_partials_stage2(const double* mid, int nmid, int R, double* out) {
+  const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;  // one warp per column, fixed tree
+  if (r >= R) return;
+  double s = 0.0;
+  for (int b = lane; b < nmid; b += 32) s += mid[static_cast<long long>(b) * R + r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) out[r] = s;
 }
 
 __global__ void reduce_cpartials_kernel(const double2* partial, int nblocks, int R, double2* out) {
@@ -682,8 +676,14 @@ int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
   return nb;
 }
 
-void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s) {
-  reduce_partials_kernel<<<R, kThreads, 0, s>>>(partial, nblocks, R, out);
+// The stage-1 scratch lives right after the used partials: the caller's buffer holds at least
+// (nblocks + kReducePad) * R doubles.
+void launch_reduce_partials(double* partial, int nblocks, int R, double* out, cudaStream_t s) {
+  double* mid = partial + static_cast<long long>(nblocks) * R;
+  const int g = std::max(1, std::min(kReduceBlocks, nblocks));
+  reduce_partials_stage1<<<g, kThreads, 0, s>>>(partial, nblocks, R, mid);
+  after_launch();
+  reduce_partials_stage2<<<1, 32 * R, 0, s>>>(mid, g, R, out);
   after_launch();
 }
 

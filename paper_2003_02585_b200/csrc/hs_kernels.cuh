@@ -76,8 +76,9 @@ struct AccumArgs {
   int dvec[3];               // sweep direction of sweep l
   long long xoff;            // offset of sweep l's x buffer (elements)
   const double2* x;          // x buffers of every subdomain (elimination order, node-major x R)
-  const int2* acc_ent;       // per global node 2^dim entries (x position n_base[sub] + elim,
-                             // cell c0 | c1 << 8 | c2 << 16 | weight numerator << 24); unused: -1
+  const int2* acc_ent;       // this sweep direction's plan: per global node 2^dim entries in the
+                             // reference's accumulation order (x position n_base[sub] + elim,
+                             // sub << 4 | weight numerator); unused entries have position -1
   const unsigned* nzmask;    // [sub] for sweep l
   double2* u;                // global solution, node-major N x R
   double* partial;           // per-block partial |contrib|^2 [nblocks][R]
@@ -87,7 +88,8 @@ struct AccumArgs {
 // (src/transfer.cpp:91-102, src/sweeper.cpp:308-312); emits per-block norm partials.
 int launch_accumulate(const AccumArgs& a, cudaStream_t s);  // nodes [a.n0, a.n1); returns its block count
 // Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
-void launch_reduce_partials(const double* partial, int nblocks, int R, double* out, cudaStream_t s);
+constexpr int kReducePad = 256;  // extra partial rows every partial buffer reserves (reduction scratch)
+void launch_reduce_partials(double* partial, int nblocks, int R, double* out, cudaStream_t s);
 
 // Global CSR SpMV y = A x (x, y node-major N x R) (src/operator.cpp:7-17) and the
 // residual partials |b - y|^2, |b|^2.
