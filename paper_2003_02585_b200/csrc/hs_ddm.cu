@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "helmsweep_b200.h"
 #include "hs_kernels.cuh"
@@ -59,7 +60,29 @@ struct DBuf {
   }
 };
 
-double2* as_d2(const Complex* p) { return reinterpret_cast<double2*>(const_cast<Complex*>(p)); }
+// Host-side setup work split over the host cores (static partition; each index is independent).
+template <class F>
+void parallel_for(long long n, F&& fn) {
+  const int nt = static_cast<int>(std::max(1u, std::min(std::thread::hardware_concurrency(), 64u)));
+  if (n < 2 || nt == 1) {
+    for (long long i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (long long i = t; i < n; i += nt) fn(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
 
 struct ClassDev {
   std::unique_ptr<SymbolicClass> sym;
@@ -268,14 +291,14 @@ struct Engine {
     dinv.alloc(std::max<long long>(n_base[nsub], 1));
     val.alloc(std::max<long long>(val_base[nsub], 1));
     tol.assign(nsub, 0.0);
-    for (int s = 0; s < nsub; ++s) {
-      const CVector& v = *values[s];
+    parallel_for(nsub, [&](long long s) {
       double scale = 0.0;
-      for (const Complex& z : v) scale = std::max(scale, std::abs(z));
+      for (const Complex& z : *values[s]) scale = std::max(scale, std::abs(z));
       tol[s] = 1e-14 * scale;  // src/direct.cpp:191-193
-      HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], v.data(), v.size() * sizeof(Complex),
+    });
+    for (int s = 0; s < nsub; ++s)
+      HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], values[s]->data(), values[s]->size() * sizeof(Complex),
                               cudaMemcpyHostToDevice, stream));
-    }
     h_subs.resize(nsub);
     for (int s = 0; s < nsub; ++s) {
       DevSub& d = h_subs[s];
@@ -961,7 +984,15 @@ void DdmHandle::build(const hs_problem& P, int device) {
   if (pml.exponent < 1) config_error("PmlSpec: exponent must be >= 1");
   if (pml.width < 2) config_error("DdmSolver: pml.width must be >= 2 so trace lines stay off the shell");
   medium = medium_from(P);
-  const auto t0 = std::chrono::steady_clock::now();
+  auto t0 = std::chrono::steady_clock::now();
+  const bool prof = std::getenv("HS_SETUP_PROFILE") != nullptr;  // developer instrumentation
+  auto tprev = t0;
+  auto phase = [&](const char* name) {
+    if (!prof) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %8.1f ms\n", name, std::chrono::duration<double, std::milli>(t - tprev).count());
+    tprev = t;
+  };
   part = make_partition(interior, intervals, Vec3i{P.counts[0], P.counts[1], P.counts[2]});
   wts.p = &part;
   wts.pad = pml.width;
@@ -976,12 +1007,17 @@ void DdmHandle::build(const hs_problem& P, int device) {
   gcoeffs = build_coefficients(pml, interior, ggrid);
   gkappa = extend_to_subdomain(medium, interior, ggrid);
 
+  phase("global grid + coefficients");
   eng.init(device, dim);
+  HS_CUDA(cudaFree(nullptr));  // create the context here: process start-up, not factorization
+  phase("device init");
+  t0 = std::chrono::steady_clock::now();  // factor_seconds: subdomain setup + factorization
   const int nsub = part.cell_count();
   subs.resize(nsub);
   std::vector<CVector> vals(nsub);
   std::map<std::vector<int>, int> class_of_key;
   std::vector<PmlCoefficients> coeffs(nsub);
+  std::vector<Csr> ops(nsub);
   for (int id = 0; id < nsub; ++id) {
     SubHost& st = subs[id];
     st.sub = part.unflatten(id);
@@ -992,6 +1028,9 @@ void DdmHandle::build(const hs_problem& P, int device) {
       st.range.lo[a] -= pml.width;
       st.range.hi[a] += pml.width;
     }
+  }
+  parallel_for(nsub, [&](long long id) {  // PML coefficients, extended kappa, CSR (src/sweeper.cpp:89-124)
+    const SubHost& st = subs[id];
     LocalGrid g;
     g.dim = dim;
     g.range = st.range;
@@ -999,9 +1038,13 @@ void DdmHandle::build(const hs_problem& P, int device) {
     g.origin = ggrid.origin;
     coeffs[id] = build_coefficients(pml, st.cell, g);
     const std::vector<double> kap = extend_to_subdomain(medium, st.cell, g);
-    Csr op = assemble(g, coeffs[id], kap);
-    // symbolic class key: extents, and the lower index (or its parity when non-negative:
-    // C++ truncating mid = (lo+hi)/2 only depends on it through that)
+    ops[id] = assemble(g, coeffs[id], kap);
+  });
+  // symbolic classes: key = extents and the lower index (or its parity when non-negative: C++
+  // truncating mid = (lo+hi)/2 only depends on it through that); one symbolic build per class
+  std::vector<int> first_of_class;
+  for (int id = 0; id < nsub; ++id) {
+    SubHost& st = subs[id];
     std::vector<int> key;
     for (int a = 0; a < dim; ++a) {
       key.push_back(st.range.size(a));
@@ -1009,17 +1052,29 @@ void DdmHandle::build(const hs_problem& P, int device) {
     }
     auto it = class_of_key.find(key);
     if (it == class_of_key.end()) {
-      st.cls = eng.add_class(build_symbolic(dim, st.range, op.row_ptr, op.col));
+      st.cls = static_cast<int>(first_of_class.size());
       class_of_key[key] = st.cls;
+      first_of_class.push_back(id);
     } else {
       st.cls = it->second;
-      if (eng.classes[st.cls]->sym->csr_col.size() != op.col.size())
-        throw Error(kInternal, "symbolic class CSR mismatch");
     }
-    eng.sub_cls.push_back(st.cls);
-    vals[id] = std::move(op.val);
   }
+  std::vector<std::unique_ptr<SymbolicClass>> syms(first_of_class.size());
+  parallel_for(static_cast<long long>(syms.size()), [&](long long c) {
+    const int id = first_of_class[c];
+    syms[c] = build_symbolic(dim, subs[id].range, ops[id].row_ptr, ops[id].col);
+  });
+  for (auto& sc : syms) eng.add_class(std::move(sc));
+  for (int id = 0; id < nsub; ++id) {
+    const SubHost& st = subs[id];
+    if (eng.classes[st.cls]->sym->csr_col.size() != ops[id].col.size())
+      throw Error(kInternal, "symbolic class CSR mismatch");
+    eng.sub_cls.push_back(st.cls);
+    vals[id] = std::move(ops[id].val);
+  }
+  phase("assembly + symbolic");
   eng.upload_classes(pml.width);
+  phase("upload classes");
   // injection couplings per subdomain and incoming direction (src/transfer.cpp:80-86)
   dirs = 2 * dim;
   for (auto& cdp : eng.classes)
@@ -1049,7 +1104,9 @@ void DdmHandle::build(const hs_problem& P, int device) {
   std::vector<const CVector*> vp(nsub);
   for (int id = 0; id < nsub; ++id) vp[id] = &vals[id];
   // factorize (the DevSub array is re-uploaded with the coefficient pointers below)
+  phase("couplings");
   eng.factorize(vp);
+  phase("factorize (device)");
   for (int id = 0; id < nsub; ++id) {
     DevSub& d = eng.h_subs[id];
     for (int a = 0; a < 3; ++a) {
@@ -1065,7 +1122,7 @@ void DdmHandle::build(const hs_problem& P, int device) {
     const long long ntot = eng.n_base[nsub];
     std::vector<int> gp(std::max<long long>(ntot, 1), 0);
     std::vector<unsigned char> wn(std::max<long long>(ntot, 1), 0);
-    for (int id = 0; id < nsub; ++id) {
+    parallel_for(nsub, [&](long long id) {
       const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
       const GridRange& rg = subs[id].range;
       for (std::int64_t e = 0; e < c.n; ++e) {
@@ -1080,7 +1137,7 @@ void DdmHandle::build(const hs_problem& P, int device) {
         gp[eng.n_base[id] + e] = static_cast<int>(ggrid.range.linear(p));
         wn[eng.n_base[id] + e] = static_cast<unsigned char>(num);
       }
-    }
+    });
     split_gp.upload(gp, eng.stream);
     split_w.upload(wn, eng.stream);
     for (int id = 0; id < nsub; ++id) {
@@ -1112,6 +1169,7 @@ void DdmHandle::build(const hs_problem& P, int device) {
     geom.counts[a] = part.counts[a];
     geom.cut_w[a] = a < dim ? intervals[a] / part.counts[a] : 1;
   }
+  phase("stats + split plan");
   {  // accumulate plan (src/transfer.cpp:91-102): per global node, every subdomain whose support
      // holds it, as (x position n_base[sub] + elim, sub << 4 | weight numerator)
     const long long gn = geom.gn;
@@ -1147,17 +1205,24 @@ void DdmHandle::build(const hs_problem& P, int device) {
     });
     // one plan per sweep direction, entries in the reference's order: step, then ascending id
     const std::vector<Vec3i> dplan = sweep_plan(dim, 1);
+    std::vector<int> stab(static_cast<size_t>(ndirs) * nsub);
+    for (int di = 0; di < ndirs; ++di)
+      for (int id = 0; id < nsub; ++id) stab[static_cast<size_t>(di) * nsub + id] = step_of(part.counts, dim, dplan[di], subs[id].sub);
     ent.assign(static_cast<size_t>(gn) * E * ndirs, make_int2(-1, 0));
-    for (int di = 0; di < ndirs; ++di) {
+    const long long nchunk = 256;
+    parallel_for(ndirs * nchunk, [&](long long job) {
+      const int di = static_cast<int>(job / nchunk);
+      const long long c = job % nchunk, g0 = gn * c / nchunk, g1 = gn * (c + 1) / nchunk;
       int2* dst = ent.data() + static_cast<size_t>(di) * gn * E;
-      for (long long g = 0; g < gn; ++g) {
+      const int* st = stab.data() + static_cast<size_t>(di) * nsub;
+      for (long long g = g0; g < g1; ++g) {
         int2 tmp[8];
-        int key[8];
+        long long key[8];
         const int n = off[g];
         for (int i = 0; i < n; ++i) {
           tmp[i] = raw[static_cast<size_t>(g) * E + i];
           const int id = tmp[i].y >> 4;
-          key[i] = (step_of(part.counts, dim, dplan[di], subs[id].sub) << 20) | id;
+          key[i] = (static_cast<long long>(st[id]) << 32) | id;
         }
         for (int i = 1; i < n; ++i)
           for (int j = i; j > 0 && key[j] < key[j - 1]; --j) {
@@ -1166,9 +1231,10 @@ void DdmHandle::build(const hs_problem& P, int device) {
           }
         for (int i = 0; i < n; ++i) dst[g * E + i] = tmp[i];
       }
-    }
+    });
     acc_ent.upload(ent, eng.stream);
   }
+  phase("accumulate plan");
   // step groups and dataflow task lists per (sweep direction, step)
   steps = sweep_step_count(part.counts, dim);
   ndir = 1 << dim;
@@ -1187,6 +1253,7 @@ void DdmHandle::build(const hs_problem& P, int device) {
     }
   d_groups.upload(gflat, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
+  phase("step groups");
 }
 
 // Macro-step schedule of one application: task (l, id) runs one macro-step after the latest of
