@@ -22,6 +22,8 @@
  *   hs_ddm_apply_op
  *       SparseOperator::apply on DdmSolver::global_op include/helmsweep/operator.hpp:25,
  *                                                    include/helmsweep/sweeper.hpp:77
+ *   hs_ddm_global_solve
+ *       global_direct_solve(cfg, f)                  src/harness.cpp:185-214
  *   hs_gmres
  *       gmres(op, precond, b, cfg) as wired by run_precond
  *                                                    include/helmsweep/krylov.hpp:30-36,
@@ -158,6 +160,13 @@ int hs_ddm_apply_op(hs_ddm* s, int nrhs, const double* x, double* y);
  * independent Krylov process per RHS, batched through the device. */
 int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
              hs_gmres_report* reports);
+
+/* global_direct_solve (src/harness.cpp:185-214): u = A^-1 (J f) on the padded global grid with
+ * the device sparse-direct factorization of the global J-scaled operator (factorized on first
+ * use and kept by the handle; stats, may be NULL, receives its FactorStats). Host buffers, nrhs
+ * RHS-major vectors; HS_ERR_CONFIG above the reference's memory guard (4.5e6 nodes in 2D,
+ * 4.5e5 in 3D). nrhs = 0 only factorizes. */
+int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double* u, hs_factor_stats* stats);
 
 /* Device profile of the most recent timed hs_ddm_solve[_device] batch: total duration of the
  * multifrontal solve launches (forward + backward, CUDA events), their count, the subdomain

@@ -8,6 +8,7 @@
 //   DdmSolver(setup)              sweeper.hpp:70  helmsweep_b200::DdmSolver(problem)
 //   DdmSolver::ddm_solve(b, rounds, rep, tr) :84  DdmSolver::ddm_solve(...) (+ batched form)
 //   gmres(op, pc, b, cfg)          krylov.hpp:35  DdmSolver::gmres(...)
+//   global_direct_solve(cfg, f)   harness.cpp:185  DdmSolver::global_direct_solve(...)
 //
 // Errors are rethrown as ConfigError / DataError / SingularMatrixError(pivot_index) with the
 // reference's meaning (include/helmsweep/common.hpp:18-35); CudaError when no device works.
@@ -128,6 +129,12 @@ class DdmSolver {
     CVector y(x.size());
     check(hs_ddm_apply_op(s_, 1, dp(x.data()), dp(y.data())));
     return y;
+  }
+  // global_direct_solve (src/harness.cpp:185-214): A^-1 (J f) on the global grid, device LDL^T
+  CVector global_direct_solve(const CVector& f, hs_factor_stats* stats = nullptr) {
+    CVector u(f.size());
+    check(hs_ddm_global_solve(s_, 1, dp(f.data()), dp(u.data()), stats));
+    return u;
   }
   CVector gmres(const CVector& b, double tol, int maxit, int rounds, hs_gmres_report* report = nullptr) {
     CVector x(b.size());

@@ -93,6 +93,8 @@ SIGNATURES = {
                                            ctypes.c_int, ctypes.c_int, ctypes.POINTER(SolveReportC),
                                            ctypes.c_void_p]),
     "hs_ddm_apply_op": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p]),
+    "hs_ddm_global_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p,
+                                           ctypes.POINTER(FactorStats)]),
     "hs_gmres": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(GmresReportC)]),
     "hs_ddm_profile": (ctypes.c_int, [ctypes.c_void_p, c_dbl_p, c_i64_p, c_i64_p, c_dbl_p, c_dbl_p]),

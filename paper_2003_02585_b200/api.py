@@ -346,6 +346,21 @@ class DdmSolver:
             _raise(rc)
         return y
 
+    def global_direct_solve(self, f, stats: Optional[list] = None):
+        """global_direct_solve(cfg, f) (src/harness.cpp:185-214): u = A^-1 (J f) on the padded
+        global grid with the device sparse-direct factorization of the global operator (built on
+        first use, then kept). f: (N,) or (R, N) physical source."""
+        f = _as_c128(f)
+        u = np.zeros_like(f)
+        nrhs = 1 if f.ndim == 1 else f.shape[0]
+        st = L.FactorStats()
+        rc = L.lib().hs_ddm_global_solve(self._h, nrhs, _dptr(f), _dptr(u), ctypes.byref(st))
+        if rc:
+            _raise(rc)
+        if stats is not None:
+            stats.append(st)
+        return u
+
     def gmres(self, b, tol=1e-6, maxit=100, rounds=1):
         """gmres(A.apply, ddm_solve, b, cfg) as run_precond wires it (src/harness.cpp:285-305)."""
         b = _as_c128(b)

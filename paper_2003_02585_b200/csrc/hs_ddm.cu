@@ -732,6 +732,30 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
 }  // namespace
 }  // namespace hsb
 
+namespace hsb {
+// One sparse-direct factorization on the device (the engine of factorize(), src/direct.cpp:333-348).
+std::unique_ptr<hs_factor> make_factor(int dim, const GridRange& rng, std::vector<std::int64_t> rp,
+                                       std::vector<std::int64_t> cl, const CVector& v, int device) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto f = std::make_unique<hs_factor>();
+  FactorHandle& H = f->h;
+  H.eng.init(device, dim);
+  const std::int64_t n = rng.count(), nnz = rp[n];
+  H.eng.sub_cls.push_back(H.eng.add_class(build_symbolic(dim, rng, rp, cl)));
+  H.eng.upload_classes(-1);
+  H.eng.factorize({&v});
+  const SymbolicClass& c = *H.eng.classes[0]->sym;
+  H.nz.alloc(1);
+  HS_CUDA(cudaStreamSynchronize(H.eng.stream));
+  H.stats.n = n;
+  H.stats.matrix_nnz = nnz;
+  H.stats.factor_nnz = c.factor_nnz;
+  H.stats.peak_bytes = c.peak_bytes;
+  H.stats.factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return f;
+}
+}  // namespace hsb
+
 using namespace hsb;
 
 extern "C" {
@@ -760,24 +784,10 @@ int hs_factorize(int dim, const int lo[3], const int hi[3], int64_t n, const int
       rng.hi[a] = a < dim ? hi[a] : 0;
     }
     if (rng.count() != n) config_error("factorize: grid range does not match operator size");
-    const auto t0 = std::chrono::steady_clock::now();
-    f = std::make_unique<hs_factor>();
-    FactorHandle& H = f->h;
-    H.eng.init(device, dim);
     std::vector<std::int64_t> rp(row_ptr, row_ptr + n + 1), cl(col, col + row_ptr[n]);
     CVector v(reinterpret_cast<const Complex*>(val), reinterpret_cast<const Complex*>(val) + row_ptr[n]);
-    H.eng.sub_cls.push_back(H.eng.add_class(build_symbolic(dim, rng, rp, cl)));
-    H.eng.upload_classes(-1);
-    H.eng.factorize({&v});
-    const SymbolicClass& c = *H.eng.classes[0]->sym;
-    H.nz.alloc(1);
-    HS_CUDA(cudaStreamSynchronize(H.eng.stream));
-    H.stats.n = n;
-    H.stats.matrix_nnz = row_ptr[n];
-    H.stats.factor_nnz = c.factor_nnz;
-    H.stats.peak_bytes = c.peak_bytes;
-    H.stats.factor_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    if (stats) *stats = H.stats;
+    f = make_factor(dim, rng, std::move(rp), std::move(cl), v, device);
+    if (stats) *stats = f->h.stats;
   }, nullptr, pivot_index);
   if (rc != kOk) return rc;
   *out = f.release();
@@ -888,7 +898,8 @@ struct DdmHandle {
   DBuf<double2> bN, u, io;
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
   std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l's accumulate, then macro-step solve pairs
-  // global operator (lazy)
+  // global operator (lazy) and its direct factorization (global_direct_solve, lazy)
+  hs_factor* gfact = nullptr;
   bool gop_ready = false;
   long long g_nnz = 0;
   DBuf<std::int64_t> g_rp;
@@ -900,6 +911,7 @@ struct DdmHandle {
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
     if (cstream) cudaStreamDestroy(cstream);
+    if (gfact) hs_factor_destroy(gfact);
   }
 
   void build(const hs_problem& P, int device);
@@ -2042,4 +2054,40 @@ extern "C" int hs_route_trace(int dim, int rounds, int gen_sweep, int axis, int 
   } catch (...) {
     return -1;
   }
+}
+
+// global_direct_solve (src/harness.cpp:185-214): b = J f off the shell on the padded global grid,
+// then the direct factorization of the global J-scaled operator (built on first use and kept).
+extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double* u, hs_factor_stats* stats) {
+  return guarded([&] {
+    if (!s) config_error("global_direct_solve: null handle");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    const std::int64_t n = H.ggrid.range.count();
+    const std::int64_t guard = H.dim == 2 ? 4'500'000 : 450'000;  // src/harness.cpp:19-20
+    if (n > guard)
+      config_error("global_direct_solve: " + std::to_string(n) +
+                   " nodes exceed the direct-solve memory guard; reduce the scale");
+    if (!H.gfact) {
+      Csr op = assemble(H.ggrid, H.gcoeffs, H.gkappa);
+      H.gfact = make_factor(H.dim, H.ggrid.range, std::move(op.row_ptr), std::move(op.col), op.val, H.eng.device)
+                    .release();
+    }
+    if (stats) *stats = H.gfact->h.stats;
+    if (nrhs <= 0) return;
+    const Complex* fi = reinterpret_cast<const Complex*>(f);
+    Complex* bo = reinterpret_cast<Complex*>(u);
+    parallel_for(nrhs, [&](long long r) {
+      for (std::int64_t i = 0; i < n; ++i) {
+        const Vec3i p = H.ggrid.range.unlinear(i);
+        bo[r * n + i] = H.ggrid.on_shell(p) ? Complex(0.0) : H.gcoeffs.jacobian(p) * fi[r * n + i];
+      }
+    });
+    FactorHandle& F = H.gfact->h;
+    F.io.alloc(static_cast<size_t>(n) * nrhs);
+    HS_CUDA(cudaMemcpyAsync(F.io.p, u, sizeof(double2) * n * nrhs, cudaMemcpyHostToDevice, F.eng.stream));
+    factor_solve_device(F, nrhs, F.io.p, nullptr);
+    HS_CUDA(cudaMemcpyAsync(u, F.io.p, sizeof(double2) * n * nrhs, cudaMemcpyDeviceToHost, F.eng.stream));
+    HS_CUDA(cudaStreamSynchronize(F.eng.stream));
+  });
 }

@@ -199,3 +199,49 @@ def test_c2_subdomain_factor_against_oracle(hs):
         X = f.solve(b)
         for r in range(3):
             assert rel(X[r], fo.solve(b[r])) <= 1e-11
+
+
+@pytest.mark.parametrize("rounds", [1, 2])
+def test_streamed_host_path_equals_device_path(hs, golden, rounds):
+    """hs_ddm_solve with pinned host buffers streams b / u by stripes around the macro-step
+    schedule; it must return exactly the device-buffer result (and the pageable-buffer one)."""
+    torch = pytest.importorskip("torch")
+    z = golden("ddm_2d_3x2_r2")
+    s = hs.DdmSolver(_setup(hs, z))
+    b = np.ascontiguousarray(z["b"], dtype=np.complex128)  # (R, N) RHS-major
+    R = b.shape[0]
+    hb = torch.from_numpy(b.view(np.float64)).pin_memory()
+    hu = torch.empty_like(hb).pin_memory()
+    s.ddm_solve_host_ptr(hb.data_ptr(), hu.data_ptr(), R, rounds, True)
+    db = hb.cuda()
+    du = torch.empty_like(db)
+    s.ddm_solve_device(db.data_ptr(), du.data_ptr(), R, rounds, True)
+    torch.cuda.synchronize()
+    assert torch.equal(hu, du.cpu())
+    u_pageable = s.ddm_solve(b, rounds, None, True)
+    assert np.array_equal(hu.numpy().view(np.complex128).reshape(R, -1), np.asarray(u_pageable).reshape(R, -1))
+
+
+def test_global_direct_solve_matches_sparse_lu(hs):
+    """global_direct_solve (src/harness.cpp:185-214) on the device factorization against an
+    independent sparse LU (SuperLU) of the same J-scaled global operator; and the DDM solution
+    compared with it, as the reference's direct-solver mode does (compare.global)."""
+    spla = pytest.importorskip("scipy.sparse.linalg")
+    sp = pytest.importorskip("scipy.sparse")
+    n, pad, kap = 128, 12, 2 * math.pi * 8
+    so = O.DdmSolver(O.ProblemSetup(O.Box(2), [n, n, 1], [2, 2, 1], O.Medium("constant", kappa=kap),
+                                    O.PmlSpec(width=pad)))
+    f = O.gaussian_source(so.ggrid, O.Box(2), [[0.5, 0.5], [0.3, 0.62]], 2.0 / n).T.copy()  # (2, N)
+    s = hs.DdmSolver(hs.ProblemSetup(2, [n, n], [2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
+    stats = []
+    u = s.global_direct_solve(f, stats)
+    op = so.global_op()
+    A = sp.csr_matrix((op.val, op.col, op.row_ptr), shape=(len(op.row_ptr) - 1,) * 2).tocsc()
+    b = so.scale_source(f.T).T.copy()
+    lu = spla.splu(A)
+    for r in range(2):
+        assert rel(u[r], lu.solve(b[r])) <= TOL
+    assert stats[0].n == A.shape[0] and stats[0].matrix_nnz == A.nnz
+    U = s.ddm_solve(b, 1)
+    for r in range(2):  # sanity: one round of diagonal sweeps approximates the global solve
+        assert rel(U[r], u[r]) < 0.5
