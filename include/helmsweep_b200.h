@@ -24,6 +24,9 @@
  *                                                    include/helmsweep/sweeper.hpp:77
  *   hs_ddm_global_solve
  *       global_direct_solve(cfg, f)                  src/harness.cpp:185-214
+ *   hs_read/write_velocity_grid, hs_read_velocity_csv, hs_write_field / hs_read_field
+ *       read/write_velocity_grid, read_velocity_csv  include/helmsweep/media.hpp:22-27
+ *       write_field / read_field                     include/helmsweep/harness.hpp:10-16
  *   hs_gmres
  *       gmres(op, precond, b, cfg) as wired by run_precond
  *                                                    include/helmsweep/krylov.hpp:30-36,
@@ -177,6 +180,26 @@ int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, in
 /* Route table of the reference's route_trace (src/sweeper.cpp:58-73): target sweep of a
  * trace generated in sweep gen_sweep (1-based) travelling along (axis, sign); 0 = discard. */
 int hs_route_trace(int dim, int rounds, int gen_sweep, int axis, int sign);
+
+/* ---- On-disk formats (byte-exact with the reference) -------------------------------- */
+/* HSVG velocity grid (include/helmsweep/media.hpp:22-27, src/media.cpp:58-100): "HSVG", u32
+ * version 1, u32 dim, u32 n[3], f64 origin[3], f64 spacing[3], f32 samples (axis 0 fastest).
+ * Readers fill the header and, when c != NULL and cap >= *count, the samples (call once with
+ * c = NULL to size the buffer). Errors: HS_ERR_DATA (open, magic, version, dims, truncation,
+ * VelocityGrid::validate). */
+int hs_read_velocity_grid(const char* path, int* dim, int n[3], double origin[3], double spacing[3], float* c,
+                          int64_t cap, int64_t* count);
+int hs_write_velocity_grid(const char* path, int dim, const int n[3], const double origin[3], const double spacing[3],
+                           const float* c);
+/* CSV fallback (src/media.cpp:102-130): "dim,n..,origin..,spacing.." then one sample per line. */
+int hs_read_velocity_csv(const char* path, int* dim, int n[3], double origin[3], double spacing[3], float* c,
+                         int64_t cap, int64_t* count);
+/* HSFD field dump (src/harness.cpp:32-83): "HSFD", u32 version 1, u32 dim, u32 n[3], i32 lo[3],
+ * f64 h[3], f64 origin[3], complex128 values over the grid range [lo, hi] (axis 0 fastest). */
+int hs_write_field(const char* path, int dim, const int lo[3], const int hi[3], const double h[3],
+                   const double origin[3], const double* u);
+int hs_read_field(const char* path, int* dim, int lo[3], int hi[3], double h[3], double origin[3], double* u,
+                  int64_t cap, int64_t* count);
 
 /* Number of kernel launches issued by this library since load (evidence counter). */
 int64_t hs_kernel_launches(void);

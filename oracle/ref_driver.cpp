@@ -11,7 +11,11 @@
 //   gmres                                   proj/include/helmsweep/krylov.hpp:30-36
 //   sample_source / global_direct_solve     proj/include/helmsweep/harness.hpp:17-41
 //   parse_config_text                       proj/include/helmsweep/config.hpp:55
+//   write_velocity_grid / read_velocity_grid proj/include/helmsweep/media.hpp:22-27
+//   write_field / read_field                proj/include/helmsweep/harness.hpp:10-16
 #include <chrono>
+#include <cstdint>
+#include <span>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -333,6 +337,64 @@ int hsref_pml_operator(int dim, int n, int pad, double kappa, long long* rows, l
       for (size_t i = 0; i < op.col.size(); ++i) col[i] = op.col[i];
       std::memcpy(val, op.val.data(), op.val.size() * sizeof(Complex));
     }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+
+// On-disk formats through the reference's own writers / readers (golden fixtures of the HSVG
+// velocity grid and the HSFD field dump).
+int hsref_write_velocity_grid(const char* path, int dim, const int n[3], const double origin[3],
+                              const double spacing[3], const float* c) {
+  try {
+    VelocityGrid g;
+    g.dim = dim;
+    std::int64_t count = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.n[a] = n[a];
+      g.origin[a] = origin[a];
+      g.spacing[a] = spacing[a];
+    }
+    for (int a = 0; a < dim; ++a) count *= n[a];
+    g.c.assign(c, c + count);
+    write_velocity_grid(path, g);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int hsref_read_velocity_grid(const char* path, int* dim, int n[3], double origin[3], double spacing[3],
+                             float* c, long long cap, long long* count) {
+  try {
+    VelocityGrid g = read_velocity_grid(path);
+    *dim = g.dim;
+    for (int a = 0; a < 3; ++a) {
+      n[a] = g.n[a];
+      origin[a] = g.origin[a];
+      spacing[a] = g.spacing[a];
+    }
+    *count = static_cast<long long>(g.c.size());
+    if (c && cap >= *count) std::memcpy(c, g.c.data(), g.c.size() * sizeof(float));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+int hsref_write_field(const char* path, int dim, const int lo[3], const int hi[3], const double h[3],
+                      const double origin[3], const double* u) {
+  try {
+    LocalGrid g;
+    g.dim = dim;
+    g.range.dim = dim;
+    for (int a = 0; a < 3; ++a) {
+      g.range.lo[a] = lo[a];
+      g.range.hi[a] = hi[a];
+      g.h[a] = h[a];
+      g.origin[a] = origin[a];
+    }
+    write_field(path, g, std::span<const Complex>(cx(u), static_cast<size_t>(g.node_count())));
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

@@ -2,13 +2,15 @@
 as hand-written sm_100a CUDA behind a C-ABI (include/helmsweep_b200.h).
 
 Python here is only the test/bench plumbing over the C-ABI; see ``api`` for the mirror of
-the reference's Factorization / DdmSolver / gmres interface.
+the reference's Factorization / DdmSolver / gmres interface and its on-disk formats.
 """
-from .api import (ConfigError, CudaError, DataError, DdmSolver, Factorization, GmresResult, HelmsweepError,
-                  Medium, ProblemSetup, SingularMatrixError, SolveReport, SparseOperator, device_count,
-                  factorize, kernel_launches, route_trace)
+from .api import (ConfigError, CudaError, DataError, DdmSolver, Factorization, FieldDump, GmresResult,
+                  HelmsweepError, Medium, ProblemSetup, SingularMatrixError, SolveReport, SparseOperator,
+                  VelocityGrid, device_count, factorize, kernel_launches, read_field, read_velocity_csv,
+                  read_velocity_grid, route_trace, write_field, write_velocity_grid)
 from ._lib import LIB_PATH
 
-__all__ = ["ConfigError", "CudaError", "DataError", "DdmSolver", "Factorization", "GmresResult",
+__all__ = ["ConfigError", "CudaError", "DataError", "DdmSolver", "Factorization", "FieldDump", "GmresResult",
            "HelmsweepError", "Medium", "ProblemSetup", "SingularMatrixError", "SolveReport", "SparseOperator",
-           "device_count", "factorize", "kernel_launches", "route_trace", "LIB_PATH"]
+           "VelocityGrid", "device_count", "factorize", "kernel_launches", "read_field", "read_velocity_csv",
+           "read_velocity_grid", "route_trace", "write_field", "write_velocity_grid", "LIB_PATH"]

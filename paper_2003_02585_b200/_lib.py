@@ -95,6 +95,19 @@ SIGNATURES = {
     "hs_ddm_apply_op": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p]),
     "hs_ddm_global_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p,
                                            ctypes.POINTER(FactorStats)]),
+    "hs_read_velocity_grid": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                             c_dbl_p, c_dbl_p, ctypes.POINTER(ctypes.c_float), ctypes.c_int64,
+                                             ctypes.POINTER(ctypes.c_int64)]),
+    "hs_write_velocity_grid": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_dbl_p,
+                                              c_dbl_p, ctypes.POINTER(ctypes.c_float)]),
+    "hs_read_velocity_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                            c_dbl_p, c_dbl_p, ctypes.POINTER(ctypes.c_float), ctypes.c_int64,
+                                            ctypes.POINTER(ctypes.c_int64)]),
+    "hs_write_field": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int), c_dbl_p, c_dbl_p, c_dbl_p]),
+    "hs_read_field": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                     ctypes.POINTER(ctypes.c_int), c_dbl_p, c_dbl_p, c_dbl_p, ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int64)]),
     "hs_gmres": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(GmresReportC)]),
     "hs_ddm_profile": (ctypes.c_int, [ctypes.c_void_p, c_dbl_p, c_i64_p, c_i64_p, c_dbl_p, c_dbl_p]),

@@ -389,3 +389,96 @@ def kernel_launches():
 
 def device_count():
     return int(L.lib().hs_device_count())
+
+
+# ---------------------------------------------------------------------------------------------
+# On-disk formats (byte-exact with the reference): HSVG velocity grids, HSFD field dumps.
+
+@dataclass
+class VelocityGrid:
+    """VelocityGrid (include/helmsweep/media.hpp:11-20): samples c (float32, axis 0 fastest)."""
+    dim: int
+    n: Sequence[int]
+    origin: Sequence[float]
+    spacing: Sequence[float]
+    c: np.ndarray
+
+    def medium(self, omega: float) -> Medium:
+        """The gridded WaveNumberModel kappa = omega / c(x) (include/helmsweep/media.hpp:31-55)."""
+        return Medium("gridded", velocity=self.c, vel_n=tuple(self.n), vel_origin=tuple(self.origin),
+                      vel_spacing=tuple(self.spacing), omega=omega)
+
+
+@dataclass
+class FieldDump:
+    """FieldDump (include/helmsweep/harness.hpp:12-15): a complex field on a grid range."""
+    dim: int
+    lo: Sequence[int]
+    hi: Sequence[int]
+    h: Sequence[float]
+    origin: Sequence[float]
+    values: np.ndarray
+
+
+def _read_vel(fn, path):
+    dim, n = ctypes.c_int(), (ctypes.c_int * 3)()
+    org, sp, count = (ctypes.c_double * 3)(), (ctypes.c_double * 3)(), ctypes.c_int64()
+    rc = fn(str(path).encode(), ctypes.byref(dim), n, org, sp, None, 0, ctypes.byref(count))
+    if rc:
+        _raise(rc)
+    c = np.empty(count.value, dtype=np.float32)
+    rc = fn(str(path).encode(), ctypes.byref(dim), n, org, sp, c.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+            count.value, ctypes.byref(count))
+    if rc:
+        _raise(rc)
+    return VelocityGrid(dim.value, list(n), list(org), list(sp), c)
+
+
+def read_velocity_grid(path) -> VelocityGrid:
+    """read_velocity_grid (src/media.cpp:58-84): the HSVG binary layout."""
+    return _read_vel(L.lib().hs_read_velocity_grid, path)
+
+
+def read_velocity_csv(path) -> VelocityGrid:
+    """read_velocity_csv (src/media.cpp:102-130): header "dim,n..,origin..,spacing..", one value per line."""
+    return _read_vel(L.lib().hs_read_velocity_csv, path)
+
+
+def write_velocity_grid(path, g: VelocityGrid) -> None:
+    """write_velocity_grid (src/media.cpp:86-100)."""
+    c = np.ascontiguousarray(g.c, dtype=np.float32)
+    n = (ctypes.c_int * 3)(*(list(g.n) + [1] * 3)[:3])
+    rc = L.lib().hs_write_velocity_grid(str(path).encode(), int(g.dim), n, (ctypes.c_double * 3)(*g.origin[:3]),
+                                        (ctypes.c_double * 3)(*g.spacing[:3]),
+                                        c.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+    if rc:
+        _raise(rc)
+
+
+def write_field(path, dim, lo, hi, h, origin, u) -> None:
+    """write_field (src/harness.cpp:32-53): u over the grid range [lo, hi] (axis 0 fastest)."""
+    u = _as_c128(u).ravel()
+    lo3, hi3 = (list(lo) + [0] * 3)[:3], (list(hi) + [0] * 3)[:3]
+    count = int(np.prod([hi3[a] - lo3[a] + 1 for a in range(dim)]))
+    if u.size != count:
+        raise ConfigError("write_field: size mismatch")
+    rc = L.lib().hs_write_field(str(path).encode(), int(dim), (ctypes.c_int * 3)(*lo3), (ctypes.c_int * 3)(*hi3),
+                                (ctypes.c_double * 3)(*(list(h) + [0.0] * 3)[:3]),
+                                (ctypes.c_double * 3)(*(list(origin) + [0.0] * 3)[:3]), _dptr(u))
+    if rc:
+        _raise(rc)
+
+
+def read_field(path) -> FieldDump:
+    """read_field (src/harness.cpp:55-83)."""
+    dim, lo, hi = ctypes.c_int(), (ctypes.c_int * 3)(), (ctypes.c_int * 3)()
+    h, org, count = (ctypes.c_double * 3)(), (ctypes.c_double * 3)(), ctypes.c_int64()
+    fn = L.lib().hs_read_field
+    rc = fn(str(path).encode(), ctypes.byref(dim), lo, hi, h, org, None, 0, ctypes.byref(count))
+    if rc:
+        _raise(rc)
+    u = np.empty(count.value, dtype=np.complex128)
+    rc = fn(str(path).encode(), ctypes.byref(dim), lo, hi, h, org, _dptr(u), count.value, ctypes.byref(count))
+    if rc:
+        _raise(rc)
+    return FieldDump(dim.value, list(lo), list(hi), list(h), list(org), u)

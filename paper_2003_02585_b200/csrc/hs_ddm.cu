@@ -2091,3 +2091,7 @@ extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double*
     HS_CUDA(cudaStreamSynchronize(F.eng.stream));
   });
 }
+
+namespace hsb {
+std::string& last_error_ref() { return g_last_error; }  // shared with the on-disk format entry points (hs_io.cpp)
+}  // namespace hsb

@@ -10,6 +10,8 @@ sigma = 2h, on interior nodes, b = DdmSolver::scale_source(f) computed by the re
   ddm_*                   DdmSolver::ddm_solve u, SolveReport counters, contrib norms, residuals
   gmres_2d                run_precond-style GMRES: iterations, history, x
   routing                 route_trace tables (Appendix B of SURVEY.md)
+  io_*                    HSVG velocity grids and an HSFD field dump written by the reference's own
+                          write_velocity_grid / write_field (byte-exact format pins)
 """
 from __future__ import annotations
 
@@ -114,7 +116,41 @@ def make_routing():
     np.savez_compressed(os.path.join(HERE, "routing.npz"), **out)
 
 
+def make_io():
+    """HSVG / HSFD files written by the reference (include/helmsweep/media.hpp:22-27,
+    src/harness.cpp:32-53) plus the arrays they hold."""
+    import ctypes
+    L = R.lib()
+    rng = np.random.default_rng(7)
+    dbl3, int3 = ctypes.c_double * 3, ctypes.c_int * 3
+    arrays = {}
+    for name, dim, n, org, sp in [("io_vel2d", 2, [5, 4, 1], [0.0, -0.5, 0.0], [0.25, 0.5, 0.0]),
+                                  ("io_vel3d", 3, [3, 3, 2], [0.1, 0.2, 0.3], [0.5, 0.5, 1.0])]:
+        c = (1.0 + rng.random(int(np.prod(n[:dim])))).astype(np.float32)
+        path = os.path.join(HERE, name + ".hsvg")
+        rc = L.hsref_write_velocity_grid(path.encode(), dim, int3(*n), dbl3(*org), dbl3(*sp),
+                                         c.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+        assert rc == 0, L.hsref_last_error()
+        arrays[name] = c
+        arrays[name + "_hdr"] = np.array([dim, *n], dtype=np.int64)
+        arrays[name + "_geo"] = np.array([*org, *sp], dtype=np.float64)
+    lo, hi, h, org = [-2, -1, 0], [3, 3, 0], [0.125, 0.25, 0.0], [0.0, 0.0, 0.0]
+    u = (rng.standard_normal(6 * 5) + 1j * rng.standard_normal(6 * 5)).astype(np.complex128)
+    path = os.path.join(HERE, "io_field2d.hsfd")
+    rc = L.hsref_write_field(path.encode(), 2, int3(*lo), int3(*hi), dbl3(*h), dbl3(*org),
+                             u.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    assert rc == 0, L.hsref_last_error()
+    arrays["io_field2d"] = u
+    arrays["io_field2d_geo"] = np.array([*lo, *hi], dtype=np.int64)
+    arrays["io_field2d_hdr"] = np.array([*h, *org], dtype=np.float64)
+    np.savez(os.path.join(HERE, "io.npz"), **arrays)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["io"]:
+        make_io()
+        sys.exit(0)
+    make_io()
     make_routing()
     make_direct("direct_2d", 2, 12, 3, 9.0, 11)
     make_direct("direct_3d", 3, 8, 3, 9.0, 11)
