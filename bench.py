@@ -285,6 +285,19 @@ def run_gpu(args, rank, world, local_rank):
         "subdomain_solves_per_step": prof["subdomain_solves"],
         "device_host_paths_agree": ok,
     }
+    # The paper's pipeline cost model (src/pipeline.cpp) next to the device schedule: the model
+    # runs one processor per subdomain, one RHS per tick; the device levels the same trace-routing
+    # task graph into macro-steps and solves each task for the whole 16-RHS batch at once.
+    sched = s.schedule_info(rounds)
+    sim1 = hs.simulate_pipeline(2, list(CFG["parts"]), 1, rounds, 1.0)
+    simR = hs.simulate_pipeline(2, list(CFG["parts"]), R, rounds, 1.0)
+    line["pipeline_model"] = {
+        "device_macro_steps": sched["macro_steps"], "device_max_width": sched["max_width"],
+        "reference_sequential_steps": sched["sequential_steps"], "x_buffers": sched["buffers"],
+        "model_ticks_1_rhs": sim1.makespan, f"model_ticks_{R}_rhs": simR.makespan,
+        "model_closed_form_ticks_per_rhs": hs.average_time_per_rhs(2, list(CFG["parts"]), R, rounds, 1.0).average_per_rhs,
+        "device_t0_us_per_16rhs_task": 1e6 * prof["solve_seconds"] / max(prof["subdomain_solves"], 1),
+        "device_ms_per_macro_step": ms_max / max(sched["macro_steps"], 1)}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(b[0])
     print(json.dumps(line))

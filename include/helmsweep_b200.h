@@ -27,6 +27,8 @@
  *   hs_read/write_velocity_grid, hs_read_velocity_csv, hs_write_field / hs_read_field
  *       read/write_velocity_grid, read_velocity_csv  include/helmsweep/media.hpp:22-27
  *       write_field / read_field                     include/helmsweep/harness.hpp:10-16
+ *   hs_pipeline_cost / hs_pipeline_simulate
+ *       average_time_per_rhs / simulate_pipeline     include/helmsweep/pipeline.hpp:27-44
  *   hs_gmres
  *       gmres(op, precond, b, cfg) as wired by run_precond
  *                                                    include/helmsweep/krylov.hpp:30-36,
@@ -200,6 +202,21 @@ int hs_write_field(const char* path, int dim, const int lo[3], const int hi[3], 
                    const double origin[3], const double* u);
 int hs_read_field(const char* path, int* dim, int lo[3], int hi[3], double h[3], double origin[3], double* u,
                   int64_t cap, int64_t* count);
+
+/* Shape of the device sweep schedule for `rounds` rounds:
+ * macro-steps (dependency levels of the (sweep, subdomain) task graph), the widest one, the
+ * reference's sequential step count (sweeps x anti-diagonal steps) and the x buffers in flight. */
+int hs_ddm_schedule_info(hs_ddm* s, int rounds, int* macro_steps, int* max_width, int* sequential_steps,
+                         int* buffers);
+
+/* ---- Pipeline cost model (include/helmsweep/pipeline.hpp, src/pipeline.cpp:20-111) ------ */
+/* PipelineScenario {dim, counts, n_rhs, n_iter, t0}: closed form average_time_per_rhs and the
+ * discrete-event simulate_pipeline (one unit-capacity processor per subdomain, trace-routing
+ * precedence). completion_times (may be NULL) receives n_rhs values. HS_ERR_CONFIG on bad input. */
+int hs_pipeline_cost(int dim, const int counts[3], int n_rhs, int n_iter, double t0, double* average_per_rhs,
+                     double* idle_fraction);
+int hs_pipeline_simulate(int dim, const int counts[3], int n_rhs, int n_iter, double t0, double* completion_times,
+                         double* makespan, double* average_per_rhs);
 
 /* Number of kernel launches issued by this library since load (evidence counter). */
 int64_t hs_kernel_launches(void);

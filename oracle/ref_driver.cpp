@@ -21,6 +21,7 @@
 #include <string>
 
 #include "helmsweep/harness.hpp"
+#include "helmsweep/pipeline.hpp"
 
 using namespace helmsweep;
 
@@ -395,6 +396,30 @@ int hsref_write_field(const char* path, int dim, const int lo[3], const int hi[3
       g.origin[a] = origin[a];
     }
     write_field(path, g, std::span<const Complex>(cx(u), static_cast<size_t>(g.node_count())));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+
+// Pipeline cost model through the reference (src/pipeline.cpp:20-111).
+int hsref_pipeline(int dim, const int counts[3], int n_rhs, int n_iter, double t0, double* avg_closed,
+                   double* idle, double* makespan, double* avg_sim, double* completion) {
+  try {
+    PipelineScenario sc;
+    sc.dim = dim;
+    sc.counts = Vec3i{counts[0], counts[1], counts[2]};
+    sc.n_rhs = n_rhs;
+    sc.n_iter = n_iter;
+    sc.t0 = t0;
+    const PipelineCost c = average_time_per_rhs(sc);
+    const PipelineSimulation sim = simulate_pipeline(sc);
+    *avg_closed = c.average_per_rhs;
+    *idle = c.idle_fraction;
+    *makespan = sim.makespan;
+    *avg_sim = sim.average_per_rhs;
+    for (int r = 0; r < n_rhs; ++r) completion[r] = sim.completion_times[r];
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

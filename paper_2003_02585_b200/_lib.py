@@ -95,6 +95,13 @@ SIGNATURES = {
     "hs_ddm_apply_op": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p]),
     "hs_ddm_global_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p,
                                            ctypes.POINTER(FactorStats)]),
+    "hs_ddm_schedule_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int)]),
+    "hs_pipeline_cost": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_double, c_dbl_p, c_dbl_p]),
+    "hs_pipeline_simulate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_double, c_dbl_p, c_dbl_p, c_dbl_p]),
     "hs_read_velocity_grid": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                              c_dbl_p, c_dbl_p, ctypes.POINTER(ctypes.c_float), ctypes.c_int64,
                                              ctypes.POINTER(ctypes.c_int64)]),

@@ -346,6 +346,16 @@ class DdmSolver:
             _raise(rc)
         return y
 
+    def schedule_info(self, rounds=1):
+        """Device sweep schedule: macro-steps, widest macro-step, the reference's sequential step
+        count and x buffers in flight."""
+        v = [ctypes.c_int() for _ in range(4)]
+        rc = L.lib().hs_ddm_schedule_info(self._h, int(rounds), *[ctypes.byref(x) for x in v])
+        if rc:
+            _raise(rc)
+        return {"macro_steps": v[0].value, "max_width": v[1].value, "sequential_steps": v[2].value,
+                "buffers": v[3].value}
+
     def global_direct_solve(self, f, stats: Optional[list] = None):
         """global_direct_solve(cfg, f) (src/harness.cpp:185-214): u = A^-1 (J f) on the padded
         global grid with the device sparse-direct factorization of the global operator (built on
@@ -482,3 +492,44 @@ def read_field(path) -> FieldDump:
     if rc:
         _raise(rc)
     return FieldDump(dim.value, list(lo), list(hi), list(h), list(org), u)
+
+
+# ---------------------------------------------------------------------------------------------
+# Pipeline cost model (include/helmsweep/pipeline.hpp, src/pipeline.cpp:20-111)
+
+@dataclass
+class PipelineCost:
+    average_per_rhs: float
+    idle_fraction: float
+
+
+@dataclass
+class PipelineSimulation:
+    completion_times: np.ndarray
+    makespan: float
+    average_per_rhs: float
+
+
+def _counts3(counts):
+    return (ctypes.c_int * 3)(*(list(counts) + [1, 1, 1])[:3])
+
+
+def average_time_per_rhs(dim, counts, n_rhs, n_iter, t0) -> PipelineCost:
+    """Closed form 2^dim n_iter t0 + steps / n_rhs t0 (src/pipeline.cpp:20-27)."""
+    avg, idle = ctypes.c_double(), ctypes.c_double()
+    rc = L.lib().hs_pipeline_cost(int(dim), _counts3(counts), int(n_rhs), int(n_iter), float(t0),
+                                  ctypes.byref(avg), ctypes.byref(idle))
+    if rc:
+        _raise(rc)
+    return PipelineCost(avg.value, idle.value)
+
+
+def simulate_pipeline(dim, counts, n_rhs, n_iter, t0) -> PipelineSimulation:
+    """Discrete-event schedule of (rhs, sweep, subdomain) tasks (src/pipeline.cpp:29-111)."""
+    comp = np.zeros(int(n_rhs), dtype=np.float64)
+    mk, avg = ctypes.c_double(), ctypes.c_double()
+    rc = L.lib().hs_pipeline_simulate(int(dim), _counts3(counts), int(n_rhs), int(n_iter), float(t0), _dptr(comp),
+                                      ctypes.byref(mk), ctypes.byref(avg))
+    if rc:
+        _raise(rc)
+    return PipelineSimulation(comp, mk.value, avg.value)

@@ -2095,3 +2095,17 @@ extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double*
 namespace hsb {
 std::string& last_error_ref() { return g_last_error; }  // shared with the on-disk format entry points (hs_io.cpp)
 }  // namespace hsb
+
+extern "C" int hs_ddm_schedule_info(hs_ddm* s, int rounds, int* macro_steps, int* max_width, int* sequential_steps,
+                                    int* buffers) {
+  return guarded([&] {
+    if (!s) config_error("schedule_info: null handle");
+    DdmHandle& H = s->h;
+    HS_CUDA(cudaSetDevice(H.eng.device));
+    H.ensure_state(H.R > 0 ? H.R : 1, rounds);
+    if (macro_steps) *macro_steps = static_cast<int>(H.msteps.size());
+    if (max_width) *max_width = H.max_width;
+    if (sequential_steps) *sequential_steps = H.nsweeps * H.steps;
+    if (buffers) *buffers = H.nbuf;
+  });
+}
