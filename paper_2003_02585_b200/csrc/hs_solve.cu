@@ -181,17 +181,36 @@ __device__ __forceinline__ bool split_reduce(Acc<NT>& c, double* base, long long
   if (lane == 0) last = atom_add_acq_rel(arr, 1) == nch - 1;
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return false;
+  // chunk order, own partial read back like the others; CB chunks' loads in flight per round
+  constexpr int CB = NT == 1 ? 2 : 1;
   acc_zero(c);
-  for (int cc = 0; cc < nch; ++cc) {  // chunk order; own partial read back like the others
-    const double* pc = base + cc * cstride + lane;
+  for (int c0 = 0; c0 < nch; c0 += CB) {
+    double t[CB][4][NT][2][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int b = 0; b < CB; ++b) {
+      const double* pc = base + (c0 + b) * cstride + lane;
 #pragma unroll
-      for (int q = 0; q < NT; ++q)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+        for (int q = 0; q < NT; ++q)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) c.v[i][q][p][e] += __ldcg(pc + ((((i * NT + q) * 2 + p) * 2 + e) << 5));
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              t[b][i][q][p][e] = c0 + b < nch ? __ldcg(pc + ((((i * NT + q) * 2 + p) * 2 + e) << 5)) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      if (c0 + b >= nch) break;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) c.v[i][q][p][e] += t[b][i][q][p][e];
+    }
   }
   return true;
 }
