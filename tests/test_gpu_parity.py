@@ -245,3 +245,20 @@ def test_global_direct_solve_matches_sparse_lu(hs):
     U = s.ddm_solve(b, 1)
     for r in range(2):  # sanity: one round of diagonal sweeps approximates the global solve
         assert rel(U[r], u[r]) < 0.5
+
+
+def test_3d_moderate_against_oracle(hs):
+    """3D at a size with real fronts (32^3 grid, 2x2x2 subdomains of 29^3 nodes, separators up to
+    29^2): batched device sweeps against the numpy restatement, counters bit-exact."""
+    n, pad, kap = 32, 6, 2 * math.pi * 3
+    so = O.DdmSolver(O.ProblemSetup(O.Box(3), [n, n, n], [2, 2, 2], O.Medium("constant", kappa=kap),
+                                    O.PmlSpec(width=pad)))
+    f = O.gaussian_source(so.ggrid, O.Box(3), [[0.5, 0.5, 0.5], [0.3, 0.6, 0.45]], 2.0 / n)
+    b = so.scale_source(f).T.copy()
+    s = hs.DdmSolver(hs.ProblemSetup(3, [n] * 3, [2, 2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
+    reps = []
+    U = s.ddm_solve(b, 1, reps, True)
+    for r in range(2):
+        uo, ro = so.ddm_solve(b[r].copy(), 1, True)
+        assert rel(U[r], uo) <= TOL
+        assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
