@@ -541,9 +541,21 @@ __global__ void residual_kernel(long long n, const std::int64_t* row_ptr, const 
   const long long idx = row * R + r;
   double num = 0.0, den = 0.0;
   if (threadIdx.x < npb * R && row < n) {
+    // all of the row's loads in flight before the sum (rows hold <= 7 entries: 2D 5, 3D 7)
+    const long long e0 = row_ptr[row], e1 = row_ptr[row + 1];
     double2 s = czero();
-    for (long long e = row_ptr[row]; e < row_ptr[row + 1]; ++e)
-      cfma(s, val[e], x[static_cast<long long>(col[e]) * R + r]);
+    for (long long eb = e0; eb < e1; eb += 8) {
+      double2 v[8], xv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool ok = eb + q < e1;
+        v[q] = ok ? val[eb + q] : czero();
+        xv[q] = ok ? x[static_cast<long long>(col[eb + q]) * R + r] : czero();
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (eb + q < e1) cfma(s, v[q], xv[q]);
+    }
     const double2 bv = b[idx];
     const double2 dv = csub(bv, s);
     num = dv.x * dv.x + dv.y * dv.y;
@@ -608,21 +620,34 @@ __global__ void scale_cols_kernel(double2* y, const double* inv, long long n, in
   y[idx] = make_double2(y[idx].x * s, y[idx].y * s);
 }
 
+// RHS-major [R][N] <-> node-major [N][R] for nodes [n0, n1): 32 nodes x R per block through
+// shared memory, so both sides are coalesced.
+constexpr int kTransNodes = 32;
 __global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
-  const long long idx = n0 * R + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= n1 * R) return;
-  const long long node = idx / R;
-  const int r = static_cast<int>(idx % R);
-  dst[idx] = src[static_cast<long long>(r) * n + node];
+  __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
+  const long long base = n0 + static_cast<long long>(blockIdx.x) * kTransNodes;
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // read rows of src: r, then node
+    const int r = e / kTransNodes, i = e % kTransNodes;
+    if (base + i < n1) tile[i][r] = src[static_cast<long long>(r) * n + base + i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // write node-major
+    const int i = e / R, r = e % R;
+    if (base + i < n1) dst[(base + i) * R + r] = tile[i][r];
+  }
 }
-
 __global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
-  const long long w = n1 - n0;
-  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= w * R) return;
-  const int r = static_cast<int>(idx / w);
-  const long long node = n0 + idx % w;
-  dst[static_cast<long long>(r) * n + node] = src[node * R + r];
+  __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
+  const long long base = n0 + static_cast<long long>(blockIdx.x) * kTransNodes;
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // read node-major
+    const int i = e / R, r = e % R;
+    if (base + i < n1) tile[i][r] = src[(base + i) * R + r];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // write rows of dst
+    const int r = e / kTransNodes, i = e % kTransNodes;
+    if (base + i < n1) dst[static_cast<long long>(r) * n + base + i] = tile[i][r];
+  }
 }
 
 __global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
@@ -725,25 +750,27 @@ void launch_scale_cols(double2* y, const double* inv, long long n, int R, cudaSt
 }
 
 void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_in_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R, 0, n);
+  transpose_in_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n);
   after_launch();
 }
 
 void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_out_kernel<<<blocks_for(n * R), kThreads, 0, s>>>(src, dst, n, R, 0, n);
+  transpose_out_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n);
   after_launch();
 }
 
 void launch_transpose_in_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                cudaStream_t s) {
   if (n1 <= n0) return;
-  transpose_in_kernel<<<blocks_for((n1 - n0) * R), kThreads, 0, s>>>(src, dst, n, R, n0, n1);
+  transpose_in_kernel<<<static_cast<int>((n1 - n0 + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R,
+                                                                                                     n0, n1);
   after_launch();
 }
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                 cudaStream_t s) {
   if (n1 <= n0) return;
-  transpose_out_kernel<<<blocks_for((n1 - n0) * R), kThreads, 0, s>>>(src, dst, n, R, n0, n1);
+  transpose_out_kernel<<<static_cast<int>((n1 - n0 + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R,
+                                                                                                      n0, n1);
   after_launch();
 }
 
