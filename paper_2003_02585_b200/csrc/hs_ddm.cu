@@ -339,38 +339,54 @@ struct Engine {
       for (int s = s0; s < s1; ++s) fb[s - s0 + 1] = fb[s - s0] + classes[sub_cls[s]]->sym->f_total;
       int hmax = 0;
       for (int s = s0; s < s1; ++s) hmax = std::max(hmax, classes[sub_cls[s]]->sym->max_height);
+      // per height: small fronts (one CTA each) then large fronts (one CTA cluster each)
       std::vector<FactorTask> tasks;
-      std::vector<int> lstart(hmax + 2, 0), lmaxm(hmax + 1, 0);
+      std::vector<int> lstart(hmax + 2, 0), lbig(hmax + 1, 0), lmaxm(hmax + 1, 0), lmaxm_big(hmax + 1, 0);
       for (int h = 0; h <= hmax; ++h) {
         lstart[h] = static_cast<int>(tasks.size());
-        for (int s = s0; s < s1; ++s) {
-          const SymbolicClass& c = *classes[sub_cls[s]]->sym;
-          if (h > c.max_height) continue;
-          for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
-            const int f = c.order_up[q];
-            tasks.push_back(FactorTask{s, f, fb[s - s0]});
-            lmaxm[h] = std::max(lmaxm[h], c.fronts[f].m);
+        for (int pass = 0; pass < 2; ++pass) {
+          if (pass == 1) lbig[h] = static_cast<int>(tasks.size());
+          for (int s = s0; s < s1; ++s) {
+            const SymbolicClass& c = *classes[sub_cls[s]]->sym;
+            if (h > c.max_height) continue;
+            for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
+              const int f = c.order_up[q];
+              const bool big = c.fronts[f].m >= kFactorBigM;
+              if (big != (pass == 1)) continue;
+              tasks.push_back(FactorTask{s, f, fb[s - s0]});
+              int& mx = big ? lmaxm_big[h] : lmaxm[h];
+              mx = std::max(mx, c.fronts[f].m);
+            }
           }
         }
       }
       lstart[hmax + 1] = static_cast<int>(tasks.size());
       d_tasks.upload(tasks, stream);
       for (int h = 0; h <= hmax; ++h) {
-        const int nt = lstart[h + 1] - lstart[h];
-        if (nt == 0) continue;
         FactorArgs fa{};
-        fa.tasks = d_tasks.p + lstart[h];
-        fa.ntasks = nt;
         fa.cls = d_cls.p;
         fa.subs = d_subs.p;
         fa.work = work.p;
         fa.err_key = err.p;
-        if (factor_smem_bytes(lmaxm[h]) > 200 * 1024) {
-          const size_t sz = static_cast<size_t>(nt) * 2 * lmaxm[h] * 16;
+        const int nsmall = lbig[h] - lstart[h], nbig = lstart[h + 1] - lbig[h];
+        if (nsmall > 0) {
+          fa.tasks = d_tasks.p + lstart[h];
+          fa.ntasks = nsmall;
+          if (factor_smem_bytes(lmaxm[h]) > 200 * 1024) {
+            const size_t sz = static_cast<size_t>(nsmall) * 2 * lmaxm[h] * 16;
+            if (scratch.n < sz) scratch.alloc(sz);
+            fa.scratch = scratch.p;
+          }
+          launch_factor_level(fa, lmaxm[h], stream);
+        }
+        if (nbig > 0) {
+          fa.tasks = d_tasks.p + lbig[h];
+          fa.ntasks = nbig;
+          const size_t sz = static_cast<size_t>(nbig) * kFactorCluster * 2 * lmaxm_big[h] * 16;
           if (scratch.n < sz) scratch.alloc(sz);
           fa.scratch = scratch.p;
+          launch_factor_level_cluster(fa, lmaxm_big[h], stream);
         }
-        launch_factor_level(fa, lmaxm[h], stream);
       }
       HS_CUDA(cudaStreamSynchronize(stream));
       s0 = s1;

@@ -11,6 +11,9 @@
 //   residual / spmv / dots  global operator and Krylov vector kernels
 #include "hs_kernels.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -75,23 +78,37 @@ __device__ __forceinline__ long long band_base_dev(int t, int kb) {  // hs_symbo
   return s * 256;
 }
 
+// One front per CTA (NC = 1), or per thread-block cluster of NC CTAs for large fronts (m up to
+// several thousand in 3D): element loops, trailing-update tiles, the rows of M and W are split
+// over the cluster; the panel LDL^T of each block column runs on rank 0 into its scratch, which
+// the other CTAs read after a cluster barrier. Every phase boundary is a cluster barrier
+// (release/acquire at cluster scope, which also orders the global-memory front).
+template <int NC>
 __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, int use_smem,
                                                               long long scratch_stride) {
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
-  const FactorTask task = a.tasks[blockIdx.x];
+  const int rank = NC == 1 ? 0 : static_cast<int>(blockIdx.x % NC);
+  const int gtid = rank * kThreads + tid;   // thread index within the front's CTAs
+  constexpr int GT = NC * kThreads;        // threads per front
+  auto sync_front = [&]() {
+    if constexpr (NC == 1)
+      __syncthreads();
+    else
+      cg::this_cluster().sync();
+  };
+  const FactorTask task = a.tasks[blockIdx.x / NC];
   const DevSub& S = a.subs[task.sub];
   const DevClass& C = a.cls[S.cls];
   const DevFront f = C.fronts[task.front];
   const int m = f.m, k = f.k;
   double2* F = a.work + task.fbase + f.f_off;
   const long long mm = static_cast<long long>(m) * m;
-  for (long long idx = tid; idx < mm; idx += kThreads) F[idx] = czero();
-  __syncthreads();
+  for (long long idx = gtid; idx < mm; idx += GT) F[idx] = czero();
+  sync_front();
   // original entries of the separator rows, lower triangle (src/direct.cpp:219-237)
-  for (int q = tid; q < f.orig_cnt; q += kThreads)
-    cacc(&F[C.orig_fpos[f.orig_off + q]], S.val[C.orig_eidx[f.orig_off + q]]);
-  __syncthreads();
+  for (int q = gtid; q < f.orig_cnt; q += GT) cacc(&F[C.orig_fpos[f.orig_off + q]], S.val[C.orig_eidx[f.orig_off + q]]);
+  sync_front();
   // extend-add of the children's Schur complements (src/direct.cpp:239-265)
 #pragma unroll 1
   for (int q = 0; q < 2; ++q) {
@@ -101,19 +118,22 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
     const double2* Fc = a.work + task.fbase + cf.f_off;
     const int cb = cf.m - cf.k;
     const int* cmap = C.child_map + (q ? f.cmap1 : f.cmap0);
-    for (int idx = tid; idx < cb * cb; idx += kThreads) {
+    for (int idx = gtid; idx < cb * cb; idx += GT) {
       const int i = idx % cb, j = idx / cb;
       if (i >= j)
         cacc(&F[static_cast<long long>(cmap[j]) * m + cmap[i]],
              Fc[static_cast<long long>(cf.k + j) * cf.m + cf.k + i]);
     }
-    __syncthreads();
+    sync_front();  // child by child: two children may add into the same entry
   }
-  double2* Ps = use_smem ? sm : a.scratch + blockIdx.x * scratch_stride;
+  // panel buffers: rank 0's (shared by the cluster through global memory); own scratch for rows
+  double2* Ps = use_smem ? sm : a.scratch + (blockIdx.x - rank) * scratch_stride;
   double2* Ws = Ps + static_cast<long long>(m) * kNB;
+  double2* own = use_smem ? sm : a.scratch + blockIdx.x * scratch_stride;
 #pragma unroll 1
   for (int p0 = 0; p0 < k; p0 += kNB) {
     const int p1 = min(p0 + kNB, k), nbw = p1 - p0, rows = m - p0, rows2 = m - p1;
+    if (rank == 0) {  // panel LDL^T on rank 0 (CTA-local barriers)
     for (int idx = tid; idx < nbw * rows; idx += kThreads) {
       const int c = idx / rows, i = idx % rows;
       Ps[idx] = F[static_cast<long long>(p0 + c) * m + p0 + i];
@@ -147,13 +167,14 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
       const int c = idx / rows, i = idx % rows;
       F[static_cast<long long>(p0 + c) * m + p0 + i] = Ps[idx];
     }
-    __syncthreads();
-    // trailing lower update F[p1:, p1:] -= L W^T in 64x64 tiles, 4x4 per thread
+    }  // rank 0
+    sync_front();
+    // trailing lower update F[p1:, p1:] -= L W^T in 64x64 tiles (split over the cluster), 4x4 per thread
     if (rows2 > 0) {
       const int nt = (rows2 + 63) / 64;
       const int ty = tid / 16, tx = tid % 16;
 #pragma unroll 1
-      for (int tp = 0; tp < nt * (nt + 1) / 2; ++tp) {
+      for (int tp = rank; tp < nt * (nt + 1) / 2; tp += NC) {
         int ti = 0;
         while ((ti + 1) * (ti + 2) / 2 <= tp) ++ti;
         const int tc = tp - ti * (ti + 1) / 2;
@@ -191,28 +212,28 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
             }
       }
     }
-    __syncthreads();
+    sync_front();
   }
   // D^-1, then the partitioned inverse of the eliminated columns: M = L11^-1 (unit lower)
   // and W = L21 M replace L11 / L21, so each front's solve is a dense product (hs_solve.cu).
-  for (int j = tid; j < k; j += kThreads) S.dinv[f.sep_off + j] = crecip(F[static_cast<long long>(j) * m + j]);
-  double2* rowbuf = Ps;  // >= 32 m entries of scratch (smem or global)
-  __syncthreads();
+  for (int j = gtid; j < k; j += GT) S.dinv[f.sep_off + j] = crecip(F[static_cast<long long>(j) * m + j]);
+  double2* rowbuf = own;  // >= 32 m entries of this CTA's scratch (smem or global)
+  sync_front();
 #pragma unroll 1
   for (int i = 1; i < k; ++i) {  // M row i: M[i][j] = -sum_{l=j}^{i-1} L[i][l] M[l][j]
     for (int l = tid; l < i; l += kThreads) rowbuf[l] = F[static_cast<long long>(l) * m + i];
-    __syncthreads();
-    for (int j = tid; j < i; j += kThreads) {
+    sync_front();  // every CTA holds row i of L before any CTA overwrites it with row i of M
+    for (int j = gtid; j < i; j += GT) {
       double2 acc = rowbuf[j];
       for (int l = j + 1; l < i; ++l) cfma(acc, rowbuf[l], F[static_cast<long long>(j) * m + l]);
       F[static_cast<long long>(j) * m + i] = make_double2(-acc.x, -acc.y);
     }
-    __syncthreads();
+    sync_front();
   }
   {  // W rows: one warp per row, the row of L21 staged in a per-warp buffer
     const int warp = tid >> 5, lane = tid & 31;
     double2* wb = rowbuf + static_cast<long long>(warp) * k;
-    for (int r = k + warp; r < m; r += kWarps) {
+    for (int r = k + rank * kWarps + warp; r < m; r += NC * kWarps) {
       for (int l = lane; l < k; l += 32) wb[l] = F[static_cast<long long>(l) * m + r];
       __syncwarp();
       for (int j = lane; j < k; j += 32) {
@@ -223,7 +244,7 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
       __syncwarp();
     }
   }
-  __syncthreads();
+  sync_front();
   // [M; W] in the solve layout (hs_symbolic.hpp front_block_elems): padded rows [sep | bnd],
   // 8x8 complex blocks row-major, bands of 4 block rows holding column blocks [0, min(kb, 4t+4)).
   {
@@ -243,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) factor_level_kernel(FactorArgs a, in
       const int rbs = min(4, nrb - 4 * t), ncb = min(kb, 4 * t + 4);
       double2* B = P + band_base_dev(t, kb);
       const int tot = ncb * rbs * 64;
-      for (int idx = tid; idx < tot; idx += kThreads) {
+      for (int idx = gtid; idx < tot; idx += GT) {
         const int blk = idx >> 6, e = idx & 63, cb = blk / rbs, i = blk % rbs;
         B[idx] = val(8 * (4 * t + i) + (e >> 3), 8 * cb + (e & 7));
       }
@@ -661,13 +682,31 @@ size_t factor_smem_bytes(int max_m) { return static_cast<size_t>(2) * max_m * kN
 void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    HS_CUDA(cudaFuncSetAttribute(factor_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HS_CUDA(cudaFuncSetAttribute(factor_level_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     configured = true;
   }
   const size_t need = factor_smem_bytes(max_m);
   const bool use_smem = need <= 200 * 1024;
-  factor_level_kernel<<<a.ntasks, kThreads, use_smem ? need : 0, s>>>(
+  factor_level_kernel<1><<<a.ntasks, kThreads, use_smem ? need : 0, s>>>(
       a, use_smem ? 1 : 0, static_cast<long long>(2) * max_m * kNB);
+  after_launch();
+}
+
+// Large fronts: one thread-block cluster of kFactorCluster CTAs per front, scratch (global) per CTA.
+void launch_factor_level_cluster(const FactorArgs& a, int max_m, cudaStream_t s) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(a.ntasks) * kFactorCluster);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kFactorCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, factor_level_kernel<kFactorCluster>, a, 0, static_cast<long long>(2) * max_m * kNB));
   after_launch();
 }
 

@@ -43,6 +43,11 @@ struct FactorArgs {
 // Assembly + extend-add + partial LDL^T of every front at one tree height
 // (src/direct.cpp:55-87, 181-281).
 void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s);
+// The same with one thread-block cluster of kFactorCluster CTAs per front (large fronts); scratch
+// must hold kFactorCluster * ntasks * 2 * max_m * kNB entries.
+constexpr int kFactorCluster = 8;
+constexpr int kFactorBigM = 640;  // fronts with m >= this go to the cluster path
+void launch_factor_level_cluster(const FactorArgs& a, int max_m, cudaStream_t s);
 size_t factor_smem_bytes(int max_m);
 
 struct SweepArgs {

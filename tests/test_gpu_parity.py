@@ -157,6 +157,9 @@ def test_c1_config_against_oracle(hs):
         uo, ro = so.ddm_solve(b[r].copy(), 1, True)
         assert rel(U[r], uo) <= TOL
         assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
+    # large fronts are factorized by CTA clusters: an independent factorization is bitwise equal
+    s2 = hs.DdmSolver(hs.ProblemSetup(3, [n] * 3, [2, 2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
+    assert np.array_equal(s2.ddm_solve(b, 1), U)
     assert [reps[0].local_solves, reps[0].skipped_zero_solves] == [48, 16]  # SURVEY §6.2 (C1 centre)
 
 
@@ -262,3 +265,6 @@ def test_3d_moderate_against_oracle(hs):
         uo, ro = so.ddm_solve(b[r].copy(), 1, True)
         assert rel(U[r], uo) <= TOL
         assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
+    # large fronts are factorized by CTA clusters: an independent factorization is bitwise equal
+    s2 = hs.DdmSolver(hs.ProblemSetup(3, [n] * 3, [2, 2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
+    assert np.array_equal(s2.ddm_solve(b, 1), U)
