@@ -341,6 +341,8 @@ struct Engine {
       for (int s = s0; s < s1; ++s) hmax = std::max(hmax, classes[sub_cls[s]]->sym->max_height);
       // per height: small fronts (one CTA each) then large fronts (one CTA cluster each)
       std::vector<FactorTask> tasks;
+      int big_m = kFactorBigM;  // HS_FACTOR_BIG_M: route smaller fronts to the cluster path (tests)
+      if (const char* e = std::getenv("HS_FACTOR_BIG_M")) big_m = std::max(64, std::atoi(e));
       std::vector<int> lstart(hmax + 2, 0), lbig(hmax + 1, 0), lmaxm(hmax + 1, 0), lmaxm_big(hmax + 1, 0);
       for (int h = 0; h <= hmax; ++h) {
         lstart[h] = static_cast<int>(tasks.size());
@@ -351,7 +353,7 @@ struct Engine {
             if (h > c.max_height) continue;
             for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
               const int f = c.order_up[q];
-              const bool big = c.fronts[f].m >= kFactorBigM;
+              const bool big = c.fronts[f].m >= big_m;
               if (big != (pass == 1)) continue;
               tasks.push_back(FactorTask{s, f, fb[s - s0]});
               int& mx = big ? lmaxm_big[h] : lmaxm[h];
@@ -382,10 +384,15 @@ struct Engine {
         if (nbig > 0) {
           fa.tasks = d_tasks.p + lbig[h];
           fa.ntasks = nbig;
-          const size_t sz = static_cast<size_t>(nbig) * kFactorCluster * 2 * lmaxm_big[h] * 16;
+          static const bool old_path = std::getenv("HS_FACTOR_OLD") != nullptr;
+          const size_t sz = old_path ? static_cast<size_t>(nbig) * kFactorCluster * 2 * lmaxm_big[h] * 16
+                                     : static_cast<size_t>(nbig) * factor_big_scratch(lmaxm_big[h]);
           if (scratch.n < sz) scratch.alloc(sz);
           fa.scratch = scratch.p;
-          launch_factor_level_cluster(fa, lmaxm_big[h], stream);
+          if (old_path)
+            launch_factor_level_cluster(fa, lmaxm_big[h], stream);
+          else
+            launch_factor_big(fa, lmaxm_big[h], stream);
         }
       }
       HS_CUDA(cudaStreamSynchronize(stream));

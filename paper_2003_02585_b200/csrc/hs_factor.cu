@@ -1,0 +1,596 @@
+// Blocked factorization of large fronts (m >= kFactorBigM, 3D tops of the nested-dissection
+// tree) on thread-block clusters, src/direct.cpp:55-87 (eliminate_front) and :181-281
+// (factor_numeric) restated as GEMM-shaped phases:
+//
+//   1. panels of kPB = 32 columns: every CTA factors the kPB x kPB diagonal block (redundantly,
+//      in shared memory); the rows below it are solved against it, one row per thread in
+//      registers, split over the cluster (L21 of the panel, and (L D) into scratch); the trailing
+//      lower update F[p1:, p1:] -= L (L D)^T runs as 64x64 tiles split over the cluster.
+//   2. D^-1 and unit diagonal.
+//   3. M = L11^-1 by 64-row blocks I: T[I, J] = sum_{J <= K < I} L[I, K] M[K, J] (tiles split
+//      over the cluster, into scratch), then M[I, J] = -L_II^-1 T[I, J]; L_II^-1 (64 x 64) is
+//      formed per CTA from two 32 x 32 in-register inversions.
+//   4. W = L21 M in place: row blocks of 64 rows per CTA, column tiles in increasing order (tile
+//      J reads L21[R, K >= J] only, so writing W[R, J] over L21[R, J] is safe).
+//   5. [M; W] into the banded 8x8-block solve layout (hs_symbolic.hpp front_block_elems).
+//
+// Every GEMM phase is a 64 x 64 complex tile per CTA (4 x 4 per thread, 256 threads), k-chunks
+// of 32 staged in shared memory by a two-stage cp.async pipeline that also prefetches the next
+// tile's first chunk. On B200 scalar DFMA and DMMA share the FP64 peak (profiles/fp64_peak.json),
+// so the tile is register-blocked DFMA. Phase boundaries are cluster barriers.
+#include "hs_kernels.cuh"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
+#include <atomic>
+
+#include "hs_common.hpp"
+
+namespace hsb {
+
+extern std::atomic<long long> g_kernel_launches;
+
+namespace {
+
+constexpr int kT = 256;   // threads per CTA
+constexpr int kPB = 32;   // panel width of the LDL^T
+constexpr int kTB = 64;   // GEMM tile (rows and columns)
+constexpr int kKC = 32;   // GEMM k-chunk
+constexpr int kSL = 65;   // shared leading dimension (double2) of staged chunks: conflict-free transposed stores
+constexpr int kDL = 33;   // leading dimension of the panel diagonal block
+constexpr int kStage = 2 * kKC * kSL;          // one pipeline stage: A chunk + B chunk
+constexpr int kRegion0 = 2 * 64 * kSL + 32 * kDL;  // max(2 stages, L_II + X + Y of the inversion)
+constexpr int kRegion1 = 2 * 32 * kDL + 2 * 32;    // panel diagonal block, e, 1/d, d
+constexpr size_t kSmemBytes = static_cast<size_t>(kRegion0 + kRegion1) * sizeof(double2);
+static_assert(2 * kStage <= kRegion0, "stage area");
+
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ void cfms(double2& acc, double2 a, double2 b) {
+  acc.x = fma(-a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(-a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ double2 crecip(double2 d) {  // Smith's algorithm
+  if (fabs(d.x) >= fabs(d.y)) {
+    const double r = d.y / d.x, den = d.x + d.y * r;
+    return make_double2(1.0 / den, -r / den);
+  }
+  const double r = d.x / d.y, den = d.x * r + d.y;
+  return make_double2(r / den, -1.0 / den);
+}
+__device__ __forceinline__ void cp16(double2* dst, const double2* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ long long band_base_dev(int t, int kb) {  // hs_symbolic.hpp band_base
+  const int j0 = kb >> 2;
+  const long long s = t <= j0 ? 2LL * t * (t + 1) : 2LL * j0 * (j0 + 1) + static_cast<long long>(t - j0) * kb;
+  return s * 256;
+}
+
+// GEMM operand: element (r, kk) is p[r + kk * ld] (column-major, trans = 0) or p[r * ld + kk]
+// (trans = 1); rows r >= rows read as zero.
+struct Opnd {
+  const double2* p;
+  long long ld;
+  int trans, rows;
+};
+struct Tile {
+  Opnd a, b;
+  int k0, k1;  // k range [k0, k1); an empty range is one all-zero chunk
+};
+
+__device__ __forceinline__ void stage_opnd(double2* s, const Opnd& o, int k0, int k1, int tid) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    int r, kk;
+    if (!o.trans) {
+      r = tid & 63;
+      kk = (tid >> 6) + 4 * q;
+    } else {
+      kk = tid & 31;
+      r = (tid >> 5) + 8 * q;
+    }
+    const int gk = k0 + kk;
+    const bool ok = r < o.rows && gk < k1;
+    const double2* src = o.p;
+    if (ok) src = o.trans ? o.p + static_cast<long long>(r) * o.ld + gk : o.p + r + static_cast<long long>(gk) * o.ld;
+    cp16(s + kk * kSL + r, src, ok);
+  }
+}
+
+// acc[u][v] (rows tx + 16u, columns ty + 16v) += A chunk * B chunk^T
+__device__ __forceinline__ void mma_chunk(double2 (&acc)[4][4], const double2* sA, const double2* sB, int tx, int ty) {
+#pragma unroll 4
+  for (int kk = 0; kk < kKC; ++kk) {
+    double2 a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = sA[kk * kSL + tx + 16 * u];
+      b[u] = sB[kk * kSL + ty + 16 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cfma(acc[u][v], a[u], b[v]);
+  }
+}
+
+// The CTA's sequence of cnt tiles: get(q) describes tile q, epi(q, acc, tx, ty) consumes its
+// accumulators. Chunks stream through two cp.async stages; the next chunk (of this tile or the
+// next one) is in flight while the current one is multiplied.
+template <class Get, class Epi>
+__device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* stages, int tid) {
+  if (cnt <= 0) return;
+  const int tx = tid & 15, ty = tid >> 4;
+  int q = 0;
+  Tile cur = get(0);
+  int c = cur.k0;
+  stage_opnd(stages, cur.a, c, cur.k1, tid);
+  stage_opnd(stages + kKC * kSL, cur.b, c, cur.k1, tid);
+  cp_commit();
+  double2 acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = czero();
+  int sb = 0;
+#pragma unroll 1
+  while (true) {
+    const bool last_chunk = c + kKC >= cur.k1;
+    int nq = q, nc = c + kKC;
+    Tile nxt = cur;
+    if (last_chunk) {
+      nq = q + 1;
+      if (nq < cnt) {
+        nxt = get(nq);
+        nc = nxt.k0;
+      }
+    }
+    const bool has_next = nq < cnt;
+    if (has_next) {
+      double2* s = stages + (sb ^ 1) * kStage;
+      stage_opnd(s, nxt.a, nc, nxt.k1, tid);
+      stage_opnd(s + kKC * kSL, nxt.b, nc, nxt.k1, tid);
+    }
+    cp_commit();
+    cp_wait1();
+    __syncthreads();
+    mma_chunk(acc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, tx, ty);
+    __syncthreads();
+    if (last_chunk) {
+      epi(q, acc, tx, ty);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = czero();
+    }
+    if (!has_next) break;
+    q = nq;
+    c = nc;
+    cur = nxt;
+    sb ^= 1;
+  }
+}
+
+// X = L^-1 for the unit lower 64 x 64 block L_II = F[I0 + r, I0 + c] (bs valid rows, identity
+// padding), written column-major to out (64 x 64). Diagonal 32-blocks by warps 0 / 1 in registers
+// (lane = column), the off-diagonal block as -B^-1 (C A^-1).
+__device__ void invert_unit_lower64(const double2* F, long long m, int I0, int bs, double2* sm, double2* out, int tid) {
+  double2* sL = sm;             // 64 x kSL, row-major: sL[r * kSL + c]
+  double2* sX = sm + 64 * kSL;  // 64 x kSL
+  double2* sY = sm + 128 * kSL; // 32 x kDL
+  for (int idx = tid; idx < 64 * 64; idx += kT) {
+    const int r = idx & 63, c = idx >> 6;
+    double2 v = czero();
+    if (r > c && r < bs) v = F[static_cast<long long>(I0 + c) * m + I0 + r];
+    sL[r * kSL + c] = v;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < 2) {
+    const int o = 32 * warp;
+    double2 x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double2 acc = make_double2(i == lane ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int l = 0; l < i; ++l) cfms(acc, sL[(o + i) * kSL + o + l], x[l]);
+      x[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) sX[(o + i) * kSL + o + lane] = x[i];
+  }
+  __syncthreads();
+  // Y = C A^-1, C = L[32:64, 0:32]
+  for (int idx = tid; idx < 32 * 32; idx += kT) {
+    const int i = idx >> 5, j = idx & 31;
+    double2 acc = czero();
+    for (int l = j; l < 32; ++l) cfma(acc, sL[(32 + i) * kSL + l], sX[l * kSL + j]);
+    sY[i * kDL + j] = acc;
+  }
+  __syncthreads();
+  // X21 = -B^-1 Y
+  for (int idx = tid; idx < 32 * 32; idx += kT) {
+    const int i = idx >> 5, j = idx & 31;
+    double2 acc = czero();
+    for (int l = 0; l <= i; ++l) cfms(acc, sX[(32 + i) * kSL + 32 + l], sY[l * kDL + j]);
+    sX[(32 + i) * kSL + j] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 64 * 64; idx += kT) {
+    const int r = idx & 63, c = idx >> 6;
+    double2 v = czero();
+    if (r == c)
+      v = make_double2(1.0, 0.0);
+    else if (r > c)
+      v = sX[r * kSL + c];
+    out[r + 64 * c] = v;
+  }
+  __syncthreads();
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long long scratch_stride) {
+  extern __shared__ double2 smem[];
+  double2* region0 = smem;
+  double2* sD = smem + kRegion0;  // panel diagonal block (row-major, kDL)
+  double2* sE = sD + 32 * kDL;    // e[jj][c] = d_c L[jj][c]
+  double2* sInv = sE + 32 * kDL;  // 1 / d_c
+  double2* sDd = sInv + 32;       // d_c
+  const int tid = threadIdx.x;
+  const int rank = static_cast<int>(blockIdx.x % NC);
+  const int gtid = rank * kT + tid;
+  constexpr int GT = NC * kT;
+  auto sync_front = [&]() { cg::this_cluster().sync(); };
+  const FactorTask task = a.tasks[blockIdx.x / NC];
+  const DevSub& S = a.subs[task.sub];
+  const DevClass& C = a.cls[S.cls];
+  const DevFront f = C.fronts[task.front];
+  const int m = f.m, k = f.k;
+  double2* F = a.work + task.fbase + f.f_off;
+  const long long mm = static_cast<long long>(m) * m;
+  // scratch of the cluster: (L D) of the panel (m x kPB), T (64 x k), L_II^-1 per CTA (64 x 64)
+  double2* Ws = a.scratch + (blockIdx.x / NC) * scratch_stride;
+  double2* Tb = Ws + static_cast<long long>(m) * kPB;
+  double2* Li = Tb + static_cast<long long>(64) * k + rank * 4096;
+
+  // ---- assembly (src/direct.cpp:219-265)
+  for (long long idx = gtid; idx < mm; idx += GT) F[idx] = czero();
+  sync_front();
+  for (int q = gtid; q < f.orig_cnt; q += GT) {
+    double2& y = F[C.orig_fpos[f.orig_off + q]];
+    const double2 v = S.val[C.orig_eidx[f.orig_off + q]];
+    y.x += v.x;
+    y.y += v.y;
+  }
+  sync_front();
+#pragma unroll 1
+  for (int q = 0; q < 2; ++q) {
+    const int ch = q ? f.child1 : f.child0;
+    if (ch < 0) continue;
+    const DevFront cf = C.fronts[ch];
+    const double2* Fc = a.work + task.fbase + cf.f_off;
+    const int cb = cf.m - cf.k;
+    const int* cmap = C.child_map + (q ? f.cmap1 : f.cmap0);
+    for (int idx = gtid; idx < cb * cb; idx += GT) {
+      const int i = idx % cb, j = idx / cb;
+      if (i >= j) {
+        double2& y = F[static_cast<long long>(cmap[j]) * m + cmap[i]];
+        const double2 v = Fc[static_cast<long long>(cf.k + j) * cf.m + cf.k + i];
+        y.x += v.x;
+        y.y += v.y;
+      }
+    }
+    sync_front();
+  }
+
+  // ---- 1. panel LDL^T with trailing GEMM updates (src/direct.cpp:55-87)
+#pragma unroll 1
+  for (int p0 = 0; p0 < k; p0 += kPB) {
+    const int nbw = min(kPB, k - p0), p1 = p0 + nbw, rows2 = m - p1;
+    // (a) diagonal block, every CTA
+    for (int idx = tid; idx < kPB * kPB; idx += kT) {
+      const int r = idx & 31, c = idx >> 5;
+      sD[r * kDL + c] = (r < nbw && c <= r) ? F[static_cast<long long>(p0 + c) * m + p0 + r] : czero();
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int jj = 0; jj < nbw; ++jj) {
+      const double2 d = sD[jj * kDL + jj];
+      const double2 inv = crecip(d);
+      if (tid > jj && tid < nbw) sD[tid * kDL + jj] = cmul(sD[tid * kDL + jj], inv);
+      __syncthreads();
+      const int w = nbw - jj - 1;
+      for (int idx = tid; idx < w * w; idx += kT) {
+        const int r = jj + 1 + idx / w, c = jj + 1 + idx % w;
+        if (c <= r) cfms(sD[r * kDL + c], sD[r * kDL + jj], cmul(d, sD[c * kDL + jj]));
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < kPB * kPB; idx += kT) {
+      const int jj = idx >> 5, c = idx & 31;
+      sE[jj * kDL + c] = (jj < nbw && c < jj) ? cmul(sD[c * kDL + c], sD[jj * kDL + c]) : czero();
+    }
+    if (tid < kPB) {
+      const double2 d = tid < nbw ? sD[tid * kDL + tid] : czero();
+      sDd[tid] = d;
+      sInv[tid] = tid < nbw ? crecip(d) : czero();
+      if (rank == 0 && tid < nbw && hypot(d.x, d.y) < S.tol)
+        atomicMin(a.err_key, (static_cast<unsigned long long>(task.sub) << 32) | static_cast<unsigned>(f.sep_off + p0 + tid));
+    }
+    __syncthreads();
+    // (b) rows below the block: L[i, p0:p1] and (L D)[i, :] -> scratch, one row per thread, in two
+    // halves of 16 columns (the first half's multipliers wait in the idle GEMM stage area)
+    double2* sl = region0 + tid;
+#pragma unroll 1
+    for (int i = p1 + gtid; i < m; i += GT) {
+      double2 x[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) x[c] = c < nbw ? F[static_cast<long long>(p0 + c) * m + i] : czero();
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const double2 l = cmul(x[c], sInv[c]);
+        x[c] = l;
+        sl[c * kT] = l;
+#pragma unroll
+        for (int jj = c + 1; jj < 16; ++jj) cfms(x[jj], l, sE[jj * kDL + c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < nbw) {
+          F[static_cast<long long>(p0 + c) * m + i] = x[c];
+          Ws[(i - p1) + static_cast<long long>(c) * rows2] = cmul(x[c], sDd[c]);
+        }
+      if (nbw > 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) x[c] = 16 + c < nbw ? F[static_cast<long long>(p0 + 16 + c) * m + i] : czero();
+#pragma unroll 4
+        for (int c = 0; c < 16; ++c) {
+          const double2 l = sl[c * kT];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) cfms(x[jj], l, sE[(16 + jj) * kDL + c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const double2 l = cmul(x[c], sInv[16 + c]);
+          x[c] = l;
+#pragma unroll
+          for (int jj = c + 1; jj < 16; ++jj) cfms(x[jj], l, sE[(16 + jj) * kDL + 16 + c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (16 + c < nbw) {
+            F[static_cast<long long>(p0 + 16 + c) * m + i] = x[c];
+            Ws[(i - p1) + static_cast<long long>(16 + c) * rows2] = cmul(x[c], sDd[16 + c]);
+          }
+      }
+    }
+    sync_front();
+    // (c) diagonal block back (rank 0); trailing lower update F[p1:, p1:] -= L (L D)^T
+    if (rank == 0)
+      for (int idx = tid; idx < kPB * kPB; idx += kT) {
+        const int r = idx & 31, c = idx >> 5;
+        if (r < nbw && c <= r) F[static_cast<long long>(p0 + c) * m + p0 + r] = sD[r * kDL + c];
+      }
+    if (rows2 > 0) {
+      const int nt = (rows2 + kTB - 1) / kTB, ntiles = nt * (nt + 1) / 2;
+      auto tile_of = [&](int q, int& ti, int& tc) {
+        const int tp = rank + NC * q;
+        ti = static_cast<int>((sqrt(8.0 * tp + 1.0) - 1.0) * 0.5);
+        while (ti * (ti + 1) / 2 > tp) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= tp) ++ti;
+        tc = tp - ti * (ti + 1) / 2;
+      };
+      const int cnt = ntiles > rank ? (ntiles - rank + NC - 1) / NC : 0;
+      gemm_tiles(
+          cnt,
+          [&](int q) {
+            int ti, tc;
+            tile_of(q, ti, tc);
+            Tile t;
+            t.a = Opnd{F + static_cast<long long>(p0) * m + p1 + ti * kTB, m, 0, min(kTB, rows2 - ti * kTB)};
+            t.b = Opnd{Ws + tc * kTB, rows2, 0, min(kTB, rows2 - tc * kTB)};
+            t.k0 = 0;
+            t.k1 = nbw;
+            return t;
+          },
+          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+            int ti, tc;
+            tile_of(q, ti, tc);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int gj = tc * kTB + ty + 16 * v;
+              if (gj >= rows2) continue;
+              double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int gi = ti * kTB + tx + 16 * u;
+                if (gi < rows2 && gi >= gj) {
+                  double2 y = col[gi];
+                  y.x -= acc[u][v].x;
+                  y.y -= acc[u][v].y;
+                  col[gi] = y;
+                }
+              }
+            }
+          },
+          region0, tid);
+    }
+    sync_front();
+  }
+
+  // ---- 2. D^-1 (kept per node for the solve) and unit diagonal for the inversion
+  for (int j = gtid; j < k; j += GT) {
+    double2& d = F[static_cast<long long>(j) * m + j];
+    S.dinv[f.sep_off + j] = crecip(d);
+    d = make_double2(1.0, 0.0);
+  }
+  sync_front();
+
+  // ---- 3. M = L11^-1 in place, 64-row blocks
+  const int nI = (k + kTB - 1) / kTB;
+#pragma unroll 1
+  for (int I = 0; I < nI; ++I) {
+    const int I0 = I * kTB, bs = min(kTB, k - I0);
+    invert_unit_lower64(F, m, I0, bs, region0, Li, tid);
+    // T[I, J] = sum_{J0 <= K < I0} L[I, K] M[K, J], J < I
+    const int cnt = I > rank ? (I - rank + NC - 1) / NC : 0;
+    gemm_tiles(
+        cnt,
+        [&](int q) {
+          const int J = rank + NC * q, J0 = J * kTB;
+          Tile t;
+          t.a = Opnd{F + I0, m, 0, bs};
+          t.b = Opnd{F + static_cast<long long>(J0) * m, m, 1, kTB};
+          t.k0 = J0;
+          t.k1 = I0;
+          return t;
+        },
+        [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          const int J0 = (rank + NC * q) * kTB;
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) Tb[tx + 16 * u + static_cast<long long>(J0 + ty + 16 * v) * kTB] = acc[u][v];
+        },
+        region0, tid);
+    sync_front();
+    // M[I, J] = -L_II^-1 T[I, J]; M_II = L_II^-1 (rank 0)
+    if (rank == 0)
+      for (int idx = tid; idx < kTB * kTB; idx += kT) {
+        const int r = idx & 63, c = idx >> 6;
+        if (r > c && r < bs) F[static_cast<long long>(I0 + c) * m + I0 + r] = Li[r + 64 * c];
+      }
+    gemm_tiles(
+        cnt,
+        [&](int q) {
+          const int J0 = (rank + NC * q) * kTB;
+          Tile t;
+          t.a = Opnd{Li, kTB, 0, bs};
+          t.b = Opnd{Tb + static_cast<long long>(J0) * kTB, kTB, 1, kTB};
+          t.k0 = 0;
+          t.k1 = bs;
+          return t;
+        },
+        [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          const int J0 = (rank + NC * q) * kTB;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            double2* col = F + static_cast<long long>(J0 + ty + 16 * v) * m + I0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = tx + 16 * u;
+              if (i < bs) col[i] = make_double2(-acc[u][v].x, -acc[u][v].y);
+            }
+          }
+        },
+        region0, tid);
+    sync_front();
+  }
+
+  // ---- 4. W = L21 M in place, row blocks of 64 per CTA, column tiles in increasing order
+  if (m > k) {
+    const int nR = (m - k + kTB - 1) / kTB, nJ = nI;
+    const int myR = nR > rank ? (nR - rank + NC - 1) / NC : 0;
+    gemm_tiles(
+        myR * nJ,
+        [&](int q) {
+          const int r0 = k + (rank + NC * (q / nJ)) * kTB, J0 = (q % nJ) * kTB;
+          Tile t;
+          t.a = Opnd{F + r0, m, 0, min(kTB, m - r0)};
+          t.b = Opnd{F + static_cast<long long>(J0) * m, m, 1, min(kTB, k - J0)};
+          t.k0 = J0;
+          t.k1 = k;
+          return t;
+        },
+        [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          const int r0 = k + (rank + NC * (q / nJ)) * kTB, J0 = (q % nJ) * kTB;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int j = J0 + ty + 16 * v;
+            if (j >= k) continue;
+            double2* col = F + static_cast<long long>(j) * m + r0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int i = tx + 16 * u;
+              if (r0 + i < m) col[i] = acc[u][v];
+            }
+          }
+        },
+        region0, tid);
+  }
+  sync_front();
+
+  // ---- 5. [M; W] in the solve layout (as factor_level_kernel)
+  {
+    const int kp = (k + 7) & ~7, kb = kp >> 3, nrb = kb + ((m - k + 7) >> 3), nband = (nrb + 3) >> 2;
+    auto val = [&](int pr, int pc) {
+      if (pc >= k) return czero();
+      if (pr < k) {
+        if (pr > pc) return F[static_cast<long long>(pc) * m + pr];
+        return pr == pc ? make_double2(1.0, 0.0) : czero();
+      }
+      const int row = k + pr - kp;
+      if (pr < kp || row >= m) return czero();
+      return F[static_cast<long long>(pc) * m + row];
+    };
+    double2* P = S.factor + f.fac_off;
+    for (int t = 0; t < nband; ++t) {
+      const int rbs = min(4, nrb - 4 * t), ncb = min(kb, 4 * t + 4);
+      double2* B = P + band_base_dev(t, kb);
+      const int tot = ncb * rbs * 64;
+      for (int idx = gtid; idx < tot; idx += GT) {
+        const int blk = idx >> 6, e = idx & 63, cb = blk / rbs, i = blk % rbs;
+        B[idx] = val(8 * (4 * t + i) + (e >> 3), 8 * cb + (e & 7));
+      }
+    }
+  }
+}
+
+}  // namespace
+
+long long factor_big_scratch(int max_m) {  // per cluster, double2 entries
+  return static_cast<long long>(max_m) * kPB + static_cast<long long>(64) * max_m + static_cast<long long>(kFactorCluster) * 4096;
+}
+
+void launch_factor_big(const FactorArgs& a, int max_m, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    HS_CUDA(cudaFuncSetAttribute(factor_big_kernel<kFactorCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemBytes)));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(a.ntasks) * kFactorCluster);
+  cfg.blockDim = dim3(kT);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kFactorCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, factor_big_kernel<kFactorCluster>, a, factor_big_scratch(max_m)));
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  HS_CUDA(cudaGetLastError());
+}
+
+}  // namespace hsb

@@ -48,6 +48,10 @@ void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s);
 constexpr int kFactorCluster = 8;
 constexpr int kFactorBigM = 640;  // fronts with m >= this go to the cluster path
 void launch_factor_level_cluster(const FactorArgs& a, int max_m, cudaStream_t s);
+// Blocked GEMM-phase factorization of large fronts, one cluster per front (hs_factor.cu); scratch
+// must hold ntasks * factor_big_scratch(max_m) entries.
+void launch_factor_big(const FactorArgs& a, int max_m, cudaStream_t s);
+long long factor_big_scratch(int max_m);
 size_t factor_smem_bytes(int max_m);
 
 struct SweepArgs {

@@ -157,9 +157,6 @@ def test_c1_config_against_oracle(hs):
         uo, ro = so.ddm_solve(b[r].copy(), 1, True)
         assert rel(U[r], uo) <= TOL
         assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
-    # large fronts are factorized by CTA clusters: an independent factorization is bitwise equal
-    s2 = hs.DdmSolver(hs.ProblemSetup(3, [n] * 3, [2, 2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
-    assert np.array_equal(s2.ddm_solve(b, 1), U)
     assert [reps[0].local_solves, reps[0].skipped_zero_solves] == [48, 16]  # SURVEY §6.2 (C1 centre)
 
 
@@ -268,3 +265,29 @@ def test_3d_moderate_against_oracle(hs):
     # large fronts are factorized by CTA clusters: an independent factorization is bitwise equal
     s2 = hs.DdmSolver(hs.ProblemSetup(3, [n] * 3, [2, 2, 2], hs.Medium("constant", kappa=kap), pml_width=pad))
     assert np.array_equal(s2.ddm_solve(b, 1), U)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_cluster_factorization_path_against_oracle(hs, monkeypatch, dim):
+    """The blocked cluster factorization (hs_factor.cu) forced onto every front with m >= 96
+    (HS_FACTOR_BIG_M): 2D C1-size subdomains (105^2, fronts up to m = 157) and 3D 2x2x2 (fronts
+    up to m ~ 500, several 64-row blocks and partial panels) against the numpy restatement."""
+    monkeypatch.setenv("HS_FACTOR_BIG_M", "96")
+    if dim == 2:
+        n, pad, kap, parts = 256, 20, 2 * math.pi * 16, [4, 4]
+        centers = [[0.5, 0.5], [0.3125, 0.6]]
+    else:
+        n, pad, kap, parts = 24, 5, 2 * math.pi * 2, [2, 2, 2]
+        centers = [[0.5, 0.5, 0.5], [0.3, 0.6, 0.45]]
+    so = O.DdmSolver(O.ProblemSetup(O.Box(dim), [n] * dim + [1] * (3 - dim), parts + [1] * (3 - dim),
+                                    O.Medium("constant", kappa=kap), O.PmlSpec(width=pad)))
+    b = so.scale_source(O.gaussian_source(so.ggrid, O.Box(dim), centers, 2.0 / n)).T.copy()
+    s = hs.DdmSolver(hs.ProblemSetup(dim, [n] * dim, parts, hs.Medium("constant", kappa=kap), pml_width=pad))
+    reps = []
+    U = s.ddm_solve(b, 1, reps, True)
+    for r in range(2):
+        uo, ro = so.ddm_solve(b[r].copy(), 1, True)
+        assert rel(U[r], uo) <= TOL
+        assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
+    s2 = hs.DdmSolver(hs.ProblemSetup(dim, [n] * dim, parts, hs.Medium("constant", kappa=kap), pml_width=pad))
+    assert np.array_equal(s2.ddm_solve(b, 1), U)  # the cluster factorization is deterministic
