@@ -232,14 +232,17 @@ def run_gpu(args, rank, world, local_rank):
     # e2e through the public API with pinned host buffers
     hb = torch.from_numpy(b.view(np.float64)).pin_memory()
     hu = torch.empty_like(hb).pin_memory()
-    s.ddm_solve_host_ptr(hb.data_ptr(), hu.data_ptr(), R, rounds, track)
+    for _ in range(max(args.warmup, 3)):
+        s.ddm_solve_host_ptr(hb.data_ptr(), hu.data_ptr(), R, rounds, track)
     if world > 1:
         dist.barrier()
-    n_e2e = max(1, min(args.steps, 5))
-    te = time.perf_counter()
+    n_e2e = max(3, min(args.steps, 10))
+    e2e_samples = []
     for _ in range(n_e2e):
+        te = time.perf_counter()
         s.ddm_solve_host_ptr(hb.data_ptr(), hu.data_ptr(), R, rounds, track)
-    e2e_ms = 1e3 * (time.perf_counter() - te) / n_e2e
+        e2e_samples.append(1e3 * (time.perf_counter() - te))
+    e2e_ms = sum(e2e_samples) / n_e2e
     t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -276,7 +279,8 @@ def run_gpu(args, rank, world, local_rank):
                      "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
                                   "peak_source": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)"}},
         "e2e": {"value": e2e_val, "unit": "RHS/s", "h2d_bytes_per_step": int(b.nbytes),
-                "d2h_bytes_per_step": int(b.nbytes)},
+                "d2h_bytes_per_step": int(b.nbytes), "steps": n_e2e,
+                "ms_per_step_samples": [round(x, 3) for x in e2e_samples]},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "factorization_seconds": s.factor_seconds(),

@@ -209,6 +209,38 @@ int hs_read_field(const char* path, int* dim, int lo[3], int hi[3], double h[3],
 int hs_ddm_schedule_info(hs_ddm* s, int rounds, int* macro_steps, int* max_width, int* sequential_steps,
                          int* buffers);
 
+/* ---- Subdomain-partitioned DdmSolver over several ranks ------------
+ * The reference runs every subdomain in one process (src/sweeper.cpp:263-283); here each rank
+ * (one process per GPU) factorizes and solves only the subdomains `owner` assigns to it. All
+ * ranks call hs_ddm_solve / hs_ddm_solve_device collectively with the same b. After each
+ * macro-step a rank sends the traces it deposited for other ranks' subdomains (mailbox slot +
+ * presence word, src/transfer.cpp:24-36) and the values of its subdomain solutions on nodes
+ * another rank accumulates (each global node is accumulated by one "home" rank in the
+ * reference's order, src/transfer.cpp:91-102), so u and the counters equal the single-process
+ * result bit for bit. The transport is the caller's: `exchange` moves one message to / from
+ * each listed peer (device buffers, offsets and counts in doubles, ordered on `stream`, e.g.
+ * NCCL send/recv pairs); `allreduce` sums `count` device doubles over all ranks (the home-node
+ * u slices, sweep norms, counters). Both return 0 on success. */
+typedef int (*hs_exchange_fn)(void* user, int npeers, const int* peers, const int64_t* send_off,
+                              const int64_t* send_count, const int64_t* recv_off, const int64_t* recv_count,
+                              const double* send_buf, double* recv_buf, void* stream);
+typedef int (*hs_allreduce_fn)(void* user, double* buf, int64_t count, void* stream);
+/* Balanced default ownership (host only): owner[nsub], subdomains in flattened id order
+ * (axis 0 fastest, src/geometry.cpp:105-122). */
+int hs_partition_owners(int dim, const int counts[3], int world, int* owner);
+/* Cost of an ownership (host only): macro-steps, sum over macro-steps of the busiest rank's task
+ * count, cross-rank faces, and traces[src * world + dst] routed per application. */
+int hs_partition_traffic(int dim, const int counts[3], int rounds, int world, const int* owner, int* macro_steps,
+                         int64_t* makespan_tasks, int64_t* cross_faces, int64_t* traces);
+/* owner may be NULL (hs_partition_owners). world == 1 is the plain hs_ddm_create. */
+int hs_ddm_create_partitioned(const hs_problem* setup, int device, int rank, int world, const int* owner,
+                              hs_exchange_fn exchange, hs_allreduce_fn allreduce, void* user, hs_ddm** out,
+                              int* pivot_sub, int64_t* pivot_index);
+/* Owned subdomains of this rank and the exchange volume (doubles sent per application, for the
+ * last batch width and rounds solved). */
+int hs_ddm_partition_info(const hs_ddm* s, int* rank, int* world, int* owned, int64_t* sent_doubles,
+                          int64_t* messages);
+
 /* ---- Pipeline cost model (include/helmsweep/pipeline.hpp, src/pipeline.cpp:20-111) ------ */
 /* PipelineScenario {dim, counts, n_rhs, n_iter, t0}: closed form average_time_per_rhs and the
  * discrete-event simulate_pipeline (one unit-capacity processor per subdomain, trace-routing

@@ -69,6 +69,11 @@ class GmresReportC(ctypes.Structure):
                 ("n_history", ctypes.c_int), ("history", ctypes.c_double * HS_MAX_GMRES_HISTORY)]
 
 
+# Callbacks of the partitioned solver (hs_exchange_fn / hs_allreduce_fn)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, c_int_p, c_i64_p, c_i64_p, c_i64_p,
+                               c_i64_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
 # Every symbol declared in include/helmsweep_b200.h, with its ctypes signature.
 SIGNATURES = {
     "hs_last_error": (ctypes.c_char_p, []),
@@ -119,6 +124,13 @@ SIGNATURES = {
                                 ctypes.c_int, ctypes.POINTER(GmresReportC)]),
     "hs_ddm_profile": (ctypes.c_int, [ctypes.c_void_p, c_dbl_p, c_i64_p, c_i64_p, c_dbl_p, c_dbl_p]),
     "hs_route_trace": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "hs_partition_owners": (ctypes.c_int, [ctypes.c_int, c_int_p, ctypes.c_int, c_int_p]),
+    "hs_partition_traffic": (ctypes.c_int, [ctypes.c_int, c_int_p, ctypes.c_int, ctypes.c_int, c_int_p, c_int_p,
+                                            c_i64_p, c_i64_p, c_i64_p]),
+    "hs_ddm_create_partitioned": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                 c_int_p, EXCHANGE_FN, ALLREDUCE_FN, ctypes.c_void_p,
+                                                 ctypes.POINTER(ctypes.c_void_p), c_int_p, c_i64_p]),
+    "hs_ddm_partition_info": (ctypes.c_int, [ctypes.c_void_p, c_int_p, c_int_p, c_int_p, c_i64_p, c_i64_p]),
 }
 
 _lib = None

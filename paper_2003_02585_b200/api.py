@@ -92,6 +92,9 @@ class Factorization:
         self._h = handle
         self._stats = stats
 
+    def _create(self, p, device, h, sub, piv):
+        return L.lib().hs_ddm_create(ctypes.byref(p), device, ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
+
     def __del__(self):
         if getattr(self, "_h", None):
             try:  # at interpreter shutdown the binding may already be torn down
@@ -251,7 +254,7 @@ class DdmSolver:
         p = setup.to_c()
         h = ctypes.c_void_p()
         sub, piv = ctypes.c_int(-1), ctypes.c_int64(-1)
-        rc = L.lib().hs_ddm_create(ctypes.byref(p), int(device), ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
+        rc = self._create(p, int(device), h, sub, piv)
         if rc:
             _raise(rc, piv.value, sub.value)
         self._h = h
@@ -261,6 +264,9 @@ class DdmSolver:
         self.dim, self.global_n, self.nsub = dim.value, n.value, ns.value
         self._factor_seconds = fs.value
         self.lo, self.hi = list(lo), list(hi)
+
+    def _create(self, p, device, h, sub, piv):
+        return L.lib().hs_ddm_create(ctypes.byref(p), device, ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -21,6 +21,7 @@
 
 #include "helmsweep_b200.h"
 #include "hs_kernels.cuh"
+#include "hs_partition.hpp"
 #include "hs_symbolic.hpp"
 
 namespace hsb {
@@ -276,6 +277,11 @@ struct Engine {
   }
 
   // Factorizes every subdomain (values[sub] = CSR values in the class's CSR structure).
+  // Subdomains this engine factorizes and solves (empty: all). A subdomain-partitioned solver
+  // keeps only its own factors; vectors keep a slot for every subdomain.
+  std::vector<char> owned;
+  bool owns(int s) const { return owned.empty() || owned[s]; }
+
   void factorize(const std::vector<const CVector*>& values) {
     const int nsub = static_cast<int>(sub_cls.size());
     fac_base.assign(nsub + 1, 0);
@@ -283,9 +289,9 @@ struct Engine {
     std::vector<long long> val_base(nsub + 1, 0);
     for (int s = 0; s < nsub; ++s) {
       const SymbolicClass& c = *classes[sub_cls[s]]->sym;
-      fac_base[s + 1] = fac_base[s] + c.fac_total;
+      fac_base[s + 1] = fac_base[s] + (owns(s) ? c.fac_total : 0);
       n_base[s + 1] = n_base[s] + c.n;
-      val_base[s + 1] = val_base[s] + static_cast<long long>(values[s]->size());
+      val_base[s + 1] = val_base[s] + (owns(s) ? static_cast<long long>(values[s]->size()) : 0);
     }
     factor.alloc(std::max<long long>(fac_base[nsub], 1));
     dinv.alloc(std::max<long long>(n_base[nsub], 1));
@@ -297,7 +303,8 @@ struct Engine {
       tol[s] = 1e-14 * scale;  // src/direct.cpp:191-193
     });
     for (int s = 0; s < nsub; ++s)
-      HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], values[s]->data(), values[s]->size() * sizeof(Complex),
+      if (owns(s))
+        HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], values[s]->data(), values[s]->size() * sizeof(Complex),
                               cudaMemcpyHostToDevice, stream));
     h_subs.resize(nsub);
     for (int s = 0; s < nsub; ++s) {
@@ -329,16 +336,17 @@ struct Engine {
       long long need = 0;
       int s1 = s0;
       while (s1 < nsub) {
-        const long long ft = classes[sub_cls[s1]]->sym->f_total;
+        const long long ft = owns(s1) ? classes[sub_cls[s1]]->sym->f_total : 0;
         if (s1 > s0 && need + ft > budget) break;
         need += ft;
         ++s1;
       }
       if (static_cast<long long>(work.n) < need) work.alloc(need);
       std::vector<long long> fb(s1 - s0 + 1, 0);
-      for (int s = s0; s < s1; ++s) fb[s - s0 + 1] = fb[s - s0] + classes[sub_cls[s]]->sym->f_total;
+      for (int s = s0; s < s1; ++s) fb[s - s0 + 1] = fb[s - s0] + (owns(s) ? classes[sub_cls[s]]->sym->f_total : 0);
       int hmax = 0;
-      for (int s = s0; s < s1; ++s) hmax = std::max(hmax, classes[sub_cls[s]]->sym->max_height);
+      for (int s = s0; s < s1; ++s)
+        if (owns(s)) hmax = std::max(hmax, classes[sub_cls[s]]->sym->max_height);
       // per height: small fronts (one CTA each) then large fronts (one CTA cluster each)
       std::vector<FactorTask> tasks;
       int big_m = kFactorBigM;  // HS_FACTOR_BIG_M: route smaller fronts to the cluster path (tests)
@@ -350,7 +358,7 @@ struct Engine {
           if (pass == 1) lbig[h] = static_cast<int>(tasks.size());
           for (int s = s0; s < s1; ++s) {
             const SymbolicClass& c = *classes[sub_cls[s]]->sym;
-            if (h > c.max_height) continue;
+            if (!owns(s) || h > c.max_height) continue;
             for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
               const int f = c.order_up[q];
               const bool big = c.fronts[f].m >= big_m;
@@ -928,6 +936,31 @@ struct DdmHandle {
   DBuf<std::int64_t> g_rp;
   DBuf<int> g_col;
   DBuf<double2> g_val;
+  // subdomain partition over ranks; world == 1: every subdomain is local
+  int rank = 0, world = 1;
+  std::vector<int> owner;                       // per subdomain
+  hs_exchange_fn xfn = nullptr;
+  hs_allreduce_fn arfn = nullptr;
+  void* cuser = nullptr;
+  std::vector<std::vector<int2>> msteps_own;    // per macro-step: this rank's tasks
+  // ghost x positions (n_base[sub] + elimination position) per (subdomain, home rank): values of
+  // the subdomain's solution that rank accumulates although another rank owns the subdomain
+  std::vector<std::vector<std::vector<long long>>> ghost;
+  std::vector<long long> ghost_off;             // [sub * world + rank] into d_gpos
+  DBuf<long long> d_gpos;
+  struct XPlan {
+    std::vector<int> peers;
+    std::vector<std::int64_t> soff, scnt, roff, rcnt;
+    int s0 = 0, ns = 0, r0 = 0, nr = 0;         // segments in d_xseg
+  };
+  std::vector<XPlan> xplan;
+  DBuf<XSeg> d_xseg;
+  DBuf<double> xsend, xrecv, dtmp;
+  DBuf<double2> ufull;
+  long long x_sent = 0, x_msgs = 0;
+  bool partitioned() const { return world > 1; }
+  void build_xplan();
+  void comm_allreduce(double* buf, long long count);
 
   ~DdmHandle() {
     for (auto e : ev) cudaEventDestroy(e);
@@ -937,7 +970,7 @@ struct DdmHandle {
     if (gfact) hs_factor_destroy(gfact);
   }
 
-  void build(const hs_problem& P, int device);
+  void build(const hs_problem& P, int device, int rank_ = 0, int world_ = 1, const int* owner_ = nullptr);
   void ensure_state(int r, int nrounds);
   void build_schedule();
   void build_items();
@@ -1000,7 +1033,7 @@ Medium medium_from(const hs_problem& P) {
 }  // namespace
 
 // DdmSolver ctor + build_subdomain_states (src/sweeper.cpp:75-157).
-void DdmHandle::build(const hs_problem& P, int device) {
+void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, const int* owner_) {
   dim = P.dim;
   if (dim != 2 && dim != 3) config_error("Box: dim must be 2 or 3");
   interior.dim = dim;
@@ -1136,6 +1169,20 @@ void DdmHandle::build(const hs_problem& P, int device) {
   }
   d_coef.alloc(coef.size());
   HS_CUDA(cudaMemcpyAsync(d_coef.p, coef.data(), coef.size() * sizeof(Complex), cudaMemcpyHostToDevice, eng.stream));
+  rank = rank_;
+  world = world_;
+  if (world < 1 || rank < 0 || rank >= world) config_error("partition: rank out of range");
+  if (owner_) {
+    owner.assign(owner_, owner_ + nsub);
+  } else {
+    owner = default_owners(dim, part.counts, world);
+  }
+  for (int id = 0; id < nsub; ++id)
+    if (owner[id] < 0 || owner[id] >= world) config_error("partition: owner out of range");
+  if (partitioned()) {
+    eng.owned.assign(nsub, 0);
+    for (int id = 0; id < nsub; ++id) eng.owned[id] = owner[id] == rank;
+  }
   std::vector<const CVector*> vp(nsub);
   for (int id = 0; id < nsub; ++id) vp[id] = &vals[id];
   // factorize (the DevSub array is re-uploaded with the coefficient pointers below)
@@ -1267,6 +1314,39 @@ void DdmHandle::build(const hs_problem& P, int device) {
         for (int i = 0; i < n; ++i) dst[g * E + i] = tmp[i];
       }
     });
+    if (partitioned()) {
+      // home rank of a node: the owner of its lowest-id subdomain; only the home rank
+      // accumulates the node, reading other ranks' values from ghost copies of their x
+      ghost.assign(nsub, std::vector<std::vector<long long>>(world));
+      for (long long g = 0; g < gn; ++g) {
+        const int n = off[g];
+        if (n == 0) continue;
+        int lo = 1 << 30;
+        for (int i = 0; i < n; ++i) lo = std::min(lo, raw[static_cast<size_t>(g) * E + i].y >> 4);
+        const int home = owner[lo];
+        for (int i = 0; i < n; ++i) {
+          const int2 e = raw[static_cast<size_t>(g) * E + i];
+          const int id = e.y >> 4;
+          if (owner[id] != home) ghost[id][home].push_back(e.x);
+        }
+        if (home != rank)
+          for (int di = 0; di < ndirs; ++di)
+            for (int i = 0; i < E; ++i) ent[(static_cast<size_t>(di) * gn + g) * E + i] = make_int2(-1, 0);
+      }
+      std::vector<long long> flat;
+      ghost_off.assign(static_cast<size_t>(nsub) * world + 1, 0);
+      for (int id = 0; id < nsub; ++id)
+        for (int q = 0; q < world; ++q) {
+          auto& v = ghost[id][q];
+          std::sort(v.begin(), v.end());
+          v.erase(std::unique(v.begin(), v.end()), v.end());
+          ghost_off[static_cast<size_t>(id) * world + q] = static_cast<long long>(flat.size());
+          flat.insert(flat.end(), v.begin(), v.end());
+        }
+      ghost_off.back() = static_cast<long long>(flat.size());
+      if (flat.empty()) flat.push_back(0);
+      d_gpos.upload(flat, eng.stream);
+    }
     acc_ent.upload(ent, eng.stream);
   }
   phase("accumulate plan");
@@ -1303,31 +1383,8 @@ void DdmHandle::build_schedule() {
   nbuf = 4;
   if (const char* e = std::getenv("HS_NBUF")) nbuf = std::max(1, std::atoi(e));
   nbuf = std::min(nbuf, nsweeps);
-  std::vector<int> level(static_cast<size_t>(nsweeps) * nsub, 0), accl(nsweeps + 1, 0);
-  for (int l = 1; l <= nsweeps; ++l) {
-    std::vector<int> order(nsub);
-    for (int id = 0; id < nsub; ++id) order[id] = id;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-      return step_of(part.counts, dim, plan[l - 1], subs[x].sub) < step_of(part.counts, dim, plan[l - 1], subs[y].sub);
-    });
-    int done = 0;
-    for (int id : order) {
-      int lev = l > nbuf ? accl[l - nbuf] : 0;
-      for (int ax = 0; ax < dim; ++ax)
-        for (int sg = -1; sg <= 1; sg += 2) {
-          Vec3i nb = subs[id].sub;
-          nb[ax] -= sg;  // the neighbour whose trace travels along (ax, sg) into id
-          if (nb[ax] < 0 || nb[ax] >= part.counts[ax]) continue;
-          const int nbid = static_cast<int>(part.flatten(nb));
-          const int d = 2 * ax + (sg > 0 ? 1 : 0);
-          for (int lp = 1; lp <= l; ++lp)
-            if (route_h[(lp - 1) * dirs + d] == l) lev = std::max(lev, level[static_cast<size_t>(lp - 1) * nsub + nbid]);
-        }
-      level[static_cast<size_t>(l - 1) * nsub + id] = lev + 1;
-      done = std::max(done, lev + 1);
-    }
-    accl[l] = std::max(done, accl[l - 1]);
-  }
+  std::vector<int> level, accl;
+  task_levels(dim, part.counts, plan, route_h, nsweeps, nbuf, level, accl);
   const int nmacro = accl[nsweeps];
   msteps.assign(nmacro, {});
   acc_after.assign(nmacro, {});
@@ -1377,14 +1434,20 @@ void DdmHandle::build_schedule() {
       if (l == nsweeps) v.erase(std::remove(v.begin(), v.end(), l), v.end());
     }
   }
+  // this rank's tasks (all of them unless partitioned)
+  msteps_own.assign(nmacro, {});
+  for (int m = 0; m < nmacro; ++m)
+    for (const int2& t : msteps[m])
+      if (owner[t.x] == rank) msteps_own[m].push_back(t);
   std::vector<int2> flat;
   mt_off.assign(nmacro, 0);
   max_width = 1;
   for (int m = 0; m < nmacro; ++m) {
     mt_off[m] = static_cast<int>(flat.size());
-    flat.insert(flat.end(), msteps[m].begin(), msteps[m].end());
-    max_width = std::max(max_width, static_cast<int>(msteps[m].size()));
+    flat.insert(flat.end(), msteps_own[m].begin(), msteps_own[m].end());
+    max_width = std::max(max_width, static_cast<int>(msteps_own[m].size()));
   }
+  if (flat.empty()) flat.push_back(make_int2(0, 1));
   d_mtasks.upload(flat, eng.stream);
 }
 
@@ -1398,7 +1461,7 @@ void DdmHandle::build_items() {
   bwd_cnt.assign(nm, 0);
   for (int m = 0; m < nm; ++m) {
     std::vector<Engine::TaskRef> refs;
-    for (const int2& t : msteps[m]) refs.push_back(Engine::TaskRef{t.x, t.y, (t.y - 1) % nbuf});
+    for (const int2& t : msteps_own[m]) refs.push_back(Engine::TaskRef{t.x, t.y, (t.y - 1) % nbuf});
     std::vector<SolveItem> fw, bw;
     eng.build_items(refs, fw, bw);
     fwd_off[m] = static_cast<int>(tasks.size());
@@ -1408,7 +1471,96 @@ void DdmHandle::build_items() {
     bwd_cnt[m] = static_cast<int>(bw.size());
     tasks.insert(tasks.end(), bw.begin(), bw.end());
   }
+  if (tasks.empty()) tasks.push_back(SolveItem{});
   d_tasks.upload(tasks, eng.stream);
+  if (partitioned()) build_xplan();
+}
+
+// Exchange plan of every macro-step for the current batch width: message (src -> dst) lists,
+// in the global task order of the macro-step, the traces src deposited for dst's subdomains
+// (mailbox slot of the generating sweep + presence word) and src's solution values on dst's
+// home nodes (ghost x + the task's nonzero word). Sender and receiver enumerate the same list.
+void DdmHandle::build_xplan() {
+  const int nm = static_cast<int>(msteps.size()), nsub = geom.nsub;
+  const long long dstride = 2 * line_max * R;
+  std::vector<XSeg> segs;
+  xplan.assign(nm, XPlan{});
+  x_sent = x_msgs = 0;
+  long long smax = 1, rmax = 1;
+  auto message = [&](int m, int src, int dst, long long base, std::vector<XSeg>* out) {
+    long long at = base;
+    for (const int2& t : msteps[m]) {
+      const int id = t.x, l = t.y;
+      if (owner[id] != src) continue;
+      const Vec3i sb = subs[id].sub;
+      const DevClass& C = eng.classes[subs[id].cls]->dev;
+      for (int d = 0; d < dirs; ++d) {
+        const int ax = d / 2, sg = (d & 1) ? 1 : -1;
+        if (!part.has_neighbor(sb, ax, sg) || route_h[(l - 1) * dirs + d] == 0) continue;
+        Vec3i tb = sb;
+        tb[ax] += sg;
+        const int tid = part.flatten(tb);
+        if (owner[tid] != dst) continue;
+        const long long slot = (static_cast<long long>(tid) * nsweeps + (l - 1)) * dirs + d;
+        if (out) out->push_back(XSeg{1, 1, slot, at, 0});
+        at += 1;
+        const int cnt = 2 * C.line_len[d] * R;
+        if (out) out->push_back(XSeg{0, cnt, slot * dstride, at, 0});
+        at += 2LL * cnt;
+      }
+      const long long g0 = ghost_off[static_cast<size_t>(id) * world + dst],
+                      g1 = ghost_off[static_cast<size_t>(id) * world + dst + 1];
+      if (g1 > g0) {
+        if (out) out->push_back(XSeg{3, 1, static_cast<long long>(l - 1) * nsub + id, at, 0});
+        at += 1;
+        const long long xoff = static_cast<long long>((l - 1) % nbuf) * eng.xstride;
+        for (long long q = g0; q < g1; q += 1024) {  // runs of <= 1024 positions per segment
+          const int np = static_cast<int>(std::min<long long>(1024, g1 - q));
+          if (out) out->push_back(XSeg{2, np * R, q, at, xoff});
+          at += 2LL * np * R;
+        }
+      }
+    }
+    return at - base;
+  };
+  for (int m = 0; m < nm; ++m) {
+    XPlan& xp = xplan[m];
+    std::vector<XSeg> send, recv;
+    long long so = 0, ro = 0;
+    for (int p = 0; p < world; ++p) {
+      if (p == rank) continue;
+      const long long ns = message(m, rank, p, so, nullptr), nr = message(m, p, rank, ro, nullptr);
+      if (ns == 0 && nr == 0) continue;
+      message(m, rank, p, so, &send);
+      message(m, p, rank, ro, &recv);
+      xp.peers.push_back(p);
+      xp.soff.push_back(so);
+      xp.scnt.push_back(ns);
+      xp.roff.push_back(ro);
+      xp.rcnt.push_back(nr);
+      so += ns;
+      ro += nr;
+      x_sent += ns;
+      x_msgs += ns > 0;
+    }
+    smax = std::max(smax, so);
+    rmax = std::max(rmax, ro);
+    xp.s0 = static_cast<int>(segs.size());
+    xp.ns = static_cast<int>(send.size());
+    segs.insert(segs.end(), send.begin(), send.end());
+    xp.r0 = static_cast<int>(segs.size());
+    xp.nr = static_cast<int>(recv.size());
+    segs.insert(segs.end(), recv.begin(), recv.end());
+  }
+  if (segs.empty()) segs.push_back(XSeg{});
+  d_xseg.upload(segs, eng.stream);
+  xsend.alloc(smax);
+  xrecv.alloc(rmax);
+}
+
+void DdmHandle::comm_allreduce(double* buf, long long count) {
+  if (!arfn) throw Error(kConfig, "partitioned solve: no allreduce callback");
+  if (arfn(cuser, buf, count, eng.stream) != 0) throw Error(kCuda, "partitioned solve: allreduce callback failed");
 }
 
 void DdmHandle::ensure_state(int r, int nrounds) {
@@ -1493,6 +1645,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
   sa.route = route.p;
   const int nm = static_cast<int>(msteps.size());
   int waited = -1, stripes_done = 0;
+  bool u_reduced = false;
   std::vector<int> stripe_blocks(acc_stripe_m.size(), 0);
   auto stripe_pbase = [&](int j) {  // partial blocks of the stripes before j (worst case per stripe)
     const int npb = 256 / R;
@@ -1506,14 +1659,24 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
       HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
     }
     sa.tasks = d_mtasks.p + mt_off[m];
-    sa.ntasks = static_cast<int>(msteps[m].size());
-    launch_build_rhs(sa, eng.n_max, static_cast<int>(line_max), s);
+    sa.ntasks = static_cast<int>(msteps_own[m].size());
+    if (sa.ntasks > 0) launch_build_rhs(sa, eng.n_max, static_cast<int>(line_max), s);
     if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * m], s));
     const char* tstep = std::getenv("HS_TRACE_STEP");
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
-    eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
+    if (sa.ntasks > 0)
+      eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
     if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
-    launch_extract_deposit(sa, static_cast<int>(line_max), s);
+    if (sa.ntasks > 0) launch_extract_deposit(sa, static_cast<int>(line_max), s);
+    if (partitioned() && !xplan[m].peers.empty()) {  // traces and ghost values to / from other ranks
+      const XPlan& xp = xplan[m];
+      launch_xpack(d_xseg.p + xp.s0, xp.ns, true, xsend.p, mbox.p, mpres.p, eng.x.p, nzmask.p, d_gpos.p, R, s);
+      if (!xfn) throw Error(kConfig, "partitioned solve: no exchange callback");
+      if (xfn(cuser, static_cast<int>(xp.peers.size()), xp.peers.data(), xp.soff.data(), xp.scnt.data(),
+              xp.roff.data(), xp.rcnt.data(), xsend.p, xrecv.p, s) != 0)
+        throw Error(kCuda, "partitioned solve: exchange callback failed");
+      launch_xpack(d_xseg.p + xp.r0, xp.nr, false, xrecv.p, mbox.p, mpres.p, eng.x.p, nzmask.p, d_gpos.p, R, s);
+    }
     auto accumulate = [&](int l, long long n0, long long n1, long long pbase) {
       AccumArgs aa{};
       aa.g = geom;
@@ -1540,7 +1703,20 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
           HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
         }
         const int rr = l / ndir - 1;
-        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, u.p, bN.p, R, pnum.p, pden.p, s);
+        const double2* ures = u.p;
+        if (partitioned()) {  // every node is nonzero on its home rank only: the sum is exact
+          double2* t = u.p;
+          if (l != nsweeps) {
+            ufull.alloc(u.n);
+            HS_CUDA(cudaMemcpyAsync(ufull.p, u.p, u.n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+            t = ufull.p;
+          } else {
+            u_reduced = true;
+          }
+          comm_allreduce(reinterpret_cast<double*>(t), 2LL * geom.gn * R);
+          ures = t;
+        }
+        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s);
         launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
         launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
       }
@@ -1559,6 +1735,10 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
       }
     }
   }
+  if (partitioned()) {  // home-node slices of u, and the per-sweep |contribution|^2 sums
+    if (!u_reduced) comm_allreduce(reinterpret_cast<double*>(u.p), 2LL * geom.gn * R);
+    comm_allreduce(norms.p, static_cast<long long>(nsweeps) * R);
+  }
 }
 
 // SolveReport per RHS: counters replayed from the device's per-task nonzero masks in the
@@ -1575,6 +1755,20 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
     HS_CUDA(cudaMemcpyAsync(den.data(), rden.p, den.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
   }
   HS_CUDA(cudaStreamSynchronize(eng.stream));
+  if (partitioned()) {  // every task's mask from its owner (ghost copies are dropped first)
+    std::vector<double> w(nz.size());
+    for (int l = 1; l <= nsweeps; ++l)
+      for (int id = 0; id < nsub; ++id) {
+        const size_t i = static_cast<size_t>(l - 1) * nsub + id;
+        w[i] = owner[id] == rank ? static_cast<double>(nz[i]) : 0.0;
+      }
+    dtmp.alloc(w.size());
+    HS_CUDA(cudaMemcpyAsync(dtmp.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, eng.stream));
+    comm_allreduce(dtmp.p, static_cast<long long>(w.size()));
+    HS_CUDA(cudaMemcpyAsync(w.data(), dtmp.p, w.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
+    HS_CUDA(cudaStreamSynchronize(eng.stream));
+    for (size_t i = 0; i < nz.size(); ++i) nz[i] = static_cast<unsigned>(w[i]);
+  }
   const int nm = static_cast<int>(msteps.size());
   std::vector<double> sweep_sec(nsweeps, 0.0), step_sec(nm, 0.0);
   std::vector<int> active(nm, 0);
@@ -1582,7 +1776,7 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
   for (int m = 0; m < nm; ++m) {
     HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * m], ev[2 + nsweeps + 2 * m]));
     step_sec[m] = ms * 1e-3;
-    for (const int2& t : msteps[m]) active[m] += nz[static_cast<size_t>(t.y - 1) * nsub + t.x] != 0;
+    for (const int2& t : msteps_own[m]) active[m] += nz[static_cast<size_t>(t.y - 1) * nsub + t.x] != 0;
   }
   for (int l = 1; l <= nsweeps; ++l) {  // from the sweep's first macro-step to its accumulate
     HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * sweep_first_m[l]], ev[l]));
@@ -1730,6 +1924,76 @@ extern "C" int hs_ddm_create(const hs_problem* setup, int device, hs_ddm** out, 
 
 extern "C" void hs_ddm_destroy(hs_ddm* s) { delete s; }
 
+extern "C" int hs_ddm_create_partitioned(const hs_problem* setup, int device, int rank, int world, const int* owner,
+                                         hs_exchange_fn exchange, hs_allreduce_fn allreduce, void* user, hs_ddm** out,
+                                         int* pivot_sub, int64_t* pivot_index) {
+  std::unique_ptr<hs_ddm> s;
+  const int rc = guarded(
+      [&] {
+        if (!setup || !out) config_error("hs_ddm_create_partitioned: null argument");
+        if (world > 1 && (!exchange || !allreduce)) config_error("hs_ddm_create_partitioned: missing callbacks");
+        s = std::make_unique<hs_ddm>();
+        s->h.xfn = exchange;
+        s->h.arfn = allreduce;
+        s->h.cuser = user;
+        s->h.build(*setup, device, rank, world, owner);
+      },
+      pivot_sub, pivot_index);
+  if (rc != kOk) return rc;
+  *out = s.release();
+  return kOk;
+}
+
+extern "C" int hs_ddm_partition_info(const hs_ddm* s, int* rank, int* world, int* owned, int64_t* sent_doubles,
+                                     int64_t* messages) {
+  if (!s) return kConfig;
+  const DdmHandle& H = s->h;
+  if (rank) *rank = H.rank;
+  if (world) *world = H.world;
+  if (owned) *owned = static_cast<int>(std::count(H.owner.begin(), H.owner.end(), H.rank));
+  if (sent_doubles) *sent_doubles = H.x_sent;
+  if (messages) *messages = H.x_msgs;
+  return kOk;
+}
+
+namespace {
+Vec3i counts_of(int dim, const int counts[3]) {
+  if (dim != 2 && dim != 3) config_error("Box: dim must be 2 or 3");
+  Vec3i c{1, 1, 1};
+  for (int a = 0; a < dim; ++a) {
+    if (counts[a] < 1) config_error("partition: counts must be >= 1");
+    c[a] = counts[a];
+  }
+  return c;
+}
+}  // namespace
+
+extern "C" int hs_partition_owners(int dim, const int counts[3], int world, int* owner) {
+  return guarded([&] {
+    if (!counts || !owner || world < 1) config_error("hs_partition_owners: bad argument");
+    const std::vector<int> o = default_owners(dim, counts_of(dim, counts), world);
+    std::copy(o.begin(), o.end(), owner);
+  });
+}
+
+extern "C" int hs_partition_traffic(int dim, const int counts[3], int rounds, int world, const int* owner,
+                                    int* macro_steps, int64_t* makespan_tasks, int64_t* cross_faces,
+                                    int64_t* traces) {
+  return guarded([&] {
+    if (!counts || !owner || world < 1 || rounds < 1) config_error("hs_partition_traffic: bad argument");
+    const Vec3i c = counts_of(dim, counts);
+    const int nsub = c[0] * c[1] * (dim == 3 ? c[2] : 1);
+    std::vector<int> o(owner, owner + nsub);
+    for (int v : o)
+      if (v < 0 || v >= world) config_error("hs_partition_traffic: owner out of range");
+    const PartitionCost pc = partition_cost(dim, c, rounds, world, o);
+    if (macro_steps) *macro_steps = pc.macro_steps;
+    if (makespan_tasks) *makespan_tasks = pc.makespan_tasks;
+    if (cross_faces) *cross_faces = pc.cross_faces;
+    if (traces) std::copy(pc.traces.begin(), pc.traces.end(), traces);
+  });
+}
+
 extern "C" int hs_ddm_info(const hs_ddm* s, int* dim, int64_t* global_n, int* nsub, double* factor_seconds,
                            int lo[3], int hi[3]) {
   if (!s) return kConfig;
@@ -1807,7 +2071,7 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
     const bool pinned = cudaPointerGetAttributes(&pa, b) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
                         cudaPointerGetAttributes(&pu, u) == cudaSuccess && pu.type == cudaMemoryTypeHost;
     (void)cudaGetLastError();  // pageable pointers may leave an error on older runtimes
-    if (pinned) {
+    if (pinned && !H.partitioned()) {  // (a partitioned u is final only after its reduction)
       for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
         const int R = std::min(kMaxRhs, nrhs - b0);
         H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,
@@ -2053,7 +2317,7 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
       HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * m], H.ev[2 + H.nsweeps + 2 * m]));
       sec += ms * 1e-3;
       launches += 2;  // forward + backward dataflow launches (the counter reset is a memset)
-      for (const int2& t : H.msteps[m]) {
+      for (const int2& t : H.msteps_own[m]) {  // this rank's solves
         if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
         const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
         ++solves;

@@ -710,6 +710,47 @@ void launch_factor_level_cluster(const FactorArgs& a, int max_m, cudaStream_t s)
   after_launch();
 }
 
+// Pack (arrays -> message) or unpack (message -> arrays) of one exchange, a block per segment.
+__global__ void __launch_bounds__(kThreads) xpack_kernel(const XSeg* segs, bool pack, double* buf, double2* mbox,
+                                                         unsigned* mpres, double2* x, unsigned* nz,
+                                                         const long long* gpos, int R) {
+  const XSeg sg = segs[blockIdx.x];
+  double* B = buf + sg.b;
+  if (sg.kind == 1 || sg.kind == 3) {
+    unsigned* w = sg.kind == 1 ? mpres + sg.a : nz + sg.a;
+    if (threadIdx.x == 0) {
+      if (pack)
+        B[0] = static_cast<double>(*w);
+      else
+        *w = static_cast<unsigned>(B[0]);
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < sg.count; i += blockDim.x) {
+    double2* p;
+    if (sg.kind == 0) {
+      p = mbox + sg.a + i;
+    } else {
+      const long long pos = gpos[sg.a + i / R];
+      p = x + sg.c + pos * R + i % R;
+    }
+    if (pack) {
+      const double2 v = *p;
+      B[2 * i] = v.x;
+      B[2 * i + 1] = v.y;
+    } else {
+      *p = make_double2(B[2 * i], B[2 * i + 1]);
+    }
+  }
+}
+
+void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, unsigned* mpres, double2* x,
+                  unsigned* nzmask, const long long* gpos, int R, cudaStream_t s) {
+  if (nseg <= 0) return;
+  xpack_kernel<<<nseg, kThreads, 0, s>>>(segs, pack, buf, mbox, mpres, x, nzmask, gpos, R);
+  after_launch();
+}
+
 void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStream_t s) {
   const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 512));
   rhs_init_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);

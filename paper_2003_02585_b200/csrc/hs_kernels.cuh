@@ -100,6 +100,19 @@ int launch_accumulate(const AccumArgs& a, cudaStream_t s);  // nodes [a.n0, a.n1
 constexpr int kReducePad = 256;  // extra partial rows every partial buffer reserves (reduction scratch)
 void launch_reduce_partials(double* partial, int nblocks, int R, double* out, cudaStream_t s);
 
+// Cross-rank exchange of a partitioned solve: one segment per mailbox slot,
+// presence word, ghost x run or nonzero word, copied between the solver's arrays and a flat
+// message buffer of doubles (words travel as exactly representable doubles).
+struct XSeg {
+  int kind;        // 0 mailbox data, 1 presence word, 2 ghost x values, 3 nonzero word
+  int count;       // complex values (kinds 0, 2), 1 for words
+  long long a;     // mbox element / mpres slot / ghost position-table offset / nzmask index
+  long long b;     // offset in the message buffer (doubles)
+  long long c;     // kind 2: x buffer offset (elements)
+};
+void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, unsigned* mpres, double2* x,
+                  unsigned* nzmask, const long long* gpos, int R, cudaStream_t s);
+
 // Global CSR SpMV y = A x (x, y node-major N x R) (src/operator.cpp:7-17) and the
 // residual partials |b - y|^2, |b|^2.
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,

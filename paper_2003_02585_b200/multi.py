@@ -1,16 +1,27 @@
-"""Multi-GPU plumbing: one process per GPU, RHS sharded across ranks.
+"""Multi-GPU plumbing: one process per GPU.
 
-Right-hand sides are independent units of the DDM hot path (each one is a full set of diagonal
-sweeps against the same resident subdomain factors), so the B200 design scales by giving every
-rank its own contiguous block of RHS and its own device-resident factorization: no collective
-touches the data path. Collectives appear only for (a) the max-over-ranks timing and (b) an
-optional gather of the solutions to one rank. See DESIGN.md "Multi-GPU".
+Two ways to spread the DDM hot path over ranks:
+
+* **RHS sharding** (`shard_rhs`, `solve_sharded`). Right-hand sides are independent units (each
+  one is a full set of diagonal sweeps against the same resident subdomain factors), so every
+  rank solves its own block of RHS against its own device-resident factorization: no collective
+  touches the data path. This is what `bench.py --gpus N` measures (weak scaling).
+* **Subdomain partitioning** (`PartitionedDdmSolver`). Each rank factorizes and
+  solves only the subdomains it owns, so one problem's factors are spread over the GPUs (C5's
+  106 GB of packed factors). After each macro-step of the sweep schedule the library hands this
+  module one message per neighbouring rank (traces deposited for that rank's subdomains and
+  solution values on its home nodes); they travel as NCCL send/recv pairs ordered on the
+  library's stream (no host synchronisation), or, for gloo groups, staged through host memory.
 """
 from __future__ import annotations
 
-from typing import Callable, Tuple
+import ctypes
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
+
+from . import _lib as L
+from .api import DdmSolver, ProblemSetup, _raise
 
 
 def shard_rhs(n_total: int, rank: int, world: int) -> Tuple[int, int]:
@@ -49,3 +60,153 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# ---------------------------------------------------------------------------------------------
+# subdomain partitioning
+
+def partition_owners(dim: int, counts: Sequence[int], world: int) -> List[int]:
+    """The library's balanced default ownership (hs_partition_owners), flattened id order."""
+    c = (ctypes.c_int * 3)(*(list(counts) + [1, 1, 1])[:3])
+    nsub = int(np.prod(list(counts)[:dim]))
+    o = (ctypes.c_int * nsub)()
+    rc = L.lib().hs_partition_owners(int(dim), c, int(world), o)
+    if rc:
+        _raise(rc)
+    return list(o)
+
+
+def partition_traffic(dim: int, counts: Sequence[int], rounds: int, world: int, owner: Sequence[int]):
+    """(macro_steps, makespan_tasks, cross_faces, traces[world][world]) of an ownership."""
+    c = (ctypes.c_int * 3)(*(list(counts) + [1, 1, 1])[:3])
+    o = (ctypes.c_int * len(owner))(*owner)
+    ms, mk, cf = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+    tr = (ctypes.c_int64 * (world * world))()
+    rc = L.lib().hs_partition_traffic(int(dim), c, int(rounds), int(world), o, ctypes.byref(ms), ctypes.byref(mk),
+                                      ctypes.byref(cf), tr)
+    if rc:
+        _raise(rc)
+    return ms.value, mk.value, cf.value, np.array(list(tr), dtype=np.int64).reshape(world, world)
+
+
+class _DevArray:
+    """A raw device pointer as a torch-importable array (__cuda_array_interface__, no copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def exchange_host(send: np.ndarray, recv: np.ndarray, peers, soff, scnt, roff, rcnt, group=None):
+    """One exchange round over host buffers (gloo): message i goes to / comes from peers[i]."""
+    import torch
+    import torch.distributed as dist
+    st = torch.from_numpy(send)
+    rt = torch.from_numpy(recv)
+    reqs = []
+    for i, p in enumerate(peers):
+        if scnt[i]:
+            reqs.append(dist.isend(st[soff[i]:soff[i] + scnt[i]], int(p), group=group))
+        if rcnt[i]:
+            reqs.append(dist.irecv(rt[roff[i]:roff[i] + rcnt[i]], int(p), group=group))
+    for r in reqs:
+        r.wait()
+
+
+class PartitionedDdmSolver(DdmSolver):
+    """DdmSolver whose subdomains are spread over the ranks of a torch.distributed group
+    (hs_ddm_create_partitioned). Every rank constructs it with the same setup and calls
+    ddm_solve / ddm_solve_device collectively with the same b; every rank receives the full u.
+    NCCL groups exchange device buffers on the library's stream; other backends (gloo) stage
+    through host memory."""
+
+    def __init__(self, setup: ProblemSetup, device: int = 0, group=None, owner: Optional[Sequence[int]] = None):
+        import torch
+        import torch.distributed as dist
+        self._group = group
+        self._rank = dist.get_rank(group)
+        self._world = dist.get_world_size(group)
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._device = torch.device("cuda", device)
+        self._owner = None if owner is None else (ctypes.c_int * len(owner))(*owner)
+        self._error = None
+        self._xcb = L.EXCHANGE_FN(self._exchange)
+        self._arcb = L.ALLREDUCE_FN(self._allreduce)
+        super().__init__(setup, device)
+
+    def _create(self, p, device, h, sub, piv):
+        return L.lib().hs_ddm_create_partitioned(ctypes.byref(p), device, self._rank, self._world, self._owner,
+                                                 self._xcb, self._arcb, None, ctypes.byref(h), ctypes.byref(sub),
+                                                 ctypes.byref(piv))
+
+    def _peer(self, p):  # group rank -> global rank (torch.distributed p2p takes global ranks)
+        import torch.distributed as dist
+        return dist.get_global_rank(self._group, p) if self._group is not None else p
+
+    def _exchange(self, user, npeers, peers, soff, scnt, roff, rcnt, send_ptr, recv_ptr, stream):
+        try:
+            import torch
+            import torch.distributed as dist
+            pe = [self._peer(peers[i]) for i in range(npeers)]
+            so = [soff[i] for i in range(npeers)]
+            sc = [scnt[i] for i in range(npeers)]
+            ro = [roff[i] for i in range(npeers)]
+            rc = [rcnt[i] for i in range(npeers)]
+            ns, nr = max(o + c for o, c in zip(so, sc)), max(o + c for o, c in zip(ro, rc))
+            ext = torch.cuda.ExternalStream(stream, device=self._device)
+            send = torch.as_tensor(_DevArray(send_ptr, max(ns, 1)), device=self._device)
+            recv = torch.as_tensor(_DevArray(recv_ptr, max(nr, 1)), device=self._device)
+            if self._nccl:  # device-to-device over NVLink, ordered on the library's stream
+                with torch.cuda.stream(ext):
+                    ops = []
+                    for i, p in enumerate(pe):
+                        if sc[i]:
+                            ops.append(dist.P2POp(dist.isend, send[so[i]:so[i] + sc[i]], p, self._group))
+                        if rc[i]:
+                            ops.append(dist.P2POp(dist.irecv, recv[ro[i]:ro[i] + rc[i]], p, self._group))
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+            else:  # host-staged (gloo)
+                ext.synchronize()
+                hs = send[:ns].cpu().numpy() if ns else np.zeros(0)
+                hr = np.zeros(nr)
+                exchange_host(hs, hr, pe, so, sc, ro, rc, self._group)
+                if nr:
+                    with torch.cuda.stream(ext):
+                        recv[:nr].copy_(torch.from_numpy(hr))
+                    ext.synchronize()
+            return 0
+        except Exception as e:  # reported by the C-ABI as HS_ERR_CUDA; kept for re-raise
+            self._error = e
+            return 1
+
+    def _allreduce(self, user, ptr, count, stream):
+        try:
+            import torch
+            import torch.distributed as dist
+            ext = torch.cuda.ExternalStream(stream, device=self._device)
+            t = torch.as_tensor(_DevArray(ptr, count), device=self._device)
+            if self._nccl:
+                with torch.cuda.stream(ext):
+                    dist.all_reduce(t, group=self._group)
+            else:
+                ext.synchronize()
+                h = t.cpu()
+                dist.all_reduce(h, group=self._group)
+                with torch.cuda.stream(ext):
+                    t.copy_(h)
+                ext.synchronize()
+            return 0
+        except Exception as e:
+            self._error = e
+            return 1
+
+    def partition_info(self):
+        """(rank, world, owned subdomains, doubles sent per application, messages per application)."""
+        r, w, o = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        sd, ms = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.lib().hs_ddm_partition_info(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(o),
+                                           ctypes.byref(sd), ctypes.byref(ms))
+        if rc:
+            _raise(rc)
+        return r.value, w.value, o.value, sd.value, ms.value
