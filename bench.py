@@ -189,12 +189,20 @@ def run_gpu(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     setup = hs.ProblemSetup(2, [CFG["n"]] * 2, list(CFG["parts"]), hs.Medium("constant", kappa=CFG["kappa"]),
                             pml_width=CFG["pad"])
+    # --partition subdomain (N > 1): one problem, its subdomains spread over the ranks (SURVEY.md
+    # §8(e)); every rank solves the same 16 RHS -> strong scaling. Default: RHS sharding (weak).
+    part = world > 1 and args.partition == "subdomain"
     t0 = time.perf_counter()
-    s = hs.DdmSolver(setup, device=local_rank)
+    if part:
+        from paper_2003_02585_b200.multi import PartitionedDdmSolver
+        s = PartitionedDdmSolver(setup, device=local_rank)
+    else:
+        s = hs.DdmSolver(setup, device=local_rank)
     setup_seconds = time.perf_counter() - t0
     N, R = s.global_n, CFG["nrhs"]
+    units = R if part else R * world  # RHS the whole job completes per step
     hgrid = [1.0 / CFG["n"]] * 2
-    f = make_sources(1000 + rank, s.lo, s.hi, hgrid, [0.0, 0.0])
+    f = make_sources(1000 + (0 if part else rank), s.lo, s.hi, hgrid, [0.0, 0.0])
     b = s.scale_source(f)  # (R, N) RHS-major
     db = torch.from_numpy(b.view(np.float64)).to(dev)
     du = torch.empty_like(db)
@@ -227,7 +235,7 @@ def run_gpu(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = R * world / (ms_max * 1e-3)
+    value = units / (ms_max * 1e-3)
 
     # e2e through the public API with pinned host buffers
     hb = torch.from_numpy(b.view(np.float64)).pin_memory()
@@ -246,7 +254,7 @@ def run_gpu(args, rank, world, local_rank):
     t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_val = R * world / (float(t2.item()) * 1e-3)
+    e2e_val = units / (float(t2.item()) * 1e-3)
     # parity sanity of what was timed: device result == host-path result
     ok = bool(torch.equal(du.cpu(), hu))
 
@@ -260,10 +268,12 @@ def run_gpu(args, rank, world, local_rank):
     nl = max(prof["solve_launches"], 1)
     line = {
         "metric": METRIC, "value": value, "unit": "RHS/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if part else "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": WORKLOAD, "rhs_per_gpu": R, "subdomains": s.nsub, "global_nodes": N,
-                   "parallelism": f"rhs-sharded x{world} (weak), subdomain steps batched per GPU",
+                   "parallelism": (f"subdomain-partitioned x{world} (strong; NCCL trace/ghost exchange per macro-step)"
+                                   if part else f"rhs-sharded x{world} (weak), subdomain steps batched per GPU"),
                    "l2": "inputs larger than L2 (2.5 GB resident factors streamed every step)"},
         # At 16 RHS the solve streams 16 B of factor per 8*16 flop: 8 flop/B > the 5.75 flop/B ridge
         # (37.1 TF FP64 DMMA / 6.46 TB/s), so the dominant kernels are FP64 tensor-core bound.
@@ -289,6 +299,10 @@ def run_gpu(args, rank, world, local_rank):
         "subdomain_solves_per_step": prof["subdomain_solves"],
         "device_host_paths_agree": ok,
     }
+    if part:
+        _, _, owned, sent, msgs = s.partition_info()
+        line["partition"] = {"mode": "subdomain", "owned_subdomains_rank0": owned,
+                             "exchange_bytes_per_application_rank0": 8 * sent, "messages_per_application_rank0": msgs}
     # The paper's pipeline cost model (src/pipeline.cpp) next to the device schedule: the model
     # runs one processor per subdomain, one RHS per tick; the device levels the same trace-routing
     # task graph into macro-steps and solves each task for the whole 16-RHS batch at once.
@@ -315,6 +329,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="rhs", choices=["rhs", "subdomain"],
+                    help="multi-GPU layout: RHS sharding (weak scaling) or subdomain partitioning (strong)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

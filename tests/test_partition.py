@@ -166,3 +166,80 @@ def test_partitioned_equals_single_process(golden, name, owner):
     assert np.array_equal(U1, z["u"]) or float(np.linalg.norm(U1 - z["u"]) / np.linalg.norm(z["u"])) <= 1e-9
     for p in procs:
         assert p.exitcode == 0
+
+
+def _gpu_worker_case(rank, world, port, case, q):
+    import torch
+    import torch.distributed as dist
+    import paper_2003_02585_b200 as hs
+    from paper_2003_02585_b200.multi import PartitionedDdmSolver
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        setup, b, kind = _case(hs, case)
+        s = PartitionedDdmSolver(setup, device=0)
+        if kind != "gmres":
+            b = s.scale_source(b)
+        if kind == "gmres":
+            g = s.gmres(b, 1e-8, 30, 1)
+            q.put((rank, g.x, g.iterations, g.history))
+        else:
+            reps = []
+            U = s.ddm_solve(b, 1, reps, True)
+            q.put((rank, U, [[getattr(r, k) for k in COUNTERS] for r in reps], None))
+    except Exception as e:
+        q.put((rank, repr(e), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _case(hs, case):
+    from paper_2003_02585_b200 import sources
+    if case == "gmres":  # tests/golden/gmres_2d: GMRES preconditioned by partitioned sweeps
+        z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gmres_2d.npz"))
+        med = ast.literal_eval(str(z["medium"]))
+        setup = hs.ProblemSetup(2, [int(z["n"])] * 2, list(z["parts"]),
+                                hs.Medium("constant", kappa=med["media.kappa"]), pml_width=int(z["pad"]))
+        return setup, z["b"], "gmres"
+    # BASELINE config 1 geometry (256^2, 4x4, PML 20, omega = 2 pi 16), two seeded sources
+    setup = hs.ProblemSetup(2, [256, 256], [4, 4], hs.Medium("constant", kappa=2 * math.pi * 16), pml_width=20)
+    lo, hi = [-20, -20], [276, 276]  # the padded global grid
+    f = sources.gaussian_sources(2, lo, hi, [1 / 256] * 2, [0.0, 0.0], sources.seeded_centers(7, 2, 2), 2.0 / 256)
+    return setup, f, "ddm"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,world", [("c1", 4), ("gmres", 2)])
+def test_partitioned_cases(case, world):
+    import paper_2003_02585_b200 as hs
+    setup, b, kind = _case(hs, case)
+    single = hs.DdmSolver(setup)
+    if kind == "gmres":
+        g1 = single.gmres(b, 1e-8, 30, 1)
+    else:
+        b = single.scale_source(b)
+        reps1 = []
+        U1 = single.ddm_solve(b, 1, reps1, True)
+    del single
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker_case, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=600) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+    for r in range(world):
+        x, a, h = res[r]
+        assert not isinstance(x, str), x
+        if kind == "gmres":
+            assert np.array_equal(x, g1.x) and a == g1.iterations and h == g1.history
+        else:
+            assert np.array_equal(x, U1)
+            assert a == [[getattr(x1, k) for k in COUNTERS] for x1 in reps1]
+    for p in procs:
+        assert p.exitcode == 0
