@@ -975,7 +975,17 @@ struct DdmHandle {
   void build_schedule();
   void build_items();
   void ensure_gop();
-  void run(int nrounds, bool track, bool timed, const cudaEvent_t* in_ev = nullptr);
+  // Streamed host transfers (solve_streamed): per stripe, the event of its H2D copy into the
+  // RHS-major staging buffer din; run() transposes each stripe into bN on the compute stream when
+  // a macro-step first needs it, and each final stripe of u out to dout. Every kernel stays on the
+  // compute stream: nothing runs beside the dataflow solve kernels, whose items assume the
+  // whole grid is resident.
+  struct StreamIO {
+    const cudaEvent_t* copied;
+    const double2* din;
+    double2* dout;
+  };
+  void run(int nrounds, bool track, bool timed, const StreamIO* io = nullptr);
   void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps);
   void reports(int nrounds, bool track, hs_solve_report* out);
 };
@@ -1620,7 +1630,7 @@ void DdmHandle::ensure_gop() {
 }
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
-void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_ev) {
+void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
   cudaStream_t s = eng.stream;
   const int nsub = geom.nsub;
   if (track) ensure_gop();
@@ -1646,6 +1656,13 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
   const int nm = static_cast<int>(msteps.size());
   int waited = -1, stripes_done = 0;
   bool u_reduced = false;
+  auto stage_in = [&](int upto) {  // stripes (waited, upto] of b: copied -> transposed into bN
+    for (int j = waited + 1; j <= upto; ++j) {
+      HS_CUDA(cudaStreamWaitEvent(s, io->copied[j], 0));
+      launch_transpose_in_range(io->din, bN.p, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
+    }
+    waited = std::max(waited, upto);
+  };
   std::vector<int> stripe_blocks(acc_stripe_m.size(), 0);
   auto stripe_pbase = [&](int j) {  // partial blocks of the stripes before j (worst case per stripe)
     const int npb = 256 / R;
@@ -1654,9 +1671,8 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
     return b;
   };
   for (int m = 0; m < nm; ++m) {
-    if (in_ev && need_stripe[m] > waited) {  // streamed b: the stripes this macro-step's sources read
-      waited = need_stripe[m];
-      HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
+    if (io && need_stripe[m] > waited) {  // streamed b: the stripes this macro-step's sources read
+      stage_in(need_stripe[m]);
     }
     sa.tasks = d_mtasks.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps_own[m].size());
@@ -1698,10 +1714,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
       if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
         const int last = static_cast<int>(stripe_n.size()) - 2;
-        if (in_ev && waited < last) {  // the residual reads all of b
-          waited = last;
-          HS_CUDA(cudaStreamWaitEvent(s, in_ev[waited], 0));
-        }
+        if (io && waited < last) stage_in(last);  // the residual reads all of b
         const int rr = l / ndir - 1;
         const double2* ures = u.p;
         if (partitioned()) {  // every node is nonzero on its home rank only: the sum is exact
@@ -1727,6 +1740,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const cudaEvent_t* in_e
     for (int j = 0; j < nst; ++j) {
       if (acc_stripe_m[j] != m) continue;
       stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
+      if (io) launch_transpose_out_range(u.p, io->dout, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
       HS_CUDA(cudaEventRecord(ev_out[j], s));
       if (++stripes_done == nst) {
         int nbt = 0;
@@ -1857,7 +1871,8 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
   double2* din = io.p;
   double2* dout = io.p + static_cast<size_t>(n) * kMaxRhs;
-  // the copy stream may overwrite din / bN only after earlier work on the compute stream
+  // the copy stream may overwrite din only after earlier work on the compute stream; it carries
+  // the copies only (DMA engines), never kernels
   HS_CUDA(cudaEventRecord(ev_in[ns], eng.stream));
   HS_CUDA(cudaStreamWaitEvent(cstream, ev_in[ns], 0));
   const size_t pitch = static_cast<size_t>(n) * sizeof(double2);
@@ -1865,19 +1880,18 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
     HS_CUDA(cudaMemcpy2DAsync(din + n0, pitch, reinterpret_cast<const double2*>(b) + n0, pitch,
                               static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyHostToDevice, cstream));
-    launch_transpose_in_range(din, bN.p, n, nr, n0, n1, cstream);
     HS_CUDA(cudaEventRecord(ev_in[j], cstream));
   }
-  run(nrounds, track, true, ev_in.data());
-  // each stripe of u is final after its accumulate of the last sweep (ev_out); stream the stripes
-  // out in the order they complete, while the tail of the application still runs
+  const StreamIO sio{ev_in.data(), din, dout};
+  run(nrounds, track, true, &sio);
+  // each stripe of u is transposed out after its accumulate of the last sweep (ev_out); copy the
+  // stripes to the host in the order they complete, while the tail of the application still runs
   std::vector<int> order(ns);
   for (int j = 0; j < ns; ++j) order[j] = j;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return acc_stripe_m[x] < acc_stripe_m[y]; });
   for (int j : order) {
     HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
     const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
-    launch_transpose_out_range(u.p, dout, n, nr, n0, n1, cstream);
     HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
                               static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
   }

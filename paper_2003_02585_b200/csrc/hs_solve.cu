@@ -138,26 +138,32 @@ __device__ __forceinline__ void acc_zero(Acc<NT>& c) {
 // one k-step (4 columns of the product's inner dimension) of the complex 32 x (8 NT) tile
 // Only m-tiles in `mask` (warp-uniform) are computed: the others are structural zeros (rows past
 // the front, columns past k, the upper triangle of M in the diagonal band).
-template <int NT>
+// NEG: the k-step's B enters negated (the backward pass's -x_bnd rows); the signs fold into the
+// DMMA operand modifiers instead of costing FP64-pipe negations.
+template <int NT, bool NEG = false>
 __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
-  double nb[NT];
+  double bx[NT], by[NT], nby[NT];
 #pragma unroll
-  for (int q = 0; q < NT; ++q) nb[q] = -B[q].y;
+  for (int q = 0; q < NT; ++q) {
+    bx[q] = NEG ? -B[q].x : B[q].x;
+    by[q] = NEG ? -B[q].y : B[q].y;
+    nby[q] = NEG ? B[q].y : -B[q].y;
+  }
 #pragma unroll
   for (int q = 0; q < NT; ++q)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (mask & (1u << i)) {
-        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, B[q].x);
-        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, B[q].y);
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, by[q]);
       }
 #pragma unroll
   for (int q = 0; q < NT; ++q)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (mask & (1u << i)) {
-        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nb[q]);
-        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, B[q].x);
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nby[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, bx[q]);
       }
 }
 
@@ -242,19 +248,23 @@ constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 #ifndef HS_NS_BWD
 #define HS_NS_BWD 3
 #endif
+// Forward items also stage, per band row, the extend-add source of boundary rows (int2) and
+// 1/d of separator rows (double2), so their finalize issues no dependent loads.
 template <bool FWD>
 struct Ring {
   static constexpr int NS = FWD ? HS_NS_FWD : HS_NS_BWD;
   static constexpr int NB = FWD ? 3 : 1;
   static constexpr int kStage = (4 + NB * 2) * 32;  // double2
-  static constexpr int kWarp = NS * kStage + kIdx / 2;
+  static constexpr int kFin = FWD ? 32 / 2 + 32 : 0;
+  static constexpr int kWarp = NS * kStage + kIdx / 2 + kFin;
 };
 
 // The pipelined k-loop shared by both passes: issue(s, stage) stages k-step s with cp.async,
 // use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight data
 // costs shared memory, not registers.
-template <bool FWD, int NT, class Issue, class Use, class Mask>
-__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of) {
+template <bool FWD, int NT, class Issue, class Use, class Mask, class Neg>
+__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of,
+                                      Neg&& neg_of) {
   constexpr int NS = Ring<FWD>::NS, ST = Ring<FWD>::kStage;
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
@@ -271,7 +281,10 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
     double2 A[4], B[NT];
     use(s, ring + (s % NS) * ST, A, B);
     __syncwarp();
-    mma_step(acc, A, B, mask_of(s));
+    if (neg_of(s))
+      mma_step<NT, true>(acc, A, B, mask_of(s));
+    else
+      mma_step<NT, false>(acc, A, B, mask_of(s));
   }
   cp_wait<0>();
 }
@@ -309,10 +322,21 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
     if (lane == 0)
       prefetch_l2(J.factor + band_base(r.t, g.kb) + r.cb0 * r.rbs * 64,
                   static_cast<unsigned>((r.cb1 - r.cb0) * r.rbs) * 1024u);
-    if (J.child0 >= 0 || J.child1 >= 0) {
+    const bool leaf = J.child0 < 0 && J.child1 < 0;
+    if (!leaf) {
       const int n = min(8 * r.cb1, J.k) - 8 * r.cb0;
       for (int j = lane; j < n; j += 32) cp_small<8>(sidx + j, J.pm + 8 * r.cb0 + j);
     }
+    // finalize data of band row `lane`: boundary rows' sources (T_bnd, also the chunk-0
+    // accumulator start), separator rows' 1/d
+    int2* fsrc = sidx + kIdx;
+    double2* fdv = reinterpret_cast<double2*>(fsrc + 32);
+    const int pr = 32 * r.t + lane;
+    if (!leaf && pr >= g.kp && pr - g.kp < J.m - J.k)
+      cp_small<8>(fsrc + lane, J.pm + J.k + (pr - g.kp));
+    else
+      fsrc[lane] = make_int2(-1, -1);
+    if (pr < J.k) cp_small<16>(fdv + lane, J.dinv + pr);
   } else {
     const BwdRange r = bwd_range(J, g, it);
     if (lane == 0) {
@@ -329,16 +353,22 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
 }
 
 // ---------------------------------------------------------------------------------------
-// forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols]
+// forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols].
+// Boundary rows produce V = T_bnd - W T_sep: their chunk-0 accumulators start at -T_bnd (the
+// children's updates at the front's boundary, in the reference's child order), loaded while the
+// k-loop's first stages are in flight, so the finalize only scales and stores. Returns whether
+// this warp finalized the band (the caller signals it).
 template <int NT>
-__device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
-                         int* done, int lane, double2* ring, const int2* sidx, unsigned long long* tr) {
+__device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
+                         int lane, double2* ring, const int2* sidx, unsigned long long* tr) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
   const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
   const double2* X = J.b + static_cast<long long>(J.sep_off) * R;  // right-hand side
   const bool leaf = J.child0 < 0 && J.child1 < 0;
+  const int2* fsrc = sidx + kIdx;
+  const double2* fdv = reinterpret_cast<const double2*>(fsrc + 32);
   // live m-tiles of k-step s: row blocks of the band, minus M's zero blocks above the diagonal
   auto mask_of = [&](int s) {
     const int cb = cb0 + (s >> 1);
@@ -384,7 +414,31 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of);
+  if (it.chunk == 0 && !leaf) {  // -T_bnd = -((0 + child0 V) + child1 V) on boundary rows
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (4 * t + i < g.kb) continue;  // separator row block
+      const int2 src = fsrc[8 * i + rl];
+#pragma unroll
+      for (int q = 0; q < NT; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+          double2 tb = czero();
+          if (src.x >= 0 && r < R) {
+            const double2 w = __ldcg(V + static_cast<long long>(src.x) * R + r);
+            tb = make_double2(tb.x + w.x, tb.y + w.y);
+          }
+          if (src.y >= 0 && r < R) {
+            const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
+            tb = make_double2(tb.x + w.x, tb.y + w.y);
+          }
+          acc.v[i][q][0][e] = -tb.x;
+          acc.v[i][q][1][e] = -tb.y;
+        }
+    }
+  }
+  kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of, [](int) { return false; });
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (cb1 - cb0);
@@ -396,74 +450,42 @@ __device__ void fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 8) * kTileDoubles;
     int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + t) * a.ngr + r0 / 8;
-    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
+    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return false;
   }
   if (tr && lane == 0) tr[3] = gtime();
-  // finalize: z = D^-1 (M T_sep) for separator rows, V = T_bnd - W T_sep for boundary rows, with
-  // T_bnd = child0 V + child1 V. Index and dinv loads first, then each half-band's child updates
-  // all in flight before any store (one round trip per stage instead of a dependent chain).
-  int2 src[4];
-  double2 dv[4];
+  // finalize: z = D^-1 (M T_sep) on separator rows, V = -(acc) = T_bnd - W T_sep on boundary rows
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int pr = 32 * t + 8 * i + rl;
-    const bool bnd = pr >= g.kp && pr - g.kp < J.m - J.k;
-    src[i] = (bnd && !leaf) ? __ldg(J.pm + J.k + (pr - g.kp)) : make_int2(-1, -1);
-    dv[i] = pr < J.k ? J.dinv[pr] : czero();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int pr = 32 * t + 8 * i + rl;
-    if (pr >= J.k) continue;
-    double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
-#pragma unroll
-    for (int q = 0; q < NT; ++q)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = r0 + 8 * q + 2 * (lane & 3) + e;
-        if (r < R) __stcg(zo + r, cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), dv[i]));
-      }
-  }
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double2 w0[2][NT][2], w1[2][NT][2];
-#pragma unroll
-    for (int ii = 0; ii < 2; ++ii)
+    if (pr < J.k) {
+      const double2 dv = fdv[8 * i + rl];
+      double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int i = 2 * h + ii, r = r0 + 8 * q + 2 * (lane & 3) + e;
-          w0[ii][q][e] = (src[i].x >= 0 && r < R) ? __ldcg(V + static_cast<long long>(src[i].x) * R + r) : czero();
-          w1[ii][q][e] = (src[i].y >= 0 && r < R) ? __ldcg(V + static_cast<long long>(src[i].y) * R + r) : czero();
+          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+          if (r < R) __stcg(zo + r, cmul(make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]), dv));
         }
-#pragma unroll
-    for (int ii = 0; ii < 2; ++ii) {
-      const int i = 2 * h + ii, pr = 32 * t + 8 * i + rl;
-      if (!(pr >= g.kp && pr - g.kp < J.m - J.k)) continue;
+    } else if (pr >= g.kp && pr - g.kp < J.m - J.k) {
       double2* vo = V + static_cast<long long>(J.v_off + pr - g.kp) * R;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int r = r0 + 8 * q + 2 * (lane & 3) + e;
-          if (r >= R) continue;
-          // T_bnd = (0 + child0) + child1 in the reference's child order; absent children add nothing
-          double2 tb = czero();
-          if (src[i].x >= 0) tb = make_double2(tb.x + w0[ii][q][e].x, tb.y + w0[ii][q][e].y);
-          if (src[i].y >= 0) tb = make_double2(tb.x + w1[ii][q][e].x, tb.y + w1[ii][q][e].y);
-          __stcg(vo + r, make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
+          if (r < R) __stcg(vo + r, make_double2(-acc.v[i][q][0][e], -acc.v[i][q][1][e]));
         }
     }
   }
-  signal(done + it.front, lane);
+  return true;
 }
 
 // ---------------------------------------------------------------------------------------
 // backward column-band item: x_sep[32 cols][8 NT RHS] = sum over the chunk's rows of
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
 template <int NT>
-__device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int* done, int lane,
+__device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane,
                          double2* ring, const int2* sidx, unsigned long long* tr) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const BwdRange rg = bwd_range(J, g, it);
@@ -509,16 +531,15 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   auto use = [&](int s, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) A[i] = st[i * 32 + lane];
-    const bool neg = row_of(s) >= J.k;  // boundary rows enter as -x_bnd (zeros stay zero)
 #pragma unroll
-    for (int q = 0; q < NT; ++q) {
-      const double2 v = st[(4 + q) * 32 + lane];
-      B[q] = neg ? make_double2(-v.x, -v.y) : v;
-    }
+    for (int q = 0; q < NT; ++q) B[q] = st[(4 + q) * 32 + lane];
   };
+  // boundary row blocks enter as -x_bnd (zeros stay zero): warp-uniform per k-step, folded into
+  // the DMMA operand signs
+  auto neg_of = [&](int s) { return a0 + (s >> 1) >= g.kb; };
   Acc<NT> acc;
   acc_zero(acc);
-  kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of);
+  kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (a1 - a0);
@@ -530,7 +551,7 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const long long slot_part = static_cast<long long>(it.slot) * a.part_stride + J.part_off + loc;
     double* base = a.part + (slot_part * a.ngr + r0 / 8) * kTileDoubles;
     int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + u) * a.ngr + r0 / 8;
-    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return;
+    if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return false;
   }
   if (tr && lane == 0) tr[3] = gtime();
 #pragma unroll
@@ -546,7 +567,7 @@ __device__ void bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
         if (r < R) __stcg(xo + r, make_double2(acc.v[i][q][0][e], acc.v[i][q][1][e]));
       }
   }
-  signal(done + it.front, lane);
+  return true;
 }
 
 __device__ __forceinline__ Geo geo_km(int k, int m) {
@@ -567,52 +588,51 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
   int2* sidx = reinterpret_cast<int2*>(ring + Ring<FWD>::NS * Ring<FWD>::kStage);
   // First round static: item i goes to warp i / gridDim.x of CTA i % gridDim.x, so the head
   // of the list (the critical-path fronts of the backward pass) spreads over all SMs instead
-  // of packing onto the first CTAs' warps. Then dynamic dequeue past the static range. Every
-  // item below the dynamic ticket is held by a resident warp, so progress is guaranteed.
+  // of packing onto the first CTAs' warps. Then dynamic tickets past the static range, each
+  // dequeued one item ahead (its atomic and the next item's record load overlap the current
+  // item; the release of a finalized band overlaps that load). A held ticket is always above
+  // its holder's current item, so the lowest current item can always finish: no deadlock.
   const int nstatic = gridDim.x * (kThreads / 32);
-  int first = blockIdx.x + warp * gridDim.x;
-  for (;;) {
-    int it_idx = first;
-    if (first < 0) {
-      if (lane == 0) it_idx = nstatic + static_cast<int>(atomicAdd(a.queue, 1u));
-      it_idx = __shfl_sync(0xffffffffu, it_idx, 0);
-    }
-    first = -1;
-    if (it_idx >= a.nitems) break;
-    const SolveItem it = a.items[it_idx];
-    if (a.nzmask[it.nzi] == 0) continue;  // skipped task (exactly-zero RHS): nothing depends on it
-    unsigned long long* tr = a.trace ? a.trace + 8LL * it_idx : nullptr;
-    if (tr && lane == 0) tr[0] = gtime();
-    const SolveJob J = a.jobs[it.job];
-    const Geo g = geo_km(J.k, J.m);
+  int cur = blockIdx.x + warp * gridDim.x;
+  SolveItem it{};
+  if (cur < a.nitems) it = a.items[cur];
+  while (cur < a.nitems) {
+    unsigned tk = 0;
+    if (lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
+    bool fin = false;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
-    item_prefetch<FWD>(a, J, g, it, sidx, lane);
-    if (FWD) {
-      if (J.child0 >= 0) wait_count(done + J.child0, J.tgt_c0, lane);
-      if (J.child1 >= 0) wait_count(done + J.child1, J.tgt_c1, lane);
-    } else if (J.parent >= 0) {
-      wait_count(done + J.parent, J.tgt_p, lane);
-    }
-    cp_wait<0>();
-    __syncwarp();
-    if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
-    double2* V = a.vbuf + it.slot * a.vslot_stride;
-    if (FWD) {
-      if (it.rw > 8)
-        fwd_item<2>(a, J, g, it, V, done, lane, ring, sidx, tr);
+    if (a.nzmask[it.nzi] != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it
+      unsigned long long* tr = a.trace ? a.trace + 8LL * cur : nullptr;
+      if (tr && lane == 0) tr[0] = gtime();
+      const SolveJob J = a.jobs[it.job];
+      const Geo g = geo_km(J.k, J.m);
+      item_prefetch<FWD>(a, J, g, it, sidx, lane);
+      if (FWD) {
+        if (J.child0 >= 0) wait_count(done + J.child0, J.tgt_c0, lane);
+        if (J.child1 >= 0) wait_count(done + J.child1, J.tgt_c1, lane);
+      } else if (J.parent >= 0) {
+        wait_count(done + J.parent, J.tgt_p, lane);
+      }
+      cp_wait<0>();
+      __syncwarp();
+      if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
+      double2* V = a.vbuf + it.slot * a.vslot_stride;
+      if (FWD)
+        fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr) : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr);
       else
-        fwd_item<1>(a, J, g, it, V, done, lane, ring, sidx, tr);
-    } else {
-      if (it.rw > 8)
-        bwd_item<2>(a, J, g, it, done, lane, ring, sidx, tr);
-      else
-        bwd_item<1>(a, J, g, it, done, lane, ring, sidx, tr);
+        fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr) : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr);
+      if (tr && lane == 0) {
+        tr[4] = gtime();
+        tr[5] = smid();
+      }
     }
-    if (tr && lane == 0) {
-      tr[4] = gtime();
-      tr[5] = smid();
-    }
+    const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
+    SolveItem nit{};
+    if (nxt < a.nitems) nit = a.items[nxt];
+    if (fin) signal(done + it.front, lane);
     __syncwarp();  // the index slice is rewritten by the next item
+    cur = nxt;
+    it = nit;
   }
 }
 
@@ -650,10 +670,23 @@ void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
     grid = sms * std::max(per, 1);
   }
   const int g = std::max(1, std::min(grid, (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
+  // Cooperative launch: the whole grid is co-resident, which the static first round relies on
+  // (a static item of a CTA that is not yet resident could otherwise be waited for by every
+  // resident warp, e.g. while another stream's kernel holds part of the GPU).
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = fwd ? ring_bytes<true>() : ring_bytes<false>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (fwd)
-    solve6_kernel<true><<<g, kThreads, ring_bytes<true>(), s>>>(a);
+    HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<true>, a));
   else
-    solve6_kernel<false><<<g, kThreads, ring_bytes<false>(), s>>>(a);
+    HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<false>, a));
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   HS_CUDA(cudaGetLastError());
 }
