@@ -140,8 +140,11 @@ __device__ __forceinline__ void acc_zero(Acc<NT>& c) {
 // the front, columns past k, the upper triangle of M in the diagonal band).
 // NEG: the k-step's B enters negated (the backward pass's -x_bnd rows); the signs fold into the
 // DMMA operand modifiers instead of costing FP64-pipe negations.
-template <int NT, bool NEG = false>
+// FULL: every m-tile live (the common case) -- no per-tile predicate, so the warp-synchronous
+// DMMAs issue back to back instead of each behind a WARPSYNC / NOP pair.
+template <int NT, bool NEG = false, bool FULL = false>
 __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
+  if (FULL) mask = 0xFu;
   double bx[NT], by[NT], nby[NT];
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
@@ -281,10 +284,18 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
     double2 A[4], B[NT];
     use(s, ring + (s % NS) * ST, A, B);
     __syncwarp();
-    if (neg_of(s))
-      mma_step<NT, true>(acc, A, B, mask_of(s));
-    else
-      mma_step<NT, false>(acc, A, B, mask_of(s));
+    const unsigned mk = mask_of(s);
+    if (neg_of(s)) {
+      if (mk == 0xFu)
+        mma_step<NT, true, true>(acc, A, B, mk);
+      else
+        mma_step<NT, true, false>(acc, A, B, mk);
+    } else {
+      if (mk == 0xFu)
+        mma_step<NT, false, true>(acc, A, B, mk);
+      else
+        mma_step<NT, false, false>(acc, A, B, mk);
+    }
   }
   cp_wait<0>();
 }
