@@ -165,6 +165,13 @@ int hs_ddm_apply_op(hs_ddm* s, int nrhs, const double* x, double* y);
  * independent Krylov process per RHS, batched through the device. */
 int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
              hs_gmres_report* reports);
+/* GMRES(restart): cycles of at most `restart` Arnoldi steps from the current iterate (residual
+ * b - A x recomputed, convergence still |g_{j+1}| / ||b|| <= tol) until tol or `maxit` total
+ * iterations; BASELINE config 4 asks for GMRES(30). The reference's gmres never restarts
+ * (include/helmsweep/krylov.hpp:32-34), which is hs_gmres (restart = maxit); the two agree
+ * whenever the iteration count stays within `restart`. */
+int hs_gmres_restarted(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart,
+                       int rounds, hs_gmres_report* reports);
 
 /* global_direct_solve (src/harness.cpp:185-214): u = A^-1 (J f) on the padded global grid with
  * the device sparse-direct factorization of the global J-scaled operator (factorized on first

@@ -122,6 +122,8 @@ SIGNATURES = {
                                      ctypes.POINTER(ctypes.c_int64)]),
     "hs_gmres": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double, ctypes.c_int,
                                 ctypes.c_int, ctypes.POINTER(GmresReportC)]),
+    "hs_gmres_restarted": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(GmresReportC)]),
     "hs_ddm_profile": (ctypes.c_int, [ctypes.c_void_p, c_dbl_p, c_i64_p, c_i64_p, c_dbl_p, c_dbl_p]),
     "hs_route_trace": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hs_partition_owners": (ctypes.c_int, [ctypes.c_int, c_int_p, ctypes.c_int, c_int_p]),

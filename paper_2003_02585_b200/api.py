@@ -92,9 +92,6 @@ class Factorization:
         self._h = handle
         self._stats = stats
 
-    def _create(self, p, device, h, sub, piv):
-        return L.lib().hs_ddm_create(ctypes.byref(p), device, ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
-
     def __del__(self):
         if getattr(self, "_h", None):
             try:  # at interpreter shutdown the binding may already be torn down
@@ -377,13 +374,18 @@ class DdmSolver:
             stats.append(st)
         return u
 
-    def gmres(self, b, tol=1e-6, maxit=100, rounds=1):
-        """gmres(A.apply, ddm_solve, b, cfg) as run_precond wires it (src/harness.cpp:285-305)."""
+    def gmres(self, b, tol=1e-6, maxit=100, rounds=1, restart=None):
+        """gmres(A.apply, ddm_solve, b, cfg) as run_precond wires it (src/harness.cpp:285-305).
+        restart=None is the reference's full GMRES; restart=m runs GMRES(m) cycles up to maxit."""
         b = _as_c128(b)
         nrhs = 1 if b.ndim == 1 else b.shape[0]
         x = np.zeros_like(b)
         reps = (L.GmresReportC * nrhs)()
-        rc = L.lib().hs_gmres(self._h, nrhs, _dptr(b), _dptr(x), float(tol), int(maxit), int(rounds), reps)
+        if restart is None:
+            rc = L.lib().hs_gmres(self._h, nrhs, _dptr(b), _dptr(x), float(tol), int(maxit), int(rounds), reps)
+        else:
+            rc = L.lib().hs_gmres_restarted(self._h, nrhs, _dptr(b), _dptr(x), float(tol), int(maxit), int(restart),
+                                            int(rounds), reps)
         if rc:
             _raise(rc)
         out = []

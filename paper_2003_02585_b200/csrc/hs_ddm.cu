@@ -2130,76 +2130,109 @@ extern "C" int hs_ddm_apply_op(hs_ddm* s, int nrhs, const double* x, double* y) 
 // Right-preconditioned full GMRES with MGS and complex Givens (src/krylov.cpp:17-123), the
 // DDM application as preconditioner and the global operator as A (src/harness.cpp:285-305).
 // One Krylov process per RHS column; the preconditioner and operator are batched.
-extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
-                        hs_gmres_report* reports) {
-  return guarded([&] {
-    if (!s) config_error("gmres: null handle");
-    if (!(tol > 0.0)) config_error("GmresConfig: tol must be positive");
-    if (maxit < 1) config_error("GmresConfig: max_iterations must be >= 1");
-    if (maxit + 1 > HS_MAX_GMRES_HISTORY) config_error("gmres: maxit too large for the report");
-    DdmHandle& H = s->h;
-    HS_CUDA(cudaSetDevice(H.eng.device));
-    H.ensure_gop();
-    cudaStream_t st = H.eng.stream;
-    const long long n = H.geom.gn;
-    size_t free_b = 0, total_b = 0;
-    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const double per_col = static_cast<double>(maxit + 4) * n * sizeof(double2);
-    const int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
-    for (int b0 = 0; b0 < nrhs; b0 += rmax) {
-      const int R = std::min(rmax, nrhs - b0);
-      H.ensure_state(R, rounds);
-      const size_t nr = static_cast<size_t>(n) * R;
-      DBuf<double2> Bv, V, W, X, io, part, hcol;
-      DBuf<double> inv;
-      Bv.alloc(nr);
-      V.alloc(nr * (maxit + 1));
-      W.alloc(nr);
-      X.alloc(nr);
-      io.alloc(nr);
-      const int nb = static_cast<int>((nr + 255) / 256);
-      part.alloc(static_cast<size_t>(nb) * R);
-      hcol.alloc(static_cast<size_t>(maxit + 2) * R);
-      inv.alloc(R);
-      HS_CUDA(cudaMemcpyAsync(io.p, b + 2 * b0 * n, sizeof(double2) * nr, cudaMemcpyHostToDevice, st));
-      launch_transpose_in(io.p, Bv.p, n, R, st);
-      auto dot = [&](const double2* a, const double2* c, double2* out) {
-        const int blocks = launch_dot_partials(a, c, n, R, part.p, st);
-        launch_reduce_cpartials(part.p, blocks, R, out, st);
-      };
-      std::vector<double2> hh(static_cast<size_t>(maxit + 2) * R);
-      dot(Bv.p, Bv.p, hcol.p);
+namespace {
+
+// Right-preconditioned GMRES with MGS and complex Givens (src/krylov.cpp:17-123), the DDM
+// application as preconditioner and the global operator as A (src/harness.cpp:285-305). One
+// Krylov process per RHS column; the preconditioner and operator are batched. restart >= maxit
+// is the reference's full GMRES; a smaller restart runs GMRES(restart) cycles from the current
+// iterate (r = b - A x recomputed, the convergence test stays |g_{j+1}| / ||b|| <= tol) until
+// tol or maxit total iterations. When no restart happens the result is the full GMRES's.
+void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart, int rounds,
+                hs_gmres_report* reports) {
+  if (!s) config_error("gmres: null handle");
+  if (!(tol > 0.0)) config_error("GmresConfig: tol must be positive");
+  if (maxit < 1) config_error("GmresConfig: max_iterations must be >= 1");
+  if (maxit + 1 > HS_MAX_GMRES_HISTORY) config_error("gmres: maxit too large for the report");
+  if (restart < 1) config_error("gmres: restart must be >= 1");
+  const int mk = std::min(restart, maxit);  // Krylov basis per cycle
+  DdmHandle& H = s->h;
+  HS_CUDA(cudaSetDevice(H.eng.device));
+  H.ensure_gop();
+  cudaStream_t st = H.eng.stream;
+  const long long n = H.geom.gn;
+  size_t free_b = 0, total_b = 0;
+  HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  // per RHS column: the Krylov basis and work vectors, plus the DDM application's per-RHS
+  // buffers (x / z / rhs per subdomain and x buffer, b / u / staging on the global grid)
+  const double ddm_col = (3.0 * 4 * static_cast<double>(H.eng.n_base.back()) + 6.0 * n) * sizeof(double2);
+  const double per_col = static_cast<double>(mk + 5) * n * sizeof(double2) + ddm_col;
+  int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
+  if (H.partitioned()) rmax = kMaxRhs;  // every rank must batch identically
+  for (int b0 = 0; b0 < nrhs; b0 += rmax) {
+    const int R = std::min(rmax, nrhs - b0);
+    H.ensure_state(R, rounds);
+    const size_t nr = static_cast<size_t>(n) * R;
+    DBuf<double2> Bv, V, W, X, io, part, hcol, ones;
+    DBuf<double> inv;
+    Bv.alloc(nr);
+    V.alloc(nr * (mk + 1));
+    W.alloc(nr);
+    X.alloc(nr);
+    io.alloc(nr);
+    const int nb = static_cast<int>((nr + 255) / 256);
+    part.alloc(static_cast<size_t>(nb) * R);
+    hcol.alloc(static_cast<size_t>(mk + 2) * R);
+    inv.alloc(R);
+    ones.alloc(R);
+    {
+      const std::vector<double2> o(R, make_double2(1.0, 0.0));
+      HS_CUDA(cudaMemcpyAsync(ones.p, o.data(), sizeof(double2) * R, cudaMemcpyHostToDevice, st));
+    }
+    HS_CUDA(cudaMemcpyAsync(io.p, b + 2 * b0 * n, sizeof(double2) * nr, cudaMemcpyHostToDevice, st));
+    launch_transpose_in(io.p, Bv.p, n, R, st);
+    HS_CUDA(cudaMemsetAsync(X.p, 0, sizeof(double2) * nr, st));
+    auto dot = [&](const double2* a, const double2* c, double2* out) {
+      const int blocks = launch_dot_partials(a, c, n, R, part.p, st);
+      launch_reduce_cpartials(part.p, blocks, R, out, st);
+    };
+    std::vector<double2> hh(static_cast<size_t>(mk + 2) * R);
+    std::vector<double> bnorm(R), invh(R), fin(R, 1.0);
+    std::vector<int> iters(R, 0), active(R, 1), breakdown(R, 0);
+    std::vector<std::vector<double>> hist(R);
+    for (int cycle = 0;; ++cycle) {
+      // r0 = b (first cycle, x = 0) or b - A x; its norm starts the Givens right-hand side
+      const double2* r0 = Bv.p;
+      if (cycle > 0) {
+        launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, W.p, R, st);
+        HS_CUDA(cudaMemcpyAsync(V.p, Bv.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+        launch_axpy_cols(V.p, W.p, ones.p, 1, n, R, st);
+        r0 = V.p;
+      }
+      dot(r0, r0, hcol.p);
       HS_CUDA(cudaMemcpyAsync(hh.data(), hcol.p, sizeof(double2) * R, cudaMemcpyDeviceToHost, st));
       HS_CUDA(cudaStreamSynchronize(st));
-      std::vector<double> bnorm(R), invh(R);
-      std::vector<int> iters(R, 0), active(R, 1), breakdown(R, 0);
-      std::vector<std::vector<double>> hist(R);
+      std::vector<int> cyc_it(R, 0), live(R, 0);
       std::vector<std::vector<std::vector<Complex>>> hess(R);
-      std::vector<std::vector<Complex>> cs(R, std::vector<Complex>(maxit)), sn(R, std::vector<Complex>(maxit)),
-          g(R, std::vector<Complex>(maxit + 1, Complex(0.0)));
+      std::vector<std::vector<Complex>> cs(R, std::vector<Complex>(mk)), sn(R, std::vector<Complex>(mk)),
+          g(R, std::vector<Complex>(mk + 1, Complex(0.0)));
       for (int r = 0; r < R; ++r) {
-        bnorm[r] = std::sqrt(hh[r].x);
-        if (bnorm[r] == 0.0) {
-          active[r] = 0;
-          hist[r].push_back(0.0);
-          invh[r] = 0.0;
-        } else {
-          invh[r] = 1.0 / bnorm[r];
-          g[r][0] = bnorm[r];
-          hist[r].push_back(1.0);
+        const double beta = std::sqrt(hh[r].x);
+        if (cycle == 0) {
+          bnorm[r] = beta;
+          hist[r].push_back(beta == 0.0 ? 0.0 : 1.0);
+          if (beta == 0.0) active[r] = 0;
         }
+        invh[r] = 0.0;
+        if (!active[r] || beta == 0.0) continue;
+        live[r] = 1;
+        invh[r] = 1.0 / beta;
+        g[r][0] = beta;
       }
-      // v0 = b / ||b||
-      HS_CUDA(cudaMemcpyAsync(V.p, Bv.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
+      bool any = false;
+      for (int r = 0; r < R; ++r) any |= live[r] != 0;
+      if (!any) break;
+      // v0 = r0 / ||r0|| (columns not iterating this cycle are zero)
+      if (r0 != V.p) HS_CUDA(cudaMemcpyAsync(V.p, r0, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
       HS_CUDA(cudaMemcpyAsync(inv.p, invh.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
       launch_scale_cols(V.p, inv.p, n, R, st);
       int j = 0;
-      auto any_active = [&] {
+      auto any_live = [&] {
         for (int r = 0; r < R; ++r)
-          if (active[r]) return true;
+          if (live[r]) return true;
         return false;
       };
-      while (j < maxit && any_active()) {
+      while (j < mk && any_live()) {
         double2* vj = V.p + static_cast<size_t>(j) * nr;
         HS_CUDA(cudaMemcpyAsync(H.bN.p, vj, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
         H.run(rounds, false, false);                                          // z = M^-1 v_j
@@ -2214,7 +2247,7 @@ extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double 
         HS_CUDA(cudaStreamSynchronize(st));
         for (int r = 0; r < R; ++r) {
           invh[r] = 0.0;
-          if (!active[r]) continue;
+          if (!live[r]) continue;
           std::vector<Complex> h(j + 2);
           for (int i = 0; i <= j; ++i) h[i] = Complex(hh[static_cast<size_t>(i) * R + r].x, hh[static_cast<size_t>(i) * R + r].y);
           const double wnorm = std::sqrt(hh[static_cast<size_t>(j + 1) * R + r].x);
@@ -2242,33 +2275,35 @@ extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double 
           g[r][j] = cs[r][j] * g[r][j];
           const double rel = std::abs(g[r][j + 1]) / bnorm[r];
           hist[r].push_back(rel);
+          fin[r] = rel;
+          ++iters[r];
+          cyc_it[r] = j + 1;
           if (wnorm <= 1e-14 * bnorm[r]) {
             breakdown[r] = 1;
-            active[r] = 0;
-            iters[r] = j + 1;
+            live[r] = active[r] = 0;
+            continue;
+          }
+          if (rel <= tol) {
+            live[r] = active[r] = 0;
+            continue;
+          }
+          if (iters[r] >= maxit) {
+            live[r] = active[r] = 0;
             continue;
           }
           invh[r] = 1.0 / wnorm;
-          if (rel <= tol) {
-            active[r] = 0;
-            iters[r] = j + 1;
-          }
         }
-        for (int r = 0; r < R; ++r)
-          if (!active[r] && iters[r] != j + 1) invh[r] = 0.0;  // frozen columns stay zero
         double2* vn = V.p + static_cast<size_t>(j + 1) * nr;
         HS_CUDA(cudaMemcpyAsync(vn, W.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
         HS_CUDA(cudaMemcpyAsync(inv.p, invh.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
-        launch_scale_cols(vn, inv.p, n, R, st);
+        launch_scale_cols(vn, inv.p, n, R, st);  // columns that stopped get a zero vector
         ++j;
       }
-      for (int r = 0; r < R; ++r)
-        if (active[r]) iters[r] = j;
-      // y by back substitution, then x = M^-1 (V y)
+      // y by back substitution, then x += M^-1 (V y) (columns that did not iterate add M^-1 0 = 0)
       std::vector<std::vector<Complex>> y(R);
       int jmax = 0;
       for (int r = 0; r < R; ++r) {
-        const int jr = iters[r];
+        const int jr = cyc_it[r];
         jmax = std::max(jmax, jr);
         y[r].assign(jr, Complex(0.0));
         for (int i = jr - 1; i >= 0; --i) {
@@ -2281,36 +2316,49 @@ extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double 
       std::vector<double2> alpha(R);
       for (int k2 = 0; k2 < jmax; ++k2) {
         for (int r = 0; r < R; ++r)
-          alpha[r] = k2 < iters[r] ? make_double2(y[r][k2].real(), y[r][k2].imag()) : make_double2(0.0, 0.0);
+          alpha[r] = k2 < cyc_it[r] ? make_double2(y[r][k2].real(), y[r][k2].imag()) : make_double2(0.0, 0.0);
         HS_CUDA(cudaMemcpyAsync(hcol.p, alpha.data(), sizeof(double2) * R, cudaMemcpyHostToDevice, st));
         launch_axpy_cols(H.bN.p, V.p + static_cast<size_t>(k2) * nr, hcol.p, 0, n, R, st);
       }
       H.run(rounds, false, false);
-      HS_CUDA(cudaMemcpyAsync(X.p, H.u.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
-      // true residual ||b - A x|| / ||b||
-      const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st);
-      DBuf<double> tn;
-      tn.alloc(R);
-      launch_reduce_partials(H.pnum.p, nb2, R, tn.p, st);
-      std::vector<double> tnh(R);
-      HS_CUDA(cudaMemcpyAsync(tnh.data(), tn.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
-      launch_transpose_out(X.p, io.p, n, R, st);
-      HS_CUDA(cudaMemcpyAsync(x + 2 * b0 * n, io.p, sizeof(double2) * nr, cudaMemcpyDeviceToHost, st));
-      HS_CUDA(cudaStreamSynchronize(st));
-      if (reports)
-        for (int r = 0; r < R; ++r) {
-          hs_gmres_report& rep = reports[b0 + r];
-          std::memset(&rep, 0, sizeof(rep));
-          rep.iterations = iters[r];
-          const double fin = iters[r] > 0 ? std::abs(g[r][iters[r]]) / bnorm[r] : 1.0;
-          rep.final_residual = bnorm[r] == 0.0 ? 0.0 : fin;
-          rep.converged = bnorm[r] == 0.0 || breakdown[r] || fin <= tol;
-          rep.true_residual = bnorm[r] == 0.0 ? 0.0 : std::sqrt(tnh[r]) / bnorm[r];
-          rep.n_history = static_cast<int>(hist[r].size());
-          for (int q = 0; q < rep.n_history; ++q) rep.history[q] = hist[r][q];
-        }
+      launch_axpy_cols(X.p, H.u.p, ones.p, 0, n, R, st);
+      HS_CUDA(cudaStreamSynchronize(st));  // alpha / hcol host buffers are reused
     }
-  });
+    // true residual ||b - A x|| / ||b||
+    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st);
+    DBuf<double> tn;
+    tn.alloc(R);
+    launch_reduce_partials(H.pnum.p, nb2, R, tn.p, st);
+    std::vector<double> tnh(R);
+    HS_CUDA(cudaMemcpyAsync(tnh.data(), tn.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
+    launch_transpose_out(X.p, io.p, n, R, st);
+    HS_CUDA(cudaMemcpyAsync(x + 2 * b0 * n, io.p, sizeof(double2) * nr, cudaMemcpyDeviceToHost, st));
+    HS_CUDA(cudaStreamSynchronize(st));
+    if (reports)
+      for (int r = 0; r < R; ++r) {
+        hs_gmres_report& rep = reports[b0 + r];
+        std::memset(&rep, 0, sizeof(rep));
+        rep.iterations = iters[r];
+        const double f = iters[r] > 0 ? fin[r] : 1.0;
+        rep.final_residual = bnorm[r] == 0.0 ? 0.0 : f;
+        rep.converged = bnorm[r] == 0.0 || breakdown[r] || f <= tol;
+        rep.true_residual = bnorm[r] == 0.0 ? 0.0 : std::sqrt(tnh[r]) / bnorm[r];
+        rep.n_history = static_cast<int>(hist[r].size());
+        for (int q = 0; q < rep.n_history; ++q) rep.history[q] = hist[r][q];
+      }
+  }
+}
+
+}  // namespace
+
+extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
+                        hs_gmres_report* reports) {
+  return guarded([&] { gmres_impl(s, nrhs, b, x, tol, maxit, maxit, rounds, reports); });
+}
+
+extern "C" int hs_gmres_restarted(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart,
+                                  int rounds, hs_gmres_report* reports) {
+  return guarded([&] { gmres_impl(s, nrhs, b, x, tol, maxit, restart, rounds, reports); });
 }
 
 extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, int64_t* subdomain_solves,

@@ -69,3 +69,26 @@ def gaussian_sources(dim, glo, ghi, h, origin, centers, sigma, interior_lo=(0.0,
             m = inside[0][None, None, :] & inside[1][None, :, None] & inside[2][:, None, None]
         out[r] = np.where(m, np.exp(-r2 / (2.0 * sigma * sigma)), 0.0).ravel()
     return out
+
+
+def gaussian_random_velocity(n, seed, corr_len=0.05, lo=0.0, hi=1.0, dtype=np.float32):
+    """BASELINE config 4's smooth heterogeneous medium on an (n+1)^2 node lattice over [lo, hi]^2
+    (axis 0 fastest, the HSVG sample order, include/helmsweep/media.hpp:22-27):
+    c = 1 + 0.5 (1 + tanh g) / 2, g a seeded stationary Gaussian field with Gaussian covariance
+    exp(-|r|^2 / (2 corr_len^2)), unit variance. g is white noise filtered in Fourier space by the
+    square root of the covariance's spectral density, exp(-|k|^2 corr_len^2 / 4) (periodic
+    synthesis on a lattice padded by 4 correlation lengths, then cropped), and normalised to zero
+    mean and unit variance. The reference defines no generator; this one is archived with its
+    seed so both paths read the same file."""
+    m = n + 1
+    h = (hi - lo) / n
+    pad = int(np.ceil(4 * corr_len / h))
+    M = m + pad
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal((M, M))
+    k = 2 * np.pi * np.fft.fftfreq(M, d=h)
+    k2 = k[:, None] ** 2 + k[None, :] ** 2
+    g = np.fft.ifft2(np.fft.fft2(w) * np.exp(-k2 * corr_len ** 2 / 4)).real[:m, :m]
+    g = (g - g.mean()) / g.std()
+    c = 1.0 + 0.5 * (1.0 + np.tanh(g)) / 2.0
+    return np.ascontiguousarray(c.T, dtype=dtype)  # [y][x] rows -> axis 0 (x) fastest when flattened

@@ -172,6 +172,22 @@ def test_gmres_matches_reference(hs, golden):
     assert g.true_residual <= 1e-7
 
 
+def test_gmres_restarted(hs, golden):
+    z = golden("gmres_2d")
+    med = ast.literal_eval(str(z["medium"]))
+    s = hs.DdmSolver(hs.ProblemSetup(2, [int(z["n"])] * 2, list(z["parts"]), hs.Medium("constant", kappa=med["media.kappa"]),
+                                     pml_width=int(z["pad"])))
+    full = s.gmres(z["b"], float(z["tol"]), int(z["maxit"]), 1)
+    # a restart length the iteration count never reaches is the reference's full GMRES, bit for bit
+    same = s.gmres(z["b"], float(z["tol"]), int(z["maxit"]), 1, restart=full.iterations + 1)
+    assert np.array_equal(same.x, full.x) and same.history == full.history
+    # GMRES(2): restarts from the current iterate still reach the tolerance
+    g2 = s.gmres(z["b"], float(z["tol"]), 200, 1, restart=2)
+    assert g2.converged and g2.iterations >= full.iterations
+    assert g2.true_residual <= 1e-7 and rel(g2.x, z["x"]) <= 1e-6
+    assert len(g2.history) == g2.iterations + 1
+
+
 def test_apply_op_matches_oracle(hs, golden):
     z = golden("ddm_2d_layered")
     s = hs.DdmSolver(_setup(hs, z))
