@@ -93,6 +93,7 @@ struct ClassDev {
   std::vector<DevFront> h_fronts;
   std::vector<int> fkc, fkr;   // per front split-K chunk (column blocks / block rows)
   std::vector<int> fgw;        // per front RHS group width (8 on the critical path, else 16)
+  std::vector<unsigned> fbits; // per front: faces whose injection lines lie in its subtree
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   DBuf<unsigned char> on_line;
   std::vector<int> level_start_down;
@@ -165,6 +166,7 @@ struct Engine {
       return false;
     };
     std::vector<unsigned char> fl(c.n, 0);
+    std::vector<int> front_of_pos;
     for (int d = 0; d < 2 * c.dim; ++d) {
       const int a = d / 2, sign = (d & 1) ? 1 : -1;
       GridRange line = loc;
@@ -197,6 +199,19 @@ struct Engine {
         if (p0[i] >= 0) fl[p0[i]] = 1;
         if (pm[i] >= 0) fl[pm[i]] = 1;
       }
+      // fronts whose subtree holds an injection position of face d (the front owning the
+      // position's separator slot and its ancestors)
+      if (front_of_pos.empty()) {
+        front_of_pos.assign(c.n, -1);
+        for (size_t f = 0; f < c.fronts.size(); ++f)
+          for (int q = 0; q < c.fronts[f].k; ++q) front_of_pos[c.fronts[f].sep_off + q] = static_cast<int>(f);
+        cd.fbits.assign(c.fronts.size(), 0u);
+      }
+      for (std::int64_t i = 0; i < cnt; ++i)
+        for (int pos : {p0[i], pm[i]}) {
+          if (pos < 0) continue;
+          for (int f = front_of_pos[pos]; f >= 0 && !(cd.fbits[f] >> d & 1u); f = c.fronts[f].parent) cd.fbits[f] |= 1u << d;
+        }
     }
     cd.on_line.upload(fl, stream);
     cd.dev.on_line = cd.on_line.p;
@@ -525,6 +540,8 @@ struct Engine {
         J.parent = fd.parent;
         J.tgt_p = fd.parent >= 0 ? ncband_of(c.fronts[fd.parent]) * groups_of(cd, fd.parent) : 0;
         J.gw = cd.fgw[f];
+        auto fb = [&](int q) { return q < 0 ? 0u : cd.fbits.empty() ? 0xFFu : cd.fbits[q]; };
+        J.act = static_cast<int>(fb(static_cast<int>(f)) | fb(fd.child[0]) << 8 | fb(fd.child[1]) << 16);
         J.arr_off = cd.h_fronts[f].arr_off;
         J.part_off = cd.h_fronts[f].part_off;
         J.kc = cd.fkc[f];
@@ -597,7 +614,7 @@ struct Engine {
   // One forward and one backward launch over the items of a step group.
   DBuf<unsigned long long> trace;
   void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const unsigned* nzmask,
-                 bool traced = false) {
+                 bool traced = false, const unsigned* tface = nullptr) {
     const long long per = static_cast<long long>(nslots) * nf_max;
     const long long arr = static_cast<long long>(nslots) * arr_total * ngr;
     HS_CUDA(cudaMemsetAsync(cnt.p, 0, cnt_ints() * sizeof(int), stream));
@@ -612,6 +629,7 @@ struct Engine {
     a.part_stride = part_total;
     a.arr_stride = arr_total;
     a.nzmask = nzmask;
+    a.tface = tface;
     a.items = fwd;
     a.nitems = nfwd;
     a.done = cnt.p;
@@ -924,7 +942,7 @@ struct DdmHandle {
   std::vector<Vec3i> plan;
   std::vector<int> route_h;
   DBuf<double2> mbox;
-  DBuf<unsigned> mpres, nzmask;
+  DBuf<unsigned> mpres, nzmask, tface;
   DBuf<int> route;
   DBuf<double2> bN, u, io;
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
@@ -1597,6 +1615,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   mbox.alloc(static_cast<size_t>(nsub) * nsweeps * dirs * 2 * line_max * R);
   mpres.alloc(static_cast<size_t>(nsub) * nsweeps * dirs);
   nzmask.alloc(static_cast<size_t>(nsweeps) * nsub);
+  tface.alloc(static_cast<size_t>(nsweeps) * nsub);
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
   // + striped rounding + reduction scratch
@@ -1637,6 +1656,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
   HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
   HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(unsigned), s));
   HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(unsigned), s));
+  HS_CUDA(cudaMemsetAsync(tface.p, 0, tface.n * sizeof(unsigned), s));
   if (timed) HS_CUDA(cudaEventRecord(ev[0], s));
   SweepArgs sa{};
   sa.g = geom;
@@ -1652,6 +1672,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
   sa.mbox_dir_stride = 2 * line_max * R;
   sa.mpres = mpres.p;
   sa.nzmask = nzmask.p;
+  sa.tface = tface.p;
   sa.route = route.p;
   const int nm = static_cast<int>(msteps.size());
   int waited = -1, stripes_done = 0;
@@ -1681,7 +1702,8 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     const char* tstep = std::getenv("HS_TRACE_STEP");
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
     if (sa.ntasks > 0)
-      eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced);
+      eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced,
+                    std::getenv("HS_NO_FRONT_SKIP") ? nullptr : tface.p);
     if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
     if (sa.ntasks > 0) launch_extract_deposit(sa, static_cast<int>(line_max), s);
     if (partitioned() && !xplan[m].peers.empty()) {  // traces and ghost values to / from other ranks
@@ -2370,8 +2392,23 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
     HS_CUDA(cudaSetDevice(H.eng.device));
     HS_CUDA(cudaStreamSynchronize(H.eng.stream));
     const int nsub = H.geom.nsub;
-    std::vector<unsigned> nz(static_cast<size_t>(H.nsweeps) * nsub);
+    std::vector<unsigned> nz(static_cast<size_t>(H.nsweeps) * nsub), tf(nz.size());
     HS_CUDA(cudaMemcpy(nz.data(), H.nzmask.p, nz.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    HS_CUDA(cudaMemcpy(tf.data(), H.tface.p, tf.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    // the work the solve performs: the backward pass over every front, the forward pass over the
+    // live fronts only (past sweep 1, fronts whose subtree holds no nonzero injection line have
+    // T = z = V = 0 and are skipped; their packed entries are neither read nor multiplied)
+    auto live_packed = [&](int cls, unsigned fm) {
+      const ClassDev& cd = *H.eng.classes[cls];
+      if (fm & 0x100u || cd.fbits.empty()) return static_cast<double>(cd.sym->packed_entries);
+      double p = 0.0;
+      for (size_t f = 0; f < cd.sym->fronts.size(); ++f) {
+        if (!(cd.fbits[f] & fm & 0xFFu)) continue;
+        const double m = cd.sym->fronts[f].m, k = cd.sym->fronts[f].k;
+        p += m * k - k * (k - 1) / 2;
+      }
+      return p;
+    };
     double sec = 0.0, bytes = 0.0, flops = 0.0;
     int64_t launches = 0, solves = 0;
     float ms = 0.f;
@@ -2382,9 +2419,10 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
       for (const int2& t : H.msteps_own[m]) {  // this rank's solves
         if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
         const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
+        const double pf = live_packed(H.subs[t.x].cls, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
         ++solves;
-        bytes += 2.0 * c.packed_entries * 16 + 2.0 * H.R * c.n * 16;
-        flops += 16.0 * c.packed_entries * H.R;
+        bytes += (pf + c.packed_entries) * 16 + 2.0 * H.R * c.n * 16;
+        flops += 8.0 * (pf + c.packed_entries) * H.R;
       }
     }
     if (solve_seconds) *solve_seconds = sec;

@@ -91,7 +91,11 @@ struct SolveJob {
   int child0, child1, tgt_c0, tgt_c1;      // children and their finalized-item counts (forward waits)
   int parent, tgt_p, arr_off, part_off;    // parent and its finalized-item count (backward waits)
   int kc, kr;                              // split-K chunk: column blocks (forward) / block rows (backward)
-  int gw, pad_;                            // RHS per item group (8 on the critical path, else 16)
+  int gw;                                  // RHS per item group (8 on the critical path, else 16)
+  // Faces whose injection lines lie in the subtree of this front (bits 0-7), of child0 (8-15) and
+  // child1 (16-23). Past sweep 1 a task's right-hand side is zero off the lines of the faces that
+  // received traces, so a front whose subtree holds none of them has T = 0, z = 0 and V = 0.
+  int act;
 };
 
 struct FactorTask {

@@ -409,10 +409,12 @@ __global__ void nonzero_kernel(SweepArgs a) {
   const DevClass& C = a.cls[S.cls];
   const double2* B = task_b(a, S, l);
   const int R = a.R;
-  unsigned bits = 0;
+  unsigned bits = 0, faces = 0;
   {
     for (int d = 0; d < a.dirs; ++d) {
       const int len = C.line_len[d];
+      const unsigned b0 = bits;
+      bits = 0;
       for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * R;
            idx += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
@@ -426,10 +428,16 @@ __global__ void nonzero_kernel(SweepArgs a) {
           if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
         }
       }
+      if (bits) faces |= 1u << d;
+      bits |= b0;
     }
   }
   bits = __reduce_or_sync(kFull, bits);
-  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
+  faces = __reduce_or_sync(kFull, faces);
+  const long long ti = static_cast<long long>(l - 1) * a.g.nsub + sub;
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[ti], bits);
+  // sweep 1 also carries the split source anywhere in the subdomain: every front is live (0x100)
+  if ((threadIdx.x & 31) == 0 && (faces || l == 1)) atomicOr(&a.tface[ti], l == 1 ? 0x100u : faces);
 }
 
 // extract_trace (src/transfer.cpp:47-66) + route_trace (src/sweeper.cpp:58-73) + deposit into the

@@ -22,6 +22,8 @@ struct SolveArgs {
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
+  const unsigned* tface;   // per task: faces with nonzero injected data, 0x100 = every front live
+                           // (sweep 1); null = every front live
 };
 
 // Multifrontal forward (z = D^-1 L^-1 b) or backward (x = L^-T z) pass over the work items of
@@ -70,6 +72,7 @@ struct SweepArgs {
   long long mbox_dir_stride;  // elements per (sub, sweep, dir) slot
   unsigned* mpres;         // presence bitmask [target sub][generating sweep][dir]
   unsigned* nzmask;        // [sweep][sub]
+  unsigned* tface;         // [sweep][sub]: faces whose injection lines carry a nonzero value
   const int* route;        // [sweep][dir] target sweep (0 = discard)
 };
 // RHS of each subdomain task: split source (sweep 1) plus injected traces, and the

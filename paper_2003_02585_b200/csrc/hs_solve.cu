@@ -119,6 +119,8 @@ __device__ __forceinline__ long long band_base(int t, int kb) {
 __device__ __forceinline__ int nch_fwd(const Geo& g, int t, int kc) { return (min(g.kb, 4 * t + 4) + kc - 1) / kc; }
 __device__ __forceinline__ int nch_bwd(const Geo& g, int u, int kr) { return (g.nrb - 4 * u + kr - 1) / kr; }
 
+constexpr unsigned kAllLive = 0x100u;  // task face mask bit: every front is live
+
 template <int NT>
 struct Acc {
   double v[4][NT][2][2];  // m-tile i, n-tile q, re/im, fragment element e
@@ -371,7 +373,7 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
 // this warp finalized the band (the caller signals it).
 template <int NT>
 __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
-                         int lane, double2* ring, const int2* sidx, unsigned long long* tr) {
+                         int lane, double2* ring, const int2* sidx, unsigned long long* tr, unsigned clive) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
@@ -400,7 +402,9 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
       cp16(st + i * 32 + lane, ok ? p + i * 64 : P, ok);
     }
     const int col = 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3);
-    const int2 src = (!leaf && col < J.k) ? sidx[col - 8 * cb0] : make_int2(-1, -1);
+    int2 src = (!leaf && col < J.k) ? sidx[col - 8 * cb0] : make_int2(-1, -1);
+    if (!(clive & 1u)) src.x = -1;  // a structurally zero child contributes nothing (its V is stale)
+    if (!(clive & 2u)) src.y = -1;
     double2* sb = st + 4 * 32 + lane;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
@@ -429,7 +433,9 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (4 * t + i < g.kb) continue;  // separator row block
-      const int2 src = fsrc[8 * i + rl];
+      int2 src = fsrc[8 * i + rl];
+      if (!(clive & 1u)) src.x = -1;
+      if (!(clive & 2u)) src.y = -1;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
@@ -497,7 +503,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
 template <int NT>
 __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane,
-                         double2* ring, const int2* sidx, unsigned long long* tr) {
+                         double2* ring, const int2* sidx, unsigned long long* tr, bool zlive) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const BwdRange rg = bwd_range(J, g, it);
   const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
@@ -529,7 +535,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const int row = row_of(s);
     const double2* src = nullptr;
     if (row < J.k)
-      src = Z + static_cast<long long>(row) * R;
+      src = zlive ? Z + static_cast<long long>(row) * R : nullptr;  // structurally zero front: z = 0
     else if (row >= g.kp && row - g.kp < nb)
       src = J.x + static_cast<long long>(sidx[row - 8 * a0].x) * R;
 #pragma unroll
@@ -616,25 +622,38 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
       unsigned long long* tr = a.trace ? a.trace + 8LL * cur : nullptr;
       if (tr && lane == 0) tr[0] = gtime();
       const SolveJob J = a.jobs[it.job];
-      const Geo g = geo_km(J.k, J.m);
-      item_prefetch<FWD>(a, J, g, it, sidx, lane);
-      if (FWD) {
-        if (J.child0 >= 0) wait_count(done + J.child0, J.tgt_c0, lane);
-        if (J.child1 >= 0) wait_count(done + J.child1, J.tgt_c1, lane);
-      } else if (J.parent >= 0) {
-        wait_count(done + J.parent, J.tgt_p, lane);
-      }
-      cp_wait<0>();
-      __syncwarp();
-      if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
-      double2* V = a.vbuf + it.slot * a.vslot_stride;
-      if (FWD)
-        fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr) : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr);
-      else
-        fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr) : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr);
-      if (tr && lane == 0) {
-        tr[4] = gtime();
-        tr[5] = smid();
+      // live fronts: past sweep 1 the right-hand side is zero off the injection lines of the faces
+      // that received traces; a front whose subtree holds none of them has T = z = V = 0 exactly.
+      // Its forward items are skipped (nothing waits for them: a live parent ignores the child),
+      // and its backward items read z = 0.
+      const unsigned fm = a.tface ? a.tface[it.nzi] : kAllLive;  // kAllLive: sweep 1 (split source)
+      const unsigned act = static_cast<unsigned>(J.act);
+      const bool all = (fm & kAllLive) != 0;
+      const bool live = all || (act & fm & 0xFFu) != 0;
+      if (!FWD || live) {
+        const unsigned clive = (all || ((act >> 8) & fm & 0xFFu) ? 1u : 0u) | (all || ((act >> 16) & fm & 0xFFu) ? 2u : 0u);
+        const Geo g = geo_km(J.k, J.m);
+        item_prefetch<FWD>(a, J, g, it, sidx, lane);
+        if (FWD) {
+          if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
+          if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
+        } else if (J.parent >= 0) {
+          wait_count(done + J.parent, J.tgt_p, lane);
+        }
+        cp_wait<0>();
+        __syncwarp();
+        if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
+        double2* V = a.vbuf + it.slot * a.vslot_stride;
+        if (FWD)
+          fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr, clive)
+                          : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr, clive);
+        else
+          fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr, live)
+                          : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr, live);
+        if (tr && lane == 0) {
+          tr[4] = gtime();
+          tr[5] = smid();
+        }
       }
     }
     const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
