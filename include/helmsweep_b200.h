@@ -183,9 +183,11 @@ int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double* u, hs_fact
 /* Device profile of the most recent timed hs_ddm_solve[_device] batch: total duration of the
  * multifrontal solve launches (forward + backward, CUDA events), their count, the subdomain
  * solves they executed, and the algorithmic bytes / flops of those solves (SURVEY.md §8(d):
- * per solve (P_f + P)*16 + 2*R*N_loc*16 bytes and 8*(P_f + P)*R flops, P = packed factor
- * entries, P_f = those of the fronts the forward pass needs: all of them in sweep 1, past it
- * only fronts whose subtree holds a nonzero injection line -- the others are exactly zero). */
+ * per solve (P_f + P_b)*16 + 2*R*N_loc*16 bytes and 8*(P_f + P_b)*R flops over packed factor
+ * entries: P_f those of the fronts the forward pass needs -- all of them in sweep 1, past it
+ * only fronts whose subtree holds a nonzero injection line, the others being exactly zero --
+ * and P_b those of the fronts whose subtree holds a position the application reads back,
+ * accumulated with a nonzero weight or extracted as a trace). */
 int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, int64_t* subdomain_solves,
                    double* alg_bytes, double* alg_flops);
 /* Route table of the reference's route_trace (src/sweeper.cpp:58-73): target sweep of a

@@ -94,6 +94,8 @@ struct ClassDev {
   std::vector<int> fkc, fkr;   // per front split-K chunk (column blocks / block rows)
   std::vector<int> fgw;        // per front RHS group width (8 on the critical path, else 16)
   std::vector<unsigned> fbits; // per front: faces whose injection lines lie in its subtree
+  std::vector<int> front_of_pos;  // elimination position -> front whose separator holds it
+  std::vector<int> ext_pos;       // elimination positions of every trace-extraction line
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   DBuf<unsigned char> on_line;
   std::vector<int> level_start_down;
@@ -166,7 +168,9 @@ struct Engine {
       return false;
     };
     std::vector<unsigned char> fl(c.n, 0);
-    std::vector<int> front_of_pos;
+    std::vector<int>& front_of_pos = cd.front_of_pos;
+    front_of_pos.clear();
+    cd.ext_pos.clear();
     for (int d = 0; d < 2 * c.dim; ++d) {
       const int a = d / 2, sign = (d & 1) ? 1 : -1;
       GridRange line = loc;
@@ -199,6 +203,8 @@ struct Engine {
         if (p0[i] >= 0) fl[p0[i]] = 1;
         if (pm[i] >= 0) fl[pm[i]] = 1;
       }
+      cd.ext_pos.insert(cd.ext_pos.end(), u0.begin(), u0.end());
+      cd.ext_pos.insert(cd.ext_pos.end(), um1.begin(), um1.end());
       // fronts whose subtree holds an injection position of face d (the front owning the
       // position's separator slot and its ancestors)
       if (front_of_pos.empty()) {
@@ -614,7 +620,8 @@ struct Engine {
   // One forward and one backward launch over the items of a step group.
   DBuf<unsigned long long> trace;
   void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const unsigned* nzmask,
-                 bool traced = false, const unsigned* tface = nullptr) {
+                 bool traced = false, const unsigned* tface = nullptr, const unsigned* need = nullptr,
+                 int need_words = 0) {
     const long long per = static_cast<long long>(nslots) * nf_max;
     const long long arr = static_cast<long long>(nslots) * arr_total * ngr;
     HS_CUDA(cudaMemsetAsync(cnt.p, 0, cnt_ints() * sizeof(int), stream));
@@ -630,6 +637,9 @@ struct Engine {
     a.arr_stride = arr_total;
     a.nzmask = nzmask;
     a.tface = tface;
+    a.need = need;
+    a.need_words = need_words;
+    a.nsub = static_cast<int>(sub_cls.size());
     a.items = fwd;
     a.nitems = nfwd;
     a.done = cnt.p;
@@ -934,6 +944,12 @@ struct DdmHandle {
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
+  // per subdomain, a bitset over fronts: the front's subtree holds a position the application
+  // reads back (accumulated with a nonzero weight, or on a trace-extraction line); the backward
+  // pass skips the others, whose x nobody reads (the PML frame away from the support)
+  DBuf<unsigned> need;
+  int need_words = 0;
+  std::vector<unsigned> need_h;
   DBuf<int> split_gp;          // split-source plan per (subdomain, elimination position): global node
   DBuf<unsigned char> split_w; // and weight numerator (0: shell or outside the support)
   DBuf<double2> d_coef;
@@ -1313,6 +1329,28 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
       if (off[g] >= E) throw Error(kInternal, "accumulate plan: more than 2^dim subdomains at a node");
       raw[static_cast<size_t>(g) * E + off[g]++] = make_int2(static_cast<int>(eng.n_base[id] + e), (id << 4) | num);
     });
+    {  // fronts whose x is read back: support positions with a nonzero weight and extraction lines
+      int nfm = 1;
+      for (auto& cdp : eng.classes) nfm = std::max(nfm, static_cast<int>(cdp->sym->fronts.size()));
+      need_words = (nfm + 31) / 32;
+      need_h.assign(static_cast<size_t>(nsub) * need_words, 0u);
+      auto mark = [&](int id, int e) {
+        const ClassDev& cd = *eng.classes[subs[id].cls];
+        unsigned* w = need_h.data() + static_cast<size_t>(id) * need_words;
+        for (int f = cd.front_of_pos.empty() ? -1 : cd.front_of_pos[e]; f >= 0 && !(w[f >> 5] >> (f & 31) & 1u);
+             f = cd.sym->fronts[f].parent)
+          w[f >> 5] |= 1u << (f & 31);
+      };
+      for (long long g = 0; g < gn; ++g)
+        for (int i = 0; i < off[g]; ++i) {
+          const int2 en = raw[static_cast<size_t>(g) * E + i];
+          const int id = en.y >> 4;
+          mark(id, static_cast<int>(en.x - eng.n_base[id]));
+        }
+      for (int id = 0; id < nsub; ++id)
+        for (int e : eng.classes[subs[id].cls]->ext_pos) mark(id, e);
+      need.upload(need_h, eng.stream);
+    }
     // one plan per sweep direction, entries in the reference's order: step, then ascending id
     const std::vector<Vec3i> dplan = sweep_plan(dim, 1);
     std::vector<int> stab(static_cast<size_t>(ndirs) * nsub);
@@ -1677,6 +1715,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
   const int nm = static_cast<int>(msteps.size());
   int waited = -1, stripes_done = 0;
   bool u_reduced = false;
+  static const bool no_skip = std::getenv("HS_NO_FRONT_SKIP") != nullptr;  // developer A/B switch
   auto stage_in = [&](int upto) {  // stripes (waited, upto] of b: copied -> transposed into bN
     for (int j = waited + 1; j <= upto; ++j) {
       HS_CUDA(cudaStreamWaitEvent(s, io->copied[j], 0));
@@ -1703,7 +1742,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
     if (sa.ntasks > 0)
       eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced,
-                    std::getenv("HS_NO_FRONT_SKIP") ? nullptr : tface.p);
+                    no_skip ? nullptr : tface.p, no_skip ? nullptr : need.p, need_words);
     if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
     if (sa.ntasks > 0) launch_extract_deposit(sa, static_cast<int>(line_max), s);
     if (partitioned() && !xplan[m].peers.empty()) {  // traces and ghost values to / from other ranks
@@ -2409,6 +2448,19 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
       }
       return p;
     };
+    // ... and the backward pass over the fronts whose x the application reads back
+    auto needed_packed = [&](int sub) {
+      const ClassDev& cd = *H.eng.classes[H.subs[sub].cls];
+      if (H.need_h.empty()) return static_cast<double>(cd.sym->packed_entries);
+      const unsigned* w = H.need_h.data() + static_cast<size_t>(sub) * H.need_words;
+      double p = 0.0;
+      for (size_t f = 0; f < cd.sym->fronts.size(); ++f) {
+        if (!(w[f >> 5] >> (f & 31) & 1u)) continue;
+        const double m = cd.sym->fronts[f].m, k = cd.sym->fronts[f].k;
+        p += m * k - k * (k - 1) / 2;
+      }
+      return p;
+    };
     double sec = 0.0, bytes = 0.0, flops = 0.0;
     int64_t launches = 0, solves = 0;
     float ms = 0.f;
@@ -2420,9 +2472,10 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
         if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
         const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
         const double pf = live_packed(H.subs[t.x].cls, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
+        const double pb = needed_packed(t.x);
         ++solves;
-        bytes += (pf + c.packed_entries) * 16 + 2.0 * H.R * c.n * 16;
-        flops += 8.0 * (pf + c.packed_entries) * H.R;
+        bytes += (pf + pb) * 16 + 2.0 * H.R * c.n * 16;
+        flops += 8.0 * (pf + pb) * H.R;
       }
     }
     if (solve_seconds) *solve_seconds = sec;

@@ -24,6 +24,9 @@ struct SolveArgs {
   const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
   const unsigned* tface;   // per task: faces with nonzero injected data, 0x100 = every front live
                            // (sweep 1); null = every front live
+  const unsigned* need;    // per subdomain bitset over fronts: x read back (backward pass); null = all
+  int need_words;          // 32-bit words per subdomain in `need`
+  int nsub;                // subdomains (task index nzi = (sweep - 1) * nsub + sub)
 };
 
 // Multifrontal forward (z = D^-1 L^-1 b) or backward (x = L^-T z) pass over the work items of

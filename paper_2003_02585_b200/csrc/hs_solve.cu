@@ -630,7 +630,14 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
       const unsigned act = static_cast<unsigned>(J.act);
       const bool all = (fm & kAllLive) != 0;
       const bool live = all || (act & fm & 0xFFu) != 0;
-      if (!FWD || live) {
+      // backward: a front whose subtree holds no position the application reads back (PML frame
+      // away from the support and the extraction lines) is skipped, and so is its subtree
+      bool needed = true;
+      if (!FWD && a.need) {
+        const int sub = it.nzi % a.nsub;
+        needed = (a.need[static_cast<long long>(sub) * a.need_words + (it.front >> 5)] >> (it.front & 31)) & 1u;
+      }
+      if (FWD ? live : needed) {
         const unsigned clive = (all || ((act >> 8) & fm & 0xFFu) ? 1u : 0u) | (all || ((act >> 16) & fm & 0xFFu) ? 2u : 0u);
         const Geo g = geo_km(J.k, J.m);
         item_prefetch<FWD>(a, J, g, it, sidx, lane);
