@@ -255,6 +255,11 @@ constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 #endif
 // Forward items also stage, per band row, the extend-add source of boundary rows (int2) and
 // 1/d of separator rows (double2), so their finalize issues no dependent loads.
+#ifndef HS_KUNROLL
+#define HS_KUNROLL 1
+#endif
+constexpr int kKUnroll = HS_KUNROLL;  // k-loop unroll (tuning experiments)
+
 template <bool FWD>
 struct Ring {
   static constexpr int NS = FWD ? HS_NS_FWD : HS_NS_BWD;
@@ -276,7 +281,7 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
     if (j < ns) issue(j, ring + j * ST);
     cp_commit();
   }
-#pragma unroll 1
+#pragma unroll kKUnroll
   for (int s = 0; s < ns; ++s) {
     const int si = s + NS - 1;
     if (si < ns) issue(si, ring + (si % NS) * ST);

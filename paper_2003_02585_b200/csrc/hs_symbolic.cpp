@@ -241,6 +241,37 @@ std::unique_ptr<SymbolicClass> build_symbolic(int dim, const GridRange& range,
   }
   c.fac_total = fac;
   c.v_total = v;
+  // Dense front workspaces (m x m each) live from their front's level (assembly, elimination)
+  // to their parent's level (extend-add of the Schur complement), the device factorizing one tree
+  // height at a time. Fronts whose lifetimes overlap get disjoint ranges: first fit, largest
+  // first. The workspace is the peak over heights instead of the sum over all fronts (3D 57^3
+  // subdomains: about 6x less), so more subdomains are factorized side by side.
+  {
+    std::vector<int> ord(nf);
+    std::iota(ord.begin(), ord.end(), 0);
+    auto sz = [&](int f) { return static_cast<long long>(c.fronts[f].m) * c.fronts[f].m; };
+    auto life_hi = [&](int f) { return c.fronts[f].parent >= 0 ? c.fronts[c.fronts[f].parent].height : c.fronts[f].height; };
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return sz(a) > sz(b); });
+    std::vector<int> placed;
+    std::vector<std::pair<long long, long long>> busy;
+    long long top = 0;
+    for (int f : ord) {
+      const int lo = c.fronts[f].height, hi = life_hi(f);
+      busy.clear();
+      for (int g : placed)
+        if (c.fronts[g].height <= hi && lo <= life_hi(g)) busy.emplace_back(c.fronts[g].f_off, c.fronts[g].f_off + sz(g));
+      std::sort(busy.begin(), busy.end());
+      long long off = 0;
+      for (const auto& iv : busy) {
+        if (iv.first >= off + sz(f)) break;
+        off = std::max(off, iv.second);
+      }
+      c.fronts[f].f_off = off;
+      top = std::max(top, off + sz(f));
+      placed.push_back(f);
+    }
+    fw = top;
+  }
   c.f_total = fw;
   c.t_total = tt;
   c.peak_bytes = peak;
