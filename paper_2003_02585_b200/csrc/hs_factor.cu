@@ -114,7 +114,8 @@ __device__ __forceinline__ void stage_opnd(double2* s, const Opnd& o, int k0, in
   }
 }
 
-// acc[u][v] (rows tx + 16u, columns ty + 16v) += A chunk * B chunk^T
+// acc[u][v] (rows tx + 16u, columns ty + 16v) += A chunk * B chunk^T (NEG: -=)
+template <bool NEG = false>
 __device__ __forceinline__ void mma_chunk(double2 (&acc)[4][4], const double2* sA, const double2* sB, int tx, int ty) {
 #pragma unroll 4
   for (int kk = 0; kk < kKC; ++kk) {
@@ -127,15 +128,31 @@ __device__ __forceinline__ void mma_chunk(double2 (&acc)[4][4], const double2* s
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) cfma(acc[u][v], a[u], b[v]);
+      for (int v = 0; v < 4; ++v) {
+        if (NEG)
+          cfms(acc[u][v], a[u], b[v]);
+        else
+          cfma(acc[u][v], a[u], b[v]);
+      }
   }
 }
 
-// The CTA's sequence of cnt tiles: get(q) describes tile q, epi(q, acc, tx, ty) consumes its
-// accumulators. Chunks stream through two cp.async stages; the next chunk (of this tile or the
+struct ZeroInit {
+  __device__ __forceinline__ void operator()(int, double2 (&acc)[4][4], int, int) const {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = make_double2(0.0, 0.0);
+  }
+};
+
+// The CTA's sequence of cnt tiles: get(q) describes tile q, init(q, acc, tx, ty) sets its
+// accumulators (zero, or C for an update C -= A B^T with NEG, so the epilogue only stores and
+// C's loads overlap the tile's first chunk instead of stalling the epilogue), epi(q, acc, tx, ty)
+// consumes them. Chunks stream through two cp.async stages; the next chunk (of this tile or the
 // next one) is in flight while the current one is multiplied.
-template <class Get, class Epi>
-__device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* stages, int tid) {
+template <bool NEG = false, class Get, class Epi, class Init = ZeroInit>
+__device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* stages, int tid, Init init = Init{}) {
   if (cnt <= 0) return;
   const int tx = tid & 15, ty = tid >> 4;
   int q = 0;
@@ -145,10 +162,7 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
   stage_opnd(stages + kKC * kSL, cur.b, c, cur.k1, tid);
   cp_commit();
   double2 acc[4][4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = czero();
+  init(0, acc, tx, ty);
   int sb = 0;
 #pragma unroll 1
   while (true) {
@@ -171,14 +185,11 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
     cp_commit();
     cp_wait1();
     __syncthreads();
-    mma_chunk(acc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, tx, ty);
+    mma_chunk<NEG>(acc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, tx, ty);
     __syncthreads();
     if (last_chunk) {
       epi(q, acc, tx, ty);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = czero();
+      if (has_next) init(nq, acc, tx, ty);
     }
     if (!has_next) break;
     q = nq;
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
         tc = tp - ti * (ti + 1) / 2;
       };
       const int cnt = ntiles > rank ? (ntiles - rank + NC - 1) / NC : 0;
-      gemm_tiles(
+      gemm_tiles<true>(
           cnt,
           [&](int q) {
             int ti, tc;
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
             t.k1 = nbw;
             return t;
           },
-          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          [&](int q, double2(&acc)[4][4], int tx, int ty) {  // F = acc = F - L (L D)^T
             int ti, tc;
             tile_of(q, ti, tc);
 #pragma unroll
@@ -421,16 +432,25 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int gi = ti * kTB + tx + 16 * u;
-                if (gi < rows2 && gi >= gj) {
-                  double2 y = col[gi];
-                  y.x -= acc[u][v].x;
-                  y.y -= acc[u][v].y;
-                  col[gi] = y;
-                }
+                if (gi < rows2 && gi >= gj) col[gi] = acc[u][v];
               }
             }
           },
-          region0, tid);
+          region0, tid,
+          [&](int q, double2(&acc)[4][4], int tx, int ty) {  // start from the F tile
+            int ti, tc;
+            tile_of(q, ti, tc);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const int gj = tc * kTB + ty + 16 * v;
+              const double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int gi = ti * kTB + tx + 16 * u;
+                acc[u][v] = (gj < rows2 && gi < rows2 && gi >= gj) ? col[gi] : czero();
+              }
+            }
+          });
     }
     sync_front();
   }
