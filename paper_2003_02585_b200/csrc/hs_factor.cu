@@ -35,6 +35,8 @@ namespace {
 
 constexpr int kT = 256;   // threads per CTA
 constexpr int kPB = 32;   // panel width of the LDL^T
+constexpr int kOB = 128;  // outer block: panels update only the block's columns, the rest of the
+                          // front is updated once per block (a 128-deep GEMM) instead of per panel
 constexpr int kTB = 64;   // GEMM tile (rows and columns)
 constexpr int kKC = 32;   // GEMM k-chunk
 constexpr int kSL = 65;   // shared leading dimension (double2) of staged chunks: conflict-free transposed stores
@@ -276,9 +278,9 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
   const int m = f.m, k = f.k;
   double2* F = a.work + task.fbase + f.f_off;
   const long long mm = static_cast<long long>(m) * m;
-  // scratch of the cluster: (L D) of the panel (m x kPB), T (64 x k), L_II^-1 per CTA (64 x 64)
+  // scratch of the cluster: (L D) of the outer block (m x kOB), T (64 x k), L_II^-1 per CTA (64 x 64)
   double2* Ws = a.scratch + (blockIdx.x / NC) * scratch_stride;
-  double2* Tb = Ws + static_cast<long long>(m) * kPB;
+  double2* Tb = Ws + static_cast<long long>(m) * kOB;
   double2* Li = Tb + static_cast<long long>(64) * k + rank * 4096;
 
   // ---- assembly (src/direct.cpp:219-265)
@@ -311,9 +313,14 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
     sync_front();
   }
 
-  // ---- 1. panel LDL^T with trailing GEMM updates (src/direct.cpp:55-87)
+  // ---- 1. panel LDL^T with GEMM updates (src/direct.cpp:55-87), outer blocks of kOB columns:
+  // each panel updates the rest of its outer block, each outer block the rest of the front
 #pragma unroll 1
-  for (int p0 = 0; p0 < k; p0 += kPB) {
+  for (int B0 = 0; B0 < k; B0 += kOB) {
+  const int B1 = min(k, B0 + kOB);
+  const long long ldw = m - B0;  // Ws(r, c) = (L D)[B0 + r, B0 + c]
+#pragma unroll 1
+  for (int p0 = B0; p0 < B1; p0 += kPB) {
     const int nbw = min(kPB, k - p0), p1 = p0 + nbw, rows2 = m - p1;
     // (a) diagonal block, every CTA
     for (int idx = tid; idx < kPB * kPB; idx += kT) {
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
       for (int c = 0; c < 16; ++c)
         if (c < nbw) {
           F[static_cast<long long>(p0 + c) * m + i] = x[c];
-          Ws[(i - p1) + static_cast<long long>(c) * rows2] = cmul(x[c], sDd[c]);
+          Ws[(i - B0) + static_cast<long long>(p0 - B0 + c) * ldw] = cmul(x[c], sDd[c]);
         }
       if (nbw > 16) {
 #pragma unroll
@@ -388,46 +395,48 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
         for (int c = 0; c < 16; ++c)
           if (16 + c < nbw) {
             F[static_cast<long long>(p0 + 16 + c) * m + i] = x[c];
-            Ws[(i - p1) + static_cast<long long>(16 + c) * rows2] = cmul(x[c], sDd[16 + c]);
+            Ws[(i - B0) + static_cast<long long>(p0 - B0 + 16 + c) * ldw] = cmul(x[c], sDd[16 + c]);
           }
       }
     }
     sync_front();
-    // (c) diagonal block back (rank 0); trailing lower update F[p1:, p1:] -= L (L D)^T
+    // (c) diagonal block back (rank 0); update of the rest of the outer block,
+    // F[p1:, p1:B1] -= L[p1:, p0:p1] (L D)[p1:B1, p0:p1]^T (lower part)
     if (rank == 0)
       for (int idx = tid; idx < kPB * kPB; idx += kT) {
         const int r = idx & 31, c = idx >> 5;
         if (r < nbw && c <= r) F[static_cast<long long>(p0 + c) * m + p0 + r] = sD[r * kDL + c];
       }
-    if (rows2 > 0) {
-      const int nt = (rows2 + kTB - 1) / kTB, ntiles = nt * (nt + 1) / 2;
-      auto tile_of = [&](int q, int& ti, int& tc) {
-        const int tp = rank + NC * q;
-        ti = static_cast<int>((sqrt(8.0 * tp + 1.0) - 1.0) * 0.5);
-        while (ti * (ti + 1) / 2 > tp) --ti;
-        while ((ti + 1) * (ti + 2) / 2 <= tp) ++ti;
-        tc = tp - ti * (ti + 1) / 2;
-      };
+    if (p1 < B1) {
+      const int ncol = B1 - p1, nti = (rows2 + kTB - 1) / kTB, ntj = (ncol + kTB - 1) / kTB;
+      const int ntiles = nti * ntj;  // tiles above the diagonal (ti < tj) hold no lower entries
       const int cnt = ntiles > rank ? (ntiles - rank + NC - 1) / NC : 0;
+      auto tile_of = [&](int q, int& ti, int& tj) {
+        const int tp = rank + NC * q;
+        ti = tp / ntj;
+        tj = tp % ntj;
+      };
       gemm_tiles<true>(
           cnt,
           [&](int q) {
-            int ti, tc;
-            tile_of(q, ti, tc);
+            int ti, tj;
+            tile_of(q, ti, tj);
             Tile t;
-            t.a = Opnd{F + static_cast<long long>(p0) * m + p1 + ti * kTB, m, 0, min(kTB, rows2 - ti * kTB)};
-            t.b = Opnd{Ws + tc * kTB, rows2, 0, min(kTB, rows2 - tc * kTB)};
+            t.a = Opnd{F + static_cast<long long>(p0) * m + p1 + ti * kTB, m, 0, ti < tj ? 0 : min(kTB, rows2 - ti * kTB)};
+            t.b = Opnd{Ws + (p1 - B0) + tj * kTB + static_cast<long long>(p0 - B0) * ldw, ldw, 0,
+                       min(kTB, ncol - tj * kTB)};
             t.k0 = 0;
-            t.k1 = nbw;
+            t.k1 = ti < tj ? 0 : nbw;
             return t;
           },
-          [&](int q, double2(&acc)[4][4], int tx, int ty) {  // F = acc = F - L (L D)^T
-            int ti, tc;
-            tile_of(q, ti, tc);
+          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+            int ti, tj;
+            tile_of(q, ti, tj);
+            if (ti < tj) return;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-              const int gj = tc * kTB + ty + 16 * v;
-              if (gj >= rows2) continue;
+              const int gj = tj * kTB + ty + 16 * v;
+              if (gj >= ncol) continue;
               double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -437,22 +446,79 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
             }
           },
           region0, tid,
-          [&](int q, double2(&acc)[4][4], int tx, int ty) {  // start from the F tile
-            int ti, tc;
-            tile_of(q, ti, tc);
+          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+            int ti, tj;
+            tile_of(q, ti, tj);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-              const int gj = tc * kTB + ty + 16 * v;
+              const int gj = tj * kTB + ty + 16 * v;
               const double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int gi = ti * kTB + tx + 16 * u;
-                acc[u][v] = (gj < rows2 && gi < rows2 && gi >= gj) ? col[gi] : czero();
+                acc[u][v] = (ti >= tj && gj < ncol && gi < rows2 && gi >= gj) ? col[gi] : czero();
               }
             }
           });
     }
     sync_front();
+  }
+  // (d) the rest of the front, F[B1:, B1:] -= L[B1:, B0:B1] (L D)[B1:, B0:B1]^T (lower triangle)
+  if (B1 < m) {
+    const int rows2 = m - B1;
+    const int nt = (rows2 + kTB - 1) / kTB, ntiles = nt * (nt + 1) / 2;
+    auto tile_of = [&](int q, int& ti, int& tc) {
+      const int tp = rank + NC * q;
+      ti = static_cast<int>((sqrt(8.0 * tp + 1.0) - 1.0) * 0.5);
+      while (ti * (ti + 1) / 2 > tp) --ti;
+      while ((ti + 1) * (ti + 2) / 2 <= tp) ++ti;
+      tc = tp - ti * (ti + 1) / 2;
+    };
+    const int cnt = ntiles > rank ? (ntiles - rank + NC - 1) / NC : 0;
+    gemm_tiles<true>(
+        cnt,
+        [&](int q) {
+          int ti, tc;
+          tile_of(q, ti, tc);
+          Tile t;
+          t.a = Opnd{F + static_cast<long long>(B0) * m + B1 + ti * kTB, m, 0, min(kTB, rows2 - ti * kTB)};
+          t.b = Opnd{Ws + (B1 - B0) + tc * kTB, ldw, 0, min(kTB, rows2 - tc * kTB)};
+          t.k0 = 0;
+          t.k1 = B1 - B0;
+          return t;
+        },
+        [&](int q, double2(&acc)[4][4], int tx, int ty) {  // F = acc = F - L (L D)^T
+          int ti, tc;
+          tile_of(q, ti, tc);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int gj = tc * kTB + ty + 16 * v;
+            if (gj >= rows2) continue;
+            double2* col = F + static_cast<long long>(B1 + gj) * m + B1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int gi = ti * kTB + tx + 16 * u;
+              if (gi < rows2 && gi >= gj) col[gi] = acc[u][v];
+            }
+          }
+        },
+        region0, tid,
+        [&](int q, double2(&acc)[4][4], int tx, int ty) {  // start from the F tile
+          int ti, tc;
+          tile_of(q, ti, tc);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int gj = tc * kTB + ty + 16 * v;
+            const double2* col = F + static_cast<long long>(B1 + gj) * m + B1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int gi = ti * kTB + tx + 16 * u;
+              acc[u][v] = (gj < rows2 && gi < rows2 && gi >= gj) ? col[gi] : czero();
+            }
+          }
+        });
+  }
+  sync_front();
   }
 
   // ---- 2. D^-1 (kept per node for the solve) and unit diagonal for the inversion
@@ -586,7 +652,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
 }  // namespace
 
 long long factor_big_scratch(int max_m) {  // per cluster, double2 entries
-  return static_cast<long long>(max_m) * kPB + static_cast<long long>(64) * max_m + static_cast<long long>(kFactorCluster) * 4096;
+  return static_cast<long long>(max_m) * kOB + static_cast<long long>(64) * max_m + static_cast<long long>(kFactorCluster) * 4096;
 }
 
 void launch_factor_big(const FactorArgs& a, int max_m, cudaStream_t s) {
