@@ -139,6 +139,86 @@ __device__ __forceinline__ void mma_chunk(double2 (&acc)[4][4], const double2* s
   }
 }
 
+// FP64 tensor-core path of the tile GEMM (mma.sync m8n8k4 f64 = SASS DMMA): warp w owns the
+// 32 x 16 complex sub-tile (rows 32 (w & 1), columns 16 (w >> 1)) as 4 x 2 blocks of 8 x 8, complex
+// arithmetic as four real products (the solve kernel's mma_step); one DMMA replaces 256 DFMAs
+// of issue. Accumulators cross to the (tx, ty) layout of the epilogues through shared memory.
+#ifndef HS_FACTOR_DMMA
+#define HS_FACTOR_DMMA 1
+#endif
+struct DAcc {
+  double v[4][2][2][2];  // m-tile i, n-tile q, re/im, element e
+};
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+template <bool NEG>
+__device__ __forceinline__ void dmma_chunk(DAcc& c, const double2* sA, const double2* sB, int lane, int warp) {
+  const int r0 = 32 * (warp & 1) + (lane >> 2), c0 = 16 * (warp >> 1) + (lane >> 2);
+#pragma unroll 2
+  for (int ks = 0; ks < kKC / 4; ++ks) {
+    const int kk = 4 * ks + (lane & 3);
+    double2 A[4], B[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) A[i] = sA[kk * kSL + r0 + 8 * i];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) B[q] = sB[kk * kSL + c0 + 8 * q];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double bx = NEG ? -B[q].x : B[q].x, by = NEG ? -B[q].y : B[q].y, nby = NEG ? B[q].y : -B[q].y;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, by);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nby);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, bx);
+      }
+    }
+  }
+}
+constexpr int kTL = 65;  // leading dimension of the 64 x 64 transposition tile (double2)
+// DMMA fragments <-> the (tx, ty) layout (rows tx + 16u, columns ty + 16v) through shared memory
+__device__ __forceinline__ void dacc_to_smem(const DAcc& c, double2* T, int lane, int warp) {
+  const int r0 = 32 * (warp & 1) + (lane >> 2), c0 = 16 * (warp >> 1) + 2 * (lane & 3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) T[(c0 + 8 * q + e) * kTL + r0 + 8 * i] = make_double2(c.v[i][q][0][e], c.v[i][q][1][e]);
+}
+__device__ __forceinline__ void smem_to_dacc(DAcc& c, const double2* T, int lane, int warp) {
+  const int r0 = 32 * (warp & 1) + (lane >> 2), c0 = 16 * (warp >> 1) + 2 * (lane & 3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double2 v = T[(c0 + 8 * q + e) * kTL + r0 + 8 * i];
+        c.v[i][q][0][e] = v.x;
+        c.v[i][q][1][e] = v.y;
+      }
+}
+__device__ __forceinline__ void smem_to_acc(double2 (&acc)[4][4], const double2* T, int tx, int ty) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = T[(ty + 16 * v) * kTL + tx + 16 * u];
+}
+__device__ __forceinline__ void acc_to_smem(const double2 (&acc)[4][4], double2* T, int tx, int ty) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) T[(ty + 16 * v) * kTL + tx + 16 * u] = acc[u][v];
+}
+static_assert(64 * kTL <= kKC * kSL * 2, "transposition tile fits one stage");
+
 struct ZeroInit {
   __device__ __forceinline__ void operator()(int, double2 (&acc)[4][4], int, int) const {
 #pragma unroll
@@ -165,6 +245,17 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
   cp_commit();
   double2 acc[4][4];
   init(0, acc, tx, ty);
+#if HS_FACTOR_DMMA
+  const int lane = tid & 31, warp = tid >> 5;
+  DAcc dacc;
+  {  // the first tile's start values through the free stage
+    double2* T = stages + kStage;
+    acc_to_smem(acc, T, tx, ty);
+    __syncthreads();
+    smem_to_dacc(dacc, T, lane, warp);
+    __syncthreads();
+  }
+#endif
   int sb = 0;
 #pragma unroll 1
   while (true) {
@@ -187,12 +278,32 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
     cp_commit();
     cp_wait1();
     __syncthreads();
+#if HS_FACTOR_DMMA
+    dmma_chunk<NEG>(dacc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, lane, warp);
+    __syncthreads();
+    if (last_chunk) {  // stage sb is free: the next tile's first chunk is in flight in sb ^ 1
+      double2* T = stages + sb * kStage;
+      dacc_to_smem(dacc, T, lane, warp);
+      __syncthreads();
+      smem_to_acc(acc, T, tx, ty);
+      epi(q, acc, tx, ty);
+      if (has_next) {
+        init(nq, acc, tx, ty);
+        __syncthreads();
+        acc_to_smem(acc, T, tx, ty);
+        __syncthreads();
+        smem_to_dacc(dacc, T, lane, warp);
+      }
+      __syncthreads();
+    }
+#else
     mma_chunk<NEG>(acc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, tx, ty);
     __syncthreads();
     if (last_chunk) {
       epi(q, acc, tx, ty);
       if (has_next) init(nq, acc, tx, ty);
     }
+#endif
     if (!has_next) break;
     q = nq;
     c = nc;
