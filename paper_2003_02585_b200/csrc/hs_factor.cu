@@ -219,6 +219,41 @@ __device__ __forceinline__ void acc_to_smem(const double2 (&acc)[4][4], double2*
 }
 static_assert(64 * kTL <= kKC * kSL * 2, "transposition tile fits one stage");
 
+// Load (STORE = false; element missing -> 0) or store the tile's elements through addr(r, c)
+// (nullptr: not part of the tile) in either accumulator layout.
+template <bool STORE, class Addr>
+__device__ __forceinline__ void tile_rw(double2 (&acc)[4][4], int tx, int ty, Addr addr) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double2* p = addr(tx + 16 * u, ty + 16 * v);
+      if (STORE) {
+        if (p) *p = acc[u][v];
+      } else {
+        acc[u][v] = p ? *p : make_double2(0.0, 0.0);
+      }
+    }
+}
+template <bool STORE, class Addr>
+__device__ __forceinline__ void tile_rw(DAcc& c, int r0, int c0, Addr addr) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double2* p = addr(r0 + 8 * i, c0 + 8 * q + e);
+        if (STORE) {
+          if (p) *p = make_double2(c.v[i][q][0][e], c.v[i][q][1][e]);
+        } else {
+          const double2 v = p ? *p : make_double2(0.0, 0.0);
+          c.v[i][q][0][e] = v.x;
+          c.v[i][q][1][e] = v.y;
+        }
+      }
+}
+
 struct ZeroInit {
   __device__ __forceinline__ void operator()(int, double2 (&acc)[4][4], int, int) const {
 #pragma unroll
@@ -233,7 +268,9 @@ struct ZeroInit {
 // C's loads overlap the tile's first chunk instead of stalling the epilogue), epi(q, acc, tx, ty)
 // consumes them. Chunks stream through two cp.async stages; the next chunk (of this tile or the
 // next one) is in flight while the current one is multiplied.
-template <bool NEG = false, class Get, class Epi, class Init = ZeroInit>
+// FRAG (DMMA path): init / epi take the DMMA fragments directly, (q, dacc, r0, c0) with lane
+// element (i, q2, e) at tile row r0 + 8 i, column c0 + 8 q2 + e -- no transposition.
+template <bool NEG = false, bool FRAG = false, class Get, class Epi, class Init = ZeroInit>
 __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* stages, int tid, Init init = Init{}) {
   if (cnt <= 0) return;
   const int tx = tid & 15, ty = tid >> 4;
@@ -243,18 +280,24 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
   stage_opnd(stages, cur.a, c, cur.k1, tid);
   stage_opnd(stages + kKC * kSL, cur.b, c, cur.k1, tid);
   cp_commit();
-  double2 acc[4][4];
-  init(0, acc, tx, ty);
 #if HS_FACTOR_DMMA
   const int lane = tid & 31, warp = tid >> 5;
+  const int fr0 = 32 * (warp & 1) + (lane >> 2), fc0 = 16 * (warp >> 1) + 2 * (lane & 3);
   DAcc dacc;
-  {  // the first tile's start values through the free stage
+  double2 acc[4][4];
+  if constexpr (FRAG) {
+    init(0, dacc, fr0, fc0);
+  } else {  // the first tile's start values through the free stage
+    init(0, acc, tx, ty);
     double2* T = stages + kStage;
     acc_to_smem(acc, T, tx, ty);
     __syncthreads();
     smem_to_dacc(dacc, T, lane, warp);
     __syncthreads();
   }
+#else
+  double2 acc[4][4];
+  init(0, acc, tx, ty);
 #endif
   int sb = 0;
 #pragma unroll 1
@@ -281,7 +324,12 @@ __device__ __forceinline__ void gemm_tiles(int cnt, Get get, Epi epi, double2* s
 #if HS_FACTOR_DMMA
     dmma_chunk<NEG>(dacc, stages + sb * kStage, stages + sb * kStage + kKC * kSL, lane, warp);
     __syncthreads();
-    if (last_chunk) {  // stage sb is free: the next tile's first chunk is in flight in sb ^ 1
+    if constexpr (FRAG) {
+      if (last_chunk) {
+        epi(q, dacc, fr0, fc0);
+        if (has_next) init(nq, dacc, fr0, fc0);
+      }
+    } else if (last_chunk) {  // stage sb is free: the next tile's first chunk is in flight in sb ^ 1
       double2* T = stages + sb * kStage;
       dacc_to_smem(dacc, T, lane, warp);
       __syncthreads();
@@ -527,7 +575,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
         ti = tp / ntj;
         tj = tp % ntj;
       };
-      gemm_tiles<true>(
+      gemm_tiles<true, HS_FACTOR_DMMA != 0>(
           cnt,
           [&](int q) {
             int ti, tj;
@@ -540,36 +588,24 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
             t.k1 = ti < tj ? 0 : nbw;
             return t;
           },
-          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          [&](int q, auto& acc, int tx, int ty) {  // F = acc = F - L (L D)^T, lower part
             int ti, tj;
             tile_of(q, ti, tj);
             if (ti < tj) return;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int gj = tj * kTB + ty + 16 * v;
-              if (gj >= ncol) continue;
-              double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int gi = ti * kTB + tx + 16 * u;
-                if (gi < rows2 && gi >= gj) col[gi] = acc[u][v];
-              }
-            }
+            tile_rw<true>(acc, tx, ty, [&](int r, int c) -> double2* {
+              const int gi = ti * kTB + r, gj = tj * kTB + c;
+              return (gj < ncol && gi < rows2 && gi >= gj) ? F + static_cast<long long>(p1 + gj) * m + p1 + gi : nullptr;
+            });
           },
           region0, tid,
-          [&](int q, double2(&acc)[4][4], int tx, int ty) {
+          [&](int q, auto& acc, int tx, int ty) {  // start from the F tile
             int ti, tj;
             tile_of(q, ti, tj);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int gj = tj * kTB + ty + 16 * v;
-              const double2* col = F + static_cast<long long>(p1 + gj) * m + p1;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int gi = ti * kTB + tx + 16 * u;
-                acc[u][v] = (ti >= tj && gj < ncol && gi < rows2 && gi >= gj) ? col[gi] : czero();
-              }
-            }
+            tile_rw<false>(acc, tx, ty, [&](int r, int c) -> double2* {
+              const int gi = ti * kTB + r, gj = tj * kTB + c;
+              return (ti >= tj && gj < ncol && gi < rows2 && gi >= gj) ? F + static_cast<long long>(p1 + gj) * m + p1 + gi
+                                                                       : nullptr;
+            });
           });
     }
     sync_front();
@@ -586,7 +622,7 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
       tc = tp - ti * (ti + 1) / 2;
     };
     const int cnt = ntiles > rank ? (ntiles - rank + NC - 1) / NC : 0;
-    gemm_tiles<true>(
+    gemm_tiles<true, HS_FACTOR_DMMA != 0>(
         cnt,
         [&](int q) {
           int ti, tc;
@@ -598,35 +634,22 @@ __global__ void __launch_bounds__(kT, 1) factor_big_kernel(FactorArgs a, long lo
           t.k1 = B1 - B0;
           return t;
         },
-        [&](int q, double2(&acc)[4][4], int tx, int ty) {  // F = acc = F - L (L D)^T
+        [&](int q, auto& acc, int tx, int ty) {  // F = acc = F - L (L D)^T, lower triangle
           int ti, tc;
           tile_of(q, ti, tc);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int gj = tc * kTB + ty + 16 * v;
-            if (gj >= rows2) continue;
-            double2* col = F + static_cast<long long>(B1 + gj) * m + B1;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int gi = ti * kTB + tx + 16 * u;
-              if (gi < rows2 && gi >= gj) col[gi] = acc[u][v];
-            }
-          }
+          tile_rw<true>(acc, tx, ty, [&](int r, int c) -> double2* {
+            const int gi = ti * kTB + r, gj = tc * kTB + c;
+            return (gj < rows2 && gi < rows2 && gi >= gj) ? F + static_cast<long long>(B1 + gj) * m + B1 + gi : nullptr;
+          });
         },
         region0, tid,
-        [&](int q, double2(&acc)[4][4], int tx, int ty) {  // start from the F tile
+        [&](int q, auto& acc, int tx, int ty) {  // start from the F tile
           int ti, tc;
           tile_of(q, ti, tc);
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int gj = tc * kTB + ty + 16 * v;
-            const double2* col = F + static_cast<long long>(B1 + gj) * m + B1;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int gi = ti * kTB + tx + 16 * u;
-              acc[u][v] = (gj < rows2 && gi < rows2 && gi >= gj) ? col[gi] : czero();
-            }
-          }
+          tile_rw<false>(acc, tx, ty, [&](int r, int c) -> double2* {
+            const int gi = ti * kTB + r, gj = tc * kTB + c;
+            return (gj < rows2 && gi < rows2 && gi >= gj) ? F + static_cast<long long>(B1 + gj) * m + B1 + gi : nullptr;
+          });
         });
   }
   sync_front();
