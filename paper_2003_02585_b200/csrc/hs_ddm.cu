@@ -1469,7 +1469,9 @@ void DdmHandle::build_schedule() {
     const int la = dim - 1;
     long long plane = 1;
     for (int a = 0; a < la; ++a) plane *= geom.gsize[a];
-    const int rows = geom.gsize[la], ns = std::max(1, std::min(rows, 2 * part.counts[la]));
+    int spr = 2;  // stripes per subdomain row (HS_STRIPES_PER_ROW: developer knob)
+    if (const char* e = std::getenv("HS_STRIPES_PER_ROW")) spr = std::max(1, std::atoi(e));
+    const int rows = geom.gsize[la], ns = std::max(1, std::min(rows, spr * part.counts[la]));
     stripe_n.assign(ns + 1, 0);
     for (int j = 0; j <= ns; ++j) stripe_n[j] = plane * ((static_cast<long long>(rows) * j) / ns);
     need_stripe.assign(nmacro, -1);
@@ -1736,7 +1738,12 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     }
     sa.tasks = d_mtasks.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps_own[m].size());
-    if (sa.ntasks > 0) launch_build_rhs(sa, eng.n_max, static_cast<int>(line_max), s);
+    if (sa.ntasks > 0) {
+      // tasks past sweep 1 touch only their injection lines: size the init grid for that
+      bool full = false;
+      for (const int2& t : msteps_own[m]) full |= t.y == 1 || t.y - nbuf == 1;
+      launch_build_rhs(sa, full ? eng.n_max : 0, static_cast<int>(line_max), s);
+    }
     if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * m], s));
     const char* tstep = std::getenv("HS_TRACE_STEP");
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
@@ -1958,6 +1965,55 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   }
   HS_CUDA(cudaEventRecord(ev_in[ns + 1], cstream));
   HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[ns + 1], 0));  // later work may reuse io / u
+  if (const char* path = std::getenv("HS_STREAM_TRACE")) {  // developer timeline (timing events)
+    std::vector<cudaEvent_t> te(3 * ns + 2);
+    // re-run the same schedule with timing events: H2D done per stripe, u stripe out per stripe
+    HS_CUDA(cudaStreamSynchronize(cstream));
+    HS_CUDA(cudaStreamSynchronize(eng.stream));
+    for (auto& e : te) HS_CUDA(cudaEventCreate(&e));
+    HS_CUDA(cudaEventRecord(te[0], eng.stream));
+    HS_CUDA(cudaStreamWaitEvent(cstream, te[0], 0));
+    for (int j = 0; j < ns; ++j) {
+      const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
+      HS_CUDA(cudaMemcpy2DAsync(din + n0, pitch, reinterpret_cast<const double2*>(b) + n0, pitch,
+                                static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyHostToDevice, cstream));
+      HS_CUDA(cudaEventRecord(te[1 + j], cstream));
+    }
+    const StreamIO tio{te.data() + 1, din, dout};
+    run(nrounds, track, true, &tio);
+    for (int q = 0; q < ns; ++q) {
+      const int j = order[q];
+      HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
+      HS_CUDA(cudaEventRecord(te[1 + ns + j], cstream));  // stripe final on the device
+      const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
+      HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
+                                static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
+      HS_CUDA(cudaEventRecord(te[1 + 2 * ns + j], cstream));
+    }
+    HS_CUDA(cudaEventRecord(te[3 * ns + 1], eng.stream));
+    HS_CUDA(cudaStreamSynchronize(cstream));
+    HS_CUDA(cudaStreamSynchronize(eng.stream));
+    if (FILE* fp = std::fopen(path, "w")) {
+      float t = 0.f;
+      std::fprintf(fp, "what,index,ms\n");
+      for (int j = 0; j < ns; ++j) {
+        cudaEventElapsedTime(&t, te[0], te[1 + j]);
+        std::fprintf(fp, "h2d_done,%d,%.3f\n", j, t);
+        cudaEventElapsedTime(&t, te[0], te[1 + ns + j]);
+        std::fprintf(fp, "u_final,%d,%.3f\n", j, t);
+        cudaEventElapsedTime(&t, te[0], te[1 + 2 * ns + j]);
+        std::fprintf(fp, "d2h_done,%d,%.3f\n", j, t);
+      }
+      for (size_t m = 0; m < msteps.size(); ++m) {
+        cudaEventElapsedTime(&t, te[0], ev[1 + nsweeps + 2 * m]);
+        std::fprintf(fp, "mstep_solve_start,%zu,%.3f\n", m, t);
+      }
+      cudaEventElapsedTime(&t, te[0], te[3 * ns + 1]);
+      std::fprintf(fp, "compute_end,0,%.3f\n", t);
+      std::fclose(fp);
+    }
+    for (auto e : te) cudaEventDestroy(e);
+  }
   if (reps) reports(nrounds, track, reps);
   HS_CUDA(cudaStreamSynchronize(cstream));
   HS_CUDA(cudaStreamSynchronize(eng.stream));

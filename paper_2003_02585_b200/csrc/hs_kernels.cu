@@ -759,8 +759,9 @@ void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* m
   after_launch();
 }
 
+// max_n = 0: no task of the launch rewrites its whole buffer (lines only)
 void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStream_t s) {
-  const int bx = std::max(1, std::min(blocks_for(max_n * a.R), 512));
+  const int bx = std::max(1, std::min(blocks_for(std::max<long long>(max_n, max_line) * a.R), 512));
   rhs_init_kernel<<<dim3(bx, a.ntasks), kThreads, 0, s>>>(a);
   after_launch();
   const int nchunk = std::max(1, (max_line * a.R + kInjectChunk - 1) / kInjectChunk);
