@@ -101,6 +101,16 @@ class DdmSolver {
     check(hs_ddm_create(&setup, device, &s_, &sub, &pivot), pivot);
     check(hs_ddm_info(s_, &dim_, &n_, &nsub_, &factor_seconds_, nullptr, nullptr));
   }
+  // Subdomain-partitioned solver, one per rank (hs_ddm_create_partitioned): owner may be null
+  // (hs_partition_owners); exchange / allreduce carry the messages (e.g. NCCL).
+  DdmSolver(const hs_problem& setup, int device, int rank, int world, const int* owner, hs_exchange_fn exchange,
+            hs_allreduce_fn allreduce, void* user) {
+    int sub = -1;
+    std::int64_t pivot = -1;
+    check(hs_ddm_create_partitioned(&setup, device, rank, world, owner, exchange, allreduce, user, &s_, &sub, &pivot),
+          pivot);
+    check(hs_ddm_info(s_, &dim_, &n_, &nsub_, &factor_seconds_, nullptr, nullptr));
+  }
   ~DdmSolver() { hs_ddm_destroy(s_); }
   DdmSolver(const DdmSolver&) = delete;
   DdmSolver& operator=(const DdmSolver&) = delete;
@@ -140,6 +150,14 @@ class DdmSolver {
     CVector x(b.size());
     hs_gmres_report local{};
     check(hs_gmres(s_, 1, dp(b.data()), dp(x.data()), tol, maxit, rounds, report ? report : &local));
+    return x;
+  }
+  // GMRES(restart) cycles up to maxit iterations (BASELINE config 4's GMRES(30))
+  CVector gmres_restarted(const CVector& b, double tol, int maxit, int restart, int rounds,
+                          hs_gmres_report* report = nullptr) {
+    CVector x(b.size());
+    hs_gmres_report local{};
+    check(hs_gmres_restarted(s_, 1, dp(b.data()), dp(x.data()), tol, maxit, restart, rounds, report ? report : &local));
     return x;
   }
 
