@@ -307,3 +307,50 @@ def test_cluster_factorization_path_against_oracle(hs, monkeypatch, dim):
         assert [getattr(reps[r], k) for k in COUNTERS] == [getattr(ro, k) for k in COUNTERS]
     s2 = hs.DdmSolver(hs.ProblemSetup(dim, [n] * dim, parts, hs.Medium("constant", kappa=kap), pml_width=pad))
     assert np.array_equal(s2.ddm_solve(b, 1), U)  # the cluster factorization is deterministic
+
+
+def test_gridded_medium_against_reference(hs, tmp_path):
+    """BASELINE config 4's medium kind at small scale: a seeded smooth velocity grid (HSVG file
+    for the reference, the same samples for the device), one DDM application and GMRES against
+    oracle/_ref (the reference compiled in place) on the same inputs."""
+    from oracle import ref
+    from paper_2003_02585_b200 import sources
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    nl, n, pad, omega = 64, 64, 8, 2 * math.pi * 4
+    c = sources.gaussian_random_velocity(nl, 7, corr_len=0.1)
+    path = str(tmp_path / "v.hsvg")
+    hs.write_velocity_grid(path, hs.VelocityGrid(2, [nl + 1, nl + 1, 1], [0.0, 0.0, 0.0], [1 / nl, 1 / nl, 0.0], c.ravel()))
+    med = hs.Medium("gridded", velocity=c.ravel(), vel_n=(nl + 1, nl + 1, 1), vel_origin=(0.0, 0.0, 0.0),
+                    vel_spacing=(1 / nl, 1 / nl, 0.0), omega=omega)
+    s = hs.DdmSolver(hs.ProblemSetup(2, [n, n], [2, 2], med, pml_width=pad))
+    r = ref.RefSolver({"dim": 2, "grid.n": [n, n], "partition": [2, 2], "pml.width": pad, "media.kind": "gridded",
+                       "media.velocity_file": path, "media.omega": omega}, 4)
+    f = sources.gaussian_sources(2, s.lo, s.hi, [1 / n] * 2, [0.0, 0.0], [[0.3, 0.4], [0.7, 0.2]], 2.0 / n)
+    b = s.scale_source(f)
+    assert np.array_equal(b[0], r.scale_source(f[0]))
+    reps = []
+    U = s.ddm_solve(b, 1, reps, True)
+    for i in range(2):
+        u0, rep0 = r.ddm_solve(b[i], 1, True)
+        assert rel(U[i], u0) <= TOL
+        assert [getattr(reps[i], k) for k in COUNTERS] == [rep0[k] for k in COUNTERS]
+    g = s.gmres(b[0], 1e-8, 60, 1)
+    xr, gr = r.gmres(b[0], 1e-8, 60, 1)
+    assert abs(g.iterations - gr["iterations"]) <= 1 and rel(g.x, xr) <= 1e-7
+
+
+def test_batches_beyond_the_device_batch_and_zero_rhs(hs, golden):
+    """nrhs above the 32-RHS device batch (two batches) equals per-RHS solves; an all-zero RHS
+    gives an exactly zero field with every task skipped (src/sweeper.cpp:240-251)."""
+    z = golden("ddm_2d_2x2")
+    s = hs.DdmSolver(_setup(hs, z))
+    rng = np.random.default_rng(5)
+    B = np.repeat(z["b"], 17, axis=0) * (1.0 + 0.25 * rng.standard_normal((34, 1)))
+    B[33] = 0.0
+    reps = []
+    U = s.ddm_solve(B, 1, reps, True)
+    for r in (0, 31, 32):
+        assert np.array_equal(U[r], s.ddm_solve(B[r], 1))
+    assert not np.any(U[33])
+    assert reps[33].local_solves == 0 and reps[33].skipped_zero_solves == 4 * s.nsub
