@@ -54,10 +54,30 @@ def main():
                      "warps_active_pct": g(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
                      "registers": g(r, "launch__registers_per_thread"), "grid": g(r, "launch__grid_size")})
     traffic = [c["dram_read_MB"] + c["dram_write_MB"] for c in caps]
-    json.dump({"source": f"ncu --set full --clock-control none, tools/prof_step.py (C2, 16 RHS), solve6 launches 29-30 "
-                         f"= the forward and backward launch of macro-step 14 (15 tasks), {tag}",
-               "bytes_per_launch": 1e6 * sum(traffic) / len(traffic), "launches": caps},
-              open(os.path.join(PROF, "solve_traffic.json"), "w"), indent=1)
+    out = {"source": f"ncu --set full --clock-control none, tools/prof_step.py (C2, 16 RHS), solve6 launches 29-30 "
+                     f"= the forward and backward launch of macro-step 14 (15 tasks), {tag}",
+           "bytes_per_launch": 1e6 * sum(traffic) / len(traffic), "launches": caps}
+    # every solve launch of one application (ncu --metrics dram__bytes_*), comparable with the bench's
+    # alg_bytes_per_launch, which averages over the same launches
+    allp = os.path.join(OUT, "solve_dram_all.csv")
+    if os.path.exists(allp):
+        per = collections.defaultdict(float)
+        rows = list(csv.reader(open(allp)))
+        hdr = None
+        for r in rows:
+            if r and r[0] == "ID":
+                hdr = r
+                continue
+            if hdr and len(r) == len(hdr):
+                d = dict(zip(hdr, r))
+                if d["Metric Name"].startswith("dram__bytes"):
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["Metric Unit"]]
+                    per[d["ID"]] += float(d["Metric Value"].replace(",", "")) * scale
+        out["source_all_launches"] = (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+                                      f"over all {len(per)} solve launches of one C2 application (tools/prof_step.py)")
+        out["bytes_per_launch"] = sum(per.values()) / max(len(per), 1)
+        out["bytes_per_launch_macro_step_14"] = 1e6 * sum(traffic) / len(traffic)
+    json.dump(out, open(os.path.join(PROF, "solve_traffic.json"), "w"), indent=1)
     bench = json.load(open(os.path.join(PROF, f"{tag}_bench.json")))
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
