@@ -939,6 +939,10 @@ struct DdmHandle {
   // the last sweep is accumulated stripe by stripe, after the macro-step that completes the
   // stripe (acc_stripe_m), so streamed transfers can copy u out while the tail still runs
   std::vector<int> acc_stripe_m;
+  // every sweep in its own x buffer (sweeps <= buffers): all contributions are accumulated in one
+  // pass per stripe at the end (accumulate_all_kernel) instead of one pass per sweep
+  bool fuse_acc = false;
+  std::vector<int> sweep_end_m;  // per sweep: the macro-step its last task runs in
   cudaStream_t cstream = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   DBuf<int2> d_mtasks;
@@ -962,6 +966,7 @@ struct DdmHandle {
   DBuf<int> route;
   DBuf<double2> bN, u, io;
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
+  long long partial_stride = 0;  // elements between sweeps' partials (fused accumulate)
   std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l's accumulate, then macro-step solve pairs
   // global operator (lazy) and its direct factorization (global_direct_solve, lazy)
   hs_factor* gfact = nullptr;
@@ -1487,19 +1492,23 @@ void DdmHandle::build_schedule() {
       }
       need_stripe[m] = need;
     }
-    // stripes of the last sweep's accumulate
+    // stripes of the last sweep's accumulate (of every sweep's, fused)
+    fuse_acc = nsweeps <= nbuf && nsweeps <= HS_MAX_ACC_SWEEPS && !std::getenv("HS_NO_FUSED_ACC");
+    sweep_end_m.assign(nsweeps + 1, 0);
+    for (int l = 1; l <= nsweeps; ++l) sweep_end_m[l] = accl[l] - 1;
     acc_stripe_m.assign(ns, nsweeps > 1 ? accl[nsweeps - 1] - 1 : 0);
-    for (int id = 0; id < nsub; ++id) {
-      const int m = mstep_of[static_cast<size_t>(nsweeps - 1) * nsub + id];
-      const GridRange sup = wts.support(subs[id].sub);
-      const long long lo = static_cast<long long>(sup.lo[la] - geom.glo[la]) * plane;
-      const long long hi = (static_cast<long long>(sup.hi[la] - geom.glo[la]) + 1) * plane;
-      for (int j = 0; j < ns; ++j)
-        if (stripe_n[j] < hi && stripe_n[j + 1] > lo) acc_stripe_m[j] = std::max(acc_stripe_m[j], m);
-    }
-    for (int l = 1; l <= nsweeps; ++l) {  // the last sweep's whole-domain accumulate is replaced
+    for (int l = fuse_acc ? 1 : nsweeps; l <= nsweeps; ++l)
+      for (int id = 0; id < nsub; ++id) {
+        const int m = mstep_of[static_cast<size_t>(l - 1) * nsub + id];
+        const GridRange sup = wts.support(subs[id].sub);
+        const long long lo = static_cast<long long>(sup.lo[la] - geom.glo[la]) * plane;
+        const long long hi = (static_cast<long long>(sup.hi[la] - geom.glo[la]) + 1) * plane;
+        for (int j = 0; j < ns; ++j)
+          if (stripe_n[j] < hi && stripe_n[j + 1] > lo) acc_stripe_m[j] = std::max(acc_stripe_m[j], m);
+      }
+    for (int l = 1; l <= nsweeps; ++l) {  // the striped accumulate replaces the whole-domain ones
       auto& v = acc_after[accl[l] - 1];
-      if (l == nsweeps) v.erase(std::remove(v.begin(), v.end(), l), v.end());
+      if (l == nsweeps || fuse_acc) v.erase(std::remove(v.begin(), v.end(), l), v.end());
     }
   }
   // this rank's tasks (all of them unless partitioned)
@@ -1660,7 +1669,8 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   u.alloc(static_cast<size_t>(geom.gn) * R);
   // + striped rounding + reduction scratch
   const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(stripe_n.size()) + kReducePad;
-  partial.alloc(static_cast<size_t>(nb) * R);
+  partial_stride = nb * R;
+  partial.alloc(static_cast<size_t>(nb) * R * (fuse_acc ? nsweeps : 1));
   pnum.alloc(static_cast<size_t>(nb) * R);
   pden.alloc(static_cast<size_t>(nb) * R);
   norms.alloc(static_cast<size_t>(nsweeps) * R);
@@ -1777,8 +1787,8 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
       aa.n1 = n1;
       return launch_accumulate(aa, s);
     };
-    auto after_sweep = [&](int l, int nb) {  // sweep l fully accumulated
-      launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
+    auto after_sweep = [&](int l, int nb) {  // sweep l fully accumulated (nb < 0: norms reduced already)
+      if (nb >= 0) launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
       if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
         const int last = static_cast<int>(stripe_n.size()) - 2;
@@ -1803,17 +1813,46 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
       }
     };
     for (int l : acc_after[m]) after_sweep(l, accumulate(l, 0, geom.gn, 0));
-    // the last sweep, stripe by stripe (partials in stripe order: a fixed reduction order)
+    if (fuse_acc && timed)  // sweeps that end here (their contributions are accumulated at the end)
+      for (int l = 1; l < nsweeps; ++l)
+        if (sweep_end_m[l] == m) HS_CUDA(cudaEventRecord(ev[l], s));
+    // the last sweep (every sweep, fused), stripe by stripe (partials in stripe order: a fixed
+    // reduction order)
     const int nst = static_cast<int>(acc_stripe_m.size());
     for (int j = 0; j < nst; ++j) {
       if (acc_stripe_m[j] != m) continue;
-      stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
+      if (fuse_acc) {
+        AccumAllArgs aa{};
+        aa.g = geom;
+        aa.R = R;
+        aa.L = nsweeps;
+        for (int l = 1; l <= nsweeps; ++l) {
+          aa.acc_ent[l - 1] = acc_ent.p + static_cast<size_t>((l - 1) % ndir) * geom.gn * (1 << dim);
+          aa.xoff[l - 1] = static_cast<long long>((l - 1) % nbuf) * eng.xstride;
+          aa.nzmask[l - 1] = nzmask.p + static_cast<size_t>(l - 1) * nsub;
+        }
+        aa.x = eng.x.p;
+        aa.u = u.p;
+        aa.partial = partial.p + stripe_pbase(j) * R;
+        aa.pstride = partial_stride;
+        aa.n0 = stripe_n[j];
+        aa.n1 = stripe_n[j + 1];
+        stripe_blocks[j] = launch_accumulate_all(aa, s);
+      } else {
+        stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
+      }
       if (io) launch_transpose_out_range(u.p, io->dout, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
       HS_CUDA(cudaEventRecord(ev_out[j], s));
       if (++stripes_done == nst) {
         int nbt = 0;
         for (int q = 0; q < nst; ++q) nbt += stripe_blocks[q];
-        after_sweep(nsweeps, nbt);
+        if (fuse_acc) {
+          for (int l = 1; l <= nsweeps; ++l)
+            launch_reduce_partials(partial.p + (l - 1) * partial_stride, nbt, R, norms.p + static_cast<size_t>(l - 1) * R, s);
+          after_sweep(nsweeps, -1);
+        } else {
+          after_sweep(nsweeps, nbt);
+        }
       }
     }
   }

@@ -779,6 +779,64 @@ void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
   after_launch();
 }
 
+template <int E>
+__global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a) {
+  __shared__ double red[kThreads];
+  const int dim = a.g.dim, R = a.R;
+  const int npb = kThreads / R;
+  const long long node = a.n0 + static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const int r = threadIdx.x % R;
+  const bool live = threadIdx.x < npb * R && node < a.n1;
+  const double inv = 1.0 / static_cast<double>(1 << dim);
+  double2 uv = czero();
+#pragma unroll 1
+  for (int l = 0; l < a.L; ++l) {
+    double nrm = 0.0;
+    if (live) {
+      int2 ent[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) ent[e] = __ldg(a.acc_ent[l] + node * E + e);
+      double2 xv[E];
+      bool on[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        on[i] = ent[i].x >= 0 && ((a.nzmask[l][ent[i].y >> 4] >> r) & 1u);
+        xv[i] = on[i] ? a.x[a.xoff[l] + static_cast<long long>(ent[i].x) * R + r] : czero();
+      }
+      double2 acc = czero();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        if (!on[i]) continue;
+        const double w = (ent[i].y & 15) * inv;
+        acc.x += w * xv[i].x;
+        acc.y += w * xv[i].y;
+      }
+      uv = cadd(uv, acc);
+      nrm = acc.x * acc.x + acc.y * acc.y;
+    }
+    red[threadIdx.x] = nrm;
+    __syncthreads();
+    if (threadIdx.x < R) {
+      double sm = 0.0;
+      for (int q = threadIdx.x; q < kThreads; q += R) sm += red[q];
+      a.partial[l * a.pstride + static_cast<long long>(blockIdx.x) * R + threadIdx.x] = sm;
+    }
+    __syncthreads();
+  }
+  if (live) a.u[node * R + r] = uv;
+}
+
+int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s) {
+  const int nb = blocks_for(a.n1 - a.n0, kThreads / a.R);
+  if (nb == 0) return 0;
+  if (a.g.dim == 3)
+    accumulate_all_kernel<8><<<nb, kThreads, 0, s>>>(a);
+  else
+    accumulate_all_kernel<4><<<nb, kThreads, 0, s>>>(a);
+  after_launch();
+  return nb;
+}
+
 int launch_accumulate(const AccumArgs& a, cudaStream_t s) {
   const int nb = blocks_for(a.n1 - a.n0, kThreads / a.R);
   if (nb == 0) return 0;

@@ -84,6 +84,7 @@ void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStr
 // Trace extraction -> routing -> mailbox deposit (src/transfer.cpp:13-66, src/sweeper.cpp:295-307).
 void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s);
 
+#define HS_MAX_ACC_SWEEPS 8
 struct AccumArgs {
   DevGeom g;
   int R;
@@ -102,6 +103,23 @@ struct AccumArgs {
 // u += sum_sub w * u_local over the subdomain supports in the reference's order
 // (src/transfer.cpp:91-102, src/sweeper.cpp:308-312); emits per-block norm partials.
 int launch_accumulate(const AccumArgs& a, cudaStream_t s);  // nodes [a.n0, a.n1); returns its block count
+
+// Every sweep of an application in one pass (all x buffers distinct): u = (((0 + c_1) + c_2) + ...)
+// with c_l the sweep-l contribution, node by node in sweep order -- the same sums as L separate
+// accumulates, one read of each x and one write of u; partials of |c_l|^2 per sweep.
+struct AccumAllArgs {
+  DevGeom g;
+  int R, L;
+  const int2* acc_ent[HS_MAX_ACC_SWEEPS];   // plan of sweep l's direction
+  long long xoff[HS_MAX_ACC_SWEEPS];        // x buffer of sweep l
+  const unsigned* nzmask[HS_MAX_ACC_SWEEPS];
+  const double2* x;
+  double2* u;
+  double* partial;     // sweep l's partials at partial + l * pstride
+  long long pstride;
+  long long n0, n1;
+};
+int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s);
 // Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
 constexpr int kReducePad = 256;  // extra partial rows every partial buffer reserves (reduction scratch)
 void launch_reduce_partials(double* partial, int nblocks, int R, double* out, cudaStream_t s);
