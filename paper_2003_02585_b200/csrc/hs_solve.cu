@@ -65,12 +65,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+#ifndef HS_SPIN_MAX_NS
+#define HS_SPIN_MAX_NS 256
+#endif
 __device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
   if (lane == 0) {
     unsigned ns = 32;  // short backoff: waiters on the critical path must react quickly
     while (ld_relaxed(p) < target) {
       __nanosleep(ns);
-      ns = min(ns * 2, 256u);
+      ns = min(ns * 2, static_cast<unsigned>(HS_SPIN_MAX_NS));
     }
     (void)ld_acquire(p);
   }
