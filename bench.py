@@ -128,9 +128,11 @@ def ncu_traffic():
         return None
 
 
-def cpu_baseline_sample(b0):
+def cpu_baseline_sample(b0, u0=None):
     """oracle/_ref (the reference compiled in place) on this host's cores: DdmSolver factorizes
-    all 64 subdomains, then one RHS of the workload through one DDM application."""
+    all 64 subdomains, then one RHS of the workload through one DDM application. With u0 (the
+    device result for the same RHS) it also reports the relative L2 difference -- parity at the
+    bench's own configuration (north_star: <= 1e-9)."""
     try:
         from oracle import ref
         if not ref.available():
@@ -141,10 +143,13 @@ def cpu_baseline_sample(b0):
         t0 = time.perf_counter()
         u, rep = s.ddm_solve(b0, CFG["rounds"], True)
         dt = time.perf_counter() - t0
-        return {"value": 1.0 / dt, "unit": "RHS/s", "cores": cores, "kind": "reference",
-                "sample": f"1 of the 16 RHS through one full DDM application (4 sweeps, residual), "
-                          f"sweep.workers={cores}; factorization {s.factor_seconds:.2f}s excluded",
-                "factor_seconds": s.factor_seconds, "seconds": dt}
+        out = {"value": 1.0 / dt, "unit": "RHS/s", "cores": cores, "kind": "reference",
+               "sample": f"1 of the 16 RHS through one full DDM application (4 sweeps, residual), "
+                         f"sweep.workers={cores}; factorization {s.factor_seconds:.2f}s excluded",
+               "factor_seconds": s.factor_seconds, "seconds": dt}
+        if u0 is not None:
+            out["parity_rel_l2_rhs0"] = float(np.linalg.norm(u0 - u) / np.linalg.norm(u))
+        return out
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "RHS/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -317,7 +322,8 @@ def run_gpu(args, rank, world, local_rank):
         "device_t0_us_per_16rhs_task": 1e6 * prof["solve_seconds"] / max(prof["subdomain_solves"], 1),
         "device_ms_per_macro_step": ms_max / max(sched["macro_steps"], 1)}
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(b[0])
+        u0 = hu[0].numpy().view(np.complex128) if hu.dim() > 1 else None
+        line["cpu_baseline"] = cpu_baseline_sample(b[0], u0)
     print(json.dumps(line))
     return 0
 
