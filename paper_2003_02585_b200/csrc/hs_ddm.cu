@@ -345,7 +345,11 @@ struct Engine {
     // chunk subdomains so the dense workspaces stay within a memory budget
     size_t free_b = 0, total_b = 0;
     HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const long long budget = static_cast<long long>(std::min<double>(free_b * 0.4, 24e9)) / sizeof(double2);
+    // (the dense workspaces live only during the factorization; the per-cluster scratch of the large
+    // fronts and the solve buffers allocated later come out of the remainder)
+    double frac = 0.6;
+    if (const char* e = std::getenv("HS_FACTOR_MEM_FRAC")) frac = std::min(0.9, std::max(0.05, std::atof(e)));
+    const long long budget = static_cast<long long>(free_b * frac) / sizeof(double2);
     cudaEvent_t e0, e1;
     HS_CUDA(cudaEventCreate(&e0));
     HS_CUDA(cudaEventCreate(&e1));
