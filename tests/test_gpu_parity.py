@@ -354,3 +354,31 @@ def test_batches_beyond_the_device_batch_and_zero_rhs(hs, golden):
         assert np.array_equal(U[r], s.ddm_solve(B[r], 1))
     assert not np.any(U[33])
     assert reps[33].local_solves == 0 and reps[33].skipped_zero_solves == 4 * s.nsub
+
+
+@pytest.mark.parametrize("dim,n,parts,pad,rounds", [(2, [64, 40], [4, 2], 6, 3), (3, [24, 16, 16], [3, 2, 1], 4, 1),
+                                                    (2, [36, 36], [1, 3], 5, 2)])
+def test_anisotropic_grids_against_reference(hs, dim, n, parts, pad, rounds):
+    """Non-square grids, unequal and unit partition counts, 2-3 rounds: the device path against
+    oracle/_ref (the reference compiled in place) on the same seeded sources, u <= 1e-9 and the
+    counters exact."""
+    from oracle import ref
+    from paper_2003_02585_b200 import sources
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    kap = 2 * math.pi * 3
+    s = hs.DdmSolver(hs.ProblemSetup(dim, n, parts, hs.Medium("constant", kappa=kap), pml_width=pad))
+    r = ref.RefSolver({"dim": dim, "grid.n": n, "partition": parts, "pml.width": pad, "media.kind": "constant",
+                       "media.kappa": kap}, 4)
+    assert r.N == s.global_n
+    f = sources.gaussian_sources(dim, s.lo, s.hi, [1.0 / x for x in n], [0.0] * 3,
+                                 sources.seeded_centers(11, 2, dim), 2.0 / max(n))
+    b = s.scale_source(f)
+    reps = []
+    U = s.ddm_solve(b, rounds, reps, True)
+    for i in range(2):
+        assert np.array_equal(b[i], r.scale_source(f[i]))
+        u0, rep0 = r.ddm_solve(b[i], rounds, True)
+        assert rel(U[i], u0) <= TOL
+        assert [getattr(reps[i], k) for k in COUNTERS] == [rep0[k] for k in COUNTERS]
+        np.testing.assert_allclose(reps[i].round_residuals, rep0["round_residuals"], rtol=1e-6)
