@@ -65,17 +65,29 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+#ifndef HS_POLL_ACQUIRE
+#define HS_POLL_ACQUIRE 0
+#endif
 #ifndef HS_SPIN_MAX_NS
 #define HS_SPIN_MAX_NS 256
 #endif
 __device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
   if (lane == 0) {
     unsigned ns = 32;  // short backoff: waiters on the critical path must react quickly
+#if HS_POLL_ACQUIRE
+    // every poll is an acquire load: the one that sees the target already orders the reads that
+    // follow, saving the extra L2 round trip of a relaxed poll plus a separate acquire
+    while (ld_acquire(p) < target) {
+      __nanosleep(ns);
+      ns = min(ns * 2, static_cast<unsigned>(HS_SPIN_MAX_NS));
+    }
+#else
     while (ld_relaxed(p) < target) {
       __nanosleep(ns);
       ns = min(ns * 2, static_cast<unsigned>(HS_SPIN_MAX_NS));
     }
     (void)ld_acquire(p);
+#endif
   }
   __syncwarp();
 }
