@@ -274,6 +274,13 @@ constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 #define HS_KUNROLL 1
 #endif
 constexpr int kKUnroll = HS_KUNROLL;  // k-loop unroll (tuning experiments)
+// When a warp takes its next ticket: 1 = after the current item's k-loop (its atomic overlaps the
+// reduction / finalize, and the held ticket is blocked only for that short tail), 0 = at the
+// start of the current item (the held ticket then waits behind the whole item: at the end of a
+// pass, idle warps could not start critical-path items other warps held).
+#ifndef HS_LATE_TICKET
+#define HS_LATE_TICKET 1
+#endif
 
 template <bool FWD>
 struct Ring {
@@ -385,6 +392,14 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
   cp_commit();
 }
 
+// the warp's next ticket (lane 0's atomic; its latency is paid only where the value is used)
+__device__ __forceinline__ void take_ticket(const SolveArgs& a, unsigned& tk, bool& took, int lane) {
+  if (HS_LATE_TICKET && !took) {
+    if (lane == 0) tk = atomicAdd(a.queue, 1u);
+    took = true;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // forward band item: out[32 rows][8 NT RHS] = [M; W][band rows, chunk cols] T_sep[chunk cols].
 // Boundary rows produce V = T_bnd - W T_sep: their chunk-0 accumulators start at -T_bnd (the
@@ -393,7 +408,8 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
 // this warp finalized the band (the caller signals it).
 template <int NT>
 __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
-                         int lane, double2* ring, const int2* sidx, unsigned long long* tr, unsigned clive) {
+                         int lane, double2* ring, const int2* sidx, unsigned long long* tr, unsigned clive,
+                         unsigned& tk, bool& took) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
@@ -476,6 +492,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     }
   }
   kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of, [](int) { return false; });
+  take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (cb1 - cb0);
@@ -523,7 +540,8 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
 template <int NT>
 __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane,
-                         double2* ring, const int2* sidx, unsigned long long* tr, bool zlive) {
+                         double2* ring, const int2* sidx, unsigned long long* tr, bool zlive, unsigned& tk,
+                         bool& took) {
   const int R = a.R, r0 = it.r0, rl = lane >> 2;
   const BwdRange rg = bwd_range(J, g, it);
   const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
@@ -577,6 +595,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
+  take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] = 2 * (a1 - a0);
@@ -626,16 +645,18 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
   // First round static: item i goes to warp i / gridDim.x of CTA i % gridDim.x, so the head
   // of the list (the critical-path fronts of the backward pass) spreads over all SMs instead
   // of packing onto the first CTAs' warps. Then dynamic tickets past the static range, each
-  // dequeued one item ahead (its atomic and the next item's record load overlap the current
-  // item; the release of a finalized band overlaps that load). A held ticket is always above
-  // its holder's current item, so the lowest current item can always finish: no deadlock.
+  // taken once the current item's k-loop is done (HS_LATE_TICKET; its atomic overlaps the
+  // reduction and finalize, the next item's record load overlaps the release of a finalized
+  // band). A held ticket is always above its holder's current item, so the lowest current item
+  // can always finish: no deadlock.
   const int nstatic = gridDim.x * (kThreads / 32);
   int cur = blockIdx.x + warp * gridDim.x;
   SolveItem it{};
   if (cur < a.nitems) it = a.items[cur];
   while (cur < a.nitems) {
     unsigned tk = 0;
-    if (lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
+    bool took = !HS_LATE_TICKET;
+    if (!HS_LATE_TICKET && lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
     bool fin = false;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
     if (a.nzmask[it.nzi] != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it
@@ -672,17 +693,18 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
         if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
         double2* V = a.vbuf + it.slot * a.vslot_stride;
         if (FWD)
-          fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr, clive)
-                          : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr, clive);
+          fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
+                          : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
         else
-          fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr, live)
-                          : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr, live);
+          fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
+                          : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
         if (tr && lane == 0) {
           tr[4] = gtime();
           tr[5] = smid();
         }
       }
     }
+    if (!took && lane == 0) tk = atomicAdd(a.queue, 1u);  // skipped item: no k-loop to overlap
     const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
     SolveItem nit{};
     if (nxt < a.nitems) nit = a.items[nxt];
