@@ -119,7 +119,7 @@ struct Engine {
   long long v_total_max = 0, n_max = 0;
   // solve state
   int R = 0, nslots = 0, ngr = 1;
-  int kc = 8, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
+  int kc = 4, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
   int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
   int crit_gw = 8;             // RHS per item of the split (critical-path) fronts
   long long arr_total = 0, part_total = 0;     // per slot
@@ -573,52 +573,96 @@ struct Engine {
     return 2LL * nslots * nf_max + 2LL * nslots * arr_total * ngr + 2;
   }
 
-  // Work items of the tasks of one macro-step (slot = position of the task): forward = every
-  // front by height, its bands x column chunks x RHS groups; backward = every front by depth,
-  // its column bands x block-row chunks x RHS groups. A task is (subdomain, sweep l, x buffer).
+  // Work items of the tasks of one macro-step (slot = position of the task): every front's bands
+  // x split-K chunks x RHS groups (forward: row bands x column chunks; backward: column bands x
+  // block-row chunks). A task is (subdomain, sweep l, x buffer).
+  //
+  // List order = dequeue priority. Fronts are ordered by the estimated length of the dependency
+  // chain still ahead of them (forward: the front and its ancestors up to the root; backward: the
+  // front and its longest descendant chain), longest first, so the fronts of the critical chain
+  // are not queued behind short-chain fronts of the same level (HS_ORDER=0: the plain level order,
+  // forward by height, backward by depth). A front's chain is strictly longer than that of the
+  // fronts depending on it, so every dependency still sits earlier in the list (deadlock freedom
+  // of the dataflow launch).
   struct TaskRef {
     int sub, l, xb;
   };
-  void build_items(const std::vector<TaskRef>& tasks, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
-    const int nsub = static_cast<int>(sub_cls.size());
-    int hmax = 0, dmax = 0;
-    for (const TaskRef& tk : tasks) {
-      hmax = std::max(hmax, classes[sub_cls[tk.sub]]->sym->max_height);
-      dmax = std::max(dmax, classes[sub_cls[tk.sub]]->sym->max_depth);
+  // estimated time of one front's items (us): wake-up + the longest item's k-loop + split-K reduce
+  static double front_cost(const FrontDesc& fd, int chunk, bool fwd) {
+    const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3);
+    const int full = fwd ? kb : nrb;  // blocks of the longest band's inner dimension
+    return 4.0 + 1.1 * std::min(full, chunk) + (full > chunk ? 2.5 : 0.0);
+  }
+  void front_priorities(const ClassDev& cd, std::vector<double>& pf, std::vector<double>& pb) const {
+    const SymbolicClass& c = *cd.sym;
+    const int nf = static_cast<int>(c.fronts.size());
+    pf.assign(nf, 0.0);
+    pb.assign(nf, 0.0);
+    for (int q = nf - 1; q >= 0; --q) {  // forward: parents first (order_up reversed)
+      const int f = c.order_up[q];
+      const FrontDesc& fd = c.fronts[f];
+      pf[f] = front_cost(fd, cd.fkc[f], true) + (fd.parent >= 0 ? pf[fd.parent] : 0.0);
     }
-    for (int h = 0; h <= hmax; ++h)
-      for (size_t g = 0; g < tasks.size(); ++g) {
-        const TaskRef& tk = tasks[g];
-        const ClassDev& cd = *classes[sub_cls[tk.sub]];
-        const SymbolicClass& c = *cd.sym;
-        if (h > c.max_height) continue;
-        const int nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
-        for (int q = c.level_start_up[h]; q < c.level_start_up[h + 1]; ++q) {
-          const int f = c.order_up[q];
-          const FrontDesc& fd = c.fronts[f];
-          const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
-          for (int t = 0; t < nband; ++t)
-            for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); ++ch)
-              for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
-                fwd.push_back(SolveItem{nzi, f, jb + f, t, static_cast<int>(g), r0, std::min(cd.fgw[f], R - r0), ch});
-        }
+    for (int q = 0; q < nf; ++q) {  // backward: children first
+      const int f = c.order_up[q];
+      const FrontDesc& fd = c.fronts[f];
+      double below = 0.0;
+      for (int ch : fd.child)
+        if (ch >= 0) below = std::max(below, pb[ch]);
+      pb[f] = front_cost(fd, cd.fkr[f], false) + below;
+    }
+  }
+  void build_items(const std::vector<TaskRef>& tasks, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
+    static const int mode = std::getenv("HS_ORDER") ? std::atoi(std::getenv("HS_ORDER")) : 1;
+    const int nsub = static_cast<int>(sub_cls.size());
+    struct Ent {
+      double key;
+      int g, q, f;
+    };
+    std::vector<Ent> ef, eb;
+    std::vector<double> pf, pb;
+    const ClassDev* last = nullptr;
+    for (size_t g = 0; g < tasks.size(); ++g) {
+      const ClassDev& cd = *classes[sub_cls[tasks[g].sub]];
+      const SymbolicClass& c = *cd.sym;
+      if (&cd != last) front_priorities(cd, pf, pb);
+      last = &cd;
+      for (int q = 0; q < static_cast<int>(c.fronts.size()); ++q) {
+        const int fu = c.order_up[q], fd = c.order_down[q];
+        // level order: forward by height, backward by depth (key = -level, ties by task, order)
+        ef.push_back(Ent{mode ? pf[fu] : -static_cast<double>(c.fronts[fu].height), static_cast<int>(g), q, fu});
+        eb.push_back(Ent{mode ? pb[fd] : -static_cast<double>(c.fronts[fd].depth), static_cast<int>(g), q, fd});
       }
-    for (int d = 0; d <= dmax; ++d)
-      for (size_t g = 0; g < tasks.size(); ++g) {
-        const TaskRef& tk = tasks[g];
-        const ClassDev& cd = *classes[sub_cls[tk.sub]];
-        if (d > cd.sym->max_depth) continue;
-        const int nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
-        for (int q = cd.level_start_down[d]; q < cd.level_start_down[d + 1]; ++q) {
-          const int f = cd.sym->order_down[q];
-          const FrontDesc& fd = cd.sym->fronts[f];
-          const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
-          for (int u = 0; u < ncband; ++u)
-            for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); ++ch)
-              for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
-                bwd.push_back(SolveItem{nzi, f, jb + f, u, static_cast<int>(g), r0, std::min(cd.fgw[f], R - r0), ch});
-        }
-      }
+    }
+    auto cmp = [](const Ent& x, const Ent& y) {
+      if (x.key != y.key) return x.key > y.key;
+      if (x.g != y.g) return x.g < y.g;
+      return x.q < y.q;
+    };
+    std::sort(ef.begin(), ef.end(), cmp);
+    std::sort(eb.begin(), eb.end(), cmp);
+    for (const Ent& e : ef) {
+      const TaskRef& tk = tasks[e.g];
+      const ClassDev& cd = *classes[sub_cls[tk.sub]];
+      const FrontDesc& fd = cd.sym->fronts[e.f];
+      const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
+      const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
+      for (int t = 0; t < nband; ++t)
+        for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); ++ch)
+          for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
+            fwd.push_back(SolveItem{nzi, f, jb + f, t, e.g, r0, std::min(cd.fgw[f], R - r0), ch});
+    }
+    for (const Ent& e : eb) {
+      const TaskRef& tk = tasks[e.g];
+      const ClassDev& cd = *classes[sub_cls[tk.sub]];
+      const FrontDesc& fd = cd.sym->fronts[e.f];
+      const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
+      const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
+      for (int u = 0; u < ncband; ++u)
+        for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); ++ch)
+          for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
+            bwd.push_back(SolveItem{nzi, f, jb + f, u, e.g, r0, std::min(cd.fgw[f], R - r0), ch});
+    }
   }
 
   // One forward and one backward launch over the items of a step group.

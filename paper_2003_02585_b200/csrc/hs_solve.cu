@@ -659,15 +659,17 @@ __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
     if (!HS_LATE_TICKET && lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
     bool fin = false;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
-    if (a.nzmask[it.nzi] != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it
+    // the item's task and front records, loaded together (all are read-only during the launch)
+    const unsigned nzm = __ldg(a.nzmask + it.nzi);
+    const unsigned fm = a.tface ? __ldg(a.tface + it.nzi) : kAllLive;  // kAllLive: sweep 1 (split source)
+    const SolveJob J = a.jobs[it.job];
+    if (nzm != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it
       unsigned long long* tr = a.trace ? a.trace + 8LL * cur : nullptr;
       if (tr && lane == 0) tr[0] = gtime();
-      const SolveJob J = a.jobs[it.job];
       // live fronts: past sweep 1 the right-hand side is zero off the injection lines of the faces
       // that received traces; a front whose subtree holds none of them has T = z = V = 0 exactly.
       // Its forward items are skipped (nothing waits for them: a live parent ignores the child),
       // and its backward items read z = 0.
-      const unsigned fm = a.tface ? a.tface[it.nzi] : kAllLive;  // kAllLive: sweep 1 (split source)
       const unsigned act = static_cast<unsigned>(J.act);
       const bool all = (fm & kAllLive) != 0;
       const bool live = all || (act & fm & 0xFFu) != 0;
