@@ -265,8 +265,14 @@ constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 #ifndef HS_NS_FWD
 #define HS_NS_FWD 2
 #endif
+#ifndef HS_NS_FWD1
+#define HS_NS_FWD1 3
+#endif
 #ifndef HS_NS_BWD
 #define HS_NS_BWD 3
+#endif
+#ifndef HS_NS_BWD1
+#define HS_NS_BWD1 4
 #endif
 // Forward items also stage, per band row, the extend-add source of boundary rows (int2) and
 // 1/d of separator rows (double2), so their finalize issues no dependent loads.
@@ -282,13 +288,21 @@ constexpr int kKUnroll = HS_KUNROLL;  // k-loop unroll (tuning experiments)
 #define HS_LATE_TICKET 1
 #endif
 
-template <bool FWD>
+// Ring depth by RHS width: a stage of an 8-RHS (NT = 1) item is smaller, so the critical-path
+// items (8-RHS groups) get a deeper ring in the same shared memory; their lone warps are bound by
+// the latency of each k-step's loads.
+template <bool FWD, int NT>
 struct Ring {
-  static constexpr int NS = FWD ? HS_NS_FWD : HS_NS_BWD;
+  static constexpr int NS = FWD ? (NT == 1 ? HS_NS_FWD1 : HS_NS_FWD) : (NT == 1 ? HS_NS_BWD1 : HS_NS_BWD);
   static constexpr int NB = FWD ? 3 : 1;
-  static constexpr int kStage = (4 + NB * 2) * 32;  // double2
+  static constexpr int kStage = (4 + NB * NT) * 32;  // double2: A fragments, then B parts (p, q) at 4 + p NT + q
+};
+template <bool FWD>
+struct RingArea {
+  static constexpr int a1 = Ring<FWD, 1>::NS * Ring<FWD, 1>::kStage, a2 = Ring<FWD, 2>::NS * Ring<FWD, 2>::kStage;
+  static constexpr int kRing = a1 > a2 ? a1 : a2;
   static constexpr int kFin = FWD ? 32 / 2 + 32 : 0;
-  static constexpr int kWarp = NS * kStage + kIdx / 2 + kFin;
+  static constexpr int kWarp = kRing + kIdx / 2 + kFin;
 };
 
 // The pipelined k-loop shared by both passes: issue(s, stage) stages k-step s with cp.async,
@@ -297,16 +311,16 @@ struct Ring {
 template <bool FWD, int NT, class Issue, class Use, class Mask, class Neg>
 __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of,
                                       Neg&& neg_of) {
-  constexpr int NS = Ring<FWD>::NS, ST = Ring<FWD>::kStage;
+  constexpr int NS = Ring<FWD, NT>::NS, ST = Ring<FWD, NT>::kStage;
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
-    if (j < ns) issue(j, ring + j * ST);
+    if (j < ns) issue(j, ring + j * ST, true);
     cp_commit();
   }
 #pragma unroll kKUnroll
   for (int s = 0; s < ns; ++s) {
     const int si = s + NS - 1;
-    if (si < ns) issue(si, ring + (si % NS) * ST);
+    if (si < ns) issue(si, ring + (si % NS) * ST, true);
     cp_commit();
     cp_wait<NS - 1>();
     __syncwarp();
@@ -419,36 +433,48 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const int2* fsrc = sidx + kIdx;
   const double2* fdv = reinterpret_cast<const double2*>(fsrc + 32);
   // live m-tiles of k-step s: row blocks of the band, minus M's zero blocks above the diagonal
+  // Per-item constants of the k-loop (the loop body is what a lone critical-path warp waits on:
+  // per k-step it computes a mask, one shared index load and a few wide multiply-adds).
+  // live m-tiles of k-step s: row blocks of the band (base), minus M's zero blocks above the
+  // diagonal: tile i is a separator row block (i < kb - 4t) whose column block cb exceeds 4t + i
+  const unsigned mbase = (1u << rbs) - 1u;
+  const int sepn = g.kb - 4 * t;
+  const unsigned msep = sepn >= 4 ? 0xFu : sepn <= 0 ? 0u : (1u << sepn) - 1u;
   auto mask_of = [&](int s) {
-    const int cb = cb0 + (s >> 1);
-    unsigned mk = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int a = 4 * t + i;
-      if (i < rbs && !(a < g.kb && cb > a)) mk |= 1u << i;
-    }
-    return mk;
+    const int d = min(max(cb0 + (s >> 1) - 4 * t, 0), 4);
+    return mbase & ~(msep & ((1u << d) - 1u));
   };
-  auto issue = [&](int s, double2* st) {
-    const double2* p = P + ((cb0 + (s >> 1)) * rbs) * 64 + 4 * (s & 1);
-    const unsigned mk = mask_of(s);
+  const double2* PA = P + cb0 * rbs * 64;  // A of k-step 0
+  const int col0 = 8 * cb0 + (lane & 3);   // inner-dimension position of this lane in k-step 0
+  const unsigned R16 = static_cast<unsigned>(R) * 16u;
+  const char* XR = reinterpret_cast<const char*>(X + r0 + rl) + static_cast<size_t>(static_cast<unsigned>(col0)) * R16;
+  const char* VR = reinterpret_cast<const char*>(V + r0 + rl);
+  bool okr[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) okr[q] = r0 + 8 * q + rl < R;
+  const bool c0 = !leaf && (clive & 1u), c1 = !leaf && (clive & 2u);  // a structurally zero child's V is stale
+  auto issue = [&](int s, double2* st, bool live) {  // live = false: a k-step past the end (no loads)
+    const double2* p = PA + (s >> 1) * rbs * 64 + 4 * (s & 1);
+    const unsigned mk = live ? mask_of(s) : 0u;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const bool ok = (mk >> i) & 1u;
       cp16(st + i * 32 + lane, ok ? p + i * 64 : P, ok);
     }
-    const int col = 8 * (cb0 + (s >> 1)) + 4 * (s & 1) + (lane & 3);
-    int2 src = (!leaf && col < J.k) ? sidx[col - 8 * cb0] : make_int2(-1, -1);
-    if (!(clive & 1u)) src.x = -1;  // a structurally zero child contributes nothing (its V is stale)
-    if (!(clive & 2u)) src.y = -1;
+    const bool okc = live && col0 + 4 * s < J.k;
+    int2 src = make_int2(0, 0);
+    if ((c0 || c1) && okc) src = sidx[(lane & 3) + 4 * s];
+    const bool o0 = okc && c0 && src.x >= 0, o1 = okc && c1 && src.y >= 0;  // -1: not in that child
+    const char* xr = XR + static_cast<size_t>(static_cast<unsigned>(4 * s)) * R16;
+    const char* v0 = VR + static_cast<size_t>(static_cast<unsigned>(src.x)) * R16;
+    const char* v1 = VR + static_cast<size_t>(static_cast<unsigned>(src.y)) * R16;
     double2* sb = st + 4 * 32 + lane;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      const int r = r0 + 8 * q + rl;
-      const bool ok = col < J.k && r < R;
-      cp16(sb + (0 * 2 + q) * 32, ok ? X + static_cast<long long>(col) * R + r : X, ok);
-      cp16(sb + (1 * 2 + q) * 32, ok && src.x >= 0 ? V + static_cast<long long>(src.x) * R + r : X, ok && src.x >= 0);
-      cp16(sb + (2 * 2 + q) * 32, ok && src.y >= 0 ? V + static_cast<long long>(src.y) * R + r : X, ok && src.y >= 0);
+      const bool ok = okc && okr[q];
+      cp16(sb + (0 * NT + q) * 32, ok ? reinterpret_cast<const double2*>(xr) + 8 * q : X, ok);
+      cp16(sb + (1 * NT + q) * 32, ok && o0 ? reinterpret_cast<const double2*>(v0) + 8 * q : X, ok && o0);
+      cp16(sb + (2 * NT + q) * 32, ok && o1 ? reinterpret_cast<const double2*>(v1) + 8 * q : X, ok && o1);
     }
   };
   auto use = [&](int, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
@@ -457,8 +483,8 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const double2* sb = st + 4 * 32 + lane;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      double2 v = sb[(0 * 2 + q) * 32];
-      const double2 w0 = sb[(1 * 2 + q) * 32], w1 = sb[(2 * 2 + q) * 32];
+      double2 v = sb[(0 * NT + q) * 32];
+      const double2 w0 = sb[(1 * NT + q) * 32], w1 = sb[(2 * NT + q) * 32];
       v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
       B[q] = make_double2(v.x + w1.x, v.y + w1.y);
     }
@@ -548,39 +574,54 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const double2* P = J.factor + (lane & 3) * 8 + rl;
   const double2* Z = J.x1 + static_cast<long long>(J.sep_off) * R;
   const int nb = J.m - J.k;
-  auto row_of = [&](int s) { return 8 * (a0 + (s >> 1)) + 4 * (s & 1) + (lane & 3); };
-  // live m-tiles (column blocks 4u + i) of k-step s: columns below k, minus M's zero blocks
+  // live m-tiles (column blocks 4u + i) of k-step s: columns below k (mcol), minus M's zero
+  // blocks above the diagonal while the rows are separator rows (column block 4u + i > row block)
+  const int cn = g.kb - 4 * u;
+  const unsigned mcol = cn >= 4 ? 0xFu : (1u << cn) - 1u;
   auto mask_of = [&](int s) {
     const int ab = a0 + (s >> 1);
-    unsigned mk = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int cbi = 4 * u + i;
-      if (cbi < g.kb && !(ab < g.kb && cbi > ab)) mk |= 1u << i;
-    }
-    return mk;
+    if (ab >= g.kb) return mcol;
+    const int d = min(max(ab - 4 * u + 1, 0), 4);
+    return mcol & ((1u << d) - 1u);
   };
-  auto issue = [&](int s, double2* st) {
-    const int ab = a0 + (s >> 1), ta = ab >> 2, rbs = min(4, g.nrb - 4 * ta);
-    const double2* p = P + band_base(ta, g.kb) + (ab & 3) * 64 + 32 * (s & 1);
-    const unsigned mk = mask_of(s);
+  // a0 is a multiple of 4 (kr is), so k-steps 8j..8j+7 read row band (a0 >> 2) + j
+  const double2* PB = P;  // base of the k-step's row band + this item's column blocks
+  int rbs = 4;
+  const unsigned R16 = static_cast<unsigned>(R) * 16u;
+  const int row0 = 8 * a0 + (lane & 3);  // row of this lane in k-step 0
+  const char* ZR = reinterpret_cast<const char*>(Z + r0 + rl);
+  const char* XR = reinterpret_cast<const char*>(J.x + r0 + rl);
+  bool okr[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) okr[q] = r0 + 8 * q + rl < R;
+  auto issue = [&](int s, double2* st, bool live) {  // live = false: a k-step past the end (no loads)
+    {  // row band of k-step s (branch-free: stays in the k-step's basic block)
+      const int ta = (a0 >> 2) + (s >> 3);
+      rbs = min(4, g.nrb - 4 * ta);
+      PB = P + band_base(ta, g.kb) + 4 * u * rbs * 64;
+    }
+    const double2* p = PB + ((s >> 1) & 3) * 64 + 32 * (s & 1);
+    const unsigned mk = live ? mask_of(s) : 0u;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int cbi = 4 * u + i;
       const bool ok = (mk >> i) & 1u;
-      cp16(st + i * 32 + lane, ok ? p + cbi * rbs * 64 : P, ok);
+      cp16(st + i * 32 + lane, ok ? p + i * rbs * 64 : P, ok);
     }
-    const int row = row_of(s);
-    const double2* src = nullptr;
-    if (row < J.k)
-      src = zlive ? Z + static_cast<long long>(row) * R : nullptr;  // structurally zero front: z = 0
-    else if (row >= g.kp && row - g.kp < nb)
-      src = J.x + static_cast<long long>(sidx[row - 8 * a0].x) * R;
+    const int row = row0 + 4 * s;
+    const char* src;
+    bool okb;
+    if (a0 + (s >> 1) < g.kb) {  // separator rows: z (a structurally zero front has z = 0)
+      okb = live && zlive && row < J.k;
+      src = ZR + static_cast<size_t>(static_cast<unsigned>(row)) * R16;
+    } else {  // boundary rows: the parent's x at the boundary positions
+      okb = live && row - g.kp < nb;
+      const int pos = okb ? sidx[row - 8 * a0].x : 0;
+      src = XR + static_cast<size_t>(static_cast<unsigned>(pos)) * R16;
+    }
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      const int r = r0 + 8 * q + rl;
-      const bool ok = src != nullptr && r < R;
-      cp16(st + (4 + q) * 32 + lane, ok ? src + r : Z, ok);
+      const bool ok = okb && okr[q];
+      cp16(st + (4 + q) * 32 + lane, ok ? reinterpret_cast<const double2*>(src) + 8 * q : Z, ok);
     }
   };
   auto use = [&](int s, const double2* st, double2 (&A)[4], double2 (&B)[NT]) {
@@ -640,8 +681,8 @@ template <bool FWD>
 __global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double2* ring = smem_ring + warp * Ring<FWD>::kWarp;
-  int2* sidx = reinterpret_cast<int2*>(ring + Ring<FWD>::NS * Ring<FWD>::kStage);
+  double2* ring = smem_ring + warp * RingArea<FWD>::kWarp;
+  int2* sidx = reinterpret_cast<int2*>(ring + RingArea<FWD>::kRing);
   // First round static: item i goes to warp i / gridDim.x of CTA i % gridDim.x, so the head
   // of the list (the critical-path fronts of the backward pass) spreads over all SMs instead
   // of packing onto the first CTAs' warps. Then dynamic tickets past the static range, each
@@ -732,7 +773,7 @@ int solve_bwd_chunks(int m, int k, int cband, int kr) {
 
 template <bool FWD>
 constexpr size_t ring_bytes() {
-  return static_cast<size_t>(kThreads / 32) * Ring<FWD>::kWarp * sizeof(double2);
+  return static_cast<size_t>(kThreads / 32) * RingArea<FWD>::kWarp * sizeof(double2);
 }
 
 void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
