@@ -453,8 +453,10 @@ struct Engine {
 
   // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains,
   // and the split-K bookkeeping of every front (arrival counters, partial tiles).
+  long long gen = 0;  // bumped whenever solve buffers are (re)allocated (captured graphs go stale)
   void ensure_solve(int r, int slots, int nb = 1) {
     if (r == R && slots <= nslots && nb == nbuf) return;
+    ++gen;
     R = r;
     nbuf = nb;
     ngr = (R + 7) / 8;  // arrival / partial slots per (front, band): one per 8-RHS group
@@ -1050,6 +1052,7 @@ struct DdmHandle {
   void comm_allreduce(double* buf, long long count);
 
   ~DdmHandle() {
+    drop_graphs();
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
@@ -1073,6 +1076,28 @@ struct DdmHandle {
     double2* dout;
   };
   void run(int nrounds, bool track, bool timed, const StreamIO* io = nullptr);
+  void run_body(int nrounds, bool track, bool timed, const StreamIO* io);
+  // One application from device-resident b (no streamed host I/O, one process) is a fixed
+  // sequence of ~8 launches per macro-step; it is captured once per (rounds, track, timed) and
+  // state generation into a CUDA graph and replayed (HS_GRAPH=0 launches it stream by stream).
+  struct AppGraph {
+    int rounds;
+    bool track, timed;
+    long long gen;
+    long long launches;
+    cudaGraphExec_t exec;
+  };
+  std::vector<AppGraph> graphs;
+  long long state_gen = 0;
+  bool capturing = false;
+  // timing events inside a captured application must be graph event-record nodes
+  void record(cudaEvent_t e, cudaStream_t st) const {
+    HS_CUDA(cudaEventRecordWithFlags(e, st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+  }
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
   void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps);
   void reports(int nrounds, bool track, hs_solve_report* out);
 };
@@ -1706,6 +1731,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   }
   eng.ensure_solve(r, max_width, nbuf);
   if (!new_rounds && !new_r) return;
+  ++state_gen;
   R = r;
   build_items();
   const int nsub = geom.nsub;
@@ -1748,6 +1774,54 @@ void DdmHandle::ensure_gop() {
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
 void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
+  static bool use_graph = !(std::getenv("HS_GRAPH") && std::atoi(std::getenv("HS_GRAPH")) == 0);
+  if (io || partitioned() || !use_graph || std::getenv("HS_TRACE")) {
+    run_body(nrounds, track, timed, io);
+    return;
+  }
+  if (track) ensure_gop();  // synchronous setup stays outside the capture
+  const long long gen = state_gen * 1000003LL + eng.gen;
+  AppGraph* hit = nullptr;
+  for (auto& g : graphs)
+    if (g.rounds == nrounds && g.track == track && g.timed == timed && g.gen == gen) hit = &g;
+  if (!hit) {
+    for (auto& g : graphs)
+      if (g.gen != gen) {  // buffers were reallocated since: every graph is stale
+        drop_graphs();
+        break;
+      }
+    cudaStream_t s = eng.stream;
+    const long long l0 = g_kernel_launches.load();
+    cudaGraph_t graph = nullptr;
+    HS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    bool ok = true;
+    capturing = true;
+    try {
+      run_body(nrounds, track, timed, nullptr);
+    } catch (const Error&) {
+      ok = false;
+    }
+    capturing = false;
+    const cudaError_t ec = cudaStreamEndCapture(s, &graph);
+    AppGraph g{nrounds, track, timed, gen, g_kernel_launches.load() - l0, nullptr};
+    g_kernel_launches.fetch_sub(g.launches);  // counted when the graph runs
+    if (ok && ec == cudaSuccess && graph && cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
+      cudaGraphDestroy(graph);
+      graphs.push_back(g);
+    } else {  // capture unsupported here: launch stream by stream from now on
+      if (graph) cudaGraphDestroy(graph);
+      (void)cudaGetLastError();
+      use_graph = false;
+      run_body(nrounds, track, timed, nullptr);
+      return;
+    }
+    hit = &graphs.back();
+  }
+  HS_CUDA(cudaGraphLaunch(hit->exec, eng.stream));
+  g_kernel_launches.fetch_add(hit->launches);
+}
+
+void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io) {
   cudaStream_t s = eng.stream;
   const int nsub = geom.nsub;
   if (track) ensure_gop();
@@ -1755,7 +1829,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
   HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(unsigned), s));
   HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(unsigned), s));
   HS_CUDA(cudaMemsetAsync(tface.p, 0, tface.n * sizeof(unsigned), s));
-  if (timed) HS_CUDA(cudaEventRecord(ev[0], s));
+  if (timed) record(ev[0], s);
   SweepArgs sa{};
   sa.g = geom;
   sa.cls = eng.d_cls.p;
@@ -1802,13 +1876,13 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
       for (const int2& t : msteps_own[m]) full |= t.y == 1 || t.y - nbuf == 1;
       launch_build_rhs(sa, full ? eng.n_max : 0, static_cast<int>(line_max), s);
     }
-    if (timed) HS_CUDA(cudaEventRecord(ev[1 + nsweeps + 2 * m], s));
+    if (timed) record(ev[1 + nsweeps + 2 * m], s);
     const char* tstep = std::getenv("HS_TRACE_STEP");
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
     if (sa.ntasks > 0)
       eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced,
                     no_skip ? nullptr : tface.p, no_skip ? nullptr : need.p, need_words);
-    if (timed) HS_CUDA(cudaEventRecord(ev[2 + nsweeps + 2 * m], s));
+    if (timed) record(ev[2 + nsweeps + 2 * m], s);
     if (sa.ntasks > 0) launch_extract_deposit(sa, static_cast<int>(line_max), s);
     if (partitioned() && !xplan[m].peers.empty()) {  // traces and ghost values to / from other ranks
       const XPlan& xp = xplan[m];
@@ -1837,7 +1911,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     };
     auto after_sweep = [&](int l, int nb) {  // sweep l fully accumulated (nb < 0: norms reduced already)
       if (nb >= 0) launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
-      if (timed) HS_CUDA(cudaEventRecord(ev[l], s));
+      if (timed) record(ev[l], s);
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
         const int last = static_cast<int>(stripe_n.size()) - 2;
         if (io && waited < last) stage_in(last);  // the residual reads all of b
@@ -1863,7 +1937,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     for (int l : acc_after[m]) after_sweep(l, accumulate(l, 0, geom.gn, 0));
     if (fuse_acc && timed)  // sweeps that end here (their contributions are accumulated at the end)
       for (int l = 1; l < nsweeps; ++l)
-        if (sweep_end_m[l] == m) HS_CUDA(cudaEventRecord(ev[l], s));
+        if (sweep_end_m[l] == m) record(ev[l], s);
     // the last sweep (every sweep, fused), stripe by stripe (partials in stripe order: a fixed
     // reduction order)
     const int nst = static_cast<int>(acc_stripe_m.size());
@@ -1890,7 +1964,7 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
         stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
       }
       if (io) launch_transpose_out_range(u.p, io->dout, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
-      HS_CUDA(cudaEventRecord(ev_out[j], s));
+      record(ev_out[j], s);
       if (++stripes_done == nst) {
         int nbt = 0;
         for (int q = 0; q < nst; ++q) nbt += stripe_blocks[q];
