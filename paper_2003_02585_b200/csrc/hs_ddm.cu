@@ -985,7 +985,15 @@ struct DdmHandle {
   // streamed host transfers: stripes of the slowest axis, and per macro-step the last stripe of b
   // its sweep-1 tasks read (-1: none)
   std::vector<long long> stripe_n;  // node bounds, size nstripe + 1
-  std::vector<int> need_stripe;
+  // b travels in tiles (a stripe x a segment of the fastest axis), in the order the sweep-1
+  // tasks first read them: the early macro-steps wait only for their own subdomains' part of b
+  struct InTile {
+    long long row0, row1;  // rows of the fastest axis (gsize[0] nodes each)
+    int x0, x1;            // fastest-axis columns
+    int need;              // first macro-step reading it (nmacro: only the residual)
+  };
+  std::vector<InTile> in_tiles;  // copy order
+  std::vector<int> need_tiles;   // per macro-step: leading tiles (copy order) it needs
   // the last sweep is accumulated stripe by stripe, after the macro-step that completes the
   // stripe (acc_stripe_m), so streamed transfers can copy u out while the tail still runs
   std::vector<int> acc_stripe_m;
@@ -1552,18 +1560,38 @@ void DdmHandle::build_schedule() {
     const int rows = geom.gsize[la], ns = std::max(1, std::min(rows, spr * part.counts[la]));
     stripe_n.assign(ns + 1, 0);
     for (int j = 0; j <= ns; ++j) stripe_n[j] = plane * ((static_cast<long long>(rows) * j) / ns);
-    need_stripe.assign(nmacro, -1);
-    int need = -1;
-    for (int m = 0; m < nmacro; ++m) {
-      for (const int2& t : msteps[m]) {
-        if (t.y != 1) continue;
-        const GridRange sup = wts.support(subs[t.x].sub);
-        const long long last = (static_cast<long long>(sup.hi[la] - geom.glo[la]) + 1) * plane;  // nodes needed
-        int j = 0;
-        while (j < ns - 1 && stripe_n[j + 1] < last) ++j;
-        need = std::max(need, j);
+    {
+      int spx = std::max(1, part.counts[0]);  // segments of the fastest axis (HS_TILE_SEGS: developer knob)
+      if (const char* e = std::getenv("HS_TILE_SEGS")) spx = std::max(1, std::atoi(e));
+      const int gx = geom.gsize[0];
+      spx = std::min(spx, gx);
+      in_tiles.clear();
+      for (int j = 0; j < ns; ++j)
+        for (int c = 0; c < spx; ++c) {
+          InTile t{stripe_n[j] / gx, stripe_n[j + 1] / gx, static_cast<int>((static_cast<long long>(gx) * c) / spx),
+                   static_cast<int>((static_cast<long long>(gx) * (c + 1)) / spx), nmacro};
+          if (t.x1 <= t.x0 || t.row1 <= t.row0) continue;
+          const long long sl0 = stripe_n[j] / plane, sl1 = (stripe_n[j + 1] + plane - 1) / plane;  // slowest-axis rows
+          for (int m = 0; m < nmacro && t.need == nmacro; ++m)
+            for (const int2& tk : msteps[m]) {
+              if (tk.y != 1) continue;
+              const GridRange sup = wts.support(subs[tk.x].sub);
+              const long long a0 = sup.lo[la] - geom.glo[la], a1 = sup.hi[la] - geom.glo[la] + 1;
+              const int b0 = sup.lo[0] - geom.glo[0], b1 = sup.hi[0] - geom.glo[0] + 1;
+              if (a0 < sl1 && a1 > sl0 && b0 < t.x1 && b1 > t.x0) {
+                t.need = m;
+                break;
+              }
+            }
+          in_tiles.push_back(t);
+        }
+      std::stable_sort(in_tiles.begin(), in_tiles.end(), [](const InTile& a, const InTile& b) { return a.need < b.need; });
+      need_tiles.assign(nmacro, 0);
+      for (int m = 0; m < nmacro; ++m) {
+        int k = 0;
+        while (k < static_cast<int>(in_tiles.size()) && in_tiles[k].need <= m) ++k;
+        need_tiles[m] = k;
       }
-      need_stripe[m] = need;
     }
     // stripes of the last sweep's accumulate (of every sweep's, fused)
     fuse_acc = nsweeps <= nbuf && nsweeps <= HS_MAX_ACC_SWEEPS && !std::getenv("HS_NO_FUSED_ACC");
@@ -1847,13 +1875,14 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   sa.tface = tface.p;
   sa.route = route.p;
   const int nm = static_cast<int>(msteps.size());
-  int waited = -1, stripes_done = 0;
+  int waited = 0, stripes_done = 0;  // waited: tiles of b staged (copy order)
   bool u_reduced = false;
   static const bool no_skip = std::getenv("HS_NO_FRONT_SKIP") != nullptr;  // developer A/B switch
-  auto stage_in = [&](int upto) {  // stripes (waited, upto] of b: copied -> transposed into bN
-    for (int j = waited + 1; j <= upto; ++j) {
-      HS_CUDA(cudaStreamWaitEvent(s, io->copied[j], 0));
-      launch_transpose_in_range(io->din, bN.p, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
+  auto stage_in = [&](int upto) {  // tiles [waited, upto) of b: copied -> transposed into bN
+    for (int k = waited; k < upto; ++k) {
+      const InTile& t = in_tiles[k];
+      HS_CUDA(cudaStreamWaitEvent(s, io->copied[k], 0));
+      launch_transpose_in_tile(io->din, bN.p, geom.gn, R, geom.gsize[0], t.x0, t.x1, t.row0, t.row1, s);
     }
     waited = std::max(waited, upto);
   };
@@ -1865,9 +1894,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     return b;
   };
   for (int m = 0; m < nm; ++m) {
-    if (io && need_stripe[m] > waited) {  // streamed b: the stripes this macro-step's sources read
-      stage_in(need_stripe[m]);
-    }
+    if (io && need_tiles[m] > waited) stage_in(need_tiles[m]);  // streamed b: the tiles this step's sources read
     sa.tasks = d_mtasks.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps_own[m].size());
     if (sa.ntasks > 0) {
@@ -1913,7 +1940,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
       if (nb >= 0) launch_reduce_partials(partial.p, nb, R, norms.p + static_cast<size_t>(l - 1) * R, s);
       if (timed) record(ev[l], s);
       if (track && l % ndir == 0) {  // per-round relative residual (src/sweeper.cpp:313-325)
-        const int last = static_cast<int>(stripe_n.size()) - 2;
+        const int last = static_cast<int>(in_tiles.size());
         if (io && waited < last) stage_in(last);  // the residual reads all of b
         const int rr = l / ndir - 1;
         const double2* ures = u.p;
@@ -2084,15 +2111,16 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
   }
 }
 
-// One batch from / to pinned host buffers with the transfers overlapped: b streams in by
-// stripes of the slowest axis on a copy stream while the first macro-steps (which only read the
-// stripes their sweep-1 sources touch) run; u streams out by stripes while the residual runs.
+// One batch from / to pinned host buffers with the transfers overlapped: b streams in by tiles
+// (stripe of the slowest axis x segment of the fastest) on a copy stream, in the order the
+// sweep-1 sources first read them, while the first macro-steps run; u streams out by stripes
+// while the tail of the application runs.
 void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps) {
   ensure_state(nr, nrounds);
   const long long n = geom.gn;
-  const int ns = static_cast<int>(stripe_n.size()) - 1;
+  const int ns = static_cast<int>(stripe_n.size()) - 1, nt = static_cast<int>(in_tiles.size());
   if (!cstream) HS_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
-  while (static_cast<int>(ev_in.size()) < ns + 2) {
+  while (static_cast<int>(ev_in.size()) < nt + 2) {
     cudaEvent_t e;
     HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev_in.push_back(e);
@@ -2102,15 +2130,25 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   double2* dout = io.p + static_cast<size_t>(n) * kMaxRhs;
   // the copy stream may overwrite din only after earlier work on the compute stream; it carries
   // the copies only (DMA engines), never kernels
-  HS_CUDA(cudaEventRecord(ev_in[ns], eng.stream));
-  HS_CUDA(cudaStreamWaitEvent(cstream, ev_in[ns], 0));
+  HS_CUDA(cudaEventRecord(ev_in[nt], eng.stream));
+  HS_CUDA(cudaStreamWaitEvent(cstream, ev_in[nt], 0));
   const size_t pitch = static_cast<size_t>(n) * sizeof(double2);
-  for (int j = 0; j < ns; ++j) {
-    const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
-    HS_CUDA(cudaMemcpy2DAsync(din + n0, pitch, reinterpret_cast<const double2*>(b) + n0, pitch,
-                              static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyHostToDevice, cstream));
-    HS_CUDA(cudaEventRecord(ev_in[j], cstream));
-  }
+  const size_t gx = static_cast<size_t>(geom.gsize[0]), rows = static_cast<size_t>(n) / gx;
+  auto copy_in = [&](const cudaEvent_t* evs) {  // tiles of b in need order: one 3D copy each (x, rows, RHS)
+    for (int k = 0; k < nt; ++k) {
+      const InTile& t = in_tiles[k];
+      cudaMemcpy3DParms c{};
+      c.srcPtr = make_cudaPitchedPtr(const_cast<double*>(b), gx * sizeof(double2), gx * sizeof(double2), rows);
+      c.dstPtr = make_cudaPitchedPtr(din, gx * sizeof(double2), gx * sizeof(double2), rows);
+      c.srcPos = c.dstPos = make_cudaPos(t.x0 * sizeof(double2), static_cast<size_t>(t.row0), 0);
+      c.extent = make_cudaExtent(static_cast<size_t>(t.x1 - t.x0) * sizeof(double2), static_cast<size_t>(t.row1 - t.row0),
+                                 static_cast<size_t>(nr));
+      c.kind = cudaMemcpyHostToDevice;
+      HS_CUDA(cudaMemcpy3DAsync(&c, cstream));
+      HS_CUDA(cudaEventRecord(evs[k], cstream));
+    }
+  };
+  copy_in(ev_in.data());
   const StreamIO sio{ev_in.data(), din, dout};
   run(nrounds, track, true, &sio);
   // each stripe of u is transposed out after its accumulate of the last sweep (ev_out); copy the
@@ -2124,52 +2162,51 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
                               static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
   }
-  HS_CUDA(cudaEventRecord(ev_in[ns + 1], cstream));
-  HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[ns + 1], 0));  // later work may reuse io / u
+  HS_CUDA(cudaEventRecord(ev_in[nt + 1], cstream));
+  HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[nt + 1], 0));  // later work may reuse io / u
   if (const char* path = std::getenv("HS_STREAM_TRACE")) {  // developer timeline (timing events)
-    std::vector<cudaEvent_t> te(3 * ns + 2);
-    // re-run the same schedule with timing events: H2D done per stripe, u stripe out per stripe
+    // te: [0] start, [1, 1 + nt) tile copied, then per stripe u final / copied out, then compute end
+    std::vector<cudaEvent_t> te(nt + 2 * ns + 2);
+    const int uf = 1 + nt, ud = 1 + nt + ns, ce = 1 + nt + 2 * ns;
+    // re-run the same schedule with timing events: H2D done per tile, u stripe out per stripe
     HS_CUDA(cudaStreamSynchronize(cstream));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
     for (auto& e : te) HS_CUDA(cudaEventCreate(&e));
     HS_CUDA(cudaEventRecord(te[0], eng.stream));
     HS_CUDA(cudaStreamWaitEvent(cstream, te[0], 0));
-    for (int j = 0; j < ns; ++j) {
-      const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
-      HS_CUDA(cudaMemcpy2DAsync(din + n0, pitch, reinterpret_cast<const double2*>(b) + n0, pitch,
-                                static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyHostToDevice, cstream));
-      HS_CUDA(cudaEventRecord(te[1 + j], cstream));
-    }
+    copy_in(te.data() + 1);
     const StreamIO tio{te.data() + 1, din, dout};
     run(nrounds, track, true, &tio);
     for (int q = 0; q < ns; ++q) {
       const int j = order[q];
       HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
-      HS_CUDA(cudaEventRecord(te[1 + ns + j], cstream));  // stripe final on the device
+      HS_CUDA(cudaEventRecord(te[uf + j], cstream));  // stripe final on the device
       const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
       HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
                                 static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
-      HS_CUDA(cudaEventRecord(te[1 + 2 * ns + j], cstream));
+      HS_CUDA(cudaEventRecord(te[ud + j], cstream));
     }
-    HS_CUDA(cudaEventRecord(te[3 * ns + 1], eng.stream));
+    HS_CUDA(cudaEventRecord(te[ce], eng.stream));
     HS_CUDA(cudaStreamSynchronize(cstream));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
     if (FILE* fp = std::fopen(path, "w")) {
       float t = 0.f;
       std::fprintf(fp, "what,index,ms\n");
+      for (int k = 0; k < nt; ++k) {
+        cudaEventElapsedTime(&t, te[0], te[1 + k]);
+        std::fprintf(fp, "h2d_done,%d,%.3f\n", k, t);
+      }
       for (int j = 0; j < ns; ++j) {
-        cudaEventElapsedTime(&t, te[0], te[1 + j]);
-        std::fprintf(fp, "h2d_done,%d,%.3f\n", j, t);
-        cudaEventElapsedTime(&t, te[0], te[1 + ns + j]);
+        cudaEventElapsedTime(&t, te[0], te[uf + j]);
         std::fprintf(fp, "u_final,%d,%.3f\n", j, t);
-        cudaEventElapsedTime(&t, te[0], te[1 + 2 * ns + j]);
+        cudaEventElapsedTime(&t, te[0], te[ud + j]);
         std::fprintf(fp, "d2h_done,%d,%.3f\n", j, t);
       }
       for (size_t m = 0; m < msteps.size(); ++m) {
         cudaEventElapsedTime(&t, te[0], ev[1 + nsweeps + 2 * m]);
         std::fprintf(fp, "mstep_solve_start,%zu,%.3f\n", m, t);
       }
-      cudaEventElapsedTime(&t, te[0], te[3 * ns + 1]);
+      cudaEventElapsedTime(&t, te[0], te[ce]);
       std::fprintf(fp, "compute_end,0,%.3f\n", t);
       std::fclose(fp);
     }

@@ -679,6 +679,24 @@ __global__ void transpose_out_kernel(const double2* src, double2* dst, long long
   }
 }
 
+// The same for a tile of rows [row0, row0 + gridDim.y) x columns [x0, x1) of the fastest axis
+// (gx nodes per row): block (i, y) transposes 32 nodes of row row0 + y.
+__global__ void transpose_in_tile_kernel(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                                         long long row0) {
+  __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
+  const long long rowb = (row0 + blockIdx.y) * gx;
+  const long long base = rowb + x0 + static_cast<long long>(blockIdx.x) * kTransNodes, end = rowb + x1;
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
+    const int r = e / kTransNodes, i = e % kTransNodes;
+    if (base + i < end) tile[i][r] = src[static_cast<long long>(r) * n + base + i];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
+    const int i = e / R, r = e % R;
+    if (base + i < end) dst[(base + i) * R + r] = tile[i][r];
+  }
+}
+
 __global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
 
 int blocks_for(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
@@ -911,6 +929,13 @@ void launch_transpose_in_range(const double2* src, double2* dst, long long n, in
   if (n1 <= n0) return;
   transpose_in_kernel<<<static_cast<int>((n1 - n0 + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R,
                                                                                                      n0, n1);
+  after_launch();
+}
+void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                              long long row0, long long row1, cudaStream_t s) {
+  if (x1 <= x0 || row1 <= row0) return;
+  const dim3 grid((x1 - x0 + kTransNodes - 1) / kTransNodes, static_cast<unsigned>(row1 - row0));
+  transpose_in_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0);
   after_launch();
 }
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,

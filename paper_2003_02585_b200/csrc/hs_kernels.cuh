@@ -152,6 +152,8 @@ void launch_bump_epoch(unsigned* epoch, unsigned by, cudaStream_t s);
 // node range [n0, n1) only (streamed host transfers)
 void launch_transpose_in_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                cudaStream_t s);
+void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                              long long row0, long long row1, cudaStream_t s);
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                 cudaStream_t s);
 
