@@ -997,11 +997,25 @@ struct DdmHandle {
   // the last sweep is accumulated stripe by stripe, after the macro-step that completes the
   // stripe (acc_stripe_m), so streamed transfers can copy u out while the tail still runs
   std::vector<int> acc_stripe_m;
+  // final regions of u: the stripes, or (streamed, fused accumulate) the tiles of b's tiling,
+  // which the last sweep's diagonal wavefront completes earlier than whole stripes, so the copy
+  // of u to the host starts earlier
+  struct OutRegion {
+    long long row0, row1;  // rows of the fastest axis
+    int x0, x1;
+    int acc_m;  // macro-step after which the region is final
+  };
+  std::vector<OutRegion> out_stripes, out_tiles;
+  const std::vector<OutRegion>& out_regions(bool streamed) const {
+    static const bool stripes_only = std::getenv("HS_OUT_STRIPES") != nullptr;  // developer A/B switch
+    return streamed && fuse_acc && !out_tiles.empty() && !stripes_only ? out_tiles : out_stripes;
+  }
   // every sweep in its own x buffer (sweeps <= buffers): all contributions are accumulated in one
   // pass per stripe at the end (accumulate_all_kernel) instead of one pass per sweep
   bool fuse_acc = false;
   std::vector<int> sweep_end_m;  // per sweep: the macro-step its last task runs in
-  cudaStream_t cstream = nullptr;
+  static constexpr int kCopyStreams = 2;  // streamed host I/O: b in, u out
+  cudaStream_t cs[kCopyStreams] = {};
   std::vector<cudaEvent_t> ev_in, ev_out;
   DBuf<int2> d_mtasks;
   DBuf<SolveItem> d_tasks;
@@ -1064,7 +1078,8 @@ struct DdmHandle {
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
-    if (cstream) cudaStreamDestroy(cstream);
+    for (auto c : cs)
+      if (c) cudaStreamDestroy(c);
     if (gfact) hs_factor_destroy(gfact);
   }
 
@@ -1561,9 +1576,11 @@ void DdmHandle::build_schedule() {
     stripe_n.assign(ns + 1, 0);
     for (int j = 0; j <= ns; ++j) stripe_n[j] = plane * ((static_cast<long long>(rows) * j) / ns);
     {
-      int spx = std::max(1, part.counts[0]);  // segments of the fastest axis (HS_TILE_SEGS: developer knob)
-      if (const char* e = std::getenv("HS_TILE_SEGS")) spx = std::max(1, std::atoi(e));
+      // segments of the fastest axis: at most one per subdomain column, and rows of at least 4 KB
+      // (narrower 3D copies lose DMA bandwidth: C2 e2e 17.9 ms at 8 segments, 16.7 at 4)
       const int gx = geom.gsize[0];
+      int spx = std::max(1, std::min(part.counts[0], gx * static_cast<int>(sizeof(double2)) / 4096));
+      if (const char* e = std::getenv("HS_TILE_SEGS")) spx = std::max(1, std::atoi(e));  // developer knob
       spx = std::min(spx, gx);
       in_tiles.clear();
       for (int j = 0; j < ns; ++j)
@@ -1597,7 +1614,10 @@ void DdmHandle::build_schedule() {
     fuse_acc = nsweeps <= nbuf && nsweeps <= HS_MAX_ACC_SWEEPS && !std::getenv("HS_NO_FUSED_ACC");
     sweep_end_m.assign(nsweeps + 1, 0);
     for (int l = 1; l <= nsweeps; ++l) sweep_end_m[l] = accl[l] - 1;
-    acc_stripe_m.assign(ns, nsweeps > 1 ? accl[nsweeps - 1] - 1 : 0);
+    // unfused, the last sweep's striped accumulate follows the whole-domain accumulate of the one
+    // before it (u += in sweep order); fused, a region is final after its own tasks
+    const int acc_m0 = fuse_acc || nsweeps == 1 ? 0 : accl[nsweeps - 1] - 1;
+    acc_stripe_m.assign(ns, acc_m0);
     for (int l = fuse_acc ? 1 : nsweeps; l <= nsweeps; ++l)
       for (int id = 0; id < nsub; ++id) {
         const int m = mstep_of[static_cast<size_t>(l - 1) * nsub + id];
@@ -1607,6 +1627,29 @@ void DdmHandle::build_schedule() {
         for (int j = 0; j < ns; ++j)
           if (stripe_n[j] < hi && stripe_n[j + 1] > lo) acc_stripe_m[j] = std::max(acc_stripe_m[j], m);
       }
+    {
+      const int gx = geom.gsize[0];
+      out_stripes.clear();
+      for (int j = 0; j < ns; ++j) out_stripes.push_back(OutRegion{stripe_n[j] / gx, stripe_n[j + 1] / gx, 0, gx, acc_stripe_m[j]});
+      out_tiles.clear();
+      if (fuse_acc)
+        for (const InTile& t : in_tiles) {
+          OutRegion o{t.row0, t.row1, t.x0, t.x1, acc_m0};
+          const long long sl0 = t.row0 * gx / plane, sl1 = (t.row1 * gx + plane - 1) / plane;
+          for (int l = 1; l <= nsweeps; ++l)
+            for (int id = 0; id < nsub; ++id) {
+              const GridRange sup = wts.support(subs[id].sub);
+              const long long a0 = sup.lo[la] - geom.glo[la], a1 = sup.hi[la] - geom.glo[la] + 1;
+              const int b0 = sup.lo[0] - geom.glo[0], b1 = sup.hi[0] - geom.glo[0] + 1;
+              if (a0 < sl1 && a1 > sl0 && b0 < t.x1 && b1 > t.x0)
+                o.acc_m = std::max(o.acc_m, mstep_of[static_cast<size_t>(l - 1) * nsub + id]);
+            }
+          out_tiles.push_back(o);
+        }
+      std::sort(out_tiles.begin(), out_tiles.end(), [](const OutRegion& a, const OutRegion& b) {
+        return a.acc_m != b.acc_m ? a.acc_m < b.acc_m : a.row0 != b.row0 ? a.row0 < b.row0 : a.x0 < b.x0;
+      });
+    }
     for (int l = 1; l <= nsweeps; ++l) {  // the striped accumulate replaces the whole-domain ones
       auto& v = acc_after[accl[l] - 1];
       if (l == nsweeps || fuse_acc) v.erase(std::remove(v.begin(), v.end(), l), v.end());
@@ -1770,7 +1813,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   bN.alloc(static_cast<size_t>(geom.gn) * R);
   u.alloc(static_cast<size_t>(geom.gn) * R);
   // + striped rounding + reduction scratch
-  const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(stripe_n.size()) + kReducePad;
+  const long long nb = (geom.gn * R + 255) / 256 + static_cast<long long>(std::max(stripe_n.size(), out_tiles.size() + 1)) + kReducePad;
   partial_stride = nb * R;
   partial.alloc(static_cast<size_t>(nb) * R * (fuse_acc ? nsweeps : 1));
   pnum.alloc(static_cast<size_t>(nb) * R);
@@ -1782,7 +1825,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   ev.assign(1 + nsweeps + 2 * msteps.size(), nullptr);
   for (auto& e : ev) HS_CUDA(cudaEventCreate(&e));
   for (auto e : ev_out) cudaEventDestroy(e);
-  ev_out.assign(stripe_n.size() - 1, nullptr);
+  ev_out.assign(std::max(out_stripes.size(), out_tiles.size()), nullptr);
   for (auto& e : ev_out) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
@@ -1886,11 +1929,14 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     }
     waited = std::max(waited, upto);
   };
-  std::vector<int> stripe_blocks(acc_stripe_m.size(), 0);
-  auto stripe_pbase = [&](int j) {  // partial blocks of the stripes before j (worst case per stripe)
+  const std::vector<OutRegion>& regs = out_regions(io != nullptr);
+  const int gx = geom.gsize[0];
+  auto reg_cnt = [&](const OutRegion& o) { return (o.row1 - o.row0) * (o.x1 - o.x0); };
+  std::vector<int> stripe_blocks(regs.size(), 0);
+  auto stripe_pbase = [&](int j) {  // partial blocks of the regions before j (exact: one block per npb nodes)
     const int npb = 256 / R;
     long long b = 0;
-    for (int q = 0; q < j; ++q) b += (stripe_n[q + 1] - stripe_n[q] + npb - 1) / npb;
+    for (int q = 0; q < j; ++q) b += (reg_cnt(regs[q]) + npb - 1) / npb;
     return b;
   };
   for (int m = 0; m < nm; ++m) {
@@ -1967,9 +2013,10 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
         if (sweep_end_m[l] == m) record(ev[l], s);
     // the last sweep (every sweep, fused), stripe by stripe (partials in stripe order: a fixed
     // reduction order)
-    const int nst = static_cast<int>(acc_stripe_m.size());
+    const int nst = static_cast<int>(regs.size());
     for (int j = 0; j < nst; ++j) {
-      if (acc_stripe_m[j] != m) continue;
+      const OutRegion& rg = regs[j];
+      if (rg.acc_m != m) continue;
       if (fuse_acc) {
         AccumAllArgs aa{};
         aa.g = geom;
@@ -1984,13 +2031,16 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
         aa.u = u.p;
         aa.partial = partial.p + stripe_pbase(j) * R;
         aa.pstride = partial_stride;
-        aa.n0 = stripe_n[j];
-        aa.n1 = stripe_n[j + 1];
+        aa.row0 = rg.row0;
+        aa.cnt = reg_cnt(rg);
+        aa.gx = gx;
+        aa.x0 = rg.x0;
+        aa.w = rg.x1 - rg.x0;
         stripe_blocks[j] = launch_accumulate_all(aa, s);
-      } else {
-        stripe_blocks[j] = accumulate(nsweeps, stripe_n[j], stripe_n[j + 1], stripe_pbase(j));
+      } else {  // regions are the stripes here
+        stripe_blocks[j] = accumulate(nsweeps, rg.row0 * gx, rg.row1 * gx, stripe_pbase(j));
       }
-      if (io) launch_transpose_out_range(u.p, io->dout, geom.gn, R, stripe_n[j], stripe_n[j + 1], s);
+      if (io) launch_transpose_out_tile(u.p, io->dout, geom.gn, R, gx, rg.x0, rg.x1, rg.row0, rg.row1, s);
       record(ev_out[j], s);
       if (++stripes_done == nst) {
         int nbt = 0;
@@ -2112,15 +2162,17 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
 }
 
 // One batch from / to pinned host buffers with the transfers overlapped: b streams in by tiles
-// (stripe of the slowest axis x segment of the fastest) on a copy stream, in the order the
-// sweep-1 sources first read them, while the first macro-steps run; u streams out by stripes
-// while the tail of the application runs.
+// (stripe of the slowest axis x segment of the fastest), in the order the sweep-1 sources first
+// read them, while the first macro-steps run; u streams out by regions (tiles when the accumulate
+// is fused, else stripes) as the tail of the application completes them. One copy stream per
+// direction; the copy streams carry copies only, never kernels.
 void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps) {
   ensure_state(nr, nrounds);
   const long long n = geom.gn;
-  const int ns = static_cast<int>(stripe_n.size()) - 1, nt = static_cast<int>(in_tiles.size());
-  if (!cstream) HS_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
-  while (static_cast<int>(ev_in.size()) < nt + 2) {
+  const int nt = static_cast<int>(in_tiles.size());
+  for (auto& c : cs)
+    if (!c) HS_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+  while (static_cast<int>(ev_in.size()) < nt + 1 + kCopyStreams) {
     cudaEvent_t e;
     HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev_in.push_back(e);
@@ -2128,66 +2180,68 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
   double2* din = io.p;
   double2* dout = io.p + static_cast<size_t>(n) * kMaxRhs;
-  // the copy stream may overwrite din only after earlier work on the compute stream; it carries
-  // the copies only (DMA engines), never kernels
+  // the copy streams may overwrite din only after earlier work on the compute stream
   HS_CUDA(cudaEventRecord(ev_in[nt], eng.stream));
-  HS_CUDA(cudaStreamWaitEvent(cstream, ev_in[nt], 0));
-  const size_t pitch = static_cast<size_t>(n) * sizeof(double2);
+  for (auto c : cs) HS_CUDA(cudaStreamWaitEvent(c, ev_in[nt], 0));
   const size_t gx = static_cast<size_t>(geom.gsize[0]), rows = static_cast<size_t>(n) / gx;
-  auto copy_in = [&](const cudaEvent_t* evs) {  // tiles of b in need order: one 3D copy each (x, rows, RHS)
+  auto copy3d = [&](const void* src, void* dst, int x0, int x1, long long r0, long long r1, cudaMemcpyKind kind,
+                    cudaStream_t st) {  // (x, rows, RHS) box of the RHS-major grid
+    cudaMemcpy3DParms c{};
+    c.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), gx * sizeof(double2), gx * sizeof(double2), rows);
+    c.dstPtr = make_cudaPitchedPtr(dst, gx * sizeof(double2), gx * sizeof(double2), rows);
+    c.srcPos = c.dstPos = make_cudaPos(x0 * sizeof(double2), static_cast<size_t>(r0), 0);
+    c.extent = make_cudaExtent(static_cast<size_t>(x1 - x0) * sizeof(double2), static_cast<size_t>(r1 - r0),
+                               static_cast<size_t>(nr));
+    c.kind = kind;
+    HS_CUDA(cudaMemcpy3DAsync(&c, st));
+  };
+  auto copy_in = [&](const cudaEvent_t* evs) {  // tiles of b in need order
     for (int k = 0; k < nt; ++k) {
       const InTile& t = in_tiles[k];
-      cudaMemcpy3DParms c{};
-      c.srcPtr = make_cudaPitchedPtr(const_cast<double*>(b), gx * sizeof(double2), gx * sizeof(double2), rows);
-      c.dstPtr = make_cudaPitchedPtr(din, gx * sizeof(double2), gx * sizeof(double2), rows);
-      c.srcPos = c.dstPos = make_cudaPos(t.x0 * sizeof(double2), static_cast<size_t>(t.row0), 0);
-      c.extent = make_cudaExtent(static_cast<size_t>(t.x1 - t.x0) * sizeof(double2), static_cast<size_t>(t.row1 - t.row0),
-                                 static_cast<size_t>(nr));
-      c.kind = cudaMemcpyHostToDevice;
-      HS_CUDA(cudaMemcpy3DAsync(&c, cstream));
-      HS_CUDA(cudaEventRecord(evs[k], cstream));
+      copy3d(b, din, t.x0, t.x1, t.row0, t.row1, cudaMemcpyHostToDevice, cs[0]);
+      HS_CUDA(cudaEventRecord(evs[k], cs[0]));
     }
   };
   copy_in(ev_in.data());
   const StreamIO sio{ev_in.data(), din, dout};
   run(nrounds, track, true, &sio);
-  // each stripe of u is transposed out after its accumulate of the last sweep (ev_out); copy the
-  // stripes to the host in the order they complete, while the tail of the application still runs
-  std::vector<int> order(ns);
-  for (int j = 0; j < ns; ++j) order[j] = j;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return acc_stripe_m[x] < acc_stripe_m[y]; });
-  for (int j : order) {
-    HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
-    const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
-    HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
-                              static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
+  // each region of u is transposed out after its accumulate of the last sweep (ev_out); copy the
+  // regions to the host in the order they complete, while the tail of the application still runs
+  const std::vector<OutRegion>& regs = out_regions(true);
+  const int no = static_cast<int>(regs.size());
+  std::vector<int> order(no);
+  for (int j = 0; j < no; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return regs[x].acc_m < regs[y].acc_m; });
+  auto copy_out = [&](int q, const cudaEvent_t* fin, const cudaEvent_t* done) {
+    const int j = order[q];
+    const OutRegion& o = regs[j];
+    cudaStream_t st = cs[1];
+    HS_CUDA(cudaStreamWaitEvent(st, ev_out[j], 0));
+    if (fin) HS_CUDA(cudaEventRecord(fin[j], st));
+    copy3d(dout, uh, o.x0, o.x1, o.row0, o.row1, cudaMemcpyDeviceToHost, st);
+    if (done) HS_CUDA(cudaEventRecord(done[j], st));
+  };
+  for (int q = 0; q < no; ++q) copy_out(q, nullptr, nullptr);
+  for (int c = 0; c < kCopyStreams; ++c) {  // later work may reuse io / u
+    HS_CUDA(cudaEventRecord(ev_in[nt + 1 + c], cs[c]));
+    HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[nt + 1 + c], 0));
   }
-  HS_CUDA(cudaEventRecord(ev_in[nt + 1], cstream));
-  HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[nt + 1], 0));  // later work may reuse io / u
   if (const char* path = std::getenv("HS_STREAM_TRACE")) {  // developer timeline (timing events)
-    // te: [0] start, [1, 1 + nt) tile copied, then per stripe u final / copied out, then compute end
-    std::vector<cudaEvent_t> te(nt + 2 * ns + 2);
-    const int uf = 1 + nt, ud = 1 + nt + ns, ce = 1 + nt + 2 * ns;
-    // re-run the same schedule with timing events: H2D done per tile, u stripe out per stripe
-    HS_CUDA(cudaStreamSynchronize(cstream));
+    // te: [0] start, [1, 1 + nt) tile copied, then per region u final / copied out, then compute end
+    std::vector<cudaEvent_t> te(nt + 2 * no + 2);
+    const int uf = 1 + nt, ud = 1 + nt + no, ce = 1 + nt + 2 * no;
+    // re-run the same schedule with timing events
+    for (auto c : cs) HS_CUDA(cudaStreamSynchronize(c));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
     for (auto& e : te) HS_CUDA(cudaEventCreate(&e));
     HS_CUDA(cudaEventRecord(te[0], eng.stream));
-    HS_CUDA(cudaStreamWaitEvent(cstream, te[0], 0));
+    for (auto c : cs) HS_CUDA(cudaStreamWaitEvent(c, te[0], 0));
     copy_in(te.data() + 1);
     const StreamIO tio{te.data() + 1, din, dout};
     run(nrounds, track, true, &tio);
-    for (int q = 0; q < ns; ++q) {
-      const int j = order[q];
-      HS_CUDA(cudaStreamWaitEvent(cstream, ev_out[j], 0));
-      HS_CUDA(cudaEventRecord(te[uf + j], cstream));  // stripe final on the device
-      const long long n0 = stripe_n[j], n1 = stripe_n[j + 1];
-      HS_CUDA(cudaMemcpy2DAsync(reinterpret_cast<double2*>(uh) + n0, pitch, dout + n0, pitch,
-                                static_cast<size_t>(n1 - n0) * sizeof(double2), nr, cudaMemcpyDeviceToHost, cstream));
-      HS_CUDA(cudaEventRecord(te[ud + j], cstream));
-    }
+    for (int q = 0; q < no; ++q) copy_out(q, te.data() + uf, te.data() + ud);
     HS_CUDA(cudaEventRecord(te[ce], eng.stream));
-    HS_CUDA(cudaStreamSynchronize(cstream));
+    for (auto c : cs) HS_CUDA(cudaStreamSynchronize(c));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
     if (FILE* fp = std::fopen(path, "w")) {
       float t = 0.f;
@@ -2196,7 +2250,7 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
         cudaEventElapsedTime(&t, te[0], te[1 + k]);
         std::fprintf(fp, "h2d_done,%d,%.3f\n", k, t);
       }
-      for (int j = 0; j < ns; ++j) {
+      for (int j = 0; j < no; ++j) {
         cudaEventElapsedTime(&t, te[0], te[uf + j]);
         std::fprintf(fp, "u_final,%d,%.3f\n", j, t);
         cudaEventElapsedTime(&t, te[0], te[ud + j]);
@@ -2213,7 +2267,7 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     for (auto e : te) cudaEventDestroy(e);
   }
   if (reps) reports(nrounds, track, reps);
-  HS_CUDA(cudaStreamSynchronize(cstream));
+  for (auto c : cs) HS_CUDA(cudaStreamSynchronize(c));
   HS_CUDA(cudaStreamSynchronize(eng.stream));
 }
 

@@ -697,6 +697,22 @@ __global__ void transpose_in_tile_kernel(const double2* src, double2* dst, long 
   }
 }
 
+__global__ void transpose_out_tile_kernel(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                                          long long row0) {
+  __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
+  const long long rowb = (row0 + blockIdx.y) * gx;
+  const long long base = rowb + x0 + static_cast<long long>(blockIdx.x) * kTransNodes, end = rowb + x1;
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
+    const int i = e / R, r = e % R;
+    if (base + i < end) tile[i][r] = src[(base + i) * R + r];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
+    const int r = e / kTransNodes, i = e % kTransNodes;
+    if (base + i < end) dst[static_cast<long long>(r) * n + base + i] = tile[i][r];
+  }
+}
+
 __global__ void bump_epoch_kernel(unsigned* e, unsigned by) { *e += by; }
 
 int blocks_for(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
@@ -802,9 +818,10 @@ __global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a
   __shared__ double red[kThreads];
   const int dim = a.g.dim, R = a.R;
   const int npb = kThreads / R;
-  const long long node = a.n0 + static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
+  const long long li = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;  // index in the region
+  const long long node = (a.row0 + li / a.w) * a.gx + a.x0 + li % a.w;
   const int r = threadIdx.x % R;
-  const bool live = threadIdx.x < npb * R && node < a.n1;
+  const bool live = threadIdx.x < npb * R && li < a.cnt;
   const double inv = 1.0 / static_cast<double>(1 << dim);
   double2 uv = czero();
 #pragma unroll 1
@@ -845,7 +862,7 @@ __global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a
 }
 
 int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s) {
-  const int nb = blocks_for(a.n1 - a.n0, kThreads / a.R);
+  const int nb = blocks_for(a.cnt, kThreads / a.R);
   if (nb == 0) return 0;
   if (a.g.dim == 3)
     accumulate_all_kernel<8><<<nb, kThreads, 0, s>>>(a);
@@ -936,6 +953,13 @@ void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int
   if (x1 <= x0 || row1 <= row0) return;
   const dim3 grid((x1 - x0 + kTransNodes - 1) / kTransNodes, static_cast<unsigned>(row1 - row0));
   transpose_in_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0);
+  after_launch();
+}
+void launch_transpose_out_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                               long long row0, long long row1, cudaStream_t s) {
+  if (x1 <= x0 || row1 <= row0) return;
+  const dim3 grid((x1 - x0 + kTransNodes - 1) / kTransNodes, static_cast<unsigned>(row1 - row0));
+  transpose_out_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0);
   after_launch();
 }
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,

@@ -117,7 +117,9 @@ struct AccumAllArgs {
   double2* u;
   double* partial;     // sweep l's partials at partial + l * pstride
   long long pstride;
-  long long n0, n1;
+  // region: rows [row0, row0 + cnt / w) of gx nodes, columns [x0, x0 + w) (a stripe: x0 = 0, w = gx)
+  long long row0, cnt;
+  int gx, x0, w;
 };
 int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s);
 // Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
@@ -154,6 +156,8 @@ void launch_transpose_in_range(const double2* src, double2* dst, long long n, in
                                cudaStream_t s);
 void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
                               long long row0, long long row1, cudaStream_t s);
+void launch_transpose_out_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
+                               long long row0, long long row1, cudaStream_t s);
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                 cudaStream_t s);
 
