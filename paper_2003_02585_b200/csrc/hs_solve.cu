@@ -136,9 +136,21 @@ __device__ __forceinline__ int nch_bwd(const Geo& g, int u, int kr) { return (g.
 
 constexpr unsigned kAllLive = 0x100u;  // task face mask bit: every front is live
 
+// Complex products as three real products (HS_3M): with P1 = Ar Br, P2 = Ai Bi and
+// P3 = (Ar + Ai)(Br + Bi), Re = P1 - P2 and Im = P3 - P1 - P2, so a complex k-step costs 3 DMMAs
+// per tile instead of 4 (the FP64 tensor pipe is the bound when many items run at once). The
+// k-loop accumulates P1, P2, P3 in planes 0, 1, 2; acc_finish turns them into re / im (planes
+// 0, 1), which is all the split-K reduction and the finalize see.
+#ifndef HS_3M
+#define HS_3M 1
+#endif
+constexpr int kPlanes = HS_3M ? 3 : 2;
+#ifndef HS_SOLVE_CTAS
+#define HS_SOLVE_CTAS (HS_3M ? 3 : 4)  // CTAs per SM: the 3M accumulators need 170 registers
+#endif
 template <int NT>
 struct Acc {
-  double v[4][NT][2][2];  // m-tile i, n-tile q, re/im, fragment element e
+  double v[4][NT][kPlanes][2];  // m-tile i, n-tile q, re/im (3M: P1 / P2 / P3), fragment element e
 };
 constexpr int kTileDoubles = 1024;  // partial tile: 32 lanes x up to 32 accumulator doubles
 
@@ -149,7 +161,33 @@ __device__ __forceinline__ void acc_zero(Acc<NT>& c) {
 #pragma unroll
     for (int q = 0; q < NT; ++q)
 #pragma unroll
-      for (int p = 0; p < 2; ++p) c.v[i][q][p][0] = c.v[i][q][p][1] = 0.0;
+      for (int p = 0; p < kPlanes; ++p) c.v[i][q][p][0] = c.v[i][q][p][1] = 0.0;
+}
+// start value x + iy of one accumulator element (before the k-loop)
+template <int NT>
+__device__ __forceinline__ void acc_set(Acc<NT>& c, int i, int q, int e, double x, double y) {
+  c.v[i][q][0][e] = x;
+  if (HS_3M) {  // Re = P1 - P2 = x, Im = P3 - P1 - P2 = y
+    c.v[i][q][1][e] = 0.0;
+    c.v[i][q][kPlanes - 1][e] = x + y;
+  } else {
+    c.v[i][q][1][e] = y;
+  }
+}
+// after the k-loop: planes 0 / 1 = re / im
+template <int NT>
+__device__ __forceinline__ void acc_finish(Acc<NT>& c) {
+  if (!HS_3M) return;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double p1 = c.v[i][q][0][e], p2 = c.v[i][q][1][e], p3 = c.v[i][q][kPlanes - 1][e];
+        c.v[i][q][0][e] = p1 - p2;
+        c.v[i][q][1][e] = p3 - p1 - p2;
+      }
 }
 
 // one k-step (4 columns of the product's inner dimension) of the complex 32 x (8 NT) tile
@@ -162,6 +200,26 @@ __device__ __forceinline__ void acc_zero(Acc<NT>& c) {
 template <int NT, bool NEG = false, bool FULL = false>
 __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
   if (FULL) mask = 0xFu;
+#if HS_3M
+  double bx[NT], by[NT], bs[NT], as[4];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    bx[q] = NEG ? -B[q].x : B[q].x;
+    by[q] = NEG ? -B[q].y : B[q].y;
+    bs[q] = bx[q] + by[q];
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) as[i] = A[i].x + A[i].y;
+#pragma unroll
+  for (int q = 0; q < NT; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (mask & (1u << i)) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, by[q]);
+        dmma(c.v[i][q][kPlanes - 1][0], c.v[i][q][kPlanes - 1][1], as[i], bs[q]);
+      }
+#else
   double bx[NT], by[NT], nby[NT];
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
@@ -185,6 +243,7 @@ __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], cons
         dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nby[q]);
         dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, bx[q]);
       }
+#endif
 }
 
 // Split-K: store this chunk's partial, and if it arrived last, replace acc by the sum of all
@@ -512,12 +571,12 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
             const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
             tb = make_double2(tb.x + w.x, tb.y + w.y);
           }
-          acc.v[i][q][0][e] = -tb.x;
-          acc.v[i][q][1][e] = -tb.y;
+          acc_set(acc, i, q, e, -tb.x, -tb.y);
         }
     }
   }
   kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of, [](int) { return false; });
+  acc_finish(acc);
   take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
@@ -636,6 +695,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   Acc<NT> acc;
   acc_zero(acc);
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
+  acc_finish(acc);
   take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
@@ -678,7 +738,7 @@ __device__ __forceinline__ Geo geo_km(int k, int m) {
 }
 
 template <bool FWD>
-__global__ void __launch_bounds__(kThreads, 4) solve6_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kThreads, HS_SOLVE_CTAS) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* ring = smem_ring + warp * RingArea<FWD>::kWarp;
