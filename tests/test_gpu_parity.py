@@ -217,12 +217,19 @@ def test_c2_subdomain_factor_against_oracle(hs):
             assert rel(X[r], fo.solve(b[r])) <= 1e-11
 
 
-@pytest.mark.parametrize("rounds", [1, 2])
-def test_streamed_host_path_equals_device_path(hs, golden, rounds):
-    """hs_ddm_solve with pinned host buffers streams b / u by stripes around the macro-step
-    schedule; it must return exactly the device-buffer result (and the pageable-buffer one)."""
+@pytest.mark.parametrize("name,rounds,segs", [("ddm_2d_3x2_r2", 1, None), ("ddm_2d_3x2_r2", 2, None),
+                                               ("ddm_2d_3x2_r2", 1, 3), ("ddm_2d_2x2", 1, 5),
+                                               ("ddm_3d_2x2x2", 1, None), ("ddm_3d_2x2x2", 1, 2)])
+def test_streamed_host_path_equals_device_path(hs, golden, monkeypatch, name, rounds, segs):
+    """hs_ddm_solve with pinned host buffers streams b in by tiles (stripe x fastest-axis
+    segment, in the order the sweep-1 sources read them) and u out by tiles / stripes around the
+    macro-step schedule; it must return exactly the device-buffer result (and the pageable-buffer
+    one). segs forces the number of fastest-axis segments (HS_TILE_SEGS), so the multi-segment
+    tiling is exercised at golden sizes too; 1 round also checks the result against the reference."""
     torch = pytest.importorskip("torch")
-    z = golden("ddm_2d_3x2_r2")
+    if segs is not None:
+        monkeypatch.setenv("HS_TILE_SEGS", str(segs))
+    z = golden(name)
     s = hs.DdmSolver(_setup(hs, z))
     b = np.ascontiguousarray(z["b"], dtype=np.complex128)  # (R, N) RHS-major
     R = b.shape[0]
@@ -235,7 +242,11 @@ def test_streamed_host_path_equals_device_path(hs, golden, rounds):
     torch.cuda.synchronize()
     assert torch.equal(hu, du.cpu())
     u_pageable = s.ddm_solve(b, rounds, None, True)
-    assert np.array_equal(hu.numpy().view(np.complex128).reshape(R, -1), np.asarray(u_pageable).reshape(R, -1))
+    uh = hu.numpy().view(np.complex128).reshape(R, -1)
+    assert np.array_equal(uh, np.asarray(u_pageable).reshape(R, -1))
+    if rounds == int(z["rounds"]):
+        for r in range(R):
+            assert rel(uh[r], z["u"][r]) <= 1e-9
 
 
 def test_global_direct_solve_matches_sparse_lu(hs):
