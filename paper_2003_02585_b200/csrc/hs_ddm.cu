@@ -122,6 +122,7 @@ struct Engine {
   int kc = 4, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
   int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
   int crit_gw = 8;             // RHS per item of the split (critical-path) fronts
+  int max_chunks = 16;         // split-K chunks per band at most (HS_MAX_CHUNKS)
   long long arr_total = 0, part_total = 0;     // per slot
   DBuf<double2> x, x1, rb, vbuf;
   DBuf<double> part;
@@ -464,6 +465,10 @@ struct Engine {
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
     if (const char* e = std::getenv("HS_CRIT_GW")) crit_gw = std::atoi(e) <= 8 ? 8 : 16;
+    // chunks per band at most: 16 in 2D (the C2 / C3 fronts never need more), 4 in 3D, whose big
+    // top fronts have bands enough (C5 application 0.456 s uncapped -> 0.399 at 16 -> 0.388 at 4)
+    max_chunks = dim == 3 ? 4 : 16;
+    if (const char* e = std::getenv("HS_MAX_CHUNKS")) max_chunks = std::max(1, std::atoi(e));
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;
@@ -477,8 +482,12 @@ struct Engine {
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const int m = c.fronts[f].m, k = c.fronts[f].k;
         if (c.fronts[f].depth < split_depth) {  // critical path: split long bands over many warps
-          cd.fkc[f] = kc;
-          cd.fkr[f] = kr;
+          // at most max_chunks chunks per band: the last arriver sums the partials serially, and
+          // the big (3D) top fronts have bands enough to fill the GPU without fine splits
+          const int kb0 = pad8(k) >> 3, nrb0 = kb0 + (pad8(m - k) >> 3);
+          // (chunks stay <= 16 blocks: the solve kernel stages an item's index slice in 128 entries)
+          cd.fkc[f] = std::min(16, std::max(kc, (kb0 + max_chunks - 1) / max_chunks));
+          cd.fkr[f] = std::min(16, std::max(kr, (((nrb0 + max_chunks - 1) / max_chunks) + 3) & ~3));
           cd.fgw[f] = crit_gw;
         }
         const int fkc = cd.fkc[f], fkr = cd.fkr[f];
@@ -687,6 +696,9 @@ struct Engine {
     a.arr_stride = arr_total;
     a.nzmask = nzmask;
     a.tface = tface;
+    // 3M products (3 CTAs per SM) unless HS_M3=0: C2 12.5 vs 12.8 ms, C5 0.384 vs 0.394 s
+    static const int m3env = std::getenv("HS_M3") ? std::atoi(std::getenv("HS_M3")) : 1;
+    a.m3 = m3env != 0;
     a.need = need;
     a.need_words = need_words;
     a.nsub = static_cast<int>(sub_cls.size());

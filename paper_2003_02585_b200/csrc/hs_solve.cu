@@ -141,50 +141,46 @@ constexpr unsigned kAllLive = 0x100u;  // task face mask bit: every front is liv
 // per tile instead of 4 (the FP64 tensor pipe is the bound when many items run at once). The
 // k-loop accumulates P1, P2, P3 in planes 0, 1, 2; acc_finish turns them into re / im (planes
 // 0, 1), which is all the split-K reduction and the finalize see.
-#ifndef HS_3M
-#define HS_3M 1
-#endif
-constexpr int kPlanes = HS_3M ? 3 : 2;
-#ifndef HS_SOLVE_CTAS
-#define HS_SOLVE_CTAS (HS_3M ? 3 : 4)  // CTAs per SM: the 3M accumulators need 170 registers
-#endif
-template <int NT>
+// Both forms are compiled (template M3): 3M needs 162-168 registers and so runs 3 CTAs per SM,
+// the four-product form 4 (SolveArgs::m3 selects; 3M measured faster on C2 and C5).
+template <int NT, bool M3>
 struct Acc {
-  double v[4][NT][kPlanes][2];  // m-tile i, n-tile q, re/im (3M: P1 / P2 / P3), fragment element e
+  static constexpr int P = M3 ? 3 : 2;
+  double v[4][NT][P][2];  // m-tile i, n-tile q, re/im (3M: P1 / P2 / P3), fragment element e
 };
 constexpr int kTileDoubles = 1024;  // partial tile: 32 lanes x up to 32 accumulator doubles
 
-template <int NT>
-__device__ __forceinline__ void acc_zero(Acc<NT>& c) {
+template <int NT, bool M3>
+__device__ __forceinline__ void acc_zero(Acc<NT, M3>& c) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < NT; ++q)
 #pragma unroll
-      for (int p = 0; p < kPlanes; ++p) c.v[i][q][p][0] = c.v[i][q][p][1] = 0.0;
+      for (int p = 0; p < Acc<NT, M3>::P; ++p) c.v[i][q][p][0] = c.v[i][q][p][1] = 0.0;
 }
 // start value x + iy of one accumulator element (before the k-loop)
-template <int NT>
-__device__ __forceinline__ void acc_set(Acc<NT>& c, int i, int q, int e, double x, double y) {
+template <int NT, bool M3>
+__device__ __forceinline__ void acc_set(Acc<NT, M3>& c, int i, int q, int e, double x, double y) {
   c.v[i][q][0][e] = x;
-  if (HS_3M) {  // Re = P1 - P2 = x, Im = P3 - P1 - P2 = y
+  if (M3) {  // Re = P1 - P2 = x, Im = P3 - P1 - P2 = y
     c.v[i][q][1][e] = 0.0;
-    c.v[i][q][kPlanes - 1][e] = x + y;
+    c.v[i][q][Acc<NT, M3>::P - 1][e] = x + y;
   } else {
     c.v[i][q][1][e] = y;
   }
 }
 // after the k-loop: planes 0 / 1 = re / im
-template <int NT>
-__device__ __forceinline__ void acc_finish(Acc<NT>& c) {
-  if (!HS_3M) return;
+template <int NT, bool M3>
+__device__ __forceinline__ void acc_finish(Acc<NT, M3>& c) {
+  if (!M3) return;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < NT; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const double p1 = c.v[i][q][0][e], p2 = c.v[i][q][1][e], p3 = c.v[i][q][kPlanes - 1][e];
+        const double p1 = c.v[i][q][0][e], p2 = c.v[i][q][1][e], p3 = c.v[i][q][Acc<NT, M3>::P - 1][e];
         c.v[i][q][0][e] = p1 - p2;
         c.v[i][q][1][e] = p3 - p1 - p2;
       }
@@ -197,10 +193,10 @@ __device__ __forceinline__ void acc_finish(Acc<NT>& c) {
 // DMMA operand modifiers instead of costing FP64-pipe negations.
 // FULL: every m-tile live (the common case) -- no per-tile predicate, so the warp-synchronous
 // DMMAs issue back to back instead of each behind a WARPSYNC / NOP pair.
-template <int NT, bool NEG = false, bool FULL = false>
-__device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
+template <bool NEG, bool FULL, int NT, bool M3>
+__device__ __forceinline__ void mma_step(Acc<NT, M3>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mask) {
   if (FULL) mask = 0xFu;
-#if HS_3M
+  if constexpr (M3) {
   double bx[NT], by[NT], bs[NT], as[4];
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
@@ -217,9 +213,9 @@ __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], cons
       if (mask & (1u << i)) {
         dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx[q]);
         dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, by[q]);
-        dmma(c.v[i][q][kPlanes - 1][0], c.v[i][q][kPlanes - 1][1], as[i], bs[q]);
+        dmma(c.v[i][q][Acc<NT, M3>::P - 1][0], c.v[i][q][Acc<NT, M3>::P - 1][1], as[i], bs[q]);
       }
-#else
+  } else {
   double bx[NT], by[NT], nby[NT];
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
@@ -243,14 +239,14 @@ __device__ __forceinline__ void mma_step(Acc<NT>& c, const double2 (&A)[4], cons
         dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nby[q]);
         dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, bx[q]);
       }
-#endif
+  }
 }
 
 // Split-K: store this chunk's partial, and if it arrived last, replace acc by the sum of all
 // chunks in chunk order (read back from memory, own partial included). Returns whether this
 // warp finalizes the band.
-template <int NT>
-__device__ __forceinline__ bool split_reduce(Acc<NT>& c, double* base, long long cstride, int nch, int chunk,
+template <int NT, bool M3>
+__device__ __forceinline__ bool split_reduce(Acc<NT, M3>& c, double* base, long long cstride, int nch, int chunk,
                                              int* arr, int lane) {
   double* mine = base + chunk * cstride + lane;
 #pragma unroll
@@ -367,8 +363,8 @@ struct RingArea {
 // The pipelined k-loop shared by both passes: issue(s, stage) stages k-step s with cp.async,
 // use(s, stage, A, B) reads it back. All global loads go through the ring, so in-flight data
 // costs shared memory, not registers.
-template <bool FWD, int NT, class Issue, class Use, class Mask, class Neg>
-__device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of,
+template <bool FWD, int NT, bool M3, class Issue, class Use, class Mask, class Neg>
+__device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, Issue&& issue, Use&& use, Mask&& mask_of,
                                       Neg&& neg_of) {
   constexpr int NS = Ring<FWD, NT>::NS, ST = Ring<FWD, NT>::kStage;
 #pragma unroll
@@ -389,14 +385,14 @@ __device__ __forceinline__ void kloop(Acc<NT>& acc, int ns, double2* ring, Issue
     const unsigned mk = mask_of(s);
     if (neg_of(s)) {
       if (mk == 0xFu)
-        mma_step<NT, true, true>(acc, A, B, mk);
+        mma_step<true, true>(acc, A, B, mk);
       else
-        mma_step<NT, true, false>(acc, A, B, mk);
+        mma_step<true, false>(acc, A, B, mk);
     } else {
       if (mk == 0xFu)
-        mma_step<NT, false, true>(acc, A, B, mk);
+        mma_step<false, true>(acc, A, B, mk);
       else
-        mma_step<NT, false, false>(acc, A, B, mk);
+        mma_step<false, false>(acc, A, B, mk);
     }
   }
   cp_wait<0>();
@@ -479,7 +475,7 @@ __device__ __forceinline__ void take_ticket(const SolveArgs& a, unsigned& tk, bo
 // children's updates at the front's boundary, in the reference's child order), loaded while the
 // k-loop's first stages are in flight, so the finalize only scales and stores. Returns whether
 // this warp finalized the band (the caller signals it).
-template <int NT>
+template <int NT, bool M3>
 __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
                          int lane, double2* ring, const int2* sidx, unsigned long long* tr, unsigned clive,
                          unsigned& tk, bool& took) {
@@ -548,7 +544,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
       B[q] = make_double2(v.x + w1.x, v.y + w1.y);
     }
   };
-  Acc<NT> acc;
+  Acc<NT, M3> acc;
   acc_zero(acc);
   if (it.chunk == 0 && !leaf) {  // -T_bnd = -((0 + child0 V) + child1 V) on boundary rows
 #pragma unroll
@@ -623,7 +619,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 // ---------------------------------------------------------------------------------------
 // backward column-band item: x_sep[32 cols][8 NT RHS] = sum over the chunk's rows of
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
-template <int NT>
+template <int NT, bool M3>
 __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane,
                          double2* ring, const int2* sidx, unsigned long long* tr, bool zlive, unsigned& tk,
                          bool& took) {
@@ -692,7 +688,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   // boundary row blocks enter as -x_bnd (zeros stay zero): warp-uniform per k-step, folded into
   // the DMMA operand signs
   auto neg_of = [&](int s) { return a0 + (s >> 1) >= g.kb; };
-  Acc<NT> acc;
+  Acc<NT, M3> acc;
   acc_zero(acc);
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
   acc_finish(acc);
@@ -737,8 +733,8 @@ __device__ __forceinline__ Geo geo_km(int k, int m) {
   return g;
 }
 
-template <bool FWD>
-__global__ void __launch_bounds__(kThreads, HS_SOLVE_CTAS) solve6_kernel(SolveArgs a) {
+template <bool FWD, bool M3>
+__global__ void __launch_bounds__(kThreads, M3 ? 3 : 4) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* ring = smem_ring + warp * RingArea<FWD>::kWarp;
@@ -796,11 +792,11 @@ __global__ void __launch_bounds__(kThreads, HS_SOLVE_CTAS) solve6_kernel(SolveAr
         if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
         double2* V = a.vbuf + it.slot * a.vslot_stride;
         if (FWD)
-          fin = it.rw > 8 ? fwd_item<2>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
-                          : fwd_item<1>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
+          fin = it.rw > 8 ? fwd_item<2, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
+                          : fwd_item<1, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
         else
-          fin = it.rw > 8 ? bwd_item<2>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
-                          : bwd_item<1>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
+          fin = it.rw > 8 ? bwd_item<2, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
+                          : bwd_item<1, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
         if (tr && lane == 0) {
           tr[4] = gtime();
           tr[5] = smid();
@@ -818,7 +814,6 @@ __global__ void __launch_bounds__(kThreads, HS_SOLVE_CTAS) solve6_kernel(SolveAr
   }
 }
 
-int g_grid[2] = {0, 0};
 
 }  // namespace
 
@@ -836,39 +831,44 @@ constexpr size_t ring_bytes() {
   return static_cast<size_t>(kThreads / 32) * RingArea<FWD>::kWarp * sizeof(double2);
 }
 
-void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
-  int& grid = g_grid[fwd ? 1 : 0];
+template <bool FWD, bool M3>
+int solve_grid() {
+  static int grid = 0;
   if (!grid) {
     int dev = 0, sms = 0, per = 0;
     HS_CUDA(cudaGetDevice(&dev));
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (fwd) {
-      HS_CUDA(cudaFuncSetAttribute(solve6_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<true>()));
-      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<true>, kThreads, ring_bytes<true>()));
-    } else {
-      HS_CUDA(cudaFuncSetAttribute(solve6_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<false>()));
-      HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<false>, kThreads, ring_bytes<false>()));
-    }
+    HS_CUDA(cudaFuncSetAttribute(solve6_kernel<FWD, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<FWD>()));
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<FWD, M3>, kThreads, ring_bytes<FWD>()));
     grid = sms * std::max(per, 1);
   }
-  const int g = std::max(1, std::min(grid, (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
+  return grid;
+}
+
+template <bool FWD, bool M3>
+void launch_solve_t(const SolveArgs& a, cudaStream_t s) {
+  const int g = std::max(1, std::min(solve_grid<FWD, M3>(), (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
   // Cooperative launch: the whole grid is co-resident, which the static first round relies on
   // (a static item of a CTA that is not yet resident could otherwise be waited for by every
   // resident warp, e.g. while another stream's kernel holds part of the GPU).
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = fwd ? ring_bytes<true>() : ring_bytes<false>();
+  cfg.dynamicSmemBytes = ring_bytes<FWD>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<FWD, M3>, a));
+}
+
+void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
   if (fwd)
-    HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<true>, a));
+    a.m3 ? launch_solve_t<true, true>(a, s) : launch_solve_t<true, false>(a, s);
   else
-    HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<false>, a));
+    a.m3 ? launch_solve_t<false, true>(a, s) : launch_solve_t<false, false>(a, s);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   HS_CUDA(cudaGetLastError());
 }
