@@ -120,7 +120,7 @@ struct Engine {
   // solve state
   int R = 0, nslots = 0, ngr = 1;
   int kc = 4, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
-  int split_depth = 8;         // fronts at depth < split_depth are split; the others run whole
+  int split_depth = 7;         // fronts at depth < split_depth are split; the others run whole (swept: C2 12.9 / 12.7 / 12.4 / 12.3 / 12.55 / 16.1 ms at 4 / 5 / 6 / 7 / 8 / 10)
   int crit_gw = 8;             // RHS per item of the split (critical-path) fronts
   int max_chunks = 16;         // split-K chunks per band at most (HS_MAX_CHUNKS)
   long long arr_total = 0, part_total = 0;     // per slot
