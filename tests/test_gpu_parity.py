@@ -393,3 +393,42 @@ def test_anisotropic_grids_against_reference(hs, dim, n, parts, pad, rounds):
         assert rel(U[i], u0) <= TOL
         assert [getattr(reps[i], k) for k in COUNTERS] == [rep0[k] for k in COUNTERS]
         np.testing.assert_allclose(reps[i].round_residuals, rep0["round_residuals"], rtol=1e-6)
+
+
+_ALT_SCRIPT = r"""
+import ast, sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2003_02585_b200 as hs
+worst = 0.0
+for name in ["ddm_2d_3x2_r2", "ddm_3d_2x2x2", "ddm_2d_layered"]:
+    z = np.load({root!r} + "/tests/golden/" + name + ".npz")
+    med = ast.literal_eval(str(z["medium"]))
+    if med["media.kind"] == "constant":
+        m = hs.Medium("constant", kappa=med["media.kappa"])
+    else:
+        m = hs.Medium("two_layered", kappa_down=med["media.kappa_down"], kappa_up=med["media.kappa_up"],
+                      axis=med["media.axis"], eta=med["media.eta_L"], eps=med["media.epsilon"])
+    dim = int(z["dim"])
+    s = hs.DdmSolver(hs.ProblemSetup(dim, [int(z["n"])] * dim, list(z["parts"]), m, pml_width=int(z["pad"])))
+    U = s.ddm_solve(z["b"], int(z["rounds"]), None, True)
+    for r in range(U.shape[0]):
+        worst = max(worst, float(np.linalg.norm(U[r] - z["u"][r]) / np.linalg.norm(z["u"][r])))
+print("WORST", worst)
+"""
+
+
+@pytest.mark.parametrize("env", [{"HS_M3": "0"}, {"HS_GRAPH": "0"}, {"HS_ORDER": "0", "HS_MAX_CHUNKS": "1"}])
+def test_alternate_engine_paths_match_reference(env):
+    """The engine's alternates, each selected per process by an environment switch, against the
+    reference's golden u: the four-product solve kernels (HS_M3=0, 4 CTAs/SM), stream-by-stream
+    launches instead of the captured CUDA graph (HS_GRAPH=0), and the plain level order with
+    one split-K chunk size per band (HS_ORDER=0, HS_MAX_CHUNKS=1: the longest chunks)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _ALT_SCRIPT.format(root=root)], capture_output=True, text=True,
+                       env={**os.environ, **env}, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst = float(r.stdout.split("WORST")[-1])
+    assert worst <= TOL
