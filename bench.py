@@ -1,17 +1,21 @@
 """Benchmark: RHS/s through full 2^n diagonal sweeps (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1], "C2"): 2D constant medium, 1024^2 interior + 32-cell PML,
-omega = 2 pi 64 (c = 1), 8x8 checkerboard subdomains each with its own 32-cell PML, 16 RHS =
-Gaussian point sources (sigma = 2h, unit amplitude) at seeded uniform interior locations,
-complex128, direct-solver mode: one DDM application = 1 round of 4 diagonal sweeps with the
-per-round residual the reference's run_direct tracks (src/harness.cpp:269-283).
+Headline workload (BASELINE.json configs[2], "C3" -- the largest single-GPU configuration; C5 is
+the 8-GPU configuration and C4 is GMRES mode): 2D two-layered medium, 2048^2 interior + 32-cell
+PML, c = 1 below y = 0.5 + h/2 and 1.5 above (omega = 2 pi 96 referenced to c = 1), 16x16
+checkerboard subdomains each with its own 32-cell PML, 64 RHS = Gaussian point sources (sigma = 2h,
+unit amplitude) at seeded uniform interior locations, complex128, direct-solver mode: one DDM
+application = 2 rounds of 4 diagonal sweeps with the per-round residual the reference's
+run_direct tracks (src/harness.cpp:269-283). ``--config c2`` runs BASELINE configs[1] (1024^2,
+8x8, 16 RHS, 1 round) instead.
 
-A step is one DDM application over the batch of 16 RHS (lockstep-batched through every
-subdomain solve). ``value`` = RHS/s with b already resident in HBM, device-timed with CUDA
-events; ``e2e`` = the same through hs_ddm_solve with pinned host buffers (H2D of b and D2H of
-u inside the timed region). Multi-GPU (torchrun): one process per GPU, each rank sweeps its own
-16-RHS batch against its own resident factors (RHS are independent units; no data-path
-collective) -> weak scaling, time = max over ranks.
+A step is one DDM application over the batch of RHS (lockstep-batched through every subdomain
+solve). ``value`` = RHS/s with b already resident in HBM, device-timed with CUDA events;
+``e2e`` = the same through hs_ddm_solve with pinned host buffers (H2D of b and D2H of u inside
+the timed region). Multi-GPU (torchrun): one process per GPU, each rank sweeps its own RHS batch
+against its own resident factors (RHS are independent units; no data-path collective) -> weak
+scaling, time = max over ranks; ``--partition subdomain`` spreads one problem's subdomains over
+the ranks instead.
 
 ``--impl reference`` runs the reference's own CPU implementation (oracle/_ref, the unmodified
 reference compiled in place) on the host cores, one RHS per step.
@@ -22,6 +26,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -34,15 +39,71 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "RHS/sec through full 2^n diagonal sweeps"
-WORKLOAD = ("C2: 2D constant medium c=1, 1024^2 grid + 32-cell PML, omega=2pi*64, 8x8 subdomains, "
-            "16 RHS seeded Gaussian sources (sigma=2h), direct-solver mode (1 round = 4 diagonal sweeps, "
-            "per-round residual)")
-CFG = dict(dim=2, n=1024, parts=(8, 8), pad=32, kappa=2 * math.pi * 64, nrhs=16, rounds=1)
+CONFIGS = {
+    "c3": dict(
+        workload=("C3: 2D two-layered medium (c=1 for y<0.5+h/2, c=1.5 above), 2048^2 grid + 32-cell PML, "
+                  "omega=2pi*96 (c=1), 16x16 subdomains, 64 RHS seeded Gaussian sources (sigma=2h), direct-solver "
+                  "mode (2 rounds = 8 diagonal sweeps, per-round residual)"),
+        dim=2, n=2048, parts=(16, 16), pad=32, nrhs=64, rounds=2, kind="two_layered",
+        kappa_down=2 * math.pi * 96, kappa_up=2 * math.pi * 64, eta=0.5 + 1.0 / 4096, seed=3000),
+    "c2": dict(
+        workload=("C2: 2D constant medium c=1, 1024^2 grid + 32-cell PML, omega=2pi*64, 8x8 subdomains, "
+                  "16 RHS seeded Gaussian sources (sigma=2h), direct-solver mode (1 round = 4 diagonal sweeps, "
+                  "per-round residual)"),
+        dim=2, n=1024, parts=(8, 8), pad=32, nrhs=16, rounds=1, kind="constant", kappa=2 * math.pi * 64, seed=1000),
+}
+CFG = dict(CONFIGS["c3"])
+WORKLOAD = CFG["workload"]
+
+
+def select(name):
+    global WORKLOAD
+    CFG.clear()
+    CFG.update(CONFIGS[name])
+    WORKLOAD = CFG["workload"]
 
 
 def ref_config():
-    return {"dim": 2, "grid.n": [CFG["n"]] * 2, "partition": list(CFG["parts"]), "pml.width": CFG["pad"],
-            "media.kind": "constant", "media.kappa": CFG["kappa"]}
+    c = {"dim": 2, "grid.n": [CFG["n"]] * 2, "partition": list(CFG["parts"]), "pml.width": CFG["pad"]}
+    if CFG["kind"] == "constant":
+        c.update({"media.kind": "constant", "media.kappa": CFG["kappa"]})
+    else:
+        c.update({"media.kind": "two_layered", "media.kappa_down": CFG["kappa_down"],
+                  "media.kappa_up": CFG["kappa_up"], "media.axis": 1, "media.eta_L": CFG["eta"],
+                  "media.epsilon": 0.0})
+    return c
+
+
+def medium(hs):
+    if CFG["kind"] == "constant":
+        return hs.Medium("constant", kappa=CFG["kappa"])
+    return hs.Medium("two_layered", kappa_down=CFG["kappa_down"], kappa_up=CFG["kappa_up"], axis=1,
+                     eta=CFG["eta"], eps=0.0)
+
+
+def host_info():
+    """CPU model, core count and RAM of the host the CPU baseline ran on."""
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal"):
+                    ram = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram,
+            "reference_build": "g++ -O3 -march=native, reference sources compiled in place against the "
+                               "from-scratch Eigen-subset shim oracle/shim (naive dense loops, no BLAS)"}
 
 
 def make_sources(seed, lo, hi, hgrid, origin):
@@ -130,7 +191,7 @@ def ncu_traffic():
 
 def cpu_baseline_sample(b0, u0=None):
     """oracle/_ref (the reference compiled in place) on this host's cores: DdmSolver factorizes
-    all 64 subdomains, then one RHS of the workload through one DDM application. With u0 (the
+    every subdomain, then one RHS of the workload through one DDM application. With u0 (the
     device result for the same RHS) it also reports the relative L2 difference -- parity at the
     bench's own configuration (north_star: <= 1e-9)."""
     try:
@@ -144,9 +205,12 @@ def cpu_baseline_sample(b0, u0=None):
         u, rep = s.ddm_solve(b0, CFG["rounds"], True)
         dt = time.perf_counter() - t0
         out = {"value": 1.0 / dt, "unit": "RHS/s", "cores": cores, "kind": "reference",
-               "sample": f"1 of the 16 RHS through one full DDM application (4 sweeps, residual), "
-                         f"sweep.workers={cores}; factorization {s.factor_seconds:.2f}s excluded",
-               "factor_seconds": s.factor_seconds, "seconds": dt}
+               "sample": f"1 of the {CFG['nrhs']} RHS through one full DDM application "
+                         f"({4 * CFG['rounds']} sweeps, residual), sweep.workers={cores}; factorization "
+                         f"{s.factor_seconds:.2f}s excluded",
+               "factor_seconds": s.factor_seconds, "seconds": dt, "host": host_info(),
+               "counters": {k: rep[k] for k in ("local_solves", "skipped_zero_solves", "traces_generated",
+                                                "traces_routed", "traces_discarded")}}
         if u0 is not None:
             out["parity_rel_l2_rhs0"] = float(np.linalg.norm(u0 - u) / np.linalg.norm(u))
         return out
@@ -166,8 +230,9 @@ def run_reference(args, rank, world):
         return 0
     cores = os.cpu_count() or 1
     s = ref.RefSolver(ref_config(), cores)
-    f = make_sources(1000 + rank, s.lo, s.hi, s.hgrid, s.origin)
-    B = [s.scale_source(f[r]) for r in range(CFG["nrhs"])]
+    f = make_sources(CFG["seed"], s.lo, s.hi, s.hgrid, s.origin)
+    B = [s.scale_source(f[r]) for r in range(min(CFG["nrhs"], args.warmup + args.steps))]
+    del f
     for w in range(args.warmup):
         s.ddm_solve(B[w % len(B)], CFG["rounds"], True)
     t0 = time.perf_counter()
@@ -178,7 +243,7 @@ def run_reference(args, rank, world):
     base.update(value=v, ms_per_step=1e3 * dt / args.steps, scaling="weak", vs_baseline=None,
                 cpu_baseline={"value": v, "unit": "RHS/s", "cores": cores, "kind": "reference",
                               "sample": f"{args.steps} RHS of the workload, one full DDM application each, "
-                                        f"sweep.workers={cores}"},
+                                        f"sweep.workers={cores}", "host": host_info()},
                 e2e={"value": v, "unit": "RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                 factorization_seconds=s.factor_seconds)
     print(json.dumps(base))
@@ -192,10 +257,9 @@ def run_gpu(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    setup = hs.ProblemSetup(2, [CFG["n"]] * 2, list(CFG["parts"]), hs.Medium("constant", kappa=CFG["kappa"]),
-                            pml_width=CFG["pad"])
+    setup = hs.ProblemSetup(2, [CFG["n"]] * 2, list(CFG["parts"]), medium(hs), pml_width=CFG["pad"])
     # --partition subdomain (N > 1): one problem, its subdomains spread over the ranks (SURVEY.md
-    # §8(e)); every rank solves the same 16 RHS -> strong scaling. Default: RHS sharding (weak).
+    # §8(e)); every rank solves the same RHS batch -> strong scaling. Default: RHS sharding (weak).
     part = world > 1 and args.partition == "subdomain"
     t0 = time.perf_counter()
     if part:
@@ -207,7 +271,7 @@ def run_gpu(args, rank, world, local_rank):
     N, R = s.global_n, CFG["nrhs"]
     units = R if part else R * world  # RHS the whole job completes per step
     hgrid = [1.0 / CFG["n"]] * 2
-    f = make_sources(1000 + (0 if part else rank), s.lo, s.hi, hgrid, [0.0, 0.0])
+    f = make_sources(CFG["seed"] + (0 if part else rank), s.lo, s.hi, hgrid, [0.0, 0.0])
     b = s.scale_source(f)  # (R, N) RHS-major
     db = torch.from_numpy(b.view(np.float64)).to(dev)
     du = torch.empty_like(db)
@@ -262,10 +326,12 @@ def run_gpu(args, rank, world, local_rank):
     e2e_val = units / (float(t2.item()) * 1e-3)
     # parity sanity of what was timed: device result == host-path result
     ok = bool(torch.equal(du.cpu(), hu))
+    reps0 = s.ddm_solve_device(db.data_ptr(), du.data_ptr(), R, rounds, track, stream, want_reports=True)
 
     if rank != 0:
         return 0
     hbm, hbm_kind, fp64 = peaks()
+    fac_gb = s.factor_bytes() / 1e9
     sec = prof["solve_seconds"]
     tflops = prof["alg_flops"] / sec / 1e12
     gbs = prof["alg_bytes"] / sec / 1e9
@@ -279,12 +345,20 @@ def run_gpu(args, rank, world, local_rank):
         "config": {"workload": WORKLOAD, "rhs_per_gpu": R, "subdomains": s.nsub, "global_nodes": N,
                    "parallelism": (f"subdomain-partitioned x{world} (strong; NCCL trace/ghost exchange per macro-step)"
                                    if part else f"rhs-sharded x{world} (weak), subdomain steps batched per GPU"),
-                   "l2": "inputs larger than L2 (2.5 GB resident factors streamed every step)"},
-        # At 16 RHS the solve streams 16 B of factor per 8*16 flop: 8 flop/B > the 5.75 flop/B ridge
-        # (37.1 TF FP64 DMMA / 6.46 TB/s), so the dominant kernels are FP64 tensor-core bound.
+                   "l2": f"inputs larger than L2 ({fac_gb:.1f} GB resident factors streamed every step, "
+                         f"126 MB L2)"},
+        # A batch of R RHS streams 16 B of factor per 8*R flop per pass: at R >= 16 that is >= 8 flop/B,
+        # above the 5.75 flop/B ridge (37.1 TF FP64 DMMA / 6.46 TB/s), so the dominant kernels are FP64
+        # tensor-core bound. `achieved` counts effective complex flops (8 real flops per complex
+        # multiply-add of the algorithm); with the 3M products the pipe executes 6 real
+        # flops per complex MAC on 8x8-block-padded tiles (pipe_view).
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": fp64, "unit": "TFLOP/s", "frac": tflops / fp64,
+                     "flops": "effective complex flops (8 per complex MAC of the packed factor, work performed)",
                      "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.json, tools/bench_fp64.cu); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
+                     "pipe_view": {"real_flops_per_complex_mac": 6 if prof.get("m3", True) else 8,
+                                   "note": "pipe flops = achieved x 6/8 (3M) x block padding; ncu DMMA pipe-active "
+                                           "share in profiles/"},
                      "traffic": tr.get("bytes_per_launch") if tr else None,
                      "kernel": "solve6_kernel<fwd|bwd> (multifrontal partitioned-inverse solve on DMMA, dataflow)",
                      "alg_flops_per_launch": prof["alg_flops"] / nl,
@@ -308,22 +382,35 @@ def run_gpu(args, rank, world, local_rank):
         _, _, owned, sent, msgs = s.partition_info()
         line["partition"] = {"mode": "subdomain", "owned_subdomains_rank0": owned,
                              "exchange_bytes_per_application_rank0": 8 * sent, "messages_per_application_rank0": msgs}
-    # The paper's pipeline cost model (src/pipeline.cpp) next to the device schedule: the model
-    # runs one processor per subdomain, one RHS per tick; the device levels the same trace-routing
-    # task graph into macro-steps and solves each task for the whole 16-RHS batch at once.
+    # The paper's pipeline cost model (src/pipeline.cpp:20-111) against the
+    # measured application. The model runs one processor per subdomain and one
+    # unit of work per tick; on the device the unit is one RHS batch (every task of a macro-step runs
+    # concurrently, the batch's RHS in lockstep), so T0 = the measured device time of one macro-step's
+    # solve launches and the model's makespan for `batches` units predicts the application time.
     sched = s.schedule_info(rounds)
-    sim1 = hs.simulate_pipeline(2, list(CFG["parts"]), 1, rounds, 1.0)
-    simR = hs.simulate_pipeline(2, list(CFG["parts"]), R, rounds, 1.0)
+    parts = list(CFG["parts"])
+    batches = s.batches_per_application(R)
+    t0 = sec / max(nl / 2, 1)  # seconds per macro-step (forward + backward launch), last batch
+    sim1 = hs.simulate_pipeline(2, parts, 1, rounds, 1.0)
+    simB = hs.simulate_pipeline(2, parts, batches, rounds, t0)
     line["pipeline_model"] = {
         "device_macro_steps": sched["macro_steps"], "device_max_width": sched["max_width"],
         "reference_sequential_steps": sched["sequential_steps"], "x_buffers": sched["buffers"],
-        "model_ticks_1_rhs": sim1.makespan, f"model_ticks_{R}_rhs": simR.makespan,
-        "model_closed_form_ticks_per_rhs": hs.average_time_per_rhs(2, list(CFG["parts"]), R, rounds, 1.0).average_per_rhs,
-        "device_t0_us_per_16rhs_task": 1e6 * prof["solve_seconds"] / max(prof["subdomain_solves"], 1),
-        "device_ms_per_macro_step": ms_max / max(sched["macro_steps"], 1)}
+        "model_ticks_1_unit": sim1.makespan, "batches_per_application": batches,
+        "t0_ms_per_macro_step_measured": 1e3 * t0,
+        "model_predicted_solve_ms": 1e3 * simB.makespan,
+        "model_closed_form_ms_per_batch": 1e3 * hs.average_time_per_rhs(2, parts, batches, rounds, t0).average_per_rhs,
+        "measured_ms_per_application": ms_max,
+        "measured_solve_ms_per_application": 1e3 * sec * batches,
+        "predicted_over_measured": simB.makespan / (ms_max * 1e-3)}
     if world == 1 and not args.no_cpu_baseline:
         u0 = hu[0].numpy().view(np.complex128) if hu.dim() > 1 else None
-        line["cpu_baseline"] = cpu_baseline_sample(b[0], u0)
+        cb = cpu_baseline_sample(b[0], u0)
+        if "counters" in cb:
+            keys = list(cb["counters"])
+            cb["counters_equal_rhs0"] = {k: getattr(reps0[0], k) for k in keys} == cb["counters"]
+            cb["round_residuals_rhs0_gpu"] = reps0[0].round_residuals
+        line["cpu_baseline"] = cb
     print(json.dumps(line))
     return 0
 
@@ -335,12 +422,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS),
+                    help="BASELINE configuration: c3 (configs[2], the headline) or c2 (configs[1])")
     ap.add_argument("--partition", default="rhs", choices=["rhs", "subdomain"],
                     help="multi-GPU layout: RHS sharding (weak scaling) or subdomain partitioning (strong)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    select(args.config)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:

@@ -261,6 +261,11 @@ int hs_pipeline_cost(int dim, const int counts[3], int n_rhs, int n_iter, double
 int hs_pipeline_simulate(int dim, const int counts[3], int n_rhs, int n_iter, double t0, double* completion_times,
                          double* makespan, double* average_per_rhs);
 
+/* Device memory of a solver: bytes of resident solve factors (packed 8x8-block layout), bytes of
+ * the solve state for the current batch width, and the RHS the device solves per batch (wider
+ * requests run as consecutive batches). */
+int hs_ddm_memory(const hs_ddm* s, int64_t* factor_bytes, int64_t* state_bytes, int* max_batch);
+
 /* Number of kernel launches issued by this library since load (evidence counter). */
 int64_t hs_kernel_launches(void);
 

@@ -349,6 +349,21 @@ class DdmSolver:
             _raise(rc)
         return y
 
+    def memory(self):
+        """Resident factor bytes, solve-state bytes and the device batch width (hs_ddm_memory)."""
+        fb, sb, mb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+        rc = L.lib().hs_ddm_memory(self._h, ctypes.byref(fb), ctypes.byref(sb), ctypes.byref(mb))
+        if rc:
+            _raise(rc)
+        return {"factor_bytes": fb.value, "state_bytes": sb.value, "max_batch": mb.value}
+
+    def factor_bytes(self):
+        return self.memory()["factor_bytes"]
+
+    def batches_per_application(self, nrhs):
+        mb = self.memory()["max_batch"]
+        return (int(nrhs) + mb - 1) // mb
+
     def schedule_info(self, rounds=1):
         """Device sweep schedule: macro-steps, widest macro-step, the reference's sequential step
         count and x buffers in flight."""

@@ -6,6 +6,7 @@
 #include <stdexcept>
 #include <string>
 #include <array>
+#include <mutex>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -44,5 +45,22 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
                            std::to_string(line));
 }
 #define HS_CUDA(x) ::hsb::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Per-device cached launch setup. CUDA function attributes (the >48 KB dynamic shared memory
+// opt-in) and occupancy-derived grid sizes belong to one device context, so they are set and
+// cached per device ordinal, not once per process.
+struct PerDevice {
+  std::mutex mu;
+  std::array<int, 64> val{};  // 0: not configured on that device yet
+  template <class F>
+  int get(F&& configure) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice", __FILE__, __LINE__);
+    if (dev < 0 || dev >= static_cast<int>(val.size())) throw Error(kCuda, "device ordinal out of range");
+    std::lock_guard<std::mutex> lk(mu);
+    if (!val[dev]) val[dev] = configure(dev);
+    return val[dev];
+  }
+};
 
 }  // namespace hsb

@@ -122,7 +122,7 @@ struct Engine {
   int kc = 4, kr = 4;          // split-K chunks of the top-of-tree fronts (column blocks / block rows)
   int split_depth = 7;         // fronts at depth < split_depth are split; the others run whole (swept: C2 12.9 / 12.7 / 12.4 / 12.3 / 12.55 / 16.1 ms at 4 / 5 / 6 / 7 / 8 / 10)
   int crit_gw = 8;             // RHS per item of the split (critical-path) fronts
-  int max_chunks = 16;         // split-K chunks per band at most (HS_MAX_CHUNKS)
+  int max_chunks = 16;         // target split-K chunks per band (HS_MAX_CHUNKS); chunks stay <= 16 blocks
   long long arr_total = 0, part_total = 0;     // per slot
   DBuf<double2> x, x1, rb, vbuf;
   DBuf<double> part;
@@ -465,8 +465,9 @@ struct Engine {
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
     if (const char* e = std::getenv("HS_CRIT_GW")) crit_gw = std::atoi(e) <= 8 ? 8 : 16;
-    // chunks per band at most: 16 in 2D (the C2 / C3 fronts never need more), 4 in 3D, whose big
-    // top fronts have bands enough (C5 application 0.456 s uncapped -> 0.399 at 16 -> 0.388 at 4)
+    // target chunks per band: 16 in 2D (the C2 / C3 fronts never need more), 4 in 3D, whose big
+    // top fronts have bands enough (C5 application 0.456 s uncapped -> 0.399 at 16 -> 0.388 at 4);
+    // chunks are never wider than 16 blocks, which bounds the 3D top fronts' count from below
     max_chunks = dim == 3 ? 4 : 16;
     if (const char* e = std::getenv("HS_MAX_CHUNKS")) max_chunks = std::max(1, std::atoi(e));
     nslots = std::max(slots, nslots);
@@ -482,10 +483,12 @@ struct Engine {
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const int m = c.fronts[f].m, k = c.fronts[f].k;
         if (c.fronts[f].depth < split_depth) {  // critical path: split long bands over many warps
-          // at most max_chunks chunks per band: the last arriver sums the partials serially, and
-          // the big (3D) top fronts have bands enough to fill the GPU without fine splits
+          // chunk width raised so a band splits into about max_chunks chunks (the last arriver sums
+          // the partials serially, and the big 3D top fronts have bands enough to fill the GPU
+          // without fine splits) -- but a chunk never exceeds 16 blocks, since the solve kernel
+          // stages an item's index slice in 128 entries: bands longer than 16 x max_chunks blocks
+          // (C5's top fronts, k = 3249: about 26 chunks) still split into more than max_chunks
           const int kb0 = pad8(k) >> 3, nrb0 = kb0 + (pad8(m - k) >> 3);
-          // (chunks stay <= 16 blocks: the solve kernel stages an item's index slice in 128 entries)
           cd.fkc[f] = std::min(16, std::max(kc, (kb0 + max_chunks - 1) / max_chunks));
           cd.fkr[f] = std::min(16, std::max(kr, (((nrb0 + max_chunks - 1) / max_chunks) + 3) & ~3));
           cd.fgw[f] = crit_gw;
@@ -772,6 +775,10 @@ struct FactorHandle {
   DBuf<SolveItem> d_fwd, d_bwd;
   DBuf<unsigned> nz;
   DBuf<double2> io;
+  // Factorization::solve is "reentrant; safe for concurrent calls on one factorization"
+  // (include/helmsweep/direct.hpp:29). The device solve shares the engine's buffers, so
+  // concurrent calls on one handle are serialised here; calls on different handles overlap.
+  std::mutex mu;
 };
 
 struct DdmHandle;
@@ -922,7 +929,10 @@ extern "C" int hs_factor_solve_device(hs_factor* f, int nrhs, double* d_x, void*
     if (!f) config_error("hs_factor_solve_device: null handle");
     if (nrhs <= 0) return;
     HS_CUDA(cudaSetDevice(f->h.eng.device));
-    factor_solve_device(f->h, nrhs, reinterpret_cast<double2*>(d_x), static_cast<cudaStream_t>(stream));
+    std::lock_guard<std::mutex> lk(f->h.mu);  // one solve at a time per factorization (shared engine buffers)
+    // NULL is the legacy default stream: order the solve after the caller's work there too
+    cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    factor_solve_device(f->h, nrhs, reinterpret_cast<double2*>(d_x), user);
     if (!stream) HS_CUDA(cudaStreamSynchronize(f->h.eng.stream));
   });
 }
@@ -933,6 +943,7 @@ extern "C" int hs_factor_solve(hs_factor* f, int nrhs, double* x) {
     if (nrhs <= 0) return;
     FactorHandle& H = f->h;
     HS_CUDA(cudaSetDevice(H.eng.device));
+    std::lock_guard<std::mutex> lk(H.mu);  // one solve at a time per factorization (shared engine buffers)
     const long long n = H.stats.n;
     H.io.alloc(static_cast<size_t>(n) * nrhs);
     HS_CUDA(cudaMemcpyAsync(H.io.p, x, sizeof(double2) * n * nrhs, cudaMemcpyHostToDevice, H.eng.stream));
@@ -1123,6 +1134,8 @@ struct DdmHandle {
     cudaGraphExec_t exec;
   };
   std::vector<AppGraph> graphs;
+  // graphs on unless HS_GRAPH=0; a capture this handle cannot do turns them off for this handle only
+  bool use_graph = !(std::getenv("HS_GRAPH") && std::atoi(std::getenv("HS_GRAPH")) == 0);
   long long state_gen = 0;
   bool capturing = false;
   // timing events inside a captured application must be graph event-record nodes
@@ -1857,7 +1870,6 @@ void DdmHandle::ensure_gop() {
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
 void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
-  static bool use_graph = !(std::getenv("HS_GRAPH") && std::atoi(std::getenv("HS_GRAPH")) == 0);
   if (io || partitioned() || !use_graph || std::getenv("HS_TRACE")) {
     run_body(nrounds, track, timed, io);
     return;
@@ -1879,13 +1891,23 @@ void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
     HS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
     bool ok = true;
     capturing = true;
+    std::exception_ptr err;
     try {
       run_body(nrounds, track, timed, nullptr);
     } catch (const Error&) {
       ok = false;
+    } catch (...) {  // anything else (e.g. host allocation): end the capture, then rethrow
+      ok = false;
+      err = std::current_exception();
     }
     capturing = false;
     const cudaError_t ec = cudaStreamEndCapture(s, &graph);
+    if (err) {
+      if (graph) cudaGraphDestroy(graph);
+      (void)cudaGetLastError();
+      g_kernel_launches.fetch_sub(g_kernel_launches.load() - l0);
+      std::rethrow_exception(err);
+    }
     AppGraph g{nrounds, track, timed, gen, g_kernel_launches.load() - l0, nullptr};
     g_kernel_launches.fetch_sub(g.launches);  // counted when the graph runs
     if (ok && ec == cudaSuccess && graph && cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
@@ -2435,10 +2457,10 @@ extern "C" int hs_ddm_solve_device(hs_ddm* s, int nrhs, const double* d_b, doubl
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaEvent_t evw;
     HS_CUDA(cudaEventCreateWithFlags(&evw, cudaEventDisableTiming));
-    if (user) {
-      HS_CUDA(cudaEventRecord(evw, user));
-      HS_CUDA(cudaStreamWaitEvent(H.eng.stream, evw, 0));
-    }
+    // NULL is the legacy default stream: the solver stream is non-blocking, so order the
+    // application after the caller's work there explicitly (b may be written by it)
+    HS_CUDA(cudaEventRecord(evw, user ? user : cudaStreamLegacy));
+    HS_CUDA(cudaStreamWaitEvent(H.eng.stream, evw, 0));
     const long long n = H.geom.gn;
     for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
       const int R = std::min(kMaxRhs, nrhs - b0);
@@ -2844,6 +2866,7 @@ extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double*
       }
     });
     FactorHandle& F = H.gfact->h;
+    std::lock_guard<std::mutex> lk(F.mu);
     F.io.alloc(static_cast<size_t>(n) * nrhs);
     HS_CUDA(cudaMemcpyAsync(F.io.p, u, sizeof(double2) * n * nrhs, cudaMemcpyHostToDevice, F.eng.stream));
     factor_solve_device(F, nrhs, F.io.p, nullptr);
@@ -2855,6 +2878,18 @@ extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double*
 namespace hsb {
 std::string& last_error_ref() { return g_last_error; }  // shared with the on-disk format entry points (hs_io.cpp)
 }  // namespace hsb
+
+extern "C" int hs_ddm_memory(const hs_ddm* s, int64_t* factor_bytes, int64_t* state_bytes, int* max_batch) {
+  if (!s) return kConfig;
+  const DdmHandle& H = s->h;
+  const Engine& E = H.eng;
+  if (factor_bytes) *factor_bytes = static_cast<int64_t>(E.factor.n * sizeof(double2));
+  if (state_bytes)
+    *state_bytes = static_cast<int64_t>((E.x.n + E.x1.n + E.rb.n + E.vbuf.n) * sizeof(double2) + E.part.n * sizeof(double) +
+                                        (H.mbox.n + H.bN.n + H.u.n + H.io.n) * sizeof(double2));
+  if (max_batch) *max_batch = kMaxRhs;
+  return kOk;
+}
 
 extern "C" int hs_ddm_schedule_info(hs_ddm* s, int rounds, int* macro_steps, int* max_width, int* sequential_steps,
                                     int* buffers) {

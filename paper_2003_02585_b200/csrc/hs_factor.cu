@@ -790,12 +790,12 @@ long long factor_big_scratch(int max_m) {  // per cluster, double2 entries
 }
 
 void launch_factor_big(const FactorArgs& a, int max_m, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDevice configured;
+  configured.get([](int) {
     HS_CUDA(cudaFuncSetAttribute(factor_big_kernel<kFactorCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kSmemBytes)));
-    configured = true;
-  }
+    return 1;
+  });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(a.ntasks) * kFactorCluster);
   cfg.blockDim = dim3(kT);

@@ -722,11 +722,11 @@ int blocks_for(long long n, int t = kThreads) { return static_cast<int>((n + t -
 size_t factor_smem_bytes(int max_m) { return static_cast<size_t>(2) * max_m * kNB * sizeof(double2); }
 
 void launch_factor_level(const FactorArgs& a, int max_m, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static PerDevice configured;
+  configured.get([](int) {
     HS_CUDA(cudaFuncSetAttribute(factor_level_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    configured = true;
-  }
+    return 1;
+  });
   const size_t need = factor_smem_bytes(max_m);
   const bool use_smem = need <= 200 * 1024;
   factor_level_kernel<1><<<a.ntasks, kThreads, use_smem ? need : 0, s>>>(

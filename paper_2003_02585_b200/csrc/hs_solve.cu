@@ -833,16 +833,14 @@ constexpr size_t ring_bytes() {
 
 template <bool FWD, bool M3>
 int solve_grid() {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 0, per = 0;
-    HS_CUDA(cudaGetDevice(&dev));
+  static PerDevice grid;  // per device: the attribute opt-in and the co-resident grid size
+  return grid.get([](int dev) {
+    int sms = 0, per = 0;
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     HS_CUDA(cudaFuncSetAttribute(solve6_kernel<FWD, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<FWD>()));
     HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<FWD, M3>, kThreads, ring_bytes<FWD>()));
-    grid = sms * std::max(per, 1);
-  }
-  return grid;
+    return sms * std::max(per, 1);
+  });
 }
 
 template <bool FWD, bool M3>

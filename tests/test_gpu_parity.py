@@ -422,7 +422,8 @@ def test_alternate_engine_paths_match_reference(env):
     """The engine's alternates, each selected per process by an environment switch, against the
     reference's golden u: the four-product solve kernels (HS_M3=0, 4 CTAs/SM), stream-by-stream
     launches instead of the captured CUDA graph (HS_GRAPH=0), and the plain level order with
-    one split-K chunk size per band (HS_ORDER=0, HS_MAX_CHUNKS=1: the longest chunks)."""
+    the widest split-K chunks (HS_ORDER=0, HS_MAX_CHUNKS=1: 16-block chunks; a band
+    longer than 16 blocks still splits)."""
     import os
     import subprocess
     import sys
@@ -432,3 +433,72 @@ def test_alternate_engine_paths_match_reference(env):
     assert r.returncode == 0, r.stderr[-2000:]
     worst = float(r.stdout.split("WORST")[-1])
     assert worst <= TOL
+
+
+def test_concurrent_solves_on_one_factorization(hs, golden):
+    """Factorization::solve is "reentrant; safe for concurrent calls on one factorization"
+    (include/helmsweep/direct.hpp:29): two host threads solving different right-hand sides on one
+    handle (ctypes releases the GIL) each get exactly the single-threaded result."""
+    import threading
+    z = golden("direct_3d")
+    f = hs.factorize(sparse_op(hs, z))
+    n = f.stats().n
+    g = np.random.default_rng(29)
+    B = [g.standard_normal((3, n)) + 1j * g.standard_normal((3, n)) for _ in range(4)]
+    want = [f.solve(b) for b in B]
+    got = [None] * len(B)
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(5):
+                got[i] = f.solve(B[i])
+                if not np.array_equal(got[i], want[i]):
+                    errs.append(i)
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(B))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+
+
+def test_null_stream_is_ordered_after_legacy_default_stream(hs, golden):
+    """stream = NULL means the legacy default stream (include/helmsweep_b200.h): b written there by
+    a kernel, with no host synchronisation, must be read only after that kernel (the solver's own
+    stream is non-blocking). Checked for hs_ddm_solve_device and hs_factor_solve_device."""
+    torch = pytest.importorskip("torch")
+    z = golden("ddm_2d_3x2_r2")
+    s = hs.DdmSolver(_setup(hs, z))
+    b = np.ascontiguousarray(z["b"], dtype=np.complex128)
+    R = b.shape[0]
+    rounds = int(z["rounds"])
+    want = s.ddm_solve(b, rounds, None, False)
+    src = torch.from_numpy(b.view(np.float64)).cuda()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(torch.cuda.default_stream()):
+        db = torch.zeros_like(src)
+        du = torch.zeros_like(src)
+        big = torch.ones(64 << 20, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        for _ in range(20):  # keep the legacy stream busy before b gets its values
+            big.mul_(1.0000001)
+        db.copy_(src)
+        s.ddm_solve_device(db.data_ptr(), du.data_ptr(), R, rounds, False, 0)
+    torch.cuda.synchronize()
+    got = du.cpu().numpy().view(np.complex128).reshape(R, -1)
+    assert np.array_equal(got, np.asarray(want).reshape(R, -1))
+    zf = golden("direct_2d")
+    f = hs.factorize(sparse_op(hs, zf))
+    xb = torch.from_numpy(np.ascontiguousarray(zf["b"], dtype=np.complex128).view(np.float64)).cuda()
+    torch.cuda.synchronize()
+    dx = torch.zeros_like(xb)
+    for _ in range(20):
+        big.mul_(1.0000001)
+    dx.copy_(xb)
+    f.solve_device(dx.data_ptr(), 1, 0)
+    torch.cuda.synchronize()
+    assert rel(dx.cpu().numpy().view(np.complex128), zf["x"]) <= 1e-12
