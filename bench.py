@@ -364,7 +364,7 @@ def run_gpu(args, rank, world, local_rank):
                      "alg_flops_per_launch": prof["alg_flops"] / nl,
                      "alg_bytes_per_launch": prof["alg_bytes"] / nl,
                      "avg_launch_us": 1e6 * sec / nl,
-                     "solve_share_of_step": sec / (ms_max * 1e-3),
+                     "solve_share_of_step": sec * s.batches_per_application(R) / (ms_max * 1e-3),
                      "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
                                   "peak_source": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)"}},
         "e2e": {"value": e2e_val, "unit": "RHS/s", "h2d_bytes_per_step": int(b.nbytes),

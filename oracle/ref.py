@@ -173,6 +173,11 @@ class RefSolver:
         return u
 
 
+def blas_active():
+    """Whether the shim's large dense products run on OpenBLAS (HSREF_BLAS=0 forces naive loops)."""
+    return bool(lib().hsref_blas_active())
+
+
 def route(dim, rounds, gen_sweep, axis, sign):
     return lib().hsref_route(int(dim), int(rounds), int(gen_sweep), int(axis), int(sign))
 

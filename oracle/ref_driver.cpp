@@ -13,6 +13,7 @@
 //   parse_config_text                       proj/include/helmsweep/config.hpp:55
 //   write_velocity_grid / read_velocity_grid proj/include/helmsweep/media.hpp:22-27
 //   write_field / read_field                proj/include/helmsweep/harness.hpp:10-16
+#include <Eigen/Dense>  // the oracle shim (hsref_blas_active)
 #include <chrono>
 #include <cstdint>
 #include <span>
@@ -59,6 +60,9 @@ struct hsref_report {
 };
 
 const char* hsref_last_error() { return g_err.c_str(); }
+
+// 1 when the Eigen-subset shim routes large dense products to OpenBLAS (shim/Eigen/Dense).
+int hsref_blas_active() { return hsref_blas::active() ? 1 : 0; }
 
 // Parses reference config text (key = value lines, src/config.cpp:90-196); an
 // optional workers override (>0) replaces sweep.workers; builds DdmSolver
