@@ -263,8 +263,8 @@ def run_gpu(args, rank, world, local_rank):
     part = world > 1 and args.partition == "subdomain"
     t0 = time.perf_counter()
     if part:
-        from paper_2003_02585_b200.multi import PartitionedDdmSolver
-        s = PartitionedDdmSolver(setup, device=local_rank)
+        from paper_2003_02585_b200.multi import make_partitioned
+        s = make_partitioned(setup, device=local_rank)  # native NCCL transport inside the library
     else:
         s = hs.DdmSolver(setup, device=local_rank)
     setup_seconds = time.perf_counter() - t0

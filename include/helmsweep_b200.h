@@ -247,6 +247,16 @@ int hs_partition_traffic(int dim, const int counts[3], int rounds, int world, co
 int hs_ddm_create_partitioned(const hs_problem* setup, int device, int rank, int world, const int* owner,
                               hs_exchange_fn exchange, hs_allreduce_fn allreduce, void* user, hs_ddm** out,
                               int* pivot_sub, int64_t* pivot_index);
+/* Native NCCL transport (libnccl loaded at run time; no caller callbacks). One rank calls
+ * hs_nccl_unique_id and distributes the 128 bytes to every rank (any channel); every rank then
+ * calls hs_ddm_create_nccl with them (collective: it builds the library's own communicator). The
+ * per-macro-step exchange runs as ncclSend/ncclRecv groups and the reductions as ncclAllReduce on
+ * the solver stream, so applications stay CUDA-graph captured. world == 1 runs the partitioned
+ * machinery over one rank (every node home, no peers). HS_ERR_CUDA when libnccl is missing. */
+int hs_nccl_unique_id(unsigned char id[128]);
+int hs_nccl_version(int* version);
+int hs_ddm_create_nccl(const hs_problem* setup, int device, int rank, int world, const int* owner,
+                       const unsigned char id[128], hs_ddm** out, int* pivot_sub, int64_t* pivot_index);
 /* Owned subdomains of this rank and the exchange volume (doubles sent per application, for the
  * last batch width and rounds solved). */
 int hs_ddm_partition_info(const hs_ddm* s, int* rank, int* world, int* owned, int64_t* sent_doubles,

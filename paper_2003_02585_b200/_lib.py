@@ -132,6 +132,11 @@ SIGNATURES = {
     "hs_ddm_create_partitioned": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                  c_int_p, EXCHANGE_FN, ALLREDUCE_FN, ctypes.c_void_p,
                                                  ctypes.POINTER(ctypes.c_void_p), c_int_p, c_i64_p]),
+    "hs_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
+    "hs_nccl_version": (ctypes.c_int, [c_int_p]),
+    "hs_ddm_create_nccl": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int, c_int_p,
+                                          ctypes.POINTER(ctypes.c_ubyte), ctypes.POINTER(ctypes.c_void_p), c_int_p,
+                                          c_i64_p]),
     "hs_ddm_memory": (ctypes.c_int, [ctypes.c_void_p, c_i64_p, c_i64_p, c_int_p]),
     "hs_ddm_partition_info": (ctypes.c_int, [ctypes.c_void_p, c_int_p, c_int_p, c_int_p, c_i64_p, c_i64_p]),
 }

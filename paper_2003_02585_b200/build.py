@@ -67,7 +67,7 @@ def build(verbose=False, force=False):
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         list(ex.map(run, jobs))
     if jobs or not os.path.exists(OUT):
-        run([nvcc] + ARCH + ["-ccbin", HOST_CXX, "-shared", "-o", OUT] + objs + ["-lcudart_static"])
+        run([nvcc] + ARCH + ["-ccbin", HOST_CXX, "-shared", "-o", OUT] + objs + ["-lcudart_static", "-ldl"])
     return OUT
 
 

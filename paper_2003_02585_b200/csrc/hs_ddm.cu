@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -21,6 +22,7 @@
 
 #include "helmsweep_b200.h"
 #include "hs_kernels.cuh"
+#include "hs_nccl.hpp"
 #include "hs_partition.hpp"
 #include "hs_symbolic.hpp"
 
@@ -600,6 +602,12 @@ struct Engine {
   // of the dataflow launch).
   struct TaskRef {
     int sub, l, xb;
+    // static pruning of the item lists (the kernels also skip at run time, but every listed item
+    // costs a ticket and its record loads): faces that can ever carry injected data in this task
+    // (0x100: every front is live, sweep 1's split source) and the subdomain's bitset of fronts whose
+    // x the application reads back (null: every front)
+    unsigned faces = 0x100u;
+    const unsigned* need = nullptr;
   };
   // estimated time of one front's items (us): wake-up + the longest item's k-loop + split-K reduce
   static double front_cost(const FrontDesc& fd, int chunk, bool fwd) {
@@ -628,6 +636,7 @@ struct Engine {
   }
   void build_items(const std::vector<TaskRef>& tasks, std::vector<SolveItem>& fwd, std::vector<SolveItem>& bwd) const {
     static const int mode = std::getenv("HS_ORDER") ? std::atoi(std::getenv("HS_ORDER")) : 1;
+    static const bool no_prune = std::getenv("HS_NO_PRUNE") != nullptr;  // developer A/B switch
     const int nsub = static_cast<int>(sub_cls.size());
     struct Ent {
       double key;
@@ -641,11 +650,18 @@ struct Engine {
       const SymbolicClass& c = *cd.sym;
       if (&cd != last) front_priorities(cd, pf, pb);
       last = &cd;
+      const TaskRef& tk = tasks[g];
+      const bool all_live = (tk.faces & 0x100u) != 0 || cd.fbits.empty() || no_prune;
       for (int q = 0; q < static_cast<int>(c.fronts.size()); ++q) {
         const int fu = c.order_up[q], fd = c.order_down[q];
         // level order: forward by height, backward by depth (key = -level, ties by task, order)
-        ef.push_back(Ent{mode ? pf[fu] : -static_cast<double>(c.fronts[fu].height), static_cast<int>(g), q, fu});
-        eb.push_back(Ent{mode ? pb[fd] : -static_cast<double>(c.fronts[fd].depth), static_cast<int>(g), q, fd});
+        // forward: a front whose subtree holds no injection line of a face that can receive data has
+        // T = z = V = 0 (its live parent ignores it); backward: a front whose x is never read back
+        // (nor its subtree's) is skipped -- neither is listed
+        if (all_live || (cd.fbits[fu] & tk.faces & 0xFFu))
+          ef.push_back(Ent{mode ? pf[fu] : -static_cast<double>(c.fronts[fu].height), static_cast<int>(g), q, fu});
+        if (!tk.need || no_prune || ((tk.need[fd >> 5] >> (fd & 31)) & 1u))
+          eb.push_back(Ent{mode ? pb[fd] : -static_cast<double>(c.fronts[fd].depth), static_cast<int>(g), q, fd});
       }
     }
     auto cmp = [](const Ent& x, const Ent& y) {
@@ -655,27 +671,45 @@ struct Engine {
     };
     std::sort(ef.begin(), ef.end(), cmp);
     std::sort(eb.begin(), eb.end(), cmp);
+    // Unsplit bands of a front are merged into items of at most merge_ksteps k-steps (every RHS
+    // group of a band in the same item, consecutive bands while they fit): a unit of a small front
+    // is a few k-steps, so per-item costs (records, dependency wait, ticket, release) dominated.
+    static const int merge_ksteps = std::getenv("HS_MERGE") ? std::atoi(std::getenv("HS_MERGE")) : 64;
+    auto emit = [&](std::vector<SolveItem>& out, int nzi, int f, int job, int slot, int gw, int nb,
+                    const std::function<int(int)>& nch, const std::function<int(int)>& ksteps) {
+      const int ngrp = (R + gw - 1) / gw;
+      int t = 0;
+      while (t < nb) {
+        if (nch(t) > 1 || merge_ksteps <= 0) {  // split band (or merging off): one item per unit
+          for (int ch = 0; ch < nch(t); ++ch)
+            for (int r0 = 0; r0 < R; r0 += gw)
+              out.push_back(SolveItem{nzi, f, job, t, slot, r0, std::min(gw, R - r0), ch, t + 1, r0 + std::min(gw, R - r0)});
+          ++t;
+          continue;
+        }
+        int t1 = t, ks = 0;
+        while (t1 < nb && nch(t1) == 1 && (t1 == t || ks + ksteps(t1) * ngrp <= merge_ksteps)) ks += ksteps(t1++) * ngrp;
+        out.push_back(SolveItem{nzi, f, job, t, slot, 0, std::min(gw, R), 0, t1, R});
+        t = t1;
+      }
+    };
     for (const Ent& e : ef) {
       const TaskRef& tk = tasks[e.g];
       const ClassDev& cd = *classes[sub_cls[tk.sub]];
       const FrontDesc& fd = cd.sym->fronts[e.f];
       const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
       const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
-      for (int t = 0; t < nband; ++t)
-        for (int ch = 0; ch < solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); ++ch)
-          for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
-            fwd.push_back(SolveItem{nzi, f, jb + f, t, e.g, r0, std::min(cd.fgw[f], R - r0), ch});
+      emit(fwd, nzi, f, jb + f, e.g, cd.fgw[f], nband, [&](int t) { return solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); },
+           [&](int t) { return 2 * std::min(kb, 4 * t + 4); });
     }
     for (const Ent& e : eb) {
       const TaskRef& tk = tasks[e.g];
       const ClassDev& cd = *classes[sub_cls[tk.sub]];
       const FrontDesc& fd = cd.sym->fronts[e.f];
       const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
-      const int ncband = ((pad8(fd.k) >> 3) + 3) / 4;
-      for (int u = 0; u < ncband; ++u)
-        for (int ch = 0; ch < solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); ++ch)
-          for (int r0 = 0; r0 < R; r0 += cd.fgw[f])
-            bwd.push_back(SolveItem{nzi, f, jb + f, u, e.g, r0, std::min(cd.fgw[f], R - r0), ch});
+      const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), ncband = (kb + 3) / 4;
+      emit(bwd, nzi, f, jb + f, e.g, cd.fgw[f], ncband, [&](int u) { return solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); },
+           [&](int u) { return 2 * (nrb - 4 * u); });
     }
   }
 
@@ -1092,7 +1126,11 @@ struct DdmHandle {
   DBuf<double> xsend, xrecv, dtmp;
   DBuf<double2> ufull;
   long long x_sent = 0, x_msgs = 0;
-  bool partitioned() const { return world > 1; }
+  // the library's own NCCL communicator (hs_ddm_create_nccl): exchange and reductions issued on the
+  // solver stream without caller callbacks, so partitioned applications are graph-captured too. With
+  // it the partitioned machinery runs even at world 1 (every node home, no peers).
+  std::unique_ptr<NcclComm> ncomm;
+  bool partitioned() const { return world > 1 || ncomm != nullptr; }
   void build_xplan();
   void comm_allreduce(double* buf, long long count);
 
@@ -1707,7 +1745,24 @@ void DdmHandle::build_items() {
   bwd_cnt.assign(nm, 0);
   for (int m = 0; m < nm; ++m) {
     std::vector<Engine::TaskRef> refs;
-    for (const int2& t : msteps_own[m]) refs.push_back(Engine::TaskRef{t.x, t.y, (t.y - 1) % nbuf});
+    for (const int2& t : msteps_own[m]) {
+      Engine::TaskRef r{t.x, t.y, (t.y - 1) % nbuf};
+      if (t.y > 1) {  // faces whose mailbox slots some generating sweep can fill for sweep t.y
+        r.faces = 0;
+        const Vec3i sb = subs[t.x].sub;
+        for (int d = 0; d < dirs; ++d) {
+          const int ax = d / 2, sg = (d & 1) ? 1 : -1;
+          if (!part.has_neighbor(sb, ax, -sg)) continue;  // the trace travels +sg from the neighbour at -sg
+          for (int lg = 1; lg <= t.y; ++lg)
+            if (route_h[(lg - 1) * dirs + d] == t.y) {
+              r.faces |= 1u << d;
+              break;
+            }
+        }
+      }
+      if (!need_h.empty()) r.need = need_h.data() + static_cast<size_t>(t.x) * need_words;
+      refs.push_back(r);
+    }
     std::vector<SolveItem> fw, bw;
     eng.build_items(refs, fw, bw);
     fwd_off[m] = static_cast<int>(tasks.size());
@@ -1805,6 +1860,10 @@ void DdmHandle::build_xplan() {
 }
 
 void DdmHandle::comm_allreduce(double* buf, long long count) {
+  if (ncomm) {
+    ncomm->allreduce(buf, count, eng.stream);
+    return;
+  }
   if (!arfn) throw Error(kConfig, "partitioned solve: no allreduce callback");
   if (arfn(cuser, buf, count, eng.stream) != 0) throw Error(kCuda, "partitioned solve: allreduce callback failed");
 }
@@ -1870,7 +1929,8 @@ void DdmHandle::ensure_gop() {
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
 void DdmHandle::run(int nrounds, bool track, bool timed, const StreamIO* io) {
-  if (io || partitioned() || !use_graph || std::getenv("HS_TRACE")) {
+  // caller callbacks (host-side transport) cannot be captured; the native NCCL transport can
+  if (io || (partitioned() && !ncomm) || !use_graph || std::getenv("HS_TRACE")) {
     run_body(nrounds, track, timed, io);
     return;
   }
@@ -1955,6 +2015,9 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   int waited = 0, stripes_done = 0;  // waited: tiles of b staged (copy order)
   bool u_reduced = false;
   static const bool no_skip = std::getenv("HS_NO_FRONT_SKIP") != nullptr;  // developer A/B switch
+  // the backward's unread fronts are pruned from the item lists (build_items); the run-time check
+  // of the need bitset is only needed without that pruning
+  static const bool no_prune = std::getenv("HS_NO_PRUNE") != nullptr;
   auto stage_in = [&](int upto) {  // tiles [waited, upto) of b: copied -> transposed into bN
     for (int k = waited; k < upto; ++k) {
       const InTile& t = in_tiles[k];
@@ -1988,16 +2051,21 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     const bool traced = std::getenv("HS_TRACE") && m == (tstep ? std::atoi(tstep) : nm / 2);
     if (sa.ntasks > 0)
       eng.run_solve(d_tasks.p + fwd_off[m], fwd_cnt[m], d_tasks.p + bwd_off[m], bwd_cnt[m], nzmask.p, traced,
-                    no_skip ? nullptr : tface.p, no_skip ? nullptr : need.p, need_words);
+                    no_skip ? nullptr : tface.p, no_skip || !no_prune ? nullptr : need.p, need_words);
     if (timed) record(ev[2 + nsweeps + 2 * m], s);
     if (sa.ntasks > 0) launch_extract_deposit(sa, static_cast<int>(line_max), s);
     if (partitioned() && !xplan[m].peers.empty()) {  // traces and ghost values to / from other ranks
       const XPlan& xp = xplan[m];
       launch_xpack(d_xseg.p + xp.s0, xp.ns, true, xsend.p, mbox.p, mpres.p, eng.x.p, nzmask.p, d_gpos.p, R, s);
-      if (!xfn) throw Error(kConfig, "partitioned solve: no exchange callback");
-      if (xfn(cuser, static_cast<int>(xp.peers.size()), xp.peers.data(), xp.soff.data(), xp.scnt.data(),
-              xp.roff.data(), xp.rcnt.data(), xsend.p, xrecv.p, s) != 0)
-        throw Error(kCuda, "partitioned solve: exchange callback failed");
+      if (ncomm) {
+        ncomm->exchange(static_cast<int>(xp.peers.size()), xp.peers.data(), xp.soff.data(), xp.scnt.data(),
+                        xp.roff.data(), xp.rcnt.data(), xsend.p, xrecv.p, s);
+      } else {
+        if (!xfn) throw Error(kConfig, "partitioned solve: no exchange callback");
+        if (xfn(cuser, static_cast<int>(xp.peers.size()), xp.peers.data(), xp.soff.data(), xp.scnt.data(),
+                xp.roff.data(), xp.rcnt.data(), xsend.p, xrecv.p, s) != 0)
+          throw Error(kCuda, "partitioned solve: exchange callback failed");
+      }
       launch_xpack(d_xseg.p + xp.r0, xp.nr, false, xrecv.p, mbox.p, mpres.p, eng.x.p, nzmask.p, d_gpos.p, R, s);
     }
     auto accumulate = [&](int l, long long n0, long long n1, long long pbase) {
@@ -2353,6 +2421,38 @@ extern "C" int hs_ddm_create_partitioned(const hs_problem* setup, int device, in
         s->h.xfn = exchange;
         s->h.arfn = allreduce;
         s->h.cuser = user;
+        s->h.build(*setup, device, rank, world, owner);
+      },
+      pivot_sub, pivot_index);
+  if (rc != kOk) return rc;
+  *out = s.release();
+  return kOk;
+}
+
+extern "C" int hs_nccl_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    if (!id) config_error("hs_nccl_unique_id: null argument");
+    nccl_unique_id(id);
+  });
+}
+
+extern "C" int hs_nccl_version(int* version) {
+  return guarded([&] {
+    if (!version) config_error("hs_nccl_version: null argument");
+    *version = nccl_version();
+  });
+}
+
+extern "C" int hs_ddm_create_nccl(const hs_problem* setup, int device, int rank, int world, const int* owner,
+                                  const unsigned char id[128], hs_ddm** out, int* pivot_sub, int64_t* pivot_index) {
+  std::unique_ptr<hs_ddm> s;
+  const int rc = guarded(
+      [&] {
+        if (!setup || !out || !id) config_error("hs_ddm_create_nccl: null argument");
+        if (world < 1 || rank < 0 || rank >= world) config_error("partition: rank out of range");
+        s = std::make_unique<hs_ddm>();
+        HS_CUDA(cudaSetDevice(device));
+        s->h.ncomm = std::make_unique<NcclComm>(id, rank, world);  // collective over the ranks
         s->h.build(*setup, device, rank, world, owner);
       },
       pivot_sub, pivot_index);

@@ -73,8 +73,12 @@ struct DevGeom {
 // block-row chunk `chunk`; RHS columns [r0, r0 + rw), rw <= 16. slot = position of the task
 // in its macro-step; job = its (x buffer, subdomain, front) record; nzi = the task's entry in the
 // per-(sweep, subdomain) nonzero masks.
+// A merged item (idx1 > idx + 1 or r1 > r0 + rw) runs the unsplit units (band t in [idx, idx1)) x
+// (RHS group r in [r0, r1), step gw) one after the other in one warp: one dependency wait, one
+// ticket and one release for all of them (small fronts' units are only a few k-steps long).
 struct SolveItem {
   int nzi, front, job, idx, slot, r0, rw, chunk;
+  int idx1, r1;
 };
 
 // Everything a solve item needs about its (subdomain, front), resolved on the host for the

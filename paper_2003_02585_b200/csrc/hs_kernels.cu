@@ -434,6 +434,22 @@ __global__ void nonzero_kernel(SweepArgs a) {
   }
   bits = __reduce_or_sync(kFull, bits);
   faces = __reduce_or_sync(kFull, faces);
+  // Only faces whose mailbox slots some generating sweep fills for this sweep carry injected data;
+  // lines of other faces can hold a nonzero value only where they cross a receiving face's line,
+  // at nodes whose fronts are live through that face. The host prunes the forward item lists with
+  // the same static face set (DdmHandle::build_items), so the run-time set must stay inside it: a
+  // front listed as dead must never be waited for.
+  unsigned recv = 0;
+  for (int d = 0; d < a.dirs; ++d) {
+    const int ax = d >> 1, nb = S.sub[ax] - ((d & 1) ? 1 : -1);
+    if (nb < 0 || nb >= a.g.counts[ax]) continue;
+    for (int lg = 1; lg <= l; ++lg)
+      if (a.route[(lg - 1) * a.dirs + d] == l) {
+        recv |= 1u << d;
+        break;
+      }
+  }
+  faces &= recv;
   const long long ti = static_cast<long long>(l - 1) * a.g.nsub + sub;
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[ti], bits);
   // sweep 1 also carries the split source anywhere in the subdomain: every front is live (0x100)

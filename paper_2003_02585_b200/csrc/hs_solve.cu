@@ -93,9 +93,9 @@ __device__ __forceinline__ void wait_count(const int* p, int target, int lane) {
 }
 // Release: the warp's stores are ordered before lane 0's release by the warp barrier (the
 // CUTLASS-semaphore pattern); no full fence.
-__device__ __forceinline__ void signal(int* p, int lane) {
+__device__ __forceinline__ void signal(int* p, int lane, int count = 1) {
   __syncwarp();
-  if (lane == 0) red_release_add(p, 1);
+  if (lane == 0) red_release_add(p, count);
 }
 __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
   int old;
@@ -296,6 +296,18 @@ __device__ __forceinline__ bool split_reduce(Acc<NT, M3>& c, double* base, long 
   return true;
 }
 
+// 16-byte cp.async with zero fill: when !ok no byte is read (src-size 0), so src may be any
+// address (the lean k-loops pass the computed one instead of selecting a fallback)
+__device__ __forceinline__ void cp16z(double2* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp16a(double2* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp16(double2* dst, const double2* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
                "l"(src), "r"(ok ? 16 : 0)
@@ -391,6 +403,188 @@ __device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, I
     } else {
       if (mk == 0xFu)
         mma_step<false, true>(acc, A, B, mk);
+      else
+        mma_step<false, false>(acc, A, B, mk);
+    }
+  }
+  cp_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------
+// Lean k-loops (HS_LEAN, default). The generic kloop above recomputes every address, tile mask
+// and fallback pointer of a k-step from the k-step index, which the compiler turned into ~250
+// instructions per 24 DMMAs (ncu, C3 macro-step 35: 15 instructions per DMMA, DMMA pipe 24-37%
+// active). Here each lane keeps running pointers that advance by constants, and every m-tile is
+// computed: the factor stores M's blocks above the diagonal (within the diagonal band) as zeros
+// and its padded rows / columns as zeros, so the skipped tiles only ever added 0 * finite; m-tiles
+// past the stored band (the front's last band) read tile 0 again and their rows are discarded by
+// the finalize. B rows past the front (columns >= k, boundary rows >= m - k) are zero-filled, so
+// nothing outside the vectors is read. Each lane reads back only the ring entries it staged
+// itself, so the ring needs no warp barriers.
+#ifndef HS_LEAN
+#define HS_LEAN 1
+#endif
+
+// Forward band item: out[32 band rows][8 NT RHS] += [M; W][rows, chunk cols] * T_sep[chunk cols],
+// T = rhs + child0 V + child1 V summed at use in the reference's child order.
+//   pa    this lane's A address for k-step 0, m-tile 0 (bytes)
+//   toff  byte offsets of m-tiles 1..3 (tile 0's when the band has fewer row blocks)
+//   xr    rhs row of this lane's column in k-step 0, RHS r0 + lane/4 (bytes)
+//   vr    update-vector slot base at RHS r0 + lane/4 (bytes); rows from the staged source map
+//   kcnt  k-steps whose column (col0 + 4 s) lies below k for this lane
+//   okq   bit q: RHS r0 + 8q + lane/4 exists
+template <int NT, bool M3, bool LEAF>
+__device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* ring, int lane, const char* pa,
+                                          unsigned astep, unsigned toff1, unsigned toff2, unsigned toff3,
+                                          const char* xr, unsigned xstep, int kcnt, const char* vr, unsigned R16,
+                                          const int2* sidx, bool c0, bool c1, unsigned okq, int sfull, unsigned mbase,
+                                          unsigned msep, int dshift) {
+  constexpr int NS = Ring<true, NT>::NS, ST = Ring<true, NT>::kStage;
+  double2* const last = ring + (NS - 1) * ST;
+  double2* wslot = ring;
+  double2* rslot = ring;
+  int si = 0;
+  const int2* sx = sidx + (lane & 3);
+  auto issue = [&]() {
+    double2* st = wslot + lane;
+    cp16a(st, pa);
+    cp16a(st + 32, pa + toff1);
+    cp16a(st + 64, pa + toff2);
+    cp16a(st + 96, pa + toff3);
+    const bool okc = si < kcnt;
+    double2* sb = st + 4 * 32;
+    if (LEAF) {
+#pragma unroll
+      for (int q = 0; q < NT; ++q) cp16z(sb + q * 32, xr + q * 128, okc && ((okq >> q) & 1u));
+    } else {
+      const int2 src = sx[4 * si];
+      const char* v0 = vr + static_cast<long long>(src.x) * R16;
+      const char* v1 = vr + static_cast<long long>(src.y) * R16;
+      const bool o0 = okc && c0 && src.x >= 0, o1 = okc && c1 && src.y >= 0;
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        const bool oq = (okq >> q) & 1u;
+        cp16z(sb + q * 32, xr + q * 128, okc && oq);
+        cp16z(sb + (NT + q) * 32, v0 + q * 128, o0 && oq);
+        cp16z(sb + (2 * NT + q) * 32, v1 + q * 128, o1 && oq);
+      }
+    }
+    pa += (si & 1) ? astep : 64u;
+    xr += xstep;
+    ++si;
+    wslot = wslot == last ? ring : wslot + ST;
+  };
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) {
+    if (j < ns) issue();
+    cp_commit();
+  }
+  for (int s = 0; s < ns; ++s) {
+    if (s + NS - 1 < ns) issue();
+    cp_commit();
+    cp_wait<NS - 1>();
+    const double2* st = rslot + lane;
+    double2 A[4], B[NT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) A[i] = st[i * 32];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      double2 v = st[(4 + q) * 32];
+      if (!LEAF) {
+        const double2 w0 = st[(4 + NT + q) * 32], w1 = st[(4 + 2 * NT + q) * 32];
+        v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
+        v = make_double2(v.x + w1.x, v.y + w1.y);
+      }
+      B[q] = v;
+    }
+    rslot = rslot == last ? ring : rslot + ST;
+    if (s < sfull) {
+      mma_step<false, true>(acc, A, B, 0xFu);
+    } else {  // diagonal column blocks (M's zero blocks above the diagonal) or a short last band
+      const int d = min(max(dshift + (s >> 1), 0), 4);
+      mma_step<false, false>(acc, A, B, mbase & ~(msep & ((1u << d) - 1u)));
+    }
+  }
+  cp_wait<0>();
+}
+
+// Backward column-band item: x_sep[32 band cols][8 NT RHS] = sum over the chunk's rows of
+// [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]. Row band ta = a0/4 + s/8 holds the
+// k-step's rows; its column blocks 4u..4u+3 are the m-tiles (stride rbs(ta) KB, tiles past the
+// front's column blocks re-read tile 0 and are discarded).
+template <int NT, bool M3>
+__device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* ring, int lane, const double2* P,
+                                          int kb, int nrb, int u, int a0, int cn, const char* zr, const char* XR,
+                                          unsigned R16, int row0, int k, int kp, int nb, bool zlive, unsigned okq,
+                                          const int2* sidx, int smask, unsigned mcol) {
+  constexpr int NS = Ring<false, NT>::NS, ST = Ring<false, NT>::kStage;
+  double2* const last = ring + (NS - 1) * ST;
+  double2* wslot = ring;
+  double2* rslot = ring;
+  int si = 0;
+  const char* pa = nullptr;
+  unsigned t1 = 0, t2 = 0, t3 = 0;
+  const unsigned zstep = 4u * R16;
+  const int ssep = 2 * (kb - a0);  // k-steps over separator rows (z); the rest are boundary rows
+  auto issue = [&]() {
+    if ((si & 7) == 0) {  // next row band
+      const int ta = (a0 >> 2) + (si >> 3);
+      const int rbs = min(4, nrb - 4 * ta);
+      pa = reinterpret_cast<const char*>(P + band_base(ta, kb) + 4 * u * rbs * 64);
+      const unsigned ts = static_cast<unsigned>(rbs) * 1024u;
+      t1 = cn > 1 ? ts : 0u;
+      t2 = cn > 2 ? 2u * ts : 0u;
+      t3 = cn > 3 ? 3u * ts : 0u;
+    }
+    double2* st = wslot + lane;
+    const char* p = pa + (si & 7) * 512;
+    cp16a(st, p);
+    cp16a(st + 32, p + t1);
+    cp16a(st + 64, p + t2);
+    cp16a(st + 96, p + t3);
+    const int row = row0 + 4 * si;
+    const char* src;
+    bool okb;
+    if (si < ssep) {  // separator rows: z (a structurally zero front has z = 0)
+      okb = zlive && row < k;
+      src = zr;
+    } else {  // boundary rows: the parent's x at the boundary positions
+      okb = row - kp < nb;
+      src = XR + static_cast<long long>(okb ? sidx[row - 8 * a0].x : 0) * R16;
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) cp16z(st + (4 + q) * 32, src + q * 128, okb && ((okq >> q) & 1u));
+    zr += zstep;
+    ++si;
+    wslot = wslot == last ? ring : wslot + ST;
+  };
+#pragma unroll
+  for (int j = 0; j < NS - 1; ++j) {
+    if (j < ns) issue();
+    cp_commit();
+  }
+  for (int s = 0; s < ns; ++s) {
+    if (s + NS - 1 < ns) issue();
+    cp_commit();
+    cp_wait<NS - 1>();
+    const double2* st = rslot + lane;
+    double2 A[4], B[NT];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) A[i] = st[i * 32];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) B[q] = st[(4 + q) * 32];
+    rslot = rslot == last ? ring : rslot + ST;
+    if (s >= smask) {
+      if (s >= ssep)  // boundary rows enter as -x_bnd (signs folded into the DMMA operands)
+        mma_step<true, true>(acc, A, B, 0xFu);
+      else
+        mma_step<false, true>(acc, A, B, 0xFu);
+    } else {  // M's zero blocks above the diagonal, or column blocks past the front's k
+      const int ab = a0 + (s >> 1);
+      unsigned mk = mcol;
+      if (ab < kb) mk &= (1u << min(max(ab - 4 * u + 1, 0), 4)) - 1u;
+      if (s >= ssep)
+        mma_step<true, false>(acc, A, B, mk);
       else
         mma_step<false, false>(acc, A, B, mk);
     }
@@ -571,12 +765,33 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
         }
     }
   }
+#if HS_LEAN
+  {
+    const unsigned rb1 = static_cast<unsigned>(rbs);
+    const unsigned t1 = rb1 > 1 ? 1024u : 0u, t2 = rb1 > 2 ? 2048u : 0u, t3 = rb1 > 3 ? 3072u : 0u;
+    const char* pa = reinterpret_cast<const char*>(PA);
+    const int kcnt = J.k > col0 ? (J.k - col0 + 3) >> 2 : 0;
+    unsigned okq = 0;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) okq |= okr[q] ? 1u << q : 0u;
+    const int ns = 2 * (cb1 - cb0);
+    // k-steps before the diagonal column blocks run every m-tile (when the band is full)
+    const int sfull = mbase == 0xFu ? max(0, 2 * (4 * t - cb0)) : 0;
+    if (!c0 && !c1)
+      fwd_kloop<NT, M3, true>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
+                              sidx, false, false, okq, sfull, mbase, msep, cb0 - 4 * t);
+    else
+      fwd_kloop<NT, M3, false>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
+                               sidx, c0, c1, okq, sfull, mbase, msep, cb0 - 4 * t);
+  }
+#else
   kloop<true, NT>(acc, 2 * (cb1 - cb0), ring, issue, use, mask_of, [](int) { return false; });
+#endif
   acc_finish(acc);
   take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
-    tr[6] = 2 * (cb1 - cb0);
+    tr[6] += 2 * (cb1 - cb0);
   }
   const int nch = nch_fwd(g, t, J.kc);
   if (nch > 1) {
@@ -690,12 +905,28 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   auto neg_of = [&](int s) { return a0 + (s >> 1) >= g.kb; };
   Acc<NT, M3> acc;
   acc_zero(acc);
+#if HS_LEAN
+  {
+    unsigned okq = 0;
+#pragma unroll
+    for (int q = 0; q < NT; ++q) okq |= okr[q] ? 1u << q : 0u;
+    const int cn4 = min(4, g.kb - 4 * u);
+    // masked k-steps: the diagonal block rows 4u..4u+2 (M's zero blocks above the diagonal), all of
+    // them when the column band is short
+    const int ns = 2 * (a1 - a0);
+    const int smask = mcol == 0xFu ? max(0, 2 * (4 * u + 3 - a0)) : ns;
+    bwd_kloop<NT, M3>(acc, ns, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
+                      ZR + static_cast<size_t>(static_cast<unsigned>(row0)) * R16, XR, R16, row0, J.k, g.kp, nb, zlive,
+                      okq, sidx, smask, mcol);
+  }
+#else
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
+#endif
   acc_finish(acc);
   take_ticket(a, tk, took, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
-    tr[6] = 2 * (a1 - a0);
+    tr[6] += 2 * (a1 - a0);
   }
   const int nch = nch_bwd(g, u, J.kr);
   if (nch > 1) {
@@ -755,6 +986,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? 3 : 4) solve6_kernel(SolveArgs 
     bool took = !HS_LATE_TICKET;
     if (!HS_LATE_TICKET && lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
     bool fin = false;
+    int nfin = 0;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
     // the item's task and front records, loaded together (all are read-only during the launch)
     const unsigned nzm = __ldg(a.nzmask + it.nzi);
@@ -791,12 +1023,35 @@ __global__ void __launch_bounds__(kThreads, M3 ? 3 : 4) solve6_kernel(SolveArgs 
         __syncwarp();
         if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
         double2* V = a.vbuf + it.slot * a.vslot_stride;
-        if (FWD)
-          fin = it.rw > 8 ? fwd_item<2, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
-                          : fwd_item<1, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
-        else
-          fin = it.rw > 8 ? bwd_item<2, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
-                          : bwd_item<1, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
+        // the item's units: band t x RHS group r (one unit unless merged); the ticket is taken in
+        // the last unit, the completed units are released together
+        SolveItem un = it;
+        for (int t = it.idx; t < it.idx1; ++t)
+          for (int r = it.r0; r < it.r1; r += J.gw) {
+            const bool first = t == it.idx && r == it.r0;
+            const bool lastu = t + 1 == it.idx1 && r + J.gw >= it.r1;
+            un.idx = t;
+            un.r0 = r;
+            un.rw = min(J.gw, a.R - r);
+            if (!first) {  // stage this unit's index slice / finalize data (the wait is done)
+              __syncwarp();
+              item_prefetch<FWD>(a, J, g, un, sidx, lane);
+              cp_wait<0>();
+              __syncwarp();
+            }
+            bool tku = lastu ? took : true;  // only the last unit takes the next ticket
+            bool f;
+            const SolveJob& Ju = J;
+            if (FWD)
+              f = un.rw > 8 ? fwd_item<2, M3>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku)
+                            : fwd_item<1, M3>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku);
+            else
+              f = un.rw > 8 ? bwd_item<2, M3>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku)
+                            : bwd_item<1, M3>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku);
+            if (lastu) took = tku;
+            nfin += f ? 1 : 0;
+          }
+        fin = nfin > 0;
         if (tr && lane == 0) {
           tr[4] = gtime();
           tr[5] = smid();
@@ -807,7 +1062,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? 3 : 4) solve6_kernel(SolveArgs 
     const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
     SolveItem nit{};
     if (nxt < a.nitems) nit = a.items[nxt];
-    if (fin) signal(done + it.front, lane);
+    if (fin) signal(done + it.front, lane, nfin);
     __syncwarp();  // the index slice is rewritten by the next item
     cur = nxt;
     it = nit;

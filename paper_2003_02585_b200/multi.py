@@ -113,12 +113,73 @@ def exchange_host(send: np.ndarray, recv: np.ndarray, peers, soff, scnt, roff, r
         r.wait()
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the library's own NCCL binding (hs_nccl_unique_id)."""
+    buf = (ctypes.c_ubyte * 128)()
+    rc = L.lib().hs_nccl_unique_id(buf)
+    if rc:
+        _raise(rc)
+    return bytes(buf)
+
+
+def nccl_version() -> int:
+    v = ctypes.c_int()
+    rc = L.lib().hs_nccl_version(ctypes.byref(v))
+    if rc:
+        _raise(rc)
+    return v.value
+
+
+class NcclDdmSolver(DdmSolver):
+    """DdmSolver partitioned over `world` ranks (one GPU each) with the library's native NCCL
+    transport (hs_ddm_create_nccl): the exchange and reductions are issued by the library on its
+    solver stream, no Python on the data path, applications CUDA-graph captured. `uid` is the
+    128-byte id from nccl_unique_id() on one rank, distributed to all by the caller."""
+
+    def __init__(self, setup: ProblemSetup, device: int, rank: int, world: int, uid: bytes,
+                 owner: Optional[Sequence[int]] = None):
+        self._rank, self._world = int(rank), int(world)
+        self._uid = (ctypes.c_ubyte * 128)(*uid)
+        self._owner = None if owner is None else (ctypes.c_int * len(owner))(*owner)
+        super().__init__(setup, device)
+
+    def _create(self, p, device, h, sub, piv):
+        return L.lib().hs_ddm_create_nccl(ctypes.byref(p), device, self._rank, self._world, self._owner, self._uid,
+                                          ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
+
+    def partition_info(self):
+        """(rank, world, owned subdomains, doubles sent per application, messages per application)."""
+        r, w, o = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        sd, ms = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.lib().hs_ddm_partition_info(self._h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(o),
+                                           ctypes.byref(sd), ctypes.byref(ms))
+        if rc:
+            _raise(rc)
+        return r.value, w.value, o.value, sd.value, ms.value
+
+
+def make_partitioned(setup: ProblemSetup, device: int = 0, group=None, owner: Optional[Sequence[int]] = None,
+                     transport: str = "auto"):
+    """The partitioned solver for a torch.distributed group: the native NCCL transport for NCCL
+    groups (transport "auto" / "nccl"; the id travels once through the group at construction),
+    the caller-callback transport otherwise ("callback"; gloo groups stage through host memory)."""
+    import torch.distributed as dist
+    native = transport == "nccl" or (transport == "auto" and dist.get_backend(group) == "nccl")
+    if not native:
+        return PartitionedDdmSolver(setup, device, group, owner)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return NcclDdmSolver(setup, device, rank, world, box[0], owner)
+
+
 class PartitionedDdmSolver(DdmSolver):
     """DdmSolver whose subdomains are spread over the ranks of a torch.distributed group
-    (hs_ddm_create_partitioned). Every rank constructs it with the same setup and calls
-    ddm_solve / ddm_solve_device collectively with the same b; every rank receives the full u.
-    NCCL groups exchange device buffers on the library's stream; other backends (gloo) stage
-    through host memory."""
+    (hs_ddm_create_partitioned) with a caller-supplied transport: this class's callbacks move the
+    library's messages through torch.distributed (gloo groups stage through host memory). NCCL
+    groups should use make_partitioned / NcclDdmSolver, whose transport is native. Every rank
+    constructs it with the same setup and calls ddm_solve / ddm_solve_device collectively with the
+    same b; every rank receives the full u."""
 
     def __init__(self, setup: ProblemSetup, device: int = 0, group=None, owner: Optional[Sequence[int]] = None):
         import torch

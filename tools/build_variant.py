@@ -16,7 +16,7 @@ def main():
     subprocess.run([B._nvcc()] + B._flags() + defs + ["-x", "cu", "-c", src, "-o", obj], check=True)
     objs = [os.path.join(B.BUILD, os.path.basename(s) + ".o") for s in B.sources() if not s.endswith("hs_solve.cu")]
     out = os.path.join(out_dir, f"{name}.so")
-    subprocess.run([B._nvcc()] + B.ARCH + ["-ccbin", B.HOST_CXX, "-shared", "-o", out] + objs + [obj, "-lcudart_static"], check=True)
+    subprocess.run([B._nvcc()] + B.ARCH + ["-ccbin", B.HOST_CXX, "-shared", "-o", out] + objs + [obj, "-lcudart_static", "-ldl"], check=True)
     print(out)
 
 if __name__ == "__main__":
