@@ -674,7 +674,7 @@ struct Engine {
     // Unsplit bands of a front are merged into items of at most merge_ksteps k-steps (every RHS
     // group of a band in the same item, consecutive bands while they fit): a unit of a small front
     // is a few k-steps, so per-item costs (records, dependency wait, ticket, release) dominated.
-    static const int merge_ksteps = std::getenv("HS_MERGE") ? std::atoi(std::getenv("HS_MERGE")) : 64;
+    static const int merge_ksteps = std::getenv("HS_MERGE") ? std::atoi(std::getenv("HS_MERGE")) : 0;
     auto emit = [&](std::vector<SolveItem>& out, int nzi, int f, int job, int slot, int gw, int nb,
                     const std::function<int(int)>& nch, const std::function<int(int)>& ksteps) {
       const int ngrp = (R + gw - 1) / gw;
@@ -1141,6 +1141,10 @@ struct DdmHandle {
     for (auto e : ev_out) cudaEventDestroy(e);
     for (auto c : cs)
       if (c) cudaStreamDestroy(c);
+    for (int q = 0; q < 2; ++q) {
+      if (ev_din_free[q]) cudaEventDestroy(ev_din_free[q]);
+      if (ev_dout_free[q]) cudaEventDestroy(ev_dout_free[q]);
+    }
     if (gfact) hs_factor_destroy(gfact);
   }
 
@@ -1184,7 +1188,9 @@ struct DdmHandle {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   }
-  void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps);
+  void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps, int slot = 0,
+                      bool last = true);
+  cudaEvent_t ev_din_free[2] = {}, ev_dout_free[2] = {};
   void reports(int nrounds, bool track, hs_solve_report* out);
 };
 
@@ -2268,7 +2274,8 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
 // read them, while the first macro-steps run; u streams out by regions (tiles when the accumulate
 // is fused, else stripes) as the tail of the application completes them. One copy stream per
 // direction; the copy streams carry copies only, never kernels.
-void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps) {
+void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps,
+                               int slot, bool last) {
   ensure_state(nr, nrounds);
   const long long n = geom.gn;
   const int nt = static_cast<int>(in_tiles.size());
@@ -2279,12 +2286,20 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev_in.push_back(e);
   }
-  io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
-  double2* din = io.p;
-  double2* dout = io.p + static_cast<size_t>(n) * kMaxRhs;
-  // the copy streams may overwrite din only after earlier work on the compute stream
-  HS_CUDA(cudaEventRecord(ev_in[nt], eng.stream));
-  for (auto c : cs) HS_CUDA(cudaStreamWaitEvent(c, ev_in[nt], 0));
+  for (int q = 0; q < 2; ++q)
+    for (cudaEvent_t* e : {&ev_din_free[q], &ev_dout_free[q]})
+      if (!*e) {
+        HS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        HS_CUDA(cudaEventRecord(*e, eng.stream));
+      }
+  // Two staging slots (din, dout) so consecutive batches overlap: batch k + 1's b streams in while
+  // batch k computes, and batch k's u streams out while batch k + 1 computes. A slot is reused two
+  // batches later, after the application that read its din and the copies that read its dout.
+  io.alloc(static_cast<size_t>(n) * kMaxRhs * 4);
+  double2* din = io.p + static_cast<size_t>(slot) * 2 * n * kMaxRhs;
+  double2* dout = din + static_cast<size_t>(n) * kMaxRhs;
+  HS_CUDA(cudaStreamWaitEvent(cs[0], ev_din_free[slot], 0));
+  HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_dout_free[slot], 0));
   const size_t gx = static_cast<size_t>(geom.gsize[0]), rows = static_cast<size_t>(n) / gx;
   auto copy3d = [&](const void* src, void* dst, int x0, int x1, long long r0, long long r1, cudaMemcpyKind kind,
                     cudaStream_t st) {  // (x, rows, RHS) box of the RHS-major grid
@@ -2307,6 +2322,7 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   copy_in(ev_in.data());
   const StreamIO sio{ev_in.data(), din, dout};
   run(nrounds, track, true, &sio);
+  HS_CUDA(cudaEventRecord(ev_din_free[slot], eng.stream));
   // each region of u is transposed out after its accumulate of the last sweep (ev_out); copy the
   // regions to the host in the order they complete, while the tail of the application still runs
   const std::vector<OutRegion>& regs = out_regions(true);
@@ -2324,10 +2340,12 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     if (done) HS_CUDA(cudaEventRecord(done[j], st));
   };
   for (int q = 0; q < no; ++q) copy_out(q, nullptr, nullptr);
-  for (int c = 0; c < kCopyStreams; ++c) {  // later work may reuse io / u
-    HS_CUDA(cudaEventRecord(ev_in[nt + 1 + c], cs[c]));
-    HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[nt + 1 + c], 0));
-  }
+  HS_CUDA(cudaEventRecord(ev_dout_free[slot], cs[1]));
+  if (last)
+    for (int c = 0; c < kCopyStreams; ++c) {  // later work may reuse io / u
+      HS_CUDA(cudaEventRecord(ev_in[nt + 1 + c], cs[c]));
+      HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_in[nt + 1 + c], 0));
+    }
   if (const char* path = std::getenv("HS_STREAM_TRACE")) {  // developer timeline (timing events)
     // te: [0] start, [1, 1 + nt) tile copied, then per region u final / copied out, then compute end
     std::vector<cudaEvent_t> te(nt + 2 * no + 2);
@@ -2369,8 +2387,10 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     for (auto e : te) cudaEventDestroy(e);
   }
   if (reps) reports(nrounds, track, reps);
-  for (auto c : cs) HS_CUDA(cudaStreamSynchronize(c));
-  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  if (last) {
+    for (auto c : cs) HS_CUDA(cudaStreamSynchronize(c));
+    HS_CUDA(cudaStreamSynchronize(eng.stream));
+  }
 }
 
 }  // namespace hsb
@@ -2589,16 +2609,16 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
                         cudaPointerGetAttributes(&pu, u) == cudaSuccess && pu.type == cudaMemoryTypeHost;
     (void)cudaGetLastError();  // pageable pointers may leave an error on older runtimes
     if (pinned && !H.partitioned()) {  // (a partitioned u is final only after its reduction)
-      for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
+      for (int b0 = 0, k = 0; b0 < nrhs; b0 += kMaxRhs, ++k) {  // consecutive batches overlap (two slots)
         const int R = std::min(kMaxRhs, nrhs - b0);
         H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,
-                         reports ? reports + b0 : nullptr);
+                         reports ? reports + b0 : nullptr, k & 1, b0 + kMaxRhs >= nrhs);
       }
       return;
     }
     for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
       const int R = std::min(kMaxRhs, nrhs - b0);
-      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
+      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 4);  // same size as the streamed path (two slots), first slot used;
       double2* din = H.io.p;
       double2* dout = H.io.p + static_cast<size_t>(n) * kMaxRhs;
       HS_CUDA(cudaMemcpyAsync(din, b + 2 * b0 * n, sizeof(double2) * n * R, cudaMemcpyHostToDevice, H.eng.stream));
@@ -2890,16 +2910,18 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
       }
       return p;
     };
-    // ... and the backward pass over the fronts whose x the application reads back
-    auto needed_packed = [&](int sub) {
+    // ... and the backward pass over the fronts whose x the application reads back; of a front
+    // the forward skipped (z = 0) only the boundary block W is multiplied
+    auto needed_packed = [&](int sub, unsigned fm) {
       const ClassDev& cd = *H.eng.classes[H.subs[sub].cls];
-      if (H.need_h.empty()) return static_cast<double>(cd.sym->packed_entries);
-      const unsigned* w = H.need_h.data() + static_cast<size_t>(sub) * H.need_words;
+      const unsigned* w = H.need_h.empty() ? nullptr : H.need_h.data() + static_cast<size_t>(sub) * H.need_words;
+      const bool all = (fm & 0x100u) || cd.fbits.empty();
       double p = 0.0;
       for (size_t f = 0; f < cd.sym->fronts.size(); ++f) {
-        if (!(w[f >> 5] >> (f & 31) & 1u)) continue;
+        if (w && !(w[f >> 5] >> (f & 31) & 1u)) continue;
         const double m = cd.sym->fronts[f].m, k = cd.sym->fronts[f].k;
-        p += m * k - k * (k - 1) / 2;
+        const bool zlive = all || (cd.fbits[f] & fm & 0xFFu);
+        p += zlive ? m * k - k * (k - 1) / 2 : (m - k) * k;
       }
       return p;
     };
@@ -2914,7 +2936,7 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
         if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
         const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
         const double pf = live_packed(H.subs[t.x].cls, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
-        const double pb = needed_packed(t.x);
+        const double pb = needed_packed(t.x, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
         ++solves;
         bytes += (pf + pb) * 16 + 2.0 * H.R * c.n * 16;
         flops += 8.0 * (pf + pb) * H.R;

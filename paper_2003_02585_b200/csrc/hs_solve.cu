@@ -521,13 +521,17 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   double2* const last = ring + (NS - 1) * ST;
   double2* wslot = ring;
   double2* rslot = ring;
-  int si = 0;
-  const char* pa = nullptr;
-  unsigned t1 = 0, t2 = 0, t3 = 0;
   const unsigned zstep = 4u * R16;
   const int ssep = 2 * (kb - a0);  // k-steps over separator rows (z); the rest are boundary rows
+  // A front the forward pass skipped (structurally zero right-hand side) has z = 0: its separator
+  // rows contribute nothing, so the item starts at its first boundary row (x_sep = -W^T x_bnd).
+  const int s0 = zlive ? 0 : min(max(ssep, 0), ns);
+  int si = s0;
+  zr += static_cast<long long>(s0) * zstep;
+  const char* pa = nullptr;
+  unsigned t1 = 0, t2 = 0, t3 = 0;
   auto issue = [&]() {
-    if ((si & 7) == 0) {  // next row band
+    if ((si & 7) == 0 || si == s0) {  // next row band (or the first k-step's)
       const int ta = (a0 >> 2) + (si >> 3);
       const int rbs = min(4, nrb - 4 * ta);
       pa = reinterpret_cast<const char*>(P + band_base(ta, kb) + 4 * u * rbs * 64);
@@ -560,10 +564,10 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   };
 #pragma unroll
   for (int j = 0; j < NS - 1; ++j) {
-    if (j < ns) issue();
+    if (s0 + j < ns) issue();
     cp_commit();
   }
-  for (int s = 0; s < ns; ++s) {
+  for (int s = s0; s < ns; ++s) {
     if (s + NS - 1 < ns) issue();
     cp_commit();
     cp_wait<NS - 1>();
