@@ -1150,7 +1150,7 @@ struct DdmHandle {
 
   void build(const hs_problem& P, int device, int rank_ = 0, int world_ = 1, const int* owner_ = nullptr);
   void ensure_state(int r, int nrounds);
-  void build_schedule();
+  void build_schedule(int r);
   void build_items();
   void ensure_gop();
   // Streamed host transfers (solve_streamed): per stripe, the event of its H2D copy into the
@@ -1614,9 +1614,24 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
 // Sweep accumulates stay in sweep order (u += contribution_l, src/sweeper.cpp:311), and every
 // mailbox slot has one writer, so the results equal the sequential order's: only independent
 // work is reordered. C2 (8x8, 4 sweeps): 60 sequential steps -> 29 macro-steps.
-void DdmHandle::build_schedule() {
+void DdmHandle::build_schedule(int r) {
   const int nsub = geom.nsub;
+  // x buffers in flight: one per sweep when they fit (every sweep then overlaps as the routing
+  // allows and all contributions are accumulated in one fused pass per region at the end; C3's 8
+  // sweeps: 267 -> 249 ms per 64-RHS application), else 4
   nbuf = 4;
+  {
+    const int want = std::min(nsweeps, HS_MAX_ACC_SWEEPS);
+    if (want > nbuf) {
+      size_t free_b = 0, total_b = 0;
+      HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double have = static_cast<double>(free_b) +
+                          static_cast<double>(eng.x.n + eng.x1.n + eng.rb.n) * sizeof(double2);
+      const double per_buf = 3.0 * static_cast<double>(eng.n_base.back()) * r * sizeof(double2);  // x, x1, rb
+      const double reserve = (4.0 * kMaxRhs + 4.0 * r) * static_cast<double>(geom.gn) * sizeof(double2) + 4e9;
+      if (want * per_buf + reserve <= 0.9 * have) nbuf = want;
+    }
+  }
   if (const char* e = std::getenv("HS_NBUF")) nbuf = std::max(1, std::atoi(e));
   nbuf = std::min(nbuf, nsweeps);
   std::vector<int> level, accl;
@@ -1888,7 +1903,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
     for (int l = 1; l <= nsweeps; ++l)
       for (int d = 0; d < dirs; ++d) route_h[(l - 1) * dirs + d] = route_trace(plan, dim, l, d / 2, (d & 1) ? 1 : -1);
     route.upload(route_h, eng.stream);
-    build_schedule();
+    build_schedule(r);
   }
   eng.ensure_solve(r, max_width, nbuf);
   if (!new_rounds && !new_r) return;
@@ -2678,7 +2693,8 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
   HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
   // per RHS column: the Krylov basis and work vectors, plus the DDM application's per-RHS
   // buffers (x / z / rhs per subdomain and x buffer, b / u / staging on the global grid)
-  const double ddm_col = (3.0 * 4 * static_cast<double>(H.eng.n_base.back()) + 6.0 * n) * sizeof(double2);
+  const int nbuf_max = std::max(4, std::min(rounds * H.ndir, HS_MAX_ACC_SWEEPS));  // x buffers (build_schedule)
+  const double ddm_col = (3.0 * nbuf_max * static_cast<double>(H.eng.n_base.back()) + 6.0 * n) * sizeof(double2);
   const double per_col = static_cast<double>(mk + 5) * n * sizeof(double2) + ddm_col;
   int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
   if (H.partitioned()) rmax = kMaxRhs;  // every rank must batch identically
