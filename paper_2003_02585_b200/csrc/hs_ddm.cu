@@ -1094,6 +1094,7 @@ struct DdmHandle {
   DBuf<unsigned> mpres, nzmask, tface;
   DBuf<int> route;
   DBuf<double2> bN, u, io;
+  DBuf<double2> uround;  // fused accumulate over several rounds: u after each round but the last
   DBuf<double> partial, norms, pnum, pden, rnum, rden;
   long long partial_stride = 0;  // elements between sweeps' partials (fused accumulate)
   std::vector<cudaEvent_t> ev;  // [0]=start, [1..nsweeps]=after sweep l's accumulate, then macro-step solve pairs
@@ -1925,6 +1926,7 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   pden.alloc(static_cast<size_t>(nb) * R);
   norms.alloc(static_cast<size_t>(nsweeps) * R);
   rnum.alloc(static_cast<size_t>(nrounds) * R);
+  uround.alloc(fuse_acc && nrounds > 1 ? static_cast<size_t>(nrounds - 1) * geom.gn * R : 0);
   rden.alloc(static_cast<size_t>(nrounds) * R);
   for (auto e : ev) cudaEventDestroy(e);
   ev.assign(1 + nsweeps + 2 * msteps.size(), nullptr);
@@ -2152,6 +2154,11 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
         }
         aa.x = eng.x.p;
         aa.u = u.p;
+        if (track && nrounds > 1) {
+          aa.uround = uround.p;
+          aa.rstride = geom.gn * R;
+          aa.rlen = ndir;
+        }
         aa.partial = partial.p + stripe_pbase(j) * R;
         aa.pstride = partial_stride;
         aa.row0 = rg.row0;
@@ -2171,6 +2178,14 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
         if (fuse_acc) {
           for (int l = 1; l <= nsweeps; ++l)
             launch_reduce_partials(partial.p + (l - 1) * partial_stride, nbt, R, norms.p + static_cast<size_t>(l - 1) * R, s);
+          if (track)  // residuals of the rounds before the last, on u as it stood after each of them
+            for (int q = 0; q + 1 < nrounds; ++q) {
+              double2* uq = uround.p + static_cast<size_t>(q) * geom.gn * R;
+              if (partitioned()) comm_allreduce(reinterpret_cast<double*>(uq), 2LL * geom.gn * R);
+              const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s);
+              launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(q) * R, s);
+              launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(q) * R, s);
+            }
           after_sweep(nsweeps, -1);
         } else {
           after_sweep(nsweeps, nbt);

@@ -864,6 +864,8 @@ __global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a
       }
       uv = cadd(uv, acc);
       nrm = acc.x * acc.x + acc.y * acc.y;
+      if (a.uround && (l + 1) % a.rlen == 0 && l + 1 < a.L)  // u after this round
+        a.uround[static_cast<long long>((l + 1) / a.rlen - 1) * a.rstride + node * R + r] = uv;
     }
     red[threadIdx.x] = nrm;
     __syncthreads();

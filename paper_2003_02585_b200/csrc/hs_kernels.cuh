@@ -121,6 +121,11 @@ struct AccumAllArgs {
   // region: rows [row0, row0 + cnt / w) of gx nodes, columns [x0, x0 + w) (a stripe: x0 = 0, w = gx)
   long long row0, cnt;
   int gx, x0, w;
+  // u after every completed round but the last (per-round residuals, src/sweeper.cpp:313-325):
+  // uround + (q - 1) * rstride after sweep q * rlen; null: none
+  double2* uround;
+  long long rstride;
+  int rlen;
 };
 int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s);
 // Deterministic final reduction of per-block partials: out[r] = sum_b partial[b][r].
