@@ -271,6 +271,10 @@ int hs_pipeline_cost(int dim, const int counts[3], int n_rhs, int n_iter, double
 int hs_pipeline_simulate(int dim, const int counts[3], int n_rhs, int n_iter, double t0, double* completion_times,
                          double* makespan, double* average_per_rhs);
 
+/* CSR of one subdomain's J-scaled PML operator as the solver assembled it (on the device unless
+ * HS_HOST_SETUP=1), in the reference's layout (include/helmsweep/operator.hpp:14-29; rows over
+ * the subdomain's local grid, axis 0 fastest). Pass NULL arrays to query n / nnz first. */
+int hs_ddm_sub_csr(const hs_ddm* s, int sub, int64_t* row_ptr, int64_t* col, double* val, int64_t* n, int64_t* nnz);
 /* Device memory of a solver: bytes of resident solve factors (packed 8x8-block layout), bytes of
  * the solve state for the current batch width, and the RHS the device solves per batch (wider
  * requests run as consecutive batches). */

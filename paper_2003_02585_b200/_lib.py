@@ -137,6 +137,7 @@ SIGNATURES = {
     "hs_ddm_create_nccl": (ctypes.c_int, [ctypes.POINTER(Problem), ctypes.c_int, ctypes.c_int, ctypes.c_int, c_int_p,
                                           ctypes.POINTER(ctypes.c_ubyte), ctypes.POINTER(ctypes.c_void_p), c_int_p,
                                           c_i64_p]),
+    "hs_ddm_sub_csr": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i64_p, c_i64_p, c_dbl_p, c_i64_p, c_i64_p]),
     "hs_ddm_memory": (ctypes.c_int, [ctypes.c_void_p, c_i64_p, c_i64_p, c_int_p]),
     "hs_ddm_partition_info": (ctypes.c_int, [ctypes.c_void_p, c_int_p, c_int_p, c_int_p, c_i64_p, c_i64_p]),
 }

@@ -349,6 +349,21 @@ class DdmSolver:
             _raise(rc)
         return y
 
+    def sub_csr(self, sub):
+        """(row_ptr, col, val) of subdomain `sub`'s operator as assembled by the solver (hs_ddm_sub_csr)."""
+        n, nnz = ctypes.c_int64(), ctypes.c_int64()
+        rc = L.lib().hs_ddm_sub_csr(self._h, int(sub), None, None, None, ctypes.byref(n), ctypes.byref(nnz))
+        if rc:
+            _raise(rc)
+        rp = np.zeros(n.value + 1, dtype=np.int64)
+        col = np.zeros(nnz.value, dtype=np.int64)
+        val = np.zeros(nnz.value, dtype=np.complex128)
+        rc = L.lib().hs_ddm_sub_csr(self._h, int(sub), rp.ctypes.data_as(L.c_i64_p), col.ctypes.data_as(L.c_i64_p),
+                                    _dptr(val), None, None)
+        if rc:
+            _raise(rc)
+        return rp, col, val
+
     def memory(self):
         """Resident factor bytes, solve-state bytes and the device batch width (hs_ddm_memory)."""
         fb, sb, mb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()

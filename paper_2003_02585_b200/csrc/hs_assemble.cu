@@ -170,7 +170,139 @@ __global__ void assemble_kernel(AsmArgs a) {
   atomicMax(S.maxabs, __double_as_longlong(mx));  // non-negative doubles order as their bit patterns
 }
 
+__device__ __forceinline__ int weight2_dev(const PlanGeom& g, int axis, int cell, int index) {
+  const int lo = cell * g.w[axis], hi = (cell + 1) * g.w[axis];
+  const int lo_ext = cell == 0 ? lo - g.pad : lo;
+  const int hi_ext = cell == g.counts[axis] - 1 ? hi + g.pad : hi;
+  if (index < lo_ext || index > hi_ext) return 0;
+  if (index == lo && cell > 0) return 1;
+  if (index == hi && cell < g.counts[axis] - 1) return 1;
+  return 2;
+}
+
+struct PlanDirs {
+  int d[8][3];
+};
+
+template <int E>
+__global__ void acc_plan_kernel(PlanGeom g, int ndirs, PlanDirs dirs, int2* acc_ent) {
+  const long long node = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (node >= g.gn) return;
+  int p[3] = {0, 0, 0}, cand[3][2], nc[3] = {1, 1, 1};
+  {
+    long long t = node;
+    for (int a = 0; a < g.dim; ++a) {
+      p[a] = g.glo[a] + static_cast<int>(t % g.gsize[a]);
+      t /= g.gsize[a];
+      int c = p[a] >= 0 ? p[a] / g.w[a] : 0;
+      c = min(c, g.counts[a] - 1);
+      nc[a] = 0;
+      if (c > 0 && p[a] == c * g.w[a]) cand[a][nc[a]++] = c - 1;  // shared face: the lower cell first
+      cand[a][nc[a]++] = c;
+    }
+  }
+  int2 ent[E];
+  int sub[E][3];
+  int n = 0;
+  // every combination of per-axis cells, in ascending flattened id (axis 0 fastest)
+  const int n2 = g.dim > 2 ? nc[2] : 1;
+  for (int i2 = 0; i2 < n2; ++i2)
+    for (int i1 = 0; i1 < nc[1]; ++i1)
+      for (int i0 = 0; i0 < nc[0]; ++i0) {
+        const int s3[3] = {cand[0][i0], cand[1][i1], g.dim > 2 ? cand[2][i2] : 0};
+        int num = 1;
+        for (int a = 0; a < g.dim; ++a) num *= weight2_dev(g, a, s3[a], p[a]);
+        if (num == 0) continue;
+        const int id = s3[0] + g.counts[0] * (s3[1] + g.counts[1] * s3[2]);
+        const DevClass& C = g.cls[g.sub_cls[id]];
+        long long loc = 0, ls = 1;
+        for (int a = 0; a < g.dim; ++a) {
+          loc += static_cast<long long>(p[a] - (s3[a] * g.w[a] - g.pad)) * ls;
+          ls *= C.size[a];
+        }
+        ent[n] = make_int2(static_cast<int>(g.n_base[id] + C.elim_of_local[loc]), (id << 4) | num);
+        for (int a = 0; a < 3; ++a) sub[n][a] = s3[a];
+        ++n;
+      }
+  for (int di = 0; di < ndirs; ++di) {
+    long long key[E];
+    int2 e2[E];
+    for (int i = 0; i < n; ++i) {
+      int st = 1;
+      for (int a = 0; a < g.dim; ++a) st += dirs.d[di][a] == 1 ? sub[i][a] : g.counts[a] - 1 - sub[i][a];
+      key[i] = (static_cast<long long>(st) << 32) | (ent[i].y >> 4);
+      e2[i] = ent[i];
+    }
+    for (int i = 1; i < n; ++i)
+      for (int j = i; j > 0 && key[j] < key[j - 1]; --j) {
+        const long long tk = key[j];
+        key[j] = key[j - 1];
+        key[j - 1] = tk;
+        const int2 te = e2[j];
+        e2[j] = e2[j - 1];
+        e2[j - 1] = te;
+      }
+    int2* dst = acc_ent + (static_cast<long long>(di) * g.gn + node) * E;
+    for (int i = 0; i < E; ++i) dst[i] = i < n ? e2[i] : make_int2(-1, 0);
+  }
+}
+
+__global__ void split_plan_kernel(PlanGeom g, int* split_gp, unsigned char* split_w) {
+  const int id = blockIdx.y;
+  const DevClass& C = g.cls[g.sub_cls[id]];
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= C.n) return;
+  int s3[3];
+  {
+    int t = id;
+    for (int a = 0; a < 3; ++a) {
+      s3[a] = t % g.counts[a];
+      t /= g.counts[a];
+    }
+  }
+  long long loc = C.local_of_elim[e];
+  bool shell = false;
+  int num = 1;
+  long long gl = 0, gs = 1;
+  for (int a = 0; a < g.dim; ++a) {
+    const int li = static_cast<int>(loc % C.size[a]);
+    loc /= C.size[a];
+    const int pa = s3[a] * g.w[a] - g.pad + li;
+    shell |= li == 0 || li == C.size[a] - 1;
+    num *= weight2_dev(g, a, s3[a], pa);
+    gl += static_cast<long long>(pa - g.glo[a]) * gs;
+    gs *= g.gsize[a];
+  }
+  const long long o = g.n_base[id] + e;
+  const bool on = num != 0 && !shell;
+  split_gp[o] = on ? static_cast<int>(gl) : 0;
+  split_w[o] = on ? static_cast<unsigned char>(num) : 0;
+}
+
 }  // namespace
+
+void launch_acc_plan(const PlanGeom& g, int ndirs, const int (*dvec)[3], int2* acc_ent, cudaStream_t s) {
+  PlanDirs d{};
+  for (int i = 0; i < ndirs && i < 8; ++i)
+    for (int a = 0; a < 3; ++a) d.d[i][a] = dvec[i][a];
+  const int threads = 128;
+  const unsigned blocks = static_cast<unsigned>((g.gn + threads - 1) / threads);
+  if (g.dim == 3)
+    acc_plan_kernel<8><<<blocks, threads, 0, s>>>(g, ndirs, d, acc_ent);
+  else
+    acc_plan_kernel<4><<<blocks, threads, 0, s>>>(g, ndirs, d, acc_ent);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  HS_CUDA(cudaGetLastError());
+}
+
+void launch_split_plan(const PlanGeom& g, int nsub, long long max_n, int* split_gp, unsigned char* split_w,
+                       cudaStream_t s) {
+  const int threads = 128;
+  const dim3 grid(static_cast<unsigned>((max_n + threads - 1) / threads), static_cast<unsigned>(nsub));
+  split_plan_kernel<<<grid, threads, 0, s>>>(g, split_gp, split_w);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  HS_CUDA(cudaGetLastError());
+}
 
 void launch_assemble(const AsmArgs& a, long long max_rows, cudaStream_t s) {
   if (a.nsub <= 0 || max_rows <= 0) return;

@@ -22,6 +22,7 @@
 
 #include "helmsweep_b200.h"
 #include "hs_kernels.cuh"
+#include "hs_assemble.cuh"
 #include "hs_nccl.hpp"
 #include "hs_partition.hpp"
 #include "hs_symbolic.hpp"
@@ -100,6 +101,7 @@ struct ClassDev {
   std::vector<int> ext_pos;       // elimination positions of every trace-extraction line
   DBuf<int> ext_u0[kMaxDirs], ext_um1[kMaxDirs], inj_p0[kMaxDirs], inj_pm[kMaxDirs];
   DBuf<unsigned char> on_line;
+  DBuf<std::int64_t> csr_rp, csr_col;  // CSR structure on the device (device subdomain assembly)
   std::vector<int> level_start_down;
   DevClass dev{};
 };
@@ -306,30 +308,46 @@ struct Engine {
   std::vector<char> owned;
   bool owns(int s) const { return owned.empty() || owned[s]; }
 
-  void factorize(const std::vector<const CVector*>& values) {
+  // Factor / vector / CSR-value layout of every subdomain (values in the class's CSR structure).
+  std::vector<long long> val_base;
+  void layout() {
     const int nsub = static_cast<int>(sub_cls.size());
     fac_base.assign(nsub + 1, 0);
     n_base.assign(nsub + 1, 0);
-    std::vector<long long> val_base(nsub + 1, 0);
+    val_base.assign(nsub + 1, 0);
     for (int s = 0; s < nsub; ++s) {
       const SymbolicClass& c = *classes[sub_cls[s]]->sym;
       fac_base[s + 1] = fac_base[s] + (owns(s) ? c.fac_total : 0);
       n_base[s + 1] = n_base[s] + c.n;
-      val_base[s + 1] = val_base[s] + (owns(s) ? static_cast<long long>(values[s]->size()) : 0);
+      val_base[s + 1] = val_base[s] + (owns(s) ? static_cast<long long>(c.csr_col.size()) : 0);
     }
     factor.alloc(std::max<long long>(fac_base[nsub], 1));
     dinv.alloc(std::max<long long>(n_base[nsub], 1));
     val.alloc(std::max<long long>(val_base[nsub], 1));
     tol.assign(nsub, 0.0);
+  }
+  // Host CSR values (standalone factorization, host setup): uploaded, pivot tolerances on the host.
+  void factorize(const std::vector<const CVector*>& values) {
+    layout();
+    const int nsub = static_cast<int>(sub_cls.size());
     parallel_for(nsub, [&](long long s) {
+      if (!owns(static_cast<int>(s))) return;
       double scale = 0.0;
       for (const Complex& z : *values[s]) scale = std::max(scale, std::abs(z));
       tol[s] = 1e-14 * scale;  // src/direct.cpp:191-193
     });
     for (int s = 0; s < nsub; ++s)
-      if (owns(s))
+      if (owns(s)) {
+        if (static_cast<long long>(values[s]->size()) != val_base[s + 1] - val_base[s])
+          throw Error(kInternal, "factorize: CSR values do not match the class structure");
         HS_CUDA(cudaMemcpyAsync(val.p + val_base[s], values[s]->data(), values[s]->size() * sizeof(Complex),
-                              cudaMemcpyHostToDevice, stream));
+                                cudaMemcpyHostToDevice, stream));
+      }
+    factorize_numeric();
+  }
+  // CSR values already on the device (val, device assembly) with the pivot tolerances in tol.
+  void factorize_numeric() {
+    const int nsub = static_cast<int>(sub_cls.size());
     h_subs.resize(nsub);
     for (int s = 0; s < nsub; ++s) {
       DevSub& d = h_subs[s];
@@ -1022,7 +1040,6 @@ struct DdmHandle {
   Weights wts;
   LocalGrid ggrid;
   PmlCoefficients gcoeffs;
-  std::vector<double> gkappa;
   std::vector<SubHost> subs;
   std::vector<hs_factor_stats> sub_stats;
   double factor_seconds = 0.0;
@@ -1150,6 +1167,13 @@ struct DdmHandle {
   }
 
   void build(const hs_problem& P, int device, int rank_ = 0, int world_ = 1, const int* owner_ = nullptr);
+  // device subdomain setup: extended wavenumber + CSR values of every owned subdomain into eng.val,
+  // pivot tolerances into eng.tol (hs_assemble.cu)
+  DBuf<float> vel_dev;
+  DBuf<double2> alpha_dev;
+  DBuf<AsmSub> asm_subs;
+  AsmMedium asm_medium();
+  void assemble_device(const std::vector<PmlCoefficients>& coeffs);
   void ensure_state(int r, int nrounds);
   void build_schedule(int r);
   void build_items();
@@ -1288,7 +1312,6 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
     ggrid.range.hi[a] = intervals[a] + pml.width;
   }
   gcoeffs = build_coefficients(pml, interior, ggrid);
-  gkappa = extend_to_subdomain(medium, interior, ggrid);
 
   phase("global grid + coefficients");
   eng.init(device, dim);
@@ -1312,17 +1335,21 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
       st.range.hi[a] += pml.width;
     }
   }
-  parallel_for(nsub, [&](long long id) {  // PML coefficients, extended kappa, CSR (src/sweeper.cpp:89-124)
-    const SubHost& st = subs[id];
+  // Subdomain setup (src/sweeper.cpp:89-124). The 1-D PML tables are built on the host (O(n) per
+  // axis); the extended wavenumber and the CSR values of every subdomain are computed on the device
+  // (hs_assemble.cu, bit for bit with the host restatement). Only one representative per symbolic
+  // class is assembled on the host, for the CSR structure the symbolic analysis needs.
+  // HS_HOST_SETUP=1 assembles every subdomain on the host instead (A/B, tests).
+  const bool host_setup = std::getenv("HS_HOST_SETUP") != nullptr;
+  auto local_grid = [&](const SubHost& st) {
     LocalGrid g;
     g.dim = dim;
     g.range = st.range;
     g.h = ggrid.h;
     g.origin = ggrid.origin;
-    coeffs[id] = build_coefficients(pml, st.cell, g);
-    const std::vector<double> kap = extend_to_subdomain(medium, st.cell, g);
-    ops[id] = assemble(g, coeffs[id], kap);
-  });
+    return g;
+  };
+  parallel_for(nsub, [&](long long id) { coeffs[id] = build_coefficients(pml, subs[id].cell, local_grid(subs[id])); });
   // symbolic classes: key = extents and the lower index (or its parity when non-negative: C++
   // truncating mid = (lo+hi)/2 only depends on it through that); one symbolic build per class
   std::vector<int> first_of_class;
@@ -1342,6 +1369,13 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
       st.cls = it->second;
     }
   }
+  std::vector<char> assemble_host(nsub, host_setup ? 1 : 0);
+  for (int id : first_of_class) assemble_host[id] = 1;
+  parallel_for(nsub, [&](long long id) {
+    if (!assemble_host[id]) return;
+    const LocalGrid g = local_grid(subs[id]);
+    ops[id] = assemble(g, coeffs[id], extend_to_subdomain(medium, subs[id].cell, g));
+  });
   std::vector<std::unique_ptr<SymbolicClass>> syms(first_of_class.size());
   parallel_for(static_cast<long long>(syms.size()), [&](long long c) {
     const int id = first_of_class[c];
@@ -1350,10 +1384,10 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
   for (auto& sc : syms) eng.add_class(std::move(sc));
   for (int id = 0; id < nsub; ++id) {
     const SubHost& st = subs[id];
-    if (eng.classes[st.cls]->sym->csr_col.size() != ops[id].col.size())
+    if (assemble_host[id] && eng.classes[st.cls]->sym->csr_col.size() != ops[id].col.size())
       throw Error(kInternal, "symbolic class CSR mismatch");
     eng.sub_cls.push_back(st.cls);
-    vals[id] = std::move(ops[id].val);
+    if (host_setup) vals[id] = std::move(ops[id].val);
   }
   phase("assembly + symbolic");
   eng.upload_classes(pml.width);
@@ -1398,11 +1432,18 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
     eng.owned.assign(nsub, 0);
     for (int id = 0; id < nsub; ++id) eng.owned[id] = owner[id] == rank;
   }
-  std::vector<const CVector*> vp(nsub);
-  for (int id = 0; id < nsub; ++id) vp[id] = &vals[id];
   // factorize (the DevSub array is re-uploaded with the coefficient pointers below)
   phase("couplings");
-  eng.factorize(vp);
+  if (host_setup) {
+    std::vector<const CVector*> vp(nsub);
+    for (int id = 0; id < nsub; ++id) vp[id] = &vals[id];
+    eng.factorize(vp);
+  } else {
+    eng.layout();
+    assemble_device(coeffs);  // eng.val and the pivot tolerances
+    phase("assembly (device)");
+    eng.factorize_numeric();
+  }
   phase("factorize (device)");
   for (int id = 0; id < nsub; ++id) {
     DevSub& d = eng.h_subs[id];
@@ -1414,7 +1455,51 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
       d.coef[q] = q < dirs ? reinterpret_cast<const double2*>(d_coef.p) + (static_cast<size_t>(id) * dirs + q) * line_max
                            : nullptr;
   }
-  {  // split-source plan (src/sweeper.cpp:189-202): per elimination position, the global node and
+  // geometry for the sweep kernels
+  geom.dim = dim;
+  geom.pad = pml.width;
+  geom.nsub = nsub;
+  geom.gn = ggrid.range.count();
+  for (int a = 0; a < 3; ++a) {
+    geom.glo[a] = a < dim ? ggrid.range.lo[a] : 0;
+    geom.gsize[a] = a < dim ? ggrid.range.size(a) : 1;
+    geom.counts[a] = part.counts[a];
+    geom.cut_w[a] = a < dim ? intervals[a] / part.counts[a] : 1;
+  }
+  // The setup plans (split source, accumulate) are built by device kernels (hs_assemble.cu) from
+  // the partition geometry; a partitioned solver (home nodes, ghost lists) or HS_HOST_SETUP=1 builds
+  // them on the host.
+  const bool host_plans = host_setup || partitioned();
+  PlanGeom pg{};
+  DBuf<int> d_subcls;
+  DBuf<long long> d_nbase;
+  if (!host_plans) {
+    pg.dim = dim;
+    pg.gn = geom.gn;
+    pg.pad = pml.width;
+    for (int a = 0; a < 3; ++a) {
+      pg.glo[a] = geom.glo[a];
+      pg.gsize[a] = geom.gsize[a];
+      pg.counts[a] = geom.counts[a];
+      pg.w[a] = geom.cut_w[a];
+    }
+    d_subcls.upload(eng.sub_cls, eng.stream);
+    d_nbase.upload(eng.n_base, eng.stream);
+    pg.cls = eng.d_cls.p;
+    pg.sub_cls = d_subcls.p;
+    pg.n_base = d_nbase.p;
+  }
+  if (!host_plans) {  // split-source plan on the device
+    split_gp.alloc(std::max<long long>(eng.n_base[nsub], 1));
+    split_w.alloc(std::max<long long>(eng.n_base[nsub], 1));
+    long long max_n = 1;
+    for (auto& cdp : eng.classes) max_n = std::max<long long>(max_n, cdp->sym->n);
+    launch_split_plan(pg, nsub, max_n, split_gp.p, split_w.p, eng.stream);
+    for (int id = 0; id < nsub; ++id) {
+      eng.h_subs[id].split_gp = split_gp.p + eng.n_base[id];
+      eng.h_subs[id].split_w = split_w.p + eng.n_base[id];
+    }
+  } else {  // split-source plan (src/sweeper.cpp:189-202): per elimination position, the global node and
      // the weight numerator of w(sub, p) * b[p] (0 on the local shell or outside the support)
     const long long ntot = eng.n_base[nsub];
     std::vector<int> gp(std::max<long long>(ntot, 1), 0);
@@ -1450,24 +1535,67 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
     const SymbolicClass& c = *eng.classes[subs[id].cls]->sym;
     hs_factor_stats& s = sub_stats[id];
     s.n = c.n;
-    s.matrix_nnz = static_cast<int64_t>(vals[id].size());
+    s.matrix_nnz = static_cast<int64_t>(c.csr_col.size());
     s.factor_nnz = c.factor_nnz;
     s.peak_bytes = c.peak_bytes;
     s.factor_seconds = eng.factor_gpu_seconds;
   }
-  // geometry for the sweep kernels
-  geom.dim = dim;
-  geom.pad = pml.width;
-  geom.nsub = nsub;
-  geom.gn = ggrid.range.count();
-  for (int a = 0; a < 3; ++a) {
-    geom.glo[a] = a < dim ? ggrid.range.lo[a] : 0;
-    geom.gsize[a] = a < dim ? ggrid.range.size(a) : 1;
-    geom.counts[a] = part.counts[a];
-    geom.cut_w[a] = a < dim ? intervals[a] / part.counts[a] : 1;
-  }
   phase("stats + split plan");
-  {  // accumulate plan (src/transfer.cpp:91-102): per global node, every subdomain whose support
+  if (!host_plans) {
+    // accumulate plan on the device, one plan per sweep direction (entries in the reference's order)
+    const int E = 1 << dim, ndirs = 1 << dim;
+    if (nsub >= (1 << 27)) config_error("partition: too many subdomains");
+    const std::vector<Vec3i> dplan = sweep_plan(dim, 1);
+    int dv[8][3] = {};
+    for (int di = 0; di < ndirs; ++di)
+      for (int a = 0; a < 3; ++a) dv[di][a] = dplan[di][a];
+    acc_ent.alloc(static_cast<size_t>(geom.gn) * E * ndirs);
+    launch_acc_plan(pg, ndirs, dv, acc_ent.p, eng.stream);
+    // fronts whose x is read back (support positions, all of nonzero weight, and the trace
+    // extraction lines), per subdomain; the set depends only on the class and the support box
+    // within the local grid, so it is computed once per such pair
+    int nfm = 1;
+    for (auto& cdp : eng.classes) nfm = std::max(nfm, static_cast<int>(cdp->sym->fronts.size()));
+    need_words = (nfm + 31) / 32;
+    need_h.assign(static_cast<size_t>(nsub) * need_words, 0u);
+    std::map<std::vector<int>, int> memo;
+    for (int id = 0; id < nsub; ++id) {
+      const GridRange sup = wts.support(subs[id].sub);
+      std::vector<int> key{subs[id].cls};
+      for (int a = 0; a < dim; ++a) {
+        key.push_back(sup.lo[a] - subs[id].range.lo[a]);
+        key.push_back(sup.hi[a] - subs[id].range.lo[a]);
+      }
+      unsigned* w = need_h.data() + static_cast<size_t>(id) * need_words;
+      auto it = memo.find(key);
+      if (it != memo.end()) {
+        std::copy(need_h.begin() + static_cast<size_t>(it->second) * need_words,
+                  need_h.begin() + static_cast<size_t>(it->second + 1) * need_words, w);
+        continue;
+      }
+      memo[key] = id;
+      const ClassDev& cd = *eng.classes[subs[id].cls];
+      const SymbolicClass& c = *cd.sym;
+      auto mark = [&](int e) {
+        for (int f = cd.front_of_pos.empty() ? -1 : cd.front_of_pos[e]; f >= 0 && !(w[f >> 5] >> (f & 31) & 1u);
+             f = c.fronts[f].parent)
+          w[f >> 5] |= 1u << (f & 31);
+      };
+      Vec3i p{0, 0, 0};
+      for (p[2] = sup.lo[2]; p[2] <= (dim > 2 ? sup.hi[2] : sup.lo[2]); ++p[2])
+        for (p[1] = sup.lo[1]; p[1] <= sup.hi[1]; ++p[1])
+          for (p[0] = sup.lo[0]; p[0] <= sup.hi[0]; ++p[0]) {
+            long long loc = 0, ls = 1;
+            for (int a = 0; a < dim; ++a) {
+              loc += static_cast<long long>(p[a] - subs[id].range.lo[a]) * ls;
+              ls *= c.size[a];
+            }
+            mark(c.elim_of_local[loc]);
+          }
+      for (int e : cd.ext_pos) mark(e);
+    }
+    need.upload(need_h, eng.stream);
+  } else {  // accumulate plan (src/transfer.cpp:91-102): per global node, every subdomain whose support
      // holds it, as (x position n_base[sub] + elim, sub << 4 | weight numerator)
     const long long gn = geom.gn;
     std::vector<int> off(gn, 0);
@@ -1606,6 +1734,108 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
   d_groups.upload(gflat, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
   phase("step groups");
+}
+
+AsmMedium DdmHandle::asm_medium() {
+  AsmMedium m{};
+  m.kind = static_cast<int>(medium.kind);
+  m.kappa = medium.kappa;
+  m.kd = medium.kappa_down;
+  m.ku = medium.kappa_up;
+  m.eta = medium.eta;
+  m.eps = medium.eps;
+  m.omega = medium.omega;
+  m.axis = medium.axis;
+  if (medium.kind == Medium::Gridded) {
+    const VelocityGrid& g = medium.velocity;
+    m.vdim = g.dim;
+    for (int a = 0; a < 3; ++a) {
+      m.vn[a] = g.n[a];
+      m.vorg[a] = g.origin[a];
+      m.vsp[a] = g.spacing[a];
+    }
+    if (vel_dev.n != g.c.size()) {
+      vel_dev.alloc(g.c.size());
+      HS_CUDA(cudaMemcpyAsync(vel_dev.p, g.c.data(), g.c.size() * sizeof(float), cudaMemcpyHostToDevice, eng.stream));
+    }
+    m.vc = vel_dev.p;
+  }
+  return m;
+}
+
+void DdmHandle::assemble_device(const std::vector<PmlCoefficients>& coeffs) {
+  const int nsub = geom.nsub > 0 ? geom.nsub : static_cast<int>(subs.size());
+  // class CSR structures
+  long long max_rows = 0;
+  for (auto& cdp : eng.classes) {
+    ClassDev& cd = *cdp;
+    if (!cd.csr_rp.p) {
+      cd.csr_rp.upload(cd.sym->csr_row_ptr, eng.stream);
+      cd.csr_col.upload(cd.sym->csr_col, eng.stream);
+    }
+    max_rows = std::max<long long>(max_rows, cd.sym->n);
+  }
+  // 1-D PML tables of the owned subdomains, flattened
+  std::vector<Complex> tab;
+  std::vector<std::array<long long, 6>> off(nsub);
+  for (int id = 0; id < nsub; ++id) {
+    if (!eng.owns(id)) continue;
+    for (int a = 0; a < dim; ++a) {
+      off[id][2 * a] = static_cast<long long>(tab.size());
+      tab.insert(tab.end(), coeffs[id].node[a].begin(), coeffs[id].node[a].end());
+      off[id][2 * a + 1] = static_cast<long long>(tab.size());
+      tab.insert(tab.end(), coeffs[id].half[a].begin(), coeffs[id].half[a].end());
+    }
+  }
+  alpha_dev.alloc(std::max<size_t>(tab.size(), 1));
+  HS_CUDA(cudaMemcpyAsync(alpha_dev.p, tab.data(), tab.size() * sizeof(Complex), cudaMemcpyHostToDevice, eng.stream));
+  DBuf<unsigned long long> dmax;
+  dmax.alloc(nsub + 1);  // [nsub]: the bad-sample flag
+  dmax.zero(eng.stream);
+  std::vector<AsmSub> hs;
+  std::vector<int> ids;
+  for (int id = 0; id < nsub; ++id) {
+    if (!eng.owns(id)) continue;
+    const SubHost& st = subs[id];
+    const ClassDev& cd = *eng.classes[st.cls];
+    AsmSub a{};
+    for (int ax = 0; ax < 3; ++ax) {
+      a.lo[ax] = ax < dim ? st.range.lo[ax] : 0;
+      a.size[ax] = ax < dim ? st.range.size(ax) : 1;
+      a.cell_lo[ax] = st.cell.lo[ax];
+      a.cell_hi[ax] = st.cell.hi[ax];
+      a.anode[ax] = ax < dim ? alpha_dev.p + off[id][2 * ax] : nullptr;
+      a.ahalf[ax] = ax < dim ? alpha_dev.p + off[id][2 * ax + 1] : nullptr;
+    }
+    a.row_ptr = cd.csr_rp.p;
+    a.col = cd.csr_col.p;
+    a.val = eng.val.p + eng.val_base[id];
+    a.maxabs = dmax.p + id;
+    hs.push_back(a);
+    ids.push_back(id);
+  }
+  if (hs.empty()) return;
+  asm_subs.upload(hs, eng.stream);
+  AsmArgs args{};
+  args.dim = dim;
+  for (int ax = 0; ax < 3; ++ax) {
+    args.h[ax] = ggrid.h[ax];
+    args.origin[ax] = ggrid.origin[ax];
+  }
+  args.med = asm_medium();
+  args.subs = asm_subs.p;
+  args.nsub = static_cast<int>(hs.size());
+  args.bad = reinterpret_cast<unsigned*>(dmax.p + nsub);
+  launch_assemble(args, max_rows, eng.stream);
+  std::vector<unsigned long long> mx(nsub + 1);
+  HS_CUDA(cudaMemcpyAsync(mx.data(), dmax.p, mx.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, eng.stream));
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  if (mx[nsub]) data_error("eval_kappa: non-positive velocity sample");
+  for (int id : ids) {
+    double scale = 0.0;
+    std::memcpy(&scale, &mx[id], sizeof(double));
+    eng.tol[id] = 1e-14 * scale;  // src/direct.cpp:191-193
+  }
 }
 
 // Macro-step schedule of one application: task (l, id) runs one macro-step after the latest of
@@ -1936,16 +2166,91 @@ void DdmHandle::ensure_state(int r, int nrounds) {
   for (auto& e : ev_out) HS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
+// The global J-scaled operator (DdmSolver::global_op, src/sweeper.cpp:159-162) on the device: its
+// CSR structure is integer work on the host (the class-independent stencil pattern), its values
+// come from the device assembly (hs_assemble.cu) with the interior box as the extension cell.
 void DdmHandle::ensure_gop() {
   if (gop_ready) return;
-  Csr op = assemble(ggrid, gcoeffs, gkappa);
-  g_nnz = static_cast<long long>(op.col.size());
-  std::vector<int> col32(op.col.begin(), op.col.end());
-  g_rp.upload(op.row_ptr, eng.stream);
+  if (std::getenv("HS_HOST_SETUP")) {
+    Csr op = assemble(ggrid, gcoeffs, extend_to_subdomain(medium, interior, ggrid));
+    g_nnz = static_cast<long long>(op.col.size());
+    std::vector<int> col32(op.col.begin(), op.col.end());
+    g_rp.upload(op.row_ptr, eng.stream);
+    g_col.upload(col32, eng.stream);
+    g_val.alloc(op.val.size());
+    HS_CUDA(cudaMemcpyAsync(g_val.p, op.val.data(), op.val.size() * sizeof(Complex), cudaMemcpyHostToDevice,
+                            eng.stream));
+    HS_CUDA(cudaStreamSynchronize(eng.stream));
+    gop_ready = true;
+    return;
+  }
+  const GridRange& rg = ggrid.range;
+  const std::int64_t n = rg.count();
+  std::vector<std::int64_t> rp(n + 1, 0);
+  std::vector<int> col32;
+  col32.reserve(static_cast<size_t>(n) * (2 * dim + 1));
+  long long stride[3] = {1, 1, 1};
+  for (int a = 1; a < dim; ++a) stride[a] = stride[a - 1] * rg.size(a - 1);
+  for (std::int64_t r = 0; r < n; ++r) {  // src/operator.cpp:41-86: sorted columns, shell rows identity
+    const Vec3i p = rg.unlinear(r);
+    if (ggrid.on_shell(p)) {
+      col32.push_back(static_cast<int>(r));
+    } else {
+      for (int a = dim - 1; a >= 0; --a)  // lower neighbours, farthest first
+        if (!(p[a] - 1 == rg.lo[a])) col32.push_back(static_cast<int>(r - stride[a]));
+        else (void)0;
+      col32.push_back(static_cast<int>(r));
+      for (int a = 0; a < dim; ++a)
+        if (!(p[a] + 1 == rg.hi[a])) col32.push_back(static_cast<int>(r + stride[a]));
+    }
+    rp[r + 1] = static_cast<std::int64_t>(col32.size());
+  }
+  g_nnz = static_cast<long long>(col32.size());
+  g_rp.upload(rp, eng.stream);
   g_col.upload(col32, eng.stream);
-  g_val.alloc(op.val.size());
-  HS_CUDA(cudaMemcpyAsync(g_val.p, op.val.data(), op.val.size() * sizeof(Complex), cudaMemcpyHostToDevice,
-                          eng.stream));
+  g_val.alloc(col32.size());
+  DBuf<std::int64_t> col64;
+  col64.upload(std::vector<std::int64_t>(col32.begin(), col32.end()), eng.stream);
+  std::vector<Complex> tab;
+  std::array<long long, 6> off{};
+  for (int a = 0; a < dim; ++a) {
+    off[2 * a] = static_cast<long long>(tab.size());
+    tab.insert(tab.end(), gcoeffs.node[a].begin(), gcoeffs.node[a].end());
+    off[2 * a + 1] = static_cast<long long>(tab.size());
+    tab.insert(tab.end(), gcoeffs.half[a].begin(), gcoeffs.half[a].end());
+  }
+  DBuf<double2> gtab;
+  gtab.alloc(tab.size());
+  HS_CUDA(cudaMemcpyAsync(gtab.p, tab.data(), tab.size() * sizeof(Complex), cudaMemcpyHostToDevice, eng.stream));
+  DBuf<unsigned long long> flags;
+  flags.alloc(2);
+  flags.zero(eng.stream);
+  AsmSub g{};
+  for (int a = 0; a < 3; ++a) {
+    g.lo[a] = a < dim ? rg.lo[a] : 0;
+    g.size[a] = a < dim ? rg.size(a) : 1;
+    g.cell_lo[a] = interior.lo[a];
+    g.cell_hi[a] = interior.hi[a];
+    g.anode[a] = a < dim ? gtab.p + off[2 * a] : nullptr;
+    g.ahalf[a] = a < dim ? gtab.p + off[2 * a + 1] : nullptr;
+  }
+  g.row_ptr = g_rp.p;
+  g.col = col64.p;
+  g.val = g_val.p;
+  g.maxabs = flags.p;
+  DBuf<AsmSub> dg;
+  dg.upload(std::vector<AsmSub>{g}, eng.stream);
+  AsmArgs args{};
+  args.dim = dim;
+  for (int a = 0; a < 3; ++a) {
+    args.h[a] = ggrid.h[a];
+    args.origin[a] = ggrid.origin[a];
+  }
+  args.med = asm_medium();
+  args.subs = dg.p;
+  args.nsub = 1;
+  args.bad = reinterpret_cast<unsigned*>(flags.p + 1);
+  launch_assemble(args, n, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
   gop_ready = true;
 }
@@ -2479,6 +2784,26 @@ extern "C" int hs_ddm_create_partitioned(const hs_problem* setup, int device, in
   return kOk;
 }
 
+extern "C" int hs_ddm_sub_csr(const hs_ddm* s, int sub, int64_t* row_ptr, int64_t* col, double* val, int64_t* n,
+                              int64_t* nnz) {
+  return guarded([&] {
+    if (!s) config_error("hs_ddm_sub_csr: null handle");
+    const DdmHandle& H = s->h;
+    if (sub < 0 || sub >= static_cast<int>(H.subs.size())) config_error("hs_ddm_sub_csr: subdomain out of range");
+    if (!H.eng.owns(sub)) config_error("hs_ddm_sub_csr: subdomain owned by another rank");
+    const SymbolicClass& c = *H.eng.classes[H.subs[sub].cls]->sym;
+    if (n) *n = c.n;
+    if (nnz) *nnz = static_cast<int64_t>(c.csr_col.size());
+    if (row_ptr) std::copy(c.csr_row_ptr.begin(), c.csr_row_ptr.end(), row_ptr);
+    if (col) std::copy(c.csr_col.begin(), c.csr_col.end(), col);
+    if (val) {
+      HS_CUDA(cudaSetDevice(H.eng.device));
+      HS_CUDA(cudaMemcpy(val, H.eng.val.p + H.eng.val_base[sub], c.csr_col.size() * sizeof(double2),
+                         cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
 extern "C" int hs_nccl_unique_id(unsigned char id[128]) {
   return guarded([&] {
     if (!id) config_error("hs_nccl_unique_id: null argument");
@@ -3004,7 +3329,7 @@ extern "C" int hs_ddm_global_solve(hs_ddm* s, int nrhs, const double* f, double*
       config_error("global_direct_solve: " + std::to_string(n) +
                    " nodes exceed the direct-solve memory guard; reduce the scale");
     if (!H.gfact) {
-      Csr op = assemble(H.ggrid, H.gcoeffs, H.gkappa);
+      Csr op = assemble(H.ggrid, H.gcoeffs, extend_to_subdomain(H.medium, H.interior, H.ggrid));
       H.gfact = make_factor(H.dim, H.ggrid.range, std::move(op.row_ptr), std::move(op.col), op.val, H.eng.device)
                     .release();
     }
