@@ -14,8 +14,9 @@ solve). ``value`` = RHS/s with b already resident in HBM, device-timed with CUDA
 ``e2e`` = the same through hs_ddm_solve with pinned host buffers (H2D of b and D2H of u inside
 the timed region). Multi-GPU (torchrun): one process per GPU, each rank sweeps its own RHS batch
 against its own resident factors (RHS are independent units; no data-path collective) -> weak
-scaling, time = max over ranks; ``--partition subdomain`` spreads one problem's subdomains over
-the ranks instead.
+scaling, time = max over ranks, with ``--partition rhs``; the default for N > 1 spreads one
+problem's subdomains over the ranks (BASELINE north_star) with the library's own
+NCCL transport (hs_ddm_create_nccl) -> strong scaling.
 
 ``--impl reference`` runs the reference's own CPU implementation (oracle/_ref, the unmodified
 reference compiled in place) on the host cores, one RHS per step.
@@ -424,8 +425,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS),
                     help="BASELINE configuration: c3 (configs[2], the headline) or c2 (configs[1])")
-    ap.add_argument("--partition", default="rhs", choices=["rhs", "subdomain"],
-                    help="multi-GPU layout: RHS sharding (weak scaling) or subdomain partitioning (strong)")
+    ap.add_argument("--partition", default="subdomain", choices=["rhs", "subdomain"],
+                    help="multi-GPU layout (N > 1): subdomain partitioning over the ranks with the library's "
+                         "native NCCL trace exchange (strong scaling, BASELINE north_star) or RHS sharding (weak)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

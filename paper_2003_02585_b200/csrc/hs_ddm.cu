@@ -485,6 +485,8 @@ struct Engine {
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
     if (const char* e = std::getenv("HS_CRIT_GW")) crit_gw = std::atoi(e) <= 8 ? 8 : 16;
+    int gw_bulk = 16;  // RHS per item of the unsplit fronts (HS_GW: 8 or 16)
+    if (const char* e = std::getenv("HS_GW")) gw_bulk = std::atoi(e) <= 8 ? 8 : 16;
     // target chunks per band: 16 in 2D (the C2 / C3 fronts never need more), 4 in 3D, whose big
     // top fronts have bands enough (C5 application 0.456 s uncapped -> 0.399 at 16 -> 0.388 at 4);
     // chunks are never wider than 16 blocks, which bounds the 3D top fronts' count from below
@@ -499,7 +501,7 @@ struct Engine {
       long long arr = 0, parts = 0;
       cd.fkc.assign(c.fronts.size(), 16);
       cd.fkr.assign(c.fronts.size(), 16);
-      cd.fgw.assign(c.fronts.size(), 16);
+      cd.fgw.assign(c.fronts.size(), gw_bulk);
       for (size_t f = 0; f < c.fronts.size(); ++f) {
         const int m = c.fronts[f].m, k = c.fronts[f].k;
         if (c.fronts[f].depth < split_depth) {  // critical path: split long bands over many warps

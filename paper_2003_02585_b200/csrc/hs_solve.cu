@@ -968,8 +968,11 @@ __device__ __forceinline__ Geo geo_km(int k, int m) {
   return g;
 }
 
+#ifndef HS_MINB_M3
+#define HS_MINB_M3 3  // CTAs per SM the 3M kernels are register-budgeted for (tuning experiments)
+#endif
 template <bool FWD, bool M3>
-__global__ void __launch_bounds__(kThreads, M3 ? 3 : 4) solve6_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* ring = smem_ring + warp * RingArea<FWD>::kWarp;

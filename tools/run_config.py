@@ -95,6 +95,46 @@ def c4(args, out):
                    converged=all(g.converged for g in G), max_true_residual=max(g.true_residual for g in G))
         print(json.dumps(out), flush=True)
         del s
+    if args.ref_full:
+        # SURVEY.md §8(d) C4 pin at full scale (32x32 subdomains of 209^2, 4096^2 + 40 PML): one DDM
+        # application's per-round residual and u, then 30 GMRES iterations (the reference's gmres is
+        # unrestarted, so its first 30 iterations are GMRES(30)'s first cycle) for one RHS, on the
+        # GPU and on the reference (oracle/_ref, all host cores)
+        from oracle import ref
+        n = 4096
+        path = "/tmp/c4_velocity_full.hsvg"
+        hs.write_velocity_grid(path, hs.VelocityGrid(2, [4097, 4097, 1], [0.0, 0.0, 0.0], [1 / 4096, 1 / 4096, 0.0],
+                                                     c.ravel()))
+        s = hs.DdmSolver(hs.ProblemSetup(2, [n, n], [32, 32], med, pml_width=pad))
+        b = s.scale_source(srcs(s, n, 1, 4000))
+        reps = []
+        U = s.ddm_solve(b, 1, reps, True)
+        G = s.gmres(b, tol, 30, 1, restart=30)
+        full = {"geometry": "full C4: 4096^2 + 40 PML, 32x32 subdomains of 209^2", "gpu_round_residual": reps[0].round_residuals,
+                "gpu_gmres_iterations": G[0].iterations, "gpu_history": G[0].history}
+        print(json.dumps(full), flush=True)
+        cores = os.cpu_count()
+        t = time.perf_counter()
+        r = ref.RefSolver({"dim": 2, "grid.n": [n, n], "partition": [32, 32], "pml.width": pad, "media.kind": "gridded",
+                           "media.velocity_file": path, "media.omega": 2 * math.pi * 160}, cores)
+        full["ref_factor_seconds"] = time.perf_counter() - t
+        br = r.scale_source(srcs(s, n, 1, 4000)[0])
+        full["rhs_bitwise_equal"] = bool(np.array_equal(b[0], br))
+        t = time.perf_counter()
+        u0, rep0 = r.ddm_solve(br, 1, True)
+        full.update(ref_application_seconds=time.perf_counter() - t, ref_round_residual=rep0["round_residuals"],
+                    ddm_rel_l2_vs_reference=rel(U[0], u0),
+                    counters_equal=[getattr(reps[0], k) for k in ("local_solves", "skipped_zero_solves", "traces_routed",
+                                                                    "traces_discarded")] ==
+                    [rep0[k] for k in ("local_solves", "skipped_zero_solves", "traces_routed", "traces_discarded")])
+        print(json.dumps(full), flush=True)
+        xr, gr = r.gmres(br, tol, 30, 1)
+        h_gpu, h_ref = np.array(G[0].history), np.array(gr["history"])
+        k = min(len(h_gpu), len(h_ref))
+        full.update(ref_gmres_iterations=gr["iterations"], ref_history=gr["history"], ref_gmres_seconds=gr["seconds"],
+                    history_max_rel_diff=float(np.max(np.abs(h_gpu[:k] - h_ref[:k]) / np.abs(h_ref[:k]))),
+                    gmres_x_rel_l2=rel(G[0].x, xr), ref_cores=cores)
+        out["full_parity"] = full
     if args.ref_small:
         from oracle import ref
         n = 1024
