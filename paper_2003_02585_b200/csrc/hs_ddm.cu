@@ -481,6 +481,20 @@ struct Engine {
     R = r;
     nbuf = nb;
     ngr = (R + 7) / 8;  // arrival / partial slots per (front, band): one per 8-RHS group
+    // Critical-path shaping by batch width. A 32-RHS batch (C3: 31-34 tasks per macro-step) is
+    // throughput-bound: fewer, wider split items win (C3 257 -> 220 ms per 64-RHS application with
+    // 16-RHS groups, chunks of 8 blocks, split above depth 5). Narrower batches keep the finer split
+    // of the latency-bound tree top (C2, 16 RHS: 12.2 ms with 8-RHS groups, chunks of 4, depth 7;
+    // 13.0-13.3 ms with the wide settings).
+    if (r >= 32) {
+      kc = kr = 8;
+      split_depth = 5;
+      crit_gw = 16;
+    } else {
+      kc = kr = 4;
+      split_depth = 7;
+      crit_gw = 8;
+    }
     if (const char* e = std::getenv("HS_KC")) kc = std::min(16, std::max(1, std::atoi(e)));
     if (const char* e = std::getenv("HS_KR")) kr = std::min(16, std::max(4, std::atoi(e) & ~3));
     if (const char* e = std::getenv("HS_SPLIT_DEPTH")) split_depth = std::atoi(e);
@@ -1177,6 +1191,8 @@ struct DdmHandle {
   AsmMedium asm_medium();
   void assemble_device(const std::vector<PmlCoefficients>& coeffs);
   void ensure_state(int r, int nrounds);
+  void ensure_state_body(int r, int nrounds);
+  int nbuf_cap = HS_MAX_ACC_SWEEPS;  // x buffers at most (4 after an allocation failure)
   void build_schedule(int r);
   void build_items();
   void ensure_gop();
@@ -1854,7 +1870,7 @@ void DdmHandle::build_schedule(int r) {
   // sweeps: 267 -> 249 ms per 64-RHS application), else 4
   nbuf = 4;
   {
-    const int want = std::min(nsweeps, HS_MAX_ACC_SWEEPS);
+    const int want = std::min(std::min(nsweeps, HS_MAX_ACC_SWEEPS), nbuf_cap);
     if (want > nbuf) {
       size_t free_b = 0, total_b = 0;
       HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -2122,7 +2138,26 @@ void DdmHandle::comm_allreduce(double* buf, long long count) {
   if (arfn(cuser, buf, count, eng.stream) != 0) throw Error(kCuda, "partitioned solve: allreduce callback failed");
 }
 
+// With one x buffer per sweep the solve state can exceed what the factors leave free (C5: 106 GB
+// of factors); an allocation failure then rebuilds the state with the 4-buffer schedule.
 void DdmHandle::ensure_state(int r, int nrounds) {
+  try {
+    ensure_state_body(r, nrounds);
+  } catch (const Error& e) {
+    if (e.code != kCuda || nbuf <= 4 || std::string(e.what()).find("out of memory") == std::string::npos) throw;
+    (void)cudaGetLastError();
+    nbuf_cap = 4;
+    eng.x.release();
+    eng.x1.release();
+    eng.rb.release();
+    eng.R = 0;  // force the solve buffers to be rebuilt
+    rounds = 0;
+    R = 0;
+    ensure_state_body(r, nrounds);
+  }
+}
+
+void DdmHandle::ensure_state_body(int r, int nrounds) {
   if (r < 1 || r > kMaxRhs) config_error("ddm_solve: batch size out of range");
   if (nrounds < 1) config_error("SweepPlan: rounds must be >= 1");
   const int ns = nrounds * ndir;
@@ -2975,7 +3010,7 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
     }
     for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
       const int R = std::min(kMaxRhs, nrhs - b0);
-      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 4);  // same size as the streamed path (two slots), first slot used;
+      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
       double2* din = H.io.p;
       double2* dout = H.io.p + static_cast<size_t>(n) * kMaxRhs;
       HS_CUDA(cudaMemcpyAsync(din, b + 2 * b0 * n, sizeof(double2) * n * R, cudaMemcpyHostToDevice, H.eng.stream));
