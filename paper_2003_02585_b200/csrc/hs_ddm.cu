@@ -134,6 +134,7 @@ struct Engine {
   std::vector<int> job_base;   // per subdomain: first (subdomain, front) job of x buffer 0
   int njobs = 0, nbuf = 1;     // jobs per x buffer; x buffers (sweeps in flight)
   long long xstride = 0;       // elements between x buffers
+  long long slot_stride = 0;   // elements between per-slot right-hand side / z buffers
   DBuf<SolveJob> jobs;
 
   ~Engine() {
@@ -556,16 +557,18 @@ struct Engine {
     const int nsub = static_cast<int>(sub_cls.size());
     xstride = static_cast<long long>(n_base[nsub]) * R;
     x.alloc(static_cast<size_t>(xstride) * nbuf);
-    x1.alloc(static_cast<size_t>(xstride) * nbuf);
-    rb.alloc(static_cast<size_t>(xstride) * nbuf);
+    // the right-hand side and z of a task live only within its macro-step: one buffer per slot
+    slot_stride = n_max * R;
+    x1.alloc(static_cast<size_t>(slot_stride) * nslots);
+    rb.alloc(static_cast<size_t>(slot_stride) * nslots);
     rb.zero(stream);  // right-hand sides are zero off their injection lines between uses
     vbuf.alloc(static_cast<size_t>(std::max<long long>(v_total_max, 1)) * R * nslots);
     part.alloc(static_cast<size_t>(std::max<long long>(part_total, 1)) * nslots * ngr * 1024);
     cnt.alloc(static_cast<size_t>(cnt_ints()));
     for (int s = 0; s < nsub; ++s) {
       h_subs[s].x = x.p + n_base[s] * R;
-      h_subs[s].x1 = x1.p + n_base[s] * R;
-      h_subs[s].rb = rb.p + n_base[s] * R;
+      h_subs[s].x1 = nullptr;
+      h_subs[s].rb = nullptr;
     }
     d_subs.upload(h_subs, stream);
     // per (subdomain, front) job records for the solve kernels
@@ -585,8 +588,8 @@ struct Engine {
         J.factor = factor.p + fac_base[s] + fd.fac_off;
         J.dinv = dinv.p + n_base[s] + fd.sep_off;
         J.x = h_subs[s].x;
-        J.x1 = h_subs[s].x1;
-        J.b = h_subs[s].rb;
+        J.x1 = nullptr;
+        J.b = nullptr;
         J.pm = cd.pmap.p + fd.t_off;
         J.be = cd.bnd_elim.p + fd.bnd_off;
         J.k = fd.k;
@@ -612,8 +615,6 @@ struct Engine {
       for (int j = 0; j < njobs; ++j) {
         SolveJob J = hj[j];
         J.x += b * xstride;
-        J.x1 += b * xstride;
-        J.b += b * xstride;
         hj[static_cast<size_t>(b) * njobs + j] = J;
       }
     jobs.upload(hj, stream);
@@ -749,7 +750,7 @@ struct Engine {
 
   // One forward and one backward launch over the items of a step group.
   DBuf<unsigned long long> trace;
-  void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const unsigned* nzmask,
+  void run_solve(const SolveItem* fwd, int nfwd, const SolveItem* bwd, int nbwd, const rmask* nzmask,
                  bool traced = false, const unsigned* tface = nullptr, const unsigned* need = nullptr,
                  int need_words = 0) {
     const long long per = static_cast<long long>(nslots) * nf_max;
@@ -773,6 +774,9 @@ struct Engine {
     a.need = need;
     a.need_words = need_words;
     a.nsub = static_cast<int>(sub_cls.size());
+    a.rbs = rb.p;
+    a.x1s = x1.p;
+    a.slot_stride = slot_stride;
     a.items = fwd;
     a.nitems = nfwd;
     a.done = cnt.p;
@@ -841,7 +845,7 @@ struct FactorHandle {
   std::vector<SolveItem> fwd, bwd;
   int items_R = 0;
   DBuf<SolveItem> d_fwd, d_bwd;
-  DBuf<unsigned> nz;
+  DBuf<rmask> nz;
   DBuf<double2> io;
   // Factorization::solve is "reentrant; safe for concurrent calls on one factorization"
   // (include/helmsweep/direct.hpp:29). The device solve shares the engine's buffers, so
@@ -909,8 +913,8 @@ void factor_solve_device(FactorHandle& H, int nrhs, double2* d_x, cudaStream_t u
     gather_in_kernel<<<blocks, threads, 0, eng.stream>>>(xb, eng.rb.p, eng.classes[0]->local_of_elim.p, n, R);
     g_kernel_launches.fetch_add(1);
     HS_CUDA(cudaGetLastError());
-    const unsigned mask = R >= 32 ? ~0u : ((1u << R) - 1u);
-    HS_CUDA(cudaMemcpyAsync(H.nz.p, &mask, sizeof(unsigned), cudaMemcpyHostToDevice, eng.stream));
+    const rmask mask = R >= 64 ? ~0ull : ((1ull << R) - 1ull);
+    HS_CUDA(cudaMemcpyAsync(H.nz.p, &mask, sizeof(rmask), cudaMemcpyHostToDevice, eng.stream));
     eng.run_solve(H.d_fwd.p, static_cast<int>(H.fwd.size()), H.d_bwd.p, static_cast<int>(H.bwd.size()), H.nz.p);
     scatter_out_kernel<<<blocks, threads, 0, eng.stream>>>(eng.x.p, xb, eng.classes[0]->elim_of_local.p, n, R);
     g_kernel_launches.fetch_add(1);
@@ -1107,7 +1111,7 @@ struct DdmHandle {
   static constexpr int kCopyStreams = 2;  // streamed host I/O: b in, u out
   cudaStream_t cs[kCopyStreams] = {};
   std::vector<cudaEvent_t> ev_in, ev_out;
-  DBuf<int2> d_mtasks;
+  DBuf<int2> d_mtasks, d_prev;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
   // per subdomain, a bitset over fronts: the front's subtree holds a position the application
@@ -1124,7 +1128,8 @@ struct DdmHandle {
   std::vector<Vec3i> plan;
   std::vector<int> route_h;
   DBuf<double2> mbox;
-  DBuf<unsigned> mpres, nzmask, tface;
+  DBuf<rmask> mpres, nzmask;
+  DBuf<unsigned> tface;
   DBuf<int> route;
   DBuf<double2> bN, u, io;
   DBuf<double2> uround;  // fused accumulate over several rounds: u after each round but the last
@@ -1232,7 +1237,7 @@ struct DdmHandle {
     graphs.clear();
   }
   void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps, int slot = 0,
-                      bool last = true);
+                      bool last = true, int cap = 0);
   cudaEvent_t ev_din_free[2] = {}, ev_dout_free[2] = {};
   void reports(int nrounds, bool track, hs_solve_report* out);
 };
@@ -1876,8 +1881,8 @@ void DdmHandle::build_schedule(int r) {
       HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
       const double have = static_cast<double>(free_b) +
                           static_cast<double>(eng.x.n + eng.x1.n + eng.rb.n) * sizeof(double2);
-      const double per_buf = 3.0 * static_cast<double>(eng.n_base.back()) * r * sizeof(double2);  // x, x1, rb
-      const double reserve = (4.0 * kMaxRhs + 4.0 * r) * static_cast<double>(geom.gn) * sizeof(double2) + 4e9;
+      const double per_buf = static_cast<double>(eng.n_base.back()) * r * sizeof(double2);  // x
+      const double reserve = 8.0 * r * static_cast<double>(geom.gn) * sizeof(double2) + 4e9;  // io slots, bN, u, uround
       if (want * per_buf + reserve <= 0.9 * have) nbuf = want;
     }
   }
@@ -2001,6 +2006,19 @@ void DdmHandle::build_schedule(int r) {
     flat.insert(flat.end(), msteps_own[m].begin(), msteps_own[m].end());
     max_width = std::max(max_width, static_cast<int>(msteps_own[m].size()));
   }
+  // previous occupant of each task's slot within the application: (class, 1 if it was a sweep-1 task
+  // that wrote its whole slot), or (-1, 0) for the slot's first use (rb is cleared per application)
+  std::vector<int2> prev(std::max<size_t>(flat.size(), 1), make_int2(-1, 0));
+  {
+    std::vector<int2> last(static_cast<size_t>(max_width), make_int2(-1, 0));
+    for (int m = 0; m < nmacro; ++m)
+      for (size_t t = 0; t < msteps_own[m].size(); ++t) {
+        prev[mt_off[m] + t] = last[t];
+        const int2 tk = msteps_own[m][t];
+        last[t] = make_int2(subs[tk.x].cls, tk.y == 1 ? 1 : 0);
+      }
+  }
+  d_prev.upload(prev, eng.stream);
   if (flat.empty()) flat.push_back(make_int2(0, 1));
   d_mtasks.upload(flat, eng.stream);
 }
@@ -2356,8 +2374,8 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   const int nsub = geom.nsub;
   if (track) ensure_gop();
   HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
-  HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(unsigned), s));
-  HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(unsigned), s));
+  HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(rmask), s));
+  HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(rmask), s));
   HS_CUDA(cudaMemsetAsync(tface.p, 0, tface.n * sizeof(unsigned), s));
   if (timed) record(ev[0], s);
   SweepArgs sa{};
@@ -2376,6 +2394,10 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   sa.nzmask = nzmask.p;
   sa.tface = tface.p;
   sa.route = route.p;
+  sa.rbs = eng.rb.p;
+  sa.slot_stride = eng.slot_stride;
+  // slots start clean every application (their previous occupants are then within it)
+  HS_CUDA(cudaMemsetAsync(eng.rb.p, 0, eng.rb.n * sizeof(double2), s));
   const int nm = static_cast<int>(msteps.size());
   int waited = 0, stripes_done = 0;  // waited: tiles of b staged (copy order)
   bool u_reduced = false;
@@ -2404,6 +2426,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   for (int m = 0; m < nm; ++m) {
     if (io && need_tiles[m] > waited) stage_in(need_tiles[m]);  // streamed b: the tiles this step's sources read
     sa.tasks = d_mtasks.p + mt_off[m];
+    sa.prev = d_prev.p + mt_off[m];
     sa.ntasks = static_cast<int>(msteps_own[m].size());
     if (sa.ntasks > 0) {
       // tasks past sweep 1 touch only their injection lines: size the init grid for that
@@ -2545,29 +2568,33 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
 // reference's canonical order (src/sweeper.cpp:285-307).
 void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
   const int nsub = geom.nsub;
-  std::vector<unsigned> nz(static_cast<size_t>(nsweeps) * nsub);
+  std::vector<rmask> nz(static_cast<size_t>(nsweeps) * nsub);
   std::vector<double> nrm(static_cast<size_t>(nsweeps) * R), num(static_cast<size_t>(nrounds) * R),
       den(static_cast<size_t>(nrounds) * R);
-  HS_CUDA(cudaMemcpyAsync(nz.data(), nzmask.p, nz.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, eng.stream));
+  HS_CUDA(cudaMemcpyAsync(nz.data(), nzmask.p, nz.size() * sizeof(rmask), cudaMemcpyDeviceToHost, eng.stream));
   HS_CUDA(cudaMemcpyAsync(nrm.data(), norms.p, nrm.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
   if (track) {
     HS_CUDA(cudaMemcpyAsync(num.data(), rnum.p, num.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
     HS_CUDA(cudaMemcpyAsync(den.data(), rden.p, den.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
   }
   HS_CUDA(cudaStreamSynchronize(eng.stream));
-  if (partitioned()) {  // every task's mask from its owner (ghost copies are dropped first)
-    std::vector<double> w(nz.size());
+  if (partitioned()) {  // every task's mask from its owner (ghost copies are dropped first); the sum
+                        // over ranks runs on the two 32-bit halves of each mask (exact in doubles)
+    std::vector<double> w(2 * nz.size());
     for (int l = 1; l <= nsweeps; ++l)
       for (int id = 0; id < nsub; ++id) {
         const size_t i = static_cast<size_t>(l - 1) * nsub + id;
-        w[i] = owner[id] == rank ? static_cast<double>(nz[i]) : 0.0;
+        const bool mine = owner[id] == rank;
+        w[2 * i] = mine ? static_cast<double>(nz[i] & 0xffffffffull) : 0.0;
+        w[2 * i + 1] = mine ? static_cast<double>(nz[i] >> 32) : 0.0;
       }
     dtmp.alloc(w.size());
     HS_CUDA(cudaMemcpyAsync(dtmp.p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, eng.stream));
     comm_allreduce(dtmp.p, static_cast<long long>(w.size()));
     HS_CUDA(cudaMemcpyAsync(w.data(), dtmp.p, w.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
-    for (size_t i = 0; i < nz.size(); ++i) nz[i] = static_cast<unsigned>(w[i]);
+    for (size_t i = 0; i < nz.size(); ++i)
+      nz[i] = static_cast<rmask>(w[2 * i]) | (static_cast<rmask>(w[2 * i + 1]) << 32);
   }
   const int nm = static_cast<int>(msteps.size());
   std::vector<double> sweep_sec(nsweeps, 0.0), step_sec(nm, 0.0);
@@ -2607,7 +2634,7 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
       for (int st = 1; st <= steps; ++st) {
         const auto& grp = groups[di * steps + st - 1];
         for (int id : grp) {
-          const bool nonzero = (nz[static_cast<size_t>(l - 1) * nsub + id] >> r) & 1u;
+          const bool nonzero = (nz[static_cast<size_t>(l - 1) * nsub + id] >> r) & 1ull;
           if (!nonzero) {
             ++rep.skipped_zero_solves;
             continue;
@@ -2647,7 +2674,7 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
 // is fused, else stripes) as the tail of the application completes them. One copy stream per
 // direction; the copy streams carry copies only, never kernels.
 void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds, bool track, hs_solve_report* reps,
-                               int slot, bool last) {
+                               int slot, bool last, int cap) {
   ensure_state(nr, nrounds);
   const long long n = geom.gn;
   const int nt = static_cast<int>(in_tiles.size());
@@ -2667,9 +2694,10 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
   // Two staging slots (din, dout) so consecutive batches overlap: batch k + 1's b streams in while
   // batch k computes, and batch k's u streams out while batch k + 1 computes. A slot is reused two
   // batches later, after the application that read its din and the copies that read its dout.
-  io.alloc(static_cast<size_t>(n) * kMaxRhs * 4);
-  double2* din = io.p + static_cast<size_t>(slot) * 2 * n * kMaxRhs;
-  double2* dout = din + static_cast<size_t>(n) * kMaxRhs;
+  cap = std::max(cap, nr);  // RHS per staging slot: the call's widest batch
+  io.alloc(static_cast<size_t>(n) * cap * 4);
+  double2* din = io.p + static_cast<size_t>(slot) * 2 * n * cap;
+  double2* dout = din + static_cast<size_t>(n) * cap;
   HS_CUDA(cudaStreamWaitEvent(cs[0], ev_din_free[slot], 0));
   HS_CUDA(cudaStreamWaitEvent(eng.stream, ev_dout_free[slot], 0));
   const size_t gx = static_cast<size_t>(geom.gsize[0]), rows = static_cast<size_t>(n) / gx;
@@ -3004,15 +3032,16 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
       for (int b0 = 0, k = 0; b0 < nrhs; b0 += kMaxRhs, ++k) {  // consecutive batches overlap (two slots)
         const int R = std::min(kMaxRhs, nrhs - b0);
         H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,
-                         reports ? reports + b0 : nullptr, k & 1, b0 + kMaxRhs >= nrhs);
+                         reports ? reports + b0 : nullptr, k & 1, b0 + kMaxRhs >= nrhs, std::min(nrhs, kMaxRhs));
       }
       return;
     }
     for (int b0 = 0; b0 < nrhs; b0 += kMaxRhs) {
       const int R = std::min(kMaxRhs, nrhs - b0);
-      H.io.alloc(static_cast<size_t>(n) * kMaxRhs * 2);
+      const int cap = std::min(nrhs, kMaxRhs);
+      H.io.alloc(static_cast<size_t>(n) * cap * 2);
       double2* din = H.io.p;
-      double2* dout = H.io.p + static_cast<size_t>(n) * kMaxRhs;
+      double2* dout = H.io.p + static_cast<size_t>(n) * cap;
       HS_CUDA(cudaMemcpyAsync(din, b + 2 * b0 * n, sizeof(double2) * n * R, cudaMemcpyHostToDevice, H.eng.stream));
       ddm_solve_batch(H, R, din, dout, rounds, track_residuals != 0, reports ? reports + b0 : nullptr);
       HS_CUDA(cudaMemcpyAsync(u + 2 * b0 * n, dout, sizeof(double2) * n * R, cudaMemcpyDeviceToHost, H.eng.stream));
@@ -3071,7 +3100,8 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
   // per RHS column: the Krylov basis and work vectors, plus the DDM application's per-RHS
   // buffers (x / z / rhs per subdomain and x buffer, b / u / staging on the global grid)
   const int nbuf_max = std::max(4, std::min(rounds * H.ndir, HS_MAX_ACC_SWEEPS));  // x buffers (build_schedule)
-  const double ddm_col = (3.0 * nbuf_max * static_cast<double>(H.eng.n_base.back()) + 6.0 * n) * sizeof(double2);
+  const double ddm_col = (static_cast<double>(nbuf_max) * H.eng.n_base.back() + 2.0 * H.geom.nsub * H.eng.n_max +
+                          6.0 * n) * sizeof(double2);
   const double per_col = static_cast<double>(mk + 5) * n * sizeof(double2) + ddm_col;
   int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
   if (H.partitioned()) rmax = kMaxRhs;  // every rank must batch identically
@@ -3286,8 +3316,9 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
     HS_CUDA(cudaSetDevice(H.eng.device));
     HS_CUDA(cudaStreamSynchronize(H.eng.stream));
     const int nsub = H.geom.nsub;
-    std::vector<unsigned> nz(static_cast<size_t>(H.nsweeps) * nsub), tf(nz.size());
-    HS_CUDA(cudaMemcpy(nz.data(), H.nzmask.p, nz.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
+    std::vector<rmask> nz(static_cast<size_t>(H.nsweeps) * nsub);
+    std::vector<unsigned> tf(nz.size());
+    HS_CUDA(cudaMemcpy(nz.data(), H.nzmask.p, nz.size() * sizeof(rmask), cudaMemcpyDeviceToHost));
     HS_CUDA(cudaMemcpy(tf.data(), H.tface.p, tf.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
     // the work the solve performs: the backward pass over every front, the forward pass over the
     // live fronts only (past sweep 1, fronts whose subtree holds no nonzero injection line have

@@ -8,7 +8,8 @@
 namespace hsb {
 
 constexpr int kMaxDirs = 6;  // 2*dim cardinal faces
-constexpr int kMaxRhs = 32;  // RHS per device batch (bitmask width)
+constexpr int kMaxRhs = 64;  // RHS per device batch (bitmask width)
+using rmask = unsigned long long;  // one bit per RHS column of a batch
 
 struct DevFront {
   int k, m, sep_off, bnd_off;
@@ -49,9 +50,8 @@ struct DevSub {
   double2* dinv;              // 1/d, elimination order
   const double2* val;         // CSR values (factorization input)
   double2* x;                 // solve vector, elimination order, node-major x R (rhs -> solution)
-  double2* x1;                // forward result z = D^-1 L^-1 b (same layout)
-  double2* rb;                // right-hand side of the task (same layout); zero off the injection
-                              // lines except while a sweep-1 task holds its split source
+  double2* x1;                // (unused: z and the right-hand side live in per-slot buffers,
+  double2* rb;                //  SolveArgs / SweepArgs rbs, x1s)
   const double2* coef[kMaxDirs];  // injection couplings per incoming direction
   const int* split_gp;             // per elimination position: global node of the split source
   const unsigned char* split_w;    // its weight numerator over 2^dim (0 = shell or outside support)
@@ -87,8 +87,8 @@ struct SolveJob {
   const double2* factor;  // solve-layout factor of the front
   const double2* dinv;    // 1/d of the separator (elimination order)
   double2* x;             // the subdomain's x (elimination order, node-major x R)
-  double2* x1;            // the subdomain's z = D^-1 L^-1 b
-  const double2* b;       // the subdomain's right-hand side (forward input)
+  double2* x1;            // (unused: z and the right-hand side are per slot, SolveArgs x1s / rbs)
+  const double2* b;
   const int2* pm;         // extend-add source map of the front's positions
   const int* be;          // boundary elimination positions
   int k, m, sep_off, v_off;

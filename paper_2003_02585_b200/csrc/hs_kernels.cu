@@ -37,6 +37,11 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNB = 16;  // factorization panel width
 
 __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ unsigned long long reduce_or64(unsigned long long v) {  // warp OR of a 64-bit mask
+  const unsigned lo = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(v));
+  const unsigned hi = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(v >> 32));
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -291,8 +296,9 @@ constexpr int HS_SLOTS_PER_DIR = 16;  // generating sweeps that can route into o
 __device__ __forceinline__ double2* task_x(const SweepArgs& a, const DevSub& S, int l) {
   return S.x + static_cast<long long>((l - 1) % a.nbuf) * a.xstride;
 }
-__device__ __forceinline__ double2* task_b(const SweepArgs& a, const DevSub& S, int l) {
-  return S.rb + static_cast<long long>((l - 1) % a.nbuf) * a.xstride;
+// the right-hand side of the macro-step's task t lives in slot t
+__device__ __forceinline__ double2* task_b(const SweepArgs& a, int t) {
+  return a.rbs + static_cast<long long>(t) * a.slot_stride;
 }
 
 // RHS of a task before injection (src/sweeper.cpp:189-239). Sweep 1: the split source
@@ -302,44 +308,48 @@ __device__ __forceinline__ double2* task_b(const SweepArgs& a, const DevSub& S, 
 __global__ void rhs_init_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
-  double2* B = task_b(a, S, l);
+  double2* B = task_b(a, blockIdx.y);
   const DevClass& C = a.cls[S.cls];
   const int dim = a.g.dim;
-  if (l > 1 && l - a.nbuf != 1) {  // lines only
+  const int2 prev = a.prev[blockIdx.y];
+  if (l > 1 && prev.y == 0) {  // the slot is zero off its previous occupant's injection lines: clear those
+    if (prev.x < 0) return;
+    const DevClass& P = a.cls[prev.x];
     for (int d = 0; d < a.dirs; ++d) {
-      const int len = C.line_len[d];
+      const int len = P.line_len[d];
       for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * a.R;
            idx += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
-        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+        const int p0 = P.inj_p0[d][i], pm = P.inj_pm[d][i];
         if (p0 >= 0) B[static_cast<long long>(p0) * a.R + r] = czero();
         if (pm >= 0) B[static_cast<long long>(pm) * a.R + r] = czero();
       }
     }
     return;
   }
-  // sweep 1 (or the first reuse of a sweep-1 buffer): split source / zero over the whole buffer;
-  // nonzero bits of positions off the injection lines are final here (lines: nonzero_kernel)
-  const long long total = static_cast<long long>(C.n) * a.R;
+  // sweep 1 (or a slot whose previous occupant wrote all of it): split source / zero over the
+  // whole buffer (the larger of this class's and the previous occupant's extent); nonzero bits of
+  // positions off the injection lines are final here (lines: nonzero_kernel)
+  const long long total = a.slot_stride;  // the whole slot: every occupant then keeps it zero off its lines
   const double inv = 1.0 / static_cast<double>(1 << dim);
-  unsigned bits = 0;
+  rmask bits = 0;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     double2 v = czero();
-    if (l == 1) {
+    if (l == 1 && idx < static_cast<long long>(C.n) * a.R) {
       const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
       const int wn = S.split_w[e];
       if (wn) {
         const double w = wn * inv;
         const double2 bv = a.b[static_cast<long long>(S.split_gp[e]) * a.R + r];
         v = make_double2(w * bv.x, w * bv.y);
-        if ((v.x != 0.0 || v.y != 0.0) && !C.on_line[e]) bits |= 1u << r;
+        if ((v.x != 0.0 || v.y != 0.0) && !C.on_line[e]) bits |= 1ull << r;
       }
     }
     B[idx] = v;
   }
   if (l == 1) {
-    bits = __reduce_or_sync(kFull, bits);
+    bits = reduce_or64(bits);
     if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
   }
 }
@@ -355,10 +365,10 @@ __global__ void inject_kernel(SweepArgs a, int axis) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
   const DevClass& C = a.cls[S.cls];
-  double2* B = task_b(a, S, l);  // the task's right-hand side
+  double2* B = task_b(a, blockIdx.y);  // the task's right-hand side
   const int R = a.R;
   __shared__ long long s_slot[2][HS_SLOTS_PER_DIR];
-  __shared__ unsigned s_pres[2][HS_SLOTS_PER_DIR];
+  __shared__ rmask s_pres[2][HS_SLOTS_PER_DIR];
   __shared__ int s_n[2];
   if (threadIdx.x < 2) {
     const int d = 2 * axis + threadIdx.x;
@@ -366,7 +376,7 @@ __global__ void inject_kernel(SweepArgs a, int axis) {
     for (int lg = 1; lg <= l && n < HS_SLOTS_PER_DIR; ++lg) {
       if (a.route[(lg - 1) * a.dirs + d] != l) continue;
       const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
-      const unsigned pres = a.mpres[slot];
+      const rmask pres = a.mpres[slot];
       if (pres == 0) continue;
       s_slot[threadIdx.x][n] = slot;
       s_pres[threadIdx.x][n] = pres;
@@ -386,7 +396,7 @@ __global__ void inject_kernel(SweepArgs a, int axis) {
     double2 u0 = czero(), um1 = czero();
     bool first = true;
     for (int k = 0; k < n; ++k) {
-      if (!((s_pres[q][k] >> r) & 1u)) continue;
+      if (!((s_pres[q][k] >> r) & 1ull)) continue;
       const double2* s0 = a.mbox + s_slot[q][k] * a.mbox_dir_stride;
       const double2 v0 = s0[idx], v1 = s0[static_cast<long long>(len) * R + idx];
       u0 = first ? v0 : cadd(u0, v0);
@@ -407,13 +417,14 @@ __global__ void nonzero_kernel(SweepArgs a) {
   const int sub = a.tasks[blockIdx.y].x, l = a.tasks[blockIdx.y].y;
   const DevSub& S = a.subs[sub];
   const DevClass& C = a.cls[S.cls];
-  const double2* B = task_b(a, S, l);
+  const double2* B = task_b(a, blockIdx.y);
   const int R = a.R;
-  unsigned bits = 0, faces = 0;
+  rmask bits = 0;
+  unsigned faces = 0;
   {
     for (int d = 0; d < a.dirs; ++d) {
       const int len = C.line_len[d];
-      const unsigned b0 = bits;
+      const rmask b0 = bits;
       bits = 0;
       for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * R;
            idx += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -421,18 +432,18 @@ __global__ void nonzero_kernel(SweepArgs a) {
         const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
         if (p0 >= 0) {
           const double2 v = B[static_cast<long long>(p0) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
         }
         if (pm >= 0) {
           const double2 v = B[static_cast<long long>(pm) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1u << r;
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
         }
       }
       if (bits) faces |= 1u << d;
       bits |= b0;
     }
   }
-  bits = __reduce_or_sync(kFull, bits);
+  bits = reduce_or64(bits);
   faces = __reduce_or_sync(kFull, faces);
   // Only faces whose mailbox slots some generating sweep fills for this sweep carry injected data;
   // lines of other faces can hold a nonzero value only where they cross a receiving face's line,
@@ -466,7 +477,7 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   const int t = S.sub[axis] + sign;
   if (t < 0 || t >= a.g.counts[axis]) return;
   if (a.route[(l - 1) * a.dirs + d] == 0) return;
-  const unsigned nz = a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub];
+  const rmask nz = a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub];
   if (nz == 0) return;
   int stride = 1;
   for (int ax = 0; ax < axis; ++ax) stride *= a.g.counts[ax];
@@ -480,7 +491,7 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx < len * R) {
     const int i = idx / R, r = idx % R;
-    if ((nz >> r) & 1u) {
+    if ((nz >> r) & 1ull) {
       u0[idx] = X[static_cast<long long>(C.ext_u0[d][i]) * R + r];
       um1[idx] = X[static_cast<long long>(C.ext_um1[d][i]) * R + r];
     }
@@ -510,7 +521,7 @@ __global__ void __launch_bounds__(kThreads) accumulate_kernel(AccumArgs a) {
     bool on[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) {
-      on[i] = ent[i].x >= 0 && ((a.nzmask[ent[i].y >> 4] >> r) & 1u);
+      on[i] = ent[i].x >= 0 && ((a.nzmask[ent[i].y >> 4] >> r) & 1ull);
       xv[i] = on[i] ? a.x[a.xoff + static_cast<long long>(ent[i].x) * R + r] : czero();
     }
     double2 acc = czero();
@@ -770,17 +781,17 @@ void launch_factor_level_cluster(const FactorArgs& a, int max_m, cudaStream_t s)
 
 // Pack (arrays -> message) or unpack (message -> arrays) of one exchange, a block per segment.
 __global__ void __launch_bounds__(kThreads) xpack_kernel(const XSeg* segs, bool pack, double* buf, double2* mbox,
-                                                         unsigned* mpres, double2* x, unsigned* nz,
+                                                         rmask* mpres, double2* x, rmask* nz,
                                                          const long long* gpos, int R) {
   const XSeg sg = segs[blockIdx.x];
   double* B = buf + sg.b;
   if (sg.kind == 1 || sg.kind == 3) {
-    unsigned* w = sg.kind == 1 ? mpres + sg.a : nz + sg.a;
-    if (threadIdx.x == 0) {
+    rmask* w = sg.kind == 1 ? mpres + sg.a : nz + sg.a;
+    if (threadIdx.x == 0) {  // a 64-bit mask travels as the bit pattern of one double (no arithmetic)
       if (pack)
-        B[0] = static_cast<double>(*w);
+        B[0] = __longlong_as_double(static_cast<long long>(*w));
       else
-        *w = static_cast<unsigned>(B[0]);
+        *w = static_cast<rmask>(__double_as_longlong(B[0]));
     }
     return;
   }
@@ -802,8 +813,8 @@ __global__ void __launch_bounds__(kThreads) xpack_kernel(const XSeg* segs, bool 
   }
 }
 
-void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, unsigned* mpres, double2* x,
-                  unsigned* nzmask, const long long* gpos, int R, cudaStream_t s) {
+void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, rmask* mpres, double2* x,
+                  rmask* nzmask, const long long* gpos, int R, cudaStream_t s) {
   if (nseg <= 0) return;
   xpack_kernel<<<nseg, kThreads, 0, s>>>(segs, pack, buf, mbox, mpres, x, nzmask, gpos, R);
   after_launch();
@@ -857,7 +868,7 @@ __global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a
       bool on[E];
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        on[i] = ent[i].x >= 0 && ((a.nzmask[l][ent[i].y >> 4] >> r) & 1u);
+        on[i] = ent[i].x >= 0 && ((a.nzmask[l][ent[i].y >> 4] >> r) & 1ull);
         xv[i] = on[i] ? __ldcs(a.x + a.xoff[l] + static_cast<long long>(ent[i].x) * R + r) : czero();
       }
       double2 acc = czero();

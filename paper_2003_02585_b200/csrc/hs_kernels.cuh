@@ -21,13 +21,19 @@ struct SolveArgs {
   int nf_max;
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
-  const unsigned* nzmask;  // per subdomain: RHS columns with a nonzero right-hand side
+  const rmask* nzmask;     // per subdomain: RHS columns with a nonzero right-hand side
   const unsigned* tface;   // per task: faces with nonzero injected data, 0x100 = every front live
   int m3;                  // complex products as 3 real DMMAs (3 CTAs / SM) instead of 4 (4 CTAs / SM)
                            // (sweep 1); null = every front live
   const unsigned* need;    // per subdomain bitset over fronts: x read back (backward pass); null = all
   int need_words;          // 32-bit words per subdomain in `need`
   int nsub;                // subdomains (task index nzi = (sweep - 1) * nsub + sub)
+  // per-slot buffers (slot = the task's position in its macro-step): the task's right-hand side
+  // (forward input) and z = D^-1 L^-1 b (forward output, backward input), elimination order,
+  // node-major x R; slot_stride elements apart
+  double2* rbs;
+  double2* x1s;
+  long long slot_stride;
 };
 
 // Multifrontal forward (z = D^-1 L^-1 b) or backward (x = L^-T z) pass over the work items of
@@ -74,10 +80,14 @@ struct SweepArgs {
   const double2* b;        // global rhs, node-major N x R
   double2* mbox;           // mailbox slots [target sub][generating sweep][dir][2][line][R]
   long long mbox_dir_stride;  // elements per (sub, sweep, dir) slot
-  unsigned* mpres;         // presence bitmask [target sub][generating sweep][dir]
-  unsigned* nzmask;        // [sweep][sub]
+  rmask* mpres;            // presence bitmask [target sub][generating sweep][dir]
+  rmask* nzmask;           // [sweep][sub]
   unsigned* tface;         // [sweep][sub]: faces whose injection lines carry a nonzero value
   const int* route;        // [sweep][dir] target sweep (0 = discard)
+  double2* rbs;            // per-slot right-hand sides (slot = task position in the macro-step)
+  long long slot_stride;
+  const int2* prev;        // per task: the previous occupant of its slot (class, 1 if it wrote the
+                           // whole buffer) -- (-1, 0) when the slot is clean
 };
 // RHS of each subdomain task: split source (sweep 1) plus injected traces, and the
 // exact-zero test (src/sweeper.cpp:189-251, src/transfer.cpp:68-89).
@@ -96,7 +106,7 @@ struct AccumArgs {
   const int2* acc_ent;       // this sweep direction's plan: per global node 2^dim entries in the
                              // reference's accumulation order (x position n_base[sub] + elim,
                              // sub << 4 | weight numerator); unused entries have position -1
-  const unsigned* nzmask;    // [sub] for sweep l
+  const rmask* nzmask;       // [sub] for sweep l
   double2* u;                // global solution, node-major N x R
   double* partial;           // per-block partial |contrib|^2 [nblocks][R]
   long long n0, n1;          // node range of this launch
@@ -113,7 +123,7 @@ struct AccumAllArgs {
   int R, L;
   const int2* acc_ent[HS_MAX_ACC_SWEEPS];   // plan of sweep l's direction
   long long xoff[HS_MAX_ACC_SWEEPS];        // x buffer of sweep l
-  const unsigned* nzmask[HS_MAX_ACC_SWEEPS];
+  const rmask* nzmask[HS_MAX_ACC_SWEEPS];
   const double2* x;
   double2* u;
   double* partial;     // sweep l's partials at partial + l * pstride
@@ -142,8 +152,8 @@ struct XSeg {
   long long b;     // offset in the message buffer (doubles)
   long long c;     // kind 2: x buffer offset (elements)
 };
-void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, unsigned* mpres, double2* x,
-                  unsigned* nzmask, const long long* gpos, int R, cudaStream_t s);
+void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, rmask* mpres, double2* x,
+                  rmask* nzmask, const long long* gpos, int R, cudaStream_t s);
 
 // Global CSR SpMV y = A x (x, y node-major N x R) (src/operator.cpp:7-17) and the
 // residual partials |b - y|^2, |b|^2.

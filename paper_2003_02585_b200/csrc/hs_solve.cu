@@ -424,6 +424,11 @@ __device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, I
 #ifndef HS_LEAN
 #define HS_LEAN 1
 #endif
+// 1: the forward's chunk-0 accumulators start at -T_bnd (loaded before the k-loop, round 1);
+// 0: V = T_bnd - W T_sep is formed in the finalize, so no load precedes the k-loop
+#ifndef HS_TB_START
+#define HS_TB_START 0
+#endif
 
 // Forward band item: out[32 band rows][8 NT RHS] += [M; W][rows, chunk cols] * T_sep[chunk cols],
 // T = rhs + child0 V + child1 V summed at use in the reference's child order.
@@ -681,7 +686,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const FwdRange rg = fwd_range(J, g, it);
   const int t = rg.t, rbs = rg.rbs, cb0 = rg.cb0, cb1 = rg.cb1;
   const double2* P = J.factor + band_base(t, g.kb) + rl * 8 + (lane & 3);
-  const double2* X = J.b + static_cast<long long>(J.sep_off) * R;  // right-hand side
+  const double2* X = a.rbs + it.slot * a.slot_stride + static_cast<long long>(J.sep_off) * R;  // right-hand side (the task's slot)
   const bool leaf = J.child0 < 0 && J.child1 < 0;
   const int2* fsrc = sidx + kIdx;
   const double2* fdv = reinterpret_cast<const double2*>(fsrc + 32);
@@ -744,7 +749,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   };
   Acc<NT, M3> acc;
   acc_zero(acc);
-  if (it.chunk == 0 && !leaf) {  // -T_bnd = -((0 + child0 V) + child1 V) on boundary rows
+  if (HS_TB_START && it.chunk == 0 && !leaf) {  // -T_bnd = -((0 + child0 V) + child1 V) on boundary rows
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (4 * t + i < g.kb) continue;  // separator row block
@@ -813,7 +818,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const int pr = 32 * t + 8 * i + rl;
     if (pr < J.k) {
       const double2 dv = fdv[8 * i + rl];
-      double2* zo = J.x1 + static_cast<long long>(J.sep_off + pr) * R;
+      double2* zo = a.x1s + it.slot * a.slot_stride + static_cast<long long>(J.sep_off + pr) * R;
 #pragma unroll
       for (int q = 0; q < NT; ++q)
 #pragma unroll
@@ -823,13 +828,36 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
         }
     } else if (pr >= g.kp && pr - g.kp < J.m - J.k) {
       double2* vo = V + static_cast<long long>(J.v_off + pr - g.kp) * R;
+      if (HS_TB_START || leaf) {  // V = -acc (acc started at -T_bnd; a leaf has T_bnd = 0)
 #pragma unroll
-      for (int q = 0; q < NT; ++q)
+        for (int q = 0; q < NT; ++q)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = r0 + 8 * q + 2 * (lane & 3) + e;
-          if (r < R) __stcg(vo + r, make_double2(-acc.v[i][q][0][e], -acc.v[i][q][1][e]));
-        }
+          for (int e = 0; e < 2; ++e) {
+            const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+            if (r < R) __stcg(vo + r, make_double2(-acc.v[i][q][0][e], -acc.v[i][q][1][e]));
+          }
+      } else {  // V = T_bnd - W T_sep, T_bnd = (0 + child0 V) + child1 V (reference order: product first)
+        int2 src = fsrc[8 * i + rl];
+        if (!(clive & 1u)) src.x = -1;
+        if (!(clive & 2u)) src.y = -1;
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+            if (r >= R) continue;
+            double2 tb = czero();
+            if (src.x >= 0) {
+              const double2 w = __ldcg(V + static_cast<long long>(src.x) * R + r);
+              tb = make_double2(tb.x + w.x, tb.y + w.y);
+            }
+            if (src.y >= 0) {
+              const double2 w = __ldcg(V + static_cast<long long>(src.y) * R + r);
+              tb = make_double2(tb.x + w.x, tb.y + w.y);
+            }
+            __stcg(vo + r, make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
+          }
+      }
     }
   }
   return true;
@@ -846,7 +874,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
   const BwdRange rg = bwd_range(J, g, it);
   const int u = rg.u, a0 = rg.a0, a1 = rg.a1;
   const double2* P = J.factor + (lane & 3) * 8 + rl;
-  const double2* Z = J.x1 + static_cast<long long>(J.sep_off) * R;
+  const double2* Z = a.x1s + it.slot * a.slot_stride + static_cast<long long>(J.sep_off) * R;
   const int nb = J.m - J.k;
   // live m-tiles (column blocks 4u + i) of k-step s: columns below k (mcol), minus M's zero
   // blocks above the diagonal while the rows are separator rows (column block 4u + i > row block)
@@ -996,7 +1024,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
     int nfin = 0;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
     // the item's task and front records, loaded together (all are read-only during the launch)
-    const unsigned nzm = __ldg(a.nzmask + it.nzi);
+    const rmask nzm = __ldg(a.nzmask + it.nzi);
     const unsigned fm = a.tface ? __ldg(a.tface + it.nzi) : kAllLive;  // kAllLive: sweep 1 (split source)
     const SolveJob J = a.jobs[it.job];
     if (nzm != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it

@@ -71,13 +71,14 @@ def test_c3_full_scale_against_reference(hs, ref):
     """BASELINE configs[2] (C3, the bench headline) at full scale: 2048^2 two-layered medium,
     16x16 subdomains of 193^2, 2 rounds = 8 sweeps; RHS 0 of the bench's seeded batch."""
     s, b, U = _check_against_reference(hs, ref, "c3")
-    # the same RHS inside a full 64-RHS batch (two device batches) gives the same u, bit for bit
+    # the same RHS inside the full 64-RHS batch gives the same u (to roundoff: the split-K shape of
+    # the critical path depends on the batch width, src order of the partial sums with it)
     import bench
     f = bench.make_sources(bench.CFG["seed"], s.lo, s.hi, [1.0 / bench.CFG["n"]] * 2, [0.0, 0.0])
     B = s.scale_source(f)
     assert np.array_equal(B[0], b[0])
     U64 = s.ddm_solve(B, bench.CFG["rounds"], None, True)
-    assert np.array_equal(U64[0], U[0])
+    assert rel(U64[0], U[0]) <= 1e-12
 
 
 def test_c5_subdomain_size_against_reference_golden(hs, golden):
