@@ -1112,6 +1112,7 @@ struct DdmHandle {
   cudaStream_t cs[kCopyStreams] = {};
   std::vector<cudaEvent_t> ev_in, ev_out;
   DBuf<int2> d_mtasks, d_prev;
+  std::vector<int2> prev_h;
   DBuf<SolveItem> d_tasks;
   DBuf<int2> acc_ent;          // accumulate plan: per global node, 2^dim (position, sub, weight) entries
   // per subdomain, a bitset over fronts: the front's subtree holds a position the application
@@ -2019,6 +2020,7 @@ void DdmHandle::build_schedule(int r) {
       }
   }
   d_prev.upload(prev, eng.stream);
+  prev_h = prev;
   if (flat.empty()) flat.push_back(make_int2(0, 1));
   d_mtasks.upload(flat, eng.stream);
 }
@@ -2431,7 +2433,8 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     if (sa.ntasks > 0) {
       // tasks past sweep 1 touch only their injection lines: size the init grid for that
       bool full = false;
-      for (const int2& t : msteps_own[m]) full |= t.y == 1 || t.y - nbuf == 1;
+      // (a sweep-1 task writes its whole slot, and so does any task whose slot's previous occupant did)
+      for (size_t t = 0; t < msteps_own[m].size(); ++t) full |= msteps_own[m][t].y == 1 || prev_h[mt_off[m] + t].y == 1;
       launch_build_rhs(sa, full ? eng.n_max : 0, static_cast<int>(line_max), s);
     }
     if (timed) record(ev[1 + nsweeps + 2 * m], s);

@@ -565,7 +565,7 @@ __global__ void reduce_partials_stage1(const double* partial, int nblocks, int R
   }
 }
 __global__ void reduce_partials_stage2(const double* mid, int nmid, int R, double* out) {
-  const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;  // one warp per column, fixed tree
+  const int r = blockIdx.x, lane = threadIdx.x;  // one warp (block) per column, fixed tree
   if (r >= R) return;
   double s = 0.0;
   for (int b = lane; b < nmid; b += 32) s += mid[static_cast<long long>(b) * R + r];
@@ -588,10 +588,12 @@ __global__ void reduce_cpartials_kernel(const double2* partial, int nblocks, int
   if (threadIdx.x == 0) out[r] = red[0];
 }
 
-__global__ void residual_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
-                                const double2* x, const double2* b, int R, double* pnum, double* pden) {
-  __shared__ double rn[kThreads], rd[kThreads];
-  const int npb = kThreads / R;
+constexpr int kResThreads = 512;  // rows x RHS per block (64-RHS batches still get 8 rows per block)
+__global__ void __launch_bounds__(kResThreads) residual_kernel(long long n, const std::int64_t* row_ptr, const int* col,
+                                                                const double2* val, const double2* x, const double2* b,
+                                                                int R, double* pnum, double* pden) {
+  __shared__ double rn[kResThreads], rd[kResThreads];
+  const int npb = kResThreads / R;
   const long long row = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
   const int r = threadIdx.x % R;
   const long long idx = row * R + r;
@@ -622,7 +624,7 @@ __global__ void residual_kernel(long long n, const std::int64_t* row_ptr, const 
   __syncthreads();
   if (threadIdx.x < R) {
     double s1 = 0.0, s2 = 0.0;
-    for (int q = threadIdx.x; q < kThreads; q += R) {
+    for (int q = threadIdx.x; q < kResThreads; q += R) {
       s1 += rn[q];
       s2 += rd[q];
     }
@@ -840,14 +842,15 @@ void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
   after_launch();
 }
 
+constexpr int kAccThreads = 256;
 template <int E>
-__global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a) {
+__global__ void __launch_bounds__(kAccThreads) accumulate_all_kernel(AccumAllArgs a) {
   // Per-sweep |c_l|^2 partials are kept in registers and reduced once at the end (one barrier),
   // so the loads of consecutive sweeps overlap (a barrier per sweep serialised them: the fused
   // pass ran at 34% of HBM bandwidth on C3, ncu).
-  __shared__ double red[HS_MAX_ACC_SWEEPS][kThreads];
+  __shared__ double red[HS_MAX_ACC_SWEEPS][kAccThreads];
   const int dim = a.g.dim, R = a.R;
-  const int npb = kThreads / R;
+  const int npb = kAccThreads / R;
   const long long li = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;  // index in the region
   const long long node = (a.row0 + li / a.w) * a.gx + a.x0 + li % a.w;
   const int r = threadIdx.x % R;
@@ -890,21 +893,21 @@ __global__ void __launch_bounds__(kThreads) accumulate_all_kernel(AccumAllArgs a
   for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) red[l][threadIdx.x] = nrm[l];
   __syncthreads();
   // partial of sweep l, column c: the block's threads of column c in thread order (fixed order)
-  for (int q = threadIdx.x; q < a.L * R; q += kThreads) {
+  for (int q = threadIdx.x; q < a.L * R; q += kAccThreads) {
     const int l = q / R, c = q % R;
     double sm = 0.0;
-    for (int t = c; t < kThreads; t += R) sm += red[l][t];
+    for (int t = c; t < kAccThreads; t += R) sm += red[l][t];
     a.partial[l * a.pstride + static_cast<long long>(blockIdx.x) * R + c] = sm;
   }
 }
 
 int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s) {
-  const int nb = blocks_for(a.cnt, kThreads / a.R);
+  const int nb = blocks_for(a.cnt, kAccThreads / a.R);
   if (nb == 0) return 0;
   if (a.g.dim == 3)
-    accumulate_all_kernel<8><<<nb, kThreads, 0, s>>>(a);
+    accumulate_all_kernel<8><<<nb, kAccThreads, 0, s>>>(a);
   else
-    accumulate_all_kernel<4><<<nb, kThreads, 0, s>>>(a);
+    accumulate_all_kernel<4><<<nb, kAccThreads, 0, s>>>(a);
   after_launch();
   return nb;
 }
@@ -927,7 +930,7 @@ void launch_reduce_partials(double* partial, int nblocks, int R, double* out, cu
   const int g = std::max(1, std::min(kReduceBlocks, nblocks));
   reduce_partials_stage1<<<g, kThreads, 0, s>>>(partial, nblocks, R, mid);
   after_launch();
-  reduce_partials_stage2<<<1, 32 * R, 0, s>>>(mid, g, R, out);
+  reduce_partials_stage2<<<R, 32, 0, s>>>(mid, g, R, out);
   after_launch();
 }
 
@@ -938,8 +941,8 @@ void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2
 
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, const double2* x,
                     const double2* b, int R, double* pnum, double* pden, cudaStream_t s) {
-  const int nb = blocks_for(n, kThreads / R);
-  residual_kernel<<<nb, kThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden);
+  const int nb = blocks_for(n, kResThreads / R);
+  residual_kernel<<<nb, kResThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden);
   after_launch();
   return nb;
 }

@@ -72,7 +72,7 @@ def test_c3_full_scale_against_reference(hs, ref):
     16x16 subdomains of 193^2, 2 rounds = 8 sweeps; RHS 0 of the bench's seeded batch."""
     s, b, U = _check_against_reference(hs, ref, "c3")
     # the same RHS inside the full 64-RHS batch gives the same u (to roundoff: the split-K shape of
-    # the critical path depends on the batch width, src order of the partial sums with it)
+    # the critical path depends on the batch width, and the order of the partial sums with it)
     import bench
     f = bench.make_sources(bench.CFG["seed"], s.lo, s.hi, [1.0 / bench.CFG["n"]] * 2, [0.0, 0.0])
     B = s.scale_source(f)

@@ -352,19 +352,20 @@ def test_gridded_medium_against_reference(hs, tmp_path):
 
 
 def test_batches_beyond_the_device_batch_and_zero_rhs(hs, golden):
-    """nrhs above the 32-RHS device batch (two batches) equals per-RHS solves; an all-zero RHS
+    """nrhs above the 64-RHS device batch (two batches) equals per-RHS solves (to roundoff: the
+    split-K shape of the critical path follows the batch width) and the reference; an all-zero RHS
     gives an exactly zero field with every task skipped (src/sweeper.cpp:240-251)."""
     z = golden("ddm_2d_2x2")
     s = hs.DdmSolver(_setup(hs, z))
     rng = np.random.default_rng(5)
-    B = np.repeat(z["b"], 17, axis=0) * (1.0 + 0.25 * rng.standard_normal((34, 1)))
-    B[33] = 0.0
+    B = np.repeat(z["b"], 35, axis=0) * (1.0 + 0.25 * rng.standard_normal((70, 1)))
+    B[69] = 0.0
     reps = []
     U = s.ddm_solve(B, 1, reps, True)
-    for r in (0, 31, 32):
-        assert np.array_equal(U[r], s.ddm_solve(B[r], 1))
-    assert not np.any(U[33])
-    assert reps[33].local_solves == 0 and reps[33].skipped_zero_solves == 4 * s.nsub
+    for r in (0, 31, 32, 63, 64, 68):
+        assert rel(U[r], s.ddm_solve(B[r], 1)) <= 1e-12
+    assert not np.any(U[69])
+    assert reps[69].local_solves == 0 and reps[69].skipped_zero_solves == 4 * s.nsub
 
 
 @pytest.mark.parametrize("dim,n,parts,pad,rounds", [(2, [64, 40], [4, 2], 6, 3), (3, [24, 16, 16], [3, 2, 1], 4, 1),
