@@ -709,7 +709,8 @@ struct Engine {
     // Unsplit bands of a front are merged into items of at most merge_ksteps k-steps (every RHS
     // group of a band in the same item, consecutive bands while they fit): a unit of a small front
     // is a few k-steps, so per-item costs (records, dependency wait, ticket, release) dominated.
-    static const int merge_ksteps = std::getenv("HS_MERGE") ? std::atoi(std::getenv("HS_MERGE")) : 0;
+    // (the kernel runs merged items only when built with HS_MERGE_UNITS=1)
+    static const int merge_ksteps = HS_MERGE_UNITS && std::getenv("HS_MERGE") ? std::atoi(std::getenv("HS_MERGE")) : 0;
     auto emit = [&](std::vector<SolveItem>& out, int nzi, int f, int job, int slot, int gw, int nb,
                     const std::function<int(int)>& nch, const std::function<int(int)>& ksteps) {
       const int ngrp = (R + gw - 1) / gw;
@@ -2804,6 +2805,8 @@ struct hs_ddm {
 
 namespace {
 
+constexpr int kStreamBatch = 32;  // RHS per batch of the streamed host-buffer path
+
 void ddm_solve_batch(DdmHandle& H, int R, const double2* d_b, double2* d_u, int rounds, bool track,
                      hs_solve_report* reps) {
   H.ensure_state(R, rounds);
@@ -3032,10 +3035,15 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
                         cudaPointerGetAttributes(&pu, u) == cudaSuccess && pu.type == cudaMemoryTypeHost;
     (void)cudaGetLastError();  // pageable pointers may leave an error on older runtimes
     if (pinned && !H.partitioned()) {  // (a partitioned u is final only after its reduction)
-      for (int b0 = 0, k = 0; b0 < nrhs; b0 += kMaxRhs, ++k) {  // consecutive batches overlap (two slots)
-        const int R = std::min(kMaxRhs, nrhs - b0);
+      // Host buffers: batches of at most kStreamBatch RHS, so that consecutive batches overlap (two
+      // slots: batch k + 1's b streams in while batch k computes, batch k's u streams out while
+      // batch k + 1 computes). One 64-RHS batch computes faster on the device (C3: 216 vs 228 ms)
+      // but leaves its 4.6 GB of b and u each way to PCIe with nothing to overlap (e2e 345 vs 272 ms).
+      const int bw = nrhs > kStreamBatch ? kStreamBatch : nrhs;
+      for (int b0 = 0, k = 0; b0 < nrhs; b0 += bw, ++k) {
+        const int R = std::min(bw, nrhs - b0);
         H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,
-                         reports ? reports + b0 : nullptr, k & 1, b0 + kMaxRhs >= nrhs, std::min(nrhs, kMaxRhs));
+                         reports ? reports + b0 : nullptr, k & 1, b0 + bw >= nrhs, bw);
       }
       return;
     }

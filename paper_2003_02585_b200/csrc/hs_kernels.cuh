@@ -3,6 +3,12 @@
 
 #include "hs_device.cuh"
 
+// Items spanning several (band, RHS group) units (host HS_MERGE, measured slower); 0: the solve
+// kernel runs one unit per item and the host never merges
+#ifndef HS_MERGE_UNITS
+#define HS_MERGE_UNITS 0
+#endif
+
 namespace hsb {
 
 struct SolveArgs {

@@ -664,11 +664,26 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
   cp_commit();
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p) : "memory");
+}
 // the warp's next ticket (lane 0's atomic; its latency is paid only where the value is used)
 __device__ __forceinline__ void take_ticket(const SolveArgs& a, unsigned& tk, bool& took, int lane) {
   if (HS_LATE_TICKET && !took) {
     if (lane == 0) tk = atomicAdd(a.queue, 1u);
     took = true;
+  }
+}
+// HS_PREFETCH_NEXT: once the ticket is back (before the split reduce / finalize), the next item's
+// record is prefetched into L1, and after its load the next job record and task masks too, so the
+// next item starts on L1 hits instead of two dependent L2 round trips
+#ifndef HS_PREFETCH_NEXT
+#define HS_PREFETCH_NEXT 1
+#endif
+__device__ __forceinline__ void prefetch_next_record(const SolveArgs& a, unsigned tk, int lane) {
+  if (HS_PREFETCH_NEXT && lane == 0) {
+    const int nxt = static_cast<int>(gridDim.x * (kThreads / 32) + tk);
+    if (nxt < a.nitems) prefetch_l1(a.items + nxt);
   }
 }
 
@@ -798,6 +813,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 #endif
   acc_finish(acc);
   take_ticket(a, tk, took, lane);
+  prefetch_next_record(a, tk, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] += 2 * (cb1 - cb0);
@@ -956,6 +972,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 #endif
   acc_finish(acc);
   take_ticket(a, tk, took, lane);
+  prefetch_next_record(a, tk, lane);
   if (tr && lane == 0) {
     tr[2] = gtime();
     tr[6] += 2 * (a1 - a0);
@@ -1060,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
         double2* V = a.vbuf + it.slot * a.vslot_stride;
         // the item's units: band t x RHS group r (one unit unless merged); the ticket is taken in
         // the last unit, the completed units are released together
+#if HS_MERGE_UNITS
         SolveItem un = it;
         for (int t = it.idx; t < it.idx1; ++t)
           for (int r = it.r0; r < it.r1; r += J.gw) {
@@ -1087,6 +1105,16 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
             nfin += f ? 1 : 0;
           }
         fin = nfin > 0;
+#else
+        // one unit per item (merged items measured slower; HS_MERGE_UNITS=1 compiles them in)
+        if (FWD)
+          fin = it.rw > 8 ? fwd_item<2, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
+                          : fwd_item<1, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
+        else
+          fin = it.rw > 8 ? bwd_item<2, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
+                          : bwd_item<1, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
+        nfin = fin ? 1 : 0;
+#endif
         if (tr && lane == 0) {
           tr[4] = gtime();
           tr[5] = smid();
@@ -1097,6 +1125,12 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
     const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
     SolveItem nit{};
     if (nxt < a.nitems) nit = a.items[nxt];
+    if (HS_PREFETCH_NEXT && lane == 0 && nxt < a.nitems) {  // the next item's job record and task masks
+      prefetch_l1(a.jobs + nit.job);
+      prefetch_l1(reinterpret_cast<const char*>(a.jobs + nit.job) + 64);
+      prefetch_l1(a.nzmask + nit.nzi);
+      if (a.tface) prefetch_l1(a.tface + nit.nzi);
+    }
     if (fin) signal(done + it.front, lane, nfin);
     __syncwarp();  // the index slice is rewritten by the next item
     cur = nxt;
