@@ -618,7 +618,9 @@ struct Engine {
         hj[static_cast<size_t>(b) * njobs + j] = J;
       }
     jobs.upload(hj, stream);
+    jobs_h = std::move(hj);
   }
+  std::vector<SolveJob> jobs_h;  // host copy of the job records (factor addresses for item prefetch)
   // counter array: [done fwd | done bwd] per slot x front, [arrivals fwd | bwd], 2 queues
   long long cnt_ints() const {
     return 2LL * nslots * nf_max + 2LL * nslots * arr_total * ngr + 2;
@@ -719,13 +721,14 @@ struct Engine {
         if (nch(t) > 1 || merge_ksteps <= 0) {  // split band (or merging off): one item per unit
           for (int ch = 0; ch < nch(t); ++ch)
             for (int r0 = 0; r0 < R; r0 += gw)
-              out.push_back(SolveItem{nzi, f, job, t, slot, r0, std::min(gw, R - r0), ch, t + 1, r0 + std::min(gw, R - r0)});
+              out.push_back(SolveItem{nzi, f, job, t, slot, r0, std::min(gw, R - r0), ch, t + 1, r0 + std::min(gw, R - r0),
+                                      nullptr, 0u, 0});
           ++t;
           continue;
         }
         int t1 = t, ks = 0;
         while (t1 < nb && nch(t1) == 1 && (t1 == t || ks + ksteps(t1) * ngrp <= merge_ksteps)) ks += ksteps(t1++) * ngrp;
-        out.push_back(SolveItem{nzi, f, job, t, slot, 0, std::min(gw, R), 0, t1, R});
+        out.push_back(SolveItem{nzi, f, job, t, slot, 0, std::min(gw, R), 0, t1, R, nullptr, 0u, 0});
         t = t1;
       }
     };
@@ -735,8 +738,16 @@ struct Engine {
       const FrontDesc& fd = cd.sym->fronts[e.f];
       const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
       const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), nband = (nrb + 3) / 4;
+      const size_t first = fwd.size();
       emit(fwd, nzi, f, jb + f, e.g, cd.fgw[f], nband, [&](int t) { return solve_fwd_chunks(fd.m, fd.k, t, cd.fkc[f]); },
            [&](int t) { return 2 * std::min(kb, 4 * t + 4); });
+      for (size_t i = first; i < fwd.size(); ++i) {  // band t, column blocks of chunk `chunk`
+        SolveItem& it = fwd[i];
+        const int t = it.idx, rbs = std::min(4, nrb - 4 * t), kc = cd.fkc[f];
+        const int cb0 = it.chunk * kc, cb1 = std::min(std::min(kb, 4 * t + 4), cb0 + kc);
+        it.pf = jobs_h[jb + f].factor + band_base(t, kb) + static_cast<long long>(cb0) * rbs * 64;
+        it.pf_bytes = static_cast<unsigned>((cb1 - cb0) * rbs) * 1024u;
+      }
     }
     for (const Ent& e : eb) {
       const TaskRef& tk = tasks[e.g];
@@ -744,8 +755,16 @@ struct Engine {
       const FrontDesc& fd = cd.sym->fronts[e.f];
       const int f = e.f, nzi = (tk.l - 1) * nsub + tk.sub, jb = tk.xb * njobs + job_base[tk.sub];
       const int kb = pad8(fd.k) >> 3, nrb = kb + (pad8(fd.m - fd.k) >> 3), ncband = (kb + 3) / 4;
+      const size_t first = bwd.size();
       emit(bwd, nzi, f, jb + f, e.g, cd.fgw[f], ncband, [&](int u) { return solve_bwd_chunks(fd.m, fd.k, u, cd.fkr[f]); },
            [&](int u) { return 2 * (nrb - 4 * u); });
+      for (size_t i = first; i < bwd.size(); ++i) {  // column band u: its first row band's blocks
+        SolveItem& it = bwd[i];
+        const int u = it.idx, a0 = 4 * u + it.chunk * cd.fkr[f], ta = a0 >> 2;
+        const int rbs = std::min(4, nrb - 4 * ta), ncol = std::min(4, kb - 4 * u);
+        it.pf = jobs_h[jb + f].factor + band_base(ta, kb) + static_cast<long long>(4 * u) * rbs * 64;
+        it.pf_bytes = static_cast<unsigned>(ncol * rbs) * 1024u;
+      }
     }
   }
 
@@ -1174,6 +1193,11 @@ struct DdmHandle {
   bool partitioned() const { return world > 1 || ncomm != nullptr; }
   void build_xplan();
   void comm_allreduce(double* buf, long long count);
+  // u summed over ranks: an owner-slab all-gather with the native NCCL transport, else an all-reduce
+  void comm_gather_u(double2* buf);
+  long long max_home = 0, home_cnt = 0;
+  DBuf<int> d_homes;
+  DBuf<double2> gsend, grecv;
 
   ~DdmHandle() {
     drop_graphs();
@@ -1708,12 +1732,14 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
       // home rank of a node: the owner of its lowest-id subdomain; only the home rank
       // accumulates the node, reading other ranks' values from ghost copies of their x
       ghost.assign(nsub, std::vector<std::vector<long long>>(world));
+      std::vector<std::vector<int>> homes(world);
       for (long long g = 0; g < gn; ++g) {
         const int n = off[g];
         if (n == 0) continue;
         int lo = 1 << 30;
         for (int i = 0; i < n; ++i) lo = std::min(lo, raw[static_cast<size_t>(g) * E + i].y >> 4);
         const int home = owner[lo];
+        homes[home].push_back(static_cast<int>(g));
         for (int i = 0; i < n; ++i) {
           const int2 e = raw[static_cast<size_t>(g) * E + i];
           const int id = e.y >> 4;
@@ -1723,6 +1749,13 @@ void DdmHandle::build(const hs_problem& P, int device, int rank_, int world_, co
           for (int di = 0; di < ndirs; ++di)
             for (int i = 0; i < E; ++i) ent[(static_cast<size_t>(di) * gn + g) * E + i] = make_int2(-1, 0);
       }
+      // owner slabs of u for the gather (every rank holds every rank's list, padded with -1)
+      max_home = 1;
+      for (const auto& h : homes) max_home = std::max<long long>(max_home, static_cast<long long>(h.size()));
+      home_cnt = static_cast<long long>(homes[rank].size());
+      std::vector<int> hl(static_cast<size_t>(world) * max_home, -1);
+      for (int q = 0; q < world; ++q) std::copy(homes[q].begin(), homes[q].end(), hl.begin() + static_cast<size_t>(q) * max_home);
+      d_homes.upload(hl, eng.stream);
       std::vector<long long> flat;
       ghost_off.assign(static_cast<size_t>(nsub) * world + 1, 0);
       for (int id = 0; id < nsub; ++id)
@@ -2150,6 +2183,19 @@ void DdmHandle::build_xplan() {
   xrecv.alloc(rmax);
 }
 
+void DdmHandle::comm_gather_u(double2* buf) {
+  if (!ncomm || !d_homes.p) {
+    comm_allreduce(reinterpret_cast<double*>(buf), 2LL * geom.gn * R);
+    return;
+  }
+  const long long slab = max_home * R;
+  gsend.alloc(static_cast<size_t>(slab));
+  grecv.alloc(static_cast<size_t>(slab) * world);
+  launch_pack_home(buf, d_homes.p + static_cast<size_t>(rank) * max_home, home_cnt, R, gsend.p, eng.stream);
+  ncomm->allgather(reinterpret_cast<const double*>(gsend.p), reinterpret_cast<double*>(grecv.p), 2 * slab, eng.stream);
+  launch_unpack_home(grecv.p, d_homes.p, max_home, world, R, buf, eng.stream);
+}
+
 void DdmHandle::comm_allreduce(double* buf, long long count) {
   if (ncomm) {
     ncomm->allreduce(buf, count, eng.stream);
@@ -2493,7 +2539,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
           } else {
             u_reduced = true;
           }
-          comm_allreduce(reinterpret_cast<double*>(t), 2LL * geom.gn * R);
+          comm_gather_u(t);
           ures = t;
         }
         const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s);
@@ -2550,7 +2596,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
           if (track)  // residuals of the rounds before the last, on u as it stood after each of them
             for (int q = 0; q + 1 < nrounds; ++q) {
               double2* uq = uround.p + static_cast<size_t>(q) * geom.gn * R;
-              if (partitioned()) comm_allreduce(reinterpret_cast<double*>(uq), 2LL * geom.gn * R);
+              if (partitioned()) comm_gather_u(uq);
               const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s);
               launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(q) * R, s);
               launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(q) * R, s);
@@ -2563,7 +2609,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     }
   }
   if (partitioned()) {  // home-node slices of u, and the per-sweep |contribution|^2 sums
-    if (!u_reduced) comm_allreduce(reinterpret_cast<double*>(u.p), 2LL * geom.gn * R);
+    if (!u_reduced) comm_gather_u(u.p);
     comm_allreduce(norms.p, static_cast<long long>(nsweeps) * R);
   }
 }

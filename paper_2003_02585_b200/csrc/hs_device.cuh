@@ -79,6 +79,11 @@ struct DevGeom {
 struct SolveItem {
   int nzi, front, job, idx, slot, r0, rw, chunk;
   int idx1, r1;
+  // the first factor range the item streams (L2 bulk prefetch issued by the warp that dequeues it,
+  // as soon as it has the record, ahead of the item's dependency wait)
+  const void* pf;
+  unsigned pf_bytes;
+  int pad_;
 };
 
 // Everything a solve item needs about its (subdomain, front), resolved on the host for the

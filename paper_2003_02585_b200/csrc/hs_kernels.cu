@@ -815,6 +815,33 @@ __global__ void __launch_bounds__(kThreads) xpack_kernel(const XSeg* segs, bool 
   }
 }
 
+// Owner-slab gather of u (partitioned solves): each rank packs the values of its home nodes, an
+// all-gather moves the slabs, and every rank scatters all slabs into u. Every node is nonzero on
+// its home rank only, so this equals the sum over ranks bit for bit, at half an all-reduce's traffic.
+__global__ void pack_home_kernel(const double2* u, const int* list, long long count, int R, double2* out) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= count * R) return;
+  out[i] = u[static_cast<long long>(list[i / R]) * R + i % R];
+}
+__global__ void unpack_home_kernel(const double2* in, const int* lists, long long max_home, int R, double2* u) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long slab = static_cast<long long>(blockIdx.y) * max_home;
+  if (i >= max_home * R) return;
+  const int node = lists[slab + i / R];
+  if (node >= 0) u[static_cast<long long>(node) * R + i % R] = in[slab * R + i];
+}
+void launch_pack_home(const double2* u, const int* list, long long count, int R, double2* out, cudaStream_t s) {
+  if (count <= 0) return;
+  pack_home_kernel<<<blocks_for(count * R), kThreads, 0, s>>>(u, list, count, R, out);
+  after_launch();
+}
+void launch_unpack_home(const double2* in, const int* lists, long long max_home, int world, int R, double2* u,
+                        cudaStream_t s) {
+  if (max_home <= 0) return;
+  unpack_home_kernel<<<dim3(blocks_for(max_home * R), world), kThreads, 0, s>>>(in, lists, max_home, R, u);
+  after_launch();
+}
+
 void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, rmask* mpres, double2* x,
                   rmask* nzmask, const long long* gpos, int R, cudaStream_t s) {
   if (nseg <= 0) return;

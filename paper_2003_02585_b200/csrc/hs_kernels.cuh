@@ -158,6 +158,9 @@ struct XSeg {
   long long b;     // offset in the message buffer (doubles)
   long long c;     // kind 2: x buffer offset (elements)
 };
+void launch_pack_home(const double2* u, const int* list, long long count, int R, double2* out, cudaStream_t s);
+void launch_unpack_home(const double2* in, const int* lists, long long max_home, int world, int R, double2* u,
+                        cudaStream_t s);
 void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* mbox, rmask* mpres, double2* x,
                   rmask* nzmask, const long long* gpos, int R, cudaStream_t s);
 

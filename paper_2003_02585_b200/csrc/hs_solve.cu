@@ -242,6 +242,69 @@ __device__ __forceinline__ void mma_step(Acc<NT, M3>& c, const double2 (&A)[4], 
   }
 }
 
+// One k-step over the m-tiles [LO, HI) only, unpredicated (a per-tile predicate puts a warp barrier
+// and a NOP in front of every DMMA: ncu showed the masked k-steps -- 63% of the backward's on C3,
+// the diagonal block rows of every chunk-0 item and the short last column bands -- dominated the
+// loop's fixed-latency stalls).
+template <bool NEG, int LO, int HI, int NT, bool M3>
+__device__ __forceinline__ void mma_range(Acc<NT, M3>& c, const double2 (&A)[4], const double2 (&B)[NT]) {
+  if constexpr (M3) {
+    double bx[NT], by[NT], bs[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      bx[q] = NEG ? -B[q].x : B[q].x;
+      by[q] = NEG ? -B[q].y : B[q].y;
+      bs[q] = bx[q] + by[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int i = LO; i < HI; ++i) {
+        const double as = A[i].x + A[i].y;
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, by[q]);
+        dmma(c.v[i][q][Acc<NT, M3>::P - 1][0], c.v[i][q][Acc<NT, M3>::P - 1][1], as, bs[q]);
+      }
+  } else {
+    double bx[NT], by[NT], nby[NT];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      bx[q] = NEG ? -B[q].x : B[q].x;
+      by[q] = NEG ? -B[q].y : B[q].y;
+      nby[q] = NEG ? B[q].y : -B[q].y;
+    }
+#pragma unroll
+    for (int q = 0; q < NT; ++q)
+#pragma unroll
+      for (int i = LO; i < HI; ++i) {
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].x, bx[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].x, by[q]);
+        dmma(c.v[i][q][0][0], c.v[i][q][0][1], A[i].y, nby[q]);
+        dmma(c.v[i][q][1][0], c.v[i][q][1][1], A[i].y, bx[q]);
+      }
+  }
+}
+// A tile mask of the lean k-loops is always a contiguous range of m-tiles (backward: a prefix,
+// forward: a suffix); dispatch it to the unpredicated range step.
+template <bool NEG, int NT, bool M3>
+__device__ __forceinline__ void mma_masked(Acc<NT, M3>& c, const double2 (&A)[4], const double2 (&B)[NT], unsigned mk) {
+  if (!mk) return;
+  const int lo = __ffs(mk) - 1, hi = 32 - __clz(mk);
+  switch (lo * 8 + hi) {
+    case 0 * 8 + 1: mma_range<NEG, 0, 1>(c, A, B); break;
+    case 0 * 8 + 2: mma_range<NEG, 0, 2>(c, A, B); break;
+    case 0 * 8 + 3: mma_range<NEG, 0, 3>(c, A, B); break;
+    case 0 * 8 + 4: mma_range<NEG, 0, 4>(c, A, B); break;
+    case 1 * 8 + 2: mma_range<NEG, 1, 2>(c, A, B); break;
+    case 1 * 8 + 3: mma_range<NEG, 1, 3>(c, A, B); break;
+    case 1 * 8 + 4: mma_range<NEG, 1, 4>(c, A, B); break;
+    case 2 * 8 + 3: mma_range<NEG, 2, 3>(c, A, B); break;
+    case 2 * 8 + 4: mma_range<NEG, 2, 4>(c, A, B); break;
+    case 3 * 8 + 4: mma_range<NEG, 3, 4>(c, A, B); break;
+    default: mma_step<NEG, false>(c, A, B, mk); break;  // (never: masks are contiguous)
+  }
+}
+
 // Split-K: store this chunk's partial, and if it arrived last, replace acc by the sum of all
 // chunks in chunk order (read back from memory, own partial included). Returns whether this
 // warp finalizes the band.
@@ -507,7 +570,7 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
       mma_step<false, true>(acc, A, B, 0xFu);
     } else {  // diagonal column blocks (M's zero blocks above the diagonal) or a short last band
       const int d = min(max(dshift + (s >> 1), 0), 4);
-      mma_step<false, false>(acc, A, B, mbase & ~(msep & ((1u << d) - 1u)));
+      mma_masked<false>(acc, A, B, mbase & ~(msep & ((1u << d) - 1u)));
     }
   }
   cp_wait<0>();
@@ -593,9 +656,9 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
       unsigned mk = mcol;
       if (ab < kb) mk &= (1u << min(max(ab - 4 * u + 1, 0), 4)) - 1u;
       if (s >= ssep)
-        mma_step<true, false>(acc, A, B, mk);
+        mma_masked<true>(acc, A, B, mk);
       else
-        mma_step<false, false>(acc, A, B, mk);
+        mma_masked<false>(acc, A, B, mk);
     }
   }
   cp_wait<0>();
@@ -674,11 +737,16 @@ __device__ __forceinline__ void take_ticket(const SolveArgs& a, unsigned& tk, bo
     took = true;
   }
 }
-// HS_PREFETCH_NEXT: once the ticket is back (before the split reduce / finalize), the next item's
+// HS_PREFETCH_NEXT (measured neutral on C3, off): once the ticket is back (before the split reduce / finalize), the next item's
 // record is prefetched into L1, and after its load the next job record and task masks too, so the
 // next item starts on L1 hits instead of two dependent L2 round trips
 #ifndef HS_PREFETCH_NEXT
-#define HS_PREFETCH_NEXT 1
+#define HS_PREFETCH_NEXT 0
+#endif
+// HS_NEXT_L2 (measured 3% slower on C3, off): the next item's first factor range prefetched to L2
+// as soon as its record is known
+#ifndef HS_NEXT_L2
+#define HS_NEXT_L2 0
 #endif
 __device__ __forceinline__ void prefetch_next_record(const SolveArgs& a, unsigned tk, int lane) {
   if (HS_PREFETCH_NEXT && lane == 0) {
@@ -1125,6 +1193,9 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
     const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
     SolveItem nit{};
     if (nxt < a.nitems) nit = a.items[nxt];
+    // the next item's first factor range toward L2 now, ahead of this item's release and the next
+    // item's record loads and dependency wait (HS_NEXT_L2)
+    if (HS_NEXT_L2 && lane == 0 && nxt < a.nitems && nit.pf_bytes) prefetch_l2(nit.pf, nit.pf_bytes);
     if (HS_PREFETCH_NEXT && lane == 0 && nxt < a.nitems) {  // the next item's job record and task masks
       prefetch_l1(a.jobs + nit.job);
       prefetch_l1(reinterpret_cast<const char*>(a.jobs + nit.job) + 64);

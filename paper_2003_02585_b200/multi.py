@@ -16,6 +16,7 @@ Two ways to spread the DDM hot path over ranks:
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -113,8 +114,27 @@ def exchange_host(send: np.ndarray, recv: np.ndarray, peers, soff, scnt, roff, r
         r.wait()
 
 
+def _same_nccl_as_torch():
+    """Point the library's dlopen at the libnccl PyTorch links (the nvidia-nccl wheel) unless the
+    caller chose one (HS_NCCL_LIB): a process holds one object per soname, so loading the system
+    libnccl.so.2 first would leave a later `import torch` bound to a different, older build."""
+    if os.environ.get("HS_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["HS_NCCL_LIB"] = cand
+            return
+
+
 def nccl_unique_id() -> bytes:
     """128-byte ncclUniqueId from the library's own NCCL binding (hs_nccl_unique_id)."""
+    _same_nccl_as_torch()
     buf = (ctypes.c_ubyte * 128)()
     rc = L.lib().hs_nccl_unique_id(buf)
     if rc:
@@ -123,6 +143,7 @@ def nccl_unique_id() -> bytes:
 
 
 def nccl_version() -> int:
+    _same_nccl_as_torch()
     v = ctypes.c_int()
     rc = L.lib().hs_nccl_version(ctypes.byref(v))
     if rc:
@@ -144,6 +165,7 @@ class NcclDdmSolver(DdmSolver):
         super().__init__(setup, device)
 
     def _create(self, p, device, h, sub, piv):
+        _same_nccl_as_torch()
         return L.lib().hs_ddm_create_nccl(ctypes.byref(p), device, self._rank, self._world, self._owner, self._uid,
                                           ctypes.byref(h), ctypes.byref(sub), ctypes.byref(piv))
 
