@@ -476,6 +476,7 @@ struct Engine {
   // Solve buffers for R right-hand sides and up to `slots` concurrently solved subdomains,
   // and the split-K bookkeeping of every front (arrival counters, partial tiles).
   long long gen = 0;  // bumped whenever solve buffers are (re)allocated (captured graphs go stale)
+  bool quad = false;  // item lists in null-padded quads of RHS groups (one CTA dequeue each)
   void ensure_solve(int r, int slots, int nb = 1) {
     if (r == R && slots <= nslots && nb == nbuf) return;
     ++gen;
@@ -507,6 +508,10 @@ struct Engine {
     // chunks are never wider than 16 blocks, which bounds the 3D top fronts' count from below
     max_chunks = dim == 3 ? 4 : 16;
     if (const char* e = std::getenv("HS_MAX_CHUNKS")) max_chunks = std::max(1, std::atoi(e));
+    // quads: with four or more RHS groups per band chunk, one CTA takes the groups of a chunk
+    // together and its warps share the factor tiles through L1 (hs_solve.cu QUAD)
+    quad = r >= 49;
+    if (const char* e = std::getenv("HS_QUAD")) quad = std::atoi(e) != 0;
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;
@@ -719,10 +724,15 @@ struct Engine {
       int t = 0;
       while (t < nb) {
         if (nch(t) > 1 || merge_ksteps <= 0) {  // split band (or merging off): one item per unit
-          for (int ch = 0; ch < nch(t); ++ch)
+          for (int ch = 0; ch < nch(t); ++ch) {
             for (int r0 = 0; r0 < R; r0 += gw)
               out.push_back(SolveItem{nzi, f, job, t, slot, r0, std::min(gw, R - r0), ch, t + 1, r0 + std::min(gw, R - r0),
                                       nullptr, 0u, 0});
+            while (quad && (out.size() & 3)) {  // null items (nzi < 0) fill the chunk's last quad
+              out.push_back(out.back());
+              out.back().nzi = -1;
+            }
+          }
           ++t;
           continue;
         }
@@ -791,6 +801,7 @@ struct Engine {
     // 3M products (3 CTAs per SM) unless HS_M3=0: C2 12.5 vs 12.8 ms, C5 0.384 vs 0.394 s
     static const int m3env = std::getenv("HS_M3") ? std::atoi(std::getenv("HS_M3")) : 1;
     a.m3 = m3env != 0;
+    a.quad = quad ? 1 : 0;
     a.need = need;
     a.need_words = need_words;
     a.nsub = static_cast<int>(sub_cls.size());
@@ -826,6 +837,7 @@ struct Engine {
         std::fprintf(fp, "pass,sub,front,kind,idx,chunk,r0,rw,t_deq,t_ready,t_loop,t_red,t_done,sm,nsteps,k,m\n");
         for (int i = 0; i < nfwd + nbwd; ++i) {
           const SolveItem& it = items[i];
+          if (it.nzi < 0) continue;  // quad padding
           const int sub = it.nzi % static_cast<int>(sub_cls.size());
           const FrontDesc& fd = classes[sub_cls[sub]]->sym->fronts[it.front];
           const unsigned long long* q = &h[8 * i];

@@ -29,8 +29,10 @@ struct SolveArgs {
   long long vslot_stride;  // elements per slot
   const rmask* nzmask;     // per subdomain: RHS columns with a nonzero right-hand side
   const unsigned* tface;   // per task: faces with nonzero injected data, 0x100 = every front live
-  int m3;                  // complex products as 3 real DMMAs (3 CTAs / SM) instead of 4 (4 CTAs / SM)
                            // (sweep 1); null = every front live
+  int quad;                // items are listed in quads (four RHS groups of one band chunk, null-padded,
+                           // nzi < 0) that one CTA dequeues together and streams through L1
+  int m3;                  // complex products as 3 real DMMAs (3 CTAs / SM) instead of 4 (4 CTAs / SM)
   const unsigned* need;    // per subdomain bitset over fronts: x read back (backward pass); null = all
   int need_words;          // 32-bit words per subdomain in `need`
   int nsub;                // subdomains (task index nzi = (sweep - 1) * nsub + sub)

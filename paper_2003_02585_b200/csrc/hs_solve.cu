@@ -366,10 +366,18 @@ __device__ __forceinline__ void cp16z(double2* dst, const void* src, bool ok) {
                "l"(src), "r"(ok ? 16 : 0)
                : "memory");
 }
+// CA: the copy allocates in L1 (factor tiles of a quad: the CTA's four warps stream the same band
+// chunk for four RHS groups, so three of the four reads hit L1 instead of going to L2)
+template <bool CA = false>
 __device__ __forceinline__ void cp16a(double2* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
+  if (CA)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
 }
 __device__ __forceinline__ void cp16(double2* dst, const double2* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
@@ -501,7 +509,7 @@ __device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, I
 //   vr    update-vector slot base at RHS r0 + lane/4 (bytes); rows from the staged source map
 //   kcnt  k-steps whose column (col0 + 4 s) lies below k for this lane
 //   okq   bit q: RHS r0 + 8q + lane/4 exists
-template <int NT, bool M3, bool LEAF>
+template <int NT, bool M3, bool LEAF, bool CA>
 __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* ring, int lane, const char* pa,
                                           unsigned astep, unsigned toff1, unsigned toff2, unsigned toff3,
                                           const char* xr, unsigned xstep, int kcnt, const char* vr, unsigned R16,
@@ -515,10 +523,10 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   const int2* sx = sidx + (lane & 3);
   auto issue = [&]() {
     double2* st = wslot + lane;
-    cp16a(st, pa);
-    cp16a(st + 32, pa + toff1);
-    cp16a(st + 64, pa + toff2);
-    cp16a(st + 96, pa + toff3);
+    cp16a<CA>(st, pa);
+    cp16a<CA>(st + 32, pa + toff1);
+    cp16a<CA>(st + 64, pa + toff2);
+    cp16a<CA>(st + 96, pa + toff3);
     const bool okc = si < kcnt;
     double2* sb = st + 4 * 32;
     if (LEAF) {
@@ -580,7 +588,7 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]. Row band ta = a0/4 + s/8 holds the
 // k-step's rows; its column blocks 4u..4u+3 are the m-tiles (stride rbs(ta) KB, tiles past the
 // front's column blocks re-read tile 0 and are discarded).
-template <int NT, bool M3>
+template <int NT, bool M3, bool CA>
 __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* ring, int lane, const double2* P,
                                           int kb, int nrb, int u, int a0, int cn, const char* zr, const char* XR,
                                           unsigned R16, int row0, int k, int kp, int nb, bool zlive, unsigned okq,
@@ -610,10 +618,10 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
     }
     double2* st = wslot + lane;
     const char* p = pa + (si & 7) * 512;
-    cp16a(st, p);
-    cp16a(st + 32, p + t1);
-    cp16a(st + 64, p + t2);
-    cp16a(st + 96, p + t3);
+    cp16a<CA>(st, p);
+    cp16a<CA>(st + 32, p + t1);
+    cp16a<CA>(st + 64, p + t2);
+    cp16a<CA>(st + 96, p + t3);
     const int row = row0 + 4 * si;
     const char* src;
     bool okb;
@@ -691,10 +699,10 @@ __device__ __forceinline__ BwdRange bwd_range(const SolveJob& J, const Geo& g, c
 // index slice -> shared memory (cp.async group, waited for after the dependency wait).
 template <bool FWD>
 __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it,
-                                              int2* sidx, int lane) {
+                                              int2* sidx, int lane, bool pf_l2 = true) {
   if (FWD) {
     const FwdRange r = fwd_range(J, g, it);
-    if (lane == 0)
+    if (lane == 0 && pf_l2)
       prefetch_l2(J.factor + band_base(r.t, g.kb) + r.cb0 * r.rbs * 64,
                   static_cast<unsigned>((r.cb1 - r.cb0) * r.rbs) * 1024u);
     const bool leaf = J.child0 < 0 && J.child1 < 0;
@@ -714,7 +722,7 @@ __device__ __forceinline__ void item_prefetch(const SolveArgs& a, const SolveJob
     if (pr < J.k) cp_small<16>(fdv + lane, J.dinv + pr);
   } else {
     const BwdRange r = bwd_range(J, g, it);
-    if (lane == 0) {
+    if (lane == 0 && pf_l2) {
       const int ncol = min(4, g.kb - 4 * r.u);
       for (int ta = r.a0 >> 2; ta <= (r.a1 - 1) >> 2; ++ta) {
         const int rbs = min(4, g.nrb - 4 * ta);
@@ -761,7 +769,7 @@ __device__ __forceinline__ void prefetch_next_record(const SolveArgs& a, unsigne
 // children's updates at the front's boundary, in the reference's child order), loaded while the
 // k-loop's first stages are in flight, so the finalize only scales and stores. Returns whether
 // this warp finalized the band (the caller signals it).
-template <int NT, bool M3>
+template <int NT, bool M3, bool CA>
 __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, double2* V,
                          int lane, double2* ring, const int2* sidx, unsigned long long* tr, unsigned clive,
                          unsigned& tk, bool& took) {
@@ -870,10 +878,10 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     // k-steps before the diagonal column blocks run every m-tile (when the band is full)
     const int sfull = mbase == 0xFu ? max(0, 2 * (4 * t - cb0)) : 0;
     if (!c0 && !c1)
-      fwd_kloop<NT, M3, true>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
+      fwd_kloop<NT, M3, true, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                               sidx, false, false, okq, sfull, mbase, msep, cb0 - 4 * t);
     else
-      fwd_kloop<NT, M3, false>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
+      fwd_kloop<NT, M3, false, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                                sidx, c0, c1, okq, sfull, mbase, msep, cb0 - 4 * t);
   }
 #else
@@ -950,7 +958,7 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
 // ---------------------------------------------------------------------------------------
 // backward column-band item: x_sep[32 cols][8 NT RHS] = sum over the chunk's rows of
 // [M; W][rows, band cols]^T y[rows], y = [z_sep; 0; -x_bnd]
-template <int NT, bool M3>
+template <int NT, bool M3, bool CA>
 __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane,
                          double2* ring, const int2* sidx, unsigned long long* tr, bool zlive, unsigned& tk,
                          bool& took) {
@@ -1031,7 +1039,7 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     // them when the column band is short
     const int ns = 2 * (a1 - a0);
     const int smask = mcol == 0xFu ? max(0, 2 * (4 * u + 3 - a0)) : ns;
-    bwd_kloop<NT, M3>(acc, ns, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
+    bwd_kloop<NT, M3, CA>(acc, ns, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
                       ZR + static_cast<size_t>(static_cast<unsigned>(row0)) * R16, XR, R16, row0, J.k, g.kp, nb, zlive,
                       okq, sidx, smask, mcol);
   }
@@ -1084,9 +1092,16 @@ __device__ __forceinline__ Geo geo_km(int k, int m) {
 #ifndef HS_MINB_M3
 #define HS_MINB_M3 3  // CTAs per SM the 3M kernels are register-budgeted for (tuning experiments)
 #endif
-template <bool FWD, bool M3>
+// QUAD: the CTA dequeues four consecutive items at a time (one ticket, taken by warp 0), which the
+// host lists as the RHS groups of one (band, chunk) -- padded with null items to a multiple of
+// four. Its warps then stream the same factor tiles at about the same time and the A copies
+// allocate in L1 (cp.async.ca), so the tiles cross the L2 -> SM path once per quad instead of once
+// per RHS group (ncu, C3 64 RHS: the per-warp loads ran L2 at 74% of its throughput with DRAM at
+// 22% and the DMMA pipe at 30%).
+template <bool FWD, bool M3, bool QUAD>
 __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(SolveArgs a) {
   extern __shared__ __align__(16) double2 smem_ring[];
+  __shared__ unsigned s_next[2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2* ring = smem_ring + warp * RingArea<FWD>::kWarp;
   int2* sidx = reinterpret_cast<int2*>(ring + RingArea<FWD>::kRing);
@@ -1098,20 +1113,22 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
   // band). A held ticket is always above its holder's current item, so the lowest current item
   // can always finish: no deadlock.
   const int nstatic = gridDim.x * (kThreads / 32);
-  int cur = blockIdx.x + warp * gridDim.x;
+  int cur = QUAD ? 4 * static_cast<int>(blockIdx.x) + warp : blockIdx.x + warp * gridDim.x;
+  int par = 0;
   SolveItem it{};
   if (cur < a.nitems) it = a.items[cur];
-  while (cur < a.nitems) {
+  while (cur < a.nitems) {  // (QUAD: the list is a multiple of four long, so the CTA's warps leave together)
     unsigned tk = 0;
-    bool took = !HS_LATE_TICKET;
-    if (!HS_LATE_TICKET && lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
+    bool took = !HS_LATE_TICKET || (QUAD && warp != 0);
+    if (!HS_LATE_TICKET && (!QUAD || warp == 0) && lane == 0) tk = atomicAdd(a.queue, 1u);  // the next ticket
     bool fin = false;
     int nfin = 0;
     int* done = a.done + static_cast<long long>(it.slot) * a.nf_max;
     // the item's task and front records, loaded together (all are read-only during the launch)
-    const rmask nzm = __ldg(a.nzmask + it.nzi);
-    const unsigned fm = a.tface ? __ldg(a.tface + it.nzi) : kAllLive;  // kAllLive: sweep 1 (split source)
-    const SolveJob J = a.jobs[it.job];
+    const bool null_item = QUAD && it.nzi < 0;  // padding of a quad
+    const rmask nzm = null_item ? 0 : __ldg(a.nzmask + it.nzi);
+    const unsigned fm = null_item ? 0u : a.tface ? __ldg(a.tface + it.nzi) : kAllLive;  // kAllLive: sweep 1 (split source)
+    const SolveJob J = a.jobs[null_item ? 0 : it.job];
     if (nzm != 0) {  // else: skipped task (exactly-zero RHS), nothing depends on it
       unsigned long long* tr = a.trace ? a.trace + 8LL * cur : nullptr;
       if (tr && lane == 0) tr[0] = gtime();
@@ -1132,7 +1149,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
       if (FWD ? live : needed) {
         const unsigned clive = (all || ((act >> 8) & fm & 0xFFu) ? 1u : 0u) | (all || ((act >> 16) & fm & 0xFFu) ? 2u : 0u);
         const Geo g = geo_km(J.k, J.m);
-        item_prefetch<FWD>(a, J, g, it, sidx, lane);
+        item_prefetch<FWD>(a, J, g, it, sidx, lane, !QUAD || warp == 0);  // (a quad shares the factor range)
         if (FWD) {
           if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
           if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
@@ -1164,11 +1181,11 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
             bool f;
             const SolveJob& Ju = J;
             if (FWD)
-              f = un.rw > 8 ? fwd_item<2, M3>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku)
-                            : fwd_item<1, M3>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku);
+              f = un.rw > 8 ? fwd_item<2, M3, QUAD>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku)
+                            : fwd_item<1, M3, QUAD>(a, Ju, g, un, V, lane, ring, sidx, tr, clive, tk, tku);
             else
-              f = un.rw > 8 ? bwd_item<2, M3>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku)
-                            : bwd_item<1, M3>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku);
+              f = un.rw > 8 ? bwd_item<2, M3, QUAD>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku)
+                            : bwd_item<1, M3, QUAD>(a, Ju, g, un, lane, ring, sidx, tr, live, tk, tku);
             if (lastu) took = tku;
             nfin += f ? 1 : 0;
           }
@@ -1176,11 +1193,11 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
 #else
         // one unit per item (merged items measured slower; HS_MERGE_UNITS=1 compiles them in)
         if (FWD)
-          fin = it.rw > 8 ? fwd_item<2, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
-                          : fwd_item<1, M3>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
+          fin = it.rw > 8 ? fwd_item<2, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
+                          : fwd_item<1, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
         else
-          fin = it.rw > 8 ? bwd_item<2, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
-                          : bwd_item<1, M3>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
+          fin = it.rw > 8 ? bwd_item<2, M3, QUAD>(a, J, g, it, lane, ring, sidx, tr, live, tk, took)
+                          : bwd_item<1, M3, QUAD>(a, J, g, it, lane, ring, sidx, tr, live, tk, took);
         nfin = fin ? 1 : 0;
 #endif
         if (tr && lane == 0) {
@@ -1190,7 +1207,17 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
       }
     }
     if (!took && lane == 0) tk = atomicAdd(a.queue, 1u);  // skipped item: no k-loop to overlap
-    const int nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
+    int nxt;
+    if (QUAD) {  // warp 0's ticket names the CTA's next quad
+      if (fin) signal(done + it.front, lane, nfin);
+      fin = false;
+      if (warp == 0 && lane == 0) s_next[par] = tk;
+      __syncthreads();
+      nxt = nstatic + 4 * static_cast<int>(s_next[par]) + warp;
+      par ^= 1;
+    } else {
+      nxt = nstatic + static_cast<int>(__shfl_sync(0xffffffffu, tk, 0));
+    }
     SolveItem nit{};
     if (nxt < a.nitems) nit = a.items[nxt];
     // the next item's first factor range toward L2 now, ahead of this item's release and the next
@@ -1226,21 +1253,21 @@ constexpr size_t ring_bytes() {
   return static_cast<size_t>(kThreads / 32) * RingArea<FWD>::kWarp * sizeof(double2);
 }
 
-template <bool FWD, bool M3>
+template <bool FWD, bool M3, bool QUAD>
 int solve_grid() {
   static PerDevice grid;  // per device: the attribute opt-in and the co-resident grid size
   return grid.get([](int dev) {
     int sms = 0, per = 0;
     HS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HS_CUDA(cudaFuncSetAttribute(solve6_kernel<FWD, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<FWD>()));
-    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<FWD, M3>, kThreads, ring_bytes<FWD>()));
+    HS_CUDA(cudaFuncSetAttribute(solve6_kernel<FWD, M3, QUAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes<FWD>()));
+    HS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, solve6_kernel<FWD, M3, QUAD>, kThreads, ring_bytes<FWD>()));
     return sms * std::max(per, 1);
   });
 }
 
-template <bool FWD, bool M3>
+template <bool FWD, bool M3, bool QUAD>
 void launch_solve_t(const SolveArgs& a, cudaStream_t s) {
-  const int g = std::max(1, std::min(solve_grid<FWD, M3>(), (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
+  const int g = std::max(1, std::min(solve_grid<FWD, M3, QUAD>(), (a.nitems + kThreads / 32 - 1) / (kThreads / 32)));
   // Cooperative launch: the whole grid is co-resident, which the static first round relies on
   // (a static item of a CTA that is not yet resident could otherwise be waited for by every
   // resident warp, e.g. while another stream's kernel holds part of the GPU).
@@ -1254,14 +1281,21 @@ void launch_solve_t(const SolveArgs& a, cudaStream_t s) {
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<FWD, M3>, a));
+  HS_CUDA(cudaLaunchKernelEx(&cfg, solve6_kernel<FWD, M3, QUAD>, a));
 }
 
 void launch_solve(const SolveArgs& a, bool fwd, cudaStream_t s) {
-  if (fwd)
-    a.m3 ? launch_solve_t<true, true>(a, s) : launch_solve_t<true, false>(a, s);
-  else
-    a.m3 ? launch_solve_t<false, true>(a, s) : launch_solve_t<false, false>(a, s);
+  if (a.quad && (a.nitems & 3)) throw Error(kInternal, "quad item list not a multiple of four");
+  if (a.quad) {
+    if (fwd)
+      a.m3 ? launch_solve_t<true, true, true>(a, s) : launch_solve_t<true, false, true>(a, s);
+    else
+      a.m3 ? launch_solve_t<false, true, true>(a, s) : launch_solve_t<false, false, true>(a, s);
+  } else if (fwd) {
+    a.m3 ? launch_solve_t<true, true, false>(a, s) : launch_solve_t<true, false, false>(a, s);
+  } else {
+    a.m3 ? launch_solve_t<false, true, false>(a, s) : launch_solve_t<false, false, false>(a, s);
+  }
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   HS_CUDA(cudaGetLastError());
 }
