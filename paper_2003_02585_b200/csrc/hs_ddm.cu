@@ -508,10 +508,12 @@ struct Engine {
     // chunks are never wider than 16 blocks, which bounds the 3D top fronts' count from below
     max_chunks = dim == 3 ? 4 : 16;
     if (const char* e = std::getenv("HS_MAX_CHUNKS")) max_chunks = std::max(1, std::atoi(e));
-    // quads: with four or more RHS groups per band chunk, one CTA takes the groups of a chunk
-    // together and its warps share the factor tiles through L1 (hs_solve.cu QUAD)
-    quad = r >= 49;
-    if (const char* e = std::getenv("HS_QUAD")) quad = std::atoi(e) != 0;
+    // quads (HS_QUAD=1, off): one CTA takes the RHS groups of a band chunk together and its warps
+    // share the factor tiles through L1 (hs_solve.cu QUAD). C3, 64 RHS: 198 -> 176 ms while the
+    // ring's cp.async bank conflicts made L1 / L2 throughput the bound; with conflict-free ring
+    // slots the per-warp dequeue runs 154 ms and quads 168 ms (CTA barrier per item)
+    quad = false;
+    if (const char* e = std::getenv("HS_QUAD")) quad = std::atoi(e) != 0 && r > 8;
     nslots = std::max(slots, nslots);
     arr_total = 0;
     part_total = 0;

@@ -501,6 +501,14 @@ __device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, I
 #define HS_TB_START 0
 #endif
 
+// Ring slot of a lane whose copy shares a 128-byte global line with the lanes of equal lane % 4
+// (B rows: 8 RHS of one row; the backward's A: 8 columns of one block row). cp.async writes shared
+// memory line by line as the data returns, so with slot = lane those 8 lanes (64 bytes apart) hit
+// two bank groups four deep (ncu: 109 M of the backward's 208 M shared wavefronts were LDGSTS
+// bank conflicts). Slot (lane % 4) * 8 + ((lane / 4 + 2 (lane % 4)) % 8) keeps a line's 8 lanes on
+// 8 distinct 16-byte bank groups and so does each quarter warp of the read-back.
+__device__ __forceinline__ int ring_slot(int lane) { return (lane & 3) * 8 + (((lane >> 2) + 2 * (lane & 3)) & 7); }
+
 // Forward band item: out[32 band rows][8 NT RHS] += [M; W][rows, chunk cols] * T_sep[chunk cols],
 // T = rhs + child0 V + child1 V summed at use in the reference's child order.
 //   pa    this lane's A address for k-step 0, m-tile 0 (bytes)
@@ -521,6 +529,7 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   double2* rslot = ring;
   int si = 0;
   const int2* sx = sidx + (lane & 3);
+  const int pl = ring_slot(lane);  // B parts (the A fragments of a block row are 64 contiguous bytes per lane quad)
   auto issue = [&]() {
     double2* st = wslot + lane;
     cp16a<CA>(st, pa);
@@ -528,7 +537,7 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
     cp16a<CA>(st + 64, pa + toff2);
     cp16a<CA>(st + 96, pa + toff3);
     const bool okc = si < kcnt;
-    double2* sb = st + 4 * 32;
+    double2* sb = wslot + 4 * 32 + pl;
     if (LEAF) {
 #pragma unroll
       for (int q = 0; q < NT; ++q) cp16z(sb + q * 32, xr + q * 128, okc && ((okq >> q) & 1u));
@@ -563,11 +572,12 @@ __device__ __forceinline__ void fwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
     double2 A[4], B[NT];
 #pragma unroll
     for (int i = 0; i < 4; ++i) A[i] = st[i * 32];
+    const double2* sb = rslot + pl;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      double2 v = st[(4 + q) * 32];
+      double2 v = sb[(4 + q) * 32];
       if (!LEAF) {
-        const double2 w0 = st[(4 + NT + q) * 32], w1 = st[(4 + 2 * NT + q) * 32];
+        const double2 w0 = sb[(4 + NT + q) * 32], w1 = sb[(4 + 2 * NT + q) * 32];
         v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
         v = make_double2(v.x + w1.x, v.y + w1.y);
       }
@@ -598,6 +608,7 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   double2* wslot = ring;
   double2* rslot = ring;
   const unsigned zstep = 4u * R16;
+  const int pl = ring_slot(lane);
   const int ssep = 2 * (kb - a0);  // k-steps over separator rows (z); the rest are boundary rows
   // A front the forward pass skipped (structurally zero right-hand side) has z = 0: its separator
   // rows contribute nothing, so the item starts at its first boundary row (x_sep = -W^T x_bnd).
@@ -616,7 +627,7 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
       t2 = cn > 2 ? 2u * ts : 0u;
       t3 = cn > 3 ? 3u * ts : 0u;
     }
-    double2* st = wslot + lane;
+    double2* st = wslot + pl;
     const char* p = pa + (si & 7) * 512;
     cp16a<CA>(st, p);
     cp16a<CA>(st + 32, p + t1);
@@ -647,7 +658,7 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
     if (s + NS - 1 < ns) issue();
     cp_commit();
     cp_wait<NS - 1>();
-    const double2* st = rslot + lane;
+    const double2* st = rslot + pl;
     double2 A[4], B[NT];
 #pragma unroll
     for (int i = 0; i < 4; ++i) A[i] = st[i * 32];
