@@ -438,7 +438,8 @@ struct Ring {
 template <bool FWD>
 struct RingArea {
   static constexpr int a1 = Ring<FWD, 1>::NS * Ring<FWD, 1>::kStage, a2 = Ring<FWD, 2>::NS * Ring<FWD, 2>::kStage;
-  static constexpr int kRing = a1 > a2 ? a1 : a2;
+  static constexpr int kRing1 = a1 > a2 ? a1 : a2;
+  static constexpr int kRing = kRing1 > 1024 ? kRing1 : 1024;  // >= kRing2, the block-granular loops' two block stages
   static constexpr int kFin = FWD ? 32 / 2 + 32 : 0;
   static constexpr int kWarp = kRing + kIdx / 2 + kFin;
 };
@@ -683,6 +684,249 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
   cp_wait<0>();
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Block-granular k-loops (HS_KLOOP2, default). ncu on the lean loops above (C3, 64 RHS): 263
+// instructions per k-step for 24 DMMAs -- under the 168-register cap the compiler rematerialises
+// the lane-derived addresses, the ring pointers and the tile masks in every k-step (S2R, BREV /
+// FLO / BRX mask dispatch, 64-bit pointer selects), and a warp's k-step takes ~1900 cycles against
+// 384 cycles of DMMA issue. Here the loop unit is a column block (forward) / block row (backward) =
+// 2 k-steps: the ring holds two block stages (2 x 2 k-steps x 4 KB per warp), a block's copies are
+// one cp.async group issued one block ahead, the tile range [lo, hi) of a block is dispatched
+// once to an unpredicated body, and the loop carries only pointers that advance by constants.
+// The forward's three-part stages (rhs + two child update vectors) at 16 RHS need 5 KB per k-step
+// and keep the k-step-granular loop above.
+#ifndef HS_KLOOP2
+#define HS_KLOOP2 1
+#endif
+constexpr int kSt2 = 256;          // double2 per k-step stage (4 KB): A tiles at i * 32, B parts at 128 + j * 32
+constexpr int kRing2 = 4 * kSt2;   // two block stages
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void cpa(unsigned s, const char* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpz(unsigned s, const char* g, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(g), "r"(ok ? 16 : 0) : "memory");
+}
+
+// both k-steps of a staged block over the m-tiles [LO, HI); NB = 3: B = rhs + child0 V + child1 V
+template <bool NEG, int LO, int HI, int NT, bool M3, int NB>
+__device__ __forceinline__ void block_mma(Acc<NT, M3>& acc, const double2* sA, const double2* sB) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 A[4], B[NT];
+#pragma unroll
+    for (int i = LO; i < HI; ++i) A[i] = sA[h * kSt2 + i * 32];
+#pragma unroll
+    for (int q = 0; q < NT; ++q) {
+      double2 v = sB[h * kSt2 + q * 32];
+      if (NB == 3) {
+        const double2 w0 = sB[h * kSt2 + (NT + q) * 32], w1 = sB[h * kSt2 + (2 * NT + q) * 32];
+        v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
+        v = make_double2(v.x + w1.x, v.y + w1.y);
+      }
+      B[q] = v;
+    }
+    mma_range<NEG, LO, HI>(acc, A, B);
+  }
+}
+// tile ranges of the two passes: the backward's are prefixes [0, hi), the forward's suffixes
+// [lo, 4) or, in a short last band, prefixes; anything else (a short last band that also crosses
+// the diagonal) takes the predicated step
+template <bool NEG, int NT, bool M3, int NB>
+__device__ __forceinline__ void block_dispatch(Acc<NT, M3>& acc, const double2* sA, const double2* sB, int lo, int hi) {
+  if (lo == 0) {
+    if (hi == 4)
+      block_mma<NEG, 0, 4, NT, M3, NB>(acc, sA, sB);
+    else if (hi == 3)
+      block_mma<NEG, 0, 3, NT, M3, NB>(acc, sA, sB);
+    else if (hi == 2)
+      block_mma<NEG, 0, 2, NT, M3, NB>(acc, sA, sB);
+    else if (hi == 1)
+      block_mma<NEG, 0, 1, NT, M3, NB>(acc, sA, sB);
+  } else if (hi == 4 && !NEG) {
+    if (lo == 1)
+      block_mma<NEG, 1, 4, NT, M3, NB>(acc, sA, sB);
+    else if (lo == 2)
+      block_mma<NEG, 2, 4, NT, M3, NB>(acc, sA, sB);
+    else if (lo == 3)
+      block_mma<NEG, 3, 4, NT, M3, NB>(acc, sA, sB);
+  } else if (lo < hi) {
+    const unsigned mk = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      double2 A[4], B[NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) A[i] = sA[h * kSt2 + i * 32];
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        double2 v = sB[h * kSt2 + q * 32];
+        if (NB == 3) {
+          const double2 w0 = sB[h * kSt2 + (NT + q) * 32], w1 = sB[h * kSt2 + (2 * NT + q) * 32];
+          v = make_double2(v.x + w0.x, v.y + w0.y);
+          v = make_double2(v.x + w1.x, v.y + w1.y);
+        }
+        B[q] = v;
+      }
+      mma_step<NEG, false>(acc, A, B, mk);
+    }
+  }
+}
+
+// Forward band item over its nblk column blocks (arguments as fwd_kloop):
+//   bstep  bytes from a column block to the next (rbs KB)      bfull  leading blocks with every tile live
+//   dl     first block's column block index minus 4 t          sepn   separator row blocks of the band
+template <int NT, bool M3, bool LEAF>
+__device__ __forceinline__ void fwd_kloop2(Acc<NT, M3>& acc, int nblk, double2* ring, int lane, const char* pa,
+                                           unsigned bstep, unsigned t1, unsigned t2, unsigned t3, const char* xr,
+                                           unsigned xstep, int kcnt, const char* vr, unsigned R16, const int2* sidx,
+                                           bool c0, bool c1, unsigned okq, int bfull, int dl, int sepn, int rbs) {
+  constexpr int NB = LEAF ? 1 : 3;
+  static_assert((4 + NB * NT) * 32 <= kSt2, "stage");
+  const int pl = ring_slot(lane);
+  const unsigned wA = smem_u32(ring) + lane * 16, wB = smem_u32(ring) + 128 * 16 + pl * 16;
+  const double2* rA = ring + lane;
+  const double2* rB = ring + 128 + pl;
+  unsigned woff = 0;
+  int irem = kcnt;  // k-steps of this lane's column still below k
+  const int2* sx = sidx + (lane & 3);
+  const bool q0 = okq & 1u, q1 = (okq >> 1) & 1u;
+  auto issue_block = [&]() {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const char* p = pa + h * 64;
+      const unsigned sa = wA + woff + h * (kSt2 * 16);
+      cpa(sa, p);
+      cpa(sa + 512, p + t1);
+      cpa(sa + 1024, p + t2);
+      cpa(sa + 1536, p + t3);
+      const bool okc = irem > h;
+      const unsigned sb = wB + woff + h * (kSt2 * 16);
+      if (LEAF) {
+        cpz(sb, xr, okc && q0);
+        if (NT > 1) cpz(sb + 512, xr + 128, okc && q1);
+      } else {
+        const int2 src = sx[4 * h];
+        const char* v0 = vr + static_cast<long long>(src.x) * R16;
+        const char* v1 = vr + static_cast<long long>(src.y) * R16;
+        const bool o0 = okc && c0 && src.x >= 0, o1 = okc && c1 && src.y >= 0;
+        cpz(sb, xr, okc && q0);
+        cpz(sb + NT * 512, v0, o0 && q0);
+        cpz(sb + 2 * NT * 512, v1, o1 && q0);
+        if (NT > 1) {
+          cpz(sb + 512, xr + 128, okc && q1);
+          cpz(sb + (NT + 1) * 512, v0 + 128, o0 && q1);
+          cpz(sb + (2 * NT + 1) * 512, v1 + 128, o1 && q1);
+        }
+      }
+      xr += xstep;
+    }
+    pa += bstep;
+    irem -= 2;
+    sx += 8;
+    woff ^= 2 * kSt2 * 16;
+  };
+  if (nblk > 0) issue_block();
+  cp_commit();
+  int roff = 0;
+#pragma unroll 1
+  for (int b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) issue_block();
+    cp_commit();
+    cp_wait<1>();
+    if (b < bfull) {
+      block_mma<false, 0, 4, NT, M3, NB>(acc, rA + roff, rB + roff);
+    } else {  // diagonal column blocks (M's zero blocks above the diagonal) or a short last band
+      const int lo = min(max(dl + b, 0), sepn);
+      block_dispatch<false, NT, M3, NB>(acc, rA + roff, rB + roff, lo, rbs);
+    }
+    roff ^= 2 * kSt2;
+  }
+  cp_wait<0>();
+}
+
+// Backward column-band item over the block rows a0 + [b0, nblk) (arguments as bwd_kloop; b0 > 0
+// skips the separator rows of a front whose z is structurally zero).
+template <int NT, bool M3>
+__device__ __forceinline__ void bwd_kloop2(Acc<NT, M3>& acc, int nblk, double2* ring, int lane, const double2* P, int kb,
+                                           int nrb, int u, int a0, int cn, const char* zr, const char* XR, unsigned R16,
+                                           int row0, int k, int kp, int nb, bool zlive, unsigned okq, const int2* sidx) {
+  const int pl = ring_slot(lane);
+  const unsigned wA = smem_u32(ring) + pl * 16;
+  const double2* rA = ring + pl;
+  const int bsep = max(min(kb - a0, nblk), 0);  // block rows of separator rows (z); the rest are boundary rows
+  const int b0 = zlive ? 0 : bsep;
+  const unsigned zstep = 4u * R16;
+  const bool q0 = okq & 1u, q1 = (okq >> 1) & 1u;
+  // issue side
+  int ib = b0;
+  unsigned woff = 0;
+  const char* pa = nullptr;
+  unsigned t1 = 0, t2 = 0, t3 = 0;
+  int zrem = k > row0 ? ((k - row0 + 3) >> 2) - 2 * b0 : 0;  // k-steps of this lane's row still below k
+  int brow = row0 + 8 * b0 - kp;                                 // this lane's boundary row index in k-step 0 of block ib
+  zr += static_cast<long long>(2 * b0) * zstep;
+  const int* bx = reinterpret_cast<const int*>(sidx) + 2 * (lane & 3) + 16 * b0;  // .x of entry (lane & 3) + 8 ib + 4 h
+  auto issue_block = [&]() {
+    if ((ib & 3) == 0 || ib == b0) {  // next row band (or the first block's)
+      const int ta = (a0 >> 2) + (ib >> 2);
+      const int rbs = min(4, nrb - 4 * ta);
+      pa = reinterpret_cast<const char*>(P + band_base(ta, kb) + 4 * u * rbs * 64) + (ib & 3) * 1024;
+      const unsigned ts = static_cast<unsigned>(rbs) * 1024u;
+      t1 = cn > 1 ? ts : 0u;
+      t2 = cn > 2 ? 2u * ts : 0u;
+      t3 = cn > 3 ? 3u * ts : 0u;
+    }
+    const bool sep = ib < bsep;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const char* p = pa + h * 512;
+      const unsigned sa = wA + woff + h * (kSt2 * 16);
+      cpa(sa, p);
+      cpa(sa + 512, p + t1);
+      cpa(sa + 1024, p + t2);
+      cpa(sa + 1536, p + t3);
+      const char* src;
+      bool okb;
+      if (sep) {  // separator rows: z
+        okb = zrem > h;
+        src = zr + h * zstep;
+      } else {  // boundary rows: the parent's x at the boundary positions
+        okb = brow + 4 * h < nb;
+        src = XR + static_cast<long long>(okb ? bx[8 * h] : 0) * R16;  // (int2 entries: .x at stride 2 ints)
+      }
+      cpz(sa + 2048, src, okb && q0);
+      if (NT > 1) cpz(sa + 2048 + 512, src + 128, okb && q1);
+    }
+    pa += 1024;
+    zr += 2 * zstep;
+    zrem -= 2;
+    brow += 8;
+    bx += 16;
+    ++ib;
+    woff ^= 2 * kSt2 * 16;
+  };
+  if (ib < nblk) issue_block();
+  cp_commit();
+  int roff = 0;
+  const int hz = 1 - 4 * u + a0;  // live tiles of separator block row a0 + b: min(b + hz, cn)
+#pragma unroll 1
+  for (int b = b0; b < nblk; ++b) {
+    if (ib < nblk) issue_block();
+    cp_commit();
+    cp_wait<1>();
+    if (b < bsep) {
+      const int hi = min(b + hz, cn);
+      block_dispatch<false, NT, M3, 1>(acc, rA + roff, rA + roff + 128, 0, hi);
+    } else {  // boundary rows enter as -x_bnd (signs folded into the DMMA operands)
+      block_dispatch<true, NT, M3, 1>(acc, rA + roff, rA + roff + 128, 0, cn);
+    }
+    roff ^= 2 * kSt2;
+  }
+  cp_wait<0>();
+}
+
 // Item ranges
 struct FwdRange {
   int t, rbs, cb0, cb1;
@@ -888,10 +1132,18 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     const int ns = 2 * (cb1 - cb0);
     // k-steps before the diagonal column blocks run every m-tile (when the band is full)
     const int sfull = mbase == 0xFu ? max(0, 2 * (4 * t - cb0)) : 0;
-    if (!c0 && !c1)
+    const int bfull = rbs == 4 ? max(0, 4 * t - cb0) : 0, sepc = min(max(sepn, 0), 4);
+    if (HS_KLOOP2 && !CA && !c0 && !c1)
+      fwd_kloop2<NT, M3, true>(acc, cb1 - cb0, ring, lane, pa, rb1 * 1024u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16, sidx,
+                               false, false, okq, bfull, cb0 - 4 * t, sepc, rbs);
+    else if (!c0 && !c1)
       fwd_kloop<NT, M3, true, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                               sidx, false, false, okq, sfull, mbase, msep, cb0 - 4 * t);
-    else
+    else if (HS_KLOOP2 && !CA && NT == 1) {
+      if constexpr (NT == 1)  // (three-part stages at 16 RHS exceed the block stage)
+        fwd_kloop2<NT, M3, false>(acc, cb1 - cb0, ring, lane, pa, rb1 * 1024u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16, sidx,
+                                  c0, c1, okq, bfull, cb0 - 4 * t, sepc, rbs);
+    } else
       fwd_kloop<NT, M3, false, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                                sidx, c0, c1, okq, sfull, mbase, msep, cb0 - 4 * t);
   }
@@ -1050,9 +1302,14 @@ __device__ bool bwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     // them when the column band is short
     const int ns = 2 * (a1 - a0);
     const int smask = mcol == 0xFu ? max(0, 2 * (4 * u + 3 - a0)) : ns;
-    bwd_kloop<NT, M3, CA>(acc, ns, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
-                      ZR + static_cast<size_t>(static_cast<unsigned>(row0)) * R16, XR, R16, row0, J.k, g.kp, nb, zlive,
-                      okq, sidx, smask, mcol);
+    if (HS_KLOOP2 && !CA)
+      bwd_kloop2<NT, M3>(acc, a1 - a0, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
+                         ZR + static_cast<size_t>(static_cast<unsigned>(row0)) * R16, XR, R16, row0, J.k, g.kp, nb, zlive,
+                         okq, sidx);
+    else
+      bwd_kloop<NT, M3, CA>(acc, ns, ring, lane, P, g.kb, g.nrb, u, a0, cn4,
+                        ZR + static_cast<size_t>(static_cast<unsigned>(row0)) * R16, XR, R16, row0, J.k, g.kp, nb, zlive,
+                        okq, sidx, smask, mcol);
   }
 #else
   kloop<false, NT>(acc, 2 * (a1 - a0), ring, issue, use, mask_of, neg_of);
