@@ -400,6 +400,9 @@ __device__ __forceinline__ void cp_wait() {
 // parts, NB x 2 x 32 double2: forward NB = 3 = rhs, child0 V, child1 V; backward NB = 1),
 // followed by the item's index slice (kIdx entries: source-map pairs / boundary positions).
 constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
+#ifndef HS_ST2
+#define HS_ST2 256  // double2 per k-step stage of the block-granular loops (below)
+#endif
 #ifndef HS_NS_FWD
 #define HS_NS_FWD 2
 #endif
@@ -439,7 +442,7 @@ template <bool FWD>
 struct RingArea {
   static constexpr int a1 = Ring<FWD, 1>::NS * Ring<FWD, 1>::kStage, a2 = Ring<FWD, 2>::NS * Ring<FWD, 2>::kStage;
   static constexpr int kRing1 = a1 > a2 ? a1 : a2;
-  static constexpr int kRing = kRing1 > 1024 ? kRing1 : 1024;  // >= kRing2, the block-granular loops' two block stages
+  static constexpr int kRing = kRing1 > 4 * HS_ST2 ? kRing1 : 4 * HS_ST2;  // >= kRing2, the block-granular loops' two block stages
   static constexpr int kFin = FWD ? 32 / 2 + 32 : 0;
   static constexpr int kWarp = kRing + kIdx / 2 + kFin;
 };
@@ -699,7 +702,8 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
 #ifndef HS_KLOOP2
 #define HS_KLOOP2 1
 #endif
-constexpr int kSt2 = 256;          // double2 per k-step stage (4 KB): A tiles at i * 32, B parts at 128 + j * 32
+constexpr int kSt2 = HS_ST2;       // double2 per k-step stage (4 KB): A tiles at i * 32, B parts at 128 + j * 32
+                                   // (192 = one-part stages only: 13.75 KB per warp, 4 CTAs per SM)
 constexpr int kRing2 = 4 * kSt2;   // two block stages
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
@@ -1139,8 +1143,8 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     else if (!c0 && !c1)
       fwd_kloop<NT, M3, true, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                               sidx, false, false, okq, sfull, mbase, msep, cb0 - 4 * t);
-    else if (HS_KLOOP2 && !CA && NT == 1) {
-      if constexpr (NT == 1)  // (three-part stages at 16 RHS exceed the block stage)
+    else if (HS_KLOOP2 && !CA && NT == 1 && (4 + 3 * NT) * 32 <= kSt2) {
+      if constexpr (NT == 1 && (4 + 3 * NT) * 32 <= kSt2)  // (three-part stages at 16 RHS exceed the block stage)
         fwd_kloop2<NT, M3, false>(acc, cb1 - cb0, ring, lane, pa, rb1 * 1024u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16, sidx,
                                   c0, c1, okq, bfull, cb0 - 4 * t, sepc, rbs);
     } else
