@@ -2481,7 +2481,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   auto reg_cnt = [&](const OutRegion& o) { return (o.row1 - o.row0) * (o.x1 - o.x0); };
   std::vector<int> stripe_blocks(regs.size(), 0);
   auto stripe_pbase = [&](int j) {  // partial blocks of the regions before j (exact: one block per npb nodes)
-    const int npb = 256 / R;
+    const int npb = fuse_acc ? 256 / ((R + 1) / 2) : 256 / R;  // (the fused pass runs a thread per RHS pair)
     long long b = 0;
     for (int q = 0; q < j; ++q) b += (reg_cnt(regs[q]) + npb - 1) / npb;
     return b;
@@ -2556,7 +2556,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
           comm_gather_u(t);
           ures = t;
         }
-        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s);
+        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s, geom.gsize[0]);
         launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
         launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
       }
@@ -2611,7 +2611,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
             for (int q = 0; q + 1 < nrounds; ++q) {
               double2* uq = uround.p + static_cast<size_t>(q) * geom.gn * R;
               if (partitioned()) comm_gather_u(uq);
-              const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s);
+              const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s, geom.gsize[0]);
               launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(q) * R, s);
               launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(q) * R, s);
             }
@@ -3342,7 +3342,7 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
       HS_CUDA(cudaStreamSynchronize(st));  // alpha / hcol host buffers are reused
     }
     // true residual ||b - A x|| / ||b||
-    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st);
+    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st, H.geom.gsize[0]);
     DBuf<double> tn;
     tn.alloc(R);
     launch_reduce_partials(H.pnum.p, nb2, R, tn.p, st);

@@ -589,16 +589,31 @@ __global__ void reduce_cpartials_kernel(const double2* partial, int nblocks, int
 }
 
 constexpr int kResThreads = 512;  // rows x RHS per block (64-RHS batches still get 8 rows per block)
+constexpr int kResRows = 8;       // grid rows a block walks: a row's x is the next row's lower neighbour (L1 hit)
+// Rows are taken in tiles of (kResThreads / R nodes along x) x kResRows grid rows: the operator is a
+// 5 / 7-point stencil, so a block walking up its columns re-reads each x row from L1 instead of
+// three times from L2 (ncu: the one-row blocks ran at 38% of HBM bandwidth with L2 as the bound).
+// gx = 0: rows in plain order (any CSR matrix; the column indices are used either way).
 __global__ void __launch_bounds__(kResThreads) residual_kernel(long long n, const std::int64_t* row_ptr, const int* col,
                                                                 const double2* val, const double2* x, const double2* b,
-                                                                int R, double* pnum, double* pden) {
+                                                                int R, double* pnum, double* pden, int gx, int tiles_x) {
   __shared__ double rn[kResThreads], rd[kResThreads];
   const int npb = kResThreads / R;
-  const long long row = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;
-  const int r = threadIdx.x % R;
-  const long long idx = row * R + r;
+  const int tn = threadIdx.x / R, r = threadIdx.x % R;
   double num = 0.0, den = 0.0;
-  if (threadIdx.x < npb * R && row < n) {
+  const int iters = gx > 0 ? kResRows : 1;
+  const long long bx = gx > 0 ? blockIdx.x % tiles_x : 0, by = gx > 0 ? blockIdx.x / tiles_x : 0;
+  for (int j = 0; j < iters; ++j) {
+    long long row;
+    bool ok = tn < npb;
+    if (gx > 0) {
+      const long long xi = bx * npb + tn;
+      row = (by * kResRows + j) * gx + xi;
+      ok = ok && xi < gx;
+    } else {
+      row = static_cast<long long>(blockIdx.x) * npb + tn;
+    }
+    if (!ok || row >= n) continue;
     // all of the row's loads in flight before the sum (rows hold <= 7 entries: 2D 5, 3D 7)
     const long long e0 = row_ptr[row], e1 = row_ptr[row + 1];
     double2 s = czero();
@@ -606,25 +621,25 @@ __global__ void __launch_bounds__(kResThreads) residual_kernel(long long n, cons
       double2 v[8], xv[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const bool ok = eb + q < e1;
-        v[q] = ok ? val[eb + q] : czero();
-        xv[q] = ok ? x[static_cast<long long>(col[eb + q]) * R + r] : czero();
+        const bool in = eb + q < e1;
+        v[q] = in ? val[eb + q] : czero();
+        xv[q] = in ? x[static_cast<long long>(col[eb + q]) * R + r] : czero();
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (eb + q < e1) cfma(s, v[q], xv[q]);
     }
-    const double2 bv = b[idx];
+    const double2 bv = b[row * R + r];
     const double2 dv = csub(bv, s);
-    num = dv.x * dv.x + dv.y * dv.y;
-    den = bv.x * bv.x + bv.y * bv.y;
+    num += dv.x * dv.x + dv.y * dv.y;
+    den += bv.x * bv.x + bv.y * bv.y;
   }
   rn[threadIdx.x] = num;
   rd[threadIdx.x] = den;
   __syncthreads();
   if (threadIdx.x < R) {
     double s1 = 0.0, s2 = 0.0;
-    for (int q = threadIdx.x; q < kResThreads; q += R) {
+    for (int q = threadIdx.x; q < npb * R; q += R) {
       s1 += rn[q];
       s2 += rd[q];
     }
@@ -872,64 +887,82 @@ void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
 constexpr int kAccThreads = 256;
 template <int E>
 __global__ void __launch_bounds__(kAccThreads) accumulate_all_kernel(AccumAllArgs a) {
-  // Per-sweep |c_l|^2 partials are kept in registers and reduced once at the end (one barrier),
-  // so the loads of consecutive sweeps overlap (a barrier per sweep serialised them: the fused
-  // pass ran at 34% of HBM bandwidth on C3, ncu).
-  __shared__ double red[HS_MAX_ACC_SWEEPS][kAccThreads];
-  const int dim = a.g.dim, R = a.R;
-  const int npb = kAccThreads / R;
-  const long long li = static_cast<long long>(blockIdx.x) * npb + threadIdx.x / R;  // index in the region
+  // One thread per (node, RHS pair): its two x values are independent 16-byte loads, so a thread
+  // keeps twice the bytes in flight of the one-RHS form (ncu: 37% of HBM bandwidth, bound by the
+  // bytes in flight per SM -- each thread walks a dependent plan entry -> nonzero word -> x chain
+  // per sweep). Per-sweep |c_l|^2 terms go straight to shared memory (no registers held across the
+  // sweeps) and are reduced once at the end (one barrier).
+  __shared__ double red[HS_MAX_ACC_SWEEPS][2][kAccThreads];
+  const int dim = a.g.dim, R = a.R, RP = (R + 1) >> 1;
+  const int npb = kAccThreads / RP;
+  const int tn = threadIdx.x / RP;
+  const long long li = static_cast<long long>(blockIdx.x) * npb + tn;  // index in the region
   const long long node = (a.row0 + li / a.w) * a.gx + a.x0 + li % a.w;
-  const int r = threadIdx.x % R;
-  const bool live = threadIdx.x < npb * R && li < a.cnt;
+  const int r = 2 * (threadIdx.x % RP);
+  const bool two = r + 1 < R;
+  const bool live = tn < npb && li < a.cnt;
   const double inv = 1.0 / static_cast<double>(1 << dim);
-  double2 uv = czero();
-  double nrm[HS_MAX_ACC_SWEEPS];
+  const double2* __restrict__ xs = a.x;
 #pragma unroll
-  for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) nrm[l] = 0.0;
+  for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) red[l][0][threadIdx.x] = red[l][1][threadIdx.x] = 0.0;
   if (live) {
+    double2 u0 = czero(), u1 = czero();
 #pragma unroll
     for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) {
       if (l >= a.L) break;
+      const int2* __restrict__ pe = a.acc_ent[l] + node * E;
+      const rmask* __restrict__ nz = a.nzmask[l];
       int2 ent[E];
 #pragma unroll
-      for (int e = 0; e < E; ++e) ent[e] = __ldg(a.acc_ent[l] + node * E + e);
-      double2 xv[E];
-      bool on[E];
+      for (int e = 0; e < E; ++e) ent[e] = __ldg(pe + e);
+      double2 x0[E], x1[E];
+      unsigned on[E];
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        on[i] = ent[i].x >= 0 && ((a.nzmask[l][ent[i].y >> 4] >> r) & 1ull);
-        xv[i] = on[i] ? __ldcs(a.x + a.xoff[l] + static_cast<long long>(ent[i].x) * R + r) : czero();
+        const rmask m = ent[i].x >= 0 ? __ldg(nz + (ent[i].y >> 4)) >> r : 0ull;
+        on[i] = static_cast<unsigned>(m & (two ? 3ull : 1ull));
+        const double2* px = xs + a.xoff[l] + static_cast<long long>(ent[i].x) * R + r;
+        x0[i] = (on[i] & 1u) ? __ldcs(px) : czero();
+        x1[i] = (on[i] & 2u) ? __ldcs(px + 1) : czero();
       }
-      double2 acc = czero();
+      double2 c0 = czero(), c1 = czero();
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        if (!on[i]) continue;
         const double w = (ent[i].y & 15) * inv;
-        acc.x += w * xv[i].x;
-        acc.y += w * xv[i].y;
+        if (on[i] & 1u) {
+          c0.x += w * x0[i].x;
+          c0.y += w * x0[i].y;
+        }
+        if (on[i] & 2u) {
+          c1.x += w * x1[i].x;
+          c1.y += w * x1[i].y;
+        }
       }
-      uv = cadd(uv, acc);
-      nrm[l] = acc.x * acc.x + acc.y * acc.y;
-      if (a.uround && (l + 1) % a.rlen == 0 && l + 1 < a.L)  // u after this round
-        a.uround[static_cast<long long>((l + 1) / a.rlen - 1) * a.rstride + node * R + r] = uv;
+      u0 = cadd(u0, c0);
+      u1 = cadd(u1, c1);
+      red[l][0][threadIdx.x] = c0.x * c0.x + c0.y * c0.y;
+      red[l][1][threadIdx.x] = c1.x * c1.x + c1.y * c1.y;
+      if (a.uround && (l + 1) % a.rlen == 0 && l + 1 < a.L) {  // u after this round
+        double2* ur = a.uround + static_cast<long long>((l + 1) / a.rlen - 1) * a.rstride + node * R + r;
+        ur[0] = u0;
+        if (two) ur[1] = u1;
+      }
     }
-    __stcs(a.u + node * R + r, uv);
+    __stcs(a.u + node * R + r, u0);
+    if (two) __stcs(a.u + node * R + r + 1, u1);
   }
-#pragma unroll
-  for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) red[l][threadIdx.x] = nrm[l];
   __syncthreads();
-  // partial of sweep l, column c: the block's threads of column c in thread order (fixed order)
+  // partial of sweep l, column c: the block's nodes in order (fixed order)
   for (int q = threadIdx.x; q < a.L * R; q += kAccThreads) {
     const int l = q / R, c = q % R;
     double sm = 0.0;
-    for (int t = c; t < kAccThreads; t += R) sm += red[l][t];
+    for (int t = 0; t < npb; ++t) sm += red[l][c & 1][t * RP + (c >> 1)];
     a.partial[l * a.pstride + static_cast<long long>(blockIdx.x) * R + c] = sm;
   }
 }
 
 int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s) {
-  const int nb = blocks_for(a.cnt, kAccThreads / a.R);
+  const int nb = blocks_for(a.cnt, kAccThreads / ((a.R + 1) / 2));
   if (nb == 0) return 0;
   if (a.g.dim == 3)
     accumulate_all_kernel<8><<<nb, kAccThreads, 0, s>>>(a);
@@ -967,9 +1000,17 @@ void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2
 }
 
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, const double2* x,
-                    const double2* b, int R, double* pnum, double* pden, cudaStream_t s) {
-  const int nb = blocks_for(n, kResThreads / R);
-  residual_kernel<<<nb, kResThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden);
+                    const double2* b, int R, double* pnum, double* pden, cudaStream_t s, int gx) {
+  const int npb = kResThreads / R;
+  int nb, tiles_x = 0;
+  if (gx > 0 && n % gx == 0) {  // grid operator: tiles of npb nodes x kResRows grid rows
+    tiles_x = (gx + npb - 1) / npb;
+    nb = tiles_x * static_cast<int>((n / gx + kResRows - 1) / kResRows);
+  } else {
+    gx = 0;
+    nb = blocks_for(n, npb);
+  }
+  residual_kernel<<<nb, kResThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden, gx, tiles_x);
   after_launch();
   return nb;
 }

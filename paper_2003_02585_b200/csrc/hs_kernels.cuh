@@ -170,7 +170,7 @@ void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* m
 // residual partials |b - y|^2, |b|^2.
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
                     const double2* x, const double2* b, int R, double* partial_num,
-                    double* partial_den, cudaStream_t s);
+                    double* partial_den, cudaStream_t s, int gx = 0);
 void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
                  const double2* x, double2* y, int R, cudaStream_t s);
 

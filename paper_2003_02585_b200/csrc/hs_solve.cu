@@ -504,6 +504,10 @@ __device__ __forceinline__ void kloop(Acc<NT, M3>& acc, int ns, double2* ring, I
 #ifndef HS_TB_START
 #define HS_TB_START 0
 #endif
+// 1: the finalize's T_bnd gathers go through the ring with cp.async (all in flight at once)
+#ifndef HS_STAGE_TB
+#define HS_STAGE_TB 1
+#endif
 
 // Ring slot of a lane whose copy shares a 128-byte global line with the lanes of equal lane % 4
 // (B rows: 8 RHS of one row; the backward's A: 8 columns of one block row). cp.async writes shared
@@ -1171,6 +1175,35 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
     if (!split_reduce(acc, base, static_cast<long long>(a.ngr) * kTileDoubles, nch, it.chunk, arr, lane)) return false;
   }
   if (tr && lane == 0) tr[3] = gtime();
+  // T_bnd of the band's boundary rows (the children's update vectors at the front's boundary)
+  // staged through the ring, which is free after the k-loop: all of a lane's up to 32 gathers are
+  // in flight at once. As plain loads feeding the sums they ran nearly one at a time under the
+  // register cap (trace, C3: fronts with k <= 16 spent 7.6 us per item here against 3.8 us in the
+  // k-loop; ncu: long-scoreboard stalls on the finalize's DADDs led the forward kernel).
+  const bool stage_tb = HS_STAGE_TB && 16 * NT * 32 <= RingArea<true>::kRing && !(HS_TB_START || leaf);
+  if (stage_tb) {
+    const unsigned sb = smem_u32(ring) + lane * 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (4 * t + i < g.kb) continue;  // separator row block
+      int2 src = fsrc[8 * i + rl];     // (-1, -1) off the boundary rows
+      if (!(clive & 1u)) src.x = -1;
+      if (!(clive & 2u)) src.y = -1;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int sr = c ? src.y : src.x;
+        const char* gp = reinterpret_cast<const char*>(V + static_cast<long long>(sr) * R + r0 + 2 * (lane & 3));
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            cpz(sb + (((i * 2 + c) * NT + q) * 2 + e) * 512, gp + (8 * q + e) * 16,
+                sr >= 0 && r0 + 8 * q + 2 * (lane & 3) + e < R);
+      }
+    }
+    cp_commit();
+    cp_wait<0>();
+  }
   // finalize: z = D^-1 (M T_sep) on separator rows, V = -(acc) = T_bnd - W T_sep on boundary rows
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -1194,6 +1227,20 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
           for (int e = 0; e < 2; ++e) {
             const int r = r0 + 8 * q + 2 * (lane & 3) + e;
             if (r < R) __stcg(vo + r, make_double2(-acc.v[i][q][0][e], -acc.v[i][q][1][e]));
+          }
+      } else if (stage_tb) {  // V = T_bnd - W T_sep from the staged T_bnd = (0 + child0 V) + child1 V (zero where absent)
+#pragma unroll
+        for (int q = 0; q < NT; ++q)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = r0 + 8 * q + 2 * (lane & 3) + e;
+            if (r >= R) continue;
+            const double2 w0 = ring[(((i * 2 + 0) * NT + q) * 2 + e) * 32 + lane];
+            const double2 w1 = ring[(((i * 2 + 1) * NT + q) * 2 + e) * 32 + lane];
+            double2 tb = czero();
+            tb = make_double2(tb.x + w0.x, tb.y + w0.y);
+            tb = make_double2(tb.x + w1.x, tb.y + w1.y);
+            __stcg(vo + r, make_double2(tb.x - acc.v[i][q][0][e], tb.y - acc.v[i][q][1][e]));
           }
       } else {  // V = T_bnd - W T_sep, T_bnd = (0 + child0 V) + child1 V (reference order: product first)
         int2 src = fsrc[8 * i + rl];
@@ -1478,6 +1525,10 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
         }
       }
     }
+    // nothing waits for a front without dependents (forward: the root; backward: the leaves, 45% of
+    // its items on C3), so its bands are not released (a release costs the warp a fence over its
+    // stores); the end of the launch publishes them
+    if (fin && !(FWD ? J.parent >= 0 : (J.child0 >= 0 || J.child1 >= 0))) fin = false;
     if (!took && lane == 0) tk = atomicAdd(a.queue, 1u);  // skipped item: no k-loop to overlap
     int nxt;
     if (QUAD) {  // warp 0's ticket names the CTA's next quad
