@@ -706,6 +706,9 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
 #ifndef HS_KLOOP2
 #define HS_KLOOP2 1
 #endif
+#ifndef HS_KLOOP3
+#define HS_KLOOP3 1
+#endif
 constexpr int kSt2 = HS_ST2;       // double2 per k-step stage (4 KB): A tiles at i * 32, B parts at 128 + j * 32
                                    // (192 = one-part stages only: 13.75 KB per warp, 4 CTAs per SM)
 constexpr int kRing2 = 4 * kSt2;   // two block stages
@@ -718,25 +721,62 @@ __device__ __forceinline__ void cpz(unsigned s, const char* g, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(g), "r"(ok ? 16 : 0) : "memory");
 }
 
-// both k-steps of a staged block over the m-tiles [LO, HI); NB = 3: B = rhs + child0 V + child1 V
+// one staged k-step over the m-tiles [LO, HI); NB = 3: B = rhs + child0 V + child1 V
+template <bool NEG, int LO, int HI, int NT, bool M3, int NB>
+__device__ __forceinline__ void kstep_mma(Acc<NT, M3>& acc, const double2* sA, const double2* sB) {
+  double2 A[4], B[NT];
+#pragma unroll
+  for (int i = LO; i < HI; ++i) A[i] = sA[i * 32];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    double2 v = sB[q * 32];
+    if (NB == 3) {
+      const double2 w0 = sB[(NT + q) * 32], w1 = sB[(2 * NT + q) * 32];
+      v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
+      v = make_double2(v.x + w1.x, v.y + w1.y);
+    }
+    B[q] = v;
+  }
+  mma_range<NEG, LO, HI>(acc, A, B);
+}
+// both k-steps of a staged block
 template <bool NEG, int LO, int HI, int NT, bool M3, int NB>
 __device__ __forceinline__ void block_mma(Acc<NT, M3>& acc, const double2* sA, const double2* sB) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < 2; ++h) kstep_mma<NEG, LO, HI, NT, M3, NB>(acc, sA + h * kSt2, sB + h * kSt2);
+}
+// one k-step, tile range [lo, hi) (the forward's cases)
+template <int NT, bool M3, int NB>
+__device__ __forceinline__ void kstep_dispatch(Acc<NT, M3>& acc, const double2* sA, const double2* sB, int lo, int hi) {
+  if (lo == 0 && hi == 4)
+    kstep_mma<false, 0, 4, NT, M3, NB>(acc, sA, sB);
+  else if (hi == 4 && lo == 1)
+    kstep_mma<false, 1, 4, NT, M3, NB>(acc, sA, sB);
+  else if (hi == 4 && lo == 2)
+    kstep_mma<false, 2, 4, NT, M3, NB>(acc, sA, sB);
+  else if (hi == 4 && lo == 3)
+    kstep_mma<false, 3, 4, NT, M3, NB>(acc, sA, sB);
+  else if (lo == 0 && hi == 3)
+    kstep_mma<false, 0, 3, NT, M3, NB>(acc, sA, sB);
+  else if (lo == 0 && hi == 2)
+    kstep_mma<false, 0, 2, NT, M3, NB>(acc, sA, sB);
+  else if (lo == 0 && hi == 1)
+    kstep_mma<false, 0, 1, NT, M3, NB>(acc, sA, sB);
+  else if (lo < hi) {
     double2 A[4], B[NT];
 #pragma unroll
-    for (int i = LO; i < HI; ++i) A[i] = sA[h * kSt2 + i * 32];
+    for (int i = 0; i < 4; ++i) A[i] = sA[i * 32];
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
-      double2 v = sB[h * kSt2 + q * 32];
+      double2 v = sB[q * 32];
       if (NB == 3) {
-        const double2 w0 = sB[h * kSt2 + (NT + q) * 32], w1 = sB[h * kSt2 + (2 * NT + q) * 32];
-        v = make_double2(v.x + w0.x, v.y + w0.y);  // rhs + child0 V + child1 V, in this order
+        const double2 w0 = sB[(NT + q) * 32], w1 = sB[(2 * NT + q) * 32];
+        v = make_double2(v.x + w0.x, v.y + w0.y);
         v = make_double2(v.x + w1.x, v.y + w1.y);
       }
       B[q] = v;
     }
-    mma_range<NEG, LO, HI>(acc, A, B);
+    mma_step<false, false>(acc, A, B, ((1u << hi) - 1u) & ~((1u << lo) - 1u));
   }
 }
 // tile ranges of the two passes: the backward's are prefixes [0, hi), the forward's suffixes
@@ -850,6 +890,71 @@ __device__ __forceinline__ void fwd_kloop2(Acc<NT, M3>& acc, int nblk, double2* 
       block_dispatch<false, NT, M3, NB>(acc, rA + roff, rB + roff, lo, rbs);
     }
     roff ^= 2 * kSt2;
+  }
+  cp_wait<0>();
+}
+
+// The forward's three-part stages at 16 RHS (a front with children: rhs + two update vectors,
+// 5 KB per k-step): a ring of three k-step stages, copies two k-steps ahead, the same constant-
+// stride pointers and per-range bodies as fwd_kloop2.
+template <bool M3>
+__device__ __forceinline__ void fwd_kloop3(Acc<2, M3>& acc, int nblk, double2* ring, int lane, const char* pa,
+                                           unsigned bstep, unsigned t1, unsigned t2, unsigned t3, const char* xr,
+                                           unsigned xstep, int kcnt, const char* vr, unsigned R16, const int2* sidx,
+                                           bool c0, bool c1, unsigned okq, int bfull, int dl, int sepn, int rbs) {
+  constexpr int NT = 2, ST = (4 + 3 * NT) * 32;  // double2 per stage
+  const int ns = 2 * nblk;
+  const int pl = ring_slot(lane);
+  const unsigned wA = smem_u32(ring) + lane * 16, wB = smem_u32(ring) + 128 * 16 + pl * 16;
+  const double2* rA = ring + lane;
+  const double2* rB = ring + 128 + pl;
+  unsigned woff = 0;
+  int irem = kcnt;
+  const int2* sx = sidx + (lane & 3);
+  const bool q0 = okq & 1u, q1 = (okq >> 1) & 1u;
+  unsigned astep = 64u;  // to the block's second k-step, then on to the next block
+  auto issue_step = [&]() {
+    const unsigned sa = wA + woff;
+    cpa(sa, pa);
+    cpa(sa + 512, pa + t1);
+    cpa(sa + 1024, pa + t2);
+    cpa(sa + 1536, pa + t3);
+    const bool okc = irem > 0;
+    const unsigned sb = wB + woff;
+    const int2 src = *sx;
+    const char* v0 = vr + static_cast<long long>(src.x) * R16;
+    const char* v1 = vr + static_cast<long long>(src.y) * R16;
+    const bool o0 = okc && c0 && src.x >= 0, o1 = okc && c1 && src.y >= 0;
+    cpz(sb, xr, okc && q0);
+    cpz(sb + 512, xr + 128, okc && q1);
+    cpz(sb + 2 * 512, v0, o0 && q0);
+    cpz(sb + 3 * 512, v0 + 128, o0 && q1);
+    cpz(sb + 4 * 512, v1, o1 && q0);
+    cpz(sb + 5 * 512, v1 + 128, o1 && q1);
+    pa += astep;
+    astep = bstep - astep;  // 64, bstep - 64, 64, ...
+    xr += xstep;
+    --irem;
+    sx += 4;
+    woff = woff == 2 * ST * 16 ? 0u : woff + ST * 16;
+  };
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    if (j < ns) issue_step();
+    cp_commit();
+  }
+  int roff = 0;
+#pragma unroll 1
+  for (int sidx_k = 0; sidx_k < ns; ++sidx_k) {
+    if (sidx_k + 2 < ns) issue_step();
+    cp_commit();
+    cp_wait<2>();
+    const int b = sidx_k >> 1;
+    if (b < bfull)
+      kstep_mma<false, 0, 4, NT, M3, 3>(acc, rA + roff, rB + roff);
+    else
+      kstep_dispatch<NT, M3, 3>(acc, rA + roff, rB + roff, min(max(dl + b, 0), sepn), rbs);
+    roff = roff == 2 * ST ? 0 : roff + ST;
   }
   cp_wait<0>();
 }
@@ -1151,6 +1256,10 @@ __device__ bool fwd_item(const SolveArgs& a, const SolveJob& J, const Geo& g, co
       if constexpr (NT == 1 && (4 + 3 * NT) * 32 <= kSt2)  // (three-part stages at 16 RHS exceed the block stage)
         fwd_kloop2<NT, M3, false>(acc, cb1 - cb0, ring, lane, pa, rb1 * 1024u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16, sidx,
                                   c0, c1, okq, bfull, cb0 - 4 * t, sepc, rbs);
+    } else if (HS_KLOOP2 && HS_KLOOP3 && !CA && NT == 2 && 3 * 320 <= RingArea<true>::kRing) {
+      if constexpr (NT == 2 && 3 * 320 <= RingArea<true>::kRing)
+        fwd_kloop3<M3>(acc, cb1 - cb0, ring, lane, pa, rb1 * 1024u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16, sidx, c0, c1,
+                       okq, bfull, cb0 - 4 * t, sepc, rbs);
     } else
       fwd_kloop<NT, M3, false, CA>(acc, ns, ring, lane, pa, rb1 * 1024u - 64u, t1, t2, t3, XR, 4u * R16, kcnt, VR, R16,
                                sidx, c0, c1, okq, sfull, mbase, msep, cb0 - 4 * t);
