@@ -397,7 +397,7 @@ def test_anisotropic_grids_against_reference(hs, dim, n, parts, pad, rounds):
 
 
 _ALT_SCRIPT = r"""
-import ast, sys, numpy as np
+import ast, os, sys, numpy as np
 sys.path.insert(0, {root!r})
 import paper_2003_02585_b200 as hs
 worst = 0.0
@@ -411,20 +411,26 @@ for name in ["ddm_2d_3x2_r2", "ddm_3d_2x2x2", "ddm_2d_layered"]:
                       axis=med["media.axis"], eta=med["media.eta_L"], eps=med["media.epsilon"])
     dim = int(z["dim"])
     s = hs.DdmSolver(hs.ProblemSetup(dim, [int(z["n"])] * dim, list(z["parts"]), m, pml_width=int(z["pad"])))
-    U = s.ddm_solve(z["b"], int(z["rounds"]), None, True)
+    rep = int(os.environ.get("HS_ALT_REPEAT", "1"))  # the fixture's RHS repeated (a wider batch)
+    n0 = z["b"].shape[0]
+    U = s.ddm_solve(np.tile(z["b"], (rep, 1)), int(z["rounds"]), None, True)
     for r in range(U.shape[0]):
-        worst = max(worst, float(np.linalg.norm(U[r] - z["u"][r]) / np.linalg.norm(z["u"][r])))
+        worst = max(worst, float(np.linalg.norm(U[r] - z["u"][r % n0]) / np.linalg.norm(z["u"][r % n0])))
 print("WORST", worst)
 """
 
 
-@pytest.mark.parametrize("env", [{"HS_M3": "0"}, {"HS_GRAPH": "0"}, {"HS_ORDER": "0", "HS_MAX_CHUNKS": "1"}])
+@pytest.mark.parametrize("env", [{"HS_M3": "0"}, {"HS_GRAPH": "0"}, {"HS_ORDER": "0", "HS_MAX_CHUNKS": "1"},
+                                 {"HS_QUAD": "1", "HS_ALT_REPEAT": "7"}, {"HS_ALT_REPEAT": "9"}])
 def test_alternate_engine_paths_match_reference(env):
     """The engine's alternates, each selected per process by an environment switch, against the
     reference's golden u: the four-product solve kernels (HS_M3=0, 4 CTAs/SM), stream-by-stream
     launches instead of the captured CUDA graph (HS_GRAPH=0), and the plain level order with
     the widest split-K chunks (HS_ORDER=0, HS_MAX_CHUNKS=1: 16-block chunks; a band
-    longer than 16 blocks still splits)."""
+    longer than 16 blocks still splits), the quad dequeue (HS_QUAD=1: one CTA takes the RHS groups of
+    a band chunk together, lists padded with null items; the fixture's RHS repeated to a ragged wide
+    batch), and a ragged wide batch on the default path (odd RHS count: the fused accumulate's RHS
+    pairs, partial last RHS group)."""
     import os
     import subprocess
     import sys
