@@ -29,7 +29,7 @@
  *       write_field / read_field                     include/helmsweep/harness.hpp:10-16
  *   hs_pipeline_cost / hs_pipeline_simulate
  *       average_time_per_rhs / simulate_pipeline     include/helmsweep/pipeline.hpp:27-44
- *   hs_gmres
+ *   hs_gmres, hs_gmres_general
  *       gmres(op, precond, b, cfg) as wired by run_precond
  *                                                    include/helmsweep/krylov.hpp:30-36,
  *                                                    src/harness.cpp:285-305
@@ -172,6 +172,21 @@ int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int ma
  * whenever the iteration count stays within `restart`. */
 int hs_gmres_restarted(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart,
                        int rounds, hs_gmres_report* reports);
+
+/* A LinearMap (include/helmsweep/krylov.hpp:30: CVector -> CVector) as a callback: y = Op x for nrhs
+ * vectors of n complex128 each, RHS-major (each vector one reference CVector). With on_device = 0
+ * x and y are host arrays and stream is NULL; with on_device = 1 they are device arrays and the
+ * callback enqueues its work on `stream` (a cudaStream_t). Returns 0, or nonzero to abort the solve
+ * (HS_ERR_DATA). */
+typedef int (*hs_linop_fn)(void* user, int nrhs, const double* x, double* y, void* stream);
+/* gmres(op, pc, b, cfg) (include/helmsweep/krylov.hpp:30-36, src/krylov.cpp:17-123) for any
+ * operator and right preconditioner: the Krylov loop of hs_gmres (MGS Arnoldi, complex Givens,
+ * breakdown and convergence tests, one process per RHS, vectors and reductions on the device) with
+ * the caller's callbacks in place of the global operator and the DDM application. pc = NULL is the
+ * identity. restart >= maxit is the reference's full GMRES. b, x: host buffers, nrhs RHS-major
+ * vectors of n complex128. */
+int hs_gmres_general(int device, int64_t n, int nrhs, hs_linop_fn op, hs_linop_fn pc, void* user, int on_device,
+                     const double* b, double* x, double tol, int maxit, int restart, hs_gmres_report* reports);
 
 /* global_direct_solve (src/harness.cpp:185-214): u = A^-1 (J f) on the padded global grid with
  * the device sparse-direct factorization of the global J-scaled operator (factorized on first

@@ -16,6 +16,8 @@
 
 #include <complex>
 #include <cstdint>
+#include <cstring>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -167,5 +169,47 @@ class DdmSolver {
   std::int64_t n_ = 0;
   double factor_seconds_ = 0.0;
 };
+
+// gmres(op, pc, b, cfg) (include/helmsweep/krylov.hpp:30-36) for any pair of LinearOperators given
+// as callables CVector -> CVector (pc may be empty: identity); the Krylov loop runs on `device`.
+using LinearOperatorFn = std::function<CVector(const CVector&)>;
+namespace detail {
+struct LinopCtx {
+  const LinearOperatorFn* op;
+  const LinearOperatorFn* pc;
+  std::size_t n;
+};
+inline int linop_apply(const LinearOperatorFn& f, std::size_t n, int nrhs, const double* x, double* y) {
+  try {
+    for (int r = 0; r < nrhs; ++r) {
+      CVector v(n);
+      std::memcpy(static_cast<void*>(v.data()), x + 2 * r * n, sizeof(Complex) * n);
+      const CVector w = f(v);
+      if (w.size() != n) return 1;
+      std::memcpy(y + 2 * r * n, static_cast<const void*>(w.data()), sizeof(Complex) * n);
+    }
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+inline int linop_op(void* u, int nrhs, const double* x, double* y, void*) {
+  const LinopCtx& c = *static_cast<const LinopCtx*>(u);
+  return linop_apply(*c.op, c.n, nrhs, x, y);
+}
+inline int linop_pc(void* u, int nrhs, const double* x, double* y, void*) {
+  const LinopCtx& c = *static_cast<const LinopCtx*>(u);
+  return linop_apply(*c.pc, c.n, nrhs, x, y);
+}
+}  // namespace detail
+inline CVector gmres(const LinearOperatorFn& op, const LinearOperatorFn& pc, const CVector& b, double tol, int maxit,
+                     hs_gmres_report* report = nullptr, int device = 0) {
+  detail::LinopCtx ctx{&op, &pc, b.size()};
+  CVector x(b.size());
+  hs_gmres_report local{};
+  check(hs_gmres_general(device, static_cast<std::int64_t>(b.size()), 1, detail::linop_op, pc ? detail::linop_pc : nullptr,
+                         &ctx, 0, dp(b.data()), dp(x.data()), tol, maxit, maxit, report ? report : &local));
+  return x;
+}
 
 }  // namespace helmsweep_b200

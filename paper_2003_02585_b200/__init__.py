@@ -6,11 +6,11 @@ the reference's Factorization / DdmSolver / gmres interface and its on-disk form
 """
 from .api import (ConfigError, CudaError, DataError, DdmSolver, Factorization, FieldDump, GmresResult,
                   HelmsweepError, Medium, ProblemSetup, SingularMatrixError, SolveReport, SparseOperator,
-                  VelocityGrid, average_time_per_rhs, device_count, factorize, kernel_launches, read_field, read_velocity_csv,
+                  VelocityGrid, average_time_per_rhs, device_count, factorize, gmres, kernel_launches, read_field, read_velocity_csv,
                   read_velocity_grid, route_trace, simulate_pipeline, write_field, write_velocity_grid)
 from ._lib import LIB_PATH
 
 __all__ = ["ConfigError", "CudaError", "DataError", "DdmSolver", "Factorization", "FieldDump", "GmresResult",
            "HelmsweepError", "Medium", "ProblemSetup", "SingularMatrixError", "SolveReport", "SparseOperator",
-           "VelocityGrid", "average_time_per_rhs", "device_count", "factorize", "kernel_launches", "read_field", "read_velocity_csv",
+           "VelocityGrid", "average_time_per_rhs", "device_count", "factorize", "gmres", "kernel_launches", "read_field", "read_velocity_csv",
            "read_velocity_grid", "route_trace", "simulate_pipeline", "write_field", "write_velocity_grid", "LIB_PATH"]

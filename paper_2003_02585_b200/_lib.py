@@ -73,6 +73,8 @@ class GmresReportC(ctypes.Structure):
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, c_int_p, c_i64_p, c_i64_p, c_i64_p,
                                c_i64_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+# hs_linop_fn: y = Op x on nrhs RHS-major vectors (host or device pointers), optional stream
+LINOP_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 
 # Every symbol declared in include/helmsweep_b200.h, with its ctypes signature.
 SIGNATURES = {
@@ -124,6 +126,9 @@ SIGNATURES = {
                                 ctypes.c_int, ctypes.POINTER(GmresReportC)]),
     "hs_gmres_restarted": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(GmresReportC)]),
+    "hs_gmres_general": (ctypes.c_int, [ctypes.c_int, ctypes.c_int64, ctypes.c_int, LINOP_FN, LINOP_FN, ctypes.c_void_p,
+                                        ctypes.c_int, c_dbl_p, c_dbl_p, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                        ctypes.POINTER(GmresReportC)]),
     "hs_ddm_profile": (ctypes.c_int, [ctypes.c_void_p, c_dbl_p, c_i64_p, c_i64_p, c_dbl_p, c_dbl_p]),
     "hs_route_trace": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hs_partition_owners": (ctypes.c_int, [ctypes.c_int, c_int_p, ctypes.c_int, c_int_p]),

@@ -426,6 +426,48 @@ class DdmSolver:
         return out[0] if b.ndim == 1 else out
 
 
+def gmres(op, pc, b, tol=1e-6, maxit=100, restart=None, device=0):
+    """gmres(op, pc, b, cfg) (include/helmsweep/krylov.hpp:30-36) for any LinearMaps: `op` and
+    `pc` (None = identity) map an (R, n) complex128 array to an (R, n) array, like
+    a LinearMap (krylov.hpp:30) applied to R CVectors. The Krylov vectors and reductions live on the device
+    (hs_gmres_general); the callbacks run on the host. b: (n,) or (R, n)."""
+    b = _as_c128(b)
+    single = b.ndim == 1
+    B = b.reshape(1, -1) if single else b
+    nrhs, n = B.shape
+    x = np.zeros_like(B)
+    reps = (L.GmresReportC * nrhs)()
+    err = []
+
+    def wrap(f):
+        def cb(_user, r, px, py, _stream):
+            try:
+                xin = np.ctypeslib.as_array(ctypes.cast(px, ctypes.POINTER(ctypes.c_double)), shape=(r, 2 * n))
+                yout = np.ctypeslib.as_array(ctypes.cast(py, ctypes.POINTER(ctypes.c_double)), shape=(r, 2 * n))
+                y = np.ascontiguousarray(f(xin.view(np.complex128).copy()), dtype=np.complex128).reshape(r, n)
+                yout[:] = y.view(np.float64)
+                return 0
+            except Exception as e:  # reported to the caller after the C call returns
+                err.append(e)
+                return 1
+        return L.LINOP_FN(cb)
+
+    c_op = wrap(op)
+    c_pc = wrap(pc) if pc is not None else ctypes.cast(None, L.LINOP_FN)
+    rc = L.lib().hs_gmres_general(int(device), n, nrhs, c_op, c_pc, None, 0, _dptr(B), _dptr(x), float(tol), int(maxit),
+                                  int(maxit if restart is None else restart), reps)
+    if err:
+        raise err[0]
+    if rc:
+        _raise(rc)
+    out = []
+    for r in range(nrhs):
+        c = reps[r]
+        out.append(GmresResult(x[r], list(c.history[: c.n_history]), c.iterations, bool(c.converged), c.final_residual,
+                               c.true_residual))
+    return out[0] if single else out
+
+
 def route_trace(dim, rounds, gen_sweep, axis, sign):
     """route_trace (src/sweeper.cpp:58-73) as implemented by the product's host layer."""
     return int(L.lib().hs_route_trace(dim, rounds, gen_sweep, axis, sign))

@@ -3153,32 +3153,34 @@ namespace {
 // is the reference's full GMRES; a smaller restart runs GMRES(restart) cycles from the current
 // iterate (r = b - A x recomputed, the convergence test stays |g_{j+1}| / ||b|| <= tol) until
 // tol or maxit total iterations. When no restart happens the result is the full GMRES's.
-void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart, int rounds,
+// The operator / preconditioner seam of gmres(op, pc, b, cfg) (include/helmsweep/krylov.hpp:30-36):
+// everything the Krylov loop needs from its two LinearOperators, on device node-major n x R arrays.
+struct KrylovOps {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  long long n = 0;
+  std::function<int(int)> batch;                                   // RHS per batch for an nrhs-wide call
+  std::function<void(int)> prepare;                                // before a batch of R columns
+  std::function<double2*(int)> pc_in;                              // a buffer the update's V y may be built in
+  std::function<const double2*(const double2*, int)> pc;           // z = M^-1 v; returns z
+  std::function<void(const double2*, double2*, int)> op;           // w = A z
+  std::function<void(const double2*, const double2*, int, double*)> true_res;  // |b - A x|^2 per column
+};
+
+void gmres_loop(const KrylovOps& K, int nrhs, const double* b, double* x, double tol, int maxit, int restart,
                 hs_gmres_report* reports) {
-  if (!s) config_error("gmres: null handle");
   if (!(tol > 0.0)) config_error("GmresConfig: tol must be positive");
   if (maxit < 1) config_error("GmresConfig: max_iterations must be >= 1");
   if (maxit + 1 > HS_MAX_GMRES_HISTORY) config_error("gmres: maxit too large for the report");
   if (restart < 1) config_error("gmres: restart must be >= 1");
   const int mk = std::min(restart, maxit);  // Krylov basis per cycle
-  DdmHandle& H = s->h;
-  HS_CUDA(cudaSetDevice(H.eng.device));
-  H.ensure_gop();
-  cudaStream_t st = H.eng.stream;
-  const long long n = H.geom.gn;
-  size_t free_b = 0, total_b = 0;
-  HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  // per RHS column: the Krylov basis and work vectors, plus the DDM application's per-RHS
-  // buffers (x / z / rhs per subdomain and x buffer, b / u / staging on the global grid)
-  const int nbuf_max = std::max(4, std::min(rounds * H.ndir, HS_MAX_ACC_SWEEPS));  // x buffers (build_schedule)
-  const double ddm_col = (static_cast<double>(nbuf_max) * H.eng.n_base.back() + 2.0 * H.geom.nsub * H.eng.n_max +
-                          6.0 * n) * sizeof(double2);
-  const double per_col = static_cast<double>(mk + 5) * n * sizeof(double2) + ddm_col;
-  int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
-  if (H.partitioned()) rmax = kMaxRhs;  // every rank must batch identically
+  HS_CUDA(cudaSetDevice(K.device));
+  cudaStream_t st = K.st;
+  const long long n = K.n;
+  const int rmax = std::max(1, K.batch(nrhs));
   for (int b0 = 0; b0 < nrhs; b0 += rmax) {
     const int R = std::min(rmax, nrhs - b0);
-    H.ensure_state(R, rounds);
+    K.prepare(R);
     const size_t nr = static_cast<size_t>(n) * R;
     DBuf<double2> Bv, V, W, X, io, part, hcol, ones;
     DBuf<double> inv;
@@ -3211,7 +3213,7 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
       // r0 = b (first cycle, x = 0) or b - A x; its norm starts the Givens right-hand side
       const double2* r0 = Bv.p;
       if (cycle > 0) {
-        launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, W.p, R, st);
+        K.op(X.p, W.p, R);
         HS_CUDA(cudaMemcpyAsync(V.p, Bv.p, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
         launch_axpy_cols(V.p, W.p, ones.p, 1, n, R, st);
         r0 = V.p;
@@ -3251,9 +3253,7 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
       };
       while (j < mk && any_live()) {
         double2* vj = V.p + static_cast<size_t>(j) * nr;
-        HS_CUDA(cudaMemcpyAsync(H.bN.p, vj, sizeof(double2) * nr, cudaMemcpyDeviceToDevice, st));
-        H.run(rounds, false, false);                                          // z = M^-1 v_j
-        launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, H.u.p, W.p, R, st);     // w = A z
+        K.op(K.pc(vj, R), W.p, R);  // w = A M^-1 v_j
         for (int i = 0; i <= j; ++i) {                                         // modified Gram-Schmidt
           const double2* vi = V.p + static_cast<size_t>(i) * nr;
           dot(vi, W.p, hcol.p + static_cast<size_t>(i) * R);
@@ -3329,23 +3329,22 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
           y[r][i] = sacc / hess[r][i][i];
         }
       }
-      HS_CUDA(cudaMemsetAsync(H.bN.p, 0, sizeof(double2) * nr, st));
+      double2* vy = K.pc_in(R);
+      HS_CUDA(cudaMemsetAsync(vy, 0, sizeof(double2) * nr, st));
       std::vector<double2> alpha(R);
       for (int k2 = 0; k2 < jmax; ++k2) {
         for (int r = 0; r < R; ++r)
           alpha[r] = k2 < cyc_it[r] ? make_double2(y[r][k2].real(), y[r][k2].imag()) : make_double2(0.0, 0.0);
         HS_CUDA(cudaMemcpyAsync(hcol.p, alpha.data(), sizeof(double2) * R, cudaMemcpyHostToDevice, st));
-        launch_axpy_cols(H.bN.p, V.p + static_cast<size_t>(k2) * nr, hcol.p, 0, n, R, st);
+        launch_axpy_cols(vy, V.p + static_cast<size_t>(k2) * nr, hcol.p, 0, n, R, st);
       }
-      H.run(rounds, false, false);
-      launch_axpy_cols(X.p, H.u.p, ones.p, 0, n, R, st);
+      launch_axpy_cols(X.p, K.pc(vy, R), ones.p, 0, n, R, st);
       HS_CUDA(cudaStreamSynchronize(st));  // alpha / hcol host buffers are reused
     }
     // true residual ||b - A x|| / ||b||
-    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, X.p, Bv.p, R, H.pnum.p, H.pden.p, st, H.geom.gsize[0]);
     DBuf<double> tn;
     tn.alloc(R);
-    launch_reduce_partials(H.pnum.p, nb2, R, tn.p, st);
+    K.true_res(X.p, Bv.p, R, tn.p);
     std::vector<double> tnh(R);
     HS_CUDA(cudaMemcpyAsync(tnh.data(), tn.p, sizeof(double) * R, cudaMemcpyDeviceToHost, st));
     launch_transpose_out(X.p, io.p, n, R, st);
@@ -3366,6 +3365,51 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
   }
 }
 
+
+// gmres(global_op, DdmPreconditioner, b, cfg) as run_precond wires it (src/harness.cpp:285-305)
+void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart, int rounds,
+                hs_gmres_report* reports) {
+  if (!s) config_error("gmres: null handle");
+  DdmHandle& H = s->h;
+  HS_CUDA(cudaSetDevice(H.eng.device));
+  H.ensure_gop();
+  KrylovOps K;
+  K.device = H.eng.device;
+  K.st = H.eng.stream;
+  K.n = H.geom.gn;
+  const long long n = K.n;
+  cudaStream_t st = K.st;
+  K.batch = [&](int) {
+    if (!(tol > 0.0) || maxit < 1 || restart < 1) return 1;  // (reported by the loop's checks)
+    const int mk = std::min(restart, maxit);
+    size_t free_b = 0, total_b = 0;
+    HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    // per RHS column: the Krylov basis and work vectors, plus the DDM application's per-RHS
+    // buffers (x / z / rhs per subdomain and x buffer, b / u / staging on the global grid)
+    const int nbuf_max = std::max(4, std::min(rounds * H.ndir, HS_MAX_ACC_SWEEPS));  // x buffers (build_schedule)
+    const double ddm_col = (static_cast<double>(nbuf_max) * H.eng.n_base.back() + 2.0 * H.geom.nsub * H.eng.n_max +
+                            6.0 * n) * sizeof(double2);
+    const double per_col = static_cast<double>(mk + 5) * n * sizeof(double2) + ddm_col;
+    int rmax = std::max(1, std::min(kMaxRhs, static_cast<int>(0.6 * free_b / per_col)));
+    if (H.partitioned()) rmax = kMaxRhs;  // every rank must batch identically
+    return rmax;
+  };
+  K.prepare = [&](int R) { H.ensure_state(R, rounds); };
+  K.pc_in = [&](int) { return H.bN.p; };
+  K.pc = [&](const double2* v, int R) -> const double2* {  // one DDM application: z = M^-1 v
+    if (v != H.bN.p)
+      HS_CUDA(cudaMemcpyAsync(H.bN.p, v, sizeof(double2) * static_cast<size_t>(n) * R, cudaMemcpyDeviceToDevice, st));
+    H.run(rounds, false, false);
+    return H.u.p;
+  };
+  K.op = [&](const double2* z, double2* w, int R) { launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, z, w, R, st); };
+  K.true_res = [&](const double2* xx, const double2* bb, int R, double* out) {
+    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, xx, bb, R, H.pnum.p, H.pden.p, st, H.geom.gsize[0]);
+    launch_reduce_partials(H.pnum.p, nb2, R, out, st);
+  };
+  gmres_loop(K, nrhs, b, x, tol, maxit, restart, reports);
+}
+
 }  // namespace
 
 extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int rounds,
@@ -3376,6 +3420,104 @@ extern "C" int hs_gmres(hs_ddm* s, int nrhs, const double* b, double* x, double 
 extern "C" int hs_gmres_restarted(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int maxit, int restart,
                                   int rounds, hs_gmres_report* reports) {
   return guarded([&] { gmres_impl(s, nrhs, b, x, tol, maxit, restart, rounds, reports); });
+}
+
+// gmres(apply_op, apply_precond, rhs, cfg) for any pair of LinearMaps (include/helmsweep/krylov.hpp:30-36;
+// pc = NULL is identity_preconditioner(), :38-40): the Krylov loop of hs_gmres with the caller's apply
+// callbacks in place of the global operator and the DDM preconditioner. The vectors stay on the
+// device; a host callback sees them staged through pinned buffers as RHS-major CVectors.
+extern "C" int hs_gmres_general(int device, int64_t n64, int nrhs, hs_linop_fn op, hs_linop_fn pc, void* user,
+                                int on_device, const double* b, double* x, double tol, int maxit, int restart,
+                                hs_gmres_report* reports) {
+  return guarded([&] {
+    if (!op || !b || !x) config_error("gmres: null argument");
+    if (n64 < 1 || nrhs < 1) config_error("gmres: empty system");
+    if (!(tol > 0.0)) config_error("GmresConfig: tol must be positive");  // (config errors before device work)
+    if (maxit < 1) config_error("GmresConfig: max_iterations must be >= 1");
+    if (maxit + 1 > HS_MAX_GMRES_HISTORY) config_error("gmres: maxit too large for the report");
+    if (restart < 1) config_error("gmres: restart must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+      throw Error(kCuda, "gmres: no usable CUDA device");
+    HS_CUDA(cudaSetDevice(device));
+    const long long n = n64;
+    cudaStream_t st = nullptr;
+    HS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct Guard {
+      cudaStream_t s;
+      double *hx = nullptr, *hy = nullptr;
+      ~Guard() {
+        cudaStreamSynchronize(s);
+        if (hx) cudaFreeHost(hx);
+        if (hy) cudaFreeHost(hy);
+        cudaStreamDestroy(s);
+      }
+    } guard{st};
+    DBuf<double2> T, Z, W2, cin, cout, dtmp;
+    int cap = 0;
+    KrylovOps K;
+    K.device = device;
+    K.st = st;
+    K.n = n;
+    K.batch = [&](int want) {
+      if (!(tol > 0.0) || maxit < 1 || restart < 1) return 1;
+      size_t free_b = 0, total_b = 0;
+      HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const double per_col = static_cast<double>(std::min(restart, maxit) + 12) * n * sizeof(double2);
+      return std::max(1, std::min(std::min(want, kMaxRhs), static_cast<int>(0.6 * free_b / per_col)));
+    };
+    K.prepare = [&](int R) {
+      if (R <= cap) return;
+      cap = R;
+      const size_t nr = static_cast<size_t>(n) * R;
+      for (DBuf<double2>* d : {&T, &Z, &W2, &cin, &cout}) d->alloc(nr);
+      dtmp.alloc(static_cast<size_t>(R) + (nr + 255) / 256 * R);
+      if (!on_device) {
+        if (guard.hx) cudaFreeHost(guard.hx);
+        if (guard.hy) cudaFreeHost(guard.hy);
+        HS_CUDA(cudaMallocHost(&guard.hx, nr * sizeof(double2)));
+        HS_CUDA(cudaMallocHost(&guard.hy, nr * sizeof(double2)));
+      }
+    };
+    // y = F v through the caller's callback: node-major -> RHS-major CVectors -> callback -> back
+    auto apply = [&](hs_linop_fn f, const double2* v, double2* y, int R) {
+      const size_t bytes = static_cast<size_t>(n) * R * sizeof(double2);
+      launch_transpose_out(v, cin.p, n, R, st);
+      int rc;
+      if (on_device) {
+        rc = f(user, R, reinterpret_cast<const double*>(cin.p), reinterpret_cast<double*>(cout.p), st);
+      } else {
+        HS_CUDA(cudaMemcpyAsync(guard.hx, cin.p, bytes, cudaMemcpyDeviceToHost, st));
+        HS_CUDA(cudaStreamSynchronize(st));
+        rc = f(user, R, guard.hx, guard.hy, nullptr);
+        HS_CUDA(cudaMemcpyAsync(cout.p, guard.hy, bytes, cudaMemcpyHostToDevice, st));
+      }
+      if (rc != 0) data_error("gmres: operator callback failed");
+      launch_transpose_in(cout.p, y, n, R, st);
+    };
+    K.pc_in = [&](int) { return T.p; };
+    K.pc = [&](const double2* v, int R) -> const double2* {
+      if (!pc) return v;  // identity preconditioner
+      apply(pc, v, Z.p, R);
+      return Z.p;
+    };
+    K.op = [&](const double2* z, double2* w, int R) { apply(op, z, w, R); };
+    K.true_res = [&](const double2* xx, const double2* bb, int R, double* out) {  // |b - A x|^2 per column
+      apply(op, xx, W2.p, R);
+      std::vector<double2> one(R, make_double2(1.0, 0.0)), h(R);
+      HS_CUDA(cudaMemcpyAsync(dtmp.p, one.data(), sizeof(double2) * R, cudaMemcpyHostToDevice, st));
+      launch_axpy_cols(W2.p, bb, dtmp.p, 1, n, R, st);  // A x - b
+      const int blocks = launch_dot_partials(W2.p, W2.p, n, R, dtmp.p + R, st);
+      launch_reduce_cpartials(dtmp.p + R, blocks, R, dtmp.p, st);
+      HS_CUDA(cudaMemcpyAsync(h.data(), dtmp.p, sizeof(double2) * R, cudaMemcpyDeviceToHost, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+      std::vector<double> hr(R);
+      for (int r = 0; r < R; ++r) hr[r] = h[r].x;
+      HS_CUDA(cudaMemcpyAsync(out, hr.data(), sizeof(double) * R, cudaMemcpyHostToDevice, st));
+      HS_CUDA(cudaStreamSynchronize(st));
+    };
+    gmres_loop(K, nrhs, b, x, tol, maxit, restart, reports);
+  });
 }
 
 extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_launches, int64_t* subdomain_solves,

@@ -67,6 +67,18 @@ def test_config_errors_are_reported_before_device_work():
         hs.DdmSolver(thin)
 
 
+def test_general_gmres_config_errors_come_before_device_work():
+    """hs_gmres_general validates GmresConfig (include/helmsweep/krylov.hpp:10-19)
+    (cfg.validate(), src/krylov.cpp:19) before it touches a device, so the reference's ConfigErrors surface on a box without a GPU too."""
+    import numpy as np
+    import paper_2003_02585_b200 as hs
+    b = np.ones(8, dtype=np.complex128)
+    ident = lambda X: X
+    for kw in ({"tol": 0.0}, {"tol": -1.0}, {"maxit": 0}, {"restart": 0}):
+        with pytest.raises(hs.ConfigError):
+            hs.gmres(ident, None, b, **kw)
+
+
 @pytest.mark.parametrize("dim,rounds", [(2, 1), (2, 2), (3, 1), (3, 2)])
 def test_product_routing_matches_reference(golden, dim, rounds):
     import paper_2003_02585_b200 as hs

@@ -172,6 +172,46 @@ def test_gmres_matches_reference(hs, golden):
     assert g.true_residual <= 1e-7
 
 
+def test_general_gmres_seam(hs, golden):
+    """gmres(op, pc, b, cfg) for caller-supplied LinearOperators (include/helmsweep/krylov.hpp:30-36)
+    through hs_gmres_general: a dense operator with and without a right preconditioner against the
+    oracle's restatement of src/krylov.cpp (same iteration counts and histories) and numpy's solve;
+    then the reference's own wiring -- global operator and DDM application as host callbacks --
+    against hs_gmres and the reference's golden GMRES run."""
+    from oracle import hs_oracle as O
+    g = np.random.default_rng(5)
+    n = 300
+    A = np.eye(n) * 4.0 + (g.standard_normal((n, n)) + 1j * g.standard_normal((n, n))) / np.sqrt(n)
+    Dinv = 1.0 / np.diag(A)
+    B = g.standard_normal((3, n)) + 1j * g.standard_normal((3, n))
+    B[2] = 0.0  # a zero right-hand side converges at once (src/krylov.cpp:26-30)
+    op = lambda X: X @ A.T
+    pc = lambda X: X * Dinv
+    for use_pc in (None, pc):
+        res = hs.gmres(op, use_pc, B, tol=1e-10, maxit=80)
+        for r in range(3):
+            ro = O.gmres(lambda v: A @ v, (lambda v: v) if use_pc is None else (lambda v: Dinv * v), B[r].copy(), 1e-10, 80)
+            assert res[r].iterations == ro.iterations and res[r].converged == ro.converged
+            np.testing.assert_allclose(res[r].history, ro.history, rtol=1e-9, atol=1e-14)
+            if r < 2:
+                assert rel(res[r].x, np.linalg.solve(A, B[r])) <= 1e-8
+                assert res[r].true_residual <= 1e-9
+    few = hs.gmres(op, None, B[0], tol=1e-12, maxit=5, restart=5)  # stops at maxit, not converged
+    assert few.iterations == 5 and not few.converged and len(few.history) == 6
+    with pytest.raises(ValueError):  # a failing callback aborts the solve (HS_ERR_DATA); its own exception is re-raised
+        hs.gmres(lambda X: X[:, :-1], None, B[0])
+    z = golden("gmres_2d")
+    med = ast.literal_eval(str(z["medium"]))
+    s = hs.DdmSolver(hs.ProblemSetup(2, [int(z["n"])] * 2, list(z["parts"]), hs.Medium("constant", kappa=med["media.kappa"]),
+                                     pml_width=int(z["pad"])))
+    wired = s.gmres(z["b"], float(z["tol"]), int(z["maxit"]), 1)
+    seam = hs.gmres(lambda X: s.apply_op(X), lambda X: s.ddm_solve(X, 1, None, False), z["b"], float(z["tol"]),
+                    int(z["maxit"]))
+    assert seam.iterations == wired.iterations and abs(seam.iterations - int(z["iterations"])) <= 1
+    np.testing.assert_allclose(seam.history, wired.history, rtol=1e-8)
+    assert rel(seam.x, wired.x) <= 1e-9 and rel(seam.x, z["x"]) <= 1e-7
+
+
 def test_gmres_restarted(hs, golden):
     z = golden("gmres_2d")
     med = ast.literal_eval(str(z["medium"]))
