@@ -1178,6 +1178,9 @@ struct DdmHandle {
   DBuf<std::int64_t> g_rp;
   DBuf<int> g_col;
   DBuf<double2> g_val;
+  DBuf<double2> g_sten;  // the same operator in stencil form (StencilOp), for the residual kernel
+  StencilOp g_sop;
+  void build_stencil_op();
   // subdomain partition over ranks; world == 1: every subdomain is local
   int rank = 0, world = 1;
   std::vector<int> owner;                       // per subdomain
@@ -2299,6 +2302,7 @@ void DdmHandle::ensure_gop() {
     HS_CUDA(cudaMemcpyAsync(g_val.p, op.val.data(), op.val.size() * sizeof(Complex), cudaMemcpyHostToDevice,
                             eng.stream));
     HS_CUDA(cudaStreamSynchronize(eng.stream));
+    build_stencil_op();
     gop_ready = true;
     return;
   }
@@ -2370,7 +2374,41 @@ void DdmHandle::ensure_gop() {
   args.bad = reinterpret_cast<unsigned*>(flags.p + 1);
   launch_assemble(args, n, eng.stream);
   HS_CUDA(cudaStreamSynchronize(eng.stream));
+  build_stencil_op();
   gop_ready = true;
+}
+
+// The global operator's values regrouped by stencil offset (column order: -stride[dim-1] ... -1, 0,
+// +1 ... +stride[dim-1]), so the residual kernel's loads are independent (hs_kernels.cu). Dropped
+// (the CSR kernels are used) when memory is short or an entry is off the stencil.
+void DdmHandle::build_stencil_op() {
+  g_sop = StencilOp();
+  if (std::getenv("HS_NO_STENCIL_OP")) return;  // developer A/B switch
+  const GridRange& rg = ggrid.range;
+  const long long n = rg.count();
+  StencilOp op;
+  op.S = 2 * dim + 1;
+  long long stride[3] = {1, 1, 1};
+  for (int a = 1; a < dim; ++a) stride[a] = stride[a - 1] * rg.size(a - 1);
+  for (int a = 0; a < dim; ++a) {
+    op.off[dim - 1 - a] = -stride[a];
+    op.off[dim + 1 + a] = stride[a];
+  }
+  op.off[dim] = 0;
+  size_t free_b = 0, total_b = 0;
+  HS_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (static_cast<double>(n) * op.S * sizeof(double2) > 0.05 * static_cast<double>(free_b)) return;
+  g_sten.alloc(static_cast<size_t>(n) * op.S);
+  DBuf<unsigned> bad;
+  bad.alloc(1);
+  bad.zero(eng.stream);
+  launch_stencil_build(n, g_rp.p, g_col.p, g_val.p, op, g_sten.p, bad.p, eng.stream);
+  unsigned hbad = 0;
+  HS_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(unsigned), cudaMemcpyDeviceToHost, eng.stream));
+  HS_CUDA(cudaStreamSynchronize(eng.stream));
+  if (hbad) return;
+  op.val = g_sten.p;
+  g_sop = op;
 }
 
 // One DDM application on bN -> u (node-major), src/sweeper.cpp:176-334.
@@ -2556,7 +2594,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
           comm_gather_u(t);
           ures = t;
         }
-        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s, geom.gsize[0]);
+        const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, ures, bN.p, R, pnum.p, pden.p, s, geom.gsize[0], g_sop);
         launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(rr) * R, s);
         launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(rr) * R, s);
       }
@@ -2611,7 +2649,7 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
             for (int q = 0; q + 1 < nrounds; ++q) {
               double2* uq = uround.p + static_cast<size_t>(q) * geom.gn * R;
               if (partitioned()) comm_gather_u(uq);
-              const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s, geom.gsize[0]);
+              const int nb2 = launch_residual(geom.gn, g_rp.p, g_col.p, g_val.p, uq, bN.p, R, pnum.p, pden.p, s, geom.gsize[0], g_sop);
               launch_reduce_partials(pnum.p, nb2, R, rnum.p + static_cast<size_t>(q) * R, s);
               launch_reduce_partials(pden.p, nb2, R, rden.p + static_cast<size_t>(q) * R, s);
             }
@@ -3404,7 +3442,7 @@ void gmres_impl(hs_ddm* s, int nrhs, const double* b, double* x, double tol, int
   };
   K.op = [&](const double2* z, double2* w, int R) { launch_spmv(n, H.g_rp.p, H.g_col.p, H.g_val.p, z, w, R, st); };
   K.true_res = [&](const double2* xx, const double2* bb, int R, double* out) {
-    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, xx, bb, R, H.pnum.p, H.pden.p, st, H.geom.gsize[0]);
+    const int nb2 = launch_residual(n, H.g_rp.p, H.g_col.p, H.g_val.p, xx, bb, R, H.pnum.p, H.pden.p, st, H.geom.gsize[0], H.g_sop);
     launch_reduce_partials(H.pnum.p, nb2, R, out, st);
   };
   gmres_loop(K, nrhs, b, x, tol, maxit, restart, reports);

@@ -671,6 +671,70 @@ __global__ void __launch_bounds__(kResThreads) residual_kernel(long long n, cons
   }
 }
 
+// Residual partials with the operator in stencil form (StencilOp): the coefficients (broadcast) and
+// the x values of a row are all independent loads. The CSR form walks row pointer -> column index
+// -> x (ncu: 70% long-scoreboard stalls, 36% of HBM bandwidth). Same tiles and the same per-row
+// sums in CSR column order as residual_kernel.
+template <int S>
+__global__ void __launch_bounds__(kResThreads) residual_stencil_kernel(long long n, StencilOp op, const double2* x,
+                                                                        const double2* b, int R, double* pnum,
+                                                                        double* pden, int gx, int tiles_x) {
+  __shared__ double rn[kResThreads], rd[kResThreads];
+  const int npb = kResThreads / R;
+  const int tn = threadIdx.x / R, r = threadIdx.x % R;
+  double num = 0.0, den = 0.0;
+  const long long bx = blockIdx.x % tiles_x, by = blockIdx.x / tiles_x;
+  const long long xi = bx * npb + tn;
+#pragma unroll 2
+  for (int j = 0; j < kResRows; ++j) {
+    const long long row = (by * kResRows + j) * gx + xi;
+    if (tn >= npb || xi >= gx || row >= n) continue;
+    double2 v[S], xv[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      v[q] = __ldg(op.val + row * S + q);
+      const long long c = min(max(row + op.off[q], 0LL), n - 1);  // (an absent entry's coefficient is zero)
+      xv[q] = x[c * R + r];
+    }
+    const double2 bv = b[row * R + r];
+    double2 s = czero();
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (v[q].x != 0.0 || v[q].y != 0.0) cfma(s, v[q], xv[q]);
+    const double2 dv = csub(bv, s);
+    num += dv.x * dv.x + dv.y * dv.y;
+    den += bv.x * bv.x + bv.y * bv.y;
+  }
+  rn[threadIdx.x] = num;
+  rd[threadIdx.x] = den;
+  __syncthreads();
+  if (threadIdx.x < R) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int q = threadIdx.x; q < npb * R; q += R) {
+      s1 += rn[q];
+      s2 += rd[q];
+    }
+    pnum[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s1;
+    pden[static_cast<long long>(blockIdx.x) * R + threadIdx.x] = s2;
+  }
+}
+
+__global__ void stencil_build_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
+                                     StencilOp op, double2* out, unsigned* bad) {
+  const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (row >= n) return;
+  for (int q = 0; q < op.S; ++q) out[row * op.S + q] = czero();
+  for (std::int64_t e = row_ptr[row]; e < row_ptr[row + 1]; ++e) {
+    const long long d = static_cast<long long>(col[e]) - row;
+    int q = 0;
+    while (q < op.S && op.off[q] != d) ++q;
+    if (q < op.S)
+      out[row * op.S + q] = val[e];
+    else
+      *bad = 1u;
+  }
+}
+
 __global__ void spmv_kernel(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
                             const double2* x, double2* y, int R) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -1022,8 +1086,14 @@ void launch_reduce_cpartials(const double2* partial, int nblocks, int R, double2
   after_launch();
 }
 
+void launch_stencil_build(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, StencilOp op,
+                          double2* out, unsigned* bad, cudaStream_t s) {
+  stencil_build_kernel<<<blocks_for(n), kThreads, 0, s>>>(n, row_ptr, col, val, op, out, bad);
+  after_launch();
+}
+
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, const double2* x,
-                    const double2* b, int R, double* pnum, double* pden, cudaStream_t s, int gx) {
+                    const double2* b, int R, double* pnum, double* pden, cudaStream_t s, int gx, StencilOp sop) {
   const int npb = kResThreads / R;
   int nb, tiles_x = 0;
   if (gx > 0 && n % gx == 0) {  // grid operator: tiles of npb nodes x kResRows grid rows
@@ -1033,7 +1103,14 @@ int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, co
     gx = 0;
     nb = blocks_for(n, npb);
   }
-  residual_kernel<<<nb, kResThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden, gx, tiles_x);
+  if (gx > 0 && sop.val && (sop.S == 5 || sop.S == 7)) {
+    if (sop.S == 5)
+      residual_stencil_kernel<5><<<nb, kResThreads, 0, s>>>(n, sop, x, b, R, pnum, pden, gx, tiles_x);
+    else
+      residual_stencil_kernel<7><<<nb, kResThreads, 0, s>>>(n, sop, x, b, R, pnum, pden, gx, tiles_x);
+  } else {
+    residual_kernel<<<nb, kResThreads, 0, s>>>(n, row_ptr, col, val, x, b, R, pnum, pden, gx, tiles_x);
+  }
   after_launch();
   return nb;
 }

@@ -168,9 +168,20 @@ void launch_xpack(const XSeg* segs, int nseg, bool pack, double* buf, double2* m
 
 // Global CSR SpMV y = A x (x, y node-major N x R) (src/operator.cpp:7-17) and the
 // residual partials |b - y|^2, |b|^2.
+// The global operator in stencil form: every row's entries sit at row + off[q] (a 2 dim + 1 point
+// stencil in CSR column order; absent entries hold zero), so a row's x loads need no row-pointer /
+// column-index loads first. val = nullptr: not available (use the CSR arrays).
+struct StencilOp {
+  const double2* val = nullptr;  // [n][S]
+  int S = 0;
+  long long off[7] = {0, 0, 0, 0, 0, 0, 0};
+};
+// Builds the stencil form from CSR; *bad is set when some entry is off the stencil.
+void launch_stencil_build(long long n, const std::int64_t* row_ptr, const int* col, const double2* val, StencilOp op,
+                          double2* out, unsigned* bad, cudaStream_t s);
 int launch_residual(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
                     const double2* x, const double2* b, int R, double* partial_num,
-                    double* partial_den, cudaStream_t s, int gx = 0);
+                    double* partial_den, cudaStream_t s, int gx = 0, StencilOp sop = StencilOp());
 void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const double2* val,
                  const double2* x, double2* y, int R, cudaStream_t s);
 
