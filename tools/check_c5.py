@@ -25,6 +25,18 @@ for it in range(2):
     out["local_solves"] = reps[0].local_solves
     out["skipped"] = reps[0].skipped_zero_solves
 out["rhs_per_s_device"] = R / out["sweep_device_s"]
+# the solve launches of the last application: algorithmic bytes (packed factor entries the passes
+# multiply + the vectors) over their CUDA-event time; at 8 RHS the solve is HBM-bound (4 flop / B)
+pr = s.profile()
+hbm = 6551.0
+try:
+    hbm = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    pass
+out["solve"] = {"seconds": pr["solve_seconds"], "launches": pr["solve_launches"], "alg_bytes": pr["alg_bytes"],
+                "alg_flops": pr["alg_flops"], "achieved_gbs": pr["alg_bytes"] / pr["solve_seconds"] / 1e9,
+                "hbm_peak_gbs": hbm, "hbm_frac": pr["alg_bytes"] / pr["solve_seconds"] / 1e9 / hbm,
+                "tflops": pr["alg_flops"] / pr["solve_seconds"] / 1e12}
 out["gpu_mem_used"] = subprocess.run(["nvidia-smi", "--query-gpu=memory.used,memory.total", "--format=csv,noheader"],
                                      capture_output=True, text=True).stdout.strip()
 print(json.dumps(out), flush=True)
