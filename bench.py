@@ -162,6 +162,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def hbm_bound_companion():
+    """The same solve kernels where they are HBM-bound (8 RHS: 4 flop per factor byte, below the
+    5.7 flop/B ridge): the committed C5 run (tools/check_c5.py -> profiles/r2_c5.json), not measured
+    by this command."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_c5.json")) as f:
+            c = json.load(f)["solve"]
+        return {"config": "C5 (3D, 64 subdomains of 57^3, 8 RHS)", "achieved_gbs": c["achieved_gbs"],
+                "frac": c["hbm_frac"], "source": "profiles/r2_c5.json (tools/check_c5.py; not measured by this run)"}
+    except Exception:
+        return None
+
+
 def peaks():
     """HBM copy bandwidth from MEASURED_PEAKS.json (driver-written) and the FP64 tensor-core
     (DMMA) peak measured by tools/bench_fp64.cu (profiles/fp64_peak.json)."""
@@ -367,7 +380,8 @@ def run_gpu(args, rank, world, local_rank):
                      "avg_launch_us": 1e6 * sec / nl,
                      "solve_share_of_step": sec * s.batches_per_application(R) / (ms_max * 1e-3),
                      "hbm_view": {"achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
-                                  "peak_source": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)"}},
+                                  "peak_source": f"{hbm_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                                  "hbm_bound_regime": hbm_bound_companion()}},
         "e2e": {"value": e2e_val, "unit": "RHS/s", "h2d_bytes_per_step": int(b.nbytes),
                 "d2h_bytes_per_step": int(b.nbytes), "steps": n_e2e,
                 "ms_per_step_samples": [round(x, 3) for x in e2e_samples]},
