@@ -47,11 +47,6 @@ __device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__device__ __forceinline__ double2 ld_stream(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
 __device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -173,17 +168,18 @@ __device__ __forceinline__ void acc_set(Acc<NT, M3>& c, int i, int q, int e, dou
 // after the k-loop: planes 0 / 1 = re / im
 template <int NT, bool M3>
 __device__ __forceinline__ void acc_finish(Acc<NT, M3>& c) {
-  if (!M3) return;
+  if constexpr (M3) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int q = 0; q < NT; ++q)
+      for (int q = 0; q < NT; ++q)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double p1 = c.v[i][q][0][e], p2 = c.v[i][q][1][e], p3 = c.v[i][q][Acc<NT, M3>::P - 1][e];
-        c.v[i][q][0][e] = p1 - p2;
-        c.v[i][q][1][e] = p3 - p1 - p2;
-      }
+        for (int e = 0; e < 2; ++e) {
+          const double p1 = c.v[i][q][0][e], p2 = c.v[i][q][1][e], p3 = c.v[i][q][Acc<NT, M3>::P - 1][e];
+          c.v[i][q][0][e] = p1 - p2;
+          c.v[i][q][1][e] = p3 - p1 - p2;
+        }
+  }
 }
 
 // one k-step (4 columns of the product's inner dimension) of the complex 32 x (8 NT) tile
@@ -420,7 +416,7 @@ constexpr int kIdx = 128;  // >= 8 * max(kc, kr)
 #ifndef HS_KUNROLL
 #define HS_KUNROLL 1
 #endif
-constexpr int kKUnroll = HS_KUNROLL;  // k-loop unroll (tuning experiments)
+[[maybe_unused]] constexpr int kKUnroll = HS_KUNROLL;  // k-loop unroll (tuning experiments)
 // When a warp takes its next ticket: 1 = after the current item's k-loop (its atomic overlaps the
 // reduction / finalize, and the held ticket is blocked only for that short tail), 0 = at the
 // start of the current item (the held ticket then waits behind the whole item: at the end of a
@@ -442,7 +438,7 @@ template <bool FWD>
 struct RingArea {
   static constexpr int a1 = Ring<FWD, 1>::NS * Ring<FWD, 1>::kStage, a2 = Ring<FWD, 2>::NS * Ring<FWD, 2>::kStage;
   static constexpr int kRing1 = a1 > a2 ? a1 : a2;
-  static constexpr int kRing = kRing1 > 4 * HS_ST2 ? kRing1 : 4 * HS_ST2;  // >= kRing2, the block-granular loops' two block stages
+  static constexpr int kRing = kRing1 > 4 * HS_ST2 ? kRing1 : 4 * HS_ST2;  // the block-granular loops need two block stages
   static constexpr int kFin = FWD ? 32 / 2 + 32 : 0;
   static constexpr int kWarp = kRing + kIdx / 2 + kFin;
 };
@@ -711,7 +707,6 @@ __device__ __forceinline__ void bwd_kloop(Acc<NT, M3>& acc, int ns, double2* rin
 #endif
 constexpr int kSt2 = HS_ST2;       // double2 per k-step stage (4 KB): A tiles at i * 32, B parts at 128 + j * 32
                                    // (192 = one-part stages only: 13.75 KB per warp, 4 CTAs per SM)
-constexpr int kRing2 = 4 * kSt2;   // two block stages
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void cpa(unsigned s, const char* g) {
