@@ -338,8 +338,13 @@ def run_gpu(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_val = units / (float(t2.item()) * 1e-3)
-    # parity sanity of what was timed: device result == host-path result
-    ok = bool(torch.equal(du.cpu(), hu))
+    # parity sanity of what was timed: device result vs host-path result. The device call runs one
+    # R-RHS batch, the host-buffer call streams 32-RHS batches whose split-K shape differs, so the
+    # two agree to roundoff (bitwise only when the batch widths coincide).
+    duh = du.cpu()
+    bitwise = bool(torch.equal(duh, hu))
+    path_diff = float(torch.linalg.vector_norm(duh - hu) / torch.linalg.vector_norm(duh))
+    del duh
     reps0 = s.ddm_solve_device(db.data_ptr(), du.data_ptr(), R, rounds, track, stream, want_reports=True)
 
     if rank != 0:
@@ -391,7 +396,9 @@ def run_gpu(args, rank, world, local_rank):
         "setup_seconds": setup_seconds,
         "sweep_seconds_per_rhs": ms_max * 1e-3 / R,
         "subdomain_solves_per_step": prof["subdomain_solves"],
-        "device_host_paths_agree": ok,
+        "device_host_paths_agree": path_diff <= 1e-11,
+        "device_host_paths_rel_l2": path_diff,
+        "device_host_paths_bitwise": bitwise,
     }
     if part:
         _, _, owned, sent, msgs = s.partition_info()
