@@ -566,6 +566,7 @@ struct Engine {
     x.alloc(static_cast<size_t>(xstride) * nbuf);
     // the right-hand side and z of a task live only within its macro-step: one buffer per slot
     slot_stride = n_max * R;
+    if (slot_stride >= (1ll << 31)) config_error("solve: subdomain too large for a batch of this width");
     x1.alloc(static_cast<size_t>(slot_stride) * nslots);
     rb.alloc(static_cast<size_t>(slot_stride) * nslots);
     rb.zero(stream);  // right-hand sides are zero off their injection lines between uses
@@ -2474,7 +2475,8 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
   cudaStream_t s = eng.stream;
   const int nsub = geom.nsub;
   if (track) ensure_gop();
-  HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
+  // (the fused accumulate writes every node of u, region by region)
+  if (!fuse_acc || partitioned()) HS_CUDA(cudaMemsetAsync(u.p, 0, u.n * sizeof(double2), s));
   HS_CUDA(cudaMemsetAsync(mpres.p, 0, mpres.n * sizeof(rmask), s));
   HS_CUDA(cudaMemsetAsync(nzmask.p, 0, nzmask.n * sizeof(rmask), s));
   HS_CUDA(cudaMemsetAsync(tface.p, 0, tface.n * sizeof(unsigned), s));
@@ -3137,7 +3139,9 @@ extern "C" int hs_ddm_solve(hs_ddm* s, int nrhs, const double* b, double* u, int
       // slots: batch k + 1's b streams in while batch k computes, batch k's u streams out while
       // batch k + 1 computes). One 64-RHS batch computes faster on the device (C3: 216 vs 228 ms)
       // but leaves its 4.6 GB of b and u each way to PCIe with nothing to overlap (e2e 345 vs 272 ms).
-      const int bw = nrhs > kStreamBatch ? kStreamBatch : nrhs;
+      int sb = kStreamBatch;
+      if (const char* e = std::getenv("HS_STREAM_BATCH")) sb = std::min(kMaxRhs, std::max(1, std::atoi(e)));
+      const int bw = nrhs > sb ? sb : nrhs;
       for (int b0 = 0, k = 0; b0 < nrhs; b0 += bw, ++k) {
         const int R = std::min(bw, nrhs - b0);
         H.solve_streamed(R, b + 2 * b0 * n, u + 2 * b0 * n, rounds, track_residuals != 0,

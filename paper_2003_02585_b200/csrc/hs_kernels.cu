@@ -334,20 +334,43 @@ __global__ void rhs_init_kernel(SweepArgs a) {
   const long long total = a.slot_stride;  // the whole slot: every occupant then keeps it zero off its lines
   const double inv = 1.0 / static_cast<double>(1 << dim);
   rmask bits = 0;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    double2 v = czero();
-    if (l == 1 && idx < static_cast<long long>(C.n) * a.R) {
-      const int e = static_cast<int>(idx / a.R), r = static_cast<int>(idx % a.R);
-      const int wn = S.split_w[e];
-      if (wn) {
-        const double w = wn * inv;
-        const double2 bv = a.b[static_cast<long long>(S.split_gp[e]) * a.R + r];
-        v = make_double2(w * bv.x, w * bv.y);
-        if ((v.x != 0.0 || v.y != 0.0) && !C.on_line[e]) bits |= 1ull << r;
-      }
+  // Four elements per thread and iteration, their loads issued in two waves (weight / global node /
+  // on-line flag, then b): one element at a time the weight -> node -> b chain left a thread with
+  // 16 bytes in flight per three memory round trips (ncu: 43% of HBM bandwidth on sweep-1 steps).
+  constexpr int U = 4;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long nloc = l == 1 ? static_cast<long long>(C.n) * a.R : 0;
+  const unsigned R = static_cast<unsigned>(a.R);
+  for (long long base = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; base < total; base += U * stride) {
+    int wn[U], gp[U];
+    unsigned rr[U];
+    bool line[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const long long idx = base + q * stride;
+      const bool in = idx < nloc;
+      // (element indices fit 32 bits: a slot holds n_max * R < 2^31 values)
+      const unsigned e = static_cast<unsigned>(idx) / R;
+      rr[q] = static_cast<unsigned>(idx) - e * R;
+      wn[q] = in ? S.split_w[e] : 0;
+      gp[q] = in ? S.split_gp[e] : 0;
+      line[q] = in ? C.on_line[e] != 0 : true;
     }
-    B[idx] = v;
+    double2 bv[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) bv[q] = wn[q] ? a.b[static_cast<long long>(gp[q]) * a.R + rr[q]] : czero();
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const long long idx = base + q * stride;
+      if (idx >= total) break;
+      double2 v = czero();
+      if (wn[q]) {
+        const double w = wn[q] * inv;
+        v = make_double2(w * bv[q].x, w * bv[q].y);
+        if ((v.x != 0.0 || v.y != 0.0) && !line[q]) bits |= 1ull << rr[q];
+      }
+      B[idx] = v;
+    }
   }
   if (l == 1) {
     bits = reduce_or64(bits);
@@ -371,19 +394,30 @@ __global__ void inject_kernel(SweepArgs a, int axis) {
   __shared__ long long s_slot[2][HS_SLOTS_PER_DIR];
   __shared__ rmask s_pres[2][HS_SLOTS_PER_DIR];
   __shared__ int s_n[2];
-  if (threadIdx.x < 2) {
-    const int d = 2 * axis + threadIdx.x;
+  if (threadIdx.x < 64) {
+    // warp q lists face q's generating sweeps with a deposit, in ascending order: a lane per
+    // candidate sweep, compacted by ballot (one thread walking route -> presence word sweep by
+    // sweep was a chain of up to 2 * l dependent loads ahead of every block's work)
+    const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int d = 2 * axis + q;
     int n = 0;
-    for (int lg = 1; lg <= l && n < HS_SLOTS_PER_DIR; ++lg) {
-      if (a.route[(lg - 1) * a.dirs + d] != l) continue;
-      const long long slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
-      const rmask pres = a.mpres[slot];
-      if (pres == 0) continue;
-      s_slot[threadIdx.x][n] = slot;
-      s_pres[threadIdx.x][n] = pres;
-      ++n;
+    for (int lg0 = 1; lg0 <= l && n < HS_SLOTS_PER_DIR; lg0 += 32) {
+      const int lg = lg0 + lane;
+      long long slot = 0;
+      rmask pres = 0;
+      if (lg <= l && a.route[(lg - 1) * a.dirs + d] == l) {
+        slot = (static_cast<long long>(sub) * a.nsweeps + (lg - 1)) * a.dirs + d;
+        pres = a.mpres[slot];
+      }
+      const unsigned have = __ballot_sync(kFull, pres != 0);
+      const int at = n + __popc(have & ((1u << lane) - 1u));
+      if (pres != 0 && at < HS_SLOTS_PER_DIR) {
+        s_slot[q][at] = slot;
+        s_pres[q][at] = pres;
+      }
+      n = min(n + __popc(have), HS_SLOTS_PER_DIR);
     }
-    s_n[threadIdx.x] = n;
+    if (lane == 0) s_n[q] = n;
   }
   __syncthreads();
 #pragma unroll 1
@@ -423,25 +457,33 @@ __global__ void nonzero_kernel(SweepArgs a) {
   rmask bits = 0;
   unsigned faces = 0;
   {
-    for (int d = 0; d < a.dirs; ++d) {
-      const int len = C.line_len[d];
-      const rmask b0 = bits;
-      bits = 0;
-      for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * R;
-           idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
-        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
-        if (p0 >= 0) {
-          const double2 v = B[static_cast<long long>(p0) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
-        }
-        if (pm >= 0) {
-          const double2 v = B[static_cast<long long>(pm) * R + r];
-          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
-        }
+    // every face's line positions are loaded together, then every value (face by face this was
+    // 2 * dirs dependent memory round trips per thread)
+    constexpr int DM = 6;
+    int maxlen = 0;
+    for (int d = 0; d < a.dirs; ++d) maxlen = max(maxlen, C.line_len[d]);
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < static_cast<long long>(maxlen) * R;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+      const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
+      int p0[DM], pm[DM];
+#pragma unroll
+      for (int d = 0; d < DM; ++d) {
+        const bool in = d < a.dirs && i < C.line_len[d];
+        p0[d] = in ? C.inj_p0[d][i] : -1;
+        pm[d] = in ? C.inj_pm[d][i] : -1;
       }
-      if (bits) faces |= 1u << d;
-      bits |= b0;
+      double2 v0[DM], v1[DM];
+#pragma unroll
+      for (int d = 0; d < DM; ++d) {
+        v0[d] = p0[d] >= 0 ? B[static_cast<long long>(p0[d]) * R + r] : czero();
+        v1[d] = pm[d] >= 0 ? B[static_cast<long long>(pm[d]) * R + r] : czero();
+      }
+#pragma unroll
+      for (int d = 0; d < DM; ++d)
+        if (v0[d].x != 0.0 || v0[d].y != 0.0 || v1[d].x != 0.0 || v1[d].y != 0.0) {
+          bits |= 1ull << r;
+          faces |= 1u << d;
+        }
     }
   }
   bits = reduce_or64(bits);
@@ -470,6 +512,7 @@ __global__ void nonzero_kernel(SweepArgs a) {
 
 // extract_trace (src/transfer.cpp:47-66) + route_trace (src/sweeper.cpp:58-73) + deposit into the
 // target's slot of this generating sweep (unique writer: plain stores, presence = RHS columns).
+constexpr int kExtractPer = 4;  // line x RHS elements per thread
 __global__ void extract_deposit_kernel(SweepArgs a) {
   const int task = blockIdx.y / a.dirs, d = blockIdx.y % a.dirs;
   const int sub = a.tasks[task].x, l = a.tasks[task].y;
@@ -489,12 +532,31 @@ __global__ void extract_deposit_kernel(SweepArgs a) {
   const long long slot = (static_cast<long long>(target) * a.nsweeps + (l - 1)) * a.dirs + d;
   double2* u0 = a.mbox + slot * a.mbox_dir_stride;
   double2* um1 = u0 + static_cast<long long>(len) * R;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < len * R) {
-    const int i = idx / R, r = idx % R;
-    if ((nz >> r) & 1ull) {
-      u0[idx] = X[static_cast<long long>(C.ext_u0[d][i]) * R + r];
-      um1[idx] = X[static_cast<long long>(C.ext_um1[d][i]) * R + r];
+  // kExtractPer elements per thread, all of a thread's index loads, then all of its x loads in
+  // flight together (one element per thread made 8000 blocks of one index -> x -> store chain
+  // each: 7 block waves per launch, 17 us for 70 MB)
+  int e0[kExtractPer], e1[kExtractPer];
+#pragma unroll
+  for (int q = 0; q < kExtractPer; ++q) {
+    const int idx = (blockIdx.x * kExtractPer + q) * blockDim.x + threadIdx.x;
+    const bool on = idx < len * R && ((nz >> (idx % R)) & 1ull);
+    e0[q] = on ? C.ext_u0[d][idx / R] : -1;
+    e1[q] = on ? C.ext_um1[d][idx / R] : -1;
+  }
+  double2 v0[kExtractPer], v1[kExtractPer];
+#pragma unroll
+  for (int q = 0; q < kExtractPer; ++q) {
+    const int idx = (blockIdx.x * kExtractPer + q) * blockDim.x + threadIdx.x;
+    const int r = idx % R;
+    v0[q] = e0[q] >= 0 ? X[static_cast<long long>(e0[q]) * R + r] : czero();
+    v1[q] = e1[q] >= 0 ? X[static_cast<long long>(e1[q]) * R + r] : czero();
+  }
+#pragma unroll
+  for (int q = 0; q < kExtractPer; ++q) {
+    const int idx = (blockIdx.x * kExtractPer + q) * blockDim.x + threadIdx.x;
+    if (e0[q] >= 0) {
+      u0[idx] = v0[q];
+      um1[idx] = v1[q];
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.mpres[slot] = nz;
@@ -961,26 +1023,34 @@ void launch_build_rhs(const SweepArgs& a, long long max_n, int max_line, cudaStr
     inject_kernel<<<dim3(nchunk, a.ntasks), kInjectChunk, 0, s>>>(a, axis);
     after_launch();
   }
-  nonzero_kernel<<<dim3(std::max(1, std::min(bx, 16)), a.ntasks), kThreads, 0, s>>>(a);
+  // a block per kThreads line elements of the longest face (each element is an index -> value chain)
+  nonzero_kernel<<<dim3(std::max(1, std::min(blocks_for(static_cast<long long>(max_line) * a.R), 128)), a.ntasks),
+                   kThreads, 0, s>>>(a);
   after_launch();
 }
 
 void launch_extract_deposit(const SweepArgs& a, int max_line, cudaStream_t s) {
-  const int nchunk = std::max(1, (max_line * a.R + kThreads - 1) / kThreads);
+  const int nchunk = std::max(1, (max_line * a.R + kThreads * kExtractPer - 1) / (kThreads * kExtractPer));
   extract_deposit_kernel<<<dim3(nchunk, a.ntasks * a.dirs), kThreads, 0, s>>>(a);
   after_launch();
 }
 
 constexpr int kAccThreads = 256;
-template <int E>
-__global__ void __launch_bounds__(kAccThreads) accumulate_all_kernel(AccumAllArgs a) {
+#ifndef HS_ACC_MINB
+#define HS_ACC_MINB 4
+#endif
+// LT: the number of sweeps when it is 4 or 8 (one straight-line body the compiler can schedule
+// across sweeps), 0: any number up to HS_MAX_ACC_SWEEPS (early exit per sweep).
+template <int E, int LT>
+__global__ void __launch_bounds__(kAccThreads, HS_ACC_MINB) accumulate_all_kernel(AccumAllArgs a) {
   // One thread per (node, RHS pair): its two x values are independent 16-byte loads, so a thread
   // keeps twice the bytes in flight of the one-RHS form (ncu: 37% of HBM bandwidth, bound by the
-  // bytes in flight per SM -- each thread walks a dependent plan entry -> nonzero word -> x chain
-  // per sweep). Per-sweep |c_l|^2 terms go straight to shared memory (no registers held across the
-  // sweeps) and are reduced once at the end (one barrier).
-  __shared__ double red[HS_MAX_ACC_SWEEPS][2][kAccThreads];
+  // bytes in flight per SM). Per-sweep |c_l|^2 terms go straight to shared memory (no registers
+  // held across the sweeps) and are reduced once at the end (one barrier).
+  constexpr int LM = LT ? LT : HS_MAX_ACC_SWEEPS;
+  __shared__ double red[LM][2][kAccThreads];
   const int dim = a.g.dim, R = a.R, RP = (R + 1) >> 1;
+  const int L = LT ? LT : a.L;
   const int npb = kAccThreads / RP;
   const int tn = threadIdx.x / RP;
   const long long li = static_cast<long long>(blockIdx.x) * npb + tn;  // index in the region
@@ -991,48 +1061,93 @@ __global__ void __launch_bounds__(kAccThreads) accumulate_all_kernel(AccumAllArg
   const double inv = 1.0 / static_cast<double>(1 << dim);
   const double2* __restrict__ xs = a.x;
 #pragma unroll
-  for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) red[l][0][threadIdx.x] = red[l][1][threadIdx.x] = 0.0;
+  for (int l = 0; l < LM; ++l) red[l][0][threadIdx.x] = red[l][1][threadIdx.x] = 0.0;
   if (live) {
     double2 u0 = czero(), u1 = czero();
+    // A thread's loads are issued in three waves -- the plan entries of every sweep, their nonzero
+    // words, then the x values of four sweeps at a time -- instead of a dependent entry -> nonzero
+    // word -> x chain per sweep (24 memory round trips for 8 sweeps, now 4). Only a node's first
+    // entry is on this path: interior nodes of a support have exactly one, the nodes of shared
+    // faces (2 to 2^dim entries, compacted to the front of the node's E slots) take the loop below.
+    int pos[LM];              // first entry's position in x
+    unsigned long long meta = 0;  // per sweep one byte: weight numerator (4 bits), more-entries flag, RHS pair's nonzero bits
+    {
+      int4 e01[LM];  // entries 0 and 1 of the node for sweep l's direction: (pos, id << 4 | w) x 2
+      rmask nzw[LM];
 #pragma unroll
-    for (int l = 0; l < HS_MAX_ACC_SWEEPS; ++l) {
-      if (l >= a.L) break;
-      const int2* __restrict__ pe = a.acc_ent[l] + node * E;
-      const rmask* __restrict__ nz = a.nzmask[l];
-      int2 ent[E];
+      for (int l = 0; l < LM; ++l)
+        e01[l] = l < L ? __ldg(reinterpret_cast<const int4*>(a.acc_ent[l] + node * E)) : make_int4(-1, 0, -1, 0);
 #pragma unroll
-      for (int e = 0; e < E; ++e) ent[e] = __ldg(pe + e);
-      double2 x0[E], x1[E];
-      unsigned on[E];
+      for (int l = 0; l < LM; ++l) nzw[l] = e01[l].x >= 0 ? __ldg(a.nzmask[l] + (e01[l].y >> 4)) : 0ull;
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const rmask m = ent[i].x >= 0 ? __ldg(nz + (ent[i].y >> 4)) >> r : 0ull;
-        on[i] = static_cast<unsigned>(m & (two ? 3ull : 1ull));
-        const double2* px = xs + a.xoff[l] + static_cast<long long>(ent[i].x) * R + r;
-        x0[i] = (on[i] & 1u) ? __ldcs(px) : czero();
-        x1[i] = (on[i] & 2u) ? __ldcs(px + 1) : czero();
+      for (int l = 0; l < LM; ++l) {
+        pos[l] = e01[l].x;
+        const unsigned on = static_cast<unsigned>((nzw[l] >> r) & (two ? 3ull : 1ull));
+        const unsigned byte = (e01[l].y & 15u) | (e01[l].z >= 0 ? 16u : 0u) | (on << 5);
+        meta |= static_cast<unsigned long long>(byte) << (8 * l);
       }
-      double2 c0 = czero(), c1 = czero();
+    }
+#ifndef HS_ACC_G
+#define HS_ACC_G 4
+#endif
+    constexpr int G = HS_ACC_G;  // sweeps whose x values are in flight together
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const double w = (ent[i].y & 15) * inv;
-        if (on[i] & 1u) {
-          c0.x += w * x0[i].x;
-          c0.y += w * x0[i].y;
-        }
-        if (on[i] & 2u) {
-          c1.x += w * x1[i].x;
-          c1.y += w * x1[i].y;
-        }
+    for (int l0 = 0; l0 < LM; l0 += G) {
+      if (!LT && l0 >= L) break;
+      double2 x0[G], x1[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int l = l0 + k < LM ? l0 + k : 0;
+        const unsigned on = l0 + k < LM ? static_cast<unsigned>(meta >> (8 * l + 5)) & 3u : 0u;
+        const double2* px = xs + a.xoff[l] + static_cast<long long>(pos[l]) * R + r;
+        x0[k] = (on & 1u) ? __ldcs(px) : czero();
+        x1[k] = (on & 2u) ? __ldcs(px + 1) : czero();
       }
-      u0 = cadd(u0, c0);
-      u1 = cadd(u1, c1);
-      red[l][0][threadIdx.x] = c0.x * c0.x + c0.y * c0.y;
-      red[l][1][threadIdx.x] = c1.x * c1.x + c1.y * c1.y;
-      if (a.uround && (l + 1) % a.rlen == 0 && l + 1 < a.L) {  // u after this round
-        double2* ur = a.uround + static_cast<long long>((l + 1) / a.rlen - 1) * a.rstride + node * R + r;
-        ur[0] = u0;
-        if (two) ur[1] = u1;
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int l = l0 + k;
+        if (l >= LM || (!LT && l >= L)) break;
+        const unsigned mb = static_cast<unsigned>(meta >> (8 * l)) & 255u;
+        const double w = (mb & 15u) * inv;
+        double2 c0 = czero(), c1 = czero();
+        if (mb & 32u) {
+          c0.x += w * x0[k].x;
+          c0.y += w * x0[k].y;
+        }
+        if (mb & 64u) {
+          c1.x += w * x1[k].x;
+          c1.y += w * x1[k].y;
+        }
+        if (mb & 16u) {  // a shared face: the node's other entries, in plan order
+          const int2* __restrict__ pe = a.acc_ent[l] + node * E;
+#pragma unroll 1
+          for (int i = 1; i < E; ++i) {
+            const int2 en = __ldg(pe + i);
+            if (en.x < 0) break;
+            const unsigned o = static_cast<unsigned>((__ldg(a.nzmask[l] + (en.y >> 4)) >> r) & (two ? 3ull : 1ull));
+            const double2* px = xs + a.xoff[l] + static_cast<long long>(en.x) * R + r;
+            const double wi = (en.y & 15) * inv;
+            if (o & 1u) {
+              const double2 xv = __ldcs(px);
+              c0.x += wi * xv.x;
+              c0.y += wi * xv.y;
+            }
+            if (o & 2u) {
+              const double2 xv = __ldcs(px + 1);
+              c1.x += wi * xv.x;
+              c1.y += wi * xv.y;
+            }
+          }
+        }
+        u0 = cadd(u0, c0);
+        u1 = cadd(u1, c1);
+        red[l][0][threadIdx.x] = c0.x * c0.x + c0.y * c0.y;
+        red[l][1][threadIdx.x] = c1.x * c1.x + c1.y * c1.y;
+        if (a.uround && (l + 1) % a.rlen == 0 && l + 1 < L) {  // u after this round
+          double2* ur = a.uround + static_cast<long long>((l + 1) / a.rlen - 1) * a.rstride + node * R + r;
+          ur[0] = u0;
+          if (two) ur[1] = u1;
+        }
       }
     }
     __stcs(a.u + node * R + r, u0);
@@ -1040,7 +1155,7 @@ __global__ void __launch_bounds__(kAccThreads) accumulate_all_kernel(AccumAllArg
   }
   __syncthreads();
   // partial of sweep l, column c: the block's nodes in order (fixed order)
-  for (int q = threadIdx.x; q < a.L * R; q += kAccThreads) {
+  for (int q = threadIdx.x; q < L * R; q += kAccThreads) {
     const int l = q / R, c = q % R;
     double sm = 0.0;
     for (int t = 0; t < npb; ++t) sm += red[l][c & 1][t * RP + (c >> 1)];
@@ -1052,9 +1167,13 @@ int launch_accumulate_all(const AccumAllArgs& a, cudaStream_t s) {
   const int nb = blocks_for(a.cnt, kAccThreads / ((a.R + 1) / 2));
   if (nb == 0) return 0;
   if (a.g.dim == 3)
-    accumulate_all_kernel<8><<<nb, kAccThreads, 0, s>>>(a);
+    accumulate_all_kernel<8, 0><<<nb, kAccThreads, 0, s>>>(a);
+  else if (a.L == 8)
+    accumulate_all_kernel<4, 8><<<nb, kAccThreads, 0, s>>>(a);
+  else if (a.L == 4)
+    accumulate_all_kernel<4, 4><<<nb, kAccThreads, 0, s>>>(a);
   else
-    accumulate_all_kernel<4><<<nb, kAccThreads, 0, s>>>(a);
+    accumulate_all_kernel<4, 0><<<nb, kAccThreads, 0, s>>>(a);
   after_launch();
   return nb;
 }

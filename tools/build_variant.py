@@ -1,4 +1,4 @@
-"""Developer tool: build a variant of the library with extra -D flags on hs_solve.cu / hs_ddm.cu (tuning
+"""Developer tool: build a variant of the library with extra -D flags on hs_solve.cu / hs_ddm.cu / hs_kernels.cu (tuning
 experiments). Usage: python tools/build_variant.py NAME -DHS_NS_FWD=2 ...  ->  _variants/NAME.so,
 selected at run time with HS_LIB_PATH."""
 import os, subprocess, sys
@@ -12,7 +12,7 @@ def main():
     out_dir = os.path.join(ROOT, "paper_2003_02585_b200", "_variants")
     os.makedirs(out_dir, exist_ok=True)
     # the -D flags apply to the solve kernels and to the host item builder
-    var = ["hs_solve.cu", "hs_ddm.cu"]
+    var = ["hs_solve.cu", "hs_ddm.cu", "hs_kernels.cu"]
     vobjs = []
     for f in var:
         obj = os.path.join(out_dir, f"{f}_{name}.o")
