@@ -457,33 +457,25 @@ __global__ void nonzero_kernel(SweepArgs a) {
   rmask bits = 0;
   unsigned faces = 0;
   {
-    // every face's line positions are loaded together, then every value (face by face this was
-    // 2 * dirs dependent memory round trips per thread)
-    constexpr int DM = 6;
-    int maxlen = 0;
-    for (int d = 0; d < a.dirs; ++d) maxlen = max(maxlen, C.line_len[d]);
-    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < static_cast<long long>(maxlen) * R;
-         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-      const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
-      int p0[DM], pm[DM];
-#pragma unroll
-      for (int d = 0; d < DM; ++d) {
-        const bool in = d < a.dirs && i < C.line_len[d];
-        p0[d] = in ? C.inj_p0[d][i] : -1;
-        pm[d] = in ? C.inj_pm[d][i] : -1;
-      }
-      double2 v0[DM], v1[DM];
-#pragma unroll
-      for (int d = 0; d < DM; ++d) {
-        v0[d] = p0[d] >= 0 ? B[static_cast<long long>(p0[d]) * R + r] : czero();
-        v1[d] = pm[d] >= 0 ? B[static_cast<long long>(pm[d]) * R + r] : czero();
-      }
-#pragma unroll
-      for (int d = 0; d < DM; ++d)
-        if (v0[d].x != 0.0 || v0[d].y != 0.0 || v1[d].x != 0.0 || v1[d].y != 0.0) {
-          bits |= 1ull << r;
-          faces |= 1u << d;
+    for (int d = 0; d < a.dirs; ++d) {
+      const int len = C.line_len[d];
+      const rmask b0 = bits;
+      bits = 0;
+      for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < len * R;
+           idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / R), r = static_cast<int>(idx % R);
+        const int p0 = C.inj_p0[d][i], pm = C.inj_pm[d][i];
+        if (p0 >= 0) {
+          const double2 v = B[static_cast<long long>(p0) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
         }
+        if (pm >= 0) {
+          const double2 v = B[static_cast<long long>(pm) * R + r];
+          if (v.x != 0.0 || v.y != 0.0) bits |= 1ull << r;
+        }
+      }
+      if (bits) faces |= 1u << d;
+      bits |= b0;
     }
   }
   bits = reduce_or64(bits);
