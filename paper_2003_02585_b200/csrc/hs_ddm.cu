@@ -807,6 +807,8 @@ struct Engine {
     a.quad = quad ? 1 : 0;
     a.need = need;
     a.need_words = need_words;
+    static const bool no_group_skip = std::getenv("HS_NO_GROUP_SKIP") != nullptr;  // developer A/B switch
+    a.no_group_skip = no_group_skip ? 1 : 0;
     a.nsub = static_cast<int>(sub_cls.size());
     a.rbs = rb.p;
     a.x1s = x1.p;
@@ -1280,6 +1282,14 @@ struct DdmHandle {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   }
+  // Column order of the current batch (launch_rhs_order): the device path orders from d_b, the
+  // streamed path from samples of the host buffer; reports map back through perm_h.
+  DBuf<int> rperm, rbbox;
+  std::vector<int> perm_h;
+  bool perm_on = false;    // rperm holds the batch's order (the transposes apply it)
+  bool perm_host = false;  // perm_h already holds it (ordered on the host)
+  const int* order_device(const double2* d_b, int nr);
+  const int* order_host(const double* b, int nr);
   void solve_streamed(int R, const double* b, double* u, int rounds, bool track, hs_solve_report* reps, int slot = 0,
                       bool last = true, int cap = 0);
   cudaEvent_t ev_din_free[2] = {}, ev_dout_free[2] = {};
@@ -2512,7 +2522,8 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
     for (int k = waited; k < upto; ++k) {
       const InTile& t = in_tiles[k];
       HS_CUDA(cudaStreamWaitEvent(s, io->copied[k], 0));
-      launch_transpose_in_tile(io->din, bN.p, geom.gn, R, geom.gsize[0], t.x0, t.x1, t.row0, t.row1, s);
+      launch_transpose_in_tile(io->din, bN.p, geom.gn, R, geom.gsize[0], t.x0, t.x1, t.row0, t.row1, s,
+                               perm_on ? rperm.p : nullptr);
     }
     waited = std::max(waited, upto);
   };
@@ -2639,7 +2650,9 @@ void DdmHandle::run_body(int nrounds, bool track, bool timed, const StreamIO* io
       } else {  // regions are the stripes here
         stripe_blocks[j] = accumulate(nsweeps, rg.row0 * gx, rg.row1 * gx, stripe_pbase(j));
       }
-      if (io) launch_transpose_out_tile(u.p, io->dout, geom.gn, R, gx, rg.x0, rg.x1, rg.row0, rg.row1, s);
+      if (io)
+        launch_transpose_out_tile(u.p, io->dout, geom.gn, R, gx, rg.x0, rg.x1, rg.row0, rg.row1, s,
+                                  perm_on ? rperm.p : nullptr);
       record(ev_out[j], s);
       if (++stripes_done == nst) {
         int nbt = 0;
@@ -2675,6 +2688,10 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
   std::vector<rmask> nz(static_cast<size_t>(nsweeps) * nsub);
   std::vector<double> nrm(static_cast<size_t>(nsweeps) * R), num(static_cast<size_t>(nrounds) * R),
       den(static_cast<size_t>(nrounds) * R);
+  if (perm_on && !perm_host) {  // internal column j is the caller's column perm_h[j]
+    perm_h.resize(R);
+    HS_CUDA(cudaMemcpyAsync(perm_h.data(), rperm.p, R * sizeof(int), cudaMemcpyDeviceToHost, eng.stream));
+  }
   HS_CUDA(cudaMemcpyAsync(nz.data(), nzmask.p, nz.size() * sizeof(rmask), cudaMemcpyDeviceToHost, eng.stream));
   HS_CUDA(cudaMemcpyAsync(nrm.data(), norms.p, nrm.size() * sizeof(double), cudaMemcpyDeviceToHost, eng.stream));
   if (track) {
@@ -2713,6 +2730,15 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
     HS_CUDA(cudaEventElapsedTime(&ms, ev[1 + nsweeps + 2 * sweep_first_m[l]], ev[l]));
     sweep_sec[l - 1] = ms * 1e-3;
   }
+  if (const char* path = std::getenv("HS_DUMP_NZ")) {  // developer instrumentation: per-task nonzero RHS masks
+    if (FILE* fp = std::fopen(path, "w")) {
+      std::fprintf(fp, "sweep,sub,mask\n");
+      for (int l = 1; l <= nsweeps; ++l)
+        for (int id = 0; id < nsub; ++id)
+          std::fprintf(fp, "%d,%d,%llx\n", l, id, static_cast<unsigned long long>(nz[static_cast<size_t>(l - 1) * nsub + id]));
+      std::fclose(fp);
+    }
+  }
   if (const char* path = std::getenv("HS_STEP_TIMES")) {  // developer instrumentation
     if (FILE* fp = std::fopen(path, "w")) {
       std::fprintf(fp, "mstep,ntasks,active,solve_us\n");
@@ -2725,7 +2751,7 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
   HS_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[nsweeps]));
   total = ms * 1e-3;
   for (int r = 0; r < R; ++r) {
-    hs_solve_report& rep = out[r];
+    hs_solve_report& rep = out[perm_on || perm_host ? perm_h[r] : r];
     std::memset(&rep, 0, sizeof(rep));
     rep.factor_seconds = factor_seconds;
     rep.sweep_seconds_total = total;
@@ -2770,6 +2796,59 @@ void DdmHandle::reports(int nrounds, bool track, hs_solve_report* out) {
       }
     }
   }
+}
+
+// Column order of a batch. Tasks skip RHS groups that are exactly zero for them (hs_solve.cu); with
+// the columns ordered by where their sources are, the columns of a group reach a subdomain together.
+static bool rhs_sort_enabled() {
+  static const bool off = std::getenv("HS_NO_RHS_SORT") != nullptr;  // developer A/B switch
+  return !off;
+}
+
+const int* DdmHandle::order_device(const double2* d_b, int nr) {
+  perm_host = false;
+  perm_on = rhs_sort_enabled() && nr >= 16 && !partitioned();
+  if (!perm_on) return nullptr;
+  rperm.alloc(kMaxRhs);
+  rbbox.alloc(6 * kMaxRhs);
+  launch_rhs_order(d_b, geom.gn, nr, geom, rbbox.p, rperm.p, eng.stream);
+  return rperm.p;
+}
+
+// The same order for a batch of the streamed host-buffer path, from samples of the host buffer
+// (every 32nd node of every 32nd grid row: well under a millisecond on the host cores), taken
+// while the batch's first tiles are already on their way to the device. Ordering across the
+// batches of a call would cluster better, but then every tile is one copy per column: measured
+// 403 ms against 207 ms per 64-RHS C3 call (32 K cudaMemcpy3DAsync calls).
+const int* DdmHandle::order_host(const double* b, int nr) {
+  perm_host = perm_on = rhs_sort_enabled() && nr >= 16 && !partitioned();
+  if (!perm_on) return nullptr;
+  const long long n = geom.gn;
+  const int gx = geom.gsize[0], gy = dim > 1 ? geom.gsize[1] : 1;
+  const long long rows = n / gx;
+  std::vector<unsigned> key(nr);
+  parallel_for(nr, [&](long long r) {
+    int bb[6] = {INT_MAX, INT_MAX, INT_MAX, -1, -1, -1};
+    const double* br = b + 2 * r * n;
+    for (long long row = 0; row < rows; row += 32)
+      for (int x = 0; x < gx; x += 32) {
+        const double* v = br + 2 * (row * gx + x);
+        if (v[0] != 0.0 || v[1] != 0.0) {
+          const int c[3] = {x, static_cast<int>(row % gy), static_cast<int>(row / gy)};
+          for (int a = 0; a < 3; ++a) {
+            bb[a] = std::min(bb[a], c[a]);
+            bb[3 + a] = std::max(bb[3 + a], c[a]);
+          }
+        }
+      }
+    key[r] = rhs_order_key(geom, bb);
+  });
+  perm_h.resize(nr);
+  for (int r = 0; r < nr; ++r) perm_h[r] = r;
+  std::stable_sort(perm_h.begin(), perm_h.end(), [&](int x, int y) { return key[x] < key[y]; });
+  rperm.alloc(kMaxRhs);
+  HS_CUDA(cudaMemcpyAsync(rperm.p, perm_h.data(), nr * sizeof(int), cudaMemcpyHostToDevice, eng.stream));
+  return rperm.p;
 }
 
 // One batch from / to pinned host buffers with the transfers overlapped: b streams in by tiles
@@ -2824,6 +2903,7 @@ void DdmHandle::solve_streamed(int nr, const double* b, double* uh, int nrounds,
     }
   };
   copy_in(ev_in.data());
+  order_host(b, nr);  // (the tile copies are already queued: the sampling overlaps them)
   const StreamIO sio{ev_in.data(), din, dout};
   run(nrounds, track, true, &sio);
   HS_CUDA(cudaEventRecord(ev_din_free[slot], eng.stream));
@@ -2910,9 +2990,10 @@ constexpr int kStreamBatch = 32;  // RHS per batch of the streamed host-buffer p
 void ddm_solve_batch(DdmHandle& H, int R, const double2* d_b, double2* d_u, int rounds, bool track,
                      hs_solve_report* reps) {
   H.ensure_state(R, rounds);
-  launch_transpose_in(d_b, H.bN.p, H.geom.gn, R, H.eng.stream);
+  const int* perm = H.order_device(d_b, R);
+  launch_transpose_in(d_b, H.bN.p, H.geom.gn, R, H.eng.stream, perm);
   H.run(rounds, track, true);
-  launch_transpose_out(H.u.p, d_u, H.geom.gn, R, H.eng.stream);
+  launch_transpose_out(H.u.p, d_u, H.geom.gn, R, H.eng.stream, perm);
   if (reps) H.reports(rounds, track, reps);
 }
 
@@ -3606,6 +3687,7 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
     };
     double sec = 0.0, bytes = 0.0, flops = 0.0;
     int64_t launches = 0, solves = 0;
+    const bool no_skip = std::getenv("HS_NO_GROUP_SKIP") != nullptr || H.eng.quad;
     float ms = 0.f;
     for (size_t m = 0; m < H.msteps.size(); ++m) {
       HS_CUDA(cudaEventElapsedTime(&ms, H.ev[1 + H.nsweeps + 2 * m], H.ev[2 + H.nsweeps + 2 * m]));
@@ -3617,8 +3699,14 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
         const double pf = live_packed(H.subs[t.x].cls, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
         const double pb = needed_packed(t.x, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
         ++solves;
-        bytes += (pf + pb) * 16 + 2.0 * H.R * c.n * 16;
-        flops += 8.0 * (pf + pb) * H.R;
+        // columns the items of this task compute: RHS groups that are exactly zero for it are
+        // skipped and half-zero 16-column groups run as 8-column items (hs_solve.cu)
+        int cols = 0;
+        const rmask m8 = nz[static_cast<size_t>(t.y - 1) * nsub + t.x];
+        for (int g8 = 0; 8 * g8 < H.R; ++g8)
+          if (no_skip || ((m8 >> (8 * g8)) & 0xFFull)) cols += std::min(8, H.R - 8 * g8);
+        bytes += (pf + pb) * 16 + 2.0 * cols * c.n * 16;
+        flops += 8.0 * (pf + pb) * cols;
       }
     }
     if (solve_seconds) *solve_seconds = sec;

@@ -15,6 +15,7 @@
 namespace cg = cooperative_groups;
 
 #include <algorithm>
+#include <climits>
 #include <type_traits>
 #include <atomic>
 #include <cstdio>
@@ -837,12 +838,13 @@ __global__ void scale_cols_kernel(double2* y, const double* inv, long long n, in
 // RHS-major [R][N] <-> node-major [N][R] for nodes [n0, n1): 32 nodes x R per block through
 // shared memory, so both sides are coalesced.
 constexpr int kTransNodes = 32;
-__global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
+__global__ void transpose_in_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                                    const int* perm) {
   __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
   const long long base = n0 + static_cast<long long>(blockIdx.x) * kTransNodes;
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // read rows of src: r, then node
     const int r = e / kTransNodes, i = e % kTransNodes;
-    if (base + i < n1) tile[i][r] = src[static_cast<long long>(r) * n + base + i];
+    if (base + i < n1) tile[i][r] = src[static_cast<long long>(perm ? perm[r] : r) * n + base + i];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // write node-major
@@ -850,7 +852,8 @@ __global__ void transpose_in_kernel(const double2* src, double2* dst, long long 
     if (base + i < n1) dst[(base + i) * R + r] = tile[i][r];
   }
 }
-__global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1) {
+__global__ void transpose_out_kernel(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
+                                    const int* perm) {
   __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
   const long long base = n0 + static_cast<long long>(blockIdx.x) * kTransNodes;
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // read node-major
@@ -860,20 +863,20 @@ __global__ void transpose_out_kernel(const double2* src, double2* dst, long long
   __syncthreads();
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {  // write rows of dst
     const int r = e / kTransNodes, i = e % kTransNodes;
-    if (base + i < n1) dst[static_cast<long long>(r) * n + base + i] = tile[i][r];
+    if (base + i < n1) dst[static_cast<long long>(perm ? perm[r] : r) * n + base + i] = tile[i][r];
   }
 }
 
 // The same for a tile of rows [row0, row0 + gridDim.y) x columns [x0, x1) of the fastest axis
 // (gx nodes per row): block (i, y) transposes 32 nodes of row row0 + y.
 __global__ void transpose_in_tile_kernel(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                                         long long row0) {
+                                         long long row0, const int* perm) {
   __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
   const long long rowb = (row0 + blockIdx.y) * gx;
   const long long base = rowb + x0 + static_cast<long long>(blockIdx.x) * kTransNodes, end = rowb + x1;
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
     const int r = e / kTransNodes, i = e % kTransNodes;
-    if (base + i < end) tile[i][r] = src[static_cast<long long>(r) * n + base + i];
+    if (base + i < end) tile[i][r] = src[static_cast<long long>(perm ? perm[r] : r) * n + base + i];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
@@ -883,7 +886,7 @@ __global__ void transpose_in_tile_kernel(const double2* src, double2* dst, long 
 }
 
 __global__ void transpose_out_tile_kernel(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                                          long long row0) {
+                                          long long row0, const int* perm) {
   __shared__ double2 tile[kTransNodes][kMaxRhs + 1];
   const long long rowb = (row0 + blockIdx.y) * gx;
   const long long base = rowb + x0 + static_cast<long long>(blockIdx.x) * kTransNodes, end = rowb + x1;
@@ -894,7 +897,7 @@ __global__ void transpose_out_tile_kernel(const double2* src, double2* dst, long
   __syncthreads();
   for (int e = threadIdx.x; e < kTransNodes * R; e += blockDim.x) {
     const int r = e / kTransNodes, i = e % kTransNodes;
-    if (base + i < end) dst[static_cast<long long>(r) * n + base + i] = tile[i][r];
+    if (base + i < end) dst[static_cast<long long>(perm ? perm[r] : r) * n + base + i] = tile[i][r];
   }
 }
 
@@ -1250,13 +1253,13 @@ void launch_scale_cols(double2* y, const double* inv, long long n, int R, cudaSt
   after_launch();
 }
 
-void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_in_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n);
+void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s, const int* perm) {
+  transpose_in_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n, perm);
   after_launch();
 }
 
-void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s) {
-  transpose_out_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n);
+void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s, const int* perm) {
+  transpose_out_kernel<<<static_cast<int>((n + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R, 0, n, perm);
   after_launch();
 }
 
@@ -1264,30 +1267,114 @@ void launch_transpose_in_range(const double2* src, double2* dst, long long n, in
                                cudaStream_t s) {
   if (n1 <= n0) return;
   transpose_in_kernel<<<static_cast<int>((n1 - n0 + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R,
-                                                                                                     n0, n1);
+                                                                                                     n0, n1, nullptr);
   after_launch();
 }
 void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                              long long row0, long long row1, cudaStream_t s) {
+                              long long row0, long long row1, cudaStream_t s, const int* perm) {
   if (x1 <= x0 || row1 <= row0) return;
   const dim3 grid((x1 - x0 + kTransNodes - 1) / kTransNodes, static_cast<unsigned>(row1 - row0));
-  transpose_in_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0);
+  transpose_in_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0, perm);
   after_launch();
 }
 void launch_transpose_out_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                               long long row0, long long row1, cudaStream_t s) {
+                               long long row0, long long row1, cudaStream_t s, const int* perm) {
   if (x1 <= x0 || row1 <= row0) return;
   const dim3 grid((x1 - x0 + kTransNodes - 1) / kTransNodes, static_cast<unsigned>(row1 - row0));
-  transpose_out_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0);
+  transpose_out_tile_kernel<<<grid, kThreads, 0, s>>>(src, dst, n, R, gx, x0, x1, row0, perm);
   after_launch();
 }
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                 cudaStream_t s) {
   if (n1 <= n0) return;
   transpose_out_kernel<<<static_cast<int>((n1 - n0 + kTransNodes - 1) / kTransNodes), kThreads, 0, s>>>(src, dst, n, R,
-                                                                                                      n0, n1);
+                                                                                                      n0, n1, nullptr);
   after_launch();
 }
+
+// ---- RHS ordering -------------------------------------------------------------------------------
+// A batch's columns are independent, so the library may hold them in any order. Tasks skip RHS
+// groups that are exactly zero for them (hs_solve.cu), which pays when the columns of a group
+// have their sources close together: the columns are ordered along a Morton curve over the
+// subdomain cells that hold the centres of their nonzeros' bounding boxes.
+// bbox[r] = {min x, min y, min z, max x, max y, max z} over the sampled grid rows (row % rstep == 0).
+__global__ void rhs_bbox_kernel(const double2* b, long long n, int gx, int gy, int rstep, long long srows, int* bbox) {
+  const int r = blockIdx.y;
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {-1, -1, -1};
+  const double2* br = b + static_cast<long long>(r) * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < srows * gx;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = (e / gx) * rstep;
+    const int x = static_cast<int>(e % gx);
+    const double2 v = br[row * gx + x];
+    if (v.x != 0.0 || v.y != 0.0) {
+      const int c[3] = {x, static_cast<int>(row % gy), static_cast<int>(row / gy)};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = min(lo[a], c[a]);
+        hi[a] = max(hi[a], c[a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = __reduce_min_sync(kFull, lo[a]);
+    hi[a] = __reduce_max_sync(kFull, hi[a]);
+  }
+  if ((threadIdx.x & 31) == 0 && hi[0] >= 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(bbox + 6 * r + a, lo[a]);
+      atomicMax(bbox + 6 * r + 3 + a, hi[a]);
+    }
+  }
+}
+
+__global__ void rhs_bbox_init_kernel(int R, int* bbox) {
+  if (static_cast<int>(threadIdx.x) < 6 * R) bbox[threadIdx.x] = threadIdx.x % 6 < 3 ? INT_MAX : -1;
+}
+
+__host__ __device__ inline unsigned rhs_morton_key(const DevGeom& g, const int* bb) {
+  if (bb[3] < 0) return 0xFFFFFFFFu;  // no nonzero seen: last
+  unsigned cell[3] = {0, 0, 0};
+  for (int a = 0; a < g.dim; ++a) {
+    const int c = ((bb[a] + bb[3 + a]) / 2 + g.glo[a]) / g.cut_w[a];
+    cell[a] = static_cast<unsigned>(c < 0 ? 0 : c >= g.counts[a] ? g.counts[a] - 1 : c);
+  }
+  unsigned key = 0;
+  for (int bit = 9; bit >= 0; --bit)
+    for (int a = g.dim - 1; a >= 0; --a) key = (key << 1) | ((cell[a] >> bit) & 1u);
+  return key;
+}
+
+// perm[j] = the caller's column held at internal position j: ascending key, ties by column
+__global__ void rhs_order_kernel(DevGeom g, int R, const int* bbox, int* perm) {
+  __shared__ unsigned key[kMaxRhs];
+  const int r = threadIdx.x;
+  if (r < R) key[r] = rhs_morton_key(g, bbox + 6 * r);
+  __syncthreads();
+  if (r >= R) return;
+  int rank = 0;
+  for (int q = 0; q < R; ++q) rank += key[q] < key[r] || (key[q] == key[r] && q < r);
+  perm[rank] = r;
+}
+
+void launch_rhs_order(const double2* b, long long n, int R, const DevGeom& g, int* bbox, int* perm, cudaStream_t s) {
+  rhs_bbox_init_kernel<<<1, 6 * kMaxRhs, 0, s>>>(R, bbox);
+  after_launch();
+  const int gx = g.gsize[0], gy = g.dim > 1 ? g.gsize[1] : 1;
+  const long long rows = n / gx;
+  const int rstep = 4;  // every fourth grid row: a quarter of b's bytes
+  const long long srows = (rows + rstep - 1) / rstep;
+  const int bx = std::max(1, std::min(blocks_for(srows * gx), 1184));
+  rhs_bbox_kernel<<<dim3(bx, R), kThreads, 0, s>>>(b, n, gx, gy, rstep, srows, bbox);
+  after_launch();
+  rhs_order_kernel<<<1, kMaxRhs, 0, s>>>(g, R, bbox, perm);
+  after_launch();
+}
+
+unsigned rhs_order_key(const DevGeom& g, const int* bbox6) { return rhs_morton_key(g, bbox6); }
+
 
 void launch_bump_epoch(unsigned* e, unsigned by, cudaStream_t s) {
   bump_epoch_kernel<<<1, 1, 0, s>>>(e, by);

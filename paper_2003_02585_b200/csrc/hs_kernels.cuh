@@ -36,6 +36,7 @@ struct SolveArgs {
   const unsigned* need;    // per subdomain bitset over fronts: x read back (backward pass); null = all
   int need_words;          // 32-bit words per subdomain in `need`
   int nsub;                // subdomains (task index nzi = (sweep - 1) * nsub + sub)
+  int no_group_skip;       // 1: RHS groups that are all zero for a task are computed anyway (HS_NO_GROUP_SKIP, A/B)
   // per-slot buffers (slot = the task's position in its macro-step): the task's right-hand side
   // (forward input) and z = D^-1 L^-1 b (forward output, backward input), elimination order,
   // node-major x R; slot_stride elements apart
@@ -186,16 +187,21 @@ void launch_spmv(long long n, const std::int64_t* row_ptr, const int* col, const
                  const double2* x, double2* y, int R, cudaStream_t s);
 
 // RHS-major [R][N] <-> node-major [N][R] with optional per-column shell masking.
-void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
-void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s);
+void launch_transpose_in(const double2* src, double2* dst, long long n, int R, cudaStream_t s, const int* perm = nullptr);
+void launch_transpose_out(const double2* src, double2* dst, long long n, int R, cudaStream_t s, const int* perm = nullptr);
 void launch_bump_epoch(unsigned* epoch, unsigned by, cudaStream_t s);
 // node range [n0, n1) only (streamed host transfers)
 void launch_transpose_in_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                cudaStream_t s);
 void launch_transpose_in_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                              long long row0, long long row1, cudaStream_t s);
+                              long long row0, long long row1, cudaStream_t s, const int* perm = nullptr);
 void launch_transpose_out_tile(const double2* src, double2* dst, long long n, int R, int gx, int x0, int x1,
-                               long long row0, long long row1, cudaStream_t s);
+                               long long row0, long long row1, cudaStream_t s, const int* perm = nullptr);
+// Column order of a batch (perm[j] = the caller's column held at internal position j): ascending
+// Morton key of the subdomain cell at the centre of each column's nonzeros (bbox: 6 ints per column,
+// scratch). rhs_order_key is the same key on the host (the streamed path samples b there).
+void launch_rhs_order(const double2* b, long long n, int R, const DevGeom& g, int* bbox, int* perm, cudaStream_t s);
+unsigned rhs_order_key(const DevGeom& g, const int* bbox6);
 void launch_transpose_out_range(const double2* src, double2* dst, long long n, int R, long long n0, long long n1,
                                 cudaStream_t s);
 

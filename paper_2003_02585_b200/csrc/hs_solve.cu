@@ -355,6 +355,7 @@ __device__ __forceinline__ bool split_reduce(Acc<NT, M3>& c, double* base, long 
   return true;
 }
 
+
 // 16-byte cp.async with zero fill: when !ok no byte is read (src-size 0), so src may be any
 // address (the lean k-loops pass the computed one instead of selecting a fallback)
 __device__ __forceinline__ void cp16z(double2* dst, const void* src, bool ok) {
@@ -1512,6 +1513,28 @@ __device__ __forceinline__ Geo geo_km(int k, int m) {
   return g;
 }
 
+// An item whose RHS group is exactly zero for its task: no loads, no products, no stores; only the
+// arrival of a split band's chunk, so the band is still finalized (signalled) exactly once.
+template <bool FWD>
+__device__ __forceinline__ bool zero_item(const SolveArgs& a, const SolveJob& J, const Geo& g, const SolveItem& it, int lane) {
+  int band, nch;
+  if (FWD) {
+    band = fwd_range(J, g, it).t;
+    nch = nch_fwd(g, band, J.kc);
+  } else {
+    band = bwd_range(J, g, it).u;
+    nch = nch_bwd(g, band, J.kr);
+  }
+  if (nch <= 1) return true;
+  int* arr = a.arr + (static_cast<long long>(it.slot) * a.arr_stride + J.arr_off + band) * a.ngr + it.r0 / 8;
+  int last = 0;
+  if (lane == 0) last = atom_add_acq_rel(arr, 1) == nch - 1;
+  return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
+
+#ifndef HS_GROUP_SKIP
+#define HS_GROUP_SKIP 1  // items of all-zero RHS groups only signal (0: every group of a nonzero task computes)
+#endif
 #ifndef HS_MINB_M3
 #define HS_MINB_M3 3  // CTAs per SM the 3M kernels are register-budgeted for (tuning experiments)
 #endif
@@ -1569,17 +1592,36 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
         const int sub = it.nzi % a.nsub;
         needed = (a.need[static_cast<long long>(sub) * a.need_words + (it.front >> 5)] >> (it.front & 31)) & 1u;
       }
+      // An RHS group whose columns are all exactly zero for this task (the reference skips each of
+      // those solves, src/sweeper.cpp:240-251): every reader of x masks by the task's nonzero word,
+      // so the group's items neither wait nor compute, they only keep the fronts' counters whole.
+      const bool gzero = HS_GROUP_SKIP && !QUAD && !a.no_group_skip &&
+                         (nzm & (((it.rw >= 64 ? 0ull : 1ull << it.rw) - 1ull) << it.r0)) == 0;
+      if (HS_GROUP_SKIP && !QUAD && !a.no_group_skip && !gzero && it.rw > 8) {
+        // a 16-RHS item whose lower or upper 8 columns are all zero runs as an 8-RHS item on the
+        // other half (every item of the task's group narrows the same way: the word is per task)
+        const unsigned lo = static_cast<unsigned>(nzm >> it.r0) & 0xFFu;
+        const unsigned hi = static_cast<unsigned>(nzm >> (it.r0 + 8)) & ((1u << (it.rw - 8)) - 1u);
+        if (hi == 0) {
+          it.rw = 8;
+        } else if (lo == 0) {
+          it.r0 += 8;
+          it.rw -= 8;
+        }
+      }
       if (FWD ? live : needed) {
         const unsigned clive = (all || ((act >> 8) & fm & 0xFFu) ? 1u : 0u) | (all || ((act >> 16) & fm & 0xFFu) ? 2u : 0u);
         const Geo g = geo_km(J.k, J.m);
-        item_prefetch<FWD>(a, J, g, it, sidx, lane, !QUAD || warp == 0);  // (a quad shares the factor range)
-        if (FWD) {
-          if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
-          if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
-        } else if (J.parent >= 0) {
-          wait_count(done + J.parent, J.tgt_p, lane);
+        if (!gzero) {
+          item_prefetch<FWD>(a, J, g, it, sidx, lane, !QUAD || warp == 0);  // (a quad shares the factor range)
+          if (FWD) {
+            if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
+            if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
+          } else if (J.parent >= 0) {
+            wait_count(done + J.parent, J.tgt_p, lane);
+          }
+          cp_wait<0>();
         }
-        cp_wait<0>();
         __syncwarp();
         if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
         double2* V = a.vbuf + it.slot * a.vslot_stride;
@@ -1615,7 +1657,10 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
         fin = nfin > 0;
 #else
         // one unit per item (merged items measured slower; HS_MERGE_UNITS=1 compiles them in)
-        if (FWD)
+        if (gzero) {
+          take_ticket(a, tk, took, lane);
+          fin = zero_item<FWD>(a, J, g, it, lane);
+        } else if (FWD)
           fin = it.rw > 8 ? fwd_item<2, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
                           : fwd_item<1, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
         else

@@ -436,6 +436,52 @@ def test_anisotropic_grids_against_reference(hs, dim, n, parts, pad, rounds):
         np.testing.assert_allclose(reps[i].round_residuals, rep0["round_residuals"], rtol=1e-6)
 
 
+def test_sparse_sources_wide_batch_against_reference(hs):
+    """A ragged wide batch of compactly supported sources scattered over the subdomains, some
+    columns exactly zero: most (task, RHS) pairs are exact-zero solves, which the reference skips
+    one by one (src/sweeper.cpp:240-251). The device orders the columns by source location, skips
+    the RHS groups that are all zero for a task and narrows half-zero groups; every column and its
+    report (mapped back through the column order) must equal the reference's for that source."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    n, parts, pad, rounds = [64, 64], [4, 4], 6, 2
+    kap = 2 * math.pi * 4
+    s = hs.DdmSolver(hs.ProblemSetup(2, n, parts, hs.Medium("constant", kappa=kap), pml_width=pad))
+    r = ref.RefSolver({"dim": 2, "grid.n": n, "partition": parts, "pml.width": pad, "media.kind": "constant",
+                       "media.kappa": kap}, 4)
+    gx = s.hi[0] - s.lo[0] + 1
+    rng = np.random.default_rng(23)
+    R = 41
+    B = np.zeros((R, s.global_n), complex)
+    for c in range(R):
+        if c % 7 == 3:
+            continue  # an all-zero column
+        ix, iy = rng.integers(2, n[0] - 2), rng.integers(2, n[1] - 2)
+        for dx in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                B[c, (ix + dx - s.lo[0]) + gx * (iy + dy - s.lo[1])] = rng.standard_normal() + 1j * rng.standard_normal()
+    reps = []
+    U = s.ddm_solve(B, rounds, reps, True)
+    for c in (0, 3, 5, 16, 17, 24, 31, 33, 40):
+        u0, rep0 = r.ddm_solve(B[c], rounds, True)
+        if not np.any(B[c]):
+            assert not np.any(U[c]) and reps[c].local_solves == 0
+            continue
+        assert rel(U[c], u0) <= TOL
+        assert [getattr(reps[c], k) for k in COUNTERS] == [rep0[k] for k in COUNTERS]
+        assert reps[c].skipped_zero_solves > 0
+        np.testing.assert_allclose(reps[c].round_residuals, rep0["round_residuals"], rtol=1e-6)
+    # the streamed host-buffer path (its own column order, from samples of the host buffer)
+    import torch
+    hb = torch.from_numpy(B.view(np.float64)).pin_memory()
+    hu = torch.empty_like(hb).pin_memory()
+    s.ddm_solve_host_ptr(hb.data_ptr(), hu.data_ptr(), R, rounds, True)
+    Uh = hu.numpy().view(np.complex128)
+    for c in range(R):  # (32 + 9 RHS batches there, one 41-RHS batch above: equal to roundoff)
+        assert (rel(Uh[c], U[c]) <= 1e-12) if np.any(B[c]) else not np.any(Uh[c])
+
+
 _ALT_SCRIPT = r"""
 import ast, os, sys, numpy as np
 sys.path.insert(0, {root!r})
@@ -461,7 +507,8 @@ print("WORST", worst)
 
 
 @pytest.mark.parametrize("env", [{"HS_M3": "0"}, {"HS_GRAPH": "0"}, {"HS_ORDER": "0", "HS_MAX_CHUNKS": "1"},
-                                 {"HS_QUAD": "1", "HS_ALT_REPEAT": "7"}, {"HS_ALT_REPEAT": "9"}])
+                                 {"HS_QUAD": "1", "HS_ALT_REPEAT": "7"}, {"HS_ALT_REPEAT": "9"},
+                                 {"HS_NO_GROUP_SKIP": "1", "HS_NO_RHS_SORT": "1", "HS_ALT_REPEAT": "9"}])
 def test_alternate_engine_paths_match_reference(env):
     """The engine's alternates, each selected per process by an environment switch, against the
     reference's golden u: the four-product solve kernels (HS_M3=0, 4 CTAs/SM), stream-by-stream
