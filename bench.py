@@ -372,7 +372,9 @@ def run_gpu(args, rank, world, local_rank):
         # multiply-add of the algorithm); with the 3M products the pipe executes 6 real
         # flops per complex MAC on 8x8-block-padded tiles (pipe_view).
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": fp64, "unit": "TFLOP/s", "frac": tflops / fp64,
-                     "flops": "effective complex flops (8 per complex MAC of the packed factor, work performed)",
+                     "flops": "effective complex flops (8 per complex MAC of the packed factor, work performed: the RHS "
+                              "columns the items computed -- RHS groups that are exactly zero for a task are skipped, as "
+                              "the reference skips exact-zero solves, and are not counted)",
                      "peak_source": "measured FP64 DMMA peak (profiles/fp64_peak.json, tools/bench_fp64.cu); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
                      "pipe_view": {"real_flops_per_complex_mac": 6 if prof.get("m3", True) else 8,

@@ -6,4 +6,5 @@ timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_bench.log 2>&1
 timeout 600 python bench.py --config c2 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_bench_c2.log 2>&1; tail -c 300 gpurun_out/r2_bench_c2.log
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r2_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/r2_ncu_bench.log 2>&1; wc -l gpurun_out/r2_launches.csv
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:solve6 -s 70 -c 2 -o gpurun_out/r2_solve_full python tools/profile_cfg.py c3 --apps 1 > gpurun_out/r2_ncu_full.log 2>&1; tail -2 gpurun_out/r2_ncu_full.log
-timeout 900 ncu --set full --clock-control none -k regex:"accumulate_all|inject|extract|rhs_init|nonzero|residual" -c 12 -o gpurun_out/r2_sweep_full python tools/profile_cfg.py c3 --apps 1 > gpurun_out/r2_ncu_sweep.log 2>&1; tail -2 gpurun_out/r2_ncu_sweep.log
+timeout 900 ncu --set full --clock-control none -k regex:"inject|extract|rhs_init|nonzero" -s 60 -c 10 -o gpurun_out/r2_sweep_full python tools/profile_cfg.py c3 --apps 1 > gpurun_out/r2_ncu_sweep.log 2>&1; tail -2 gpurun_out/r2_ncu_sweep.log
+timeout 900 ncu --set full --clock-control none -k regex:"accumulate_all|residual|rhs_bbox|transpose" -c 8 -o gpurun_out/r2_acc_full python tools/profile_cfg.py c3 --apps 1 > gpurun_out/r2_ncu_acc.log 2>&1; tail -2 gpurun_out/r2_ncu_acc.log

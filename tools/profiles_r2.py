@@ -91,7 +91,8 @@ def main():
     with open(os.path.join(P, "r2_launch_totals.json"), "w") as f:
         json.dump({n: {"launches": a[0], "ms": a[1] / 1e6, "dram_bytes": a[2] + a[3]} for n, a in agg.items()}, f, indent=1)
     for rep, title in (("r2_solve_full.ncu-rep", "solve kernels, C3 macro-step 35 (31 tasks x 64 RHS)"),
-                       ("r2_sweep_full.ncu-rep", "sweep kernels, C3")):
+                       ("r2_sweep_full.ncu-rep", "sweep kernels, C3"),
+                       ("r2_acc_full.ncu-rep", "column order, transposes, fused accumulate, residual, C3")):
         path = os.path.join(G, rep)
         if not os.path.exists(path):
             continue
