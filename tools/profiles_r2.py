@@ -67,6 +67,49 @@ def full_metrics(rep):
     return res
 
 
+def compact_launch_list(src, dst):
+    """Per-launch list (id, kernel, ns, DRAM read / write bytes) of the ncu metrics pass."""
+    rows = list(csv.reader(open(src)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    hdr, data = rows[hi], rows[hi + 1:]
+    iK, iM, iV, iID = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+    k = collections.OrderedDict()
+    for r in data:
+        if len(r) < len(hdr):
+            continue
+        d = k.setdefault(r[iID], {})
+        d["name"] = (r[iK].split("(")[0].replace("void ", "").replace("hsb::", "").replace("<unnamed>::", "")
+                     .replace("unnamed>::", ""))
+        d[r[iM]] = float(r[iV].replace(",", ""))
+    L = [(d["name"], int(d.get("gpu__time_duration.sum", 0)), int(d.get("dram__bytes_read.sum", 0)),
+          int(d.get("dram__bytes_write.sum", 0))) for d in k.values()]
+    with open(dst, "w") as f:
+        f.write("# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none  "
+                "python bench.py --steps 1 --warmup 3 --no-cpu-baseline (C3, 64 RHS)\n")
+        f.write("id,kernel,duration_ns,dram_read_bytes,dram_write_bytes\n")
+        for i, x in enumerate(L):
+            f.write(f"{i},{x[0]},{x[1]},{x[2]},{x[3]}\n")
+    return L
+
+
+def application_traffic(L, bench, full):
+    """DRAM bytes of the solve launches of the timed device application (the 4th: after 3 warm-ups)
+    against the same application's algorithmic bytes -> profiles/solve_traffic.json (bench.py's
+    roofline.traffic)."""
+    starts = [i for i, x in enumerate(L) if x[0].startswith("transpose_in_kernel")]
+    ends = [i for i, x in enumerate(L) if x[0].startswith("transpose_out_kernel")]
+    sv = [x for x in L[starts[3]:ends[3]] if x[0].startswith("solve6")]
+    tot, t = sum(x[2] + x[3] for x in sv), sum(x[1] for x in sv)
+    alg = bench["roofline"]["alg_bytes_per_launch"] * len(sv)
+    out = {"what": "ncu dram__bytes_read + write summed over the solve launches of the timed 64-RHS C3 application "
+                   "(profiles/r2_launch_list.csv), per launch, against the same application's algorithmic bytes",
+           "bytes_per_launch": tot / len(sv), "launches": len(sv), "dram_bytes_application": tot,
+           "alg_bytes_application": alg, "dram_over_algorithmic": tot / alg, "ncu_serialised_ms": t / 1e6,
+           "dram_gbs_under_ncu": tot / t, "full_capture_step35": full}
+    json.dump(out, open(os.path.join(P, "solve_traffic.json"), "w"), indent=1)
+    return out
+
+
 def main():
     lines = []
     bench = open(os.path.join(G, "r2_bench.log")).read().strip().splitlines()[-1]
@@ -105,9 +148,14 @@ def main():
                          f"{d.get('warps_active_pct', 0):.1f} | {d.get('regs', 0):.0f} |")
         if rep.startswith("r2_solve"):
             sv = [d for d in fm if "solve6" in d["kernel"]]
-            json.dump({"what": "ncu --set full DRAM bytes per solve launch (C3 macro-step 35, fwd + bwd average)",
-                       "bytes_per_launch": sum(d.get("read", 0) + d.get("write", 0) for d in sv) / max(len(sv), 1),
-                       "launches": sv}, open(os.path.join(P, "solve_traffic.json"), "w"), indent=1)
+            full = {"what": "ncu --set full DRAM bytes per solve launch (C3 macro-step 35, fwd + bwd average)",
+                    "bytes_per_launch": sum(d.get("read", 0) + d.get("write", 0) for d in sv) / max(len(sv), 1),
+                    "launches": sv}
+            L = compact_launch_list(os.path.join(G, "r2_launches.csv"), os.path.join(P, "r2_launch_list.csv"))
+            tr = application_traffic(L, b, full)
+            lines += ["", f"Solve launches of the timed application: {tr['dram_bytes_application'] / 1e9:.0f} GB of DRAM traffic "
+                      f"against {tr['alg_bytes_application'] / 1e9:.0f} GB algorithmic = {tr['dram_over_algorithmic']:.2f}x "
+                      f"(`solve_traffic.json`)."]
     open(os.path.join(P, "r2_summary.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
