@@ -490,7 +490,9 @@ struct Engine {
     // 13.0-13.3 ms with the wide settings).
     if (r >= 32) {
       kc = kr = 8;
-      split_depth = r >= 48 ? 3 : 5;  // (64 RHS: 128.7 ms at depth 3, 129.5 at 5, 131.2 at 7; 32 RHS flat)
+      // (64 RHS: 128.7 ms at depth 3, 129.5 at 5, 131.2 at 7; with the zero-group skip 111.1 ms at
+      // depth 1, 111.4 at 2, 112.3 at 3, 112.0 at 0; 32 RHS flat)
+      split_depth = r >= 48 ? 1 : 5;
       crit_gw = 16;
     } else {
       kc = kr = 4;
