@@ -1609,19 +1609,23 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
           it.rw -= 8;
         }
       }
-      if (FWD ? live : needed) {
+      if (gzero) {  // (its own short path: the item path below stays as it is without the skip)
+        if (FWD ? live : needed) {
+          take_ticket(a, tk, took, lane);
+          fin = zero_item<FWD>(a, J, geo_km(J.k, J.m), it, lane);
+          nfin = fin ? 1 : 0;
+        }
+      } else if (FWD ? live : needed) {
         const unsigned clive = (all || ((act >> 8) & fm & 0xFFu) ? 1u : 0u) | (all || ((act >> 16) & fm & 0xFFu) ? 2u : 0u);
         const Geo g = geo_km(J.k, J.m);
-        if (!gzero) {
-          item_prefetch<FWD>(a, J, g, it, sidx, lane, !QUAD || warp == 0);  // (a quad shares the factor range)
-          if (FWD) {
-            if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
-            if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
-          } else if (J.parent >= 0) {
-            wait_count(done + J.parent, J.tgt_p, lane);
-          }
-          cp_wait<0>();
+        item_prefetch<FWD>(a, J, g, it, sidx, lane, !QUAD || warp == 0);  // (a quad shares the factor range)
+        if (FWD) {
+          if (J.child0 >= 0 && (clive & 1u)) wait_count(done + J.child0, J.tgt_c0, lane);
+          if (J.child1 >= 0 && (clive & 2u)) wait_count(done + J.child1, J.tgt_c1, lane);
+        } else if (J.parent >= 0) {
+          wait_count(done + J.parent, J.tgt_p, lane);
         }
+        cp_wait<0>();
         __syncwarp();
         if (tr && lane == 0) tr[1] = gtime();  // [0] dequeue [1] ready [2] k-loop done [3] reduced [4] done [5] sm [6] k-steps
         double2* V = a.vbuf + it.slot * a.vslot_stride;
@@ -1657,10 +1661,7 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
         fin = nfin > 0;
 #else
         // one unit per item (merged items measured slower; HS_MERGE_UNITS=1 compiles them in)
-        if (gzero) {
-          take_ticket(a, tk, took, lane);
-          fin = zero_item<FWD>(a, J, g, it, lane);
-        } else if (FWD)
+        if (FWD)
           fin = it.rw > 8 ? fwd_item<2, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took)
                           : fwd_item<1, M3, QUAD>(a, J, g, it, V, lane, ring, sidx, tr, clive, tk, took);
         else
