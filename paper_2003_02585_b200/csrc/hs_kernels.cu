@@ -335,6 +335,7 @@ __global__ void rhs_init_kernel(SweepArgs a) {
   const long long total = a.slot_stride;  // the whole slot: every occupant then keeps it zero off its lines
   const double inv = 1.0 / static_cast<double>(1 << dim);
   rmask bits = 0;
+  bool anyv = false;
   // Four elements per thread and iteration, their loads issued in two waves (weight / global node /
   // on-line flag, then b): one element at a time the weight -> node -> b chain left a thread with
   // 16 bytes in flight per three memory round trips (ncu: 43% of HBM bandwidth on sweep-1 steps).
@@ -368,7 +369,10 @@ __global__ void rhs_init_kernel(SweepArgs a) {
       if (wn[q]) {
         const double w = wn[q] * inv;
         v = make_double2(w * bv[q].x, w * bv[q].y);
-        if ((v.x != 0.0 || v.y != 0.0) && !line[q]) bits |= 1ull << rr[q];
+        if (v.x != 0.0 || v.y != 0.0) {
+          anyv = true;
+          if (!line[q]) bits |= 1ull << rr[q];
+        }
       }
       B[idx] = v;
     }
@@ -376,6 +380,11 @@ __global__ void rhs_init_kernel(SweepArgs a) {
   if (l == 1) {
     bits = reduce_or64(bits);
     if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
+    // the split source is nonzero somewhere in this subdomain (on or off the lines): every front is
+    // live (0x100). A sweep-1 task whose subdomain holds no source only carries injected traces,
+    // like the tasks of later sweeps: its live fronts follow from the receiving faces (nonzero_kernel)
+    if (__any_sync(kFull, anyv) && (threadIdx.x & 31) == 0)
+      atomicOr(&a.tface[static_cast<long long>(l - 1) * a.g.nsub + sub], 0x100u);
   }
 }
 
@@ -499,8 +508,8 @@ __global__ void nonzero_kernel(SweepArgs a) {
   faces &= recv;
   const long long ti = static_cast<long long>(l - 1) * a.g.nsub + sub;
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[ti], bits);
-  // sweep 1 also carries the split source anywhere in the subdomain: every front is live (0x100)
-  if ((threadIdx.x & 31) == 0 && (faces || l == 1)) atomicOr(&a.tface[ti], l == 1 ? 0x100u : faces);
+  // (a sweep-1 task whose subdomain holds part of the split source was marked all-live, 0x100, by rhs_init)
+  if ((threadIdx.x & 31) == 0 && faces) atomicOr(&a.tface[ti], faces);
 }
 
 // extract_trace (src/transfer.cpp:47-66) + route_trace (src/sweeper.cpp:58-73) + deposit into the
