@@ -3698,17 +3698,27 @@ extern "C" int hs_ddm_profile(hs_ddm* s, double* solve_seconds, int64_t* solve_l
       for (const int2& t : H.msteps_own[m]) {  // this rank's solves
         if (nz[static_cast<size_t>(t.y - 1) * nsub + t.x] == 0) continue;
         const SymbolicClass& c = *H.eng.classes[H.subs[t.x].cls]->sym;
-        const double pf = live_packed(H.subs[t.x].cls, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
-        const double pb = needed_packed(t.x, tf[static_cast<size_t>(t.y - 1) * nsub + t.x]);
-        ++solves;
-        // columns the items of this task compute: RHS groups that are exactly zero for it are
-        // skipped and half-zero 16-column groups run as 8-column items (hs_solve.cu)
-        int cols = 0;
+        // per 8-column group: the columns the items compute (RHS groups that are exactly zero for
+        // the task are skipped, half-zero 16-column groups run as 8-column items) over the fronts
+        // that are live for the group -- every front where the group holds part of the split source
+        // (sweep 1, bits 16-23 of the face word), else the fronts of the receiving faces
+        const unsigned fw = tf[static_cast<size_t>(t.y - 1) * nsub + t.x];
         const rmask m8 = nz[static_cast<size_t>(t.y - 1) * nsub + t.x];
-        for (int g8 = 0; 8 * g8 < H.R; ++g8)
-          if (no_skip || ((m8 >> (8 * g8)) & 0xFFull)) cols += std::min(8, H.R - 8 * g8);
-        bytes += (pf + pb) * 16 + 2.0 * cols * c.n * 16;
-        flops += 8.0 * (pf + pb) * cols;
+        const double pf_all = live_packed(H.subs[t.x].cls, 0x100u), pb_all = needed_packed(t.x, 0x100u);
+        const double pf_face = live_packed(H.subs[t.x].cls, fw & 0xFFu), pb_face = needed_packed(t.x, fw & 0xFFu);
+        ++solves;
+        double pmax = 0.0;
+        int cols = 0;
+        for (int g8 = 0; 8 * g8 < H.R; ++g8) {
+          if (!no_skip && !((m8 >> (8 * g8)) & 0xFFull)) continue;
+          const int w = std::min(8, H.R - 8 * g8);
+          const bool all = (fw & 0x100u) || ((fw >> 16) >> g8 & 1u);
+          const double p = all ? pf_all + pb_all : pf_face + pb_face;
+          pmax = std::max(pmax, p);
+          cols += w;
+          flops += 8.0 * p * w;
+        }
+        bytes += pmax * 16 + 2.0 * cols * c.n * 16;
       }
     }
     if (solve_seconds) *solve_seconds = sec;

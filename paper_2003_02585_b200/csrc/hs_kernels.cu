@@ -334,8 +334,7 @@ __global__ void rhs_init_kernel(SweepArgs a) {
   // positions off the injection lines are final here (lines: nonzero_kernel)
   const long long total = a.slot_stride;  // the whole slot: every occupant then keeps it zero off its lines
   const double inv = 1.0 / static_cast<double>(1 << dim);
-  rmask bits = 0;
-  bool anyv = false;
+  rmask bits = 0, anyb = 0;
   // Four elements per thread and iteration, their loads issued in two waves (weight / global node /
   // on-line flag, then b): one element at a time the weight -> node -> b chain left a thread with
   // 16 bytes in flight per three memory round trips (ncu: 43% of HBM bandwidth on sweep-1 steps).
@@ -370,7 +369,7 @@ __global__ void rhs_init_kernel(SweepArgs a) {
         const double w = wn[q] * inv;
         v = make_double2(w * bv[q].x, w * bv[q].y);
         if (v.x != 0.0 || v.y != 0.0) {
-          anyv = true;
+          anyb |= 1ull << rr[q];
           if (!line[q]) bits |= 1ull << rr[q];
         }
       }
@@ -380,11 +379,15 @@ __global__ void rhs_init_kernel(SweepArgs a) {
   if (l == 1) {
     bits = reduce_or64(bits);
     if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[static_cast<long long>(l - 1) * a.g.nsub + sub], bits);
-    // the split source is nonzero somewhere in this subdomain (on or off the lines): every front is
-    // live (0x100). A sweep-1 task whose subdomain holds no source only carries injected traces,
-    // like the tasks of later sweeps: its live fronts follow from the receiving faces (nonzero_kernel)
-    if (__any_sync(kFull, anyv) && (threadIdx.x & 31) == 0)
-      atomicOr(&a.tface[static_cast<long long>(l - 1) * a.g.nsub + sub], 0x100u);
+    // 8-column groups in which the split source is nonzero somewhere in this subdomain (on or off
+    // the lines): every front is live for them (bits 16 + group of the task's face word). The other
+    // columns of a sweep-1 task only carry injected traces, like the tasks of later sweeps: their
+    // live fronts follow from the receiving faces (nonzero_kernel)
+    anyb = reduce_or64(anyb);
+    unsigned gb = 0;
+    for (int g8 = 0; g8 < 8; ++g8)
+      if ((anyb >> (8 * g8)) & 0xFFull) gb |= 1u << g8;
+    if (gb && (threadIdx.x & 31) == 0) atomicOr(&a.tface[static_cast<long long>(l - 1) * a.g.nsub + sub], gb << 16);
   }
 }
 
@@ -508,7 +511,7 @@ __global__ void nonzero_kernel(SweepArgs a) {
   faces &= recv;
   const long long ti = static_cast<long long>(l - 1) * a.g.nsub + sub;
   if ((threadIdx.x & 31) == 0 && bits) atomicOr(&a.nzmask[ti], bits);
-  // (a sweep-1 task whose subdomain holds part of the split source was marked all-live, 0x100, by rhs_init)
+  // (the column groups of a sweep-1 task that hold part of the split source were marked all-live by rhs_init)
   if ((threadIdx.x & 31) == 0 && faces) atomicOr(&a.tface[ti], faces);
 }
 

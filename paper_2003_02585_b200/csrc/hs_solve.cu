@@ -1583,8 +1583,10 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
       // Its forward items are skipped (nothing waits for them: a live parent ignores the child),
       // and its backward items read z = 0.
       const unsigned act = static_cast<unsigned>(J.act);
-      const bool all = (fm & kAllLive) != 0;
-      const bool live = all || (act & fm & 0xFFu) != 0;
+      // every front is live for the task (kAllLive) or for the 8-column groups named in bits 16-23
+      // (sweep 1: the groups whose split source is nonzero in this subdomain)
+      const bool all_task = (fm & kAllLive) != 0 || (fm >> 16) != 0;
+      const bool live_task = all_task || (act & fm & 0xFFu) != 0;
       // backward: a front whose subtree holds no position the application reads back (PML frame
       // away from the support and the extraction lines) is skipped, and so is its subtree
       bool needed = true;
@@ -1609,8 +1611,14 @@ __global__ void __launch_bounds__(kThreads, M3 ? HS_MINB_M3 : 4) solve6_kernel(S
           it.rw -= 8;
         }
       }
-      if (gzero) {  // (its own short path: the item path below stays as it is without the skip)
-        if (FWD ? live : needed) {
+      // (the item's groups after the narrowing: consistent over the items of a task's group)
+      const bool all = (fm & kAllLive) != 0 ||
+                       (((fm >> 16) >> (it.r0 >> 3)) & ((1u << ((it.rw + 7) >> 3)) - 1u)) != 0;
+      const bool live = all || (act & fm & 0xFFu) != 0;
+      // A front that is live for some group of the task but not for this item's: the item only
+      // signals, like a zero group (the front's counters count the items of every group)
+      if (gzero || (FWD && live_task && !live)) {  // (its own short path: the item path below stays as it is without the skip)
+        if (FWD ? live_task : needed) {
           take_ticket(a, tk, took, lane);
           fin = zero_item<FWD>(a, J, geo_km(J.k, J.m), it, lane);
           nfin = fin ? 1 : 0;
