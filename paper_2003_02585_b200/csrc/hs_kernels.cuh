@@ -28,7 +28,8 @@ struct SolveArgs {
   double2* vbuf;           // update-vector slots
   long long vslot_stride;  // elements per slot
   const rmask* nzmask;     // per subdomain: RHS columns with a nonzero right-hand side
-  const unsigned* tface;   // per task: faces with nonzero injected data, 0x100 = every front live
+  const unsigned* tface;   // per task: faces with nonzero injected data (bits 0-7), 0x100 = every front live,
+                           // bits 16-23 = 8-column groups for which every front is live (sweep 1: split source)
                            // (sweep 1); null = every front live
   int quad;                // items are listed in quads (four RHS groups of one band chunk, null-padded,
                            // nzi < 0) that one CTA dequeues together and streams through L1
