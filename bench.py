@@ -102,9 +102,15 @@ def host_info():
                     break
     except OSError:
         pass
+    try:  # the shim's large dense products run on numpy's bundled OpenBLAS when it loads (oracle/shim)
+        from oracle import ref
+        dense = ("large dense products on numpy's bundled OpenBLAS, one thread per worker" if ref.blas_active()
+                 else "naive dense loops, no BLAS")
+    except Exception:
+        dense = "dense backing unknown"
     return {"cpu_model": model, "nproc": os.cpu_count(), "ram_gib": ram,
             "reference_build": "g++ -O3 -march=native, reference sources compiled in place against the "
-                               "from-scratch Eigen-subset shim oracle/shim (naive dense loops, no BLAS)"}
+                               f"from-scratch Eigen-subset shim oracle/shim ({dense})"}
 
 
 def make_sources(seed, lo, hi, hgrid, origin):
